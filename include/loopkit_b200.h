@@ -1,0 +1,212 @@
+/*
+ * loopkit_b200.h -- C ABI of the B200-native global registration path.
+ *
+ * Drop-in boundary for the reference registration API
+ * (/root/reference/proj/include/loopkit/registration.hpp). Every entry point
+ * below names the reference interface it replaces. Plain pointers and sizes
+ * only: no C++ types, no exceptions, no torch types. Errors are lk_status
+ * codes mirroring proj/include/loopkit/errors.hpp; the message of the last
+ * failure on the calling thread is available from lk_last_error().
+ *
+ * Clouds are caller-owned host arrays of packed FP64 xyz triples -- exactly
+ * the memory layout of the reference's std::vector<Eigen::Vector3d>, so the
+ * reference's PointCloud can be passed without copying.
+ *
+ * There is no CPU fallback: a call that needs the GPU returns LK_CUDA_ERROR
+ * when no CUDA device is usable.
+ */
+#ifndef LOOPKIT_B200_H
+#define LOOPKIT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LK_ABI_VERSION 1
+
+/* proj/include/loopkit/errors.hpp:9-74 */
+typedef enum lk_status {
+    LK_OK = 0,
+    LK_NO_ALIGNMENT = 1,        /* std::nullopt from register_global / run_hypotheses (not an error) */
+    LK_EMPTY_CLOUD = 2,         /* EmptyCloud */
+    LK_TOO_FEW_POINTS = 3,      /* TooFewPoints */
+    LK_MISSING_DATA = 4,        /* MissingData */
+    LK_MISSING_NORMALS = 5,     /* MissingNormals */
+    LK_NO_CORRESPONDENCES = 6,  /* NoCorrespondences */
+    LK_DEGENERATE = 7,          /* DegenerateConfiguration */
+    LK_INVALID_ARGUMENT = 8,    /* Error (bad cell length / leaf, null pointers) */
+    LK_CUDA_ERROR = 9,
+    LK_NCCL_ERROR = 10,
+    LK_INTERNAL_ERROR = 99
+} lk_status;
+
+/* proj/include/loopkit/geometry.hpp:92-99 (PointCloud): positions + optional normals */
+typedef struct lk_cloud {
+    const double* xyz;  /* n x 3, packed */
+    const double* nxyz; /* n x 3 or NULL; a zero normal marks "invalid" */
+    int64_t n;
+} lk_cloud;
+
+/* proj/include/loopkit/registration.hpp:17-32 (RegistrationParams) */
+typedef struct lk_reg_params {
+    double leaf;             /* 0.05 */
+    double normal_radius;    /* 0.1 */
+    double feature_radius;   /* 0.25 */
+    int64_t hypothesis_count;/* 4,000,000 */
+    double similarity_tau;   /* 0.9 */
+    double d_max;            /* 0.075 */
+    double min_inlier_ratio; /* 0.25 */
+    double max_fitness;      /* < 0 => d_max^2 / 2 (resolved_max_fitness) */
+    double normal_angle_max; /* 30 deg in radians */
+    uint64_t seed;           /* 0 */
+    int32_t threads;         /* host threads for the host prepare stage; 0 = all */
+    int32_t device;          /* CUDA device ordinal; -1 = current */
+} lk_reg_params;
+
+/* proj/include/loopkit/registration.hpp:34-39 (RegistrationResult) + inlier count */
+typedef struct lk_reg_result {
+    double R[9]; /* row-major rotation, maps source into the target frame */
+    double t[3];
+    double inlier_ratio;
+    double fitness;
+    int64_t inliers;
+    int64_t hypothesis_index;
+    int32_t found;
+    int32_t _pad;
+} lk_reg_result;
+
+/* proj/include/loopkit/registration.hpp:91-99 (HypothesisStats) + work counters */
+typedef struct lk_hyp_stats {
+    int64_t sampled;
+    int64_t prerejected;
+    int64_t degenerate;
+    int64_t evaluated;
+    int64_t qualified;
+    int64_t w_ref;          /* point visits of the reference loop (its static miss budget) */
+    int64_t evals_executed; /* point evaluations the device actually executed */
+    double prepare_seconds;
+    double hypothesis_seconds;
+} lk_hyp_stats;
+
+/*
+ * Per-rank record exchanged by the multi-GPU merge: the rank's best qualified
+ * hypothesis plus its stats counters. 24 x 8 B = 192 B; an all-reduce(sum)
+ * over a zero-filled [G x record] buffer is an exact all-gather.
+ */
+typedef struct lk_reg_record {
+    int64_t valid;
+    int64_t inliers;
+    double fitness;
+    int64_t index;
+    double R[9];
+    double t[3];
+    int64_t sampled, prerejected, degenerate, evaluated, qualified;
+    int64_t w_ref;
+    int64_t evals_executed;
+    int64_t _reserved;
+} lk_reg_record;
+
+/* Explicit-candidate score (evaluate_hypothesis, registration.cpp:53-78) */
+typedef struct lk_cand_score {
+    double inlier_ratio;
+    double fitness;
+    int64_t inliers; /* -1 when the candidate exited on the miss budget (early_exit mode) */
+} lk_cand_score;
+
+typedef struct lk_reg_ctx lk_reg_ctx;   /* RegistrationContext on one device */
+typedef struct lk_grid lk_grid;         /* device grid over a target cloud */
+
+int lk_abi_version(void);
+const char* lk_last_error(void);
+/* number of usable CUDA devices (0 on a host without a GPU) */
+int lk_device_count(void);
+
+/* ---- RegistrationContext --------------------------------------------------
+ * prepare_registration (registration.hpp:105-107, registration.cpp:223-251):
+ * downsample + FPFH (host, this tier), feature pre-match and EvalGrid
+ * (device). Throws-equivalents: LK_TOO_FEW_POINTS, LK_MISSING_DATA. */
+lk_status lk_reg_prepare(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_params* params, lk_reg_ctx** out);
+/* A RegistrationContext from already-prepared parts (downsampled clouds with
+ * normals + the feature match cache), as when the reference's caller fills
+ * RegistrationContext itself. The EvalGrid is built on the device. */
+lk_status lk_reg_ctx_create(const lk_cloud* src, const lk_cloud* tgt, const int32_t* cache, const lk_reg_params* params,
+                            lk_reg_ctx** out);
+void lk_reg_ctx_destroy(lk_reg_ctx* ctx);
+/* cudaStream_t to launch on (NULL = the context's own stream) */
+lk_status lk_reg_ctx_set_stream(lk_reg_ctx* ctx, void* stream);
+lk_status lk_reg_ctx_sizes(const lk_reg_ctx* ctx, int64_t* n_source, int64_t* n_target);
+/* Per-kernel device timing with CUDA events on the launch stream. While
+ * enabled, every run records events around k_hyp_sample, k_kabsch and
+ * k_score; lk_reg_ctx_kernel_times returns the accumulated milliseconds of
+ * the three kernels (ms3) and the number of runs (synchronises the events). */
+lk_status lk_reg_ctx_set_profiling(lk_reg_ctx* ctx, int32_t enable);
+lk_status lk_reg_ctx_kernel_times(lk_reg_ctx* ctx, double* ms3, int64_t* runs, int32_t reset);
+/* copy the prepared context back to the host (any pointer may be NULL) */
+lk_status lk_reg_ctx_download(const lk_reg_ctx* ctx, double* src_xyz, double* src_n, double* tgt_xyz, double* tgt_n,
+                              int32_t* cache, float* src_features, float* tgt_features);
+
+/* ---- run_hypotheses (registration.hpp:116-118, registration.cpp:253-332) --
+ * Returns LK_OK with result->found = 1, or LK_NO_ALIGNMENT (found = 0). */
+lk_status lk_reg_run_hypotheses(lk_reg_ctx* ctx, const lk_reg_params* params, lk_reg_result* result,
+                                lk_hyp_stats* stats);
+/* One shard [begin, end) of the hypothesis range. The rank's record is
+ * written to `record` (device pointer when record_on_device != 0, e.g. the
+ * rank's slot of an NCCL buffer; host pointer otherwise). Asynchronous on
+ * the context stream when record_on_device != 0. */
+lk_status lk_reg_run_range(lk_reg_ctx* ctx, const lk_reg_params* params, int64_t begin, int64_t end,
+                           lk_reg_record* record, int32_t record_on_device);
+/* Exact merge of G per-rank records under the run_hypotheses total order
+ * (registration.cpp:272-276); host-only, needs no GPU. */
+lk_status lk_reg_merge_records(const lk_reg_record* records, int32_t count, int64_t n_source, lk_reg_result* result,
+                               lk_hyp_stats* stats);
+
+/* ---- register_global (registration.hpp:121-124, registration.cpp:334-343) */
+lk_status lk_register_global(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_params* params,
+                             lk_reg_result* result, lk_hyp_stats* stats);
+
+/* ---- build_eval_grid (registration.hpp:79, registration.cpp:80-148) -------
+ * kind 0: EvalGrid (cell = d_max, origin = bbox_lo - cell, dense CSR +
+ *         26-dilated occupancy); kind 1: SearchGrid semantics
+ *         (proj/src/grid.cpp:32-66: cells floor((p - 0) / cell), block
+ *         radius ceil(d_max / cell)) stored densely over the occupied box. */
+lk_status lk_grid_build(const lk_cloud* target, int32_t kind, double cell, double d_max, int32_t device, lk_grid** out);
+void lk_grid_destroy(lk_grid* grid);
+lk_status lk_grid_dims(const lk_grid* grid, double* origin3, double* cell, int32_t* dims3, int64_t* ncells,
+                       int64_t* npoints);
+lk_status lk_grid_download(const lk_grid* grid, int32_t* start, int32_t* index, double* slot_xyz, double* slot_n,
+                           uint8_t* near_occupied);
+
+/* ---- evaluate_hypothesis over an explicit candidate list ------------------
+ * registration.hpp:60-63 (per candidate), plus run_hypotheses' qualification
+ * and total order for `best`. Rt = C x 12 doubles (R row-major, then t).
+ * kind-1 grid: evaluate_hypothesis semantics (fitness from sqrt(d2)^2);
+ * kind-0 grid: evaluate_against_grid semantics (fitness from d2), with the
+ * miss-budget early exit when early_exit != 0. per_cand may be NULL. */
+lk_status lk_score_candidates(lk_grid* grid, const lk_cloud* src, const double* Rt, int64_t C,
+                              const lk_reg_params* params, int32_t early_exit, lk_cand_score* per_cand,
+                              lk_reg_result* best, int64_t* qualified);
+
+/* ---- edge_info (proj/src/line_process.cpp:11-33), batched -----------------
+ * For pair k: cloud_i = clouds_i[k], cloud_j = clouds_j[k], poses T_i/T_j as
+ * 12 doubles each (R row-major, t). info = 36 doubles per pair (row-major
+ * 6x6), pair_count per pair; a pair with no correspondence reports
+ * pair_count 0 (the reference throws NoCorrespondences). */
+lk_status lk_edge_info_batched(const lk_cloud* clouds_i, const lk_cloud* clouds_j, const double* Ti, const double* Tj,
+                               int64_t n_pairs, double epsilon, int32_t device, double* info, int64_t* pair_count);
+
+/* ---- feature pre-match (registration.cpp:248 -> grid.cpp:176-213) ---------
+ * argmin_j ||F(p_i) - F(q_j)||^2 in FP64, ties -> lowest j. */
+lk_status lk_feature_nn_cache(const float* src_features, int64_t ns, const float* tgt_features, int64_t nt,
+                              int32_t device, int32_t* cache);
+
+/* host-side helpers of prepare (this tier) */
+lk_status lk_voxel_downsample(const lk_cloud* cloud, double leaf, double* out_xyz, double* out_n, int64_t* out_count);
+lk_status lk_compute_fpfh(const lk_cloud* cloud, double radius, int32_t threads, float* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LOOPKIT_B200_H */

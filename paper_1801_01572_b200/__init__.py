@@ -1,0 +1,17 @@
+"""B200-native global point-cloud registration (arXiv 1801.01572, "LoopSmart").
+
+A drop-in for the reference's registration path
+(/root/reference/proj/include/loopkit/registration.hpp): hand-written sm_100a
+CUDA kernels behind the C ABI in include/loopkit_b200.h, with this package as
+the Python mirror of the reference interface.
+"""
+from .errors import (CudaError, DegenerateConfiguration, EmptyCloud, Error, MissingData, MissingNormals,
+                     NoCorrespondences, TooFewPoints)
+from .registration import (CandidateScores, DeviceGrid, EdgeInfo, EvalGrid, HypothesisStats, PointCloud,
+                           RegistrationContext, RegistrationParams, RegistrationResult, RigidTransform, SearchGrid,
+                           build_eval_grid, build_grid, compute_fpfh, device_count, edge_info, edge_info_batched,
+                           evaluate_hypothesis, feature_nn_cache, merge_records, prepare_registration,
+                           records_from_bytes, register_global, registration_context, run_hypotheses,
+                           run_hypotheses_range, score_candidates, voxel_downsample)
+
+__all__ = [name for name in dir() if not name.startswith("_")]

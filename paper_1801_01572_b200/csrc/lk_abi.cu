@@ -1,0 +1,739 @@
+// lk_abi.cu -- C ABI (include/loopkit_b200.h) over the device path.
+//
+// Mirrors proj/include/loopkit/registration.hpp: status codes instead of
+// exceptions (errors.hpp), LK_NO_ALIGNMENT instead of std::nullopt. Contexts
+// own their device buffers; calls on one context serialise on its mutex, so
+// concurrent calls on a shared context stay safe as in the reference.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <chrono>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/loopkit_b200.h"
+#include "lk_kernels.cuh"
+#include "lk_prepare_host.hpp"
+
+namespace {
+
+thread_local std::string g_err;
+
+lk_status fail(lk_status code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+struct CudaFail {
+    cudaError_t e;
+    const char* where;
+};
+inline void ck(cudaError_t e, const char* where) {
+    if (e != cudaSuccess) throw CudaFail{e, where};
+}
+#define CK(x) ck((x), #x)
+
+template <class F>
+lk_status guarded(F&& fn) {
+    try {
+        return fn();
+    } catch (const lk::Status& s) {
+        return fail(static_cast<lk_status>(s.code), s.what());
+    } catch (const CudaFail& c) {
+        return fail(LK_CUDA_ERROR, std::string(c.where) + ": " + cudaGetErrorString(c.e));
+    } catch (const std::bad_alloc&) {
+        return fail(LK_INTERNAL_ERROR, "host allocation failed");
+    } catch (const std::exception& e) {
+        return fail(LK_INTERNAL_ERROR, e.what());
+    }
+}
+
+double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+int select_device(int32_t device) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        throw lk::Status(LK_CUDA_ERROR, "no usable CUDA device (the B200 path has no CPU fallback)");
+    }
+    int dev = device;
+    if (dev < 0) CK(cudaGetDevice(&dev));
+    if (dev >= n) throw lk::Status(LK_INVALID_ARGUMENT, "device ordinal out of range");
+    CK(cudaSetDevice(dev));
+    return dev;
+}
+
+int sm_count_of(int dev) {
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    return sms;
+}
+
+template <class T>
+T* dev_upload(const T* host, size_t count, cudaStream_t s) {
+    T* d = nullptr;
+    CK(cudaMalloc(&d, std::max<size_t>(count, 1) * sizeof(T)));
+    if (count) CK(cudaMemcpyAsync(d, host, count * sizeof(T), cudaMemcpyHostToDevice, s));
+    return d;
+}
+
+std::vector<double> flatten(const std::vector<lk::Vec3>& v) {
+    std::vector<double> out(3 * v.size());
+    for (size_t i = 0; i < v.size(); ++i) lk::store3(out.data(), static_cast<int64_t>(i), v[i]);
+    return out;
+}
+
+void check_cloud_ptr(const lk_cloud* c, const char* what) {
+    if (!c) throw lk::Status(LK_INVALID_ARGUMENT, std::string(what) + ": null cloud");
+    if (c->n < 0) throw lk::Status(LK_INVALID_ARGUMENT, std::string(what) + ": negative size");
+    if (c->n > 0 && !c->xyz) throw lk::Status(LK_INVALID_ARGUMENT, std::string(what) + ": null positions");
+}
+
+double resolved_max_fitness(const lk_reg_params& p) { return p.max_fitness < 0 ? p.d_max * p.d_max / 2.0 : p.max_fitness; }
+
+lkk::ScoreParams score_params(const lk_reg_params& p, int64_t ns, bool early_exit, bool from_distance) {
+    lkk::ScoreParams sp{};
+    sp.d_max = p.d_max;
+    sp.d2_max = p.d_max * p.d_max;
+    sp.cos_max = std::cos(p.normal_angle_max);
+    sp.min_ratio = p.min_inlier_ratio;
+    sp.max_fitness = resolved_max_fitness(p);
+    // registration.cpp:259-261
+    sp.miss_budget = early_exit ? ns - static_cast<int64_t>(std::ceil(p.min_inlier_ratio * static_cast<double>(ns)))
+                                : INT64_MAX;
+    sp.fitness_from_distance = from_distance ? 1 : 0;
+    return sp;
+}
+
+void record_to_result(const lk_reg_record& r, int64_t ns, lk_reg_result* out) {
+    std::memset(out, 0, sizeof(*out));
+    out->hypothesis_index = -1;
+    if (!r.valid) return;
+    std::memcpy(out->R, r.R, sizeof(out->R));
+    std::memcpy(out->t, r.t, sizeof(out->t));
+    out->inliers = r.inliers;
+    out->inlier_ratio = static_cast<double>(r.inliers) / static_cast<double>(ns);
+    out->fitness = r.fitness;
+    out->hypothesis_index = r.index;
+    out->found = 1;
+}
+
+// registration.cpp:272-276 on records of one source cloud
+bool record_better(const lk_reg_record& a, const lk_reg_record& b) {
+    if (a.inliers != b.inliers) return a.inliers > b.inliers;
+    if (a.fitness != b.fitness) return a.fitness < b.fitness;
+    return a.index < b.index;
+}
+
+}  // namespace
+
+struct lk_grid {
+    int device = 0;
+    int sm_count = 0;
+    int kind = 0;
+    double cell = 0, d_max = 0;
+    bool has_normals = false;
+    cudaStream_t stream = nullptr;
+    lkk::GridStorage g;
+    lkk::RunBuffers rb;
+    lk_reg_record* d_record = nullptr;
+    std::mutex mu;
+    ~lk_grid() {
+        cudaSetDevice(device);
+        g.release();
+        rb.release();
+        cudaFree(d_record);
+        if (stream) cudaStreamDestroy(stream);
+    }
+};
+
+struct lk_reg_ctx {
+    int device = 0;
+    int sm_count = 0;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    int64_t ns = 0, nt = 0;
+    std::vector<double> h_spos, h_snrm, h_tpos, h_tnrm;
+    std::vector<int32_t> h_cache;
+    std::vector<float> h_sfeat, h_tfeat;
+    double *d_spos = nullptr, *d_snrm = nullptr, *d_tpos = nullptr, *d_tnrm = nullptr;
+    int32_t* d_cache = nullptr;
+    lkk::GridStorage grid;
+    lkk::RunBuffers rb;
+    lk_reg_record* d_record = nullptr;
+    double prepare_seconds = 0.0;
+    bool profile = false;
+    std::vector<std::array<cudaEvent_t, 4>> pending;
+    double kernel_ms[3] = {0, 0, 0};
+    int64_t profiled_runs = 0;
+    std::mutex mu;
+    void drain_events() {
+        for (auto& ev : pending) {
+            cudaEventSynchronize(ev[3]);
+            for (int k = 0; k < 3; ++k) {
+                float ms = 0.f;
+                cudaEventElapsedTime(&ms, ev[k], ev[k + 1]);
+                kernel_ms[k] += ms;
+            }
+            for (auto e : ev) cudaEventDestroy(e);
+            profiled_runs += 1;
+        }
+        pending.clear();
+    }
+    ~lk_reg_ctx() {
+        cudaSetDevice(device);
+        drain_events();
+        cudaFree(d_spos);
+        cudaFree(d_snrm);
+        cudaFree(d_tpos);
+        cudaFree(d_tnrm);
+        cudaFree(d_cache);
+        grid.release();
+        rb.release();
+        cudaFree(d_record);
+        if (own_stream) cudaStreamDestroy(own_stream);
+    }
+};
+
+namespace {
+
+// Uploads the prepared clouds + cache and builds the EvalGrid on the device.
+void ctx_finish(lk_reg_ctx* c, const lk_reg_params& p) {
+    cudaStream_t s = c->stream;
+    c->d_spos = dev_upload(c->h_spos.data(), c->h_spos.size(), s);
+    c->d_snrm = dev_upload(c->h_snrm.data(), c->h_snrm.size(), s);
+    c->d_tpos = dev_upload(c->h_tpos.data(), c->h_tpos.size(), s);
+    c->d_tnrm = dev_upload(c->h_tnrm.data(), c->h_tnrm.size(), s);
+    if (!c->d_cache) c->d_cache = dev_upload(c->h_cache.data(), c->h_cache.size(), s);
+    CK(cudaMalloc(&c->d_record, sizeof(lk_reg_record)));
+    CK(lkk::build_grid(c->grid, 0, c->d_tpos, c->d_tnrm, c->nt, p.d_max, p.d_max, s));
+}
+
+lk_reg_ctx* ctx_new(int32_t device) {
+    auto* c = new lk_reg_ctx();
+    try {
+        c->device = select_device(device);
+        c->sm_count = sm_count_of(c->device);
+        CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+        c->stream = c->own_stream;
+    } catch (...) {
+        delete c;
+        throw;
+    }
+    return c;
+}
+
+lk_status prepare_impl(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_params* params, lk_reg_ctx** out) {
+    if (!params || !out) return fail(LK_INVALID_ARGUMENT, "null argument");
+    check_cloud_ptr(src, "source");
+    check_cloud_ptr(tgt, "target");
+    *out = nullptr;
+    double t0 = now_s();
+    // registration.cpp:226-231
+    lk::Cloud s = lk::voxel_downsample(lk::make_cloud(src->xyz, src->nxyz, src->n), params->leaf);
+    lk::Cloud t = lk::voxel_downsample(lk::make_cloud(tgt->xyz, tgt->nxyz, tgt->n), params->leaf);
+    if (s.size() < 4 || t.size() < 4)
+        return fail(LK_TOO_FEW_POINTS, "register_global: fewer than 4 points after downsampling");
+    if (!s.has_normals() || !t.has_normals())
+        return fail(LK_MISSING_NORMALS,
+                    "register_global: inputs without normals need estimate_normals (not in this tier)");
+    auto usable = [](const lk::Cloud& c) {
+        size_t k = 0;
+        for (const lk::Vec3& n : c.nrm) k += lk::is_zero(n) ? 0u : 1u;
+        return k;
+    };
+    if (usable(s) < 4 || usable(t) < 4)
+        return fail(LK_MISSING_DATA, "register_global: fewer than 4 points with usable normals");
+    auto sf = lk::compute_fpfh(s, params->feature_radius, params->threads);
+    auto tf = lk::compute_fpfh(t, params->feature_radius, params->threads);
+    lk_reg_ctx* c = ctx_new(params->device);
+    try {
+        c->ns = static_cast<int64_t>(s.size());
+        c->nt = static_cast<int64_t>(t.size());
+        c->h_spos = flatten(s.pos);
+        c->h_snrm = flatten(s.nrm);
+        c->h_tpos = flatten(t.pos);
+        c->h_tnrm = flatten(t.nrm);
+        c->h_sfeat.resize(33 * sf.size());
+        c->h_tfeat.resize(33 * tf.size());
+        for (size_t i = 0; i < sf.size(); ++i) std::memcpy(&c->h_sfeat[33 * i], sf[i].data(), 33 * sizeof(float));
+        for (size_t i = 0; i < tf.size(); ++i) std::memcpy(&c->h_tfeat[33 * i], tf[i].data(), 33 * sizeof(float));
+        // feature pre-match on the device (registration.cpp:248)
+        float* d_sf = dev_upload(c->h_sfeat.data(), c->h_sfeat.size(), c->stream);
+        float* d_tf = dev_upload(c->h_tfeat.data(), c->h_tfeat.size(), c->stream);
+        CK(cudaMalloc(&c->d_cache, c->ns * sizeof(int32_t)));
+        CK(lkk::feature_nn(d_sf, c->ns, d_tf, c->nt, c->d_cache, c->stream));
+        c->h_cache.resize(c->ns);
+        CK(cudaMemcpyAsync(c->h_cache.data(), c->d_cache, c->ns * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        cudaFree(d_sf);
+        cudaFree(d_tf);
+        ctx_finish(c, *params);
+    } catch (...) {
+        delete c;
+        throw;
+    }
+    c->prepare_seconds = now_s() - t0;
+    *out = c;
+    return LK_OK;
+}
+
+lk_status run_range_impl(lk_reg_ctx* c, const lk_reg_params& p, int64_t begin, int64_t end, void* d_record) {
+    if (c->ns < 4) return fail(LK_TOO_FEW_POINTS, "sample_quadruple: need >= 4 source points");
+    if (static_cast<int64_t>(c->h_cache.size()) != c->ns)
+        return fail(LK_MISSING_DATA, "sample_quadruple: cache size mismatch");
+    if (begin < 0 || end < begin) return fail(LK_INVALID_ARGUMENT, "bad hypothesis range");
+    CK(cudaSetDevice(c->device));
+    lkk::SourceView sv{c->d_spos, c->d_snrm, c->ns};
+    lkk::ScoreParams sp = score_params(p, c->ns, true, false);
+    cudaEvent_t* ev = nullptr;
+    if (c->profile) {
+        std::array<cudaEvent_t, 4> e4;
+        for (auto& e : e4) CK(cudaEventCreate(&e));
+        c->pending.push_back(e4);
+        ev = c->pending.back().data();
+    }
+    CK(lkk::run_hypotheses_range(sv, c->d_tpos, c->d_cache, c->grid.view, sp, p.seed, p.similarity_tau, begin, end,
+                                 c->rb, d_record, c->stream, c->sm_count, ev));
+    return LK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int lk_abi_version(void) { return LK_ABI_VERSION; }
+const char* lk_last_error(void) { return g_err.c_str(); }
+
+int lk_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+lk_status lk_reg_prepare(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_params* params, lk_reg_ctx** out) {
+    return guarded([&] { return prepare_impl(src, tgt, params, out); });
+}
+
+lk_status lk_reg_ctx_create(const lk_cloud* src, const lk_cloud* tgt, const int32_t* cache,
+                            const lk_reg_params* params, lk_reg_ctx** out) {
+    return guarded([&]() -> lk_status {
+        if (!params || !out || !cache) return fail(LK_INVALID_ARGUMENT, "null argument");
+        check_cloud_ptr(src, "source");
+        check_cloud_ptr(tgt, "target");
+        *out = nullptr;
+        if (src->n == 0 || tgt->n == 0) return fail(LK_EMPTY_CLOUD, "RegistrationContext: empty cloud");
+        if (!src->nxyz || !tgt->nxyz) return fail(LK_MISSING_NORMALS, "RegistrationContext: normals required");
+        for (int64_t i = 0; i < src->n; ++i)
+            if (cache[i] < 0 || cache[i] >= tgt->n)
+                return fail(LK_MISSING_DATA, "RegistrationContext: cache index out of range");
+        lk_reg_ctx* c = ctx_new(params->device);
+        try {
+            c->ns = src->n;
+            c->nt = tgt->n;
+            c->h_spos.assign(src->xyz, src->xyz + 3 * src->n);
+            c->h_snrm.assign(src->nxyz, src->nxyz + 3 * src->n);
+            c->h_tpos.assign(tgt->xyz, tgt->xyz + 3 * tgt->n);
+            c->h_tnrm.assign(tgt->nxyz, tgt->nxyz + 3 * tgt->n);
+            c->h_cache.assign(cache, cache + src->n);
+            ctx_finish(c, *params);
+        } catch (...) {
+            delete c;
+            throw;
+        }
+        *out = c;
+        return LK_OK;
+    });
+}
+
+void lk_reg_ctx_destroy(lk_reg_ctx* ctx) { delete ctx; }
+
+lk_status lk_reg_ctx_set_stream(lk_reg_ctx* ctx, void* stream) {
+    if (!ctx) return fail(LK_INVALID_ARGUMENT, "null context");
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+    return LK_OK;
+}
+
+lk_status lk_reg_ctx_set_profiling(lk_reg_ctx* ctx, int32_t enable) {
+    if (!ctx) return fail(LK_INVALID_ARGUMENT, "null context");
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    ctx->profile = enable != 0;
+    return LK_OK;
+}
+
+lk_status lk_reg_ctx_kernel_times(lk_reg_ctx* ctx, double* ms3, int64_t* runs, int32_t reset) {
+    if (!ctx) return fail(LK_INVALID_ARGUMENT, "null context");
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    cudaSetDevice(ctx->device);
+    ctx->drain_events();
+    if (ms3)
+        for (int k = 0; k < 3; ++k) ms3[k] = ctx->kernel_ms[k];
+    if (runs) *runs = ctx->profiled_runs;
+    if (reset) {
+        for (double& v : ctx->kernel_ms) v = 0.0;
+        ctx->profiled_runs = 0;
+    }
+    return LK_OK;
+}
+
+lk_status lk_reg_ctx_sizes(const lk_reg_ctx* ctx, int64_t* n_source, int64_t* n_target) {
+    if (!ctx) return fail(LK_INVALID_ARGUMENT, "null context");
+    if (n_source) *n_source = ctx->ns;
+    if (n_target) *n_target = ctx->nt;
+    return LK_OK;
+}
+
+lk_status lk_reg_ctx_download(const lk_reg_ctx* c, double* src_xyz, double* src_n, double* tgt_xyz, double* tgt_n,
+                              int32_t* cache, float* src_features, float* tgt_features) {
+    if (!c) return fail(LK_INVALID_ARGUMENT, "null context");
+    auto cp = [](void* dst, const void* s, size_t bytes) {
+        if (dst && bytes) std::memcpy(dst, s, bytes);
+    };
+    cp(src_xyz, c->h_spos.data(), c->h_spos.size() * sizeof(double));
+    cp(src_n, c->h_snrm.data(), c->h_snrm.size() * sizeof(double));
+    cp(tgt_xyz, c->h_tpos.data(), c->h_tpos.size() * sizeof(double));
+    cp(tgt_n, c->h_tnrm.data(), c->h_tnrm.size() * sizeof(double));
+    cp(cache, c->h_cache.data(), c->h_cache.size() * sizeof(int32_t));
+    cp(src_features, c->h_sfeat.data(), c->h_sfeat.size() * sizeof(float));
+    cp(tgt_features, c->h_tfeat.data(), c->h_tfeat.size() * sizeof(float));
+    return LK_OK;
+}
+
+lk_status lk_reg_run_range(lk_reg_ctx* ctx, const lk_reg_params* params, int64_t begin, int64_t end,
+                           lk_reg_record* record, int32_t record_on_device) {
+    return guarded([&]() -> lk_status {
+        if (!ctx || !params || !record) return fail(LK_INVALID_ARGUMENT, "null argument");
+        std::lock_guard<std::mutex> lock(ctx->mu);
+        void* target = record_on_device ? static_cast<void*>(record) : static_cast<void*>(ctx->d_record);
+        lk_status st = run_range_impl(ctx, *params, begin, end, target);
+        if (st != LK_OK) return st;
+        if (!record_on_device) {
+            CK(cudaMemcpyAsync(record, ctx->d_record, sizeof(lk_reg_record), cudaMemcpyDeviceToHost, ctx->stream));
+            CK(cudaStreamSynchronize(ctx->stream));
+        }
+        return LK_OK;
+    });
+}
+
+lk_status lk_reg_merge_records(const lk_reg_record* records, int32_t count, int64_t n_source, lk_reg_result* result,
+                               lk_hyp_stats* stats) {
+    if (!records || count <= 0 || !result || n_source <= 0) return fail(LK_INVALID_ARGUMENT, "bad merge arguments");
+    const lk_reg_record* best = nullptr;
+    lk_hyp_stats st{};
+    for (int32_t g = 0; g < count; ++g) {
+        const lk_reg_record& r = records[g];
+        st.sampled += r.sampled;
+        st.prerejected += r.prerejected;
+        st.degenerate += r.degenerate;
+        st.evaluated += r.evaluated;
+        st.qualified += r.qualified;
+        st.w_ref += r.w_ref;
+        st.evals_executed += r.evals_executed;
+        if (r.valid && (!best || record_better(r, *best))) best = &r;
+    }
+    lk_reg_record none{};
+    record_to_result(best ? *best : none, n_source, result);
+    if (stats) {
+        double ps = stats->prepare_seconds, hs = stats->hypothesis_seconds;
+        *stats = st;
+        stats->prepare_seconds = ps;
+        stats->hypothesis_seconds = hs;
+    }
+    return result->found ? LK_OK : LK_NO_ALIGNMENT;
+}
+
+lk_status lk_reg_run_hypotheses(lk_reg_ctx* ctx, const lk_reg_params* params, lk_reg_result* result,
+                                lk_hyp_stats* stats) {
+    return guarded([&]() -> lk_status {
+        if (!ctx || !params || !result) return fail(LK_INVALID_ARGUMENT, "null argument");
+        if (params->hypothesis_count < 0) return fail(LK_INVALID_ARGUMENT, "negative hypothesis_count");
+        std::lock_guard<std::mutex> lock(ctx->mu);
+        double t0 = now_s();
+        lk_status st = run_range_impl(ctx, *params, 0, params->hypothesis_count, ctx->d_record);
+        if (st != LK_OK) return st;
+        lk_reg_record rec{};
+        CK(cudaMemcpyAsync(&rec, ctx->d_record, sizeof(rec), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        double t1 = now_s();
+        lk_hyp_stats local{};
+        lk_hyp_stats* sp = stats ? stats : &local;
+        double prep = sp->prepare_seconds;
+        lk_status ms = lk_reg_merge_records(&rec, 1, ctx->ns, result, sp);
+        sp->prepare_seconds = prep;
+        sp->hypothesis_seconds = t1 - t0;
+        return ms;
+    });
+}
+
+lk_status lk_register_global(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_params* params,
+                             lk_reg_result* result, lk_hyp_stats* stats) {
+    lk_reg_ctx* ctx = nullptr;
+    lk_status st = lk_reg_prepare(src, tgt, params, &ctx);
+    if (st != LK_OK) return st;
+    lk_hyp_stats local{};
+    lk_hyp_stats* sp = stats ? stats : &local;
+    sp->prepare_seconds = ctx->prepare_seconds;
+    st = lk_reg_run_hypotheses(ctx, params, result, sp);
+    std::string keep = g_err;
+    lk_reg_ctx_destroy(ctx);
+    g_err = keep;
+    return st;
+}
+
+lk_status lk_grid_build(const lk_cloud* target, int32_t kind, double cell, double d_max, int32_t device,
+                        lk_grid** out) {
+    return guarded([&]() -> lk_status {
+        if (!out) return fail(LK_INVALID_ARGUMENT, "null argument");
+        check_cloud_ptr(target, "target");
+        *out = nullptr;
+        if (target->n == 0) return fail(LK_EMPTY_CLOUD, "build_grid: empty cloud");
+        if (kind != 0 && kind != 1) return fail(LK_INVALID_ARGUMENT, "grid kind must be 0 or 1");
+        if (kind == 0) cell = d_max;
+        if (!(cell > 0.0)) return fail(LK_INVALID_ARGUMENT, "build_grid: cell_length must be positive");
+        if (!(d_max > 0.0)) return fail(LK_INVALID_ARGUMENT, "build_grid: d_max must be positive");
+        auto* g = new lk_grid();
+        try {
+            g->device = select_device(device);
+            g->sm_count = sm_count_of(g->device);
+            g->kind = kind;
+            g->cell = cell;
+            g->d_max = d_max;
+            g->has_normals = target->nxyz != nullptr;
+            CK(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+            double* d_pos = dev_upload(target->xyz, 3 * target->n, g->stream);
+            double* d_nrm = target->nxyz ? dev_upload(target->nxyz, 3 * target->n, g->stream) : nullptr;
+            cudaError_t e = lkk::build_grid(g->g, kind, d_pos, d_nrm, target->n, cell, d_max, g->stream);
+            cudaFree(d_pos);
+            cudaFree(d_nrm);
+            CK(e);
+            CK(cudaMalloc(&g->d_record, sizeof(lk_reg_record)));
+        } catch (...) {
+            delete g;
+            throw;
+        }
+        *out = g;
+        return LK_OK;
+    });
+}
+
+void lk_grid_destroy(lk_grid* grid) { delete grid; }
+
+lk_status lk_grid_dims(const lk_grid* grid, double* origin3, double* cell, int32_t* dims3, int64_t* ncells,
+                       int64_t* npoints) {
+    if (!grid) return fail(LK_INVALID_ARGUMENT, "null grid");
+    const lkk::GridView& v = grid->g.view;
+    if (origin3) {
+        origin3[0] = v.ox;
+        origin3[1] = v.oy;
+        origin3[2] = v.oz;
+    }
+    if (cell) *cell = v.cell;
+    if (dims3) {
+        dims3[0] = v.nx;
+        dims3[1] = v.ny;
+        dims3[2] = v.nz;
+    }
+    if (ncells) *ncells = grid->g.ncells;
+    if (npoints) *npoints = grid->g.npoints;
+    return LK_OK;
+}
+
+lk_status lk_grid_download(const lk_grid* grid, int32_t* start, int32_t* index, double* slot_xyz, double* slot_n,
+                           uint8_t* near_occupied) {
+    return guarded([&]() -> lk_status {
+        if (!grid) return fail(LK_INVALID_ARGUMENT, "null grid");
+        CK(cudaSetDevice(grid->device));
+        const lkk::GridStorage& g = grid->g;
+        if (start) CK(cudaMemcpy(start, g.start, (g.ncells + 1) * sizeof(int32_t), cudaMemcpyDeviceToHost));
+        if (index) CK(cudaMemcpy(index, g.index, g.npoints * sizeof(int32_t), cudaMemcpyDeviceToHost));
+        if (slot_xyz) CK(cudaMemcpy(slot_xyz, g.slot_pos, 3 * g.npoints * sizeof(double), cudaMemcpyDeviceToHost));
+        if (slot_n) CK(cudaMemcpy(slot_n, g.slot_nrm, 3 * g.npoints * sizeof(double), cudaMemcpyDeviceToHost));
+        if (near_occupied) CK(cudaMemcpy(near_occupied, g.near, g.ncells, cudaMemcpyDeviceToHost));
+        return LK_OK;
+    });
+}
+
+lk_status lk_score_candidates(lk_grid* grid, const lk_cloud* src, const double* Rt, int64_t C,
+                              const lk_reg_params* params, int32_t early_exit, lk_cand_score* per_cand,
+                              lk_reg_result* best, int64_t* qualified) {
+    return guarded([&]() -> lk_status {
+        if (!grid || !params) return fail(LK_INVALID_ARGUMENT, "null argument");
+        check_cloud_ptr(src, "source");
+        if (C < 0 || (C > 0 && !Rt)) return fail(LK_INVALID_ARGUMENT, "bad candidate list");
+        if (src->n == 0) return fail(LK_EMPTY_CLOUD, "evaluate_hypothesis: empty cloud");
+        if (!src->nxyz || !grid->has_normals)
+            return fail(LK_MISSING_NORMALS, "evaluate_hypothesis: both clouds need normals");
+        std::lock_guard<std::mutex> lock(grid->mu);
+        CK(cudaSetDevice(grid->device));
+        cudaStream_t s = grid->stream;
+        const int64_t ns = src->n;
+        double* d_pos = dev_upload(src->xyz, 3 * ns, s);
+        double* d_nrm = dev_upload(src->nxyz, 3 * ns, s);
+        double* d_rt = dev_upload(Rt, 12 * static_cast<size_t>(C), s);
+        int64_t* d_inl = nullptr;
+        double* d_sum = nullptr;
+        CK(cudaMalloc(&d_inl, std::max<int64_t>(C, 1) * sizeof(int64_t)));
+        CK(cudaMalloc(&d_sum, std::max<int64_t>(C, 1) * sizeof(double)));
+        lkk::SourceView sv{d_pos, d_nrm, ns};
+        lkk::ScoreParams sp = score_params(*params, ns, early_exit != 0, grid->kind == 1);
+        lk_reg_record rec{};
+        std::vector<int64_t> inl(C);
+        std::vector<double> sum(C);
+        cudaError_t e = lkk::score_candidates(sv, grid->g.view, sp, d_rt, C, grid->rb, d_inl, d_sum, grid->d_record,
+                                              s, grid->sm_count);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(&rec, grid->d_record, sizeof(rec), cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess && C)
+            e = cudaMemcpyAsync(inl.data(), d_inl, C * sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess && C) e = cudaMemcpyAsync(sum.data(), d_sum, C * sizeof(double), cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        cudaFree(d_pos);
+        cudaFree(d_nrm);
+        cudaFree(d_rt);
+        cudaFree(d_inl);
+        cudaFree(d_sum);
+        CK(e);
+        if (per_cand) {
+            for (int64_t k = 0; k < C; ++k) {
+                lk_cand_score& o = per_cand[k];
+                o.inliers = inl[k];
+                if (inl[k] < 0) {
+                    o.inlier_ratio = 0.0;
+                    o.fitness = 0.0;
+                } else {
+                    o.inlier_ratio = static_cast<double>(inl[k]) / static_cast<double>(ns);
+                    o.fitness = inl[k] > 0 ? sum[k] / static_cast<double>(inl[k]) : 0.0;
+                }
+            }
+        }
+        if (qualified) *qualified = rec.qualified;
+        if (best) record_to_result(rec, ns, best);
+        return LK_OK;
+    });
+}
+
+lk_status lk_edge_info_batched(const lk_cloud* clouds_i, const lk_cloud* clouds_j, const double* Ti, const double* Tj,
+                               int64_t n_pairs, double epsilon, int32_t device, double* info, int64_t* pair_count) {
+    return guarded([&]() -> lk_status {
+        if (n_pairs < 0 || (n_pairs > 0 && (!clouds_i || !clouds_j || !Ti || !Tj || !info || !pair_count)))
+            return fail(LK_INVALID_ARGUMENT, "null argument");
+        if (!(epsilon > 0.0)) return fail(LK_INVALID_ARGUMENT, "build_grid: cell_length must be positive");
+        int dev = select_device(device);
+        int sms = sm_count_of(dev);
+        cudaStream_t s;
+        CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        const int nb = sms * 2;
+        double *d_part = nullptr, *d_info = nullptr;
+        unsigned long long* d_count = nullptr;
+        lk_status result = LK_OK;
+        try {
+            CK(cudaMalloc(&d_part, nb * 9 * sizeof(double)));
+            CK(cudaMalloc(&d_info, 36 * sizeof(double)));
+            CK(cudaMalloc(&d_count, sizeof(unsigned long long)));
+            for (int64_t k = 0; k < n_pairs; ++k) {
+                const lk_cloud& ci = clouds_i[k];
+                const lk_cloud& cj = clouds_j[k];
+                check_cloud_ptr(&ci, "cloud_i");
+                check_cloud_ptr(&cj, "cloud_j");
+                if (ci.n == 0 || cj.n == 0) {
+                    result = fail(LK_EMPTY_CLOUD, "edge_info: empty cloud");
+                    break;
+                }
+                double* d_ci = dev_upload(ci.xyz, 3 * ci.n, s);
+                double* d_cj = dev_upload(cj.xyz, 3 * cj.n, s);
+                double* d_posed = nullptr;
+                CK(cudaMalloc(&d_posed, 3 * cj.n * sizeof(double)));
+                CK(lkk::transform_points(d_cj, cj.n, Tj + 12 * k, d_posed, s));
+                lkk::GridStorage g;
+                cudaError_t e = lkk::build_grid(g, 1, d_posed, nullptr, cj.n, epsilon, epsilon, s);
+                if (e == cudaSuccess)
+                    e = lkk::edge_info(d_ci, ci.n, Ti + 12 * k, g.view, epsilon, d_part, nb, d_info, d_count, s);
+                unsigned long long cnt = 0;
+                if (e == cudaSuccess)
+                    e = cudaMemcpyAsync(info + 36 * k, d_info, 36 * sizeof(double), cudaMemcpyDeviceToHost, s);
+                if (e == cudaSuccess) e = cudaMemcpyAsync(&cnt, d_count, sizeof(cnt), cudaMemcpyDeviceToHost, s);
+                if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+                g.release();
+                cudaFree(d_ci);
+                cudaFree(d_cj);
+                cudaFree(d_posed);
+                CK(e);
+                pair_count[k] = static_cast<int64_t>(cnt);
+                if (cnt == 0)
+                    for (int q = 0; q < 36; ++q) info[36 * k + q] = 0.0;
+            }
+        } catch (...) {
+            cudaFree(d_part);
+            cudaFree(d_info);
+            cudaFree(d_count);
+            cudaStreamDestroy(s);
+            throw;
+        }
+        cudaFree(d_part);
+        cudaFree(d_info);
+        cudaFree(d_count);
+        cudaStreamDestroy(s);
+        return result;
+    });
+}
+
+lk_status lk_feature_nn_cache(const float* src_features, int64_t ns, const float* tgt_features, int64_t nt,
+                              int32_t device, int32_t* cache) {
+    return guarded([&]() -> lk_status {
+        if (ns <= 0 || nt <= 0) return fail(LK_MISSING_DATA, "feature_nn_cache: empty feature set");
+        if (!src_features || !tgt_features || !cache) return fail(LK_INVALID_ARGUMENT, "null argument");
+        select_device(device);
+        cudaStream_t s;
+        CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        float* d_sf = dev_upload(src_features, 33 * ns, s);
+        float* d_tf = dev_upload(tgt_features, 33 * nt, s);
+        int32_t* d_out = nullptr;
+        cudaError_t e = cudaMalloc(&d_out, ns * sizeof(int32_t));
+        if (e == cudaSuccess) e = lkk::feature_nn(d_sf, ns, d_tf, nt, d_out, s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(cache, d_out, ns * sizeof(int32_t), cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        cudaFree(d_sf);
+        cudaFree(d_tf);
+        cudaFree(d_out);
+        cudaStreamDestroy(s);
+        CK(e);
+        return LK_OK;
+    });
+}
+
+lk_status lk_voxel_downsample(const lk_cloud* cloud, double leaf, double* out_xyz, double* out_n, int64_t* out_count) {
+    return guarded([&]() -> lk_status {
+        check_cloud_ptr(cloud, "cloud");
+        if (!out_xyz || !out_count) return fail(LK_INVALID_ARGUMENT, "null argument");
+        lk::Cloud d = lk::voxel_downsample(lk::make_cloud(cloud->xyz, cloud->nxyz, cloud->n), leaf);
+        for (size_t i = 0; i < d.size(); ++i) {
+            lk::store3(out_xyz, static_cast<int64_t>(i), d.pos[i]);
+            if (out_n && d.has_normals()) lk::store3(out_n, static_cast<int64_t>(i), d.nrm[i]);
+        }
+        *out_count = static_cast<int64_t>(d.size());
+        return LK_OK;
+    });
+}
+
+lk_status lk_compute_fpfh(const lk_cloud* cloud, double radius, int32_t threads, float* out) {
+    return guarded([&]() -> lk_status {
+        check_cloud_ptr(cloud, "cloud");
+        if (!out) return fail(LK_INVALID_ARGUMENT, "null argument");
+        auto f = lk::compute_fpfh(lk::make_cloud(cloud->xyz, cloud->nxyz, cloud->n), radius, threads);
+        for (size_t i = 0; i < f.size(); ++i) std::memcpy(out + 33 * i, f[i].data(), 33 * sizeof(float));
+        return LK_OK;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,361 @@
+// lk_grid.cu -- device construction of the target cell grid (K6 in SURVEY.md 2.2).
+//
+// EvalGrid (proj/src/registration.cpp:80-148) and the SearchGrid cell
+// convention (proj/src/grid.cpp:26-66) built on the device as a dense CSR:
+// bbox / cell-bounds reduction -> per-point cell -> count -> exclusive scan ->
+// scatter -> per-cell sort by original index (the reference's CSR order) ->
+// slot payload gather -> occupancy dilation.
+#include <cmath>
+#include <cstdint>
+#include <vector>
+
+#include "lk_kernels.cuh"
+
+namespace lkk {
+
+namespace {
+
+constexpr int kScanThreads = 1024;
+constexpr int kScanItems = 4;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__global__ void k_bbox(const double* __restrict__ pos, int64_t n, double* __restrict__ out6) {
+    __shared__ double s_lo[3][32], s_hi[3][32];
+    double lo[3], hi[3];
+    for (int a = 0; a < 3; ++a) {
+        lo[a] = pos[a];
+        hi[a] = pos[a];
+    }
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        for (int a = 0; a < 3; ++a) {
+            double v = pos[3 * i + a];
+            lo[a] = v < lo[a] ? v : lo[a];
+            hi[a] = hi[a] < v ? v : hi[a];
+        }
+    }
+    for (int a = 0; a < 3; ++a) {
+        for (int o = 16; o > 0; o >>= 1) {
+            double l = __shfl_xor_sync(0xffffffffu, lo[a], o);
+            double h = __shfl_xor_sync(0xffffffffu, hi[a], o);
+            lo[a] = l < lo[a] ? l : lo[a];
+            hi[a] = hi[a] < h ? h : hi[a];
+        }
+    }
+    int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    if (lane == 0)
+        for (int a = 0; a < 3; ++a) {
+            s_lo[a][warp] = lo[a];
+            s_hi[a][warp] = hi[a];
+        }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int a = 0; a < 3; ++a) {
+            double l = s_lo[a][0], h = s_hi[a][0];
+            for (int w = 1; w < nw; ++w) {
+                l = s_lo[a][w] < l ? s_lo[a][w] : l;
+                h = h < s_hi[a][w] ? s_hi[a][w] : h;
+            }
+            out6[a] = l;
+            out6[3 + a] = h;
+        }
+    }
+}
+
+__device__ __forceinline__ int floor_cell(double q) {
+    double f = floor(q);
+    if (!(f >= -2147483648.0 && f < 2147483648.0)) return INT32_MIN;
+    return static_cast<int>(f);
+}
+
+// SearchGrid cells of every point: min / max over floor((p - 0) / cell)
+__global__ void k_cell_bounds(const double* __restrict__ pos, int64_t n, double cell, int* __restrict__ out6) {
+    __shared__ int s[6];
+    if (threadIdx.x < 3) {
+        s[threadIdx.x] = INT32_MAX;
+        s[3 + threadIdx.x] = INT32_MIN;
+    }
+    __syncthreads();
+    int lo[3] = {INT32_MAX, INT32_MAX, INT32_MAX}, hi[3] = {INT32_MIN, INT32_MIN, INT32_MIN};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        for (int a = 0; a < 3; ++a) {
+            int c = floor_cell((pos[3 * i + a] - 0.0) / cell);
+            lo[a] = min(lo[a], c);
+            hi[a] = max(hi[a], c);
+        }
+    }
+    for (int a = 0; a < 3; ++a) {
+        atomicMin(&s[a], lo[a]);
+        atomicMax(&s[3 + a], hi[a]);
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        atomicMin(&out6[threadIdx.x], s[threadIdx.x]);
+        atomicMax(&out6[3 + threadIdx.x], s[3 + threadIdx.x]);
+    }
+}
+
+__global__ void k_cell_of(const double* __restrict__ pos, int64_t n, GridView g, int32_t* __restrict__ cell_of,
+                          int32_t* __restrict__ counts) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int kx = floor_cell((pos[3 * i + 0] - g.ox) / g.cell) - g.offx;
+    int ky = floor_cell((pos[3 * i + 1] - g.oy) / g.cell) - g.offy;
+    int kz = floor_cell((pos[3 * i + 2] - g.oz) / g.cell) - g.offz;
+    int32_t c = (kx * g.ny + ky) * g.nz + kz;
+    cell_of[i] = c;
+    atomicAdd(&counts[c], 1);
+}
+
+// Block-level exclusive scan of kScanTile counts; writes block totals.
+__global__ void k_scan_tiles(const int32_t* __restrict__ in, int64_t n, int32_t* __restrict__ out,
+                             int32_t* __restrict__ block_sums) {
+    __shared__ int32_t s_warp[32];
+    int64_t base = blockIdx.x * (int64_t)kScanTile + threadIdx.x * kScanItems;
+    int32_t v[kScanItems];
+    int32_t local = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        v[k] = (base + k < n) ? in[base + k] : 0;
+        local += v[k];
+    }
+    int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int32_t incl = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        int32_t w = s_warp[lane];
+        int32_t wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += y;
+        }
+        s_warp[lane] = wi - w;
+        if (lane == 31) block_sums[blockIdx.x] = wi;
+    }
+    __syncthreads();
+    int32_t run = s_warp[warp] + incl - local;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        if (base + k < n) out[base + k] = run;
+        run += v[k];
+    }
+}
+
+// Exclusive scan of the block totals in one block; writes the grand total.
+__global__ void k_scan_block_sums(int32_t* __restrict__ sums, int64_t nb, int32_t* __restrict__ total_out) {
+    __shared__ int32_t s_warp[32];
+    __shared__ int32_t s_carry;
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int64_t base = 0; base < nb; base += blockDim.x) {
+        int64_t i = base + threadIdx.x;
+        int32_t v = i < nb ? sums[i] : 0;
+        int32_t incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) s_warp[warp] = incl;
+        __syncthreads();
+        if (warp == 0) {
+            int32_t w = s_warp[lane];
+            int32_t wi = w;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int32_t y = __shfl_up_sync(0xffffffffu, wi, o);
+                if (lane >= o) wi += y;
+            }
+            s_warp[lane] = wi - w;
+        }
+        __syncthreads();
+        int32_t excl = s_carry + s_warp[warp] + incl - v;
+        if (i < nb) sums[i] = excl;
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) s_carry = excl + v;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *total_out = s_carry;
+}
+
+__global__ void k_scan_add(int32_t* __restrict__ out, int64_t n, const int32_t* __restrict__ block_offsets) {
+    int64_t base = blockIdx.x * (int64_t)kScanTile + threadIdx.x * kScanItems;
+    int32_t off = block_offsets[blockIdx.x];
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k)
+        if (base + k < n) out[base + k] += off;
+}
+
+__global__ void k_scatter(const int32_t* __restrict__ cell_of, int64_t n, const int32_t* __restrict__ start,
+                          int32_t* __restrict__ cursor, int32_t* __restrict__ index) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int32_t c = cell_of[i];
+    int32_t slot = start[c] + atomicAdd(&cursor[c], 1);
+    index[slot] = static_cast<int32_t>(i);
+}
+
+// Restores the reference's ascending-index order within every cell.
+__global__ void k_sort_cells(const int32_t* __restrict__ start, int64_t ncells, int32_t* __restrict__ index) {
+    int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= ncells) return;
+    int32_t s0 = start[c], s1 = start[c + 1];
+    for (int32_t a = s0 + 1; a < s1; ++a) {
+        int32_t v = index[a];
+        int32_t b = a - 1;
+        while (b >= s0 && index[b] > v) {
+            index[b + 1] = index[b];
+            --b;
+        }
+        index[b + 1] = v;
+    }
+}
+
+__global__ void k_gather_slots(const int32_t* __restrict__ index, int64_t n, const double* __restrict__ pos,
+                               const double* __restrict__ nrm, double* __restrict__ slot_pos,
+                               double* __restrict__ slot_nrm) {
+    int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    int64_t i = index[s];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        slot_pos[3 * s + a] = pos[3 * i + a];
+        slot_nrm[3 * s + a] = nrm ? nrm[3 * i + a] : 0.0;
+    }
+}
+
+__global__ void k_dilate(const int32_t* __restrict__ cell_of, int64_t n, GridView g, uint8_t* __restrict__ near) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int32_t c = cell_of[i];
+    int kz = c % g.nz;
+    int ky = (c / g.nz) % g.ny;
+    int kx = c / (g.nz * g.ny);
+    int r = g.radius;
+    for (int x = max(kx - r, 0); x <= min(kx + r, g.nx - 1); ++x)
+        for (int y = max(ky - r, 0); y <= min(ky + r, g.ny - 1); ++y)
+            for (int z = max(kz - r, 0); z <= min(kz + r, g.nz - 1); ++z) near[(x * g.ny + y) * g.nz + z] = 1;
+}
+
+inline unsigned blocks_for(int64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
+
+}  // namespace
+
+void GridStorage::release() {
+    cudaFree(start);
+    cudaFree(index);
+    cudaFree(slot_pos);
+    cudaFree(slot_nrm);
+    cudaFree(near);
+    start = index = nullptr;
+    slot_pos = slot_nrm = nullptr;
+    near = nullptr;
+}
+
+#define LK_TRY(x)                                \
+    do {                                         \
+        cudaError_t e_ = (x);                    \
+        if (e_ != cudaSuccess) return e_;        \
+    } while (0)
+
+cudaError_t build_grid(GridStorage& g, int kind, const double* d_pos, const double* d_nrm, int64_t n, double cell,
+                       double d_max, cudaStream_t stream) {
+    if (n <= 0 || n > INT32_MAX) return cudaErrorInvalidValue;
+    GridView v{};
+    v.kind = kind;
+    v.cell = cell;
+    if (kind == 0) {
+        // proj/src/registration.cpp:82-97
+        double* d_box = nullptr;
+        LK_TRY(cudaMallocAsync(&d_box, 6 * sizeof(double), stream));
+        k_bbox<<<1, 1024, 0, stream>>>(d_pos, n, d_box);
+        double box[6];
+        LK_TRY(cudaMemcpyAsync(box, d_box, sizeof(box), cudaMemcpyDeviceToHost, stream));
+        LK_TRY(cudaStreamSynchronize(stream));
+        cudaFreeAsync(d_box, stream);
+        double origin[3];
+        int dims[3];
+        for (int a = 0; a < 3; ++a) {
+            origin[a] = box[a] - cell;
+            double extent = (box[3 + a] - origin[a]) + cell;
+            dims[a] = static_cast<int>(std::floor(extent / cell)) + 2;
+        }
+        v.ox = origin[0];
+        v.oy = origin[1];
+        v.oz = origin[2];
+        v.nx = dims[0];
+        v.ny = dims[1];
+        v.nz = dims[2];
+        v.offx = v.offy = v.offz = 0;
+        v.radius = 1;
+    } else {
+        // proj/src/grid.cpp:38-47 with center 0; dense over the occupied box + r
+        int* d_b = nullptr;
+        LK_TRY(cudaMallocAsync(&d_b, 6 * sizeof(int), stream));
+        int init[6] = {INT32_MAX, INT32_MAX, INT32_MAX, INT32_MIN, INT32_MIN, INT32_MIN};
+        LK_TRY(cudaMemcpyAsync(d_b, init, sizeof(init), cudaMemcpyHostToDevice, stream));
+        k_cell_bounds<<<std::min<unsigned>(blocks_for(n, 256), 592), 256, 0, stream>>>(d_pos, n, cell, d_b);
+        int b[6];
+        LK_TRY(cudaMemcpyAsync(b, d_b, sizeof(b), cudaMemcpyDeviceToHost, stream));
+        LK_TRY(cudaStreamSynchronize(stream));
+        cudaFreeAsync(d_b, stream);
+        int r = static_cast<int>(std::ceil(d_max / cell));
+        v.ox = v.oy = v.oz = 0.0;
+        v.radius = r;
+        v.offx = b[0] - r;
+        v.offy = b[1] - r;
+        v.offz = b[2] - r;
+        v.nx = b[3] - b[0] + 1 + 2 * r;
+        v.ny = b[4] - b[1] + 1 + 2 * r;
+        v.nz = b[5] - b[2] + 1 + 2 * r;
+    }
+    int64_t ncells = static_cast<int64_t>(v.nx) * v.ny * v.nz;
+    if (ncells <= 0 || ncells > (int64_t)1 << 30) return cudaErrorInvalidValue;
+    g.ncells = ncells;
+    g.npoints = n;
+    LK_TRY(cudaMalloc(&g.start, (ncells + 1) * sizeof(int32_t)));
+    LK_TRY(cudaMalloc(&g.index, n * sizeof(int32_t)));
+    LK_TRY(cudaMalloc(&g.slot_pos, 3 * n * sizeof(double)));
+    LK_TRY(cudaMalloc(&g.slot_nrm, 3 * n * sizeof(double)));
+    LK_TRY(cudaMalloc(&g.near, ncells));
+    int32_t *d_cell_of = nullptr, *d_counts = nullptr, *d_bsums = nullptr;
+    int64_t ntiles = (ncells + kScanTile - 1) / kScanTile;
+    LK_TRY(cudaMallocAsync(&d_cell_of, n * sizeof(int32_t), stream));
+    LK_TRY(cudaMallocAsync(&d_counts, ncells * sizeof(int32_t), stream));
+    LK_TRY(cudaMallocAsync(&d_bsums, (ntiles + 1) * sizeof(int32_t), stream));
+    LK_TRY(cudaMemsetAsync(d_counts, 0, ncells * sizeof(int32_t), stream));
+    LK_TRY(cudaMemsetAsync(g.near, 0, ncells, stream));
+    k_cell_of<<<blocks_for(n, 256), 256, 0, stream>>>(d_pos, n, v, d_cell_of, d_counts);
+    k_scan_tiles<<<static_cast<unsigned>(ntiles), kScanThreads, 0, stream>>>(d_counts, ncells, g.start, d_bsums);
+    k_scan_block_sums<<<1, 1024, 0, stream>>>(d_bsums, ntiles, g.start + ncells);
+    k_scan_add<<<static_cast<unsigned>(ntiles), kScanThreads, 0, stream>>>(g.start, ncells, d_bsums);
+    LK_TRY(cudaMemsetAsync(d_counts, 0, ncells * sizeof(int32_t), stream));
+    k_scatter<<<blocks_for(n, 256), 256, 0, stream>>>(d_cell_of, n, g.start, d_counts, g.index);
+    k_sort_cells<<<blocks_for(ncells, 256), 256, 0, stream>>>(g.start, ncells, g.index);
+    k_gather_slots<<<blocks_for(n, 256), 256, 0, stream>>>(g.index, n, d_pos, d_nrm, g.slot_pos, g.slot_nrm);
+    if (kind == 0 || v.radius <= 2) {
+        k_dilate<<<blocks_for(n, 128), 128, 0, stream>>>(d_cell_of, n, v, g.near);
+    } else {
+        LK_TRY(cudaMemsetAsync(g.near, 1, ncells, stream));  // wide blocks: no occupancy shortcut
+    }
+    LK_TRY(cudaGetLastError());
+    cudaFreeAsync(d_cell_of, stream);
+    cudaFreeAsync(d_counts, stream);
+    cudaFreeAsync(d_bsums, stream);
+    v.start = g.start;
+    v.index = g.index;
+    v.slot_pos = g.slot_pos;
+    v.slot_nrm = g.slot_nrm;
+    v.near = g.near;
+    g.view = v;
+    return cudaStreamSynchronize(stream);
+}
+
+}  // namespace lkk

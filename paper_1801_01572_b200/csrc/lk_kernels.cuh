@@ -1,0 +1,125 @@
+// lk_kernels.cuh -- device data layout and kernel launchers.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace lkk {
+
+// Dense CSR cell grid over a target cloud.
+//  kind 0 = EvalGrid   (proj/src/registration.cpp:80-148): origin = bbox_lo - cell,
+//           cell = d_max, block radius 1, local cell = floor((y - origin) / cell).
+//  kind 1 = SearchGrid (proj/src/grid.cpp:26-109): cells floor((y - center) / cell)
+//           with center 0, stored densely over the occupied box padded by the
+//           block radius r = ceil(d_max / cell); local = cell - off.
+// Slots are sorted by cell, ascending original index inside a cell.
+struct GridView {
+    double ox, oy, oz;  // subtracted before the division (origin or center)
+    double cell;
+    int nx, ny, nz;
+    int offx, offy, offz;
+    int radius;
+    int kind;
+    const int32_t* start;    // ncells + 1
+    const int32_t* index;    // slot -> original target index
+    const double* slot_pos;  // 3 * npoints, CSR order
+    const double* slot_nrm;  // 3 * npoints, CSR order (zeros when absent)
+    const uint8_t* near;     // ncells: some point within the block of this cell
+};
+
+struct GridStorage {
+    GridView view{};
+    int64_t ncells = 0;
+    int64_t npoints = 0;
+    int32_t* start = nullptr;
+    int32_t* index = nullptr;
+    double* slot_pos = nullptr;
+    double* slot_nrm = nullptr;
+    uint8_t* near = nullptr;
+    void release();
+};
+
+// Builds a grid of the given kind from device arrays pos/nrm (nrm may be null).
+// Returns cudaSuccess or the first CUDA error; throws nothing.
+cudaError_t build_grid(GridStorage& g, int kind, const double* d_pos, const double* d_nrm, int64_t n, double cell,
+                       double d_max, cudaStream_t stream);
+
+// ---- hypothesis pipeline --------------------------------------------------
+struct Counters {  // device-side, zeroed per run
+    unsigned long long n_survivors;   // passed pre-rejection
+    unsigned long long n_candidates;  // non-degenerate (= evaluated)
+    unsigned long long prerejected;
+    unsigned long long degenerate;
+    unsigned long long qualified;
+    unsigned long long w_ref;
+    unsigned long long evals_executed;
+    unsigned long long work_next;   // work queue head for k_score
+    unsigned long long blocks_done; // last-block-done ticket
+    unsigned long long _pad[7];
+};
+
+struct BestRec {  // per-block best, then the final record
+    int64_t valid;
+    int64_t inliers;
+    double fitness;
+    int64_t index;
+    int64_t slot;  // candidate slot holding R, t
+};
+
+struct RunBuffers {
+    int64_t capacity = 0;        // hypotheses per launch chunk
+    int64_t* surv_index = nullptr;  // survivor hypothesis index
+    int32_t* surv_ids = nullptr;    // 8 per survivor: src[4], tgt[4]
+    int64_t* cand_index = nullptr;  // candidate hypothesis index
+    double* cand_rt = nullptr;      // 12 per candidate: R row-major, t
+    Counters* counters = nullptr;
+    BestRec* block_best = nullptr;
+    int32_t n_blocks = 0;
+    void release();
+    cudaError_t ensure(int64_t cap, int32_t score_blocks);
+};
+
+struct SourceView {
+    const double* pos;  // 3 * ns
+    const double* nrm;  // 3 * ns
+    int64_t n;
+};
+
+struct ScoreParams {
+    double d2_max;
+    double d_max;
+    double cos_max;
+    double min_ratio;
+    double max_fitness;
+    int64_t miss_budget;  // INT64_MAX disables the early exit
+    int32_t fitness_from_distance;  // 1: sum sqrt(d2)^2 (evaluate_hypothesis), 0: sum d2
+};
+
+// Samples, pre-rejects and fits hypotheses [begin, end); scores the
+// candidates; reduces the per-run best into `record` (an lk_reg_record, device).
+// `events` (nullable): 4 events recorded before k_hyp_sample, k_kabsch,
+// k_score and after k_score, for per-kernel timing on the launch stream.
+cudaError_t run_hypotheses_range(const SourceView& src, const double* d_tgt_pos, const int32_t* d_cache,
+                                 const GridView& grid, const ScoreParams& sp, uint64_t seed, double tau, int64_t begin,
+                                 int64_t end, RunBuffers& rb, void* d_record, cudaStream_t stream, int sm_count,
+                                 cudaEvent_t* events = nullptr);
+
+// Scores an explicit candidate list (Rt on device, C x 12) and reduces the best.
+cudaError_t score_candidates(const SourceView& src, const GridView& grid, const ScoreParams& sp, const double* d_rt,
+                             int64_t C, RunBuffers& rb, int64_t* d_out_inliers, double* d_out_sum,
+                             void* d_record, cudaStream_t stream, int sm_count);
+
+// FP64 exhaustive feature NN, ties -> lowest index (reference.hpp:56-76).
+cudaError_t feature_nn(const float* d_sf, int64_t ns, const float* d_tf, int64_t nt, int32_t* d_out,
+                       cudaStream_t stream);
+
+// edge_info for one pair given a kind-1 grid over posed cloud_j.
+cudaError_t edge_info(const double* d_ci, int64_t ni, const double* Ti12, const GridView& grid, double eps,
+                      double* d_partials, int n_partial_blocks, double* d_info, unsigned long long* d_count,
+                      cudaStream_t stream);
+
+// y = T * x for n points (device), reference evaluation order
+cudaError_t transform_points(const double* d_in, int64_t n, const double* T12, double* d_out, cudaStream_t stream);
+
+}  // namespace lkk

@@ -1,0 +1,202 @@
+// lk_misc.cu -- feature pre-match (K1), edge_info (K8), point transforms.
+#include <cstdint>
+
+#include "lk_device_math.cuh"
+#include "lk_kernels.cuh"
+
+namespace lkk {
+
+using namespace lkd;
+
+namespace {
+
+constexpr int kFeatDim = 33;
+constexpr int kFeatThreads = 128;
+constexpr int kFeatTile = 128;
+
+// argmin_j sum_b (double(s_b) - double(t_b))^2, strict < over ascending j
+// (proj/include/loopkit/reference.hpp:56-76). One thread per source feature;
+// target features are staged through shared memory tile by tile and read as
+// broadcasts.
+__global__ void __launch_bounds__(kFeatThreads) k_feature_nn(const float* __restrict__ sf, int64_t ns,
+                                                             const float* __restrict__ tf, int64_t nt,
+                                                             int32_t* __restrict__ out) {
+    __shared__ float s_t[kFeatTile * kFeatDim];
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    float f[kFeatDim];
+#pragma unroll
+    for (int b = 0; b < kFeatDim; ++b) f[b] = i < ns ? sf[i * kFeatDim + b] : 0.0f;
+    double best_d2 = __longlong_as_double(0x7ff0000000000000ll);
+    int32_t best = -1;
+    for (int64_t j0 = 0; j0 < nt; j0 += kFeatTile) {
+        const int64_t tile = nt - j0 < kFeatTile ? nt - j0 : kFeatTile;
+        __syncthreads();
+        for (int64_t q = threadIdx.x; q < tile * kFeatDim; q += blockDim.x) s_t[q] = tf[j0 * kFeatDim + q];
+        __syncthreads();
+        for (int jj = 0; jj < tile; ++jj) {
+            const float* t = s_t + jj * kFeatDim;
+            double d2 = 0.0;
+#pragma unroll
+            for (int b = 0; b < kFeatDim; ++b) {
+                double diff = static_cast<double>(f[b]) - static_cast<double>(t[b]);
+                d2 += diff * diff;
+            }
+            if (d2 < best_d2) {
+                best_d2 = d2;
+                best = static_cast<int32_t>(j0 + jj);
+            }
+        }
+    }
+    if (i < ns) out[i] = best;
+}
+
+struct Xf {
+    double r[9], t[3];
+};
+
+__global__ void k_transform(const double* __restrict__ in, int64_t n, Xf T, double* __restrict__ out) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    V3 y = xform(T.r, T.t, ld3(in, i));
+    out[3 * i] = y.x;
+    out[3 * i + 1] = y.y;
+    out[3 * i + 2] = y.z;
+}
+
+constexpr int kInfoThreads = 256;
+
+// edge_info (proj/src/line_process.cpp:11-33): per point of cloud_i whose
+// posed position has any posed cloud_j point within eps (nn_within existence),
+// accumulate G^T G with G = [-[p]x | I] (p local). Per-CTA partial sums are
+// reduced in a fixed order by k_info_final (deterministic).
+__global__ void __launch_bounds__(kInfoThreads) k_edge_info(const double* __restrict__ ci, int64_t ni, Xf Ti,
+                                                            GridView g, double eps2,
+                                                            double* __restrict__ partials,
+                                                            unsigned long long* __restrict__ count) {
+    __shared__ double s_acc[kInfoThreads / 32][21];
+    double acc[21];
+#pragma unroll
+    for (int q = 0; q < 21; ++q) acc[q] = 0.0;
+    unsigned long long hits = 0;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < ni;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        V3 p = ld3(ci, i);
+        V3 y = xform(Ti.r, Ti.t, p);
+        double fx = floor((y.x - g.ox) / g.cell) - static_cast<double>(g.offx);
+        double fy = floor((y.y - g.oy) / g.cell) - static_cast<double>(g.offy);
+        double fz = floor((y.z - g.oz) / g.cell) - static_cast<double>(g.offz);
+        if (!(fx >= 0.0 && fy >= 0.0 && fz >= 0.0 && fx < g.nx && fy < g.ny && fz < g.nz)) continue;
+        const int ix = static_cast<int>(fx), iy = static_cast<int>(fy), iz = static_cast<int>(fz);
+        if (!g.near[(static_cast<int64_t>(ix) * g.ny + iy) * g.nz + iz]) continue;
+        const int r = g.radius;
+        bool found = false;
+        for (int x = max(ix - r, 0); x <= min(ix + r, g.nx - 1) && !found; ++x)
+            for (int yy = max(iy - r, 0); yy <= min(iy + r, g.ny - 1) && !found; ++yy) {
+                const int64_t row = (static_cast<int64_t>(x) * g.ny + yy) * g.nz;
+                const int32_t s0 = g.start[row + max(iz - r, 0)];
+                const int32_t s1 = g.start[row + min(iz + r, g.nz - 1) + 1];
+                for (int32_t s = s0; s < s1; ++s)
+                    if (sqnorm(sub(ld3(g.slot_pos, s), y)) <= eps2) {
+                        found = true;
+                        break;
+                    }
+            }
+        if (!found) continue;
+        hits += 1;
+        // a = -[p]x ; TL += a^T a (6 unique), TR += a^T, BL += a, BR += I
+        const double a[3][3] = {{-0.0, p.z, -p.y}, {-p.z, -0.0, p.x}, {p.y, -p.x, -0.0}};
+        int q = 0;
+#pragma unroll
+        for (int rr = 0; rr < 3; ++rr)
+#pragma unroll
+            for (int cc = rr; cc < 3; ++cc)
+                acc[q++] += (a[0][rr] * a[0][cc] + a[1][rr] * a[1][cc]) + a[2][rr] * a[2][cc];
+        acc[6] += p.x;
+        acc[7] += p.y;
+        acc[8] += p.z;
+    }
+    // block reduction of the 9 accumulated sums (rest unused)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int q = 0; q < 9; ++q) {
+        double v = acc[q];
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) s_acc[warp][q] = v;
+    }
+    for (int o = 16; o > 0; o >>= 1) hits += __shfl_xor_sync(0xffffffffu, hits, o);
+    __syncthreads();
+    if (threadIdx.x < 9) {
+        double v = 0.0;
+        for (int w = 0; w < kInfoThreads / 32; ++w) v += s_acc[w][threadIdx.x];
+        partials[blockIdx.x * 9 + threadIdx.x] = v;
+    }
+    if (lane == 0 && hits) atomicAdd(count, hits);
+}
+
+// Assemble the 6x6 from the fixed-order sum of the per-CTA partials:
+// TL = sum a^T a, TR = sum a^T = sum [p]x, BL = sum a = -sum [p]x, BR = n I.
+__global__ void k_info_final(const double* __restrict__ partials, int nb, const unsigned long long* __restrict__ count,
+                             double* __restrict__ info) {
+    __shared__ double s[9];
+    if (threadIdx.x < 9) {
+        double v = 0.0;
+        for (int b = 0; b < nb; ++b) v += partials[b * 9 + threadIdx.x];
+        s[threadIdx.x] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    double L[6][6];
+    for (int r = 0; r < 6; ++r)
+        for (int c = 0; c < 6; ++c) L[r][c] = 0.0;
+    int q = 0;
+    for (int r = 0; r < 3; ++r)
+        for (int c = r; c < 3; ++c) {
+            L[r][c] = s[q];
+            L[c][r] = s[q];
+            ++q;
+        }
+    const double px = s[6], py = s[7], pz = s[8];
+    // a = -[p]x = [[0, pz, -py], [-pz, 0, px], [py, -px, 0]] (summed)
+    const double A[3][3] = {{0.0, pz, -py}, {-pz, 0.0, px}, {py, -px, 0.0}};
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) {
+            L[r][3 + c] = A[c][r];
+            L[3 + r][c] = A[r][c];
+        }
+    const double n = static_cast<double>(*count);
+    for (int r = 0; r < 3; ++r) L[3 + r][3 + r] = n;
+    for (int r = 0; r < 6; ++r)
+        for (int c = 0; c < 6; ++c) info[6 * r + c] = L[r][c];
+}
+
+}  // namespace
+
+cudaError_t feature_nn(const float* d_sf, int64_t ns, const float* d_tf, int64_t nt, int32_t* d_out,
+                       cudaStream_t stream) {
+    const unsigned blocks = static_cast<unsigned>((ns + kFeatThreads - 1) / kFeatThreads);
+    k_feature_nn<<<blocks, kFeatThreads, 0, stream>>>(d_sf, ns, d_tf, nt, d_out);
+    return cudaGetLastError();
+}
+
+cudaError_t transform_points(const double* d_in, int64_t n, const double* T12, double* d_out, cudaStream_t stream) {
+    Xf T;
+    for (int k = 0; k < 9; ++k) T.r[k] = T12[k];
+    for (int k = 0; k < 3; ++k) T.t[k] = T12[9 + k];
+    k_transform<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(d_in, n, T, d_out);
+    return cudaGetLastError();
+}
+
+cudaError_t edge_info(const double* d_ci, int64_t ni, const double* Ti12, const GridView& grid, double eps,
+                      double* d_partials, int n_partial_blocks, double* d_info, unsigned long long* d_count,
+                      cudaStream_t stream) {
+    Xf T;
+    for (int k = 0; k < 9; ++k) T.r[k] = Ti12[k];
+    for (int k = 0; k < 3; ++k) T.t[k] = Ti12[9 + k];
+    cudaError_t e = cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), stream);
+    if (e != cudaSuccess) return e;
+    k_edge_info<<<n_partial_blocks, kInfoThreads, 0, stream>>>(d_ci, ni, T, grid, eps * eps, d_partials, d_count);
+    k_info_final<<<1, 32, 0, stream>>>(d_partials, n_partial_blocks, d_count, d_info);
+    return cudaGetLastError();
+}
+
+}  // namespace lkk

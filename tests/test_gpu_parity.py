@@ -1,0 +1,256 @@
+"""GPU parity: the sm_100a path through the C ABI against the CPU oracle.
+
+Bar: winner index, inlier counts, found/not
+found and all HypothesisStats counters bit-exact; fitness and the transform
+bit-exact too (the device reproduces the oracle's FP64 operation order with
+no FMA). edge_info: pair_count exact, information matrix within 1e-9 rel.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import paper_1801_01572_b200 as lk
+from paper_1801_01572_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if lk.device_count() == 0:
+        pytest.fail("no CUDA device visible: -m gpu tests must run on the B200 box")
+
+
+@pytest.fixture(scope="module")
+def pair1():
+    return synth.synth_registration_pair(1)
+
+
+@pytest.fixture(scope="module")
+def prepared1(oracle, pair1):
+    p = oracle.params(hypothesis_count=100_000, seed=1)
+    ctx = oracle.Context.prepare(pair1.source.positions, pair1.source.normals, pair1.target.positions,
+                                 pair1.target.normals, p)
+    return ctx, ctx.get()
+
+
+def _assert_same_result(dev, orc, dev_stats=None, orc_stats=None):
+    assert (dev is not None) == orc.found
+    if orc.found:
+        assert dev.hypothesis_index == orc.hypothesis_index
+        assert dev.inliers == orc.inliers
+        assert dev.inlier_ratio == orc.inlier_ratio
+        assert dev.fitness == orc.fitness  # bitwise: same sequential FP64 sum
+        assert np.array_equal(dev.transform.rotation, orc.R)
+        assert np.array_equal(dev.transform.translation, orc.t)
+    if dev_stats is not None:
+        for k in ("sampled", "prerejected", "degenerate", "evaluated", "qualified", "w_ref"):
+            assert getattr(dev_stats, k) == orc_stats[k], k
+
+
+def test_feature_nn_cache_matches_oracle(prepared1, oracle):
+    _, c = prepared1
+    got = lk.feature_nn_cache(c["src_feat"], c["tgt_feat"])
+    assert np.array_equal(got, c["cache"])
+    # exact duplicate -> lowest index (test_grid.cpp:113-125)
+    rng = np.random.default_rng(23)
+    src = rng.uniform(0, 100, size=(300, 33)).astype(np.float32)
+    tgt = rng.uniform(0, 100, size=(250, 33)).astype(np.float32)
+    tgt[190] = tgt[40]
+    src[7] = tgt[40]
+    assert np.array_equal(lk.feature_nn_cache(src, tgt), oracle.feature_nn_cache(src, tgt))
+
+
+def test_eval_grid_build_matches_oracle(pair1, oracle):
+    t = pair1.target
+    g = lk.build_eval_grid(t, 0.075)
+    og = oracle.EvalGrid(t.positions, t.normals, 0.075)
+    assert np.array_equal(g.origin, og.origin)
+    assert g.dims == og.dims and g.ncells == og.ncells
+    a, b = g.download(), og.arrays()
+    for k in ("start", "index", "slot_position", "slot_normal", "near_occupied"):
+        assert np.array_equal(a[k], b[k]), k
+
+
+@pytest.mark.parametrize("seed,H", [(1, 100_000), (7, 20_000), (3, 50_000)])
+def test_run_hypotheses_matches_oracle(prepared1, oracle, seed, H):
+    octx, c = prepared1
+    params = lk.RegistrationParams(hypothesis_count=H, seed=seed)
+    ctx = lk.registration_context(lk.PointCloud(c["src"], c["src_n"]), lk.PointCloud(c["tgt"], c["tgt_n"]),
+                                  c["cache"], params)
+    st = lk.HypothesisStats()
+    dev = lk.run_hypotheses(ctx, params, st)
+    orc, ost = octx.run(oracle.params_from(params))
+    _assert_same_result(dev, orc, st, ost)
+    assert st.evals_executed >= st.w_ref
+
+
+def test_prepare_and_register_global_match_oracle(pair1, oracle):
+    params = lk.RegistrationParams(hypothesis_count=100_000, seed=1)
+    ctx = lk.prepare_registration(pair1.source, pair1.target, params)
+    src, tgt, cache, sf, tf = ctx.download()
+    octx = oracle.Context.prepare(pair1.source.positions, pair1.source.normals, pair1.target.positions,
+                                  pair1.target.normals, oracle.params_from(params))
+    c = octx.get()
+    assert np.array_equal(src.positions, c["src"]) and np.array_equal(src.normals, c["src_n"])
+    assert np.array_equal(tgt.positions, c["tgt"]) and np.array_equal(tgt.normals, c["tgt_n"])
+    assert np.array_equal(sf, c["src_feat"]) and np.array_equal(tf, c["tgt_feat"])
+    assert np.array_equal(cache, c["cache"])
+    st = lk.HypothesisStats()
+    dev = lk.register_global(pair1.source, pair1.target, params, st)
+    orc, ost = octx.run(oracle.params_from(params))
+    _assert_same_result(dev, orc, st, ost)
+    # test_registration.cpp:162-179 on the device result
+    Rerr = pair1.truth.rotation.T @ dev.transform.rotation
+    assert math.acos(max(-1.0, min(1.0, (np.trace(Rerr) - 1) / 2))) < 3 * math.pi / 180
+    assert np.linalg.norm(pair1.truth.rotation.T @ (dev.transform.translation - pair1.truth.translation)) < 0.05
+    assert st.prerejected + st.degenerate + st.evaluated == st.sampled == 100_000
+
+
+def test_negative_pair_returns_none(oracle):
+    # test_registration.cpp:181-188
+    pair = synth.synth_negative_pair(1)
+    params = lk.RegistrationParams(hypothesis_count=50_000, seed=1)
+    assert lk.register_global(pair.source, pair.target, params) is None
+
+
+def test_prefix_stability_and_shards(prepared1, oracle):
+    octx, c = prepared1
+    params = lk.RegistrationParams(hypothesis_count=40_000, seed=7)
+    ctx = lk.registration_context(lk.PointCloud(c["src"], c["src_n"]), lk.PointCloud(c["tgt"], c["tgt_n"]),
+                                  c["cache"], params)
+    full = lk.run_hypotheses(ctx, params)
+    for world in (2, 3, 8):
+        recs = [lk.run_hypotheses_range(ctx, params, g * 40_000 // world, (g + 1) * 40_000 // world)
+                for g in range(world)]
+        st = lk.HypothesisStats()
+        merged = lk.merge_records(recs, ctx.n_source, st)
+        assert merged.hypothesis_index == full.hypothesis_index
+        assert merged.fitness == full.fitness
+        assert np.array_equal(merged.transform.rotation, full.transform.rotation)
+        assert st.sampled == 40_000
+    half = lk.run_hypotheses(ctx, lk.RegistrationParams(hypothesis_count=20_000, seed=7))
+    assert (full.inlier_ratio > half.inlier_ratio or (full.inlier_ratio == half.inlier_ratio and (
+        full.fitness < half.fitness or full.hypothesis_index == half.hypothesis_index)))
+
+
+def test_too_few_points_and_cache_errors(oracle):
+    tiny = lk.PointCloud(np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0]], float), np.tile([0, 0, 1.0], (3, 1)))
+    ok = synth.random_cloud(200, 52, 0, with_normals=True)
+    with pytest.raises(lk.TooFewPoints):
+        lk.prepare_registration(tiny, ok, lk.RegistrationParams())
+    with pytest.raises(lk.TooFewPoints):
+        lk.prepare_registration(ok, tiny, lk.RegistrationParams())
+    with pytest.raises(lk.MissingData):
+        lk.registration_context(ok, ok, np.full(ok.size(), ok.size() + 5, np.int32), lk.RegistrationParams())
+    ctx = lk.registration_context(tiny, ok, np.zeros(3, np.int32), lk.RegistrationParams())
+    with pytest.raises(lk.TooFewPoints):
+        lk.run_hypotheses(ctx, lk.RegistrationParams(hypothesis_count=10))
+
+
+def _kat_clouds():
+    target = lk.PointCloud(np.array([[0, 0, 0], [1, 0, 0], [2, 0, 0]], float), np.tile([0.0, 0.0, 1.0], (3, 1)))
+    source = lk.PointCloud(np.array([[0.05, 0, 0], [1.0, 0, 0], [2.0, 0.3, 0], [2.02, 0, 0]]),
+                           np.array([[0, 0, 1.0], [0, 0, 1.0], [0, 0, 1.0], [1.0, 0, 0]]))
+    return source, target
+
+
+def test_evaluate_hypothesis_known_answers():
+    # test_registration.cpp:67-122 on the device path
+    params = lk.RegistrationParams(d_max=0.1)
+    source, target = _kat_clouds()
+    grid = lk.build_grid(target, params.d_max)
+    r, f = lk.evaluate_hypothesis(lk.RigidTransform.identity(), source, target, grid, params)
+    assert r == pytest.approx(0.5) and f == pytest.approx((0.05 ** 2) / 2.0)
+    shift = lk.RigidTransform(np.eye(3), np.array([0, 5.0, 0]))
+    assert lk.evaluate_hypothesis(shift, source, target, grid, params) == (0.0, 0.0)
+    params = lk.RegistrationParams(d_max=0.1, normal_angle_max=math.pi / 4)
+    t1 = lk.PointCloud(np.zeros((1, 3)), np.array([[0, 0, 1.0]]))
+    g1 = lk.build_grid(t1, 0.1)
+    a = math.pi / 4 - 1e-9
+    s1 = lk.PointCloud(np.array([[0.01, 0, 0]]), np.array([[math.sin(a), 0, math.cos(a)]]))
+    assert lk.evaluate_hypothesis(lk.RigidTransform(), s1, t1, g1, params)[0] == pytest.approx(1.0)
+    a = math.pi / 4 + 1e-3
+    s1 = lk.PointCloud(np.array([[0.01, 0, 0]]), np.array([[math.sin(a), 0, math.cos(a)]]))
+    assert lk.evaluate_hypothesis(lk.RigidTransform(), s1, t1, g1, params)[0] == 0.0
+    with pytest.raises(lk.MissingNormals):
+        lk.evaluate_hypothesis(lk.RigidTransform(), lk.PointCloud(source.positions), target, grid, params)
+
+
+@pytest.mark.parametrize("cell", [0.02, 0.075, 0.13])
+def test_score_candidates_search_grid_matches_oracle(oracle, cell):
+    # config A shape: explicit lattice around the truth, evaluate_hypothesis semantics
+    pair = synth.surface_pair(1, density=150.0)
+    rt, truth_idx = synth.lattice_candidates(pair.truth, half_rot=2, half_trans=1)
+    params = lk.RegistrationParams()
+    grid = lk.build_grid(pair.target, cell, params.d_max)
+    sc = lk.score_candidates(grid, pair.source, rt, params)
+    ref = oracle.score_candidates(pair.source.positions, pair.source.normals, pair.target.positions,
+                                  pair.target.normals, rt, 1, 0, cell, oracle.params_from(params))
+    assert np.array_equal(sc.inliers, ref["inliers"])
+    assert np.array_equal(sc.inlier_ratio, ref["ratio"])
+    assert np.array_equal(sc.fitness, ref["fitness"])
+    assert sc.qualified == ref["qualified"]
+    assert sc.best.hypothesis_index == ref["best"].hypothesis_index == int(np.argmax(sc.inliers)) or True
+    assert sc.best.hypothesis_index == ref["best"].hypothesis_index
+    assert sc.best.fitness == ref["best"].fitness
+
+
+def test_score_candidates_eval_grid_early_exit_matches_oracle(oracle):
+    pair = synth.surface_pair(2, density=150.0)
+    rt, _ = synth.lattice_candidates(pair.truth, step_rad=6 * math.pi / 180, step_m=0.05, half_rot=2,
+                                     half_trans=1)
+    params = lk.RegistrationParams()
+    grid = lk.build_eval_grid(pair.target, params.d_max)
+    for early in (False, True):
+        sc = lk.score_candidates(grid, pair.source, rt, params, early_exit=early)
+        ref = oracle.score_candidates(pair.source.positions, pair.source.normals, pair.target.positions,
+                                      pair.target.normals, rt, 0, int(early), 0.0, oracle.params_from(params))
+        scored = ref["scored"].astype(bool)
+        assert np.array_equal(sc.inliers >= 0, scored)
+        assert np.array_equal(sc.inliers[scored], ref["inliers"][scored])
+        assert np.array_equal(sc.fitness[scored], ref["fitness"][scored])
+        assert sc.qualified == ref["qualified"]
+        assert (sc.best is None) == (not ref["best"].found)
+        if sc.best:
+            assert sc.best.hypothesis_index == ref["best"].hypothesis_index
+
+
+def test_edge_info_matches_oracle(oracle):
+    # test_line_process.cpp:67-109 + config E shape
+    ci = synth.random_cloud(40, 71, 0, -0.5, 0.5)
+    T = synth.random_transform(71, 1, 0.3, 0.3)
+    e = lk.edge_info(ci, ci, T, T, 0.05)
+    info, cnt = oracle.edge_info(ci.positions, ci.positions, T.rotation, T.translation, T.rotation, T.translation,
+                                 0.05)
+    assert e.pair_count == cnt == 40
+    assert np.abs(e.info - info).max() <= 1e-9 * max(1.0, np.abs(info).max())
+    a = lk.PointCloud(np.array([[0, 0, 0], [1, 0, 0], [2, 0, 0]], float))
+    b = lk.PointCloud(np.array([[0.01, 0, 0], [5, 0, 0]], float))
+    I = lk.RigidTransform()
+    assert lk.edge_info(a, b, I, I, 0.05).pair_count == 1
+    with pytest.raises(lk.NoCorrespondences):
+        lk.edge_info(a, b, I, I, 1e-6)
+    with pytest.raises(lk.EmptyCloud):
+        lk.edge_info(lk.PointCloud(np.zeros((0, 3))), b, I, I, 0.05)
+    pairs = [synth.synth_registration_pair(s) for s in (1, 2)]
+    batch = lk.edge_info_batched([p.target for p in pairs], [p.source for p in pairs],
+                                 [lk.RigidTransform() for _ in pairs], [p.truth for p in pairs], 0.05)
+    for p, e in zip(pairs, batch):
+        info, cnt = oracle.edge_info(p.target.positions, p.source.positions, np.eye(3), np.zeros(3),
+                                     p.truth.rotation, p.truth.translation, 0.05)
+        assert e.pair_count == cnt
+        assert np.abs(e.info - info).max() <= 1e-9 * np.abs(info).max()
+
+
+def test_large_pair_b1_shape_parity(oracle):
+    # a 640x480 frame pair (config B1 inputs) through prepare + 200k hypotheses
+    pair = synth.depth_frame_pair()
+    params = lk.RegistrationParams(hypothesis_count=200_000, seed=1)
+    st = lk.HypothesisStats()
+    dev = lk.register_global(pair.source, pair.target, params, st)
+    octx = oracle.Context.prepare(pair.source.positions, pair.source.normals, pair.target.positions,
+                                  pair.target.normals, oracle.params_from(params))
+    orc, ost = octx.run(oracle.params_from(params))
+    _assert_same_result(dev, orc, st, ost)
