@@ -39,7 +39,7 @@ PAPER_MS_PER_REGISTRATION = 20.50  # PAPER.md:161 (Titan X Pascal, redwood pairs
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--hypotheses", type=int, default=1_000_000)
@@ -103,6 +103,11 @@ class ClockSampler:
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
+
+    def wait_first(self, timeout=5.0):
+        t0 = time.time()
+        while self.proc and not self.lines and time.time() - t0 < timeout:
+            time.sleep(0.05)
 
     def stop(self):
         if not self.proc:
@@ -216,7 +221,10 @@ def run_b200(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
-    stream = torch.cuda.current_stream(dev)
+    # a dedicated stream: the library launches on it and the CUDA events are
+    # recorded on it (torch's default stream is the legacy NULL stream)
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
 
     pair = make_fixture()
     H = args.hypotheses
@@ -260,6 +268,7 @@ def run_b200(args):
     clocks = ClockSampler(local)
     if rank == 0:
         clocks.start()
+        clocks.wait_first()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()

@@ -1,0 +1,208 @@
+// loopkit_b200/registration.hpp -- header-only C++ shim over include/loopkit_b200.h
+// that re-exposes the reference registration API
+// (/root/reference/proj/include/loopkit/registration.hpp) with the same names,
+// argument meaning and error behaviour: lk_status codes are turned back into
+// the reference's exception types (proj/include/loopkit/errors.hpp) and
+// LK_NO_ALIGNMENT into std::nullopt.
+//
+// The shim is generic over the caller's cloud / params / result types so the
+// reference's own Eigen types plug in unchanged:
+//   Cloud   : .positions / .normals, contiguous 3-double elements
+//             (std::vector<Eigen::Vector3d> qualifies)
+//   Params  : the RegistrationParams fields (registration.hpp:17-32)
+//   Errors  : a struct with the exception types as nested typedefs; the default
+//             `DefaultErrors` below defines them in namespace loopkit_b200.
+#pragma once
+
+#include <cstdint>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "../loopkit_b200.h"
+
+namespace loopkit_b200 {
+
+// errors.hpp:9-74 (subset used by the registration path)
+struct Error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct EmptyCloud : Error { using Error::Error; };
+struct TooFewPoints : Error { using Error::Error; };
+struct MissingNormals : Error { using Error::Error; };
+struct MissingData : Error { using Error::Error; };
+struct NoCorrespondences : Error { using Error::Error; };
+struct DegenerateConfiguration : Error { using Error::Error; };
+struct CudaError : Error { using Error::Error; };
+
+struct DefaultErrors {
+    using Base = Error;
+    using EmptyCloudT = EmptyCloud;
+    using TooFewPointsT = TooFewPoints;
+    using MissingNormalsT = MissingNormals;
+    using MissingDataT = MissingData;
+    using NoCorrespondencesT = NoCorrespondences;
+    using DegenerateT = DegenerateConfiguration;
+    using DeviceT = CudaError;
+};
+
+template <class E = DefaultErrors>
+[[noreturn]] inline void throw_status(lk_status s) {
+    const char* m = lk_last_error();
+    std::string msg = m && *m ? m : "loopkit_b200 error";
+    switch (s) {
+        case LK_EMPTY_CLOUD: throw typename E::EmptyCloudT(msg);
+        case LK_TOO_FEW_POINTS: throw typename E::TooFewPointsT(msg);
+        case LK_MISSING_NORMALS: throw typename E::MissingNormalsT(msg);
+        case LK_MISSING_DATA: throw typename E::MissingDataT(msg);
+        case LK_NO_CORRESPONDENCES: throw typename E::NoCorrespondencesT(msg);
+        case LK_DEGENERATE: throw typename E::DegenerateT(msg);
+        case LK_CUDA_ERROR:
+        case LK_NCCL_ERROR: throw typename E::DeviceT(msg);
+        default: throw typename E::Base(msg);
+    }
+}
+
+template <class E = DefaultErrors>
+inline bool check(lk_status s) {  // true: found; false: no alignment
+    if (s == LK_OK) return true;
+    if (s == LK_NO_ALIGNMENT) return false;
+    throw_status<E>(s);
+}
+
+// View of a cloud with contiguous xyz triples (no copy).
+template <class Cloud>
+inline lk_cloud as_lk_cloud(const Cloud& c) {
+    lk_cloud out{};
+    out.n = static_cast<int64_t>(c.positions.size());
+    out.xyz = out.n ? reinterpret_cast<const double*>(c.positions.data()) : nullptr;
+    out.nxyz = (!c.normals.empty()) ? reinterpret_cast<const double*>(c.normals.data()) : nullptr;
+    static_assert(sizeof(c.positions[0]) == 3 * sizeof(double), "positions must be packed xyz doubles");
+    return out;
+}
+
+template <class Params>
+inline lk_reg_params to_lk_params(const Params& p, int32_t device = -1) {
+    lk_reg_params o{};
+    o.leaf = p.leaf;
+    o.normal_radius = p.normal_radius;
+    o.feature_radius = p.feature_radius;
+    o.hypothesis_count = p.hypothesis_count;
+    o.similarity_tau = p.similarity_tau;
+    o.d_max = p.d_max;
+    o.min_inlier_ratio = p.min_inlier_ratio;
+    o.max_fitness = p.max_fitness ? static_cast<double>(*p.max_fitness) : -1.0;  // std::optional<double>
+    o.normal_angle_max = p.normal_angle_max;
+    o.seed = p.seed;
+    o.threads = p.threads;
+    o.device = device;
+    return o;
+}
+
+// Result types of the shim (the reference's RegistrationResult /
+// HypothesisStats are filled through `fill` callbacks in INTEGRATION.md).
+struct Transform {
+    double R[9];  // row-major
+    double t[3];
+};
+struct RegistrationResult {
+    Transform transform;
+    double inlier_ratio = 0.0;
+    double fitness = 0.0;
+    std::int64_t hypothesis_index = -1;
+    std::int64_t inliers = 0;
+};
+using HypothesisStats = lk_hyp_stats;
+
+inline RegistrationResult from_lk(const lk_reg_result& r) {
+    RegistrationResult o;
+    for (int k = 0; k < 9; ++k) o.transform.R[k] = r.R[k];
+    for (int k = 0; k < 3; ++k) o.transform.t[k] = r.t[k];
+    o.inlier_ratio = r.inlier_ratio;
+    o.fitness = r.fitness;
+    o.hypothesis_index = r.hypothesis_index;
+    o.inliers = r.inliers;
+    return o;
+}
+
+// RegistrationContext resident on one device (registration.hpp:82-89).
+template <class E = DefaultErrors>
+class RegistrationContext {
+public:
+    RegistrationContext() = default;
+    explicit RegistrationContext(lk_reg_ctx* h) : h_(h) {}
+    RegistrationContext(RegistrationContext&& o) noexcept : h_(o.h_) { o.h_ = nullptr; }
+    RegistrationContext& operator=(RegistrationContext&& o) noexcept {
+        std::swap(h_, o.h_);
+        return *this;
+    }
+    RegistrationContext(const RegistrationContext&) = delete;
+    RegistrationContext& operator=(const RegistrationContext&) = delete;
+    ~RegistrationContext() { lk_reg_ctx_destroy(h_); }
+    lk_reg_ctx* handle() const { return h_; }
+
+private:
+    lk_reg_ctx* h_ = nullptr;
+};
+
+// prepare_registration (registration.hpp:105-107)
+template <class E = DefaultErrors, class Cloud, class Params>
+RegistrationContext<E> prepare_registration(const Cloud& source, const Cloud& target, const Params& params) {
+    lk_cloud s = as_lk_cloud(source), t = as_lk_cloud(target);
+    lk_reg_params p = to_lk_params(params);
+    lk_reg_ctx* h = nullptr;
+    lk_status st = lk_reg_prepare(&s, &t, &p, &h);
+    if (st != LK_OK) throw_status<E>(st);
+    return RegistrationContext<E>(h);
+}
+
+// run_hypotheses (registration.hpp:116-118)
+template <class E = DefaultErrors, class Params>
+std::optional<RegistrationResult> run_hypotheses(const RegistrationContext<E>& ctx, const Params& params,
+                                                 HypothesisStats* stats = nullptr) {
+    lk_reg_params p = to_lk_params(params);
+    lk_reg_result r{};
+    lk_hyp_stats local{};
+    if (!check<E>(lk_reg_run_hypotheses(ctx.handle(), &p, &r, stats ? stats : &local))) return std::nullopt;
+    return from_lk(r);
+}
+
+// register_global (registration.hpp:121-124)
+template <class E = DefaultErrors, class Cloud, class Params>
+std::optional<RegistrationResult> register_global(const Cloud& source, const Cloud& target, const Params& params,
+                                                  HypothesisStats* stats = nullptr) {
+    lk_cloud s = as_lk_cloud(source), t = as_lk_cloud(target);
+    lk_reg_params p = to_lk_params(params);
+    lk_reg_result r{};
+    lk_hyp_stats local{};
+    if (!check<E>(lk_register_global(&s, &t, &p, &r, stats ? stats : &local))) return std::nullopt;
+    return from_lk(r);
+}
+
+// evaluate_hypothesis (registration.hpp:60-63) over a device SearchGrid of
+// cell `grid_cell` built from `target` (the reference passes a SearchGrid).
+template <class E = DefaultErrors, class Cloud, class Params>
+std::pair<double, double> evaluate_hypothesis(const Transform& T, const Cloud& source, const Cloud& target,
+                                              double grid_cell, const Params& params) {
+    if (source.positions.empty() || target.positions.empty())
+        throw typename E::EmptyCloudT("evaluate_hypothesis: empty cloud");
+    if (source.normals.empty() || target.normals.empty())
+        throw typename E::MissingNormalsT("evaluate_hypothesis: both clouds need normals");
+    lk_cloud s = as_lk_cloud(source), t = as_lk_cloud(target);
+    lk_reg_params p = to_lk_params(params);
+    lk_grid* g = nullptr;
+    lk_status st = lk_grid_build(&t, 1, grid_cell, params.d_max, -1, &g);
+    if (st != LK_OK) throw_status<E>(st);
+    double rt[12];
+    for (int k = 0; k < 9; ++k) rt[k] = T.R[k];
+    for (int k = 0; k < 3; ++k) rt[9 + k] = T.t[k];
+    lk_cand_score sc{};
+    st = lk_score_candidates(g, &s, rt, 1, &p, 0, &sc, nullptr, nullptr);
+    lk_grid_destroy(g);
+    if (st != LK_OK) throw_status<E>(st);
+    return {sc.inlier_ratio, sc.fitness};
+}
+
+}  // namespace loopkit_b200

@@ -11,6 +11,7 @@
 #include <chrono>
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -113,6 +114,21 @@ lkk::ScoreParams score_params(const lk_reg_params& p, int64_t ns, bool early_exi
     return sp;
 }
 
+// The FP32 guard-band path is on unless LK_FP64_ONLY=1 (used by the tests to
+// check both paths against the oracle).
+bool fast_path_enabled() {
+    const char* v = std::getenv("LK_FP64_ONLY");
+    return !(v && v[0] == '1');
+}
+
+double max_norm(const double* xyz, int64_t n) {
+    double m = 0.0;
+    for (int64_t i = 0; i < n; ++i)
+        m = std::max(m, std::sqrt(xyz[3 * i] * xyz[3 * i] + xyz[3 * i + 1] * xyz[3 * i + 1] +
+                                  xyz[3 * i + 2] * xyz[3 * i + 2]));
+    return m;
+}
+
 void record_to_result(const lk_reg_record& r, int64_t ns, lk_reg_result* out) {
     std::memset(out, 0, sizeof(*out));
     out->hypothesis_index = -1;
@@ -165,6 +181,8 @@ struct lk_reg_ctx {
     std::vector<int32_t> h_cache;
     std::vector<float> h_sfeat, h_tfeat;
     double *d_spos = nullptr, *d_snrm = nullptr, *d_tpos = nullptr, *d_tnrm = nullptr;
+    float4* d_spos32 = nullptr;  // FP32 copy of the source for the guard-band scan
+    double src_max_norm = 0.0;
     int32_t* d_cache = nullptr;
     lkk::GridStorage grid;
     lkk::RunBuffers rb;
@@ -192,6 +210,7 @@ struct lk_reg_ctx {
         cudaSetDevice(device);
         drain_events();
         cudaFree(d_spos);
+        cudaFree(d_spos32);
         cudaFree(d_snrm);
         cudaFree(d_tpos);
         cudaFree(d_tnrm);
@@ -213,6 +232,9 @@ void ctx_finish(lk_reg_ctx* c, const lk_reg_params& p) {
     c->d_tpos = dev_upload(c->h_tpos.data(), c->h_tpos.size(), s);
     c->d_tnrm = dev_upload(c->h_tnrm.data(), c->h_tnrm.size(), s);
     if (!c->d_cache) c->d_cache = dev_upload(c->h_cache.data(), c->h_cache.size(), s);
+    CK(cudaMalloc(&c->d_spos32, std::max<int64_t>(c->ns, 1) * sizeof(float4)));
+    CK(lkk::make_source32(c->d_spos, c->ns, c->d_spos32, s));
+    c->src_max_norm = max_norm(c->h_spos.data(), c->ns);
     CK(cudaMalloc(&c->d_record, sizeof(lk_reg_record)));
     CK(lkk::build_grid(c->grid, 0, c->d_tpos, c->d_tnrm, c->nt, p.d_max, p.d_max, s));
 }
@@ -292,8 +314,9 @@ lk_status run_range_impl(lk_reg_ctx* c, const lk_reg_params& p, int64_t begin, i
         return fail(LK_MISSING_DATA, "sample_quadruple: cache size mismatch");
     if (begin < 0 || end < begin) return fail(LK_INVALID_ARGUMENT, "bad hypothesis range");
     CK(cudaSetDevice(c->device));
-    lkk::SourceView sv{c->d_spos, c->d_snrm, c->ns};
+    lkk::SourceView sv{c->d_spos, c->d_snrm, c->d_spos32, c->ns};
     lkk::ScoreParams sp = score_params(p, c->ns, true, false);
+    if (fast_path_enabled()) lkk::configure_fast_path(sp, c->grid.view, c->src_max_norm);
     cudaEvent_t* ev = nullptr;
     if (c->profile) {
         std::array<cudaEvent_t, 4> e4;
@@ -586,8 +609,12 @@ lk_status lk_score_candidates(lk_grid* grid, const lk_cloud* src, const double* 
         double* d_sum = nullptr;
         CK(cudaMalloc(&d_inl, std::max<int64_t>(C, 1) * sizeof(int64_t)));
         CK(cudaMalloc(&d_sum, std::max<int64_t>(C, 1) * sizeof(double)));
-        lkk::SourceView sv{d_pos, d_nrm, ns};
+        float4* d_pos32 = nullptr;
+        CK(cudaMalloc(&d_pos32, std::max<int64_t>(ns, 1) * sizeof(float4)));
+        CK(lkk::make_source32(d_pos, ns, d_pos32, s));
+        lkk::SourceView sv{d_pos, d_nrm, d_pos32, ns};
         lkk::ScoreParams sp = score_params(*params, ns, early_exit != 0, grid->kind == 1);
+        if (fast_path_enabled()) lkk::configure_fast_path(sp, grid->g.view, max_norm(src->xyz, ns));
         lk_reg_record rec{};
         std::vector<int64_t> inl(C);
         std::vector<double> sum(C);
@@ -600,6 +627,7 @@ lk_status lk_score_candidates(lk_grid* grid, const lk_cloud* src, const double* 
         if (e == cudaSuccess) e = cudaStreamSynchronize(s);
         cudaFree(d_pos);
         cudaFree(d_nrm);
+        cudaFree(d_pos32);
         cudaFree(d_rt);
         cudaFree(d_inl);
         cudaFree(d_sum);

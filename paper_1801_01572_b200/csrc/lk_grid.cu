@@ -5,6 +5,7 @@
 // bbox / cell-bounds reduction -> per-point cell -> count -> exclusive scan ->
 // scatter -> per-cell sort by original index (the reference's CSR order) ->
 // slot payload gather -> occupancy dilation.
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <vector>
@@ -244,7 +245,83 @@ __global__ void k_dilate(const int32_t* __restrict__ cell_of, int64_t n, GridVie
             for (int z = max(kz - r, 0); z <= min(kz + r, g.nz - 1); ++z) near[(x * g.ny + y) * g.nz + z] = 1;
 }
 
+__device__ __forceinline__ void cell_coords(int64_t c, const GridView& g, int& kx, int& ky, int& kz) {
+    kz = static_cast<int>(c % g.nz);
+    ky = static_cast<int>((c / g.nz) % g.ny);
+    kx = static_cast<int>(c / (static_cast<int64_t>(g.nz) * g.ny));
+}
+
+// points in the 3x3x3 block of every cell (rows are contiguous in z)
+__global__ void k_block_count(const int32_t* __restrict__ start, int64_t ncells, GridView g,
+                              int32_t* __restrict__ counts) {
+    int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= ncells) return;
+    int kx, ky, kz;
+    cell_coords(c, g, kx, ky, kz);
+    const int z0 = max(kz - 1, 0), z1 = min(kz + 1, g.nz - 1);
+    int32_t n = 0;
+    for (int x = max(kx - 1, 0); x <= min(kx + 1, g.nx - 1); ++x)
+        for (int y = max(ky - 1, 0); y <= min(ky + 1, g.ny - 1); ++y) {
+            const int64_t row = (static_cast<int64_t>(x) * g.ny + y) * g.nz;
+            n += start[row + z1 + 1] - start[row + z0];
+        }
+    counts[c] = n;
+}
+
+__global__ void k_block_fill(const int32_t* __restrict__ start, const int32_t* __restrict__ index,
+                             const double* __restrict__ slot_pos, const int32_t* __restrict__ offsets, int64_t ncells,
+                             GridView g, int2* __restrict__ info, double4* __restrict__ pts,
+                             float4* __restrict__ pts32) {
+    int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= ncells) return;
+    int kx, ky, kz;
+    cell_coords(c, g, kx, ky, kz);
+    const int z0 = max(kz - 1, 0), z1 = min(kz + 1, g.nz - 1);
+    const int32_t off0 = offsets[c];
+    int32_t off = off0;
+    for (int x = max(kx - 1, 0); x <= min(kx + 1, g.nx - 1); ++x)
+        for (int y = max(ky - 1, 0); y <= min(ky + 1, g.ny - 1); ++y) {
+            const int64_t row = (static_cast<int64_t>(x) * g.ny + y) * g.nz;
+            for (int32_t s = start[row + z0]; s < start[row + z1 + 1]; ++s) {
+                const double px = slot_pos[3 * s], py = slot_pos[3 * s + 1], pz = slot_pos[3 * s + 2];
+                pts[off] = make_double4(px, py, pz, static_cast<double>(index[s]));
+                // local cell coordinates for the FP32 guard-band scan
+                pts32[off] = make_float4(static_cast<float>((px - g.ox) / g.cell - g.offx),
+                                         static_cast<float>((py - g.oy) / g.cell - g.offy),
+                                         static_cast<float>((pz - g.oz) / g.cell - g.offz),
+                                         __int_as_float(index[s]));
+                ++off;
+            }
+        }
+    info[c] = make_int2(off0, off - off0);
+}
+
+__global__ void k_to_float4(const double* __restrict__ pos, int64_t n, float4* __restrict__ out) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n)
+        out[i] = make_float4(static_cast<float>(pos[3 * i]), static_cast<float>(pos[3 * i + 1]),
+                             static_cast<float>(pos[3 * i + 2]), 0.0f);
+}
+
+__global__ void k_copy_normals(const double* __restrict__ nrm, int64_t n, double* __restrict__ out) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < 3 * n) out[i] = nrm ? nrm[i] : 0.0;
+}
+
 inline unsigned blocks_for(int64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
+
+// exclusive scan of n int32 into out[0..n] (out[n] = total)
+cudaError_t exclusive_scan(const int32_t* in, int64_t n, int32_t* out, cudaStream_t stream) {
+    int64_t ntiles = (n + kScanTile - 1) / kScanTile;
+    int32_t* d_bsums = nullptr;
+    cudaError_t e = cudaMallocAsync(&d_bsums, (ntiles + 1) * sizeof(int32_t), stream);
+    if (e != cudaSuccess) return e;
+    k_scan_tiles<<<static_cast<unsigned>(ntiles), kScanThreads, 0, stream>>>(in, n, out, d_bsums);
+    k_scan_block_sums<<<1, 1024, 0, stream>>>(d_bsums, ntiles, out + n);
+    k_scan_add<<<static_cast<unsigned>(ntiles), kScanThreads, 0, stream>>>(out, n, d_bsums);
+    cudaFreeAsync(d_bsums, stream);
+    return cudaGetLastError();
+}
 
 }  // namespace
 
@@ -254,9 +331,19 @@ void GridStorage::release() {
     cudaFree(slot_pos);
     cudaFree(slot_nrm);
     cudaFree(near);
+    cudaFree(block_info);
+    cudaFree(block_pts);
+    cudaFree(nrm_orig);
+    cudaFree(block_f32);
+    cudaFree(pos_orig);
     start = index = nullptr;
     slot_pos = slot_nrm = nullptr;
     near = nullptr;
+    block_info = nullptr;
+    block_pts = nullptr;
+    nrm_orig = nullptr;
+    block_f32 = nullptr;
+    pos_orig = nullptr;
 }
 
 #define LK_TRY(x)                                \
@@ -325,37 +412,83 @@ cudaError_t build_grid(GridStorage& g, int kind, const double* d_pos, const doub
     LK_TRY(cudaMalloc(&g.slot_pos, 3 * n * sizeof(double)));
     LK_TRY(cudaMalloc(&g.slot_nrm, 3 * n * sizeof(double)));
     LK_TRY(cudaMalloc(&g.near, ncells));
-    int32_t *d_cell_of = nullptr, *d_counts = nullptr, *d_bsums = nullptr;
-    int64_t ntiles = (ncells + kScanTile - 1) / kScanTile;
+    LK_TRY(cudaMalloc(&g.nrm_orig, 3 * n * sizeof(double)));
+    int32_t *d_cell_of = nullptr, *d_counts = nullptr;
     LK_TRY(cudaMallocAsync(&d_cell_of, n * sizeof(int32_t), stream));
     LK_TRY(cudaMallocAsync(&d_counts, ncells * sizeof(int32_t), stream));
-    LK_TRY(cudaMallocAsync(&d_bsums, (ntiles + 1) * sizeof(int32_t), stream));
     LK_TRY(cudaMemsetAsync(d_counts, 0, ncells * sizeof(int32_t), stream));
     LK_TRY(cudaMemsetAsync(g.near, 0, ncells, stream));
     k_cell_of<<<blocks_for(n, 256), 256, 0, stream>>>(d_pos, n, v, d_cell_of, d_counts);
-    k_scan_tiles<<<static_cast<unsigned>(ntiles), kScanThreads, 0, stream>>>(d_counts, ncells, g.start, d_bsums);
-    k_scan_block_sums<<<1, 1024, 0, stream>>>(d_bsums, ntiles, g.start + ncells);
-    k_scan_add<<<static_cast<unsigned>(ntiles), kScanThreads, 0, stream>>>(g.start, ncells, d_bsums);
+    LK_TRY(exclusive_scan(d_counts, ncells, g.start, stream));
     LK_TRY(cudaMemsetAsync(d_counts, 0, ncells * sizeof(int32_t), stream));
     k_scatter<<<blocks_for(n, 256), 256, 0, stream>>>(d_cell_of, n, g.start, d_counts, g.index);
     k_sort_cells<<<blocks_for(ncells, 256), 256, 0, stream>>>(g.start, ncells, g.index);
     k_gather_slots<<<blocks_for(n, 256), 256, 0, stream>>>(g.index, n, d_pos, d_nrm, g.slot_pos, g.slot_nrm);
+    k_copy_normals<<<blocks_for(3 * n, 256), 256, 0, stream>>>(d_nrm, n, g.nrm_orig);
     if (kind == 0 || v.radius <= 2) {
         k_dilate<<<blocks_for(n, 128), 128, 0, stream>>>(d_cell_of, n, v, g.near);
     } else {
         LK_TRY(cudaMemsetAsync(g.near, 1, ncells, stream));  // wide blocks: no occupancy shortcut
     }
+    // 3x3x3 block lists for radius-1 grids (27 entries per point at most)
+    if (v.radius == 1 && 27 * n < INT32_MAX) {
+        k_block_count<<<blocks_for(ncells, 256), 256, 0, stream>>>(g.start, ncells, v, d_counts);
+        int32_t* d_off = nullptr;
+        LK_TRY(cudaMallocAsync(&d_off, (ncells + 1) * sizeof(int32_t), stream));
+        LK_TRY(exclusive_scan(d_counts, ncells, d_off, stream));
+        int32_t total = 0;
+        LK_TRY(cudaMemcpyAsync(&total, d_off + ncells, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
+        LK_TRY(cudaStreamSynchronize(stream));
+        g.nblock = total;
+        LK_TRY(cudaMalloc(&g.block_info, ncells * sizeof(int2)));
+        LK_TRY(cudaMalloc(&g.block_pts, (total > 0 ? total : 1) * sizeof(double4)));
+        LK_TRY(cudaMalloc(&g.block_f32, (total > 0 ? total : 1) * sizeof(float4)));
+        LK_TRY(cudaMalloc(&g.pos_orig, 3 * n * sizeof(double)));
+        LK_TRY(cudaMemcpyAsync(g.pos_orig, d_pos, 3 * n * sizeof(double), cudaMemcpyDeviceToDevice, stream));
+        k_block_fill<<<blocks_for(ncells, 256), 256, 0, stream>>>(g.start, g.index, g.slot_pos, d_off, ncells, v,
+                                                                  g.block_info, g.block_pts, g.block_f32);
+        cudaFreeAsync(d_off, stream);
+    }
     LK_TRY(cudaGetLastError());
     cudaFreeAsync(d_cell_of, stream);
     cudaFreeAsync(d_counts, stream);
-    cudaFreeAsync(d_bsums, stream);
     v.start = g.start;
     v.index = g.index;
     v.slot_pos = g.slot_pos;
     v.slot_nrm = g.slot_nrm;
     v.near = g.near;
+    v.block_info = g.block_info;
+    v.block_pts = g.block_pts;
+    v.nrm_orig = g.nrm_orig;
+    v.block_f32 = g.block_f32;
+    v.pos_orig = g.pos_orig;
     g.view = v;
     return cudaStreamSynchronize(stream);
+}
+
+cudaError_t make_source32(const double* d_pos, int64_t n, float4* d_out, cudaStream_t stream) {
+    if (n > 0) k_to_float4<<<blocks_for(n, 256), 256, 0, stream>>>(d_pos, n, d_out);
+    return cudaGetLastError();
+}
+
+// Guard bands of the FP32 fast path:
+// cell coordinates q = R' p + t' carry an absolute error below
+// 8 * 2^-24 * (3 |p|max / cell + |t'| + n) cells; the bands below are an
+// order of magnitude wider than that bound over the magnitudes admitted here.
+void configure_fast_path(ScoreParams& sp, const GridView& g, double max_abs_source) {
+    sp.fast = 0;
+    if (!g.block_f32 || g.radius != 1) return;
+    const double nmax = std::max(g.nx, std::max(g.ny, g.nz));
+    const double pmax = max_abs_source / g.cell;
+    if (nmax > 4096.0 || pmax > 4096.0) return;
+    const double thr = (sp.d_max / g.cell) * (sp.d_max / g.cell);
+    if (thr > 1.0) return;  // block radius 1 covers d_max only up to one cell
+    sp.thr_cells = static_cast<float>(thr);
+    sp.eps_cells = 2e-3f;
+    sp.band_cells = 8e-3f;
+    sp.pmax_cells = static_cast<float>(pmax);
+    sp.nmax_cells = static_cast<float>(nmax);
+    sp.fast = 1;
 }
 
 }  // namespace lkk

@@ -1,21 +1,28 @@
 // lk_hypotheses.cu -- the registration hot path on sm_100a (K2-K5, K7).
 //
-//   k_hyp_sample  RngStream(seed, i) -> 4 distinct sources -> cache -> prerejected
-//                 (proj/src/registration.cpp:21-51, 288-298); survivors compacted
-//                 with warp-aggregated atomics (Algorithm 1 "stream compact").
-//   k_kabsch      FP64 Kabsch + restated Jacobi SVD per survivor
-//                 (proj/src/geometry.cpp:62-91); degenerate ones counted.
-//   k_score       warp per candidate, 32 consecutive source points per step:
-//                 transform, exact NN within d_max over the cell block, normal
-//                 gate, inliers, sequential FP64 sum of d2 in point order, exact
-//                 miss-budget exit (proj/src/registration.cpp:155-219). The last
-//                 CTA to finish reduces the per-CTA bests under the strict total
-//                 order (registration.cpp:272-276) and writes the rank record.
+//   k_hyp_sample    RngStream(seed, i) -> 4 distinct sources -> cache -> prerejected
+//                   (proj/src/registration.cpp:21-51, 288-298); survivors compacted
+//                   with warp-aggregated atomics (Algorithm 1 "stream compact").
+//   k_kabsch        FP64 Kabsch + restated Jacobi SVD per survivor
+//                   (proj/src/geometry.cpp:62-91); degenerate ones counted.
+//   k_score_split   scoring of (candidate, 32-point chunk) work items spread over
+//                   every warp of the GPU: transform, exact NN within d_max over
+//                   the cell block, normal gate (registration.cpp:165-210). Each
+//                   item leaves its inlier / miss ballots and the inliers' d2.
+//   k_score_exits   warp per candidate: exact miss-budget decision and the
+//                   reference's visit count from the miss ballots.
+//   k_score_sums    warp per fully scored candidate: the sequential FP64 sum of
+//                   d2 in point order, qualification, per-CTA best; the last CTA
+//                   reduces under the strict total order (registration.cpp:272-276)
+//                   and writes the rank record.
+//   k_score         warp per candidate streaming its points in order (explicit
+//                   candidate lists, and candidates beyond the split capacity).
 //
-// Parity: the miss-budget exit is order-free (misses only grow), so exiting
-// on the chunk where misses first exceed the budget disqualifies exactly the
-// reference's set; the sum is accumulated lane by lane in point order so the
-// fitness of every fully scored candidate is bit-identical to the reference's.
+// Parity: disqualification by the miss budget depends only on the total miss
+// count (misses only grow), so evaluating every point and deciding afterwards
+// disqualifies exactly the reference's set; the reference's visit count is
+// recovered from the ordered miss ballots. Sums are added lane by lane in
+// point order, so every fitness is bit-identical to the reference's.
 #include <cstdint>
 
 #include "lk_device_math.cuh"
@@ -147,38 +154,215 @@ __device__ __forceinline__ bool eval_point(const GridView& g, const double* R, c
     double fz = floor((y.z - g.oz) / g.cell) - static_cast<double>(g.offz);
     if (!(fx >= 0.0 && fy >= 0.0 && fz >= 0.0 && fx < g.nx && fy < g.ny && fz < g.nz)) return false;
     const int ix = static_cast<int>(fx), iy = static_cast<int>(fy), iz = static_cast<int>(fz);
-    if (!__ldg(g.near + (static_cast<int64_t>(ix) * g.ny + iy) * g.nz + iz)) return false;
-    const int r = g.radius;
-    const int x0 = max(ix - r, 0), x1 = min(ix + r, g.nx - 1);
-    const int y0 = max(iy - r, 0), y1 = min(iy + r, g.ny - 1);
-    const int z0 = max(iz - r, 0), z1 = min(iz + r, g.nz - 1);
+    const int64_t c = (static_cast<int64_t>(ix) * g.ny + iy) * g.nz + iz;
     double best_d2 = __longlong_as_double(0x7ff0000000000000ll);  // +inf
-    int32_t best_slot = -1;
     int32_t best_orig = INT32_MAX;
-    for (int x = x0; x <= x1; ++x) {
-        for (int yy = y0; yy <= y1; ++yy) {
-            const int64_t row = (static_cast<int64_t>(x) * g.ny + yy) * g.nz;
-            const int32_t s0 = __ldg(g.start + row + z0);
-            const int32_t s1 = __ldg(g.start + row + z1 + 1);
-            for (int32_t s = s0; s < s1; ++s) {
-                V3 q = ld3(g.slot_pos, s);
-                double d2 = sqnorm(sub(q, y));
-                if (d2 > sp.d2_max) continue;
-                int32_t orig = __ldg(g.index + s);
-                if (d2 < best_d2 || (d2 == best_d2 && orig < best_orig)) {
-                    best_d2 = d2;
-                    best_slot = s;
-                    best_orig = orig;
+    if (g.block_info) {
+        const int2 bi = __ldg(g.block_info + c);
+        if (bi.y == 0) return false;  // not near-occupied
+        for (int32_t e = bi.x; e < bi.x + bi.y; ++e) {
+            const double2* bp = reinterpret_cast<const double2*>(g.block_pts + e);
+            const double2 qa = __ldg(bp), qb = __ldg(bp + 1);
+            const double dx = qa.x - y.x, dy = qa.y - y.y, dz = qb.x - y.z;
+            const double d2 = (dx * dx + dy * dy) + dz * dz;
+            if (d2 > sp.d2_max) continue;
+            const int32_t orig = static_cast<int32_t>(qb.y);
+            if (d2 < best_d2 || (d2 == best_d2 && orig < best_orig)) {
+                best_d2 = d2;
+                best_orig = orig;
+            }
+        }
+    } else {
+        if (!__ldg(g.near + c)) return false;
+        const int r = g.radius;
+        const int x0 = max(ix - r, 0), x1 = min(ix + r, g.nx - 1);
+        const int y0 = max(iy - r, 0), y1 = min(iy + r, g.ny - 1);
+        const int z0 = max(iz - r, 0), z1 = min(iz + r, g.nz - 1);
+        for (int x = x0; x <= x1; ++x) {
+            for (int yy = y0; yy <= y1; ++yy) {
+                const int64_t row = (static_cast<int64_t>(x) * g.ny + yy) * g.nz;
+                const int32_t s0 = __ldg(g.start + row + z0);
+                const int32_t s1 = __ldg(g.start + row + z1 + 1);
+                for (int32_t s = s0; s < s1; ++s) {
+                    V3 q = ld3(g.slot_pos, s);
+                    double d2 = sqnorm(sub(q, y));
+                    if (d2 > sp.d2_max) continue;
+                    int32_t orig = __ldg(g.index + s);
+                    if (d2 < best_d2 || (d2 == best_d2 && orig < best_orig)) {
+                        best_d2 = d2;
+                        best_orig = orig;
+                    }
                 }
             }
         }
     }
-    if (best_slot < 0) return false;
-    V3 nt = ld3(g.slot_nrm, best_slot);
+    if (best_orig == INT32_MAX) return false;
+    V3 nt = ld3(g.nrm_orig, best_orig);
     if (is_zero(ns) || is_zero(nt)) return false;
     if (!(dot(rot(R, ns), nt) >= sp.cos_max)) return false;
     if (sp.fitness_from_distance) {
         double dist = sqrt(best_d2);
+        addend = dist * dist;
+    } else {
+        addend = best_d2;
+    }
+    return true;
+}
+
+// ---- FP32 guard-band fast path ----------
+// Cell coordinates q = R' p + t' (R' = R / cell, t' = (t - o) / cell - off) and
+// the block scan run in FP32; every decision that the FP32 values cannot
+// certify -- a coordinate within eps of a cell face, an entry within the band
+// of d_max, two entries within twice the band of each other -- and every
+// quantity that feeds the result (the winning d2, the normal gate) is
+// evaluated in FP64 exactly as the reference does.
+struct FastRT {
+    float r[9];    // R / cell
+    float t[3];    // (t - o) / cell - off
+    float eps;     // guard on cell-coordinate fractions (cells)
+    float band;    // guard on d2 (squared cells)
+    float ok;      // 1: fast path usable for this candidate
+    float pad;
+};
+static_assert(sizeof(FastRT) == 64, "FastRT layout");
+
+// Per-candidate FP32 image of (R, t) in grid cell units and its guard bands.
+// Error bound of q = R' p + t' evaluated by the fmaf chain below (rows of R
+// have unit norm): |dq| <= 2^-24 (5 |p|max + 4 |t'|) cells; entries carry
+// <= 2^-24 n. With delta = both, d2 within one cell is off by at most
+// 2 sqrt3 delta + 3 delta^2 (+ FP32 rounding of d2 itself); bands are 4x that.
+__device__ __forceinline__ FastRT make_fast(const double* R, const double* t, const GridView& g,
+                                            const ScoreParams& sp) {
+    FastRT f;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) f.r[k] = static_cast<float>(R[k] / g.cell);
+    f.t[0] = static_cast<float>((t[0] - g.ox) / g.cell - g.offx);
+    f.t[1] = static_cast<float>((t[1] - g.oy) / g.cell - g.offy);
+    f.t[2] = static_cast<float>((t[2] - g.oz) / g.cell - g.offz);
+    const float u = 5.9604645e-8f;  // 2^-24
+    const float tn = sqrtf(f.t[0] * f.t[0] + f.t[1] * f.t[1] + f.t[2] * f.t[2]);
+    const float dq = u * (5.0f * sp.pmax_cells + 4.0f * tn + 4.0f);
+    const float de = u * (sp.nmax_cells + 2.0f);
+    const float delta = dq + de;
+    f.eps = 4.0f * dq + 1e-6f;
+    f.band = 4.0f * (3.5f * delta + 3.0f * delta * delta + 8.0f * u) + 1e-7f;
+    f.ok = (sp.fast && f.eps < 0.02f && f.band < 0.02f) ? 1.0f : 0.0f;
+    f.pad = 0.0f;
+    return f;
+}
+
+__device__ __forceinline__ FastRT load_fast(const FastRT* __restrict__ p) {
+    const float4* q = reinterpret_cast<const float4*>(p);
+    const float4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2), d = __ldg(q + 3);
+    FastRT f;
+    f.r[0] = a.x; f.r[1] = a.y; f.r[2] = a.z; f.r[3] = a.w;
+    f.r[4] = b.x; f.r[5] = b.y; f.r[6] = b.z; f.r[7] = b.w;
+    f.r[8] = c.x; f.t[0] = c.y; f.t[1] = c.z; f.t[2] = c.w;
+    f.eps = d.x; f.band = d.y; f.ok = d.z; f.pad = d.w;
+    return f;
+}
+
+// FastRT of every candidate (n_fixed >= 0, or the device candidate count).
+__global__ void k_prep_fast(const double* __restrict__ cand_rt, int64_t n_fixed, const Counters* __restrict__ ctr,
+                            GridView g, ScoreParams sp, FastRT* __restrict__ out) {
+    const int64_t n = n_fixed >= 0 ? n_fixed : static_cast<int64_t>(ctr->n_candidates);
+    for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
+         k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double R[9], t[3];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) R[q] = cand_rt[12 * k + q];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) t[q] = cand_rt[12 * k + 9 + q];
+        out[k] = make_fast(R, t, g, sp);
+    }
+}
+
+__device__ __forceinline__ bool eval_point_fast(const GridView& g, const double* R, const double* t,
+                                                const FastRT& F, const SourceView& src, int64_t i,
+                                                const ScoreParams& sp, double& addend) {
+    if (F.ok == 0.0f) return eval_point(g, R, t, ld3(src.pos, i), ld3(src.nrm, i), sp, addend);
+    const float4 P = __ldg(src.pos32 + i);
+    const float qx = fmaf(F.r[0], P.x, fmaf(F.r[1], P.y, fmaf(F.r[2], P.z, F.t[0])));
+    const float qy = fmaf(F.r[3], P.x, fmaf(F.r[4], P.y, fmaf(F.r[5], P.z, F.t[1])));
+    const float qz = fmaf(F.r[6], P.x, fmaf(F.r[7], P.y, fmaf(F.r[8], P.z, F.t[2])));
+    const float eps = F.eps;
+    // certainly outside the grid
+    if (qx < -eps || qy < -eps || qz < -eps || qx >= g.nx + eps || qy >= g.ny + eps || qz >= g.nz + eps)
+        return false;
+    const float fx = floorf(qx), fy = floorf(qy), fz = floorf(qz);
+    const float rx = qx - fx, ry = qy - fy, rz = qz - fz;
+    if (rx < eps || rx > 1.0f - eps || ry < eps || ry > 1.0f - eps || rz < eps || rz > 1.0f - eps)
+        return eval_point(g, R, t, ld3(src.pos, i), ld3(src.nrm, i), sp, addend);  // near a cell face
+    const int ix = static_cast<int>(fx), iy = static_cast<int>(fy), iz = static_cast<int>(fz);
+    if (ix < 0 || iy < 0 || iz < 0 || ix >= g.nx || iy >= g.ny || iz >= g.nz) return false;
+    const int2 bi = __ldg(g.block_info + (static_cast<int64_t>(ix) * g.ny + iy) * g.nz + iz);
+    if (bi.y == 0) return false;  // not near-occupied
+    // FP32 scan keeping the three smallest d2 (entries of the two best)
+    const float inf = __int_as_float(0x7f800000);
+    float f1 = inf, f2 = inf, f3 = inf;
+    int32_t o1 = -1, o2 = -1;
+    for (int32_t e = bi.x; e < bi.x + bi.y; ++e) {
+        const float4 E = __ldg(g.block_f32 + e);
+        const float dx = qx - E.x, dy = qy - E.y, dz = qz - E.z;
+        const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+        const int32_t o = __float_as_int(E.w);
+        if (d2 < f1) {
+            f3 = f2;
+            f2 = f1;
+            o2 = o1;
+            f1 = d2;
+            o1 = o;
+        } else if (d2 < f2) {
+            f3 = f2;
+            f2 = d2;
+            o2 = o;
+        } else if (d2 < f3) {
+            f3 = d2;
+        }
+    }
+    const float band = F.band;
+    if (f1 > sp.thr_cells + band) return false;  // every entry is certainly beyond d_max
+    // exact FP64 from here on
+    const V3 y = xform(R, t, ld3(src.pos, i));
+    double best_d2 = __longlong_as_double(0x7ff0000000000000ll);
+    int32_t best_orig = INT32_MAX;
+    const float lim = f1 + 2.0f * band;
+    if (f3 <= lim) {
+        // three or more entries tie within the guard: resolve all of them exactly
+        for (int32_t e = bi.x; e < bi.x + bi.y; ++e) {
+            const float4 E = __ldg(g.block_f32 + e);
+            const float dx = qx - E.x, dy = qy - E.y, dz = qz - E.z;
+            if (fmaf(dx, dx, fmaf(dy, dy, dz * dz)) > lim) continue;
+            const int32_t orig = __float_as_int(E.w);
+            const double d2 = sqnorm(sub(ld3(g.pos_orig, orig), y));
+            if (d2 > sp.d2_max) continue;
+            if (d2 < best_d2 || (d2 == best_d2 && orig < best_orig)) {
+                best_d2 = d2;
+                best_orig = orig;
+            }
+        }
+    } else {
+        // the FP32 winner, and the runner-up if it is within the guard
+        const double d2a = sqnorm(sub(ld3(g.pos_orig, o1), y));
+        if (d2a <= sp.d2_max) {
+            best_d2 = d2a;
+            best_orig = o1;
+        }
+        if (f2 <= lim) {
+            const double d2b = sqnorm(sub(ld3(g.pos_orig, o2), y));
+            if (d2b <= sp.d2_max && (d2b < best_d2 || (d2b == best_d2 && o2 < best_orig))) {
+                best_d2 = d2b;
+                best_orig = o2;
+            }
+        }
+    }
+    if (best_orig == INT32_MAX) return false;
+    const V3 ns = ld3(src.nrm, i);
+    const V3 nt = ld3(g.nrm_orig, best_orig);
+    if (is_zero(ns) || is_zero(nt)) return false;
+    if (!(dot(rot(R, ns), nt) >= sp.cos_max)) return false;
+    if (sp.fitness_from_distance) {
+        const double dist = sqrt(best_d2);
         addend = dist * dist;
     } else {
         addend = best_d2;
@@ -192,38 +376,120 @@ __device__ __forceinline__ bool better(int64_t ia, double fa, int64_t xa, int64_
     if (fa != fb) return fa < fb;
     return xa < xb;
 }
+__device__ __forceinline__ bool better(const BestRec& a, const BestRec& b) {
+    return a.valid && (!b.valid || better(a.inliers, a.fitness, a.index, b.inliers, b.fitness, b.index));
+}
 
 constexpr int kScoreThreads = 256;
 constexpr int kScoreWarps = kScoreThreads / 32;
 
-__global__ void __launch_bounds__(kScoreThreads) k_score(SourceView src, GridView g, ScoreParams sp,
-                                                         const double* __restrict__ cand_rt,
-                                                         const int64_t* __restrict__ cand_index, int64_t n_fixed,
-                                                         int64_t sampled, int64_t* __restrict__ out_inliers,
-                                                         double* __restrict__ out_sum, Counters* __restrict__ ctr,
-                                                         BestRec* __restrict__ block_best, RecordDev* __restrict__ rec) {
-    __shared__ BestRec s_best[kScoreWarps];
-    __shared__ unsigned long long s_ticket;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t n_cand = n_fixed >= 0 ? n_fixed : static_cast<int64_t>(ctr->n_candidates);
-    const int64_t ns = src.n;
-    const double inv_n = static_cast<double>(ns);
-
+struct WarpTally {
     BestRec best{0, 0, 0.0, INT64_MAX, -1};
     unsigned long long qualified = 0, w_ref = 0, executed = 0;
 
+    __device__ __forceinline__ void candidate(int64_t inliers, double sum, int64_t ns, const ScoreParams& sp,
+                                              int64_t hyp, int64_t slot) {
+        const double ratio = static_cast<double>(inliers) / static_cast<double>(ns);
+        const double fitness = inliers > 0 ? sum / static_cast<double>(inliers) : 0.0;
+        if (ratio < sp.min_ratio || fitness > sp.max_fitness) return;
+        qualified += 1;
+        BestRec c{1, inliers, fitness, hyp, slot};
+        if (better(c, best)) best = c;
+    }
+};
+
+// Per-CTA: fold the warps' tallies, publish the CTA best and counters.
+// Returns true in the CTA that finishes last (it then owns the final reduce).
+__device__ bool publish_cta(const WarpTally& wt, Counters* ctr, BestRec* block_best, int slot, bool want_ticket) {
+    __shared__ BestRec s_best[kScoreWarps];
+    __shared__ unsigned long long s_ticket;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) {
+        if (wt.qualified) atomicAdd(&ctr->qualified, wt.qualified);
+        if (wt.w_ref) atomicAdd(&ctr->w_ref, wt.w_ref);
+        if (wt.executed) atomicAdd(&ctr->evals_executed, wt.executed);
+        s_best[warp] = wt.best;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        BestRec b = s_best[0];
+        for (int w = 1; w < kScoreWarps; ++w)
+            if (better(s_best[w], b)) b = s_best[w];
+        block_best[slot] = b;
+        __threadfence();
+        s_ticket = want_ticket ? atomicAdd(&ctr->blocks_done, 1ull) : 0ull;
+    }
+    __syncthreads();
+    return want_ticket && s_ticket == gridDim.x - 1;
+}
+
+// Final reduce over n_best per-CTA bests (strict total order) -> record.
+__device__ void write_record(const BestRec* block_best, int n_best, const double* cand_rt, int64_t n_cand,
+                             int64_t sampled, Counters* ctr, RecordDev* rec) {
+    __threadfence();
+    if (threadIdx.x != 0) return;
+    BestRec b{0, 0, 0.0, INT64_MAX, -1};
+    for (int w = 0; w < n_best; ++w) {
+        BestRec c;
+        c.valid = __ldcg(&block_best[w].valid);
+        c.inliers = __ldcg(&block_best[w].inliers);
+        c.fitness = __ldcg(&block_best[w].fitness);
+        c.index = __ldcg(&block_best[w].index);
+        c.slot = __ldcg(&block_best[w].slot);
+        if (better(c, b)) b = c;
+    }
+    RecordDev r{};
+    r.valid = b.valid;
+    r.inliers = b.valid ? b.inliers : 0;
+    r.fitness = b.valid ? b.fitness : 0.0;
+    r.index = b.valid ? b.index : -1;
+    for (int q = 0; q < 9; ++q) r.R[q] = b.valid ? cand_rt[12 * b.slot + q] : 0.0;
+    for (int q = 0; q < 3; ++q) r.t[q] = b.valid ? cand_rt[12 * b.slot + 9 + q] : 0.0;
+    r.sampled = sampled;
+    r.prerejected = static_cast<int64_t>(__ldcg(&ctr->prerejected));
+    r.degenerate = static_cast<int64_t>(__ldcg(&ctr->degenerate));
+    r.evaluated = n_cand;
+    r.qualified = static_cast<int64_t>(__ldcg(&ctr->qualified));
+    r.w_ref = static_cast<int64_t>(__ldcg(&ctr->w_ref));
+    r.evals_executed = static_cast<int64_t>(__ldcg(&ctr->evals_executed));
+    r.reserved = 0;
+    *rec = r;
+}
+
+__device__ __forceinline__ void load_rt(const double* __restrict__ crt, double* R, double* t) {
+    const double2* p = reinterpret_cast<const double2*>(crt);
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+        double2 v = __ldg(p + q);
+        double a = v.x, b = v.y;
+        int k0 = 2 * q, k1 = 2 * q + 1;
+        if (k0 < 9) R[k0] = a; else t[k0 - 9] = a;
+        if (k1 < 9) R[k1] = b; else t[k1 - 9] = b;
+    }
+}
+
+// Warp per candidate, points streamed in order (explicit candidate lists and
+// the overflow beyond the split capacity).
+__global__ void __launch_bounds__(kScoreThreads) k_score(SourceView src, GridView g, ScoreParams sp,
+                                                         const double* __restrict__ cand_rt,
+                                                         const FastRT* __restrict__ cand_fast,
+                                                         const int64_t* __restrict__ cand_index, int64_t cand_begin,
+                                                         int64_t n_fixed, int64_t sampled,
+                                                         int64_t* __restrict__ out_inliers, double* __restrict__ out_sum,
+                                                         Counters* __restrict__ ctr, BestRec* __restrict__ block_best,
+                                                         int best_offset, RecordDev* __restrict__ rec) {
+    const int lane = threadIdx.x & 31;
+    const int64_t n_cand = n_fixed >= 0 ? n_fixed : static_cast<int64_t>(ctr->n_candidates);
+    const int64_t ns = src.n;
+    WarpTally wt;
     for (;;) {
         unsigned long long k = 0;
-        if (lane == 0) k = atomicAdd(&ctr->work_next, 1ull);
+        if (lane == 0) k = cand_begin + atomicAdd(&ctr->work_next, 1ull);
         k = __shfl_sync(kFull, k, 0);
         if (static_cast<int64_t>(k) >= n_cand) break;
         double R[9], t[3];
-        const double* crt = cand_rt + 12 * k;
-#pragma unroll
-        for (int q = 0; q < 9; ++q) R[q] = __ldg(crt + q);
-#pragma unroll
-        for (int q = 0; q < 3; ++q) t[q] = __ldg(crt + 9 + q);
-
+        load_rt(cand_rt + 12 * k, R, t);
+        const FastRT F = load_fast(cand_fast + k);
         int64_t inliers = 0, misses = 0, visited = ns, done = ns;
         double sum = 0.0;
         bool exited = false;
@@ -232,21 +498,20 @@ __global__ void __launch_bounds__(kScoreThreads) k_score(SourceView src, GridVie
             const bool valid = i < ns;
             bool inl = false;
             double addend = 0.0;
-            if (valid) inl = eval_point(g, R, t, ld3(src.pos, i), ld3(src.nrm, i), sp, addend);
+            if (valid) inl = eval_point_fast(g, R, t, F, src, i, sp, addend);
             const unsigned inl_mask = __ballot_sync(kFull, inl);
             const unsigned miss_mask = __ballot_sync(kFull, valid && !inl);
-            // sq_sum += best_d2 in point order (registration.cpp:206)
-            unsigned m = inl_mask;
-            while (m) {
-                const int L = __ffs(m) - 1;
-                m &= m - 1;
-                sum += __shfl_sync(kFull, addend, L);
+            // sq_sum += best_d2 in point order (registration.cpp:206); a
+            // non-inlier lane adds +0.0, which leaves the sum unchanged
+            if (inl_mask) {
+#pragma unroll
+                for (int L = 0; L < 32; ++L) sum += __shfl_sync(kFull, addend, L);
             }
             inliers += __popc(inl_mask);
             const int nm = __popc(miss_mask);
             if (misses + nm > sp.miss_budget) {
                 // the reference returns at its (budget + 1)-th miss
-                int need = static_cast<int>(sp.miss_budget - misses);  // misses to skip in this chunk
+                int need = static_cast<int>(sp.miss_budget - misses);
                 unsigned mm = miss_mask;
                 for (int q = 0; q < need; ++q) mm &= mm - 1;
                 visited = base + (__ffs(mm) - 1) + 1;
@@ -256,81 +521,170 @@ __global__ void __launch_bounds__(kScoreThreads) k_score(SourceView src, GridVie
             }
             misses += nm;
         }
-        w_ref += static_cast<unsigned long long>(visited);
-        executed += static_cast<unsigned long long>(done);
+        wt.w_ref += static_cast<unsigned long long>(visited);
+        wt.executed += static_cast<unsigned long long>(done);
         const int64_t hyp = cand_index ? __ldg(cand_index + k) : static_cast<int64_t>(k);
         if (out_inliers && lane == 0) {
             out_inliers[k] = exited ? -1 : inliers;
             out_sum[k] = exited ? 0.0 : sum;
         }
-        if (!exited) {
-            const double ratio = static_cast<double>(inliers) / inv_n;
-            const double fitness = inliers > 0 ? sum / static_cast<double>(inliers) : 0.0;
-            if (!(ratio < sp.min_ratio || fitness > sp.max_fitness)) {
-                qualified += 1;
-                if (!best.valid || better(inliers, fitness, hyp, best.inliers, best.fitness, best.index))
-                    best = BestRec{1, inliers, fitness, hyp, static_cast<int64_t>(k)};
+        if (!exited) wt.candidate(inliers, sum, ns, sp, hyp, static_cast<int64_t>(k));
+    }
+    const bool last = publish_cta(wt, ctr, block_best, best_offset + blockIdx.x, rec != nullptr);
+    if (last) write_record(block_best, best_offset + gridDim.x, cand_rt, n_cand, sampled, ctr, rec);
+}
+
+// (candidate, chunk) items, chunk-major so neighbouring warps share the
+// source chunk in L1. No early exit: every point of a split candidate is
+// evaluated, the exit decision is made from the ballots in k_score_exits.
+__global__ void __launch_bounds__(kScoreThreads) k_score_split(SourceView src, GridView g, ScoreParams sp,
+                                                               const double* __restrict__ cand_rt,
+                                                               const FastRT* __restrict__ cand_fast, int64_t cap,
+                                                               int32_t n_chunks, int64_t ns_pad,
+                                                               uint32_t* __restrict__ inl_masks,
+                                                               uint32_t* __restrict__ miss_masks,
+                                                               double* __restrict__ addends,
+                                                               Counters* __restrict__ ctr) {
+    const int lane = threadIdx.x & 31;
+    const int64_t n_all = static_cast<int64_t>(ctr->n_candidates);
+    const int64_t n_cand = n_all < cap ? n_all : cap;
+    const int64_t total = n_cand * n_chunks;
+    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+    const int64_t ns = src.n;
+    for (int64_t w = blockIdx.x * static_cast<int64_t>(blockDim.x >> 5) + (threadIdx.x >> 5); w < total;
+         w += nwarps) {
+        const int64_t chunk = w / n_cand;
+        const int64_t cand = w - chunk * n_cand;
+        double R[9], t[3];
+        load_rt(cand_rt + 12 * cand, R, t);
+        const FastRT F = load_fast(cand_fast + cand);
+        const int64_t i = chunk * 32 + lane;
+        const bool valid = i < ns;
+        bool inl = false;
+        double addend = 0.0;
+        if (valid) inl = eval_point_fast(g, R, t, F, src, i, sp, addend);
+        const unsigned im = __ballot_sync(kFull, inl);
+        const unsigned mm = __ballot_sync(kFull, valid && !inl);
+        if (lane == 0) {
+            inl_masks[cand * n_chunks + chunk] = im;
+            miss_masks[cand * n_chunks + chunk] = mm;
+        }
+        if (inl) addends[cand * ns_pad + i] = addend;
+    }
+}
+
+// Warp per split candidate: the exact miss-budget decision and the
+// reference's visit count from the ordered miss ballots; fully scored
+// candidates are appended to full_list for k_score_sums.
+__global__ void __launch_bounds__(kScoreThreads) k_score_exits(int64_t ns, ScoreParams sp, int64_t cap,
+                                                               int32_t n_chunks,
+                                                               const uint32_t* __restrict__ miss_masks,
+                                                               int64_t* __restrict__ full_list,
+                                                               Counters* __restrict__ ctr,
+                                                               BestRec* __restrict__ block_best, int best_offset) {
+    const int lane = threadIdx.x & 31;
+    const int64_t n_all = static_cast<int64_t>(ctr->n_candidates);
+    const int64_t n_cand = n_all < cap ? n_all : cap;
+    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+    WarpTally wt;
+    for (int64_t cand = blockIdx.x * static_cast<int64_t>(blockDim.x >> 5) + (threadIdx.x >> 5); cand < n_cand;
+         cand += nwarps) {
+        const uint32_t* mm = miss_masks + cand * n_chunks;
+        // exact miss-budget decision and the reference's visit count
+        int64_t misses = 0, visited = ns;
+        bool exited = false;
+        for (int32_t g0 = 0; g0 < n_chunks && !exited; g0 += 32) {
+            const int32_t c = g0 + lane;
+            const int cnt = c < n_chunks ? __popc(__ldg(mm + c)) : 0;
+            int incl = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int y = __shfl_up_sync(kFull, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const unsigned over = __ballot_sync(kFull, misses + incl > sp.miss_budget);
+            if (over) {
+                const int L = __ffs(over) - 1;
+                const int64_t before = misses + __shfl_sync(kFull, incl - cnt, L);
+                unsigned m = __ldg(mm + g0 + L);
+                const int need = static_cast<int>(sp.miss_budget - before);
+                for (int q = 0; q < need; ++q) m &= m - 1;
+                visited = static_cast<int64_t>(g0 + L) * 32 + (__ffs(m) - 1) + 1;
+                exited = true;
+            }
+            misses += __shfl_sync(kFull, incl, 31);
+        }
+        wt.w_ref += static_cast<unsigned long long>(visited);
+        wt.executed += static_cast<unsigned long long>(ns);
+        if (!exited && lane == 0) full_list[atomicAdd(&ctr->n_full, 1ull)] = cand;
+    }
+    publish_cta(wt, ctr, block_best, best_offset + blockIdx.x, false);
+}
+
+// Thread per fully scored candidate: inlier count and the sequential FP64
+// sum of d2 in point order (registration.cpp:206), then qualification and
+// the arg-best. Non-inlier slots contribute nothing (masked out).
+__global__ void __launch_bounds__(kScoreThreads) k_score_sums(int64_t ns, ScoreParams sp,
+                                                              const double* __restrict__ cand_rt,
+                                                              const int64_t* __restrict__ cand_index,
+                                                              int32_t n_chunks, int64_t ns_pad,
+                                                              const uint32_t* __restrict__ inl_masks,
+                                                              const double* __restrict__ addends,
+                                                              const int64_t* __restrict__ full_list, int n_best_total,
+                                                              int64_t sampled, Counters* __restrict__ ctr,
+                                                              BestRec* __restrict__ block_best,
+                                                              RecordDev* __restrict__ rec) {
+    const int lane = threadIdx.x & 31;
+    const int64_t n_full = static_cast<int64_t>(ctr->n_full);
+    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+    WarpTally wt;
+    for (int64_t f = blockIdx.x * static_cast<int64_t>(blockDim.x >> 5) + (threadIdx.x >> 5); f < n_full;
+         f += nwarps) {
+        const int64_t cand = full_list[f];
+        const uint32_t* im = inl_masks + cand * n_chunks;
+        const double* ad = addends + cand * ns_pad;
+        int64_t inliers = 0;
+        double sum = 0.0;
+        // 8 chunks per round: loads issued together, then the ordered adds
+        // (lane order within a chunk, chunks in order); non-inliers add +0.0
+        for (int32_t c0 = 0; c0 < n_chunks; c0 += 8) {
+            uint32_t m[8];
+            double a[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) m[j] = (c0 + j < n_chunks) ? __ldg(im + c0 + j) : 0u;
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                a[j] = ((m[j] >> lane) & 1u) ? __ldg(ad + static_cast<int64_t>(c0 + j) * 32 + lane) : 0.0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                inliers += __popc(m[j]);
+                if (m[j]) {
+#pragma unroll
+                    for (int L = 0; L < 32; ++L) sum += __shfl_sync(kFull, a[j], L);
+                }
             }
         }
+        wt.candidate(inliers, sum, ns, sp, __ldg(cand_index + cand), cand);
     }
-    if (lane == 0) {
-        if (qualified) atomicAdd(&ctr->qualified, qualified);
-        if (w_ref) atomicAdd(&ctr->w_ref, w_ref);
-        if (executed) atomicAdd(&ctr->evals_executed, executed);
-        s_best[warp] = best;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        BestRec b = s_best[0];
-        for (int w = 1; w < kScoreWarps; ++w) {
-            const BestRec& c = s_best[w];
-            if (c.valid && (!b.valid || better(c.inliers, c.fitness, c.index, b.inliers, b.fitness, b.index))) b = c;
-        }
-        block_best[blockIdx.x] = b;
-        __threadfence();
-        s_ticket = atomicAdd(&ctr->blocks_done, 1ull);
-    }
-    __syncthreads();
-    if (s_ticket != gridDim.x - 1) return;
-    // last CTA: reduce all per-CTA bests and write the record
-    __threadfence();
-    if (threadIdx.x == 0) {
-        BestRec b{0, 0, 0.0, INT64_MAX, -1};
-        for (unsigned w = 0; w < gridDim.x; ++w) {
-            BestRec c;
-            c.valid = __ldcg(&block_best[w].valid);
-            c.inliers = __ldcg(&block_best[w].inliers);
-            c.fitness = __ldcg(&block_best[w].fitness);
-            c.index = __ldcg(&block_best[w].index);
-            c.slot = __ldcg(&block_best[w].slot);
-            if (c.valid && (!b.valid || better(c.inliers, c.fitness, c.index, b.inliers, b.fitness, b.index))) b = c;
-        }
-        RecordDev r{};
-        r.valid = b.valid;
-        r.inliers = b.valid ? b.inliers : 0;
-        r.fitness = b.valid ? b.fitness : 0.0;
-        r.index = b.valid ? b.index : -1;
-        for (int q = 0; q < 9; ++q) r.R[q] = b.valid ? cand_rt[12 * b.slot + q] : 0.0;
-        for (int q = 0; q < 3; ++q) r.t[q] = b.valid ? cand_rt[12 * b.slot + 9 + q] : 0.0;
-        r.sampled = sampled;
-        r.prerejected = static_cast<int64_t>(__ldcg(&ctr->prerejected));
-        r.degenerate = static_cast<int64_t>(__ldcg(&ctr->degenerate));
-        r.evaluated = n_cand;
-        r.qualified = static_cast<int64_t>(__ldcg(&ctr->qualified));
-        r.w_ref = static_cast<int64_t>(__ldcg(&ctr->w_ref));
-        r.evals_executed = static_cast<int64_t>(__ldcg(&ctr->evals_executed));
-        r.reserved = 0;
-        *rec = r;
-    }
+    const bool last = publish_cta(wt, ctr, block_best, blockIdx.x, true);
+    if (last) write_record(block_best, n_best_total, cand_rt, static_cast<int64_t>(__ldcg(&ctr->n_candidates)),
+                           sampled, ctr, rec);
+}
+
+int blocks_per_sm(const void* fn) {
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, kScoreThreads, 0) != cudaSuccess || b < 1) b = 1;
+    return b;
 }
 
 int score_blocks_per_sm() {
     static int cached = 0;
-    if (!cached) {
-        int b = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_score, kScoreThreads, 0) != cudaSuccess || b < 1) b = 1;
-        cached = b;
-    }
+    if (!cached) cached = blocks_per_sm(reinterpret_cast<const void*>(k_score));
+    return cached;
+}
+int split_blocks_per_sm() {
+    static int cached = 0;
+    if (!cached) cached = blocks_per_sm(reinterpret_cast<const void*>(k_score_split));
     return cached;
 }
 
@@ -343,14 +697,26 @@ void RunBuffers::release() {
     cudaFree(cand_rt);
     cudaFree(counters);
     cudaFree(block_best);
+    cudaFree(inl_masks);
+    cudaFree(miss_masks);
+    cudaFree(addends);
+    cudaFree(full_list);
+    cudaFree(cand_fast);
+    full_list = nullptr;
+    cand_fast = nullptr;
+    fast_capacity = 0;
     surv_index = nullptr;
     surv_ids = nullptr;
     cand_index = nullptr;
     cand_rt = nullptr;
     counters = nullptr;
     block_best = nullptr;
+    inl_masks = miss_masks = nullptr;
+    addends = nullptr;
     capacity = 0;
     n_blocks = 0;
+    split_cap = 0;
+    split_ns_pad = 0;
 }
 
 cudaError_t RunBuffers::ensure(int64_t cap, int32_t score_blocks) {
@@ -380,17 +746,60 @@ cudaError_t RunBuffers::ensure(int64_t cap, int32_t score_blocks) {
     return cudaSuccess;
 }
 
+cudaError_t RunBuffers::ensure_fast(int64_t n) {
+    if (n <= fast_capacity) return cudaSuccess;
+    cudaFree(cand_fast);
+    cand_fast = nullptr;
+    fast_capacity = 0;
+    cudaError_t e = cudaMalloc(&cand_fast, n * sizeof(FastRT));
+    if (e == cudaSuccess) fast_capacity = n;
+    return e;
+}
+
+cudaError_t RunBuffers::ensure_split(int64_t ns, int64_t max_candidates) {
+    const int64_t n_chunks = (ns + 31) / 32;
+    const int64_t ns_pad = n_chunks * 32;
+    // addends are the big buffer: keep it under kSplitBytes
+    int64_t cap = kSplitBytes / (ns_pad * static_cast<int64_t>(sizeof(double)));
+    if (cap > max_candidates) cap = max_candidates;
+    if (cap < 1) cap = 1;
+    if (cap <= split_cap && ns_pad == split_ns_pad) return cudaSuccess;
+    cudaFree(inl_masks);
+    cudaFree(miss_masks);
+    cudaFree(addends);
+    cudaFree(full_list);
+    inl_masks = miss_masks = nullptr;
+    addends = nullptr;
+    full_list = nullptr;
+    split_cap = 0;
+    cudaError_t e;
+    if ((e = cudaMalloc(&full_list, cap * sizeof(int64_t))) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&inl_masks, cap * n_chunks * sizeof(uint32_t))) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&miss_masks, cap * n_chunks * sizeof(uint32_t))) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&addends, cap * ns_pad * sizeof(double))) != cudaSuccess) return e;
+    split_cap = cap;
+    split_ns_pad = ns_pad;
+    return cudaSuccess;
+}
+
 cudaError_t run_hypotheses_range(const SourceView& src, const double* d_tgt_pos, const int32_t* d_cache,
                                  const GridView& grid, const ScoreParams& sp, uint64_t seed, double tau, int64_t begin,
                                  int64_t end, RunBuffers& rb, void* d_record, cudaStream_t stream, int sm_count,
                                  cudaEvent_t* events) {
     const int64_t count = end - begin;
-    const int blocks = sm_count * score_blocks_per_sm();
-    cudaError_t e = rb.ensure(count > 0 ? count : 1, blocks);
+    const int split_blocks = sm_count * split_blocks_per_sm();
+    const int sums_blocks = sm_count * 2;  // a warp per fully scored candidate, all in flight
+    const int exit_blocks = sm_count * 2;
+    const int over_blocks = sm_count;
+    cudaError_t e = rb.ensure(count > 0 ? count : 1, sums_blocks + exit_blocks + over_blocks);
     if (e != cudaSuccess) return e;
+    if ((e = rb.ensure_split(src.n, count > 0 ? count : 1)) != cudaSuccess) return e;
+    if ((e = rb.ensure_fast(count > 0 ? count : 1)) != cudaSuccess) return e;
+    FastRT* cand_fast = static_cast<FastRT*>(rb.cand_fast);
     if ((e = cudaMemsetAsync(rb.counters, 0, sizeof(Counters), stream)) != cudaSuccess) return e;
     const uint32_t ns = static_cast<uint32_t>(src.n);
     const uint32_t thresh = static_cast<uint32_t>(0x100000000ull % ns);
+    const int32_t n_chunks = static_cast<int32_t>((src.n + 31) / 32);
     if (events) cudaEventRecord(events[0], stream);
     if (count > 0) {
         int64_t want = (count + 255) / 256;
@@ -404,9 +813,23 @@ cudaError_t run_hypotheses_range(const SourceView& src, const double* d_tgt_pos,
                                                    rb.cand_rt, rb.counters);
     }
     if (events) cudaEventRecord(events[2], stream);
-    k_score<<<blocks, kScoreThreads, 0, stream>>>(src, grid, sp, rb.cand_rt, rb.cand_index, -1, count, nullptr,
-                                                  nullptr, rb.counters, rb.block_best,
-                                                  static_cast<RecordDev*>(d_record));
+    k_prep_fast<<<sm_count * 2, 128, 0, stream>>>(rb.cand_rt, -1, rb.counters, grid, sp, cand_fast);
+    k_score_split<<<split_blocks, kScoreThreads, 0, stream>>>(src, grid, sp, rb.cand_rt, cand_fast, rb.split_cap,
+                                                              n_chunks,
+                                                              rb.split_ns_pad, rb.inl_masks, rb.miss_masks,
+                                                              rb.addends, rb.counters);
+    // candidates beyond the split capacity (normally none): streamed warp per candidate
+    k_score<<<over_blocks, kScoreThreads, 0, stream>>>(src, grid, sp, rb.cand_rt, cand_fast, rb.cand_index,
+                                                       rb.split_cap, -1,
+                                                       count, nullptr, nullptr, rb.counters, rb.block_best,
+                                                       sums_blocks + exit_blocks, nullptr);
+    k_score_exits<<<exit_blocks, kScoreThreads, 0, stream>>>(src.n, sp, rb.split_cap, n_chunks, rb.miss_masks,
+                                                             rb.full_list, rb.counters, rb.block_best, sums_blocks);
+    k_score_sums<<<sums_blocks, kScoreThreads, 0, stream>>>(src.n, sp, rb.cand_rt, rb.cand_index, n_chunks,
+                                                            rb.split_ns_pad, rb.inl_masks, rb.addends, rb.full_list,
+                                                            sums_blocks + exit_blocks + over_blocks, count,
+                                                            rb.counters, rb.block_best,
+                                                            static_cast<RecordDev*>(d_record));
     if (events) cudaEventRecord(events[3], stream);
     return cudaGetLastError();
 }
@@ -417,9 +840,13 @@ cudaError_t score_candidates(const SourceView& src, const GridView& grid, const 
     const int blocks = sm_count * score_blocks_per_sm();
     cudaError_t e = rb.ensure(1, blocks);
     if (e != cudaSuccess) return e;
+    if ((e = rb.ensure_fast(C > 0 ? C : 1)) != cudaSuccess) return e;
+    FastRT* cand_fast = static_cast<FastRT*>(rb.cand_fast);
     if ((e = cudaMemsetAsync(rb.counters, 0, sizeof(Counters), stream)) != cudaSuccess) return e;
-    k_score<<<blocks, kScoreThreads, 0, stream>>>(src, grid, sp, d_rt, nullptr, C, C, d_out_inliers, d_out_sum,
-                                                  rb.counters, rb.block_best, static_cast<RecordDev*>(d_record));
+    if (C > 0) k_prep_fast<<<sm_count * 2, 128, 0, stream>>>(d_rt, C, rb.counters, grid, sp, cand_fast);
+    k_score<<<blocks, kScoreThreads, 0, stream>>>(src, grid, sp, d_rt, cand_fast, nullptr, 0, C, C, d_out_inliers,
+                                                  d_out_sum,
+                                                  rb.counters, rb.block_best, 0, static_cast<RecordDev*>(d_record));
     return cudaGetLastError();
 }
 

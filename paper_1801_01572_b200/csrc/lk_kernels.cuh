@@ -26,17 +26,33 @@ struct GridView {
     const double* slot_pos;  // 3 * npoints, CSR order
     const double* slot_nrm;  // 3 * npoints, CSR order (zeros when absent)
     const uint8_t* near;     // ncells: some point within the block of this cell
+    // Block lists (radius-1 grids): for every cell, the points of its 3x3x3
+    // block stored contiguously, so a query is one 8-byte cell load plus a
+    // linear scan of 32-byte entries. count == 0 <=> not near-occupied.
+    const int2* block_info;    // (offset, count) per cell; null when not built
+    const double4* block_pts;  // x, y, z, original index
+    const double* nrm_orig;    // 3 * npoints normals in original point order
+    // FP32 image of the block lists for the guard-band fast path: local cell
+    // coordinates ((x - o) / cell - off) rounded to float, original index in w.
+    const float4* block_f32;
+    const double* pos_orig;    // 3 * npoints positions in original point order
 };
 
 struct GridStorage {
     GridView view{};
     int64_t ncells = 0;
     int64_t npoints = 0;
+    int64_t nblock = 0;
     int32_t* start = nullptr;
     int32_t* index = nullptr;
     double* slot_pos = nullptr;
     double* slot_nrm = nullptr;
     uint8_t* near = nullptr;
+    int2* block_info = nullptr;
+    double4* block_pts = nullptr;
+    double* nrm_orig = nullptr;
+    float4* block_f32 = nullptr;
+    double* pos_orig = nullptr;
     void release();
 };
 
@@ -56,7 +72,8 @@ struct Counters {  // device-side, zeroed per run
     unsigned long long evals_executed;
     unsigned long long work_next;   // work queue head for k_score
     unsigned long long blocks_done; // last-block-done ticket
-    unsigned long long _pad[7];
+    unsigned long long n_full;      // split candidates that were fully scored
+    unsigned long long _pad[6];
 };
 
 struct BestRec {  // per-block best, then the final record
@@ -76,13 +93,27 @@ struct RunBuffers {
     Counters* counters = nullptr;
     BestRec* block_best = nullptr;
     int32_t n_blocks = 0;
+    // split scoring: per (candidate, 32-point chunk) inlier / miss ballots and
+    // the inliers' d2, for up to split_cap candidates (addends <= kSplitBytes)
+    static constexpr int64_t kSplitBytes = int64_t(1) << 30;
+    uint32_t* inl_masks = nullptr;
+    uint32_t* miss_masks = nullptr;
+    double* addends = nullptr;
+    int64_t* full_list = nullptr;
+    void* cand_fast = nullptr;  // per-candidate FP32 transform + guard bands
+    int64_t fast_capacity = 0;
+    int64_t split_cap = 0;
+    int64_t split_ns_pad = 0;
     void release();
     cudaError_t ensure(int64_t cap, int32_t score_blocks);
+    cudaError_t ensure_split(int64_t ns, int64_t max_candidates);
+    cudaError_t ensure_fast(int64_t n);
 };
 
 struct SourceView {
-    const double* pos;  // 3 * ns
-    const double* nrm;  // 3 * ns
+    const double* pos;    // 3 * ns
+    const double* nrm;    // 3 * ns
+    const float4* pos32;  // ns float copies (x, y, z, 0) for the fast path; null -> FP64 only
     int64_t n;
 };
 
@@ -94,7 +125,19 @@ struct ScoreParams {
     double max_fitness;
     int64_t miss_budget;  // INT64_MAX disables the early exit
     int32_t fitness_from_distance;  // 1: sum sqrt(d2)^2 (evaluate_hypothesis), 0: sum d2
+    int32_t fast;         // 1: FP32 guard-band scan with exact FP64 decisions
+    float thr_cells;      // (d_max / cell)^2: d2_max in squared cell units
+    float band_cells;     // guard band on d2 in squared cell units
+    float eps_cells;      // guard on cell-coordinate fractions
+    float pmax_cells;     // max |p| over the source, in cells
+    float nmax_cells;     // max grid dimension
 };
+
+// Fills ScoreParams' fast-path fields for a grid; disables the fast path when
+// the magnitudes exceed what its guard bands cover.
+void configure_fast_path(ScoreParams& sp, const GridView& g, double max_abs_source);
+
+cudaError_t make_source32(const double* d_pos, int64_t n, float4* d_out, cudaStream_t stream);
 
 // Samples, pre-rejects and fits hypotheses [begin, end); scores the
 // candidates; reduces the per-run best into `record` (an lk_reg_record, device).

@@ -1,0 +1,88 @@
+// Compiles the C++ shim (include/loopkit_b200/registration.hpp) against
+// reference-shaped types and exercises its error mapping / results.
+// usage: test_shim cpu   -> expects CudaError (no device: no CPU fallback)
+//        test_shim gpu   -> registers a planted pair and prints the result
+#include <array>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <optional>
+#include <random>
+#include <vector>
+
+#include "loopkit_b200/registration.hpp"
+
+struct Vec3 {  // stands in for Eigen::Vector3d: 3 packed doubles
+    double x, y, z;
+};
+struct PointCloud {  // proj/include/loopkit/geometry.hpp:92-99
+    std::vector<Vec3> positions;
+    std::vector<Vec3> normals;
+};
+struct RegistrationParams {  // proj/include/loopkit/registration.hpp:17-32
+    double leaf = 0.05;
+    double normal_radius = 0.1;
+    double feature_radius = 0.25;
+    std::int64_t hypothesis_count = 4'000'000;
+    double similarity_tau = 0.9;
+    double d_max = 0.075;
+    double min_inlier_ratio = 0.25;
+    std::optional<double> max_fitness;
+    double normal_angle_max = 30.0 * M_PI / 180.0;
+    std::uint64_t seed = 0;
+    int threads = 0;
+};
+
+int main(int argc, char** argv) {
+    const bool gpu = argc > 1 && std::strcmp(argv[1], "gpu") == 0;
+    PointCloud tiny;
+    tiny.positions = {{0, 0, 0}, {1, 0, 0}, {0, 1, 0}};
+    tiny.normals = {{0, 0, 1}, {0, 0, 1}, {0, 0, 1}};
+    RegistrationParams params;
+    params.hypothesis_count = 10'000;
+    // a box-shaped cloud and a shifted copy
+    PointCloud src, tgt;
+    std::mt19937 rng(5);
+    std::uniform_real_distribution<double> u(-1.0, 1.0);
+    for (int i = 0; i < 6000; ++i) {
+        int face = i % 3;
+        Vec3 p{u(rng), u(rng), u(rng)};
+        Vec3 n{0, 0, 0};
+        if (face == 0) { p.x = -1; n.x = 1; }
+        if (face == 1) { p.y = -1; n.y = 1; }
+        if (face == 2) { p.z = -1; n.z = 1; }
+        src.positions.push_back(p);
+        src.normals.push_back(n);
+        tgt.positions.push_back({p.x + 0.1, p.y - 0.05, p.z + 0.02});
+        tgt.normals.push_back(n);
+    }
+    if (!gpu) {
+        try {
+            loopkit_b200::register_global(src, tgt, params);
+            std::puts("FAIL: expected CudaError without a device");
+            return 1;
+        } catch (const loopkit_b200::CudaError& e) {
+            std::printf("ok: CudaError (%s)\n", e.what());
+        }
+        return 0;
+    }
+    try {
+        loopkit_b200::register_global(tiny, tgt, params);
+        std::puts("FAIL: expected TooFewPoints");
+        return 1;
+    } catch (const loopkit_b200::TooFewPoints&) {
+        std::puts("ok: TooFewPoints");
+    }
+    loopkit_b200::HypothesisStats st{};
+    auto r = loopkit_b200::register_global(src, tgt, params, &st);
+    if (!r) {
+        std::puts("FAIL: no alignment");
+        return 1;
+    }
+    std::printf("ok: index %lld inliers %lld ratio %.6f t = %.4f %.4f %.4f sampled %lld\n",
+                (long long)r->hypothesis_index, (long long)r->inliers, r->inlier_ratio, r->transform.t[0],
+                r->transform.t[1], r->transform.t[2], (long long)st.sampled);
+    auto ef = loopkit_b200::evaluate_hypothesis(r->transform, src, tgt, 0.075, params);
+    std::printf("ok: evaluate_hypothesis ratio %.6f fitness %.3e\n", ef.first, ef.second);
+    return 0;
+}

@@ -217,6 +217,43 @@ def test_score_candidates_eval_grid_early_exit_matches_oracle(oracle):
             assert sc.best.hypothesis_index == ref["best"].hypothesis_index
 
 
+@pytest.mark.parametrize("fp64_only", ["0", "1"])
+@pytest.mark.parametrize("kind", [0, 1])
+def test_fast_path_and_fp64_path_match_oracle(oracle, monkeypatch, fp64_only, kind):
+    # many random candidates around the truth: lots of near-boundary points,
+    # near-ties and cell-face crossings for the FP32 guard bands to catch
+    monkeypatch.setenv("LK_FP64_ONLY", fp64_only)
+    pair = synth.synth_registration_pair(6)
+    rng = np.random.default_rng(99 + kind)
+    rts = []
+    for _ in range(1500):
+        d = synth.transform_from_twist(np.concatenate([rng.normal(0, 0.03, 3), rng.normal(0, 0.04, 3)]))
+        rts.append(synth.compose(pair.truth, d).packed())
+    rt = np.stack(rts)
+    params = lk.RegistrationParams()
+    grid = lk.build_eval_grid(pair.target, params.d_max) if kind == 0 else lk.build_grid(pair.target, 0.075)
+    sc = lk.score_candidates(grid, pair.source, rt, params)
+    ref = oracle.score_candidates(pair.source.positions, pair.source.normals, pair.target.positions,
+                                  pair.target.normals, rt, 0 if kind == 0 else 1, 0, 0.075,
+                                  oracle.params_from(params))
+    assert np.array_equal(sc.inliers, ref["inliers"])
+    assert np.array_equal(sc.fitness, ref["fitness"])
+    assert sc.qualified == ref["qualified"]
+    assert sc.best.hypothesis_index == ref["best"].hypothesis_index
+
+
+def test_run_hypotheses_fp64_only_path(prepared1, oracle, monkeypatch):
+    monkeypatch.setenv("LK_FP64_ONLY", "1")
+    octx, c = prepared1
+    params = lk.RegistrationParams(hypothesis_count=30_000, seed=5)
+    ctx = lk.registration_context(lk.PointCloud(c["src"], c["src_n"]), lk.PointCloud(c["tgt"], c["tgt_n"]),
+                                  c["cache"], params)
+    st = lk.HypothesisStats()
+    dev = lk.run_hypotheses(ctx, params, st)
+    orc, ost = octx.run(oracle.params_from(params))
+    _assert_same_result(dev, orc, st, ost)
+
+
 def test_edge_info_matches_oracle(oracle):
     # test_line_process.cpp:67-109 + config E shape
     ci = synth.random_cloud(40, 71, 0, -0.5, 0.5)
