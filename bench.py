@@ -316,9 +316,11 @@ def run_b200(args):
         if k > 0:
             e2e_times.append(t1 - t0)
         ns2, nt2 = c2.n_source, c2.n_target
-        # bytes copied by the library this step
-        h2d = 48 * (ns2 + nt2) + 132 * (ns2 + nt2) + 4 * ns2
-        d2h = 4 * ns2 + 48 + host.nbytes
+        # bytes copied by the library this step: the raw clouds (positions +
+        # normals) in; downsampled clouds, features, cache, grid bounds and the
+        # record buffer out
+        h2d = 48 * (src_h.size() + tgt_h.size())
+        d2h = 48 * (ns2 + nt2) + 132 * (ns2 + nt2) + 4 * ns2 + 4 * 64 + host.nbytes
         c2.close()
     e2e_s = torch.tensor([statistics.mean(e2e_times)], dtype=torch.float64, device=dev)
     if world > 1:
@@ -339,8 +341,8 @@ def run_b200(args):
             "kernel_ms_per_step": {k: v / max(runs, 1) for k, v in kt.items()},
             "e2e": {"value": w_step / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "ms_per_registration": e2e_s * 1e3,
-                    "note": "prepare_registration (host downsample+FPFH this tier, device feature match + grid) "
-                            "+ hypotheses + exchange + merge"},
+                    "note": "prepare_registration on the device (H2D of the raw pinned clouds, voxel "
+                            "downsample, FPFH, feature match, EvalGrid) + hypotheses + exchange + merge"},
             "paper_ms_per_registration": PAPER_MS_PER_REGISTRATION,
             "gpu_launches": 3 * args.steps,
             "clocks": clock_info,

@@ -69,6 +69,16 @@ int select_device(int32_t device) {
     if (dev < 0) CK(cudaGetDevice(&dev));
     if (dev >= n) throw lk::Status(LK_INVALID_ARGUMENT, "device ordinal out of range");
     CK(cudaSetDevice(dev));
+    // keep freed pool memory resident: contexts are created per registration
+    static std::once_flag once[64];
+    if (dev < 64)
+        std::call_once(once[dev], [dev] {
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                uint64_t thr = UINT64_MAX;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            }
+        });
     return dev;
 }
 
@@ -81,15 +91,9 @@ int sm_count_of(int dev) {
 template <class T>
 T* dev_upload(const T* host, size_t count, cudaStream_t s) {
     T* d = nullptr;
-    CK(cudaMalloc(&d, std::max<size_t>(count, 1) * sizeof(T)));
+    CK(lkk::pool_alloc(&d, std::max<size_t>(count, 1) * sizeof(T), s));
     if (count) CK(cudaMemcpyAsync(d, host, count * sizeof(T), cudaMemcpyHostToDevice, s));
     return d;
-}
-
-std::vector<double> flatten(const std::vector<lk::Vec3>& v) {
-    std::vector<double> out(3 * v.size());
-    for (size_t i = 0; i < v.size(); ++i) lk::store3(out.data(), static_cast<int64_t>(i), v[i]);
-    return out;
 }
 
 void check_cloud_ptr(const lk_cloud* c, const char* what) {
@@ -164,9 +168,10 @@ struct lk_grid {
     std::mutex mu;
     ~lk_grid() {
         cudaSetDevice(device);
+        if (stream) cudaStreamSynchronize(stream);
         g.release();
         rb.release();
-        cudaFree(d_record);
+        lkk::pool_free(d_record, stream);
         if (stream) cudaStreamDestroy(stream);
     }
 };
@@ -209,33 +214,36 @@ struct lk_reg_ctx {
     ~lk_reg_ctx() {
         cudaSetDevice(device);
         drain_events();
-        cudaFree(d_spos);
-        cudaFree(d_spos32);
-        cudaFree(d_snrm);
-        cudaFree(d_tpos);
-        cudaFree(d_tnrm);
-        cudaFree(d_cache);
+        if (stream) cudaStreamSynchronize(stream);
+        cudaStream_t s = own_stream;
+        lkk::pool_free(d_spos, s);
+        lkk::pool_free(d_spos32, s);
+        lkk::pool_free(d_snrm, s);
+        lkk::pool_free(d_tpos, s);
+        lkk::pool_free(d_tnrm, s);
+        lkk::pool_free(d_cache, s);
         grid.release();
         rb.release();
-        cudaFree(d_record);
+        lkk::pool_free(d_record, s);
         if (own_stream) cudaStreamDestroy(own_stream);
     }
 };
 
 namespace {
 
-// Uploads the prepared clouds + cache and builds the EvalGrid on the device.
+// Uploads whatever of the prepared clouds + cache is not on the device yet and
+// builds the EvalGrid on the device.
 void ctx_finish(lk_reg_ctx* c, const lk_reg_params& p) {
     cudaStream_t s = c->stream;
-    c->d_spos = dev_upload(c->h_spos.data(), c->h_spos.size(), s);
-    c->d_snrm = dev_upload(c->h_snrm.data(), c->h_snrm.size(), s);
-    c->d_tpos = dev_upload(c->h_tpos.data(), c->h_tpos.size(), s);
-    c->d_tnrm = dev_upload(c->h_tnrm.data(), c->h_tnrm.size(), s);
+    if (!c->d_spos) c->d_spos = dev_upload(c->h_spos.data(), c->h_spos.size(), s);
+    if (!c->d_snrm) c->d_snrm = dev_upload(c->h_snrm.data(), c->h_snrm.size(), s);
+    if (!c->d_tpos) c->d_tpos = dev_upload(c->h_tpos.data(), c->h_tpos.size(), s);
+    if (!c->d_tnrm) c->d_tnrm = dev_upload(c->h_tnrm.data(), c->h_tnrm.size(), s);
     if (!c->d_cache) c->d_cache = dev_upload(c->h_cache.data(), c->h_cache.size(), s);
-    CK(cudaMalloc(&c->d_spos32, std::max<int64_t>(c->ns, 1) * sizeof(float4)));
+    CK(lkk::pool_alloc(&c->d_spos32, std::max<int64_t>(c->ns, 1) * sizeof(float4), s));
     CK(lkk::make_source32(c->d_spos, c->ns, c->d_spos32, s));
     c->src_max_norm = max_norm(c->h_spos.data(), c->ns);
-    CK(cudaMalloc(&c->d_record, sizeof(lk_reg_record)));
+    CK(lkk::pool_alloc(&c->d_record, sizeof(lk_reg_record), s));
     CK(lkk::build_grid(c->grid, 0, c->d_tpos, c->d_tnrm, c->nt, p.d_max, p.d_max, s));
 }
 
@@ -246,6 +254,7 @@ lk_reg_ctx* ctx_new(int32_t device) {
         c->sm_count = sm_count_of(c->device);
         CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
         c->stream = c->own_stream;
+        c->rb.stream = c->own_stream;
     } catch (...) {
         delete c;
         throw;
@@ -259,47 +268,74 @@ lk_status prepare_impl(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_pa
     check_cloud_ptr(tgt, "target");
     *out = nullptr;
     double t0 = now_s();
-    // registration.cpp:226-231
-    lk::Cloud s = lk::voxel_downsample(lk::make_cloud(src->xyz, src->nxyz, src->n), params->leaf);
-    lk::Cloud t = lk::voxel_downsample(lk::make_cloud(tgt->xyz, tgt->nxyz, tgt->n), params->leaf);
-    if (s.size() < 4 || t.size() < 4)
-        return fail(LK_TOO_FEW_POINTS, "register_global: fewer than 4 points after downsampling");
-    if (!s.has_normals() || !t.has_normals())
+    if (src->n == 0 || tgt->n == 0) return fail(LK_EMPTY_CLOUD, "voxel_downsample: empty cloud");
+    if (!(params->leaf > 0.0)) return fail(LK_INVALID_ARGUMENT, "voxel_downsample: leaf must be positive");
+    // estimate_normals (preprocess.cpp:61-96) is not part of this tier
+    if (!src->nxyz || !tgt->nxyz)
         return fail(LK_MISSING_NORMALS,
                     "register_global: inputs without normals need estimate_normals (not in this tier)");
-    auto usable = [](const lk::Cloud& c) {
-        size_t k = 0;
-        for (const lk::Vec3& n : c.nrm) k += lk::is_zero(n) ? 0u : 1u;
-        return k;
-    };
-    if (usable(s) < 4 || usable(t) < 4)
-        return fail(LK_MISSING_DATA, "register_global: fewer than 4 points with usable normals");
-    auto sf = lk::compute_fpfh(s, params->feature_radius, params->threads);
-    auto tf = lk::compute_fpfh(t, params->feature_radius, params->threads);
     lk_reg_ctx* c = ctx_new(params->device);
+    double* raw[4] = {nullptr, nullptr, nullptr, nullptr};
+    float *d_sf = nullptr, *d_tf = nullptr;
+    auto cleanup = [&] {
+        for (double* p : raw) lkk::pool_free(p, c->stream);
+        lkk::pool_free(d_sf, c->stream);
+        lkk::pool_free(d_tf, c->stream);
+    };
     try {
-        c->ns = static_cast<int64_t>(s.size());
-        c->nt = static_cast<int64_t>(t.size());
-        c->h_spos = flatten(s.pos);
-        c->h_snrm = flatten(s.nrm);
-        c->h_tpos = flatten(t.pos);
-        c->h_tnrm = flatten(t.nrm);
-        c->h_sfeat.resize(33 * sf.size());
-        c->h_tfeat.resize(33 * tf.size());
-        for (size_t i = 0; i < sf.size(); ++i) std::memcpy(&c->h_sfeat[33 * i], sf[i].data(), 33 * sizeof(float));
-        for (size_t i = 0; i < tf.size(); ++i) std::memcpy(&c->h_tfeat[33 * i], tf[i].data(), 33 * sizeof(float));
-        // feature pre-match on the device (registration.cpp:248)
-        float* d_sf = dev_upload(c->h_sfeat.data(), c->h_sfeat.size(), c->stream);
-        float* d_tf = dev_upload(c->h_tfeat.data(), c->h_tfeat.size(), c->stream);
-        CK(cudaMalloc(&c->d_cache, c->ns * sizeof(int32_t)));
-        CK(lkk::feature_nn(d_sf, c->ns, d_tf, c->nt, c->d_cache, c->stream));
+        cudaStream_t s = c->stream;
+        // H2D of the raw clouds, then voxel_downsample on the device (registration.cpp:226-228)
+        raw[0] = dev_upload(src->xyz, 3 * src->n, s);
+        raw[1] = dev_upload(src->nxyz, 3 * src->n, s);
+        raw[2] = dev_upload(tgt->xyz, 3 * tgt->n, s);
+        raw[3] = dev_upload(tgt->nxyz, 3 * tgt->n, s);
+        CK(lkk::pool_alloc(&c->d_spos, 3 * src->n * sizeof(double), s));
+        CK(lkk::pool_alloc(&c->d_snrm, 3 * src->n * sizeof(double), s));
+        CK(lkk::pool_alloc(&c->d_tpos, 3 * tgt->n * sizeof(double), s));
+        CK(lkk::pool_alloc(&c->d_tnrm, 3 * tgt->n * sizeof(double), s));
+        int st_s = 0, st_t = 0;
+        CK(lkk::voxel_downsample(raw[0], raw[1], src->n, params->leaf, c->d_spos, c->d_snrm, &c->ns, &st_s, s));
+        if (st_s == 5) throw lk::Status(LK_MISSING_NORMALS, "normals must be unit length or exactly zero");
+        CK(lkk::voxel_downsample(raw[2], raw[3], tgt->n, params->leaf, c->d_tpos, c->d_tnrm, &c->nt, &st_t, s));
+        if (st_t == 5) throw lk::Status(LK_MISSING_NORMALS, "normals must be unit length or exactly zero");
+        if (c->ns < 4 || c->nt < 4)
+            throw lk::Status(LK_TOO_FEW_POINTS, "register_global: fewer than 4 points after downsampling");
+        // host copies of the downsampled clouds (download(), source magnitude bound)
+        c->h_spos.resize(3 * c->ns);
+        c->h_snrm.resize(3 * c->ns);
+        c->h_tpos.resize(3 * c->nt);
+        c->h_tnrm.resize(3 * c->nt);
+        CK(cudaMemcpyAsync(c->h_spos.data(), c->d_spos, 3 * c->ns * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(c->h_snrm.data(), c->d_snrm, 3 * c->ns * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(c->h_tpos.data(), c->d_tpos, 3 * c->nt * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(c->h_tnrm.data(), c->d_tnrm, 3 * c->nt * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        auto usable = [](const std::vector<double>& nrm) {
+            size_t k = 0;
+            for (size_t i = 0; i + 2 < nrm.size(); i += 3)
+                k += (nrm[i] == 0.0 && nrm[i + 1] == 0.0 && nrm[i + 2] == 0.0) ? 0u : 1u;
+            return k;
+        };
+        if (usable(c->h_snrm) < 4 || usable(c->h_tnrm) < 4)
+            throw lk::Status(LK_MISSING_DATA, "register_global: fewer than 4 points with usable normals");
+        // FPFH (registration.cpp:246-247) and the feature pre-match (:248) on the device
+        CK(lkk::pool_alloc(&d_sf, 33 * c->ns * sizeof(float), s));
+        CK(lkk::pool_alloc(&d_tf, 33 * c->nt * sizeof(float), s));
+        CK(lkk::compute_fpfh(c->d_spos, c->d_snrm, c->ns, params->feature_radius, d_sf, s));
+        CK(lkk::compute_fpfh(c->d_tpos, c->d_tnrm, c->nt, params->feature_radius, d_tf, s));
+        CK(lkk::pool_alloc(&c->d_cache, c->ns * sizeof(int32_t), s));
+        CK(lkk::feature_nn(d_sf, c->ns, d_tf, c->nt, c->d_cache, s));
         c->h_cache.resize(c->ns);
-        CK(cudaMemcpyAsync(c->h_cache.data(), c->d_cache, c->ns * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaStreamSynchronize(c->stream));
-        cudaFree(d_sf);
-        cudaFree(d_tf);
-        ctx_finish(c, *params);
+        c->h_sfeat.resize(33 * c->ns);
+        c->h_tfeat.resize(33 * c->nt);
+        CK(cudaMemcpyAsync(c->h_cache.data(), c->d_cache, c->ns * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(c->h_sfeat.data(), d_sf, 33 * c->ns * sizeof(float), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(c->h_tfeat.data(), d_tf, 33 * c->nt * sizeof(float), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        cleanup();
+        ctx_finish(c, *params);  // EvalGrid on the device (registration.cpp:249)
     } catch (...) {
+        cleanup();
         delete c;
         throw;
     }
@@ -535,6 +571,7 @@ lk_status lk_grid_build(const lk_cloud* target, int32_t kind, double cell, doubl
             g->d_max = d_max;
             g->has_normals = target->nxyz != nullptr;
             CK(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+            g->rb.stream = g->stream;
             double* d_pos = dev_upload(target->xyz, 3 * target->n, g->stream);
             double* d_nrm = target->nxyz ? dev_upload(target->nxyz, 3 * target->n, g->stream) : nullptr;
             cudaError_t e = lkk::build_grid(g->g, kind, d_pos, d_nrm, target->n, cell, d_max, g->stream);
@@ -744,22 +781,60 @@ lk_status lk_voxel_downsample(const lk_cloud* cloud, double leaf, double* out_xy
     return guarded([&]() -> lk_status {
         check_cloud_ptr(cloud, "cloud");
         if (!out_xyz || !out_count) return fail(LK_INVALID_ARGUMENT, "null argument");
-        lk::Cloud d = lk::voxel_downsample(lk::make_cloud(cloud->xyz, cloud->nxyz, cloud->n), leaf);
-        for (size_t i = 0; i < d.size(); ++i) {
-            lk::store3(out_xyz, static_cast<int64_t>(i), d.pos[i]);
-            if (out_n && d.has_normals()) lk::store3(out_n, static_cast<int64_t>(i), d.nrm[i]);
-        }
-        *out_count = static_cast<int64_t>(d.size());
+        if (cloud->n == 0) return fail(LK_EMPTY_CLOUD, "voxel_downsample: empty cloud");
+        if (!(leaf > 0.0)) return fail(LK_INVALID_ARGUMENT, "voxel_downsample: leaf must be positive");
+        select_device(-1);
+        cudaStream_t s;
+        CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        double* d_in = dev_upload(cloud->xyz, 3 * cloud->n, s);
+        double* d_inn = cloud->nxyz ? dev_upload(cloud->nxyz, 3 * cloud->n, s) : nullptr;
+        double *d_out = nullptr, *d_outn = nullptr;
+        cudaError_t e = cudaMalloc(&d_out, 3 * cloud->n * sizeof(double));
+        if (e == cudaSuccess && d_inn) e = cudaMalloc(&d_outn, 3 * cloud->n * sizeof(double));
+        int st = 0;
+        int64_t cnt = 0;
+        if (e == cudaSuccess) e = lkk::voxel_downsample(d_in, d_inn, cloud->n, leaf, d_out, d_outn, &cnt, &st, s);
+        if (e == cudaSuccess && st == 0)
+            e = cudaMemcpyAsync(out_xyz, d_out, 3 * cnt * sizeof(double), cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess && st == 0 && out_n && d_outn)
+            e = cudaMemcpyAsync(out_n, d_outn, 3 * cnt * sizeof(double), cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        cudaFree(d_in);
+        cudaFree(d_inn);
+        cudaFree(d_out);
+        cudaFree(d_outn);
+        cudaStreamDestroy(s);
+        CK(e);
+        if (st == 5) return fail(LK_MISSING_NORMALS, "normals must be unit length or exactly zero");
+        *out_count = cnt;
         return LK_OK;
     });
 }
 
 lk_status lk_compute_fpfh(const lk_cloud* cloud, double radius, int32_t threads, float* out) {
+    (void)threads;  // the device implementation has no host thread knob
     return guarded([&]() -> lk_status {
         check_cloud_ptr(cloud, "cloud");
         if (!out) return fail(LK_INVALID_ARGUMENT, "null argument");
-        auto f = lk::compute_fpfh(lk::make_cloud(cloud->xyz, cloud->nxyz, cloud->n), radius, threads);
-        for (size_t i = 0; i < f.size(); ++i) std::memcpy(out + 33 * i, f[i].data(), 33 * sizeof(float));
+        if (cloud->n == 0) return fail(LK_EMPTY_CLOUD, "compute_fpfh: empty cloud");
+        if (!cloud->nxyz) return fail(LK_MISSING_NORMALS, "compute_fpfh: cloud has no normals");
+        if (!(radius > 0.0)) return fail(LK_INVALID_ARGUMENT, "build_grid: cell_length must be positive");
+        lk::validate_cloud(lk::make_cloud(cloud->xyz, cloud->nxyz, cloud->n));
+        select_device(-1);
+        cudaStream_t s;
+        CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        double* d_p = dev_upload(cloud->xyz, 3 * cloud->n, s);
+        double* d_n = dev_upload(cloud->nxyz, 3 * cloud->n, s);
+        float* d_f = nullptr;
+        cudaError_t e = cudaMalloc(&d_f, 33 * cloud->n * sizeof(float));
+        if (e == cudaSuccess) e = lkk::compute_fpfh(d_p, d_n, cloud->n, radius, d_f, s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(out, d_f, 33 * cloud->n * sizeof(float), cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        cudaFree(d_p);
+        cudaFree(d_n);
+        cudaFree(d_f);
+        cudaStreamDestroy(s);
+        CK(e);
         return LK_OK;
     });
 }

@@ -310,6 +310,8 @@ __global__ void k_copy_normals(const double* __restrict__ nrm, int64_t n, double
 
 inline unsigned blocks_for(int64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
 
+}  // namespace
+
 // exclusive scan of n int32 into out[0..n] (out[n] = total)
 cudaError_t exclusive_scan(const int32_t* in, int64_t n, int32_t* out, cudaStream_t stream) {
     int64_t ntiles = (n + kScanTile - 1) / kScanTile;
@@ -323,19 +325,17 @@ cudaError_t exclusive_scan(const int32_t* in, int64_t n, int32_t* out, cudaStrea
     return cudaGetLastError();
 }
 
-}  // namespace
-
 void GridStorage::release() {
-    cudaFree(start);
-    cudaFree(index);
-    cudaFree(slot_pos);
-    cudaFree(slot_nrm);
-    cudaFree(near);
-    cudaFree(block_info);
-    cudaFree(block_pts);
-    cudaFree(nrm_orig);
-    cudaFree(block_f32);
-    cudaFree(pos_orig);
+    pool_free(start, stream);
+    pool_free(index, stream);
+    pool_free(slot_pos, stream);
+    pool_free(slot_nrm, stream);
+    pool_free(near, stream);
+    pool_free(block_info, stream);
+    pool_free(block_pts, stream);
+    pool_free(nrm_orig, stream);
+    pool_free(block_f32, stream);
+    pool_free(pos_orig, stream);
     start = index = nullptr;
     slot_pos = slot_nrm = nullptr;
     near = nullptr;
@@ -353,7 +353,8 @@ void GridStorage::release() {
     } while (0)
 
 cudaError_t build_grid(GridStorage& g, int kind, const double* d_pos, const double* d_nrm, int64_t n, double cell,
-                       double d_max, cudaStream_t stream) {
+                       double d_max, cudaStream_t stream, bool with_blocks) {
+    g.stream = stream;
     if (n <= 0 || n > INT32_MAX) return cudaErrorInvalidValue;
     GridView v{};
     v.kind = kind;
@@ -407,12 +408,12 @@ cudaError_t build_grid(GridStorage& g, int kind, const double* d_pos, const doub
     if (ncells <= 0 || ncells > (int64_t)1 << 30) return cudaErrorInvalidValue;
     g.ncells = ncells;
     g.npoints = n;
-    LK_TRY(cudaMalloc(&g.start, (ncells + 1) * sizeof(int32_t)));
-    LK_TRY(cudaMalloc(&g.index, n * sizeof(int32_t)));
-    LK_TRY(cudaMalloc(&g.slot_pos, 3 * n * sizeof(double)));
-    LK_TRY(cudaMalloc(&g.slot_nrm, 3 * n * sizeof(double)));
-    LK_TRY(cudaMalloc(&g.near, ncells));
-    LK_TRY(cudaMalloc(&g.nrm_orig, 3 * n * sizeof(double)));
+    LK_TRY(pool_alloc(&g.start, (ncells + 1) * sizeof(int32_t), stream));
+    LK_TRY(pool_alloc(&g.index, n * sizeof(int32_t), stream));
+    LK_TRY(pool_alloc(&g.slot_pos, 3 * n * sizeof(double), stream));
+    LK_TRY(pool_alloc(&g.slot_nrm, 3 * n * sizeof(double), stream));
+    LK_TRY(pool_alloc(&g.near, ncells, stream));
+    LK_TRY(pool_alloc(&g.nrm_orig, 3 * n * sizeof(double), stream));
     int32_t *d_cell_of = nullptr, *d_counts = nullptr;
     LK_TRY(cudaMallocAsync(&d_cell_of, n * sizeof(int32_t), stream));
     LK_TRY(cudaMallocAsync(&d_counts, ncells * sizeof(int32_t), stream));
@@ -431,7 +432,7 @@ cudaError_t build_grid(GridStorage& g, int kind, const double* d_pos, const doub
         LK_TRY(cudaMemsetAsync(g.near, 1, ncells, stream));  // wide blocks: no occupancy shortcut
     }
     // 3x3x3 block lists for radius-1 grids (27 entries per point at most)
-    if (v.radius == 1 && 27 * n < INT32_MAX) {
+    if (with_blocks && v.radius == 1 && 27 * n < INT32_MAX) {
         k_block_count<<<blocks_for(ncells, 256), 256, 0, stream>>>(g.start, ncells, v, d_counts);
         int32_t* d_off = nullptr;
         LK_TRY(cudaMallocAsync(&d_off, (ncells + 1) * sizeof(int32_t), stream));
@@ -440,10 +441,10 @@ cudaError_t build_grid(GridStorage& g, int kind, const double* d_pos, const doub
         LK_TRY(cudaMemcpyAsync(&total, d_off + ncells, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
         LK_TRY(cudaStreamSynchronize(stream));
         g.nblock = total;
-        LK_TRY(cudaMalloc(&g.block_info, ncells * sizeof(int2)));
-        LK_TRY(cudaMalloc(&g.block_pts, (total > 0 ? total : 1) * sizeof(double4)));
-        LK_TRY(cudaMalloc(&g.block_f32, (total > 0 ? total : 1) * sizeof(float4)));
-        LK_TRY(cudaMalloc(&g.pos_orig, 3 * n * sizeof(double)));
+        LK_TRY(pool_alloc(&g.block_info, ncells * sizeof(int2), stream));
+        LK_TRY(pool_alloc(&g.block_pts, (total > 0 ? total : 1) * sizeof(double4), stream));
+        LK_TRY(pool_alloc(&g.block_f32, (total > 0 ? total : 1) * sizeof(float4), stream));
+        LK_TRY(pool_alloc(&g.pos_orig, 3 * n * sizeof(double), stream));
         LK_TRY(cudaMemcpyAsync(g.pos_orig, d_pos, 3 * n * sizeof(double), cudaMemcpyDeviceToDevice, stream));
         k_block_fill<<<blocks_for(ncells, 256), 256, 0, stream>>>(g.start, g.index, g.slot_pos, d_off, ncells, v,
                                                                   g.block_info, g.block_pts, g.block_f32);

@@ -691,17 +691,17 @@ int split_blocks_per_sm() {
 }  // namespace
 
 void RunBuffers::release() {
-    cudaFree(surv_index);
-    cudaFree(surv_ids);
-    cudaFree(cand_index);
-    cudaFree(cand_rt);
-    cudaFree(counters);
-    cudaFree(block_best);
-    cudaFree(inl_masks);
-    cudaFree(miss_masks);
-    cudaFree(addends);
-    cudaFree(full_list);
-    cudaFree(cand_fast);
+    pool_free(surv_index, stream);
+    pool_free(surv_ids, stream);
+    pool_free(cand_index, stream);
+    pool_free(cand_rt, stream);
+    pool_free(counters, stream);
+    pool_free(block_best, stream);
+    pool_free(inl_masks, stream);
+    pool_free(miss_masks, stream);
+    pool_free(addends, stream);
+    pool_free(full_list, stream);
+    pool_free(cand_fast, stream);
     full_list = nullptr;
     cand_fast = nullptr;
     fast_capacity = 0;
@@ -721,26 +721,26 @@ void RunBuffers::release() {
 
 cudaError_t RunBuffers::ensure(int64_t cap, int32_t score_blocks) {
     cudaError_t e = cudaSuccess;
-    if (!counters && (e = cudaMalloc(&counters, sizeof(Counters))) != cudaSuccess) return e;
+    if (!counters && (e = pool_alloc(&counters, sizeof(Counters), stream)) != cudaSuccess) return e;
     if (score_blocks > n_blocks) {
-        cudaFree(block_best);
-        if ((e = cudaMalloc(&block_best, score_blocks * sizeof(BestRec))) != cudaSuccess) return e;
+        pool_free(block_best, stream);
+        if ((e = pool_alloc(&block_best, score_blocks * sizeof(BestRec), stream)) != cudaSuccess) return e;
         n_blocks = score_blocks;
     }
     if (cap > capacity) {
-        cudaFree(surv_index);
-        cudaFree(surv_ids);
-        cudaFree(cand_index);
-        cudaFree(cand_rt);
+        pool_free(surv_index, stream);
+        pool_free(surv_ids, stream);
+        pool_free(cand_index, stream);
+        pool_free(cand_rt, stream);
         surv_index = nullptr;
         surv_ids = nullptr;
         cand_index = nullptr;
         cand_rt = nullptr;
         capacity = 0;
-        if ((e = cudaMalloc(&surv_index, cap * sizeof(int64_t))) != cudaSuccess) return e;
-        if ((e = cudaMalloc(&surv_ids, cap * 8 * sizeof(int32_t))) != cudaSuccess) return e;
-        if ((e = cudaMalloc(&cand_index, cap * sizeof(int64_t))) != cudaSuccess) return e;
-        if ((e = cudaMalloc(&cand_rt, cap * 12 * sizeof(double))) != cudaSuccess) return e;
+        if ((e = pool_alloc(&surv_index, cap * sizeof(int64_t), stream)) != cudaSuccess) return e;
+        if ((e = pool_alloc(&surv_ids, cap * 8 * sizeof(int32_t), stream)) != cudaSuccess) return e;
+        if ((e = pool_alloc(&cand_index, cap * sizeof(int64_t), stream)) != cudaSuccess) return e;
+        if ((e = pool_alloc(&cand_rt, cap * 12 * sizeof(double), stream)) != cudaSuccess) return e;
         capacity = cap;
     }
     return cudaSuccess;
@@ -748,10 +748,10 @@ cudaError_t RunBuffers::ensure(int64_t cap, int32_t score_blocks) {
 
 cudaError_t RunBuffers::ensure_fast(int64_t n) {
     if (n <= fast_capacity) return cudaSuccess;
-    cudaFree(cand_fast);
+    pool_free(cand_fast, stream);
     cand_fast = nullptr;
     fast_capacity = 0;
-    cudaError_t e = cudaMalloc(&cand_fast, n * sizeof(FastRT));
+    cudaError_t e = pool_alloc(&cand_fast, n * sizeof(FastRT), stream);
     if (e == cudaSuccess) fast_capacity = n;
     return e;
 }
@@ -764,19 +764,19 @@ cudaError_t RunBuffers::ensure_split(int64_t ns, int64_t max_candidates) {
     if (cap > max_candidates) cap = max_candidates;
     if (cap < 1) cap = 1;
     if (cap <= split_cap && ns_pad == split_ns_pad) return cudaSuccess;
-    cudaFree(inl_masks);
-    cudaFree(miss_masks);
-    cudaFree(addends);
-    cudaFree(full_list);
+    pool_free(inl_masks, stream);
+    pool_free(miss_masks, stream);
+    pool_free(addends, stream);
+    pool_free(full_list, stream);
     inl_masks = miss_masks = nullptr;
     addends = nullptr;
     full_list = nullptr;
     split_cap = 0;
     cudaError_t e;
-    if ((e = cudaMalloc(&full_list, cap * sizeof(int64_t))) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&inl_masks, cap * n_chunks * sizeof(uint32_t))) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&miss_masks, cap * n_chunks * sizeof(uint32_t))) != cudaSuccess) return e;
-    if ((e = cudaMalloc(&addends, cap * ns_pad * sizeof(double))) != cudaSuccess) return e;
+    if ((e = pool_alloc(&full_list, cap * sizeof(int64_t), stream)) != cudaSuccess) return e;
+    if ((e = pool_alloc(&inl_masks, cap * n_chunks * sizeof(uint32_t), stream)) != cudaSuccess) return e;
+    if ((e = pool_alloc(&miss_masks, cap * n_chunks * sizeof(uint32_t), stream)) != cudaSuccess) return e;
+    if ((e = pool_alloc(&addends, cap * ns_pad * sizeof(double), stream)) != cudaSuccess) return e;
     split_cap = cap;
     split_ns_pad = ns_pad;
     return cudaSuccess;
@@ -793,7 +793,11 @@ cudaError_t run_hypotheses_range(const SourceView& src, const double* d_tgt_pos,
     const int over_blocks = sm_count;
     cudaError_t e = rb.ensure(count > 0 ? count : 1, sums_blocks + exit_blocks + over_blocks);
     if (e != cudaSuccess) return e;
-    if ((e = rb.ensure_split(src.n, count > 0 ? count : 1)) != cudaSuccess) return e;
+    // split capacity: a few percent of the hypotheses survive pre-rejection in
+    // practice; any excess is scored by the streaming k_score (exact too)
+    const int64_t want_split = count / 64 > 4096 ? count / 64 : 4096;
+    if ((e = rb.ensure_split(src.n, want_split < count ? want_split : (count > 0 ? count : 1))) != cudaSuccess)
+        return e;
     if ((e = rb.ensure_fast(count > 0 ? count : 1)) != cudaSuccess) return e;
     FastRT* cand_fast = static_cast<FastRT*>(rb.cand_fast);
     if ((e = cudaMemsetAsync(rb.counters, 0, sizeof(Counters), stream)) != cudaSuccess) return e;

@@ -7,6 +7,17 @@
 
 namespace lkk {
 
+// Stream-ordered allocations from the device's default memory pool (its
+// release threshold is raised when a device is selected), so building and
+// dropping contexts per registration does not pay cudaMalloc / cudaFree.
+template <class T>
+inline cudaError_t pool_alloc(T** p, size_t bytes, cudaStream_t s) {
+    return cudaMallocAsync(reinterpret_cast<void**>(p), bytes, s);
+}
+inline void pool_free(void* p, cudaStream_t s) {
+    if (p) cudaFreeAsync(p, s);
+}
+
 // Dense CSR cell grid over a target cloud.
 //  kind 0 = EvalGrid   (proj/src/registration.cpp:80-148): origin = bbox_lo - cell,
 //           cell = d_max, block radius 1, local cell = floor((y - origin) / cell).
@@ -53,13 +64,15 @@ struct GridStorage {
     double* nrm_orig = nullptr;
     float4* block_f32 = nullptr;
     double* pos_orig = nullptr;
+    cudaStream_t stream = nullptr;  // allocation stream
     void release();
 };
 
 // Builds a grid of the given kind from device arrays pos/nrm (nrm may be null).
 // Returns cudaSuccess or the first CUDA error; throws nothing.
+// with_blocks = false skips the 3x3x3 block lists (neighbour grids of FPFH).
 cudaError_t build_grid(GridStorage& g, int kind, const double* d_pos, const double* d_nrm, int64_t n, double cell,
-                       double d_max, cudaStream_t stream);
+                       double d_max, cudaStream_t stream, bool with_blocks = true);
 
 // ---- hypothesis pipeline --------------------------------------------------
 struct Counters {  // device-side, zeroed per run
@@ -104,6 +117,7 @@ struct RunBuffers {
     int64_t fast_capacity = 0;
     int64_t split_cap = 0;
     int64_t split_ns_pad = 0;
+    cudaStream_t stream = nullptr;  // allocation stream (set by the owner)
     void release();
     cudaError_t ensure(int64_t cap, int32_t score_blocks);
     cudaError_t ensure_split(int64_t ns, int64_t max_candidates);
@@ -152,6 +166,20 @@ cudaError_t run_hypotheses_range(const SourceView& src, const double* d_tgt_pos,
 cudaError_t score_candidates(const SourceView& src, const GridView& grid, const ScoreParams& sp, const double* d_rt,
                              int64_t C, RunBuffers& rb, int64_t* d_out_inliers, double* d_out_sum,
                              void* d_record, cudaStream_t stream, int sm_count);
+
+// exclusive scan of n int32 into out[0..n] (out[n] = total), stream-ordered
+cudaError_t exclusive_scan(const int32_t* d_in, int64_t n, int32_t* d_out, cudaStream_t stream);
+
+// ---- device prepare_registration ---------------------
+// voxel_downsample (proj/src/preprocess.cpp:14-59) on the device: returns the
+// downsampled count; out_pos / out_nrm (capacity n) in first-index order.
+// Status: 0 ok, 5 invalid normals (MissingNormals), 2 empty, or a CUDA error
+// reported through cudaError_t.
+cudaError_t voxel_downsample(const double* d_pos, const double* d_nrm, int64_t n, double leaf, double* d_out_pos,
+                             double* d_out_nrm, int64_t* out_count, int* status, cudaStream_t stream);
+// compute_fpfh (proj/src/fpfh.cpp:57-141) on the device: 33 floats per point.
+cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, double radius, float* d_out,
+                         cudaStream_t stream);
 
 // FP64 exhaustive feature NN, ties -> lowest index (reference.hpp:56-76).
 cudaError_t feature_nn(const float* d_sf, int64_t ns, const float* d_tf, int64_t nt, int32_t* d_out,

@@ -1,0 +1,582 @@
+// lk_prepare.cu -- prepare_registration on the device.
+//
+// voxel_downsample (proj/src/preprocess.cpp:14-59):
+//   k_vox_insert   voxel key floor(p / leaf) per point into an open-addressing
+//                  hash table; per voxel: first input index (atomicMin), count
+//   k_vox_mark     flag the first index of every voxel; an exclusive scan of
+//                  the flags gives each voxel its output position, which is the
+//                  reference's order (voxels sorted by first input index)
+//   k_vox_scatter  member lists per output voxel (unordered)
+//   k_vox_reduce   thread per voxel: members sorted by input index, then the
+//                  reference's sequential FP64 sums and the normalised normal
+// compute_fpfh (proj/src/fpfh.cpp:57-141):
+//   neighbour lists within r (SearchGrid cell = r, ascending, self excluded),
+//   k_spfh    warp per point: pair-angle votes as integer counts; pairs whose
+//             frame-source test (std::acos comparison) the device cannot
+//             decide are deferred to the host's libm (k_spfh_resolve), then
+//             k_spfh_scale applies fl(100 / votes) like `v *= 100.0 / votes`
+//   k_fpfh    warp per point, lane per bin: acc_b += spfh_j[b] / w_j over the
+//             neighbours in ascending order (the reference's summation order)
+#include <cmath>
+#include <cstdint>
+#include <vector>
+
+#include "lk_device_math.cuh"
+#include "lk_kernels.cuh"
+
+namespace lkk {
+
+using namespace lkd;
+
+namespace {
+
+constexpr unsigned long long kEmpty = ~0ull;
+constexpr unsigned kFull = 0xffffffffu;
+
+inline unsigned nblocks(int64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
+
+__device__ __forceinline__ int floor_cell(double q) {
+    double f = floor(q);
+    if (!(f >= -2147483648.0 && f < 2147483648.0)) return INT32_MIN;
+    return static_cast<int>(f);
+}
+
+// proj/src/preprocess.cpp:25-29 (pack of grid_index(p, 0, leaf))
+__device__ __forceinline__ unsigned long long voxel_key(const double* p, double leaf) {
+    const long long off = 1 << 20;
+    unsigned long long x = static_cast<unsigned long long>(floor_cell((p[0] - 0.0) / leaf) + off);
+    unsigned long long y = static_cast<unsigned long long>(floor_cell((p[1] - 0.0) / leaf) + off);
+    unsigned long long z = static_cast<unsigned long long>(floor_cell((p[2] - 0.0) / leaf) + off);
+    return (x << 42) | (y << 21) | z;
+}
+
+__device__ __forceinline__ unsigned long long mix64(unsigned long long k) {
+    k ^= k >> 33;
+    k *= 0xff51afd7ed558ccdull;
+    k ^= k >> 33;
+    k *= 0xc4ceb9fe1a85ec53ull;
+    k ^= k >> 33;
+    return k;
+}
+
+// validate_cloud (proj/src/geometry.cpp:93-103): unit within 1e-6 or exactly zero
+__global__ void k_validate_normals(const double* __restrict__ nrm, int64_t n, int* __restrict__ bad) {
+    int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    V3 v = ld3(nrm, i);
+    double len = sqrt(sqnorm(v));
+    if (len != 0.0 && fabs(len - 1.0) > 1e-6) atomicOr(bad, 1);
+}
+
+__global__ void k_vox_insert(const double* __restrict__ pos, int64_t n, double leaf, unsigned long long* keys,
+                             uint32_t mask, int32_t* __restrict__ point_slot, int32_t* first, int32_t* count) {
+    int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const unsigned long long key = voxel_key(pos + 3 * i, leaf);
+    uint32_t h = static_cast<uint32_t>(mix64(key)) & mask;
+    while (true) {
+        unsigned long long prev = atomicCAS(&keys[h], kEmpty, key);
+        if (prev == kEmpty || prev == key) break;
+        h = (h + 1) & mask;
+    }
+    point_slot[i] = static_cast<int32_t>(h);
+    atomicMin(&first[h], static_cast<int32_t>(i));
+    atomicAdd(&count[h], 1);
+}
+
+__global__ void k_vox_mark(const unsigned long long* __restrict__ keys, const int32_t* __restrict__ first,
+                           uint32_t table, int32_t* __restrict__ flags) {
+    uint32_t h = blockIdx.x * blockDim.x + threadIdx.x;
+    if (h < table && keys[h] != kEmpty) flags[first[h]] = 1;
+}
+
+__global__ void k_vox_out(const unsigned long long* __restrict__ keys, const int32_t* __restrict__ first,
+                          const int32_t* __restrict__ count, uint32_t table, const int32_t* __restrict__ flag_scan,
+                          int32_t* __restrict__ slot_out, int32_t* __restrict__ cnt_out) {
+    uint32_t h = blockIdx.x * blockDim.x + threadIdx.x;
+    if (h >= table || keys[h] == kEmpty) return;
+    const int32_t o = flag_scan[first[h]];
+    slot_out[h] = o;
+    cnt_out[o] = count[h];
+}
+
+__global__ void k_vox_scatter(const int32_t* __restrict__ point_slot, int64_t n, const int32_t* __restrict__ slot_out,
+                              const int32_t* __restrict__ member_start, int32_t* __restrict__ cursor,
+                              int32_t* __restrict__ members) {
+    int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const int32_t o = slot_out[point_slot[i]];
+    members[member_start[o] + atomicAdd(&cursor[o], 1)] = static_cast<int32_t>(i);
+}
+
+// Sorts seg[0..k) ascending with the 32 lanes of a warp: in shared memory
+// (bitonic network) when k <= cap, else in place by lane 0 (rare, slow, exact).
+// Returns the sorted array to read (shared buffer or seg itself).
+__device__ int32_t* warp_sort_segment(int32_t* seg, int k, int32_t* sbuf, int cap) {
+    const int lane = threadIdx.x & 31;
+    if (k <= cap) {
+        int P = 1;
+        while (P < k) P <<= 1;
+        for (int a = lane; a < P; a += 32) sbuf[a] = a < k ? seg[a] : INT32_MAX;
+        __syncwarp();
+        for (int size = 2; size <= P; size <<= 1) {
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                for (int t = lane; t < (P >> 1); t += 32) {
+                    const int i = 2 * stride * (t / stride) + (t % stride);
+                    const int j = i + stride;
+                    const bool up = (i & size) == 0;
+                    const int32_t a = sbuf[i], b = sbuf[j];
+                    if ((a > b) == up) {
+                        sbuf[i] = b;
+                        sbuf[j] = a;
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        return sbuf;
+    }
+    if (lane == 0) {
+        for (int a = 1; a < k; ++a) {
+            int32_t v = seg[a];
+            int b = a - 1;
+            while (b >= 0 && seg[b] > v) {
+                seg[b + 1] = seg[b];
+                --b;
+            }
+            seg[b + 1] = v;
+        }
+    }
+    __syncwarp();
+    return seg;
+}
+
+constexpr int kSortWarps = 4;
+constexpr int kSortCap = 2048;
+
+// proj/src/preprocess.cpp:30-58, warp per voxel: members sorted by input
+// index, then the sums in that order (lane order within 32-member chunks).
+// A skipped (zero) normal contributes +0.0, which leaves the sum unchanged.
+__global__ void __launch_bounds__(32 * kSortWarps) k_vox_reduce(int32_t* __restrict__ members,
+                                                                const int32_t* __restrict__ member_start, int64_t n_out,
+                                                                const double* __restrict__ pos,
+                                                                const double* __restrict__ nrm,
+                                                                double* __restrict__ out_pos,
+                                                                double* __restrict__ out_nrm) {
+    __shared__ int32_t s_buf[kSortWarps][kSortCap];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t o = blockIdx.x * static_cast<int64_t>(kSortWarps) + warp;
+    if (o >= n_out) return;
+    const int32_t s0 = member_start[o], s1 = member_start[o + 1];
+    const int k = s1 - s0;
+    const int32_t* sorted = warp_sort_segment(members + s0, k, s_buf[warp], kSortCap);
+    V3 ps = mk(0.0, 0.0, 0.0), nsum = mk(0.0, 0.0, 0.0);
+    for (int c0 = 0; c0 < k; c0 += 32) {
+        V3 p = mk(0.0, 0.0, 0.0), nv = mk(0.0, 0.0, 0.0);
+        if (c0 + lane < k) {
+            const int64_t i = sorted[c0 + lane];
+            p = ld3(pos, i);
+            if (nrm) {
+                nv = ld3(nrm, i);
+                if (is_zero(nv)) nv = mk(0.0, 0.0, 0.0);
+            }
+        }
+        const int m = k - c0 < 32 ? k - c0 : 32;
+        for (int L = 0; L < m; ++L) {
+            ps.x += __shfl_sync(kFull, p.x, L);
+            ps.y += __shfl_sync(kFull, p.y, L);
+            ps.z += __shfl_sync(kFull, p.z, L);
+            nsum.x += __shfl_sync(kFull, nv.x, L);
+            nsum.y += __shfl_sync(kFull, nv.y, L);
+            nsum.z += __shfl_sync(kFull, nv.z, L);
+        }
+    }
+    if (lane != 0) return;
+    const double cnt = static_cast<double>(k);
+    out_pos[3 * o] = ps.x / cnt;
+    out_pos[3 * o + 1] = ps.y / cnt;
+    out_pos[3 * o + 2] = ps.z / cnt;
+    if (nrm) {
+        const double len = sqrt(sqnorm(nsum));
+        if (len > 1e-12) {
+            out_nrm[3 * o] = nsum.x / len;
+            out_nrm[3 * o + 1] = nsum.y / len;
+            out_nrm[3 * o + 2] = nsum.z / len;
+        } else {
+            out_nrm[3 * o] = out_nrm[3 * o + 1] = out_nrm[3 * o + 2] = 0.0;
+        }
+    }
+}
+
+// ---- FPFH --------------------------------------------------------------------
+
+__device__ __forceinline__ V3 cross(V3 a, V3 b) {
+    return mk(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x);
+}
+
+// The reference's frame-source test is acos(|a1|) > acos(|a2|) evaluated with
+// the host libm's acos, which is not correctly rounded. When |a1| and |a2|
+// are more than 1e-15 apart the rounded values are certainly ordered like the
+// arguments (acos is decreasing with |slope| >= 1, ulp(acos) <= 2.3e-16 on
+// [0, pi/2], libm error < 1 ulp); closer pairs -- common on noisy planar
+// faces, where normals agree to the last bits -- are decided on the host with
+// the same libm (compute_fpfh below). Returns 0 no swap, 1 swap, 2 undecided.
+__device__ __forceinline__ int swap_decision(double x1, double x2) {
+    if (!(x1 <= 1.0 && x2 <= 1.0)) return 0;  // acos of |a| > 1 is NaN: never greater
+    if (fabs(x1 - x2) > 1e-15) return x1 < x2 ? 1 : 0;
+    if (x1 == x2) return 0;
+    return 2;
+}
+
+// proj/src/fpfh.cpp:17-48. `decide` = 0/1 forces the swap test's outcome;
+// -1 evaluates it (returns false with *undecided set when the host must).
+__device__ __forceinline__ bool pair_angles(V3 p1, V3 n1, V3 p2, V3 n2, double& alpha, double& phi,
+                                            double& theta, int decide = -1, bool* undecided = nullptr,
+                                            double* x1_out = nullptr, double* x2_out = nullptr) {
+    V3 d = sub(p2, p1);
+    double dist = sqrt(sqnorm(d));
+    if (dist <= 0.0) return false;
+    double angle1 = dot(n1, d) / dist;
+    double angle2 = dot(n2, d) / dist;
+    V3 ns = n1, nt = n2, line = d;
+    double cos_line = angle1;
+    int swap = decide;
+    if (swap < 0) {
+        swap = swap_decision(fabs(angle1), fabs(angle2));
+        if (swap == 2) {
+            *undecided = true;
+            *x1_out = fabs(angle1);
+            *x2_out = fabs(angle2);
+            return false;
+        }
+    }
+    if (swap == 1) {
+        ns = n2;
+        nt = n1;
+        line = mk(-d.x, -d.y, -d.z);
+        cos_line = -angle2;
+    }
+    V3 u = ns;
+    V3 v = cross(line, u);
+    double v_len = sqrt(sqnorm(v));
+    if (v_len <= 1e-12 * dist) return false;
+    v = mk(v.x / v_len, v.y / v_len, v.z / v_len);
+    V3 w = cross(u, v);
+    alpha = dot(v, nt);
+    phi = cos_line;
+    theta = atan2(dot(w, nt), dot(u, nt));
+    return true;
+}
+
+// proj/src/fpfh.cpp:50-53
+__device__ __forceinline__ int bin_index(double value, double lo, double hi) {
+    int b = floor_cell(11 * (value - lo) / (hi - lo));
+    return b < 0 ? 0 : (b > 10 ? 10 : b);
+}
+
+// neighbours within r (inclusive), self excluded (proj/src/fpfh.cpp:66-74)
+__global__ void k_nbr_count(const double* __restrict__ pos, int64_t n, GridView g, double r2,
+                            int32_t* __restrict__ counts) {
+    int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const V3 p = ld3(pos, i);
+    const int kx = floor_cell((p.x - g.ox) / g.cell) - g.offx;
+    const int ky = floor_cell((p.y - g.oy) / g.cell) - g.offy;
+    const int kz = floor_cell((p.z - g.oz) / g.cell) - g.offz;
+    int32_t c = 0;
+    for (int x = max(kx - g.radius, 0); x <= min(kx + g.radius, g.nx - 1); ++x)
+        for (int y = max(ky - g.radius, 0); y <= min(ky + g.radius, g.ny - 1); ++y) {
+            const int64_t row = (static_cast<int64_t>(x) * g.ny + y) * g.nz;
+            const int32_t s0 = g.start[row + max(kz - g.radius, 0)];
+            const int32_t s1 = g.start[row + min(kz + g.radius, g.nz - 1) + 1];
+            for (int32_t s = s0; s < s1; ++s)
+                if (g.index[s] != i && sqnorm(sub(ld3(g.slot_pos, s), p)) <= r2) ++c;
+        }
+    counts[i] = c;
+}
+
+// warp per point: gather the neighbours (row by row, lanes over slots,
+// ballot-compacted), then sort ascending (radius_search sorts its output)
+__global__ void __launch_bounds__(32 * kSortWarps) k_nbr_fill(const double* __restrict__ pos, int64_t n, GridView g,
+                                                              double r2, const int32_t* __restrict__ off,
+                                                              int32_t* __restrict__ nbr) {
+    __shared__ int32_t s_buf[kSortWarps][kSortCap];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t i = blockIdx.x * static_cast<int64_t>(kSortWarps) + warp;
+    if (i >= n) return;
+    const V3 p = ld3(pos, i);
+    const int kx = floor_cell((p.x - g.ox) / g.cell) - g.offx;
+    const int ky = floor_cell((p.y - g.oy) / g.cell) - g.offy;
+    const int kz = floor_cell((p.z - g.oz) / g.cell) - g.offz;
+    const int32_t o0 = off[i];
+    int32_t o = o0;
+    for (int x = max(kx - g.radius, 0); x <= min(kx + g.radius, g.nx - 1); ++x)
+        for (int y = max(ky - g.radius, 0); y <= min(ky + g.radius, g.ny - 1); ++y) {
+            const int64_t row = (static_cast<int64_t>(x) * g.ny + y) * g.nz;
+            const int32_t s0 = g.start[row + max(kz - g.radius, 0)];
+            const int32_t s1 = g.start[row + min(kz + g.radius, g.nz - 1) + 1];
+            for (int32_t b = s0; b < s1; b += 32) {
+                const int32_t s = b + lane;
+                const bool hit = s < s1 && g.index[s] != i && sqnorm(sub(ld3(g.slot_pos, s), p)) <= r2;
+                const unsigned m = __ballot_sync(kFull, hit);
+                if (hit) nbr[o + __popc(m & ((1u << lane) - 1u))] = g.index[s];
+                o += __popc(m);
+            }
+        }
+    __syncwarp();
+    const int k = o - o0;
+    const int32_t* sorted = warp_sort_segment(nbr + o0, k, s_buf[warp], kSortCap);
+    if (sorted != nbr + o0)
+        for (int a = lane; a < k; a += 32) nbr[o0 + a] = sorted[a];
+}
+
+constexpr int kFpfhWarps = 4;
+
+// pass 1 (proj/src/fpfh.cpp:76-100): warp per point, integer vote counts in
+// counts[i][0..32], votes in counts[i][33]. Pairs whose frame-source test the
+// device cannot decide are appended to the deferred list (k_spfh_resolve).
+__global__ void __launch_bounds__(32 * kFpfhWarps) k_spfh(const double* __restrict__ pos,
+                                                          const double* __restrict__ nrm, int64_t n,
+                                                          const int32_t* __restrict__ off,
+                                                          const int32_t* __restrict__ nbr, int32_t* __restrict__ counts,
+                                                          int2* __restrict__ deferred, double2* __restrict__ deferred_x,
+                                                          int32_t* __restrict__ n_deferred) {
+    __shared__ int hist[kFpfhWarps][34];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t i = blockIdx.x * static_cast<int64_t>(kFpfhWarps) + warp;
+    if (i >= n) return;
+    for (int b = lane; b < 34; b += 32) hist[warp][b] = 0;
+    __syncwarp();
+    const V3 p = ld3(pos, i), np = ld3(nrm, i);
+    int votes = 0;
+    if (!is_zero(np)) {
+        for (int32_t k = off[i] + lane; k < off[i + 1]; k += 32) {
+            const int32_t j = nbr[k];
+            const V3 nq = ld3(nrm, j);
+            if (is_zero(nq)) continue;
+            double alpha, phi, theta, x1, x2;
+            bool undecided = false;
+            if (!pair_angles(p, np, ld3(pos, j), nq, alpha, phi, theta, -1, &undecided, &x1, &x2)) {
+                if (undecided) {
+                    const int32_t slot = atomicAdd(n_deferred, 1);
+                    deferred[slot] = make_int2(static_cast<int32_t>(i), j);
+                    deferred_x[slot] = make_double2(x1, x2);
+                }
+                continue;
+            }
+            atomicAdd(&hist[warp][bin_index(alpha, -1.0, 1.0)], 1);
+            atomicAdd(&hist[warp][11 + bin_index(phi, -1.0, 1.0)], 1);
+            atomicAdd(&hist[warp][22 + bin_index(theta, -M_PI, M_PI)], 1);
+            votes += 1;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) votes += __shfl_xor_sync(kFull, votes, o);
+    __syncwarp();
+    for (int b = lane; b < 33; b += 32) counts[34 * i + b] = hist[warp][b];
+    if (lane == 0) counts[34 * i + 33] = votes;
+}
+
+// deferred pairs with the host's decisions (0/1) of the frame-source test
+__global__ void k_spfh_resolve(const double* __restrict__ pos, const double* __restrict__ nrm,
+                               const int2* __restrict__ deferred, const uint8_t* __restrict__ decision, int32_t m,
+                               int32_t* __restrict__ counts) {
+    const int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= m) return;
+    const int2 ij = deferred[k];
+    double alpha, phi, theta;
+    if (!pair_angles(ld3(pos, ij.x), ld3(nrm, ij.x), ld3(pos, ij.y), ld3(nrm, ij.y), alpha, phi, theta,
+                     decision[k]))
+        return;
+    int32_t* c = counts + 34 * static_cast<int64_t>(ij.x);
+    atomicAdd(c + bin_index(alpha, -1.0, 1.0), 1);
+    atomicAdd(c + 11 + bin_index(phi, -1.0, 1.0), 1);
+    atomicAdd(c + 22 + bin_index(theta, -M_PI, M_PI), 1);
+    atomicAdd(c + 33, 1);
+}
+
+// h[b] accumulates 1.0 per vote exactly, then h[b] *= 100.0 / votes
+__global__ void k_spfh_scale(const int32_t* __restrict__ counts, int64_t n, double* __restrict__ spfh) {
+    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (t >= 33 * n) return;
+    const int64_t i = t / 33, b = t - 33 * i;
+    const int32_t votes = counts[34 * i + 33];
+    spfh[t] = votes > 0 ? static_cast<double>(counts[34 * i + b]) * (100.0 / static_cast<double>(votes)) : 0.0;
+}
+
+// pass 2 (proj/src/fpfh.cpp:102-139): warp per point, lane per bin
+__global__ void __launch_bounds__(32 * kFpfhWarps) k_fpfh(const double* __restrict__ pos,
+                                                          const double* __restrict__ nrm, int64_t n,
+                                                          const int32_t* __restrict__ off,
+                                                          const int32_t* __restrict__ nbr,
+                                                          const double* __restrict__ spfh, float* __restrict__ out) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t i = blockIdx.x * static_cast<int64_t>(kFpfhWarps) + warp;
+    if (i >= n) return;
+    if (is_zero(ld3(nrm, i))) {
+        for (int b = lane; b < 33; b += 32) out[33 * i + b] = 0.0f;
+        return;
+    }
+    const V3 p = ld3(pos, i);
+    double acc0 = 0.0, acc1 = 0.0;  // bin lane, and bin 32 on lane 0
+    int k_count = 0;
+    for (int32_t k = off[i]; k < off[i + 1]; ++k) {
+        const int32_t j = nbr[k];
+        if (is_zero(ld3(nrm, j))) continue;
+        const double w = sqrt(sqnorm(sub(ld3(pos, j), p)));
+        if (w <= 0.0) continue;
+        acc0 += spfh[33 * static_cast<int64_t>(j) + lane] / w;
+        if (lane == 0) acc1 += spfh[33 * static_cast<int64_t>(j) + 32] / w;
+        k_count += 1;
+    }
+    {
+        double blended = spfh[33 * i + lane];
+        if (k_count > 0) blended += acc0 / static_cast<double>(k_count);
+        out[33 * i + lane] = static_cast<float>(blended);
+    }
+    if (lane == 0) {
+        double blended = spfh[33 * i + 32];
+        if (k_count > 0) blended += acc1 / static_cast<double>(k_count);
+        out[33 * i + 32] = static_cast<float>(blended);
+    }
+}
+
+#define LK_TRY(x)                         \
+    do {                                  \
+        cudaError_t e_ = (x);             \
+        if (e_ != cudaSuccess) return e_; \
+    } while (0)
+
+}  // namespace
+
+cudaError_t voxel_downsample(const double* d_pos, const double* d_nrm, int64_t n, double leaf, double* d_out_pos,
+                             double* d_out_nrm, int64_t* out_count, int* status, cudaStream_t stream) {
+    *status = 0;
+    *out_count = 0;
+    if (n <= 0) {
+        *status = 2;
+        return cudaSuccess;
+    }
+    if (n > INT32_MAX / 2) return cudaErrorInvalidValue;
+    uint32_t table = 1024;
+    while (table < 2 * n) table <<= 1;
+    unsigned long long* keys = nullptr;
+    int32_t *point_slot = nullptr, *first = nullptr, *count = nullptr, *flags = nullptr, *flag_scan = nullptr;
+    int32_t *slot_out = nullptr, *cnt_out = nullptr, *member_start = nullptr, *members = nullptr, *bad = nullptr;
+    LK_TRY(cudaMallocAsync(&keys, table * sizeof(unsigned long long), stream));
+    LK_TRY(cudaMallocAsync(&point_slot, n * sizeof(int32_t), stream));
+    LK_TRY(cudaMallocAsync(&first, table * sizeof(int32_t), stream));
+    LK_TRY(cudaMallocAsync(&count, table * sizeof(int32_t), stream));
+    LK_TRY(cudaMallocAsync(&flags, n * sizeof(int32_t), stream));
+    LK_TRY(cudaMallocAsync(&flag_scan, (n + 1) * sizeof(int32_t), stream));
+    LK_TRY(cudaMallocAsync(&slot_out, table * sizeof(int32_t), stream));
+    LK_TRY(cudaMallocAsync(&bad, sizeof(int32_t), stream));
+    LK_TRY(cudaMemsetAsync(keys, 0xff, table * sizeof(unsigned long long), stream));
+    LK_TRY(cudaMemsetAsync(first, 0x7f, table * sizeof(int32_t), stream));
+    LK_TRY(cudaMemsetAsync(count, 0, table * sizeof(int32_t), stream));
+    LK_TRY(cudaMemsetAsync(flags, 0, n * sizeof(int32_t), stream));
+    LK_TRY(cudaMemsetAsync(bad, 0, sizeof(int32_t), stream));
+    if (d_nrm) k_validate_normals<<<nblocks(n, 256), 256, 0, stream>>>(d_nrm, n, bad);
+    k_vox_insert<<<nblocks(n, 256), 256, 0, stream>>>(d_pos, n, leaf, keys, table - 1, point_slot, first, count);
+    k_vox_mark<<<nblocks(table, 256), 256, 0, stream>>>(keys, first, table, flags);
+    LK_TRY(exclusive_scan(flags, n, flag_scan, stream));
+    int32_t host[2] = {0, 0};
+    LK_TRY(cudaMemcpyAsync(&host[0], flag_scan + n, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
+    LK_TRY(cudaMemcpyAsync(&host[1], bad, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
+    LK_TRY(cudaStreamSynchronize(stream));
+    if (host[1]) {
+        *status = 5;
+    } else {
+        const int64_t n_out = host[0];
+        LK_TRY(cudaMallocAsync(&cnt_out, (n_out + 1) * sizeof(int32_t), stream));
+        LK_TRY(cudaMallocAsync(&member_start, (n_out + 1) * sizeof(int32_t), stream));
+        LK_TRY(cudaMallocAsync(&members, n * sizeof(int32_t), stream));
+        k_vox_out<<<nblocks(table, 256), 256, 0, stream>>>(keys, first, count, table, flag_scan, slot_out, cnt_out);
+        LK_TRY(exclusive_scan(cnt_out, n_out, member_start, stream));
+        LK_TRY(cudaMemsetAsync(cnt_out, 0, n_out * sizeof(int32_t), stream));
+        k_vox_scatter<<<nblocks(n, 256), 256, 0, stream>>>(point_slot, n, slot_out, member_start, cnt_out, members);
+        k_vox_reduce<<<nblocks(n_out, kSortWarps), 32 * kSortWarps, 0, stream>>>(members, member_start, n_out, d_pos,
+                                                                                  d_nrm, d_out_pos,
+                                                             d_out_nrm);
+        *out_count = n_out;
+    }
+    LK_TRY(cudaGetLastError());
+    cudaFreeAsync(keys, stream);
+    cudaFreeAsync(point_slot, stream);
+    cudaFreeAsync(first, stream);
+    cudaFreeAsync(count, stream);
+    cudaFreeAsync(flags, stream);
+    cudaFreeAsync(flag_scan, stream);
+    cudaFreeAsync(slot_out, stream);
+    cudaFreeAsync(bad, stream);
+    if (cnt_out) cudaFreeAsync(cnt_out, stream);
+    if (member_start) cudaFreeAsync(member_start, stream);
+    if (members) cudaFreeAsync(members, stream);
+    return cudaGetLastError();
+}
+
+cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, double radius, float* d_out,
+                         cudaStream_t stream) {
+    if (n <= 0) return cudaErrorInvalidValue;
+    GridStorage g;
+    LK_TRY(build_grid(g, 1, d_pos, nullptr, n, radius, radius, stream, false));
+    int32_t *counts = nullptr, *off = nullptr, *nbr = nullptr;
+    double* spfh = nullptr;
+    LK_TRY(cudaMallocAsync(&counts, n * sizeof(int32_t), stream));
+    LK_TRY(cudaMallocAsync(&off, (n + 1) * sizeof(int32_t), stream));
+    const double r2 = radius * radius;
+    k_nbr_count<<<nblocks(n, 128), 128, 0, stream>>>(d_pos, n, g.view, r2, counts);
+    LK_TRY(exclusive_scan(counts, n, off, stream));
+    int32_t total = 0;
+    LK_TRY(cudaMemcpyAsync(&total, off + n, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
+    LK_TRY(cudaStreamSynchronize(stream));
+    const int64_t cap = total > 0 ? total : 1;
+    int32_t *votes = nullptr, *n_def = nullptr;
+    int2* deferred = nullptr;
+    double2* deferred_x = nullptr;
+    uint8_t* d_decision = nullptr;
+    LK_TRY(cudaMallocAsync(&nbr, cap * sizeof(int32_t), stream));
+    LK_TRY(cudaMallocAsync(&spfh, 33 * n * sizeof(double), stream));
+    LK_TRY(cudaMallocAsync(&votes, 34 * n * sizeof(int32_t), stream));
+    LK_TRY(cudaMallocAsync(&deferred, cap * sizeof(int2), stream));
+    LK_TRY(cudaMallocAsync(&deferred_x, cap * sizeof(double2), stream));
+    LK_TRY(cudaMallocAsync(&n_def, sizeof(int32_t), stream));
+    LK_TRY(cudaMemsetAsync(n_def, 0, sizeof(int32_t), stream));
+    k_nbr_fill<<<nblocks(n, kSortWarps), 32 * kSortWarps, 0, stream>>>(d_pos, n, g.view, r2, off, nbr);
+    k_spfh<<<nblocks(n, kFpfhWarps), 32 * kFpfhWarps, 0, stream>>>(d_pos, d_nrm, n, off, nbr, votes, deferred,
+                                                                   deferred_x, n_def);
+    // frame-source tests the device cannot decide: the host's libm decides
+    // them exactly as the reference's std::acos comparison (fpfh.cpp:28)
+    int32_t m = 0;
+    LK_TRY(cudaMemcpyAsync(&m, n_def, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
+    LK_TRY(cudaStreamSynchronize(stream));
+    if (m > 0) {
+        std::vector<double2> xs(m);
+        std::vector<uint8_t> dec(m);
+        LK_TRY(cudaMemcpyAsync(xs.data(), deferred_x, m * sizeof(double2), cudaMemcpyDeviceToHost, stream));
+        LK_TRY(cudaStreamSynchronize(stream));
+#pragma omp parallel for schedule(static) if (m > 4096)
+        for (int32_t k = 0; k < m; ++k) dec[k] = std::acos(xs[k].x) > std::acos(xs[k].y) ? 1 : 0;
+        LK_TRY(cudaMallocAsync(&d_decision, m, stream));
+        LK_TRY(cudaMemcpyAsync(d_decision, dec.data(), m, cudaMemcpyHostToDevice, stream));
+        k_spfh_resolve<<<nblocks(m, 256), 256, 0, stream>>>(d_pos, d_nrm, deferred, d_decision, m, votes);
+        // the host vectors must outlive the async copy
+        LK_TRY(cudaStreamSynchronize(stream));
+    }
+    k_spfh_scale<<<nblocks(33 * n, 256), 256, 0, stream>>>(votes, n, spfh);
+    k_fpfh<<<nblocks(n, kFpfhWarps), 32 * kFpfhWarps, 0, stream>>>(d_pos, d_nrm, n, off, nbr, spfh, d_out);
+    LK_TRY(cudaGetLastError());
+    cudaFreeAsync(counts, stream);
+    cudaFreeAsync(off, stream);
+    cudaFreeAsync(nbr, stream);
+    cudaFreeAsync(spfh, stream);
+    cudaFreeAsync(votes, stream);
+    cudaFreeAsync(deferred, stream);
+    cudaFreeAsync(deferred_x, stream);
+    cudaFreeAsync(n_def, stream);
+    if (d_decision) cudaFreeAsync(d_decision, stream);
+    cudaError_t e = cudaStreamSynchronize(stream);
+    g.release();
+    return e;
+}
+
+}  // namespace lkk

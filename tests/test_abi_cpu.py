@@ -94,17 +94,17 @@ def test_no_cpu_fallback_without_gpu(has_gpu):
         lk.feature_nn_cache(np.zeros((4, 33), np.float32), np.zeros((4, 33), np.float32))
 
 
-def test_host_prepare_helpers_match_oracle(oracle):
-    # the host half of prepare (this tier) equals the oracle restatement bitwise
+def test_device_prepare_helpers_need_gpu(has_gpu):
+    if has_gpu:
+        pytest.skip("GPU present: covered by the -m gpu parity tests")
     from paper_1801_01572_b200 import synth
     pair = synth.synth_registration_pair(4)
-    for cloud in (pair.source, pair.target):
-        d = lk.voxel_downsample(cloud, 0.05)
-        ox, on = oracle.voxel_downsample(cloud.positions, cloud.normals, 0.05)
-        assert np.array_equal(d.positions, ox) and np.array_equal(d.normals, on)
-        f = lk.compute_fpfh(d, 0.25)
-        fo = oracle.compute_fpfh(ox, on, 0.25)
-        assert np.array_equal(f, fo)
+    with pytest.raises(errors.CudaError):
+        lk.voxel_downsample(pair.source, 0.05)
+    with pytest.raises(errors.CudaError):
+        lk.compute_fpfh(pair.source, 0.25)
+    with pytest.raises(errors.CudaError):
+        lk.register_global(pair.source, pair.target, lk.RegistrationParams(hypothesis_count=10))
 
 
 def test_status_mapping():

@@ -108,6 +108,35 @@ def test_prepare_and_register_global_match_oracle(pair1, oracle):
     assert st.prerejected + st.degenerate + st.evaluated == st.sampled == 100_000
 
 
+def test_device_prepare_helpers_match_oracle(oracle):
+    # device voxel_downsample (preprocess.cpp:14-59) and FPFH (fpfh.cpp:57-141), bitwise
+    pair = synth.synth_registration_pair(4)
+    for cloud in (pair.source, pair.target):
+        d = lk.voxel_downsample(cloud, 0.05)
+        ox, on = oracle.voxel_downsample(cloud.positions, cloud.normals, 0.05)
+        assert np.array_equal(d.positions, ox) and np.array_equal(d.normals, on)
+        f = lk.compute_fpfh(d, 0.25)
+        fo = oracle.compute_fpfh(ox, on, 0.25)
+        assert np.array_equal(f, fo)
+
+
+def test_device_downsample_full_frame_matches_oracle(oracle):
+    # 307k-point depth frame: dense voxels (hundreds of points each), zero normals mixed in
+    pair = synth.depth_frame_pair()
+    src = pair.source
+    nrm = src.normals.copy()
+    nrm[::97] = 0.0
+    cloud = lk.PointCloud(src.positions, nrm)
+    for leaf in (0.05, 0.02):
+        d = lk.voxel_downsample(cloud, leaf)
+        ox, on = oracle.voxel_downsample(cloud.positions, cloud.normals, leaf)
+        assert np.array_equal(d.positions, ox) and np.array_equal(d.normals, on)
+    bad = src.normals.copy()
+    bad[5] *= 1.1
+    with pytest.raises(lk.MissingNormals):
+        lk.voxel_downsample(lk.PointCloud(src.positions, bad), 0.05)
+
+
 def test_negative_pair_returns_none(oracle):
     # test_registration.cpp:181-188
     pair = synth.synth_negative_pair(1)
