@@ -1,5 +1,6 @@
 // lk_misc.cu -- feature pre-match (K1), edge_info (K8), point transforms.
 #include <cstdint>
+#include <cstdlib>
 
 #include "lk_device_math.cuh"
 #include "lk_kernels.cuh"
@@ -48,6 +49,125 @@ __global__ void __launch_bounds__(kFeatThreads) k_feature_nn(const float* __rest
         }
     }
     if (i < ns) out[i] = best;
+}
+
+// ---- FP32 pre-match with exact FP64 resolution of near-ties ---------------
+// d2f = sum_b fl(s_b - t_b)^2 via fmaf is within (2 + 33 + 1) * 2^-24 < 2.2e-6
+// relative of the exact d2 (all terms are non-negative). Every (source,
+// target-chunk) keeps its FP32 best (value, lowest index) and runner-up;
+// chunks merge in ascending order. A source whose runner-up lies within
+// kTieRel of the best is resolved exactly in FP64 over all targets within
+// that band (ties -> lowest index, as reference.hpp:56-76). d2f == 0 implies
+// identical features, hence an exact zero: no resolution needed.
+constexpr int kFnnThreads = 128;
+constexpr int kFnnTile = 64;
+constexpr int kFnnPad = 36;  // 33 bins padded to 9 float4
+constexpr float kTieRel = 1e-5f;
+
+struct Best3 {
+    float f1;
+    int32_t j1;
+    float f2;
+};
+
+__device__ __forceinline__ float feat_d2f(const float4* a, const float4* b) {
+    float acc = 0.0f;
+#pragma unroll
+    for (int q = 0; q < kFnnPad / 4; ++q) {
+        const float4 x = a[q], y = b[q];
+        float d;
+        d = x.x - y.x; acc = fmaf(d, d, acc);
+        d = x.y - y.y; acc = fmaf(d, d, acc);
+        d = x.z - y.z; acc = fmaf(d, d, acc);
+        d = x.w - y.w; acc = fmaf(d, d, acc);
+    }
+    return acc;
+}
+
+__global__ void k_pad_features(const float* __restrict__ f, int64_t n, float4* __restrict__ out) {
+    const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (t >= n * (kFnnPad / 4)) return;
+    const int64_t i = t / (kFnnPad / 4), q = t % (kFnnPad / 4);
+    float v[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const int b = static_cast<int>(4 * q + c);
+        v[c] = b < kFeatDim ? f[i * kFeatDim + b] : 0.0f;
+    }
+    out[t] = make_float4(v[0], v[1], v[2], v[3]);
+}
+
+// grid (source blocks, target chunks): FP32 best / runner-up per pair
+__global__ void __launch_bounds__(kFnnThreads) k_fnn_partial(const float4* __restrict__ sf, int64_t ns,
+                                                             const float4* __restrict__ tf, int64_t nt,
+                                                             int64_t chunk, Best3* __restrict__ partial) {
+    __shared__ float4 s_t[kFnnTile * (kFnnPad / 4)];
+    const int64_t i = blockIdx.x * static_cast<int64_t>(kFnnThreads) + threadIdx.x;
+    float4 s[kFnnPad / 4];
+#pragma unroll
+    for (int q = 0; q < kFnnPad / 4; ++q) s[q] = i < ns ? sf[i * (kFnnPad / 4) + q] : make_float4(0, 0, 0, 0);
+    const int64_t j_begin = blockIdx.y * chunk;
+    const int64_t j_end = j_begin + chunk < nt ? j_begin + chunk : nt;
+    float f1 = __int_as_float(0x7f800000), f2 = f1;
+    int32_t j1 = -1;
+    for (int64_t j0 = j_begin; j0 < j_end; j0 += kFnnTile) {
+        const int tile = static_cast<int>(j_end - j0 < kFnnTile ? j_end - j0 : kFnnTile);
+        __syncthreads();
+        for (int q = threadIdx.x; q < tile * (kFnnPad / 4); q += kFnnThreads) s_t[q] = tf[j0 * (kFnnPad / 4) + q];
+        __syncthreads();
+        for (int jj = 0; jj < tile; ++jj) {
+            const float d2 = feat_d2f(s, s_t + jj * (kFnnPad / 4));
+            if (d2 < f1) {
+                f2 = f1;
+                f1 = d2;
+                j1 = static_cast<int32_t>(j0 + jj);
+            } else if (d2 < f2) {
+                f2 = d2;
+            }
+        }
+    }
+    if (i < ns) partial[blockIdx.y * ns + i] = Best3{f1, j1, f2};
+}
+
+__global__ void k_fnn_merge(const float4* __restrict__ sf, const float* __restrict__ sraw, int64_t ns,
+                            const float4* __restrict__ tf, const float* __restrict__ traw, int64_t nt,
+                            const Best3* __restrict__ partial, int n_chunks, int32_t* __restrict__ out) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= ns) return;
+    Best3 b = partial[i];
+    for (int c = 1; c < n_chunks; ++c) {
+        const Best3 p = partial[c * ns + i];
+        if (p.f1 < b.f1) {
+            b.f2 = fminf(b.f1, p.f2);
+            b.f1 = p.f1;
+            b.j1 = p.j1;
+        } else {
+            b.f2 = fminf(b.f2, p.f1);  // equal values keep the earlier (lower) index
+        }
+    }
+    int32_t best = b.j1;
+    if (b.f1 > 0.0f && b.f2 <= b.f1 * (1.0f + kTieRel)) {
+        // near-tie: exact FP64 distances for every target within the band
+        const float lim = b.f1 * (1.0f + kTieRel);
+        float4 s[kFnnPad / 4];
+#pragma unroll
+        for (int q = 0; q < kFnnPad / 4; ++q) s[q] = sf[i * (kFnnPad / 4) + q];
+        double best_d2 = __longlong_as_double(0x7ff0000000000000ll);
+        best = -1;
+        for (int64_t j = 0; j < nt; ++j) {
+            if (feat_d2f(s, tf + j * (kFnnPad / 4)) > lim) continue;
+            double d2 = 0.0;
+            for (int q = 0; q < kFeatDim; ++q) {
+                const double diff = static_cast<double>(sraw[i * kFeatDim + q]) - static_cast<double>(traw[j * kFeatDim + q]);
+                d2 += diff * diff;
+            }
+            if (d2 < best_d2) {
+                best_d2 = d2;
+                best = static_cast<int32_t>(j);
+            }
+        }
+    }
+    out[i] = best;
 }
 
 struct Xf {
@@ -173,8 +293,35 @@ __global__ void k_info_final(const double* __restrict__ partials, int nb, const 
 
 cudaError_t feature_nn(const float* d_sf, int64_t ns, const float* d_tf, int64_t nt, int32_t* d_out,
                        cudaStream_t stream) {
-    const unsigned blocks = static_cast<unsigned>((ns + kFeatThreads - 1) / kFeatThreads);
-    k_feature_nn<<<blocks, kFeatThreads, 0, stream>>>(d_sf, ns, d_tf, nt, d_out);
+    if (const char* v = std::getenv("LK_FP64_ONLY"); v && v[0] == '1') {
+        const unsigned blocks = static_cast<unsigned>((ns + kFeatThreads - 1) / kFeatThreads);
+        k_feature_nn<<<blocks, kFeatThreads, 0, stream>>>(d_sf, ns, d_tf, nt, d_out);
+        return cudaGetLastError();
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t src_blocks = (ns + kFnnThreads - 1) / kFnnThreads;
+    int64_t n_chunks = (2 * sms + src_blocks - 1) / src_blocks;
+    if (n_chunks < 1) n_chunks = 1;
+    if (n_chunks > (nt + kFnnTile - 1) / kFnnTile) n_chunks = (nt + kFnnTile - 1) / kFnnTile;
+    const int64_t chunk = (nt + n_chunks - 1) / n_chunks;
+    n_chunks = (nt + chunk - 1) / chunk;
+    float4 *sp = nullptr, *tp = nullptr;
+    Best3* partial = nullptr;
+    cudaError_t e;
+    if ((e = pool_alloc(&sp, ns * kFnnPad * sizeof(float), stream)) != cudaSuccess) return e;
+    if ((e = pool_alloc(&tp, nt * kFnnPad * sizeof(float), stream)) != cudaSuccess) return e;
+    if ((e = pool_alloc(&partial, n_chunks * ns * sizeof(Best3), stream)) != cudaSuccess) return e;
+    k_pad_features<<<static_cast<unsigned>((ns * 9 + 255) / 256), 256, 0, stream>>>(d_sf, ns, sp);
+    k_pad_features<<<static_cast<unsigned>((nt * 9 + 255) / 256), 256, 0, stream>>>(d_tf, nt, tp);
+    k_fnn_partial<<<dim3(static_cast<unsigned>(src_blocks), static_cast<unsigned>(n_chunks)), kFnnThreads, 0,
+                    stream>>>(sp, ns, tp, nt, chunk, partial);
+    k_fnn_merge<<<static_cast<unsigned>((ns + 255) / 256), 256, 0, stream>>>(sp, d_sf, ns, tp, d_tf, nt, partial,
+                                                                            static_cast<int>(n_chunks), d_out);
+    pool_free(sp, stream);
+    pool_free(tp, stream);
+    pool_free(partial, stream);
     return cudaGetLastError();
 }
 

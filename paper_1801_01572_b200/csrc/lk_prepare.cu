@@ -228,50 +228,48 @@ __device__ __forceinline__ int swap_decision(double x1, double x2) {
     return 2;
 }
 
-// proj/src/fpfh.cpp:17-48. `decide` = 0/1 forces the swap test's outcome;
-// -1 evaluates it (returns false with *undecided set when the host must).
-__device__ __forceinline__ bool pair_angles(V3 p1, V3 n1, V3 p2, V3 n2, double& alpha, double& phi,
-                                            double& theta, int decide = -1, bool* undecided = nullptr,
-                                            double* x1_out = nullptr, double* x2_out = nullptr) {
-    V3 d = sub(p2, p1);
-    double dist = sqrt(sqnorm(d));
-    if (dist <= 0.0) return false;
-    double angle1 = dot(n1, d) / dist;
-    double angle2 = dot(n2, d) / dist;
-    V3 ns = n1, nt = n2, line = d;
-    double cos_line = angle1;
-    int swap = decide;
-    if (swap < 0) {
-        swap = swap_decision(fabs(angle1), fabs(angle2));
-        if (swap == 2) {
-            *undecided = true;
-            *x1_out = fabs(angle1);
-            *x2_out = fabs(angle2);
-            return false;
-        }
-    }
-    if (swap == 1) {
-        ns = n2;
-        nt = n1;
-        line = mk(-d.x, -d.y, -d.z);
-        cos_line = -angle2;
-    }
-    V3 u = ns;
-    V3 v = cross(line, u);
-    double v_len = sqrt(sqnorm(v));
-    if (v_len <= 1e-12 * dist) return false;
-    v = mk(v.x / v_len, v.y / v_len, v.z / v_len);
-    V3 w = cross(u, v);
-    alpha = dot(v, nt);
-    phi = cos_line;
-    theta = atan2(dot(w, nt), dot(u, nt));
-    return true;
-}
-
 // proj/src/fpfh.cpp:50-53
 __device__ __forceinline__ int bin_index(double value, double lo, double hi) {
     int b = floor_cell(11 * (value - lo) / (hi - lo));
     return b < 0 ? 0 : (b > 10 ? 10 : b);
+}
+
+// proj/src/fpfh.cpp:17-48, split at the frame-source test: pair_setup forms
+// d, dist and the two cosines; pair_bins finishes the Darboux frame for a
+// given test outcome and returns the three histogram bins (false = no vote).
+struct PairSetup {
+    V3 d;
+    double dist, a1, a2;
+};
+__device__ __forceinline__ bool pair_setup(V3 p1, V3 n1, V3 p2, V3 n2, PairSetup& s) {
+    s.d = sub(p2, p1);
+    s.dist = sqrt(sqnorm(s.d));
+    if (s.dist <= 0.0) return false;
+    s.a1 = dot(n1, s.d) / s.dist;
+    s.a2 = dot(n2, s.d) / s.dist;
+    return true;
+}
+__device__ __forceinline__ bool pair_bins(const PairSetup& s, V3 n1, V3 n2, int swap, int3& bins) {
+    V3 ns = n1, nt = n2, line = s.d;
+    double cos_line = s.a1;
+    if (swap == 1) {
+        ns = n2;
+        nt = n1;
+        line = mk(-s.d.x, -s.d.y, -s.d.z);
+        cos_line = -s.a2;
+    }
+    V3 u = ns;
+    V3 v = cross(line, u);
+    double v_len = sqrt(sqnorm(v));
+    if (v_len <= 1e-12 * s.dist) return false;
+    v = mk(v.x / v_len, v.y / v_len, v.z / v_len);
+    V3 w = cross(u, v);
+    const double alpha = dot(v, nt);
+    const double phi = cos_line;
+    const double theta = atan2(dot(w, nt), dot(u, nt));
+    bins = make_int3(bin_index(alpha, -1.0, 1.0), 11 + bin_index(phi, -1.0, 1.0),
+                     22 + bin_index(theta, -M_PI, M_PI));
+    return true;
 }
 
 // neighbours within r (inclusive), self excluded (proj/src/fpfh.cpp:66-74)
@@ -354,19 +352,29 @@ __global__ void __launch_bounds__(32 * kFpfhWarps) k_spfh(const double* __restri
             const int32_t j = nbr[k];
             const V3 nq = ld3(nrm, j);
             if (is_zero(nq)) continue;
-            double alpha, phi, theta, x1, x2;
-            bool undecided = false;
-            if (!pair_angles(p, np, ld3(pos, j), nq, alpha, phi, theta, -1, &undecided, &x1, &x2)) {
-                if (undecided) {
+            PairSetup s;
+            if (!pair_setup(p, np, ld3(pos, j), nq, s)) continue;
+            const int dec = swap_decision(fabs(s.a1), fabs(s.a2));
+            int3 bins;
+            bool valid;
+            if (dec == 2) {
+                // undecidable here: settle it only if the outcome depends on it
+                int3 b1;
+                valid = pair_bins(s, np, nq, 0, bins);
+                const bool valid1 = pair_bins(s, np, nq, 1, b1);
+                if (valid != valid1 || (valid && (bins.x != b1.x || bins.y != b1.y || bins.z != b1.z))) {
                     const int32_t slot = atomicAdd(n_deferred, 1);
                     deferred[slot] = make_int2(static_cast<int32_t>(i), j);
-                    deferred_x[slot] = make_double2(x1, x2);
+                    deferred_x[slot] = make_double2(fabs(s.a1), fabs(s.a2));
+                    continue;
                 }
-                continue;
+            } else {
+                valid = pair_bins(s, np, nq, dec, bins);
             }
-            atomicAdd(&hist[warp][bin_index(alpha, -1.0, 1.0)], 1);
-            atomicAdd(&hist[warp][11 + bin_index(phi, -1.0, 1.0)], 1);
-            atomicAdd(&hist[warp][22 + bin_index(theta, -M_PI, M_PI)], 1);
+            if (!valid) continue;
+            atomicAdd(&hist[warp][bins.x], 1);
+            atomicAdd(&hist[warp][bins.y], 1);
+            atomicAdd(&hist[warp][bins.z], 1);
             votes += 1;
         }
     }
@@ -383,14 +391,14 @@ __global__ void k_spfh_resolve(const double* __restrict__ pos, const double* __r
     const int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= m) return;
     const int2 ij = deferred[k];
-    double alpha, phi, theta;
-    if (!pair_angles(ld3(pos, ij.x), ld3(nrm, ij.x), ld3(pos, ij.y), ld3(nrm, ij.y), alpha, phi, theta,
-                     decision[k]))
-        return;
+    const V3 n1 = ld3(nrm, ij.x), n2 = ld3(nrm, ij.y);
+    PairSetup s;
+    int3 bins;
+    if (!pair_setup(ld3(pos, ij.x), n1, ld3(pos, ij.y), n2, s) || !pair_bins(s, n1, n2, decision[k], bins)) return;
     int32_t* c = counts + 34 * static_cast<int64_t>(ij.x);
-    atomicAdd(c + bin_index(alpha, -1.0, 1.0), 1);
-    atomicAdd(c + 11 + bin_index(phi, -1.0, 1.0), 1);
-    atomicAdd(c + 22 + bin_index(theta, -M_PI, M_PI), 1);
+    atomicAdd(c + bins.x, 1);
+    atomicAdd(c + bins.y, 1);
+    atomicAdd(c + bins.z, 1);
     atomicAdd(c + 33, 1);
 }
 

@@ -62,6 +62,29 @@ def test_feature_nn_cache_matches_oracle(prepared1, oracle):
     assert np.array_equal(lk.feature_nn_cache(src, tgt), oracle.feature_nn_cache(src, tgt))
 
 
+@pytest.mark.parametrize("fp64_only", ["0", "1"])
+def test_feature_nn_near_ties(oracle, monkeypatch, fp64_only):
+    # targets one ulp away from a source feature, exact duplicates, zero features:
+    # the FP32 pre-match must hand every near-tie to the exact FP64 resolution
+    monkeypatch.setenv("LK_FP64_ONLY", fp64_only)
+    rng = np.random.default_rng(5)
+    src = rng.uniform(0, 200, size=(700, 33)).astype(np.float32)
+    tgt = rng.uniform(0, 200, size=(900, 33)).astype(np.float32)
+    for k in range(0, 600, 3):
+        t = src[k].copy()
+        tgt[(7 * k) % 900] = t
+        t2 = t.copy()
+        t2[k % 33] = np.nextafter(t2[k % 33], np.float32(1e9))
+        tgt[(7 * k + 1) % 900] = t2
+        t3 = t.copy()
+        t3[(k + 5) % 33] = np.nextafter(t3[(k + 5) % 33], np.float32(-1e9))
+        tgt[(7 * k + 2) % 900] = t3
+    src[650:] = 0.0
+    tgt[100] = 0.0
+    tgt[400] = 0.0
+    assert np.array_equal(lk.feature_nn_cache(src, tgt), oracle.feature_nn_cache(src, tgt))
+
+
 def test_eval_grid_build_matches_oracle(pair1, oracle):
     t = pair1.target
     g = lk.build_eval_grid(t, 0.075)
