@@ -10,11 +10,13 @@
 //                   the cell block, normal gate (registration.cpp:165-210). Each
 //                   item leaves its inlier / miss ballots and the inliers' d2.
 //   k_score_exits   warp per candidate: exact miss-budget decision and the
-//                   reference's visit count from the miss ballots.
-//   k_score_sums    warp per fully scored candidate: the sequential FP64 sum of
-//                   d2 in point order, qualification, per-CTA best; the last CTA
-//                   reduces under the strict total order (registration.cpp:272-276)
-//                   and writes the rank record.
+//                   reference's visit count from the miss ballots; inliers and a
+//                   tree sum of d2 with a rigorous order bound decide qualification
+//                   (the sequential chain only when the bound straddles max_fitness).
+//   k_score_finalists one CTA: global max inliers / min fitness, the finalists
+//                   whose bounds overlap, their exact sequential sums in point
+//                   order; the strict total order (registration.cpp:272-276) picks
+//                   the winner and the rank record is written.
 //   k_score         warp per candidate streaming its points in order (explicit
 //                   candidate lists, and candidates beyond the split capacity).
 //
@@ -573,15 +575,66 @@ __global__ void __launch_bounds__(kScoreThreads) k_score_split(SourceView src, G
     }
 }
 
+// Per fully scored split candidate, what the final selection needs.
+struct CandInfo {
+    int64_t inliers;  // -1: exited or not qualified
+    double fitness;   // exact when exact != 0, else the tree-sum approximation
+    int64_t exact;
+};
+
+// Sequential FP64 sum of the inliers' d2 in point order (registration.cpp:206),
+// warp-cooperative: each round the lanes compact 8 chunks' inlier addends in
+// point order into `buf` (256 doubles of shared memory), then lane 0 adds them
+// in that order -- a pure dependent-add chain fed by shared-memory loads.
+__device__ double exact_chain(const uint32_t* __restrict__ im, const double* __restrict__ ad, int32_t n_chunks,
+                              double* buf) {
+    const int lane = threadIdx.x & 31;
+    const unsigned below = (1u << lane) - 1u;
+    double sum = 0.0;
+    for (int32_t c0 = 0; c0 < n_chunks; c0 += 8) {
+        int base = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const uint32_t m = (c0 + j < n_chunks) ? __ldg(im + c0 + j) : 0u;
+            if ((m >> lane) & 1u) buf[base + __popc(m & below)] = __ldg(ad + static_cast<int64_t>(c0 + j) * 32 + lane);
+            base += __popc(m);
+        }
+        __syncwarp();
+        if (lane == 0) {
+            int k = 0;
+            for (; k + 4 <= base; k += 4) {
+                const double x0 = buf[k], x1 = buf[k + 1], x2 = buf[k + 2], x3 = buf[k + 3];
+                sum += x0;
+                sum += x1;
+                sum += x2;
+                sum += x3;
+            }
+            for (; k < base; ++k) sum += buf[k];
+        }
+        __syncwarp();
+    }
+    return __shfl_sync(kFull, sum, 0);
+}
+
+// Relative bound between any two summation orders of n non-negative terms
+// (each within (n - 1) u of the exact sum), plus the final division.
+__device__ __forceinline__ double order_bound(int64_t n) { return 2.0 * static_cast<double>(n + 1) * 1.1102230246251565e-16 + 4.5e-16; }
+
 // Warp per split candidate: the exact miss-budget decision and the
-// reference's visit count from the ordered miss ballots; fully scored
-// candidates are appended to full_list for k_score_sums.
+// reference's visit count from the ordered miss ballots; for fully scored
+// candidates the inlier count, a tree-reduced sum with a rigorous bound, and
+// the qualification (the sequential chain only when the bound straddles
+// max_fitness). Publishes per-CTA (max inliers, min fitness) for the
+// finalist pass.
 __global__ void __launch_bounds__(kScoreThreads) k_score_exits(int64_t ns, ScoreParams sp, int64_t cap,
-                                                               int32_t n_chunks,
+                                                               int32_t n_chunks, int64_t ns_pad,
                                                                const uint32_t* __restrict__ miss_masks,
-                                                               int64_t* __restrict__ full_list,
+                                                               const uint32_t* __restrict__ inl_masks,
+                                                               const double* __restrict__ addends,
+                                                               CandInfo* __restrict__ info,
                                                                Counters* __restrict__ ctr,
                                                                BestRec* __restrict__ block_best, int best_offset) {
+    __shared__ double s_chain[kScoreWarps][256];
     const int lane = threadIdx.x & 31;
     const int64_t n_all = static_cast<int64_t>(ctr->n_candidates);
     const int64_t n_cand = n_all < cap ? n_all : cap;
@@ -616,60 +669,166 @@ __global__ void __launch_bounds__(kScoreThreads) k_score_exits(int64_t ns, Score
         }
         wt.w_ref += static_cast<unsigned long long>(visited);
         wt.executed += static_cast<unsigned long long>(ns);
-        if (!exited && lane == 0) full_list[atomicAdd(&ctr->n_full, 1ull)] = cand;
+        CandInfo ci{-1, 0.0, 0};
+        if (!exited) {
+            // inliers and a lane-parallel sum of the inliers' d2 (any order)
+            const uint32_t* im = inl_masks + cand * n_chunks;
+            const double* ad = addends + cand * ns_pad;
+            int64_t inl = 0;
+            double part = 0.0;
+            for (int32_t c = 0; c < n_chunks; ++c) {
+                const uint32_t m = __ldg(im + c);
+                inl += __popc(m);
+                if ((m >> lane) & 1u) part += __ldg(ad + static_cast<int64_t>(c) * 32 + lane);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(kFull, part, o);
+            const double ratio = static_cast<double>(inl) / static_cast<double>(ns);
+            if (!(ratio < sp.min_ratio)) {
+                double fit = inl > 0 ? part / static_cast<double>(inl) : 0.0;
+                int64_t exact = inl == 0 ? 1 : 0;
+                const double eb = order_bound(inl) * fit;
+                bool qualifies = fit + eb <= sp.max_fitness;
+                if (!exact && !qualifies && fit - eb <= sp.max_fitness) {
+                    // the bound straddles max_fitness: the reference's own sum decides
+                    fit = exact_chain(im, ad, n_chunks, s_chain[threadIdx.x >> 5]) / static_cast<double>(inl);
+                    exact = 1;
+                    qualifies = !(fit > sp.max_fitness);
+                }
+                if (qualifies) {
+                    ci = CandInfo{inl, fit, exact};
+                    wt.qualified += 1;
+                    BestRec c{1, inl, fit, cand, cand};
+                    if (better(c, wt.best)) wt.best = c;
+                }
+            }
+        }
+        if (lane == 0) info[cand] = ci;
     }
     publish_cta(wt, ctr, block_best, best_offset + blockIdx.x, false);
 }
 
-// Thread per fully scored candidate: inlier count and the sequential FP64
-// sum of d2 in point order (registration.cpp:206), then qualification and
-// the arg-best. Non-inlier slots contribute nothing (masked out).
-__global__ void __launch_bounds__(kScoreThreads) k_score_sums(int64_t ns, ScoreParams sp,
-                                                              const double* __restrict__ cand_rt,
-                                                              const int64_t* __restrict__ cand_index,
-                                                              int32_t n_chunks, int64_t ns_pad,
-                                                              const uint32_t* __restrict__ inl_masks,
-                                                              const double* __restrict__ addends,
-                                                              const int64_t* __restrict__ full_list, int n_best_total,
-                                                              int64_t sampled, Counters* __restrict__ ctr,
-                                                              BestRec* __restrict__ block_best,
-                                                              RecordDev* __restrict__ rec) {
-    const int lane = threadIdx.x & 31;
-    const int64_t n_full = static_cast<int64_t>(ctr->n_full);
-    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
-    WarpTally wt;
-    for (int64_t f = blockIdx.x * static_cast<int64_t>(blockDim.x >> 5) + (threadIdx.x >> 5); f < n_full;
-         f += nwarps) {
-        const int64_t cand = full_list[f];
-        const uint32_t* im = inl_masks + cand * n_chunks;
-        const double* ad = addends + cand * ns_pad;
-        int64_t inliers = 0;
-        double sum = 0.0;
-        // 8 chunks per round: loads issued together, then the ordered adds
-        // (lane order within a chunk, chunks in order); non-inliers add +0.0
-        for (int32_t c0 = 0; c0 < n_chunks; c0 += 8) {
-            uint32_t m[8];
-            double a[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) m[j] = (c0 + j < n_chunks) ? __ldg(im + c0 + j) : 0u;
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-                a[j] = ((m[j] >> lane) & 1u) ? __ldg(ad + static_cast<int64_t>(c0 + j) * 32 + lane) : 0.0;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                inliers += __popc(m[j]);
-                if (m[j]) {
-#pragma unroll
-                    for (int L = 0; L < 32; ++L) sum += __shfl_sync(kFull, a[j], L);
-                }
-            }
-        }
-        wt.candidate(inliers, sum, ns, sp, __ldg(cand_index + cand), cand);
+// Single CTA: the global (max inliers, min approximate fitness) from the
+// per-CTA bests; finalists = qualified candidates with that inlier count whose
+// fitness bound overlaps the minimum's; their exact sequential sums decide
+// under (fitness, hypothesis index) (registration.cpp:272-276); record out.
+__global__ void __launch_bounds__(kScoreThreads) k_score_finalists(int32_t n_chunks, int64_t ns_pad,
+                                                                   const uint32_t* __restrict__ inl_masks,
+                                                                   const double* __restrict__ addends,
+                                                                   const CandInfo* __restrict__ info, int64_t cap,
+                                                                   const double* __restrict__ cand_rt,
+                                                                   const int64_t* __restrict__ cand_index,
+                                                                   const BestRec* __restrict__ block_best,
+                                                                   int n_best, int64_t sampled,
+                                                                   Counters* __restrict__ ctr,
+                                                                   RecordDev* __restrict__ rec) {
+    __shared__ BestRec s_red[kScoreWarps];
+    __shared__ int64_t s_final[256];
+    __shared__ int s_nfinal;
+    __shared__ BestRec s_win[kScoreWarps];
+    __shared__ double s_chain[kScoreWarps][256];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t n_all = static_cast<int64_t>(ctr->n_candidates);
+    const int64_t n_split = n_all < cap ? n_all : cap;
+    // 1. global (max inliers, min fitness) over the per-CTA bests
+    BestRec g{0, 0, 0.0, INT64_MAX, -1};
+    for (int b = threadIdx.x; b < n_best; b += blockDim.x) {
+        const BestRec c = block_best[b];
+        if (c.valid && (!g.valid || c.inliers > g.inliers || (c.inliers == g.inliers && c.fitness < g.fitness))) g = c;
     }
-    const bool last = publish_cta(wt, ctr, block_best, blockIdx.x, true);
-    if (last) write_record(block_best, n_best_total, cand_rt, static_cast<int64_t>(__ldcg(&ctr->n_candidates)),
-                           sampled, ctr, rec);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        BestRec c;
+        c.valid = __shfl_down_sync(kFull, g.valid, o);
+        c.inliers = __shfl_down_sync(kFull, g.inliers, o);
+        c.fitness = __shfl_down_sync(kFull, g.fitness, o);
+        c.index = __shfl_down_sync(kFull, g.index, o);
+        c.slot = __shfl_down_sync(kFull, g.slot, o);
+        if (c.valid && (!g.valid || c.inliers > g.inliers || (c.inliers == g.inliers && c.fitness < g.fitness))) g = c;
+    }
+    if (lane == 0) s_red[warp] = g;
+    if (threadIdx.x == 0) s_nfinal = 0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < kScoreWarps; ++w) {
+            const BestRec c = s_red[w];
+            if (c.valid && (!g.valid || c.inliers > g.inliers || (c.inliers == g.inliers && c.fitness < g.fitness)))
+                g = c;
+        }
+        s_red[0] = g;
+    }
+    __syncthreads();
+    g = s_red[0];
+    RecordDev* out = rec;
+    if (!g.valid) {
+        if (threadIdx.x == 0) {
+            RecordDev r{};
+            r.index = -1;
+            r.sampled = sampled;
+            r.prerejected = static_cast<int64_t>(ctr->prerejected);
+            r.degenerate = static_cast<int64_t>(ctr->degenerate);
+            r.evaluated = n_all;
+            r.qualified = static_cast<int64_t>(ctr->qualified);
+            r.w_ref = static_cast<int64_t>(ctr->w_ref);
+            r.evals_executed = static_cast<int64_t>(ctr->evals_executed);
+            *out = r;
+        }
+        return;
+    }
+    // 2. finalists: same inlier count, fitness within the combined bounds
+    const double lim = g.fitness * (1.0 + 2.0 * order_bound(g.inliers)) + 1e-300;
+    for (int64_t k = threadIdx.x; k < n_split; k += blockDim.x) {
+        const CandInfo ci = info[k];
+        if (ci.inliers == g.inliers && ci.fitness <= lim) {
+            const int slot = atomicAdd(&s_nfinal, 1);
+            if (slot < 256) s_final[slot] = k;
+        }
+    }
+    __syncthreads();
+    const int nf = s_nfinal;
+    // 3. exact fitness of every finalist (warp per finalist), pick the best
+    BestRec wbest{0, 0, 0.0, INT64_MAX, -1};
+    const bool listed = nf <= 256;  // else (massive ties) rescan the candidates
+    const int64_t n_iter = listed ? nf : n_split;
+    for (int64_t f = warp; f < n_iter; f += kScoreWarps) {
+        const int64_t k = listed ? s_final[f] : f;
+        const CandInfo ci = info[k];
+        if (!listed && !(ci.inliers == g.inliers && ci.fitness <= lim)) continue;
+        double fit = ci.fitness;
+        if (!ci.exact)
+            fit = exact_chain(inl_masks + k * n_chunks, addends + k * ns_pad, n_chunks, s_chain[warp]) /
+                  static_cast<double>(ci.inliers);
+        BestRec c{1, ci.inliers, fit, __ldg(cand_index + k), k};
+        if (better(c, wbest)) wbest = c;
+    }
+    if (lane == 0) s_win[warp] = wbest;
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    BestRec b = s_win[0];
+    for (int w = 1; w < kScoreWarps; ++w)
+        if (better(s_win[w], b)) b = s_win[w];
+    // the overflow candidates (k_score, exact already) compete through block_best
+    for (int i = 0; i < n_best; ++i) {
+        const BestRec c = block_best[i];
+        if (c.valid && c.slot >= cap && better(c, b)) b = c;
+    }
+    RecordDev r{};
+    r.valid = b.valid;
+    r.inliers = b.valid ? b.inliers : 0;
+    r.fitness = b.valid ? b.fitness : 0.0;
+    r.index = b.valid ? b.index : -1;
+    for (int q = 0; q < 9; ++q) r.R[q] = b.valid ? cand_rt[12 * b.slot + q] : 0.0;
+    for (int q = 0; q < 3; ++q) r.t[q] = b.valid ? cand_rt[12 * b.slot + 9 + q] : 0.0;
+    r.sampled = sampled;
+    r.prerejected = static_cast<int64_t>(ctr->prerejected);
+    r.degenerate = static_cast<int64_t>(ctr->degenerate);
+    r.evaluated = n_all;
+    r.qualified = static_cast<int64_t>(ctr->qualified);
+    r.w_ref = static_cast<int64_t>(ctr->w_ref);
+    r.evals_executed = static_cast<int64_t>(ctr->evals_executed);
+    *out = r;
 }
+
 
 int blocks_per_sm(const void* fn) {
     int b = 0;
@@ -773,7 +932,7 @@ cudaError_t RunBuffers::ensure_split(int64_t ns, int64_t max_candidates) {
     full_list = nullptr;
     split_cap = 0;
     cudaError_t e;
-    if ((e = pool_alloc(&full_list, cap * sizeof(int64_t), stream)) != cudaSuccess) return e;
+    if ((e = pool_alloc(&full_list, cap * 3 * sizeof(int64_t), stream)) != cudaSuccess) return e;  // CandInfo
     if ((e = pool_alloc(&inl_masks, cap * n_chunks * sizeof(uint32_t), stream)) != cudaSuccess) return e;
     if ((e = pool_alloc(&miss_masks, cap * n_chunks * sizeof(uint32_t), stream)) != cudaSuccess) return e;
     if ((e = pool_alloc(&addends, cap * ns_pad * sizeof(double), stream)) != cudaSuccess) return e;
@@ -788,10 +947,9 @@ cudaError_t run_hypotheses_range(const SourceView& src, const double* d_tgt_pos,
                                  cudaEvent_t* events) {
     const int64_t count = end - begin;
     const int split_blocks = sm_count * split_blocks_per_sm();
-    const int sums_blocks = sm_count * 2;  // a warp per fully scored candidate, all in flight
     const int exit_blocks = sm_count * 2;
     const int over_blocks = sm_count;
-    cudaError_t e = rb.ensure(count > 0 ? count : 1, sums_blocks + exit_blocks + over_blocks);
+    cudaError_t e = rb.ensure(count > 0 ? count : 1, exit_blocks + over_blocks);
     if (e != cudaSuccess) return e;
     // split capacity: a few percent of the hypotheses survive pre-rejection in
     // practice; any excess is scored by the streaming k_score (exact too)
@@ -826,14 +984,15 @@ cudaError_t run_hypotheses_range(const SourceView& src, const double* d_tgt_pos,
     k_score<<<over_blocks, kScoreThreads, 0, stream>>>(src, grid, sp, rb.cand_rt, cand_fast, rb.cand_index,
                                                        rb.split_cap, -1,
                                                        count, nullptr, nullptr, rb.counters, rb.block_best,
-                                                       sums_blocks + exit_blocks, nullptr);
-    k_score_exits<<<exit_blocks, kScoreThreads, 0, stream>>>(src.n, sp, rb.split_cap, n_chunks, rb.miss_masks,
-                                                             rb.full_list, rb.counters, rb.block_best, sums_blocks);
-    k_score_sums<<<sums_blocks, kScoreThreads, 0, stream>>>(src.n, sp, rb.cand_rt, rb.cand_index, n_chunks,
-                                                            rb.split_ns_pad, rb.inl_masks, rb.addends, rb.full_list,
-                                                            sums_blocks + exit_blocks + over_blocks, count,
-                                                            rb.counters, rb.block_best,
-                                                            static_cast<RecordDev*>(d_record));
+                                                       exit_blocks, nullptr);
+    CandInfo* info = reinterpret_cast<CandInfo*>(rb.full_list);
+    k_score_exits<<<exit_blocks, kScoreThreads, 0, stream>>>(src.n, sp, rb.split_cap, n_chunks, rb.split_ns_pad,
+                                                             rb.miss_masks, rb.inl_masks, rb.addends, info,
+                                                             rb.counters, rb.block_best, 0);
+    k_score_finalists<<<1, kScoreThreads, 0, stream>>>(n_chunks, rb.split_ns_pad, rb.inl_masks, rb.addends, info,
+                                                       rb.split_cap, rb.cand_rt, rb.cand_index, rb.block_best,
+                                                       exit_blocks + over_blocks, count, rb.counters,
+                                                       static_cast<RecordDev*>(d_record));
     if (events) cudaEventRecord(events[3], stream);
     return cudaGetLastError();
 }
