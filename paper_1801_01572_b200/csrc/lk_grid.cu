@@ -296,6 +296,61 @@ __global__ void k_block_fill(const int32_t* __restrict__ start, const int32_t* _
     info[c] = make_int2(off0, off - off0);
 }
 
+// ---- fine lists ----------------------------------------------------------
+// Every point is listed in each fine cell whose box lies within d_max (+ a
+// relative 1e-9 and an absolute 1e-12 safety margin; listing extra points is
+// harmless) -- a superset of any query's d_max ball inside that cell.
+__device__ __forceinline__ bool box_within(double px, double py, double pz, double bx, double by, double bz,
+                                           double h, double r2) {
+    const double dx = fmax(0.0, fmax(bx - px, px - (bx + h)));
+    const double dy = fmax(0.0, fmax(by - py, py - (by + h)));
+    const double dz = fmax(0.0, fmax(bz - pz, pz - (bz + h)));
+    return (dx * dx + dy * dy) + dz * dz <= r2;
+}
+
+template <bool kFill>
+__global__ void k_fine_lists(const double* __restrict__ pos, int64_t n, GridView g, int rf, double r2,
+                             int32_t* __restrict__ counts, const int32_t* __restrict__ offsets,
+                             float4* __restrict__ pts) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const double px = pos[3 * i], py = pos[3 * i + 1], pz = pos[3 * i + 2];
+    const int kx = floor_cell((px - g.ox) / g.fcell) - 2 * g.offx;
+    const int ky = floor_cell((py - g.oy) / g.fcell) - 2 * g.offy;
+    const int kz = floor_cell((pz - g.oz) / g.fcell) - 2 * g.offz;
+    const float4 e = make_float4(static_cast<float>((px - g.ox) / g.fcell - 2 * g.offx),
+                                 static_cast<float>((py - g.oy) / g.fcell - 2 * g.offy),
+                                 static_cast<float>((pz - g.oz) / g.fcell - 2 * g.offz),
+                                 __int_as_float(static_cast<int32_t>(i)));
+    for (int x = max(kx - rf, 0); x <= min(kx + rf, g.fnx - 1); ++x)
+        for (int y = max(ky - rf, 0); y <= min(ky + rf, g.fny - 1); ++y)
+            for (int z = max(kz - rf, 0); z <= min(kz + rf, g.fnz - 1); ++z) {
+                const double bx = g.ox + (x + 2 * g.offx) * g.fcell;
+                const double by = g.oy + (y + 2 * g.offy) * g.fcell;
+                const double bz = g.oz + (z + 2 * g.offz) * g.fcell;
+                if (!box_within(px, py, pz, bx, by, bz, g.fcell, r2)) continue;
+                const int64_t c = (static_cast<int64_t>(x) * g.fny + y) * g.fnz + z;
+                if (kFill)
+                    pts[offsets[c] + atomicAdd(&counts[c], 1)] = e;
+                else
+                    atomicAdd(&counts[c], 1);
+            }
+}
+
+__global__ void k_fine_info(const int32_t* __restrict__ offsets, int64_t nc, int2* __restrict__ info) {
+    const int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (c < nc) info[c] = make_int2(offsets[c], offsets[c + 1] - offsets[c]);
+}
+
+// each point's local cell in this grid (the reference's cell_of)
+__global__ void k_point_cells(const double* __restrict__ pos, int64_t n, GridView g, int4* __restrict__ out) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    out[i] = make_int4(floor_cell((pos[3 * i] - g.ox) / g.cell) - g.offx,
+                       floor_cell((pos[3 * i + 1] - g.oy) / g.cell) - g.offy,
+                       floor_cell((pos[3 * i + 2] - g.oz) / g.cell) - g.offz, 0);
+}
+
 __global__ void k_to_float4(const double* __restrict__ pos, int64_t n, float4* __restrict__ out) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < n)
@@ -336,6 +391,12 @@ void GridStorage::release() {
     pool_free(nrm_orig, stream);
     pool_free(block_f32, stream);
     pool_free(pos_orig, stream);
+    pool_free(fine_info, stream);
+    pool_free(fine_pts, stream);
+    pool_free(pcell, stream);
+    fine_info = nullptr;
+    fine_pts = nullptr;
+    pcell = nullptr;
     start = index = nullptr;
     slot_pos = slot_nrm = nullptr;
     near = nullptr;
@@ -449,6 +510,37 @@ cudaError_t build_grid(GridStorage& g, int kind, const double* d_pos, const doub
         k_block_fill<<<blocks_for(ncells, 256), 256, 0, stream>>>(g.start, g.index, g.slot_pos, d_off, ncells, v,
                                                                   g.block_info, g.block_pts, g.block_f32);
         cudaFreeAsync(d_off, stream);
+        // fine lists: half-size cells, points within d_max of each fine box
+        v.fcell = cell / 2.0;
+        v.fnx = 2 * v.nx;
+        v.fny = 2 * v.ny;
+        v.fnz = 2 * v.nz;
+        v.fine_dmax = kind == 0 ? cell : d_max;
+        const int64_t nfc = static_cast<int64_t>(v.fnx) * v.fny * v.fnz;
+        if (nfc < (int64_t)1 << 30) {
+            const int rf = static_cast<int>(std::ceil(v.fine_dmax / v.fcell));
+            const double r2 = v.fine_dmax * v.fine_dmax * (1.0 + 1e-9) + 1e-12;
+            int32_t *fcnt = nullptr, *foff = nullptr;
+            LK_TRY(cudaMallocAsync(&fcnt, nfc * sizeof(int32_t), stream));
+            LK_TRY(cudaMallocAsync(&foff, (nfc + 1) * sizeof(int32_t), stream));
+            LK_TRY(cudaMemsetAsync(fcnt, 0, nfc * sizeof(int32_t), stream));
+            k_fine_lists<false><<<blocks_for(n, 128), 128, 0, stream>>>(d_pos, n, v, rf, r2, fcnt, nullptr, nullptr);
+            LK_TRY(exclusive_scan(fcnt, nfc, foff, stream));
+            int32_t ftotal = 0;
+            LK_TRY(cudaMemcpyAsync(&ftotal, foff + nfc, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
+            LK_TRY(cudaStreamSynchronize(stream));
+            g.nfine = nfc;
+            g.nfine_entries = ftotal;
+            LK_TRY(pool_alloc(&g.fine_info, nfc * sizeof(int2), stream));
+            LK_TRY(pool_alloc(&g.fine_pts, (ftotal > 0 ? ftotal : 1) * sizeof(float4), stream));
+            LK_TRY(pool_alloc(&g.pcell, n * sizeof(int4), stream));
+            LK_TRY(cudaMemsetAsync(fcnt, 0, nfc * sizeof(int32_t), stream));
+            k_fine_lists<true><<<blocks_for(n, 128), 128, 0, stream>>>(d_pos, n, v, rf, r2, fcnt, foff, g.fine_pts);
+            k_fine_info<<<blocks_for(nfc, 256), 256, 0, stream>>>(foff, nfc, g.fine_info);
+            k_point_cells<<<blocks_for(n, 256), 256, 0, stream>>>(d_pos, n, v, g.pcell);
+            cudaFreeAsync(fcnt, stream);
+            cudaFreeAsync(foff, stream);
+        }
     }
     LK_TRY(cudaGetLastError());
     cudaFreeAsync(d_cell_of, stream);
@@ -463,6 +555,9 @@ cudaError_t build_grid(GridStorage& g, int kind, const double* d_pos, const doub
     v.nrm_orig = g.nrm_orig;
     v.block_f32 = g.block_f32;
     v.pos_orig = g.pos_orig;
+    v.fine_info = g.fine_info;
+    v.fine_pts = g.fine_pts;
+    v.pcell = g.pcell;
     g.view = v;
     return cudaStreamSynchronize(stream);
 }

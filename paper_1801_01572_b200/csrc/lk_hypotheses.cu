@@ -536,17 +536,142 @@ __global__ void __launch_bounds__(kScoreThreads) k_score(SourceView src, GridVie
     if (last) write_record(block_best, best_offset + gridDim.x, cand_rt, n_cand, sampled, ctr, rec);
 }
 
-// (candidate, chunk) items, chunk-major so neighbouring warps share the
-// source chunk in L1. No early exit: every point of a split candidate is
-// evaluated, the exit decision is made from the ballots in k_score_exits.
+// ---- split scoring over the fine lists ------------------------------------
+// FP32 image of (R, t) in fine-cell units (cell / 2, offset 2 off) with the
+// same guard-band construction as make_fast.
+__device__ __forceinline__ FastRT make_fast_fine(const double* R, const double* t, const GridView& g,
+                                                 const ScoreParams& sp) {
+    FastRT f;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) f.r[k] = static_cast<float>(R[k] / g.fcell);
+    f.t[0] = static_cast<float>((t[0] - g.ox) / g.fcell - 2 * g.offx);
+    f.t[1] = static_cast<float>((t[1] - g.oy) / g.fcell - 2 * g.offy);
+    f.t[2] = static_cast<float>((t[2] - g.oz) / g.fcell - 2 * g.offz);
+    const float u = 5.9604645e-8f;
+    const float tn = sqrtf(f.t[0] * f.t[0] + f.t[1] * f.t[1] + f.t[2] * f.t[2]);
+    const float dq = u * (5.0f * 2.0f * sp.pmax_cells + 4.0f * tn + 4.0f);
+    const float de = u * (2.0f * sp.nmax_cells + 2.0f);
+    const float delta = dq + de;
+    const float thr = static_cast<float>((sp.d_max / g.fcell) * (sp.d_max / g.fcell));
+    f.eps = 4.0f * dq + 1e-6f;
+    // d2 within sqrt(thr) + 1 fine cells: error <= 2 sqrt3 (sqrt(thr) + 1) delta + 3 delta^2 (+ FP32 rounding)
+    f.band = 4.0f * (3.5f * (sqrtf(thr) + 1.0f) * delta + 3.0f * delta * delta + 16.0f * u * (thr + 1.0f)) + 1e-7f;
+    f.ok = (sp.fast && g.fine_info && sp.d_max <= g.fine_dmax && f.eps < 0.02f && f.band < 0.05f) ? 1.0f : 0.0f;
+    f.pad = thr;  // d2_max in squared fine-cell units
+    return f;
+}
+
+__global__ void k_prep_fast_fine(const double* __restrict__ cand_rt, const Counters* __restrict__ ctr, GridView g,
+                                 ScoreParams sp, FastRT* __restrict__ out) {
+    const int64_t n = static_cast<int64_t>(ctr->n_candidates);
+    for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
+         k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        double R[9], t[3];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) R[q] = cand_rt[12 * k + q];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) t[q] = cand_rt[12 * k + 9 + q];
+        out[k] = make_fast_fine(R, t, g, sp);
+    }
+}
+
+// Exact resolution of one query over its fine list: FP32 top-3 with the guard
+// band, FP64 d2 for every entry that can be the minimum, and the reference's
+// window (the winner's EvalGrid cell within +-1 of y's, computed by division
+// exactly as registration.cpp:167-169). Any doubt falls back to eval_point.
+__device__ bool resolve_fine(const GridView& g, const double* R, const double* t, const FastRT& F, V3 p, V3 ns,
+                             float qx, float qy, float qz, int32_t off, int32_t cnt, const ScoreParams& sp,
+                             double& addend) {
+    const float inf = __int_as_float(0x7f800000);
+    float f1 = inf, f2 = inf, f3 = inf;
+    int32_t o1 = -1, o2 = -1;
+    for (int32_t e = off; e < off + cnt; ++e) {
+        const float4 E = __ldg(g.fine_pts + e);
+        const float dx = qx - E.x, dy = qy - E.y, dz = qz - E.z;
+        const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+        const int32_t o = __float_as_int(E.w);
+        if (d2 < f1) {
+            f3 = f2;
+            f2 = f1;
+            o2 = o1;
+            f1 = d2;
+            o1 = o;
+        } else if (d2 < f2) {
+            f3 = f2;
+            f2 = d2;
+            o2 = o;
+        } else if (d2 < f3) {
+            f3 = d2;
+        }
+    }
+    const float band = F.band;
+    const float thr = F.pad;
+    if (f1 > thr + band) return false;  // nothing within d_max of y
+    const V3 y = xform(R, t, p);
+    // y's cell in the reference grid (division, as the reference)
+    const double cx = floor((y.x - g.ox) / g.cell) - static_cast<double>(g.offx);
+    const double cy = floor((y.y - g.oy) / g.cell) - static_cast<double>(g.offy);
+    const double cz = floor((y.z - g.oz) / g.cell) - static_cast<double>(g.offz);
+    if (!(cx >= 0.0 && cy >= 0.0 && cz >= 0.0 && cx < g.nx && cy < g.ny && cz < g.nz)) return false;
+    const int ix = static_cast<int>(cx), iy = static_cast<int>(cy), iz = static_cast<int>(cz);
+    auto in_window = [&](int32_t o) {
+        const int4 c = __ldg(g.pcell + o);
+        return abs(c.x - ix) <= 1 && abs(c.y - iy) <= 1 && abs(c.z - iz) <= 1;
+    };
+    double best_d2 = __longlong_as_double(0x7ff0000000000000ll);
+    int32_t best_orig = INT32_MAX;
+    const float lim = f1 + 2.0f * band;
+    bool doubt = false;
+    auto consider = [&](int32_t o) {
+        const double d2 = sqnorm(sub(ld3(g.pos_orig, o), y));
+        if (d2 > sp.d2_max) return;
+        if (!in_window(o)) {
+            doubt = true;
+            return;
+        }
+        if (d2 < best_d2 || (d2 == best_d2 && o < best_orig)) {
+            best_d2 = d2;
+            best_orig = o;
+        }
+    };
+    if (f3 <= lim) {
+        for (int32_t e = off; e < off + cnt; ++e) {
+            const float4 E = __ldg(g.fine_pts + e);
+            const float dx = qx - E.x, dy = qy - E.y, dz = qz - E.z;
+            if (fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= lim) consider(__float_as_int(E.w));
+        }
+    } else {
+        consider(o1);
+        if (f2 <= lim) consider(o2);
+    }
+    if (doubt) return eval_point(g, R, t, p, ns, sp, addend);  // rounding at the window edge
+    if (best_orig == INT32_MAX) return false;
+    const V3 nt = ld3(g.nrm_orig, best_orig);
+    if (is_zero(ns) || is_zero(nt)) return false;
+    if (!(dot(rot(R, ns), nt) >= sp.cos_max)) return false;
+    if (sp.fitness_from_distance) {
+        const double dist = sqrt(best_d2);
+        addend = dist * dist;
+    } else {
+        addend = best_d2;
+    }
+    return true;
+}
+
+// Pass A: (candidate, chunk) items, chunk-major so neighbouring warps share
+// the source chunk in L1. Each lane locates its point's fine cell in FP32:
+// certain misses are settled here; points with a non-empty fine list (or a
+// coordinate near a fine-cell face) go to the dense queue for pass B, so no
+// lane idles through another lane's scan. No early exit: every point of a
+// split candidate is evaluated; k_score_exits decides from the ballots.
 __global__ void __launch_bounds__(kScoreThreads) k_score_split(SourceView src, GridView g, ScoreParams sp,
                                                                const double* __restrict__ cand_rt,
-                                                               const FastRT* __restrict__ cand_fast, int64_t cap,
+                                                               const FastRT* __restrict__ cand_fine, int64_t cap,
                                                                int32_t n_chunks, int64_t ns_pad,
                                                                uint32_t* __restrict__ inl_masks,
                                                                uint32_t* __restrict__ miss_masks,
-                                                               double* __restrict__ addends,
-                                                               Counters* __restrict__ ctr) {
+                                                               double* __restrict__ addends, int4* __restrict__ queue,
+                                                               int64_t queue_cap, Counters* __restrict__ ctr) {
     const int lane = threadIdx.x & 31;
     const int64_t n_all = static_cast<int64_t>(ctr->n_candidates);
     const int64_t n_cand = n_all < cap ? n_all : cap;
@@ -557,16 +682,53 @@ __global__ void __launch_bounds__(kScoreThreads) k_score_split(SourceView src, G
          w += nwarps) {
         const int64_t chunk = w / n_cand;
         const int64_t cand = w - chunk * n_cand;
-        double R[9], t[3];
-        load_rt(cand_rt + 12 * cand, R, t);
-        const FastRT F = load_fast(cand_fast + cand);
+        const FastRT F = load_fast(cand_fine + cand);
         const int64_t i = chunk * 32 + lane;
         const bool valid = i < ns;
-        bool inl = false;
+        int state = 0;  // 0 certain miss, 1 exact fallback, 2 fine-list scan
+        int2 bi = make_int2(0, 0);
+        if (valid) {
+            if (F.ok == 0.0f) {
+                state = 1;
+            } else {
+                const float4 P = __ldg(src.pos32 + i);
+                const float qx = fmaf(F.r[0], P.x, fmaf(F.r[1], P.y, fmaf(F.r[2], P.z, F.t[0])));
+                const float qy = fmaf(F.r[3], P.x, fmaf(F.r[4], P.y, fmaf(F.r[5], P.z, F.t[1])));
+                const float qz = fmaf(F.r[6], P.x, fmaf(F.r[7], P.y, fmaf(F.r[8], P.z, F.t[2])));
+                const float eps = F.eps;
+                if (!(qx < -eps || qy < -eps || qz < -eps || qx >= g.fnx + eps || qy >= g.fny + eps ||
+                      qz >= g.fnz + eps)) {
+                    const float fx = floorf(qx), fy = floorf(qy), fz = floorf(qz);
+                    const float rx = qx - fx, ry = qy - fy, rz = qz - fz;
+                    if (rx < eps || rx > 1.0f - eps || ry < eps || ry > 1.0f - eps || rz < eps || rz > 1.0f - eps) {
+                        state = 1;
+                    } else {
+                        const int ix = static_cast<int>(fx), iy = static_cast<int>(fy), iz = static_cast<int>(fz);
+                        if (ix >= 0 && iy >= 0 && iz >= 0 && ix < g.fnx && iy < g.fny && iz < g.fnz) {
+                            bi = __ldg(g.fine_info + (static_cast<int64_t>(ix) * g.fny + iy) * g.fnz + iz);
+                            if (bi.y > 0) state = 2;
+                        }
+                    }
+                }
+            }
+        }
+        const bool need = state != 0;
+        const unsigned long long slot = warp_atomic_add(&ctr->queue_n, need);
+        bool inl = false, inline_done = false;
         double addend = 0.0;
-        if (valid) inl = eval_point_fast(g, R, t, F, src, i, sp, addend);
+        if (need) {
+            if (static_cast<int64_t>(slot) < queue_cap) {
+                queue[slot] = make_int4(static_cast<int32_t>(cand), static_cast<int32_t>(i), bi.x,
+                                        state == 1 ? -1 : bi.y);
+            } else {  // queue full: evaluate here (exact, slow, never on the bench inputs)
+                double R[9], t[3];
+                load_rt(cand_rt + 12 * cand, R, t);
+                inl = eval_point(g, R, t, ld3(src.pos, i), ld3(src.nrm, i), sp, addend);
+                inline_done = true;
+            }
+        }
         const unsigned im = __ballot_sync(kFull, inl);
-        const unsigned mm = __ballot_sync(kFull, valid && !inl);
+        const unsigned mm = __ballot_sync(kFull, (valid && state == 0) || (inline_done && !inl));
         if (lane == 0) {
             inl_masks[cand * n_chunks + chunk] = im;
             miss_masks[cand * n_chunks + chunk] = mm;
@@ -574,6 +736,50 @@ __global__ void __launch_bounds__(kScoreThreads) k_score_split(SourceView src, G
         if (inl) addends[cand * ns_pad + i] = addend;
     }
 }
+
+// Pass B: thread per queued (candidate, point): the fine-list scan and the
+// exact decisions; results are OR-ed into the chunk ballots.
+__global__ void __launch_bounds__(kScoreThreads) k_score_resolve(SourceView src, GridView g, ScoreParams sp,
+                                                                 const double* __restrict__ cand_rt,
+                                                                 const FastRT* __restrict__ cand_fine,
+                                                                 int32_t n_chunks, int64_t ns_pad,
+                                                                 const int4* __restrict__ queue, int64_t queue_cap,
+                                                                 uint32_t* __restrict__ inl_masks,
+                                                                 uint32_t* __restrict__ miss_masks,
+                                                                 double* __restrict__ addends,
+                                                                 const Counters* __restrict__ ctr) {
+    const int64_t qn = static_cast<int64_t>(ctr->queue_n);
+    const int64_t n = qn < queue_cap ? qn : queue_cap;
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int4 q = __ldg(queue + e);
+        const int64_t cand = q.x, i = q.y;
+        double R[9], t[3];
+        load_rt(cand_rt + 12 * cand, R, t);
+        const V3 p = ld3(src.pos, i), ns = ld3(src.nrm, i);
+        double addend = 0.0;
+        bool inl;
+        if (q.w < 0) {
+            inl = eval_point(g, R, t, p, ns, sp, addend);
+        } else {
+            const FastRT F = load_fast(cand_fine + cand);
+            const float4 P = __ldg(src.pos32 + i);
+            const float qx = fmaf(F.r[0], P.x, fmaf(F.r[1], P.y, fmaf(F.r[2], P.z, F.t[0])));
+            const float qy = fmaf(F.r[3], P.x, fmaf(F.r[4], P.y, fmaf(F.r[5], P.z, F.t[1])));
+            const float qz = fmaf(F.r[6], P.x, fmaf(F.r[7], P.y, fmaf(F.r[8], P.z, F.t[2])));
+            inl = resolve_fine(g, R, t, F, p, ns, qx, qy, qz, q.z, q.w, sp, addend);
+        }
+        const int64_t word = cand * n_chunks + (i >> 5);
+        const uint32_t bit = 1u << (i & 31);
+        if (inl) {
+            atomicOr(inl_masks + word, bit);
+            addends[cand * ns_pad + i] = addend;
+        } else {
+            atomicOr(miss_masks + word, bit);
+        }
+    }
+}
+
 
 // Per fully scored split candidate, what the final selection needs.
 struct CandInfo {
@@ -847,6 +1053,12 @@ int split_blocks_per_sm() {
     return cached;
 }
 
+int resolve_blocks_per_sm() {
+    static int cached = 0;
+    if (!cached) cached = blocks_per_sm(reinterpret_cast<const void*>(k_score_resolve));
+    return cached;
+}
+
 }  // namespace
 
 void RunBuffers::release() {
@@ -861,8 +1073,13 @@ void RunBuffers::release() {
     pool_free(addends, stream);
     pool_free(full_list, stream);
     pool_free(cand_fast, stream);
+    pool_free(cand_fine, stream);
+    pool_free(queue, stream);
     full_list = nullptr;
     cand_fast = nullptr;
+    cand_fine = nullptr;
+    queue = nullptr;
+    queue_cap = 0;
     fast_capacity = 0;
     surv_index = nullptr;
     surv_ids = nullptr;
@@ -908,9 +1125,12 @@ cudaError_t RunBuffers::ensure(int64_t cap, int32_t score_blocks) {
 cudaError_t RunBuffers::ensure_fast(int64_t n) {
     if (n <= fast_capacity) return cudaSuccess;
     pool_free(cand_fast, stream);
+    pool_free(cand_fine, stream);
     cand_fast = nullptr;
+    cand_fine = nullptr;
     fast_capacity = 0;
     cudaError_t e = pool_alloc(&cand_fast, n * sizeof(FastRT), stream);
+    if (e == cudaSuccess) e = pool_alloc(&cand_fine, n * sizeof(FastRT), stream);
     if (e == cudaSuccess) fast_capacity = n;
     return e;
 }
@@ -927,15 +1147,23 @@ cudaError_t RunBuffers::ensure_split(int64_t ns, int64_t max_candidates) {
     pool_free(miss_masks, stream);
     pool_free(addends, stream);
     pool_free(full_list, stream);
+    pool_free(queue, stream);
     inl_masks = miss_masks = nullptr;
     addends = nullptr;
     full_list = nullptr;
+    queue = nullptr;
+    queue_cap = 0;
     split_cap = 0;
     cudaError_t e;
     if ((e = pool_alloc(&full_list, cap * 3 * sizeof(int64_t), stream)) != cudaSuccess) return e;  // CandInfo
     if ((e = pool_alloc(&inl_masks, cap * n_chunks * sizeof(uint32_t), stream)) != cudaSuccess) return e;
     if ((e = pool_alloc(&miss_masks, cap * n_chunks * sizeof(uint32_t), stream)) != cudaSuccess) return e;
     if ((e = pool_alloc(&addends, cap * ns_pad * sizeof(double), stream)) != cudaSuccess) return e;
+    // resolve queue: a quarter of all (candidate, point) pairs; overflow is
+    // evaluated inline by k_score_split
+    const int64_t qcap = cap * ns_pad / 4 > 1024 ? cap * ns_pad / 4 : 1024;
+    if ((e = pool_alloc(&queue, qcap * sizeof(int4), stream)) != cudaSuccess) return e;
+    queue_cap = qcap;
     split_cap = cap;
     split_ns_pad = ns_pad;
     return cudaSuccess;
@@ -975,11 +1203,15 @@ cudaError_t run_hypotheses_range(const SourceView& src, const double* d_tgt_pos,
                                                    rb.cand_rt, rb.counters);
     }
     if (events) cudaEventRecord(events[2], stream);
+    FastRT* cand_fine = static_cast<FastRT*>(rb.cand_fine);
     k_prep_fast<<<sm_count * 2, 128, 0, stream>>>(rb.cand_rt, -1, rb.counters, grid, sp, cand_fast);
-    k_score_split<<<split_blocks, kScoreThreads, 0, stream>>>(src, grid, sp, rb.cand_rt, cand_fast, rb.split_cap,
-                                                              n_chunks,
-                                                              rb.split_ns_pad, rb.inl_masks, rb.miss_masks,
-                                                              rb.addends, rb.counters);
+    k_prep_fast_fine<<<sm_count * 2, 128, 0, stream>>>(rb.cand_rt, rb.counters, grid, sp, cand_fine);
+    k_score_split<<<split_blocks, kScoreThreads, 0, stream>>>(src, grid, sp, rb.cand_rt, cand_fine, rb.split_cap,
+                                                              n_chunks, rb.split_ns_pad, rb.inl_masks, rb.miss_masks,
+                                                              rb.addends, rb.queue, rb.queue_cap, rb.counters);
+    k_score_resolve<<<sm_count * resolve_blocks_per_sm(), kScoreThreads, 0, stream>>>(
+        src, grid, sp, rb.cand_rt, cand_fine, n_chunks, rb.split_ns_pad, rb.queue, rb.queue_cap, rb.inl_masks,
+        rb.miss_masks, rb.addends, rb.counters);
     // candidates beyond the split capacity (normally none): streamed warp per candidate
     k_score<<<over_blocks, kScoreThreads, 0, stream>>>(src, grid, sp, rb.cand_rt, cand_fast, rb.cand_index,
                                                        rb.split_cap, -1,

@@ -47,6 +47,17 @@ struct GridView {
     // coordinates ((x - o) / cell - off) rounded to float, original index in w.
     const float4* block_f32;
     const double* pos_orig;    // 3 * npoints positions in original point order
+    // Fine lists (radius-1 grids): cells of half the size over the same box,
+    // each listing the points within fine_dmax of the fine cell's box (a
+    // superset of every query's d_max ball inside it), FP32 fine-cell
+    // coordinates ((x - o) / fcell - 2 off), original index in w. pcell is
+    // each point's cell in this grid, for the reference-window check.
+    int fnx, fny, fnz;
+    double fcell;
+    double fine_dmax;
+    const int2* fine_info;
+    const float4* fine_pts;
+    const int4* pcell;
 };
 
 struct GridStorage {
@@ -64,6 +75,10 @@ struct GridStorage {
     double* nrm_orig = nullptr;
     float4* block_f32 = nullptr;
     double* pos_orig = nullptr;
+    int64_t nfine = 0, nfine_entries = 0;
+    int2* fine_info = nullptr;
+    float4* fine_pts = nullptr;
+    int4* pcell = nullptr;
     cudaStream_t stream = nullptr;  // allocation stream
     void release();
 };
@@ -86,7 +101,8 @@ struct Counters {  // device-side, zeroed per run
     unsigned long long work_next;   // work queue head for k_score
     unsigned long long blocks_done; // last-block-done ticket
     unsigned long long n_full;      // split candidates that were fully scored
-    unsigned long long _pad[6];
+    unsigned long long queue_n;     // fine-list resolve queue length
+    unsigned long long _pad[5];
 };
 
 struct BestRec {  // per-block best, then the final record
@@ -115,6 +131,9 @@ struct RunBuffers {
     int64_t* full_list = nullptr;
     void* cand_fast = nullptr;  // per-candidate FP32 transform + guard bands
     int64_t fast_capacity = 0;
+    void* cand_fine = nullptr;  // per-candidate FastRT in fine-cell units
+    int4* queue = nullptr;      // (candidate, point, fine offset, count | -1) for k_score_resolve
+    int64_t queue_cap = 0;
     int64_t split_cap = 0;
     int64_t split_ns_pad = 0;
     cudaStream_t stream = nullptr;  // allocation stream (set by the owner)
