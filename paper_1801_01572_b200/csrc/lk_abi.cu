@@ -11,6 +11,7 @@
 #include <chrono>
 #include <climits>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -268,6 +269,12 @@ lk_status prepare_impl(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_pa
     check_cloud_ptr(tgt, "target");
     *out = nullptr;
     double t0 = now_s();
+    static const bool trace = std::getenv("LK_TRACE") != nullptr;
+    auto mark = [&](const char* what, cudaStream_t s) {
+        if (!trace) return;
+        cudaStreamSynchronize(s);
+        std::fprintf(stderr, "[lk prepare] %-18s %8.3f ms\n", what, (now_s() - t0) * 1e3);
+    };
     if (src->n == 0 || tgt->n == 0) return fail(LK_EMPTY_CLOUD, "voxel_downsample: empty cloud");
     if (!(params->leaf > 0.0)) return fail(LK_INVALID_ARGUMENT, "voxel_downsample: leaf must be positive");
     // estimate_normals (preprocess.cpp:61-96) is not part of this tier
@@ -289,6 +296,7 @@ lk_status prepare_impl(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_pa
         raw[1] = dev_upload(src->nxyz, 3 * src->n, s);
         raw[2] = dev_upload(tgt->xyz, 3 * tgt->n, s);
         raw[3] = dev_upload(tgt->nxyz, 3 * tgt->n, s);
+        mark("upload", s);
         CK(lkk::pool_alloc(&c->d_spos, 3 * src->n * sizeof(double), s));
         CK(lkk::pool_alloc(&c->d_snrm, 3 * src->n * sizeof(double), s));
         CK(lkk::pool_alloc(&c->d_tpos, 3 * tgt->n * sizeof(double), s));
@@ -296,8 +304,10 @@ lk_status prepare_impl(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_pa
         int st_s = 0, st_t = 0;
         CK(lkk::voxel_downsample(raw[0], raw[1], src->n, params->leaf, c->d_spos, c->d_snrm, &c->ns, &st_s, s));
         if (st_s == 5) throw lk::Status(LK_MISSING_NORMALS, "normals must be unit length or exactly zero");
+        mark("downsample src", s);
         CK(lkk::voxel_downsample(raw[2], raw[3], tgt->n, params->leaf, c->d_tpos, c->d_tnrm, &c->nt, &st_t, s));
         if (st_t == 5) throw lk::Status(LK_MISSING_NORMALS, "normals must be unit length or exactly zero");
+        mark("downsample tgt", s);
         if (c->ns < 4 || c->nt < 4)
             throw lk::Status(LK_TOO_FEW_POINTS, "register_global: fewer than 4 points after downsampling");
         // host copies of the downsampled clouds (download(), source magnitude bound)
@@ -321,10 +331,14 @@ lk_status prepare_impl(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_pa
         // FPFH (registration.cpp:246-247) and the feature pre-match (:248) on the device
         CK(lkk::pool_alloc(&d_sf, 33 * c->ns * sizeof(float), s));
         CK(lkk::pool_alloc(&d_tf, 33 * c->nt * sizeof(float), s));
+        mark("d2h downsampled", s);
         CK(lkk::compute_fpfh(c->d_spos, c->d_snrm, c->ns, params->feature_radius, d_sf, s));
+        mark("fpfh src", s);
         CK(lkk::compute_fpfh(c->d_tpos, c->d_tnrm, c->nt, params->feature_radius, d_tf, s));
+        mark("fpfh tgt", s);
         CK(lkk::pool_alloc(&c->d_cache, c->ns * sizeof(int32_t), s));
         CK(lkk::feature_nn(d_sf, c->ns, d_tf, c->nt, c->d_cache, s));
+        mark("feature nn", s);
         c->h_cache.resize(c->ns);
         c->h_sfeat.resize(33 * c->ns);
         c->h_tfeat.resize(33 * c->nt);
@@ -332,8 +346,10 @@ lk_status prepare_impl(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_pa
         CK(cudaMemcpyAsync(c->h_sfeat.data(), d_sf, 33 * c->ns * sizeof(float), cudaMemcpyDeviceToHost, s));
         CK(cudaMemcpyAsync(c->h_tfeat.data(), d_tf, 33 * c->nt * sizeof(float), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
+        mark("d2h cache/features", s);
         cleanup();
         ctx_finish(c, *params);  // EvalGrid on the device (registration.cpp:249)
+        mark("eval grid", s);
     } catch (...) {
         cleanup();
         delete c;

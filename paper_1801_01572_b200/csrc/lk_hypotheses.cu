@@ -577,55 +577,70 @@ __global__ void k_prep_fast_fine(const double* __restrict__ cand_rt, const Count
 
 // Exact resolution of one query over its fine list: FP32 top-3 with the guard
 // band, FP64 d2 for every entry that can be the minimum, and the reference's
-// window (the winner's EvalGrid cell within +-1 of y's, computed by division
-// exactly as registration.cpp:167-169). Any doubt falls back to eval_point.
-__device__ bool resolve_fine(const GridView& g, const double* R, const double* t, const FastRT& F, V3 p, V3 ns,
-                             float qx, float qy, float qz, int32_t off, int32_t cnt, const ScoreParams& sp,
-                             double& addend) {
+// window (the winner's EvalGrid cell within +-1 of y's, registration.cpp:167-169).
+// y's EvalGrid cell is its certain fine cell halved: (y - o) / fcell is exactly
+// 2 (y - o) / cell in FP64, so floor of the one is twice-or-one-more the floor
+// of the other. A winner outside the window (rounding at the edge) falls back
+// to eval_point.
+// Out of line so its registers do not count against the callers' occupancy;
+// everything is reloaded from global memory (rt = the candidate's 12 doubles).
+__device__ __noinline__ bool eval_point_slow(const GridView& g, const double* rt, const SourceView& src, int64_t i,
+                                             const ScoreParams& sp, double* addend) {
+    double R[9], t[3];
+    load_rt(rt, R, t);
+    return eval_point(g, R, t, ld3(src.pos, i), ld3(src.nrm, i), sp, *addend);
+}
+
+__device__ __forceinline__ void top3(float d2, int32_t o, float& f1, float& f2, float& f3, int32_t& o1, int32_t& o2) {
+    if (d2 < f1) {
+        f3 = f2;
+        f2 = f1;
+        o2 = o1;
+        f1 = d2;
+        o1 = o;
+    } else if (d2 < f2) {
+        f3 = f2;
+        f2 = d2;
+        o2 = o;
+    } else if (d2 < f3) {
+        f3 = d2;
+    }
+}
+
+__device__ __forceinline__ bool resolve_fine(const GridView& g, const double* rt, const double* R, const double* t,
+                                             const FastRT& F, const SourceView& src, int64_t i, V3 p, V3 ns,
+                                             float qx, float qy, float qz, int32_t off, int32_t cnt,
+                                             const ScoreParams& sp, double& addend) {
     const float inf = __int_as_float(0x7f800000);
     float f1 = inf, f2 = inf, f3 = inf;
     int32_t o1 = -1, o2 = -1;
-    for (int32_t e = off; e < off + cnt; ++e) {
-        const float4 E = __ldg(g.fine_pts + e);
-        const float dx = qx - E.x, dy = qy - E.y, dz = qz - E.z;
-        const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-        const int32_t o = __float_as_int(E.w);
-        if (d2 < f1) {
-            f3 = f2;
-            f2 = f1;
-            o2 = o1;
-            f1 = d2;
-            o1 = o;
-        } else if (d2 < f2) {
-            f3 = f2;
-            f2 = d2;
-            o2 = o;
-        } else if (d2 < f3) {
-            f3 = d2;
-        }
+    int32_t e = off;
+    const int32_t end = off + cnt;
+    for (; e + 1 < end; e += 2) {  // two independent loads in flight
+        const float4 A = __ldg(g.fine_pts + e), B = __ldg(g.fine_pts + e + 1);
+        const float ax = qx - A.x, ay = qy - A.y, az = qz - A.z;
+        const float bx = qx - B.x, by = qy - B.y, bz = qz - B.z;
+        top3(fmaf(ax, ax, fmaf(ay, ay, az * az)), __float_as_int(A.w), f1, f2, f3, o1, o2);
+        top3(fmaf(bx, bx, fmaf(by, by, bz * bz)), __float_as_int(B.w), f1, f2, f3, o1, o2);
+    }
+    if (e < end) {
+        const float4 A = __ldg(g.fine_pts + e);
+        const float ax = qx - A.x, ay = qy - A.y, az = qz - A.z;
+        top3(fmaf(ax, ax, fmaf(ay, ay, az * az)), __float_as_int(A.w), f1, f2, f3, o1, o2);
     }
     const float band = F.band;
-    const float thr = F.pad;
-    if (f1 > thr + band) return false;  // nothing within d_max of y
+    if (f1 > F.pad + band) return false;  // nothing within d_max of y
+    const int cx = static_cast<int>(floorf(qx)) >> 1, cy = static_cast<int>(floorf(qy)) >> 1,
+              cz = static_cast<int>(floorf(qz)) >> 1;
     const V3 y = xform(R, t, p);
-    // y's cell in the reference grid (division, as the reference)
-    const double cx = floor((y.x - g.ox) / g.cell) - static_cast<double>(g.offx);
-    const double cy = floor((y.y - g.oy) / g.cell) - static_cast<double>(g.offy);
-    const double cz = floor((y.z - g.oz) / g.cell) - static_cast<double>(g.offz);
-    if (!(cx >= 0.0 && cy >= 0.0 && cz >= 0.0 && cx < g.nx && cy < g.ny && cz < g.nz)) return false;
-    const int ix = static_cast<int>(cx), iy = static_cast<int>(cy), iz = static_cast<int>(cz);
-    auto in_window = [&](int32_t o) {
-        const int4 c = __ldg(g.pcell + o);
-        return abs(c.x - ix) <= 1 && abs(c.y - iy) <= 1 && abs(c.z - iz) <= 1;
-    };
     double best_d2 = __longlong_as_double(0x7ff0000000000000ll);
     int32_t best_orig = INT32_MAX;
-    const float lim = f1 + 2.0f * band;
     bool doubt = false;
     auto consider = [&](int32_t o) {
         const double d2 = sqnorm(sub(ld3(g.pos_orig, o), y));
         if (d2 > sp.d2_max) return;
-        if (!in_window(o)) {
+        const int4 c = __ldg(g.pcell + o);
+        if (abs(c.x - cx) > 1 || abs(c.y - cy) > 1 || abs(c.z - cz) > 1) {
             doubt = true;
             return;
         }
@@ -634,9 +649,10 @@ __device__ bool resolve_fine(const GridView& g, const double* R, const double* t
             best_orig = o;
         }
     };
+    const float lim = f1 + 2.0f * band;
     if (f3 <= lim) {
-        for (int32_t e = off; e < off + cnt; ++e) {
-            const float4 E = __ldg(g.fine_pts + e);
+        for (int32_t k = off; k < end; ++k) {
+            const float4 E = __ldg(g.fine_pts + k);
             const float dx = qx - E.x, dy = qy - E.y, dz = qz - E.z;
             if (fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= lim) consider(__float_as_int(E.w));
         }
@@ -644,7 +660,7 @@ __device__ bool resolve_fine(const GridView& g, const double* R, const double* t
         consider(o1);
         if (f2 <= lim) consider(o2);
     }
-    if (doubt) return eval_point(g, R, t, p, ns, sp, addend);  // rounding at the window edge
+    if (doubt) return eval_point_slow(g, rt, src, i, sp, &addend);
     if (best_orig == INT32_MAX) return false;
     const V3 nt = ld3(g.nrm_orig, best_orig);
     if (is_zero(ns) || is_zero(nt)) return false;
@@ -658,30 +674,44 @@ __device__ bool resolve_fine(const GridView& g, const double* R, const double* t
     return true;
 }
 
+// The resolve queue is split into kQueueParts partitions, each with its own
+// counter on its own 128-byte line, so the warps' reservations spread over L2
+// slices instead of serialising on one address.
+constexpr int kQueueParts = 64;
+constexpr int kQueueStride = 16;  // u64 per counter line
+
 // Pass A: (candidate, chunk) items, chunk-major so neighbouring warps share
 // the source chunk in L1. Each lane locates its point's fine cell in FP32:
 // certain misses are settled here; points with a non-empty fine list (or a
 // coordinate near a fine-cell face) go to the dense queue for pass B, so no
 // lane idles through another lane's scan. No early exit: every point of a
 // split candidate is evaluated; k_score_exits decides from the ballots.
-__global__ void __launch_bounds__(kScoreThreads) k_score_split(SourceView src, GridView g, ScoreParams sp,
+__global__ void __launch_bounds__(kScoreThreads, 4) k_score_split(SourceView src, const __grid_constant__ GridView g,
+    const __grid_constant__ ScoreParams sp,
                                                                const double* __restrict__ cand_rt,
                                                                const FastRT* __restrict__ cand_fine, int64_t cap,
                                                                int32_t n_chunks, int64_t ns_pad,
                                                                uint32_t* __restrict__ inl_masks,
                                                                uint32_t* __restrict__ miss_masks,
                                                                double* __restrict__ addends, int4* __restrict__ queue,
-                                                               int64_t queue_cap, Counters* __restrict__ ctr) {
+                                                               int64_t part_cap,
+                                                               unsigned long long* __restrict__ part_count,
+                                                               const Counters* __restrict__ ctr) {
     const int lane = threadIdx.x & 31;
     const int64_t n_all = static_cast<int64_t>(ctr->n_candidates);
     const int64_t n_cand = n_all < cap ? n_all : cap;
+    if (n_cand == 0) return;
     const int64_t total = n_cand * n_chunks;
     const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
     const int64_t ns = src.n;
-    for (int64_t w = blockIdx.x * static_cast<int64_t>(blockDim.x >> 5) + (threadIdx.x >> 5); w < total;
-         w += nwarps) {
-        const int64_t chunk = w / n_cand;
-        const int64_t cand = w - chunk * n_cand;
+    const int part = blockIdx.x % kQueueParts;
+    unsigned long long* counter = part_count + part * kQueueStride;
+    int4* pq = queue + part * part_cap;
+    int64_t w = blockIdx.x * static_cast<int64_t>(blockDim.x >> 5) + (threadIdx.x >> 5);
+    // (chunk, cand) of w, advanced without dividing in the loop
+    int64_t chunk = w / n_cand, cand = w - (w / n_cand) * n_cand;
+    const int64_t dq = nwarps / n_cand, dr = nwarps - dq * n_cand;
+    for (; w < total; w += nwarps) {
         const FastRT F = load_fast(cand_fine + cand);
         const int64_t i = chunk * 32 + lane;
         const bool valid = i < ns;
@@ -713,17 +743,15 @@ __global__ void __launch_bounds__(kScoreThreads) k_score_split(SourceView src, G
             }
         }
         const bool need = state != 0;
-        const unsigned long long slot = warp_atomic_add(&ctr->queue_n, need);
+        const unsigned long long slot = warp_atomic_add(counter, need);
         bool inl = false, inline_done = false;
         double addend = 0.0;
         if (need) {
-            if (static_cast<int64_t>(slot) < queue_cap) {
-                queue[slot] = make_int4(static_cast<int32_t>(cand), static_cast<int32_t>(i), bi.x,
-                                        state == 1 ? -1 : bi.y);
-            } else {  // queue full: evaluate here (exact, slow, never on the bench inputs)
-                double R[9], t[3];
-                load_rt(cand_rt + 12 * cand, R, t);
-                inl = eval_point(g, R, t, ld3(src.pos, i), ld3(src.nrm, i), sp, addend);
+            if (static_cast<int64_t>(slot) < part_cap) {
+                pq[slot] = make_int4(static_cast<int32_t>(cand), static_cast<int32_t>(i), bi.x,
+                                     state == 1 ? -1 : bi.y);
+            } else {  // partition full: evaluate here (exact, slow, never on the bench inputs)
+                inl = eval_point_slow(g, cand_rt + 12 * cand, src, i, sp, &addend);
                 inline_done = true;
             }
         }
@@ -734,40 +762,72 @@ __global__ void __launch_bounds__(kScoreThreads) k_score_split(SourceView src, G
             miss_masks[cand * n_chunks + chunk] = mm;
         }
         if (inl) addends[cand * ns_pad + i] = addend;
+        cand += dr;
+        chunk += dq;
+        if (cand >= n_cand) {
+            cand -= n_cand;
+            chunk += 1;
+        }
     }
 }
 
-// Pass B: thread per queued (candidate, point): the fine-list scan and the
-// exact decisions; results are OR-ed into the chunk ballots.
-__global__ void __launch_bounds__(kScoreThreads) k_score_resolve(SourceView src, GridView g, ScoreParams sp,
+// Pass B: thread per queued (candidate, point) over the concatenated
+// partitions: the fine-list scan and the exact decisions; results are OR-ed
+// into the chunk ballots.
+__global__ void __launch_bounds__(kScoreThreads, 4) k_score_resolve(SourceView src, const __grid_constant__ GridView g,
+    const __grid_constant__ ScoreParams sp,
                                                                  const double* __restrict__ cand_rt,
                                                                  const FastRT* __restrict__ cand_fine,
                                                                  int32_t n_chunks, int64_t ns_pad,
-                                                                 const int4* __restrict__ queue, int64_t queue_cap,
+                                                                 const int4* __restrict__ queue, int64_t part_cap,
+                                                                 const unsigned long long* __restrict__ part_count,
                                                                  uint32_t* __restrict__ inl_masks,
                                                                  uint32_t* __restrict__ miss_masks,
-                                                                 double* __restrict__ addends,
-                                                                 const Counters* __restrict__ ctr) {
-    const int64_t qn = static_cast<int64_t>(ctr->queue_n);
-    const int64_t n = qn < queue_cap ? qn : queue_cap;
+                                                                 double* __restrict__ addends) {
+    __shared__ int64_t s_start[kQueueParts + 1];
+    if (threadIdx.x < 32) {
+        // inclusive scan of the clamped partition counts, two per lane
+        const int lane = threadIdx.x;
+        int64_t a = static_cast<int64_t>(part_count[(2 * lane) * kQueueStride]);
+        int64_t b = static_cast<int64_t>(part_count[(2 * lane + 1) * kQueueStride]);
+        a = a < part_cap ? a : part_cap;
+        b = b < part_cap ? b : part_cap;
+        int64_t v = a + b;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t u = __shfl_up_sync(kFull, v, o);
+            if (lane >= o) v += u;
+        }
+        s_start[2 * lane + 1] = v - b;
+        s_start[2 * lane + 2] = v;
+        if (lane == 0) s_start[0] = 0;
+    }
+    __syncthreads();
+    const int64_t n = s_start[kQueueParts];
     for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
          e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int4 q = __ldg(queue + e);
+        int lo = 0, hi = kQueueParts;  // s_start[lo] <= e < s_start[hi]
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (s_start[mid] <= e) lo = mid;
+            else hi = mid;
+        }
+        const int4 q = __ldg(queue + lo * part_cap + (e - s_start[lo]));
         const int64_t cand = q.x, i = q.y;
-        double R[9], t[3];
-        load_rt(cand_rt + 12 * cand, R, t);
-        const V3 p = ld3(src.pos, i), ns = ld3(src.nrm, i);
         double addend = 0.0;
         bool inl;
         if (q.w < 0) {
-            inl = eval_point(g, R, t, p, ns, sp, addend);
+            inl = eval_point_slow(g, cand_rt + 12 * cand, src, i, sp, &addend);
         } else {
+            double R[9], t[3];
+            load_rt(cand_rt + 12 * cand, R, t);
+            const V3 p = ld3(src.pos, i), ns = ld3(src.nrm, i);
             const FastRT F = load_fast(cand_fine + cand);
             const float4 P = __ldg(src.pos32 + i);
             const float qx = fmaf(F.r[0], P.x, fmaf(F.r[1], P.y, fmaf(F.r[2], P.z, F.t[0])));
             const float qy = fmaf(F.r[3], P.x, fmaf(F.r[4], P.y, fmaf(F.r[5], P.z, F.t[1])));
             const float qz = fmaf(F.r[6], P.x, fmaf(F.r[7], P.y, fmaf(F.r[8], P.z, F.t[2])));
-            inl = resolve_fine(g, R, t, F, p, ns, qx, qy, qz, q.z, q.w, sp, addend);
+            inl = resolve_fine(g, cand_rt + 12 * cand, R, t, F, src, i, p, ns, qx, qy, qz, q.z, q.w, sp, addend);
         }
         const int64_t word = cand * n_chunks + (i >> 5);
         const uint32_t bit = 1u << (i & 31);
@@ -1075,6 +1135,8 @@ void RunBuffers::release() {
     pool_free(cand_fast, stream);
     pool_free(cand_fine, stream);
     pool_free(queue, stream);
+    pool_free(queue_counts, stream);
+    queue_counts = nullptr;
     full_list = nullptr;
     cand_fast = nullptr;
     cand_fine = nullptr;
@@ -1161,8 +1223,12 @@ cudaError_t RunBuffers::ensure_split(int64_t ns, int64_t max_candidates) {
     if ((e = pool_alloc(&addends, cap * ns_pad * sizeof(double), stream)) != cudaSuccess) return e;
     // resolve queue: a quarter of all (candidate, point) pairs; overflow is
     // evaluated inline by k_score_split
-    const int64_t qcap = cap * ns_pad / 4 > 1024 ? cap * ns_pad / 4 : 1024;
+    const int64_t qcap = (cap * ns_pad * 3 / 8 > 1024 ? cap * ns_pad * 3 / 8 : 1024) / kQueueParts * kQueueParts;
     if ((e = pool_alloc(&queue, qcap * sizeof(int4), stream)) != cudaSuccess) return e;
+    if (!queue_counts &&
+        (e = pool_alloc(&queue_counts, kQueueParts * kQueueStride * sizeof(unsigned long long), stream)) !=
+            cudaSuccess)
+        return e;
     queue_cap = qcap;
     split_cap = cap;
     split_ns_pad = ns_pad;
@@ -1187,6 +1253,9 @@ cudaError_t run_hypotheses_range(const SourceView& src, const double* d_tgt_pos,
     if ((e = rb.ensure_fast(count > 0 ? count : 1)) != cudaSuccess) return e;
     FastRT* cand_fast = static_cast<FastRT*>(rb.cand_fast);
     if ((e = cudaMemsetAsync(rb.counters, 0, sizeof(Counters), stream)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(rb.queue_counts, 0, kQueueParts * kQueueStride * sizeof(unsigned long long), stream)) !=
+        cudaSuccess)
+        return e;
     const uint32_t ns = static_cast<uint32_t>(src.n);
     const uint32_t thresh = static_cast<uint32_t>(0x100000000ull % ns);
     const int32_t n_chunks = static_cast<int32_t>((src.n + 31) / 32);
@@ -1206,12 +1275,14 @@ cudaError_t run_hypotheses_range(const SourceView& src, const double* d_tgt_pos,
     FastRT* cand_fine = static_cast<FastRT*>(rb.cand_fine);
     k_prep_fast<<<sm_count * 2, 128, 0, stream>>>(rb.cand_rt, -1, rb.counters, grid, sp, cand_fast);
     k_prep_fast_fine<<<sm_count * 2, 128, 0, stream>>>(rb.cand_rt, rb.counters, grid, sp, cand_fine);
+    const int64_t part_cap = rb.queue_cap / kQueueParts;
     k_score_split<<<split_blocks, kScoreThreads, 0, stream>>>(src, grid, sp, rb.cand_rt, cand_fine, rb.split_cap,
                                                               n_chunks, rb.split_ns_pad, rb.inl_masks, rb.miss_masks,
-                                                              rb.addends, rb.queue, rb.queue_cap, rb.counters);
+                                                              rb.addends, rb.queue, part_cap, rb.queue_counts,
+                                                              rb.counters);
     k_score_resolve<<<sm_count * resolve_blocks_per_sm(), kScoreThreads, 0, stream>>>(
-        src, grid, sp, rb.cand_rt, cand_fine, n_chunks, rb.split_ns_pad, rb.queue, rb.queue_cap, rb.inl_masks,
-        rb.miss_masks, rb.addends, rb.counters);
+        src, grid, sp, rb.cand_rt, cand_fine, n_chunks, rb.split_ns_pad, rb.queue, part_cap, rb.queue_counts,
+        rb.inl_masks, rb.miss_masks, rb.addends);
     // candidates beyond the split capacity (normally none): streamed warp per candidate
     k_score<<<over_blocks, kScoreThreads, 0, stream>>>(src, grid, sp, rb.cand_rt, cand_fast, rb.cand_index,
                                                        rb.split_cap, -1,

@@ -101,8 +101,7 @@ struct Counters {  // device-side, zeroed per run
     unsigned long long work_next;   // work queue head for k_score
     unsigned long long blocks_done; // last-block-done ticket
     unsigned long long n_full;      // split candidates that were fully scored
-    unsigned long long queue_n;     // fine-list resolve queue length
-    unsigned long long _pad[5];
+    unsigned long long _pad[6];
 };
 
 struct BestRec {  // per-block best, then the final record
@@ -134,6 +133,7 @@ struct RunBuffers {
     void* cand_fine = nullptr;  // per-candidate FastRT in fine-cell units
     int4* queue = nullptr;      // (candidate, point, fine offset, count | -1) for k_score_resolve
     int64_t queue_cap = 0;
+    unsigned long long* queue_counts = nullptr;  // per-partition queue lengths
     int64_t split_cap = 0;
     int64_t split_ns_pad = 0;
     cudaStream_t stream = nullptr;  // allocation stream (set by the owner)
