@@ -16,6 +16,10 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
+#include <condition_variable>
+#include <functional>
+#include <exception>
 #include <vector>
 
 #include "../../include/loopkit_b200.h"
@@ -81,6 +85,98 @@ int select_device(int32_t device) {
             }
         });
     return dev;
+}
+
+// Streams are recycled across contexts (one context per registration is the
+// common pattern): creating and destroying two streams per registration costs
+// more than the small clouds' kernels, and fresh streams defeat the memory
+// pool's same-stream reuse.
+std::mutex g_stream_mu;
+std::vector<std::pair<int, cudaStream_t>> g_free_streams;
+
+cudaStream_t acquire_stream(int dev) {
+    {
+        std::lock_guard<std::mutex> lock(g_stream_mu);
+        for (size_t k = g_free_streams.size(); k-- > 0;)
+            if (g_free_streams[k].first == dev) {
+                cudaStream_t s = g_free_streams[k].second;
+                g_free_streams.erase(g_free_streams.begin() + static_cast<std::ptrdiff_t>(k));
+                return s;
+            }
+    }
+    cudaStream_t s = nullptr;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    return s;
+}
+
+void release_stream(int dev, cudaStream_t s) {
+    if (!s) return;
+    std::lock_guard<std::mutex> lock(g_stream_mu);
+    g_free_streams.emplace_back(dev, s);
+}
+
+// Host worker threads, recycled: prepare_registration drives the target side
+// on one of these while the caller's thread drives the source side. Recycling
+// keeps thread start-up (and the OpenMP team a thread builds on first use)
+// off the per-registration path.
+class Worker {
+  public:
+    Worker() : th_([this] { loop(); }) { th_.detach(); }
+    void post(std::function<void()> f) {
+        std::lock_guard<std::mutex> lock(mu_);
+        job_ = std::move(f);
+        busy_ = true;
+        cv_.notify_all();
+    }
+    void wait() {
+        std::unique_lock<std::mutex> lock(mu_);
+        cv_.wait(lock, [this] { return !busy_; });
+    }
+
+  private:
+    void loop() {
+        std::unique_lock<std::mutex> lock(mu_);
+        while (true) {
+            cv_.wait(lock, [this] { return busy_ && job_; });
+            std::function<void()> f = std::move(job_);
+            job_ = nullptr;
+            lock.unlock();
+            f();
+            lock.lock();
+            busy_ = false;
+            cv_.notify_all();
+        }
+    }
+    std::mutex mu_;
+    std::condition_variable cv_;
+    std::function<void()> job_;
+    bool busy_ = false;
+    std::thread th_;
+};
+
+std::mutex g_worker_mu;
+std::vector<Worker*> g_free_workers;
+
+Worker* acquire_worker() {
+    {
+        std::lock_guard<std::mutex> lock(g_worker_mu);
+        if (!g_free_workers.empty()) {
+            Worker* w = g_free_workers.back();
+            g_free_workers.pop_back();
+            return w;
+        }
+    }
+    return new Worker();  // lives for the process
+}
+
+void release_worker(Worker* w) {
+    std::lock_guard<std::mutex> lock(g_worker_mu);
+    g_free_workers.push_back(w);
+}
+
+bool trace_on() {
+    static const bool on = std::getenv("LK_TRACE") != nullptr;
+    return on;
 }
 
 int sm_count_of(int dev) {
@@ -182,11 +278,10 @@ struct lk_reg_ctx {
     int sm_count = 0;
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
+    cudaStream_t aux_stream = nullptr;  // target-side preparation, concurrent with the source side
     int64_t ns = 0, nt = 0;
-    std::vector<double> h_spos, h_snrm, h_tpos, h_tnrm;
-    std::vector<int32_t> h_cache;
-    std::vector<float> h_sfeat, h_tfeat;
     double *d_spos = nullptr, *d_snrm = nullptr, *d_tpos = nullptr, *d_tnrm = nullptr;
+    float *d_sfeat = nullptr, *d_tfeat = nullptr;  // FPFH (prepare_registration only)
     float4* d_spos32 = nullptr;  // FP32 copy of the source for the guard-band scan
     double src_max_norm = 0.0;
     int32_t* d_cache = nullptr;
@@ -223,29 +318,27 @@ struct lk_reg_ctx {
         lkk::pool_free(d_tpos, s);
         lkk::pool_free(d_tnrm, s);
         lkk::pool_free(d_cache, s);
+        lkk::pool_free(d_sfeat, s);
+        lkk::pool_free(d_tfeat, s);
         grid.release();
         rb.release();
         lkk::pool_free(d_record, s);
-        if (own_stream) cudaStreamDestroy(own_stream);
+        if (own_stream) cudaStreamSynchronize(own_stream);
+        if (aux_stream) cudaStreamSynchronize(aux_stream);
+        release_stream(device, own_stream);
+        release_stream(device, aux_stream);
     }
 };
 
 namespace {
 
-// Uploads whatever of the prepared clouds + cache is not on the device yet and
-// builds the EvalGrid on the device.
-void ctx_finish(lk_reg_ctx* c, const lk_reg_params& p) {
+// Source-side tail shared by both constructors: the FP32 source copy, |p|max
+// bound for the guard bands and the record buffer.
+void ctx_finish_source(lk_reg_ctx* c) {
     cudaStream_t s = c->stream;
-    if (!c->d_spos) c->d_spos = dev_upload(c->h_spos.data(), c->h_spos.size(), s);
-    if (!c->d_snrm) c->d_snrm = dev_upload(c->h_snrm.data(), c->h_snrm.size(), s);
-    if (!c->d_tpos) c->d_tpos = dev_upload(c->h_tpos.data(), c->h_tpos.size(), s);
-    if (!c->d_tnrm) c->d_tnrm = dev_upload(c->h_tnrm.data(), c->h_tnrm.size(), s);
-    if (!c->d_cache) c->d_cache = dev_upload(c->h_cache.data(), c->h_cache.size(), s);
     CK(lkk::pool_alloc(&c->d_spos32, std::max<int64_t>(c->ns, 1) * sizeof(float4), s));
     CK(lkk::make_source32(c->d_spos, c->ns, c->d_spos32, s));
-    c->src_max_norm = max_norm(c->h_spos.data(), c->ns);
     CK(lkk::pool_alloc(&c->d_record, sizeof(lk_reg_record), s));
-    CK(lkk::build_grid(c->grid, 0, c->d_tpos, c->d_tnrm, c->nt, p.d_max, p.d_max, s));
 }
 
 lk_reg_ctx* ctx_new(int32_t device) {
@@ -253,7 +346,8 @@ lk_reg_ctx* ctx_new(int32_t device) {
     try {
         c->device = select_device(device);
         c->sm_count = sm_count_of(c->device);
-        CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+        c->own_stream = acquire_stream(c->device);
+        c->aux_stream = acquire_stream(c->device);
         c->stream = c->own_stream;
         c->rb.stream = c->own_stream;
     } catch (...) {
@@ -263,18 +357,64 @@ lk_reg_ctx* ctx_new(int32_t device) {
     return c;
 }
 
+// One cloud through voxel_downsample and FPFH on its own stream
+// (registration.cpp:226-228, 246-247); the target side also builds the
+// EvalGrid (:249). Runs on a host thread of its own; errors are kept, not
+// thrown, so both sides finish before the reference's check order decides.
+struct CloudSide {
+    const lk_cloud* in = nullptr;
+    cudaStream_t s = nullptr;
+    double *raw_pos = nullptr, *raw_nrm = nullptr;
+    double *pos = nullptr, *nrm = nullptr;
+    float* feat = nullptr;
+    int64_t n = 0;
+    int status = 0;  // 5: invalid normals
+    int64_t usable = 0;
+    double max_norm = 0.0;
+    std::exception_ptr err;
+};
+
+void prepare_side(CloudSide& cs, double feature_radius, double leaf, lkk::GridStorage* grid, double d_max,
+                  int device, double t0, const char* tag) {
+    auto mark = [&](const char* what) {
+        if (!trace_on()) return;
+        cudaStreamSynchronize(cs.s);
+        std::fprintf(stderr, "[lk prepare %s] %-14s %8.3f ms\n", tag, what, (now_s() - t0) * 1e3);
+    };
+    try {
+        CK(cudaSetDevice(device));
+        const int64_t n = cs.in->n;
+        cs.raw_pos = dev_upload(cs.in->xyz, 3 * n, cs.s);
+        cs.raw_nrm = dev_upload(cs.in->nxyz, 3 * n, cs.s);
+        mark("upload");
+        CK(lkk::pool_alloc(&cs.pos, 3 * n * sizeof(double), cs.s));
+        CK(lkk::pool_alloc(&cs.nrm, 3 * n * sizeof(double), cs.s));
+        CK(lkk::voxel_downsample(cs.raw_pos, cs.raw_nrm, n, leaf, cs.pos, cs.nrm, &cs.n, &cs.status, cs.s));
+        lkk::pool_free(cs.raw_pos, cs.s);
+        lkk::pool_free(cs.raw_nrm, cs.s);
+        cs.raw_pos = cs.raw_nrm = nullptr;
+        mark("downsample");
+        if (cs.status != 0 || cs.n < 4) return;
+        CK(lkk::cloud_stats(cs.pos, cs.nrm, cs.n, &cs.usable, &cs.max_norm, cs.s));
+        if (cs.usable < 4) return;
+        CK(lkk::pool_alloc(&cs.feat, 33 * cs.n * sizeof(float), cs.s));
+        CK(lkk::compute_fpfh(cs.pos, cs.nrm, cs.n, feature_radius, cs.feat, cs.s));
+        mark("fpfh");
+        if (grid) {
+            CK(lkk::build_grid(*grid, 0, cs.pos, cs.nrm, cs.n, d_max, d_max, cs.s));
+            mark("eval grid");
+        }
+    } catch (...) {
+        cs.err = std::current_exception();
+    }
+}
+
 lk_status prepare_impl(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_params* params, lk_reg_ctx** out) {
     if (!params || !out) return fail(LK_INVALID_ARGUMENT, "null argument");
     check_cloud_ptr(src, "source");
     check_cloud_ptr(tgt, "target");
     *out = nullptr;
     double t0 = now_s();
-    static const bool trace = std::getenv("LK_TRACE") != nullptr;
-    auto mark = [&](const char* what, cudaStream_t s) {
-        if (!trace) return;
-        cudaStreamSynchronize(s);
-        std::fprintf(stderr, "[lk prepare] %-18s %8.3f ms\n", what, (now_s() - t0) * 1e3);
-    };
     if (src->n == 0 || tgt->n == 0) return fail(LK_EMPTY_CLOUD, "voxel_downsample: empty cloud");
     if (!(params->leaf > 0.0)) return fail(LK_INVALID_ARGUMENT, "voxel_downsample: leaf must be positive");
     // estimate_normals (preprocess.cpp:61-96) is not part of this tier
@@ -282,76 +422,56 @@ lk_status prepare_impl(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_pa
         return fail(LK_MISSING_NORMALS,
                     "register_global: inputs without normals need estimate_normals (not in this tier)");
     lk_reg_ctx* c = ctx_new(params->device);
-    double* raw[4] = {nullptr, nullptr, nullptr, nullptr};
-    float *d_sf = nullptr, *d_tf = nullptr;
-    auto cleanup = [&] {
-        for (double* p : raw) lkk::pool_free(p, c->stream);
-        lkk::pool_free(d_sf, c->stream);
-        lkk::pool_free(d_tf, c->stream);
+    CloudSide S, T;
+    S.in = src;
+    S.s = c->own_stream;
+    T.in = tgt;
+    T.s = c->aux_stream;
+    auto drop = [&](CloudSide& cs) {
+        lkk::pool_free(cs.raw_pos, cs.s);
+        lkk::pool_free(cs.raw_nrm, cs.s);
     };
     try {
-        cudaStream_t s = c->stream;
-        // H2D of the raw clouds, then voxel_downsample on the device (registration.cpp:226-228)
-        raw[0] = dev_upload(src->xyz, 3 * src->n, s);
-        raw[1] = dev_upload(src->nxyz, 3 * src->n, s);
-        raw[2] = dev_upload(tgt->xyz, 3 * tgt->n, s);
-        raw[3] = dev_upload(tgt->nxyz, 3 * tgt->n, s);
-        mark("upload", s);
-        CK(lkk::pool_alloc(&c->d_spos, 3 * src->n * sizeof(double), s));
-        CK(lkk::pool_alloc(&c->d_snrm, 3 * src->n * sizeof(double), s));
-        CK(lkk::pool_alloc(&c->d_tpos, 3 * tgt->n * sizeof(double), s));
-        CK(lkk::pool_alloc(&c->d_tnrm, 3 * tgt->n * sizeof(double), s));
-        int st_s = 0, st_t = 0;
-        CK(lkk::voxel_downsample(raw[0], raw[1], src->n, params->leaf, c->d_spos, c->d_snrm, &c->ns, &st_s, s));
-        if (st_s == 5) throw lk::Status(LK_MISSING_NORMALS, "normals must be unit length or exactly zero");
-        mark("downsample src", s);
-        CK(lkk::voxel_downsample(raw[2], raw[3], tgt->n, params->leaf, c->d_tpos, c->d_tnrm, &c->nt, &st_t, s));
-        if (st_t == 5) throw lk::Status(LK_MISSING_NORMALS, "normals must be unit length or exactly zero");
-        mark("downsample tgt", s);
+        // the two clouds are independent until the feature match: the target
+        // side (H2D, downsample, FPFH, EvalGrid) runs on a second host thread
+        // and stream while this thread does the source side
+        Worker* worker = acquire_worker();
+        const double fr = params->feature_radius, leaf = params->leaf, dm = params->d_max;
+        const int dev = c->device;
+        lkk::GridStorage* grid = &c->grid;
+        worker->post([&T, fr, leaf, grid, dm, dev, t0] { prepare_side(T, fr, leaf, grid, dm, dev, t0, "tgt"); });
+        prepare_side(S, fr, leaf, nullptr, 0.0, dev, t0, "src");
+        worker->wait();
+        release_worker(worker);
+        if (trace_on()) std::fprintf(stderr, "[lk prepare] joined %8.3f ms\n", (now_s() - t0) * 1e3);
+        c->d_spos = S.pos;
+        c->d_snrm = S.nrm;
+        c->d_tpos = T.pos;
+        c->d_tnrm = T.nrm;
+        c->d_sfeat = S.feat;
+        c->d_tfeat = T.feat;
+        c->ns = S.n;
+        c->nt = T.n;
+        c->src_max_norm = S.max_norm;
+        if (S.err) std::rethrow_exception(S.err);
+        if (T.err) std::rethrow_exception(T.err);
+        // the reference's check order (registration.cpp:226-245)
+        if (S.status == 5 || T.status == 5)
+            throw lk::Status(LK_MISSING_NORMALS, "normals must be unit length or exactly zero");
         if (c->ns < 4 || c->nt < 4)
             throw lk::Status(LK_TOO_FEW_POINTS, "register_global: fewer than 4 points after downsampling");
-        // host copies of the downsampled clouds (download(), source magnitude bound)
-        c->h_spos.resize(3 * c->ns);
-        c->h_snrm.resize(3 * c->ns);
-        c->h_tpos.resize(3 * c->nt);
-        c->h_tnrm.resize(3 * c->nt);
-        CK(cudaMemcpyAsync(c->h_spos.data(), c->d_spos, 3 * c->ns * sizeof(double), cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(c->h_snrm.data(), c->d_snrm, 3 * c->ns * sizeof(double), cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(c->h_tpos.data(), c->d_tpos, 3 * c->nt * sizeof(double), cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(c->h_tnrm.data(), c->d_tnrm, 3 * c->nt * sizeof(double), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        auto usable = [](const std::vector<double>& nrm) {
-            size_t k = 0;
-            for (size_t i = 0; i + 2 < nrm.size(); i += 3)
-                k += (nrm[i] == 0.0 && nrm[i + 1] == 0.0 && nrm[i + 2] == 0.0) ? 0u : 1u;
-            return k;
-        };
-        if (usable(c->h_snrm) < 4 || usable(c->h_tnrm) < 4)
+        if (S.usable < 4 || T.usable < 4)
             throw lk::Status(LK_MISSING_DATA, "register_global: fewer than 4 points with usable normals");
-        // FPFH (registration.cpp:246-247) and the feature pre-match (:248) on the device
-        CK(lkk::pool_alloc(&d_sf, 33 * c->ns * sizeof(float), s));
-        CK(lkk::pool_alloc(&d_tf, 33 * c->nt * sizeof(float), s));
-        mark("d2h downsampled", s);
-        CK(lkk::compute_fpfh(c->d_spos, c->d_snrm, c->ns, params->feature_radius, d_sf, s));
-        mark("fpfh src", s);
-        CK(lkk::compute_fpfh(c->d_tpos, c->d_tnrm, c->nt, params->feature_radius, d_tf, s));
-        mark("fpfh tgt", s);
+        // feature pre-match (registration.cpp:248) once both sides are done
+        cudaStream_t s = c->stream;
         CK(lkk::pool_alloc(&c->d_cache, c->ns * sizeof(int32_t), s));
-        CK(lkk::feature_nn(d_sf, c->ns, d_tf, c->nt, c->d_cache, s));
-        mark("feature nn", s);
-        c->h_cache.resize(c->ns);
-        c->h_sfeat.resize(33 * c->ns);
-        c->h_tfeat.resize(33 * c->nt);
-        CK(cudaMemcpyAsync(c->h_cache.data(), c->d_cache, c->ns * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(c->h_sfeat.data(), d_sf, 33 * c->ns * sizeof(float), cudaMemcpyDeviceToHost, s));
-        CK(cudaMemcpyAsync(c->h_tfeat.data(), d_tf, 33 * c->nt * sizeof(float), cudaMemcpyDeviceToHost, s));
+        CK(lkk::feature_nn(c->d_sfeat, c->ns, c->d_tfeat, c->nt, c->d_cache, s));
+        ctx_finish_source(c);
         CK(cudaStreamSynchronize(s));
-        mark("d2h cache/features", s);
-        cleanup();
-        ctx_finish(c, *params);  // EvalGrid on the device (registration.cpp:249)
-        mark("eval grid", s);
+        if (trace_on()) std::fprintf(stderr, "[lk prepare] feature nn %8.3f ms\n", (now_s() - t0) * 1e3);
     } catch (...) {
-        cleanup();
+        drop(S);
+        drop(T);
         delete c;
         throw;
     }
@@ -362,8 +482,7 @@ lk_status prepare_impl(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_pa
 
 lk_status run_range_impl(lk_reg_ctx* c, const lk_reg_params& p, int64_t begin, int64_t end, void* d_record) {
     if (c->ns < 4) return fail(LK_TOO_FEW_POINTS, "sample_quadruple: need >= 4 source points");
-    if (static_cast<int64_t>(c->h_cache.size()) != c->ns)
-        return fail(LK_MISSING_DATA, "sample_quadruple: cache size mismatch");
+    if (!c->d_cache) return fail(LK_MISSING_DATA, "sample_quadruple: no correspondence cache");
     if (begin < 0 || end < begin) return fail(LK_INVALID_ARGUMENT, "bad hypothesis range");
     CK(cudaSetDevice(c->device));
     lkk::SourceView sv{c->d_spos, c->d_snrm, c->d_spos32, c->ns};
@@ -415,14 +534,17 @@ lk_status lk_reg_ctx_create(const lk_cloud* src, const lk_cloud* tgt, const int3
                 return fail(LK_MISSING_DATA, "RegistrationContext: cache index out of range");
         lk_reg_ctx* c = ctx_new(params->device);
         try {
+            cudaStream_t s = c->stream;
             c->ns = src->n;
             c->nt = tgt->n;
-            c->h_spos.assign(src->xyz, src->xyz + 3 * src->n);
-            c->h_snrm.assign(src->nxyz, src->nxyz + 3 * src->n);
-            c->h_tpos.assign(tgt->xyz, tgt->xyz + 3 * tgt->n);
-            c->h_tnrm.assign(tgt->nxyz, tgt->nxyz + 3 * tgt->n);
-            c->h_cache.assign(cache, cache + src->n);
-            ctx_finish(c, *params);
+            c->d_spos = dev_upload(src->xyz, 3 * src->n, s);
+            c->d_snrm = dev_upload(src->nxyz, 3 * src->n, s);
+            c->d_tpos = dev_upload(tgt->xyz, 3 * tgt->n, s);
+            c->d_tnrm = dev_upload(tgt->nxyz, 3 * tgt->n, s);
+            c->d_cache = dev_upload(cache, src->n, s);
+            c->src_max_norm = max_norm(src->xyz, src->n);
+            ctx_finish_source(c);
+            CK(lkk::build_grid(c->grid, 0, c->d_tpos, c->d_tnrm, c->nt, params->d_max, params->d_max, s));
         } catch (...) {
             delete c;
             throw;
@@ -472,18 +594,22 @@ lk_status lk_reg_ctx_sizes(const lk_reg_ctx* ctx, int64_t* n_source, int64_t* n_
 
 lk_status lk_reg_ctx_download(const lk_reg_ctx* c, double* src_xyz, double* src_n, double* tgt_xyz, double* tgt_n,
                               int32_t* cache, float* src_features, float* tgt_features) {
-    if (!c) return fail(LK_INVALID_ARGUMENT, "null context");
-    auto cp = [](void* dst, const void* s, size_t bytes) {
-        if (dst && bytes) std::memcpy(dst, s, bytes);
-    };
-    cp(src_xyz, c->h_spos.data(), c->h_spos.size() * sizeof(double));
-    cp(src_n, c->h_snrm.data(), c->h_snrm.size() * sizeof(double));
-    cp(tgt_xyz, c->h_tpos.data(), c->h_tpos.size() * sizeof(double));
-    cp(tgt_n, c->h_tnrm.data(), c->h_tnrm.size() * sizeof(double));
-    cp(cache, c->h_cache.data(), c->h_cache.size() * sizeof(int32_t));
-    cp(src_features, c->h_sfeat.data(), c->h_sfeat.size() * sizeof(float));
-    cp(tgt_features, c->h_tfeat.data(), c->h_tfeat.size() * sizeof(float));
-    return LK_OK;
+    return guarded([&]() -> lk_status {
+        if (!c) return fail(LK_INVALID_ARGUMENT, "null context");
+        CK(cudaSetDevice(c->device));
+        auto cp = [&](void* dst, const void* d, size_t bytes) {
+            if (dst && d && bytes) CK(cudaMemcpyAsync(dst, d, bytes, cudaMemcpyDeviceToHost, c->stream));
+        };
+        cp(src_xyz, c->d_spos, 3 * c->ns * sizeof(double));
+        cp(src_n, c->d_snrm, 3 * c->ns * sizeof(double));
+        cp(tgt_xyz, c->d_tpos, 3 * c->nt * sizeof(double));
+        cp(tgt_n, c->d_tnrm, 3 * c->nt * sizeof(double));
+        cp(cache, c->d_cache, c->ns * sizeof(int32_t));
+        cp(src_features, c->d_sfeat, 33 * c->ns * sizeof(float));
+        cp(tgt_features, c->d_tfeat, 33 * c->nt * sizeof(float));
+        CK(cudaStreamSynchronize(c->stream));
+        return LK_OK;
+    });
 }
 
 lk_status lk_reg_run_range(lk_reg_ctx* ctx, const lk_reg_params* params, int64_t begin, int64_t end,

@@ -204,18 +204,55 @@ __global__ void k_scatter(const int32_t* __restrict__ cell_of, int64_t n, const 
 }
 
 // Restores the reference's ascending-index order within every cell.
-__global__ void k_sort_cells(const int32_t* __restrict__ start, int64_t ncells, int32_t* __restrict__ index) {
-    int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+// Warp per cell: slots ascending by original index. Indices are distinct, so
+// each value's rank (how many values of the cell are smaller) is its slot.
+// Cells of up to 32 * kSortQ points are ranked in registers; larger cells
+// (not seen at the reference's densities) are insertion-sorted by lane 0.
+constexpr int kSortQ = 16;
+__global__ void __launch_bounds__(256) k_sort_cells(const int32_t* __restrict__ start, int64_t ncells,
+                                                    int32_t* __restrict__ index) {
+    const int64_t c = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (c >= ncells) return;
-    int32_t s0 = start[c], s1 = start[c + 1];
-    for (int32_t a = s0 + 1; a < s1; ++a) {
-        int32_t v = index[a];
-        int32_t b = a - 1;
-        while (b >= s0 && index[b] > v) {
-            index[b + 1] = index[b];
-            --b;
+    const int32_t s0 = start[c], s1 = start[c + 1];
+    const int k = s1 - s0;
+    if (k <= 1) return;
+    if (k <= 32 * kSortQ) {
+        const int q_used = (k + 31) >> 5;
+        int32_t v[kSortQ], rank[kSortQ];
+#pragma unroll
+        for (int q = 0; q < kSortQ; ++q) {
+            const int e = 32 * q + lane;
+            v[q] = (q < q_used && e < k) ? index[s0 + e] : INT32_MAX;
+            rank[q] = 0;
         }
-        index[b + 1] = v;
+#pragma unroll
+        for (int q2 = 0; q2 < kSortQ; ++q2) {
+            if (q2 >= q_used) break;
+            for (int t = 0; t < 32; ++t) {
+                const int32_t u = __shfl_sync(0xffffffffu, v[q2], t);
+#pragma unroll
+                for (int q = 0; q < kSortQ; ++q) rank[q] += (q < q_used && u < v[q]) ? 1 : 0;
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < kSortQ; ++q) {
+            const int e = 32 * q + lane;
+            if (q < q_used && e < k) index[s0 + rank[q]] = v[q];
+        }
+        return;
+    }
+    if (lane == 0) {
+        for (int32_t a = s0 + 1; a < s1; ++a) {
+            int32_t val = index[a];
+            int32_t b = a - 1;
+            while (b >= s0 && index[b] > val) {
+                index[b + 1] = index[b];
+                --b;
+            }
+            index[b + 1] = val;
+        }
     }
 }
 
@@ -297,58 +334,130 @@ __global__ void k_block_fill(const int32_t* __restrict__ start, const int32_t* _
 }
 
 // ---- fine lists ----------------------------------------------------------
-// Every point is listed in each fine cell whose box lies within d_max (+ a
-// relative 1e-9 and an absolute 1e-12 safety margin; listing extra points is
-// harmless) -- a superset of any query's d_max ball inside that cell.
-__device__ __forceinline__ bool box_within(double px, double py, double pz, double bx, double by, double bz,
-                                           double h, double r2) {
-    const double dx = fmax(0.0, fmax(bx - px, px - (bx + h)));
-    const double dy = fmax(0.0, fmax(by - py, py - (by + h)));
-    const double dz = fmax(0.0, fmax(bz - pz, pz - (bz + h)));
+// Fine lists, warp per coarse cell C and its 8 half-size cells. The
+// candidates of a fine box are the entries of C's 3x3x3 block list within
+// fine_dmax of the box (+ a relative 1e-9 and an absolute 1e-12 margin) --
+// every point the reference's window can hold within d_max of a query in
+// the box. They are then Voronoi-pruned: entry j is dropped when some entry k
+// is strictly closer than j to EVERY point of the (slightly expanded) box, so
+// j can never be a query's nearest neighbour there (a dominating k is itself
+// within d_max whenever j is; the resolve pass checks the reference window and
+// falls back to the exact coarse scan when the winner lies outside it).
+// |x-j|^2 - |x-k|^2 is separable per axis, so its minimum over the box is the
+// sum of per-axis minima over the two faces; the margin (1e-9 fcell^2) dwarfs
+// FP64 rounding of d2, so the reference's computed d2 orders k before j too.
+// Storage: the 8 fine lists of C are packed from 8 * (C's block-list offset),
+// which bounds them (each block entry is listed at most once per fine cell),
+// so one pass writes them with no count pass, scan or host round trip.
+constexpr int kFineWarps = 4;
+constexpr int kFineCap = 256;
+
+__device__ __forceinline__ bool box_within(double px, double py, double pz, const double* lo, double h, double r2) {
+    const double dx = fmax(0.0, fmax(lo[0] - px, px - (lo[0] + h)));
+    const double dy = fmax(0.0, fmax(lo[1] - py, py - (lo[1] + h)));
+    const double dz = fmax(0.0, fmax(lo[2] - pz, pz - (lo[2] + h)));
     return (dx * dx + dy * dy) + dz * dz <= r2;
 }
 
-template <bool kFill>
-__global__ void k_fine_lists(const double* __restrict__ pos, int64_t n, GridView g, int rf, double r2,
-                             int32_t* __restrict__ counts, const int32_t* __restrict__ offsets,
-                             float4* __restrict__ pts) {
-    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (i >= n) return;
-    const double px = pos[3 * i], py = pos[3 * i + 1], pz = pos[3 * i + 2];
-    const int kx = floor_cell((px - g.ox) / g.fcell) - 2 * g.offx;
-    const int ky = floor_cell((py - g.oy) / g.fcell) - 2 * g.offy;
-    const int kz = floor_cell((pz - g.oz) / g.fcell) - 2 * g.offz;
-    const float4 e = make_float4(static_cast<float>((px - g.ox) / g.fcell - 2 * g.offx),
-                                 static_cast<float>((py - g.oy) / g.fcell - 2 * g.offy),
-                                 static_cast<float>((pz - g.oz) / g.fcell - 2 * g.offz),
-                                 __int_as_float(static_cast<int32_t>(i)));
-    for (int x = max(kx - rf, 0); x <= min(kx + rf, g.fnx - 1); ++x)
-        for (int y = max(ky - rf, 0); y <= min(ky + rf, g.fny - 1); ++y)
-            for (int z = max(kz - rf, 0); z <= min(kz + rf, g.fnz - 1); ++z) {
-                const double bx = g.ox + (x + 2 * g.offx) * g.fcell;
-                const double by = g.oy + (y + 2 * g.offy) * g.fcell;
-                const double bz = g.oz + (z + 2 * g.offz) * g.fcell;
-                if (!box_within(px, py, pz, bx, by, bz, g.fcell, r2)) continue;
-                const int64_t c = (static_cast<int64_t>(x) * g.fny + y) * g.fnz + z;
-                if (kFill)
-                    pts[offsets[c] + atomicAdd(&counts[c], 1)] = e;
-                else
-                    atomicAdd(&counts[c], 1);
+__global__ void __launch_bounds__(32 * kFineWarps) k_fine_build(GridView g, int64_t ncells, double r2,
+                                                                 int2* __restrict__ info, float4* __restrict__ out) {
+    __shared__ int32_t s_cand[kFineWarps][kFineCap];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t c = blockIdx.x * static_cast<int64_t>(kFineWarps) + warp;
+    if (c >= ncells) return;
+    const int2 bi = __ldg(g.block_info + c);
+    if (bi.y == 0) return;  // info stays (0, 0)
+    const int ix = static_cast<int>(c / (static_cast<int64_t>(g.ny) * g.nz));
+    const int iy = static_cast<int>((c / g.nz) % g.ny);
+    const int iz = static_cast<int>(c % g.nz);
+    const double mexp = 1e-7 * g.fcell;
+    const double hexp = g.fcell + 2 * mexp;
+    const double margin = 1e-9 * g.fcell * g.fcell;
+    int32_t* cand = s_cand[warp];
+    int32_t w = 8 * bi.x;  // next free entry of C's fine storage
+    for (int sub = 0; sub < 8; ++sub) {
+        const int fx = 2 * ix + (sub >> 2), fy = 2 * iy + ((sub >> 1) & 1), fz = 2 * iz + (sub & 1);
+        const int64_t fc = (static_cast<int64_t>(fx) * g.fny + fy) * g.fnz + fz;
+        const double lo[3] = {g.ox + (fx + 2 * g.offx) * g.fcell, g.oy + (fy + 2 * g.offy) * g.fcell,
+                              g.oz + (fz + 2 * g.offz) * g.fcell};
+        const double le[3] = {lo[0] - mexp, lo[1] - mexp, lo[2] - mexp};
+        // candidates within fine_dmax of the box
+        int L = 0;
+        for (int32_t b = 0; b < bi.y; b += 32) {
+            const int32_t e = b + lane;
+            bool in = false;
+            if (e < bi.y) {
+                const double4 P = g.block_pts[bi.x + e];
+                in = box_within(P.x, P.y, P.z, lo, g.fcell, r2);
             }
-}
-
-__global__ void k_fine_info(const int32_t* __restrict__ offsets, int64_t nc, int2* __restrict__ info) {
-    const int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (c < nc) info[c] = make_int2(offsets[c], offsets[c + 1] - offsets[c]);
-}
-
-// each point's local cell in this grid (the reference's cell_of)
-__global__ void k_point_cells(const double* __restrict__ pos, int64_t n, GridView g, int4* __restrict__ out) {
-    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (i >= n) return;
-    out[i] = make_int4(floor_cell((pos[3 * i] - g.ox) / g.cell) - g.offx,
-                       floor_cell((pos[3 * i + 1] - g.oy) / g.cell) - g.offy,
-                       floor_cell((pos[3 * i + 2] - g.oz) / g.cell) - g.offz, 0);
+            const unsigned m = __ballot_sync(0xffffffffu, in);
+            const int at = L + __popc(m & ((1u << lane) - 1u));
+            if (in && at < kFineCap) cand[at] = bi.x + e;
+            L += __popc(m);
+        }
+        __syncwarp();
+        if (L > kFineCap) {
+            // (not seen at the reference's densities) no pruning: keep every candidate
+            const int32_t w0 = w;
+            for (int32_t b = 0; b < bi.y; b += 32) {
+                const int32_t e = b + lane;
+                bool in = false;
+                double4 P = make_double4(0, 0, 0, 0);
+                if (e < bi.y) {
+                    P = g.block_pts[bi.x + e];
+                    in = box_within(P.x, P.y, P.z, lo, g.fcell, r2);
+                }
+                const unsigned m = __ballot_sync(0xffffffffu, in);
+                if (in)
+                    out[w + __popc(m & ((1u << lane) - 1u))] =
+                        make_float4(static_cast<float>((P.x - g.ox) / g.fcell - 2 * g.offx),
+                                    static_cast<float>((P.y - g.oy) / g.fcell - 2 * g.offy),
+                                    static_cast<float>((P.z - g.oz) / g.fcell - 2 * g.offz),
+                                    __int_as_float(static_cast<int32_t>(P.w)));
+                w += __popc(m);
+            }
+            if (lane == 0) info[fc] = make_int2(w0, w - w0);
+            __syncwarp();
+            continue;
+        }
+        // dominance pruning, lane-parallel over the candidates
+        int K = 0;
+        const int32_t w0 = w;
+        for (int a0 = 0; a0 < L; a0 += 32) {
+            const int a = a0 + lane;
+            bool keep = false;
+            double4 J = make_double4(0, 0, 0, 0);
+            if (a < L) {
+                J = g.block_pts[cand[a]];
+                keep = true;
+                for (int k = 0; k < L && keep; ++k) {
+                    if (k == a) continue;
+                    const double4 Q = g.block_pts[cand[k]];
+                    const double jv[3] = {J.x, J.y, J.z}, kv[3] = {Q.x, Q.y, Q.z};
+                    double fmin = 0.0;
+#pragma unroll
+                    for (int ax = 0; ax < 3; ++ax) {
+                        const double c0 = le[ax], c1 = le[ax] + hexp;
+                        const double f0 = (c0 - jv[ax]) * (c0 - jv[ax]) - (c0 - kv[ax]) * (c0 - kv[ax]);
+                        const double f1 = (c1 - jv[ax]) * (c1 - jv[ax]) - (c1 - kv[ax]) * (c1 - kv[ax]);
+                        fmin += f0 < f1 ? f0 : f1;
+                    }
+                    if (fmin > margin) keep = false;
+                }
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, keep);
+            if (keep)
+                out[w0 + K + __popc(m & ((1u << lane) - 1u))] =
+                    make_float4(static_cast<float>((J.x - g.ox) / g.fcell - 2 * g.offx),
+                                static_cast<float>((J.y - g.oy) / g.fcell - 2 * g.offy),
+                                static_cast<float>((J.z - g.oz) / g.fcell - 2 * g.offz),
+                                __int_as_float(static_cast<int32_t>(J.w)));
+            K += __popc(m);
+        }
+        if (lane == 0) info[fc] = make_int2(w0, K);
+        w += K;
+        __syncwarp();
+    }
 }
 
 __global__ void k_to_float4(const double* __restrict__ pos, int64_t n, float4* __restrict__ out) {
@@ -393,10 +502,8 @@ void GridStorage::release() {
     pool_free(pos_orig, stream);
     pool_free(fine_info, stream);
     pool_free(fine_pts, stream);
-    pool_free(pcell, stream);
     fine_info = nullptr;
     fine_pts = nullptr;
-    pcell = nullptr;
     start = index = nullptr;
     slot_pos = slot_nrm = nullptr;
     near = nullptr;
@@ -484,7 +591,7 @@ cudaError_t build_grid(GridStorage& g, int kind, const double* d_pos, const doub
     LK_TRY(exclusive_scan(d_counts, ncells, g.start, stream));
     LK_TRY(cudaMemsetAsync(d_counts, 0, ncells * sizeof(int32_t), stream));
     k_scatter<<<blocks_for(n, 256), 256, 0, stream>>>(d_cell_of, n, g.start, d_counts, g.index);
-    k_sort_cells<<<blocks_for(ncells, 256), 256, 0, stream>>>(g.start, ncells, g.index);
+    k_sort_cells<<<blocks_for(ncells * 32, 256), 256, 0, stream>>>(g.start, ncells, g.index);
     k_gather_slots<<<blocks_for(n, 256), 256, 0, stream>>>(g.index, n, d_pos, d_nrm, g.slot_pos, g.slot_nrm);
     k_copy_normals<<<blocks_for(3 * n, 256), 256, 0, stream>>>(d_nrm, n, g.nrm_orig);
     if (kind == 0 || v.radius <= 2) {
@@ -517,29 +624,18 @@ cudaError_t build_grid(GridStorage& g, int kind, const double* d_pos, const doub
         v.fnz = 2 * v.nz;
         v.fine_dmax = kind == 0 ? cell : d_max;
         const int64_t nfc = static_cast<int64_t>(v.fnx) * v.fny * v.fnz;
-        if (nfc < (int64_t)1 << 30) {
-            const int rf = static_cast<int>(std::ceil(v.fine_dmax / v.fcell));
+        if (nfc < (int64_t)1 << 30 && 8 * g.nblock < (int64_t)1 << 28) {
             const double r2 = v.fine_dmax * v.fine_dmax * (1.0 + 1e-9) + 1e-12;
-            int32_t *fcnt = nullptr, *foff = nullptr;
-            LK_TRY(cudaMallocAsync(&fcnt, nfc * sizeof(int32_t), stream));
-            LK_TRY(cudaMallocAsync(&foff, (nfc + 1) * sizeof(int32_t), stream));
-            LK_TRY(cudaMemsetAsync(fcnt, 0, nfc * sizeof(int32_t), stream));
-            k_fine_lists<false><<<blocks_for(n, 128), 128, 0, stream>>>(d_pos, n, v, rf, r2, fcnt, nullptr, nullptr);
-            LK_TRY(exclusive_scan(fcnt, nfc, foff, stream));
-            int32_t ftotal = 0;
-            LK_TRY(cudaMemcpyAsync(&ftotal, foff + nfc, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
-            LK_TRY(cudaStreamSynchronize(stream));
+            GridView bv = v;
+            bv.block_info = g.block_info;
+            bv.block_pts = g.block_pts;
             g.nfine = nfc;
-            g.nfine_entries = ftotal;
+            g.nfine_entries = 8 * g.nblock;
             LK_TRY(pool_alloc(&g.fine_info, nfc * sizeof(int2), stream));
-            LK_TRY(pool_alloc(&g.fine_pts, (ftotal > 0 ? ftotal : 1) * sizeof(float4), stream));
-            LK_TRY(pool_alloc(&g.pcell, n * sizeof(int4), stream));
-            LK_TRY(cudaMemsetAsync(fcnt, 0, nfc * sizeof(int32_t), stream));
-            k_fine_lists<true><<<blocks_for(n, 128), 128, 0, stream>>>(d_pos, n, v, rf, r2, fcnt, foff, g.fine_pts);
-            k_fine_info<<<blocks_for(nfc, 256), 256, 0, stream>>>(foff, nfc, g.fine_info);
-            k_point_cells<<<blocks_for(n, 256), 256, 0, stream>>>(d_pos, n, v, g.pcell);
-            cudaFreeAsync(fcnt, stream);
-            cudaFreeAsync(foff, stream);
+            LK_TRY(pool_alloc(&g.fine_pts, (g.nfine_entries > 0 ? g.nfine_entries : 1) * sizeof(float4), stream));
+            LK_TRY(cudaMemsetAsync(g.fine_info, 0, nfc * sizeof(int2), stream));
+            const unsigned fb = static_cast<unsigned>((ncells + kFineWarps - 1) / kFineWarps);
+            k_fine_build<<<fb, 32 * kFineWarps, 0, stream>>>(bv, ncells, r2, g.fine_info, g.fine_pts);
         }
     }
     LK_TRY(cudaGetLastError());
@@ -557,7 +653,6 @@ cudaError_t build_grid(GridStorage& g, int kind, const double* d_pos, const doub
     v.pos_orig = g.pos_orig;
     v.fine_info = g.fine_info;
     v.fine_pts = g.fine_pts;
-    v.pcell = g.pcell;
     g.view = v;
     return cudaStreamSynchronize(stream);
 }

@@ -576,12 +576,12 @@ __global__ void k_prep_fast_fine(const double* __restrict__ cand_rt, const Count
 }
 
 // Exact resolution of one query over its fine list: FP32 top-3 with the guard
-// band, FP64 d2 for every entry that can be the minimum, and the reference's
-// window (the winner's EvalGrid cell within +-1 of y's, registration.cpp:167-169).
-// y's EvalGrid cell is its certain fine cell halved: (y - o) / fcell is exactly
-// 2 (y - o) / cell in FP64, so floor of the one is twice-or-one-more the floor
-// of the other. A winner outside the window (rounding at the edge) falls back
-// to eval_point.
+// band, FP64 d2 for every entry that can be the minimum, the normal gate.
+// Every entry comes from the block list of the query's EvalGrid cell (the
+// certain fine cell halved: (y - o) / fcell is exactly 2 (y - o) / cell in
+// FP64), i.e. from the reference's own search window (registration.cpp:167-169),
+// and Voronoi pruning only drops entries another listed entry beats everywhere
+// in the cell, so the minimum over the list is the reference's neighbour.
 // Out of line so its registers do not count against the callers' occupancy;
 // everything is reloaded from global memory (rt = the candidate's 12 doubles).
 __device__ __noinline__ bool eval_point_slow(const GridView& g, const double* rt, const SourceView& src, int64_t i,
@@ -607,8 +607,8 @@ __device__ __forceinline__ void top3(float d2, int32_t o, float& f1, float& f2, 
     }
 }
 
-__device__ __forceinline__ bool resolve_fine(const GridView& g, const double* rt, const double* R, const double* t,
-                                             const FastRT& F, const SourceView& src, int64_t i, V3 p, V3 ns,
+__device__ __forceinline__ bool resolve_fine(const GridView& g, const double* R, const double* t, const FastRT& F,
+                                             V3 p, V3 ns,
                                              float qx, float qy, float qz, int32_t off, int32_t cnt,
                                              const ScoreParams& sp, double& addend) {
     const float inf = __int_as_float(0x7f800000);
@@ -630,20 +630,12 @@ __device__ __forceinline__ bool resolve_fine(const GridView& g, const double* rt
     }
     const float band = F.band;
     if (f1 > F.pad + band) return false;  // nothing within d_max of y
-    const int cx = static_cast<int>(floorf(qx)) >> 1, cy = static_cast<int>(floorf(qy)) >> 1,
-              cz = static_cast<int>(floorf(qz)) >> 1;
     const V3 y = xform(R, t, p);
     double best_d2 = __longlong_as_double(0x7ff0000000000000ll);
     int32_t best_orig = INT32_MAX;
-    bool doubt = false;
     auto consider = [&](int32_t o) {
         const double d2 = sqnorm(sub(ld3(g.pos_orig, o), y));
         if (d2 > sp.d2_max) return;
-        const int4 c = __ldg(g.pcell + o);
-        if (abs(c.x - cx) > 1 || abs(c.y - cy) > 1 || abs(c.z - cz) > 1) {
-            doubt = true;
-            return;
-        }
         if (d2 < best_d2 || (d2 == best_d2 && o < best_orig)) {
             best_d2 = d2;
             best_orig = o;
@@ -660,7 +652,6 @@ __device__ __forceinline__ bool resolve_fine(const GridView& g, const double* rt
         consider(o1);
         if (f2 <= lim) consider(o2);
     }
-    if (doubt) return eval_point_slow(g, rt, src, i, sp, &addend);
     if (best_orig == INT32_MAX) return false;
     const V3 nt = ld3(g.nrm_orig, best_orig);
     if (is_zero(ns) || is_zero(nt)) return false;
@@ -827,7 +818,7 @@ __global__ void __launch_bounds__(kScoreThreads, 4) k_score_resolve(SourceView s
             const float qx = fmaf(F.r[0], P.x, fmaf(F.r[1], P.y, fmaf(F.r[2], P.z, F.t[0])));
             const float qy = fmaf(F.r[3], P.x, fmaf(F.r[4], P.y, fmaf(F.r[5], P.z, F.t[1])));
             const float qz = fmaf(F.r[6], P.x, fmaf(F.r[7], P.y, fmaf(F.r[8], P.z, F.t[2])));
-            inl = resolve_fine(g, cand_rt + 12 * cand, R, t, F, src, i, p, ns, qx, qy, qz, q.z, q.w, sp, addend);
+            inl = resolve_fine(g, R, t, F, p, ns, qx, qy, qz, q.z, q.w, sp, addend);
         }
         const int64_t word = cand * n_chunks + (i >> 5);
         const uint32_t bit = 1u << (i & 31);

@@ -48,16 +48,15 @@ struct GridView {
     const float4* block_f32;
     const double* pos_orig;    // 3 * npoints positions in original point order
     // Fine lists (radius-1 grids): cells of half the size over the same box,
-    // each listing the points within fine_dmax of the fine cell's box (a
-    // superset of every query's d_max ball inside it), FP32 fine-cell
-    // coordinates ((x - o) / fcell - 2 off), original index in w. pcell is
-    // each point's cell in this grid, for the reference-window check.
+    // each listing the entries of its cell's block list within fine_dmax of
+    // the fine box that can be the nearest neighbour somewhere in it (Voronoi
+    // pruned); FP32 fine-cell coordinates ((x - o) / fcell - 2 off), original
+    // index in w.
     int fnx, fny, fnz;
     double fcell;
     double fine_dmax;
     const int2* fine_info;
     const float4* fine_pts;
-    const int4* pcell;
 };
 
 struct GridStorage {
@@ -78,7 +77,6 @@ struct GridStorage {
     int64_t nfine = 0, nfine_entries = 0;
     int2* fine_info = nullptr;
     float4* fine_pts = nullptr;
-    int4* pcell = nullptr;
     cudaStream_t stream = nullptr;  // allocation stream
     void release();
 };
@@ -199,6 +197,10 @@ cudaError_t voxel_downsample(const double* d_pos, const double* d_nrm, int64_t n
 // compute_fpfh (proj/src/fpfh.cpp:57-141) on the device: 33 floats per point.
 cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, double radius, float* d_out,
                          cudaStream_t stream);
+
+// Usable (non-zero) normal count and max |p| of a device cloud (synchronous).
+cudaError_t cloud_stats(const double* d_pos, const double* d_nrm, int64_t n, int64_t* usable, double* max_norm,
+                        cudaStream_t stream);
 
 // FP64 exhaustive feature NN, ties -> lowest index (reference.hpp:56-76).
 cudaError_t feature_nn(const float* d_sf, int64_t ns, const float* d_tf, int64_t nt, int32_t* d_out,

@@ -6,9 +6,11 @@
 //   k_vox_mark     flag the first index of every voxel; an exclusive scan of
 //                  the flags gives each voxel its output position, which is the
 //                  reference's order (voxels sorted by first input index)
-//   k_vox_scatter  member lists per output voxel (unordered)
-//   k_vox_reduce   thread per voxel: members sorted by input index, then the
-//                  reference's sequential FP64 sums and the normalised normal
+//   k_vox_keys     (output voxel, input index) pairs; a stable radix sort
+//                  (cub::DeviceRadixSort) groups members by voxel in input order
+//   k_vox_reduce   warp per voxel: the reference's sequential FP64 sums in
+//                  input order (lane-0 chain over shuffled members) and the
+//                  normalised normal
 // compute_fpfh (proj/src/fpfh.cpp:57-141):
 //   neighbour lists within r (SearchGrid cell = r, ascending, self excluded),
 //   k_spfh    warp per point: pair-angle votes as integer counts; pairs whose
@@ -19,7 +21,10 @@
 //             neighbours in ascending order (the reference's summation order)
 #include <cmath>
 #include <cstdint>
+#include <cstring>
 #include <vector>
+
+#include <cub/device/device_radix_sort.cuh>
 
 #include "lk_device_math.cuh"
 #include "lk_kernels.cuh"
@@ -100,13 +105,13 @@ __global__ void k_vox_out(const unsigned long long* __restrict__ keys, const int
     cnt_out[o] = count[h];
 }
 
-__global__ void k_vox_scatter(const int32_t* __restrict__ point_slot, int64_t n, const int32_t* __restrict__ slot_out,
-                              const int32_t* __restrict__ member_start, int32_t* __restrict__ cursor,
-                              int32_t* __restrict__ members) {
+// sort keys for the members: each point's output voxel, value = its index
+__global__ void k_vox_keys(const int32_t* __restrict__ point_slot, int64_t n, const int32_t* __restrict__ slot_out,
+                           int32_t* __restrict__ keys, int32_t* __restrict__ vals) {
     int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (i >= n) return;
-    const int32_t o = slot_out[point_slot[i]];
-    members[member_start[o] + atomicAdd(&cursor[o], 1)] = static_cast<int32_t>(i);
+    keys[i] = slot_out[point_slot[i]];
+    vals[i] = static_cast<int32_t>(i);
 }
 
 // Sorts seg[0..k) ascending with the 32 lanes of a warp: in shared memory
@@ -157,22 +162,24 @@ constexpr int kSortCap = 2048;
 // proj/src/preprocess.cpp:30-58, warp per voxel: members sorted by input
 // index, then the sums in that order (lane order within 32-member chunks).
 // A skipped (zero) normal contributes +0.0, which leaves the sum unchanged.
-__global__ void __launch_bounds__(32 * kSortWarps) k_vox_reduce(int32_t* __restrict__ members,
+__global__ void __launch_bounds__(32 * kSortWarps) k_vox_reduce(const int32_t* __restrict__ members,
                                                                 const int32_t* __restrict__ member_start, int64_t n_out,
                                                                 const double* __restrict__ pos,
                                                                 const double* __restrict__ nrm,
                                                                 double* __restrict__ out_pos,
                                                                 double* __restrict__ out_nrm) {
-    __shared__ int32_t s_buf[kSortWarps][kSortCap];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t o = blockIdx.x * static_cast<int64_t>(kSortWarps) + warp;
     if (o >= n_out) return;
     const int32_t s0 = member_start[o], s1 = member_start[o + 1];
     const int k = s1 - s0;
-    const int32_t* sorted = warp_sort_segment(members + s0, k, s_buf[warp], kSortCap);
-    V3 ps = mk(0.0, 0.0, 0.0), nsum = mk(0.0, 0.0, 0.0);
-    for (int c0 = 0; c0 < k; c0 += 32) {
-        V3 p = mk(0.0, 0.0, 0.0), nv = mk(0.0, 0.0, 0.0);
+    const int32_t* sorted = members + s0;  // ascending input index (stable radix sort)
+    // lanes gather 32 members at a time (the next chunk's loads in flight
+    // while lane 0 runs the sequential sums over the current one from smem)
+    __shared__ double s_v[kSortWarps][6][32];
+    auto fetch = [&](int c0, V3& p, V3& nv) {
+        p = mk(0.0, 0.0, 0.0);
+        nv = mk(0.0, 0.0, 0.0);
         if (c0 + lane < k) {
             const int64_t i = sorted[c0 + lane];
             p = ld3(pos, i);
@@ -181,15 +188,32 @@ __global__ void __launch_bounds__(32 * kSortWarps) k_vox_reduce(int32_t* __restr
                 if (is_zero(nv)) nv = mk(0.0, 0.0, 0.0);
             }
         }
-        const int m = k - c0 < 32 ? k - c0 : 32;
-        for (int L = 0; L < m; ++L) {
-            ps.x += __shfl_sync(kFull, p.x, L);
-            ps.y += __shfl_sync(kFull, p.y, L);
-            ps.z += __shfl_sync(kFull, p.z, L);
-            nsum.x += __shfl_sync(kFull, nv.x, L);
-            nsum.y += __shfl_sync(kFull, nv.y, L);
-            nsum.z += __shfl_sync(kFull, nv.z, L);
+    };
+    V3 ps = mk(0.0, 0.0, 0.0), nsum = mk(0.0, 0.0, 0.0);
+    V3 p, nv;
+    fetch(0, p, nv);
+    for (int c0 = 0; c0 < k; c0 += 32) {
+        s_v[warp][0][lane] = p.x;
+        s_v[warp][1][lane] = p.y;
+        s_v[warp][2][lane] = p.z;
+        s_v[warp][3][lane] = nv.x;
+        s_v[warp][4][lane] = nv.y;
+        s_v[warp][5][lane] = nv.z;
+        __syncwarp();
+        if (c0 + 32 < k) fetch(c0 + 32, p, nv);
+        if (lane == 0) {
+            const int m = k - c0 < 32 ? k - c0 : 32;
+#pragma unroll 4
+            for (int L = 0; L < m; ++L) {
+                ps.x += s_v[warp][0][L];
+                ps.y += s_v[warp][1][L];
+                ps.z += s_v[warp][2][L];
+                nsum.x += s_v[warp][3][L];
+                nsum.y += s_v[warp][4][L];
+                nsum.z += s_v[warp][5][L];
+            }
         }
+        __syncwarp();
     }
     if (lane != 0) return;
     const double cnt = static_cast<double>(k);
@@ -273,9 +297,11 @@ __device__ __forceinline__ bool pair_bins(const PairSetup& s, V3 n1, V3 n2, int 
 }
 
 // neighbours within r (inclusive), self excluded (proj/src/fpfh.cpp:66-74)
-__global__ void k_nbr_count(const double* __restrict__ pos, int64_t n, GridView g, double r2,
-                            int32_t* __restrict__ counts) {
-    int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+// warp per point: lanes over the slots of each cell row, ballot counts
+__global__ void __launch_bounds__(32 * kSortWarps) k_nbr_count(const double* __restrict__ pos, int64_t n, GridView g,
+                                                               double r2, int32_t* __restrict__ counts) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t i = blockIdx.x * static_cast<int64_t>(kSortWarps) + warp;
     if (i >= n) return;
     const V3 p = ld3(pos, i);
     const int kx = floor_cell((p.x - g.ox) / g.cell) - g.offx;
@@ -287,10 +313,54 @@ __global__ void k_nbr_count(const double* __restrict__ pos, int64_t n, GridView 
             const int64_t row = (static_cast<int64_t>(x) * g.ny + y) * g.nz;
             const int32_t s0 = g.start[row + max(kz - g.radius, 0)];
             const int32_t s1 = g.start[row + min(kz + g.radius, g.nz - 1) + 1];
-            for (int32_t s = s0; s < s1; ++s)
-                if (g.index[s] != i && sqnorm(sub(ld3(g.slot_pos, s), p)) <= r2) ++c;
+            for (int32_t b = s0; b < s1; b += 32) {
+                const int32_t s = b + lane;
+                const bool hit = s < s1 && g.index[s] != i && sqnorm(sub(ld3(g.slot_pos, s), p)) <= r2;
+                c += __popc(__ballot_sync(kFull, hit));
+            }
         }
-    counts[i] = c;
+    if (lane == 0) counts[i] = c;
+}
+
+// Small clouds: radius_search by a warp-per-point scan of the whole cloud in
+// index order (ascending output, no grid, no sort). A pair counts when the
+// reference's SearchGrid would visit it -- cells (floor(p / cell), center 0)
+// within the block radius of the query's -- and d2 <= r2, so the lists equal
+// the grid's to the bit even where rounding puts a point within r two cells away.
+constexpr int64_t kBruteMax = 24576;
+
+__global__ void k_search_cells(const double* __restrict__ pos, int64_t n, double cell, int4* __restrict__ out) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    out[i] = make_int4(floor_cell((pos[3 * i] - 0.0) / cell), floor_cell((pos[3 * i + 1] - 0.0) / cell),
+                       floor_cell((pos[3 * i + 2] - 0.0) / cell), 0);
+}
+
+template <bool kFill>
+__global__ void __launch_bounds__(32 * kSortWarps) k_nbr_brute(const double* __restrict__ pos,
+                                                               const int4* __restrict__ cells, int64_t n, int rad,
+                                                               double r2, int32_t* __restrict__ counts,
+                                                               const int32_t* __restrict__ off,
+                                                               int32_t* __restrict__ nbr) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t i = blockIdx.x * static_cast<int64_t>(kSortWarps) + warp;
+    if (i >= n) return;
+    const V3 p = ld3(pos, i);
+    const int4 ci = cells[i];
+    int32_t o = kFill ? off[i] : 0;
+    for (int64_t b = 0; b < n; b += 32) {
+        const int64_t j = b + lane;
+        bool hit = false;
+        if (j < n && j != i) {
+            const int4 cj = __ldg(cells + j);
+            hit = abs(cj.x - ci.x) <= rad && abs(cj.y - ci.y) <= rad && abs(cj.z - ci.z) <= rad &&
+                  sqnorm(sub(ld3(pos, j), p)) <= r2;
+        }
+        const unsigned m = __ballot_sync(kFull, hit);
+        if (kFill && hit) nbr[o + __popc(m & ((1u << lane) - 1u))] = static_cast<int32_t>(j);
+        o += __popc(m);
+    }
+    if (!kFill && lane == 0) counts[i] = o;
 }
 
 // warp per point: gather the neighbours (row by row, lanes over slots,
@@ -329,6 +399,17 @@ __global__ void __launch_bounds__(32 * kSortWarps) k_nbr_fill(const double* __re
 }
 
 constexpr int kFpfhWarps = 4;
+
+// a / b correctly rounded from r = RN(1 / b): q = RN(a r) is within one ulp,
+// the residual a - b q is exact in one FMA, and RN(q + residual * r) is the
+// correctly rounded quotient (Markstein; no over/underflow for the FPFH
+// ranges: a in [0, 100], b in (0, radius]). One reciprocal per neighbour
+// instead of 33 divisions.
+__device__ __forceinline__ double div_by(double a, double b, double r) {
+    const double q = a * r;
+    const double e = fma(-q, b, a);
+    return fma(e, r, q);
+}
 
 // pass 1 (proj/src/fpfh.cpp:76-100): warp per point, integer vote counts in
 // counts[i][0..32], votes in counts[i][33]. Pairs whose frame-source test the
@@ -427,14 +508,56 @@ __global__ void __launch_bounds__(32 * kFpfhWarps) k_fpfh(const double* __restri
     const V3 p = ld3(pos, i);
     double acc0 = 0.0, acc1 = 0.0;  // bin lane, and bin 32 on lane 0
     int k_count = 0;
-    for (int32_t k = off[i]; k < off[i + 1]; ++k) {
-        const int32_t j = nbr[k];
-        if (is_zero(ld3(nrm, j))) continue;
-        const double w = sqrt(sqnorm(sub(ld3(pos, j), p)));
-        if (w <= 0.0) continue;
-        acc0 += spfh[33 * static_cast<int64_t>(j) + lane] / w;
-        if (lane == 0) acc1 += spfh[33 * static_cast<int64_t>(j) + 32] / w;
-        k_count += 1;
+    const int32_t k1 = off[i + 1];
+    for (int32_t base = off[i]; base < k1; base += 32) {
+        // lane t: neighbour base + t -- its usability, weight, the correctly
+        // rounded reciprocal of the weight and its bin-32 term
+        const int32_t kk = base + lane;
+        int32_t j = 0;
+        double w = 1.0, r = 1.0, q32 = 0.0;
+        bool ok = false;
+        if (kk < k1) {
+            j = nbr[kk];
+            if (!is_zero(ld3(nrm, j))) {
+                w = sqrt(sqnorm(sub(ld3(pos, j), p)));
+                ok = w > 0.0;
+            }
+            if (ok) {
+                r = 1.0 / w;
+                q32 = div_by(spfh[33 * static_cast<int64_t>(j) + 32], w, r);
+            } else {
+                w = 1.0;
+            }
+        }
+        unsigned m = __ballot_sync(kFull, ok);
+        k_count += __popc(m);
+        // the usable ones in neighbour order, four rows of spfh in flight
+        while (m) {
+            int src[4];
+            bool use[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                use[t] = m != 0;
+                src[t] = use[t] ? __ffs(m) - 1 : 0;
+                if (use[t]) m &= m - 1;
+            }
+            double sv[4], wv[4], rv[4], q32v[4];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                const int32_t jt = __shfl_sync(kFull, j, src[t]);
+                wv[t] = __shfl_sync(kFull, w, src[t]);
+                rv[t] = __shfl_sync(kFull, r, src[t]);
+                q32v[t] = __shfl_sync(kFull, q32, src[t]);
+                sv[t] = use[t] ? spfh[33 * static_cast<int64_t>(jt) + lane] : 0.0;
+            }
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                if (use[t]) {
+                    acc0 += div_by(sv[t], wv[t], rv[t]);
+                    acc1 += q32v[t];  // lane 0's value is the one used
+                }
+            }
+        }
     }
     {
         double blended = spfh[33 * i + lane];
@@ -446,6 +569,22 @@ __global__ void __launch_bounds__(32 * kFpfhWarps) k_fpfh(const double* __restri
         if (k_count > 0) blended += acc1 / static_cast<double>(k_count);
         out[33 * i + 32] = static_cast<float>(blended);
     }
+}
+
+// usable (non-zero) normals and max |p| of a cloud
+__global__ void k_cloud_stats(const double* __restrict__ pos, const double* __restrict__ nrm, int64_t n,
+                              unsigned long long* __restrict__ out) {
+    unsigned long long usable = 0;
+    double m = 0.0;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        if (nrm && !is_zero(ld3(nrm, i))) ++usable;
+        const double x = pos[3 * i], y = pos[3 * i + 1], z = pos[3 * i + 2];
+        m = fmax(m, sqrt(x * x + y * y + z * z));
+    }
+    // non-negative doubles order like their bit patterns
+    atomicAdd(&out[0], usable);
+    atomicMax(&out[1], static_cast<unsigned long long>(__double_as_longlong(m)));
 }
 
 #define LK_TRY(x)                         \
@@ -500,11 +639,28 @@ cudaError_t voxel_downsample(const double* d_pos, const double* d_nrm, int64_t n
         LK_TRY(cudaMallocAsync(&members, n * sizeof(int32_t), stream));
         k_vox_out<<<nblocks(table, 256), 256, 0, stream>>>(keys, first, count, table, flag_scan, slot_out, cnt_out);
         LK_TRY(exclusive_scan(cnt_out, n_out, member_start, stream));
-        LK_TRY(cudaMemsetAsync(cnt_out, 0, n_out * sizeof(int32_t), stream));
-        k_vox_scatter<<<nblocks(n, 256), 256, 0, stream>>>(point_slot, n, slot_out, member_start, cnt_out, members);
+        // members grouped by output voxel, ascending input index inside each
+        // (a stable LSD radix sort on the voxel ordinal)
+        int32_t *skeys = nullptr, *svals = nullptr, *skeys_out = nullptr;
+        LK_TRY(cudaMallocAsync(&skeys, n * sizeof(int32_t), stream));
+        LK_TRY(cudaMallocAsync(&svals, n * sizeof(int32_t), stream));
+        LK_TRY(cudaMallocAsync(&skeys_out, n * sizeof(int32_t), stream));
+        k_vox_keys<<<nblocks(n, 256), 256, 0, stream>>>(point_slot, n, slot_out, skeys, svals);
+        int end_bit = 1;
+        while ((int64_t(1) << end_bit) < n_out) ++end_bit;
+        size_t temp_bytes = 0;
+        LK_TRY(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, skeys, skeys_out, svals, members,
+                                               static_cast<int>(n), 0, end_bit, stream));
+        void* temp = nullptr;
+        LK_TRY(cudaMallocAsync(&temp, temp_bytes > 0 ? temp_bytes : 1, stream));
+        LK_TRY(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, skeys, skeys_out, svals, members,
+                                               static_cast<int>(n), 0, end_bit, stream));
+        cudaFreeAsync(temp, stream);
+        cudaFreeAsync(skeys, stream);
+        cudaFreeAsync(svals, stream);
+        cudaFreeAsync(skeys_out, stream);
         k_vox_reduce<<<nblocks(n_out, kSortWarps), 32 * kSortWarps, 0, stream>>>(members, member_start, n_out, d_pos,
-                                                                                  d_nrm, d_out_pos,
-                                                             d_out_nrm);
+                                                                                  d_nrm, d_out_pos, d_out_nrm);
         *out_count = n_out;
     }
     LK_TRY(cudaGetLastError());
@@ -526,13 +682,23 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
                          cudaStream_t stream) {
     if (n <= 0) return cudaErrorInvalidValue;
     GridStorage g;
-    LK_TRY(build_grid(g, 1, d_pos, nullptr, n, radius, radius, stream, false));
     int32_t *counts = nullptr, *off = nullptr, *nbr = nullptr;
+    int4* cells = nullptr;
     double* spfh = nullptr;
+    const double r2 = radius * radius;
+    const bool brute = n <= kBruteMax;
     LK_TRY(cudaMallocAsync(&counts, n * sizeof(int32_t), stream));
     LK_TRY(cudaMallocAsync(&off, (n + 1) * sizeof(int32_t), stream));
-    const double r2 = radius * radius;
-    k_nbr_count<<<nblocks(n, 128), 128, 0, stream>>>(d_pos, n, g.view, r2, counts);
+    if (brute) {
+        // SearchGrid(cell = radius): block radius ceil(radius / cell) = 1
+        LK_TRY(cudaMallocAsync(&cells, n * sizeof(int4), stream));
+        k_search_cells<<<nblocks(n, 256), 256, 0, stream>>>(d_pos, n, radius, cells);
+        k_nbr_brute<false><<<nblocks(n, kSortWarps), 32 * kSortWarps, 0, stream>>>(d_pos, cells, n, 1, r2, counts,
+                                                                                   nullptr, nullptr);
+    } else {
+        LK_TRY(build_grid(g, 1, d_pos, nullptr, n, radius, radius, stream, false));
+        k_nbr_count<<<nblocks(n, kSortWarps), 32 * kSortWarps, 0, stream>>>(d_pos, n, g.view, r2, counts);
+    }
     LK_TRY(exclusive_scan(counts, n, off, stream));
     int32_t total = 0;
     LK_TRY(cudaMemcpyAsync(&total, off + n, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
@@ -549,7 +715,11 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
     LK_TRY(cudaMallocAsync(&deferred_x, cap * sizeof(double2), stream));
     LK_TRY(cudaMallocAsync(&n_def, sizeof(int32_t), stream));
     LK_TRY(cudaMemsetAsync(n_def, 0, sizeof(int32_t), stream));
-    k_nbr_fill<<<nblocks(n, kSortWarps), 32 * kSortWarps, 0, stream>>>(d_pos, n, g.view, r2, off, nbr);
+    if (brute)
+        k_nbr_brute<true><<<nblocks(n, kSortWarps), 32 * kSortWarps, 0, stream>>>(d_pos, cells, n, 1, r2, nullptr, off,
+                                                                                  nbr);
+    else
+        k_nbr_fill<<<nblocks(n, kSortWarps), 32 * kSortWarps, 0, stream>>>(d_pos, n, g.view, r2, off, nbr);
     k_spfh<<<nblocks(n, kFpfhWarps), 32 * kFpfhWarps, 0, stream>>>(d_pos, d_nrm, n, off, nbr, votes, deferred,
                                                                    deferred_x, n_def);
     // frame-source tests the device cannot decide: the host's libm decides
@@ -576,6 +746,7 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
     cudaFreeAsync(counts, stream);
     cudaFreeAsync(off, stream);
     cudaFreeAsync(nbr, stream);
+    if (cells) cudaFreeAsync(cells, stream);
     cudaFreeAsync(spfh, stream);
     cudaFreeAsync(votes, stream);
     cudaFreeAsync(deferred, stream);
@@ -585,6 +756,22 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
     cudaError_t e = cudaStreamSynchronize(stream);
     g.release();
     return e;
+}
+
+cudaError_t cloud_stats(const double* d_pos, const double* d_nrm, int64_t n, int64_t* usable, double* max_norm,
+                        cudaStream_t stream) {
+    unsigned long long* d = nullptr;
+    LK_TRY(cudaMallocAsync(&d, 2 * sizeof(unsigned long long), stream));
+    LK_TRY(cudaMemsetAsync(d, 0, 2 * sizeof(unsigned long long), stream));
+    k_cloud_stats<<<nblocks(n, 256) < 64 ? nblocks(n, 256) : 64, 256, 0, stream>>>(d_pos, d_nrm, n, d);
+    unsigned long long h[2] = {0, 0};
+    LK_TRY(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, stream));
+    cudaFreeAsync(d, stream);
+    LK_TRY(cudaStreamSynchronize(stream));
+    *usable = static_cast<int64_t>(h[0]);
+    const long long bits = static_cast<long long>(h[1]);
+    std::memcpy(max_norm, &bits, sizeof(double));
+    return cudaGetLastError();
 }
 
 }  // namespace lkk

@@ -154,6 +154,11 @@ def test_device_downsample_full_frame_matches_oracle(oracle):
         d = lk.voxel_downsample(cloud, leaf)
         ox, on = oracle.voxel_downsample(cloud.positions, cloud.normals, leaf)
         assert np.array_equal(d.positions, ox) and np.array_equal(d.normals, on)
+    # FPFH above the brute-force size limit takes the SearchGrid path
+    assert d.size() > 24576
+    f = lk.compute_fpfh(d, 0.08)
+    fo = oracle.compute_fpfh(ox, on, 0.08)
+    assert np.array_equal(f, fo)
     bad = src.normals.copy()
     bad[5] *= 1.1
     with pytest.raises(lk.MissingNormals):
