@@ -33,6 +33,10 @@ sys.path.insert(0, ROOT)
 
 METRIC = "candidate×point evals/sec"
 UNIT = "evals/s"
+# kernels of one hypothesis step (lk_hypotheses.cu run_hypotheses_range):
+# k_hyp_sample, k_kabsch, k_prep_fast, k_prep_fast_fine, k_score_split,
+# k_score_resolve, k_score (overflow), k_score_exits, k_score_finalists
+KERNELS_PER_STEP = 9
 PAPER_MS_PER_REGISTRATION = 20.50  # PAPER.md:161 (Titan X Pascal, redwood pairs) -- context only
 
 
@@ -77,6 +81,17 @@ def peaks():
         return float(p["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+def ncu_traffic(kernels):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernels`
+    from the committed ncu --set full capture, or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            t = json.load(f)["dram_bytes_per_launch"]
+        return float(sum(t[k] for k in kernels))
+    except Exception:
+        return None
 
 
 class ClockSampler:
@@ -289,6 +304,7 @@ def run_b200(args):
         dist.all_reduce(total_ms, op=dist.ReduceOp.MAX)
     total_ms = float(total_ms.item())
     kt, runs = ctx.kernel_times()
+    ph, _ = ctx.phase_times()
     recs = lk.records_from_bytes(xbuf.cpu().numpy())
     mstats = lk.HypothesisStats()
     merged = lk.merge_records(recs, ctx.n_source, mstats)
@@ -338,17 +354,19 @@ def run_b200(args):
             "hypothesis_index": merged.hypothesis_index if merged else -1,
             "stats_per_step": {k: getattr(mstats, k) for k in ("sampled", "prerejected", "degenerate", "evaluated",
                                                               "qualified", "w_ref", "evals_executed")},
-            "kernel_ms_per_step": {k: v / max(runs, 1) for k, v in kt.items()},
+            "kernel_ms_per_step": {k: v / max(runs, 1) for k, v in ph.items()},
             "e2e": {"value": w_step / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "ms_per_registration": e2e_s * 1e3,
                     "note": "prepare_registration on the device (H2D of the raw pinned clouds, voxel "
                             "downsample, FPFH, feature match, EvalGrid) + hypotheses + exchange + merge"},
             "paper_ms_per_registration": PAPER_MS_PER_REGISTRATION,
-            "gpu_launches": 3 * args.steps,
+            "gpu_launches": KERNELS_PER_STEP * args.steps,
             "clocks": clock_info,
         }
-        # roofline of the dominant kernel (k_score), algorithmic bytes per SURVEY.md 8d
-        score_ms = kt["k_score"] / max(runs, 1)
+        # roofline of the evaluation kernels (k_score_split + k_score_resolve:
+        # every candidate x point evaluation happens in one of the two),
+        # algorithmic bytes per SURVEY.md 8d, event-timed on the launch stream
+        score_ms = (ph["k_score_split"] + ph["k_score_resolve"]) / max(runs, 1)
         shape = None
         if world == 1 and not args.no_cpu_baseline:
             cpu = cpu_oracle_registration(pair, H, args.seed)
@@ -369,12 +387,16 @@ def run_b200(args):
         evals_per_launch = mstats.evals_executed / max(world, 1)
         if shape["bytes_per_eval"] and score_ms > 0:
             achieved = evals_per_launch * shape["bytes_per_eval"] / (score_ms / 1e3) / 1e9
+            traffic = ncu_traffic(("k_score_split", "k_score_resolve"))
             line["roofline"] = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                                "frac": achieved / hbm_peak, "traffic": None, "kernel": "k_score",
+                                "frac": achieved / hbm_peak, "traffic": traffic,
+                                "kernel": "k_score_split+k_score_resolve",
                                 "peak_kind": peak_kind, "evals_per_launch": evals_per_launch,
                                 "kernel_ms": score_ms, "work_shape": shape,
-                                "note": "algorithmic bytes/eval = 1+72o+12k+12h (SURVEY.md 8d); the working set "
-                                        "is L2-resident, the binding pipe is FP64 (see profiles/)"}
+                                "note": "achieved = evals executed per step x algorithmic bytes/eval "
+                                        "(1+72o+12k+12h, SURVEY.md 8d) / event time of the two evaluation "
+                                        "kernels; traffic = their DRAM bytes per launch from the committed ncu "
+                                        "capture (profiles/ncu_traffic.json): the working set is L2-resident"}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

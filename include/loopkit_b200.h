@@ -144,6 +144,10 @@ lk_status lk_reg_ctx_sizes(const lk_reg_ctx* ctx, int64_t* n_source, int64_t* n_
  * the three kernels (ms3) and the number of runs (synchronises the events). */
 lk_status lk_reg_ctx_set_profiling(lk_reg_ctx* ctx, int32_t enable);
 lk_status lk_reg_ctx_kernel_times(lk_reg_ctx* ctx, double* ms3, int64_t* runs, int32_t reset);
+/* The same events, per scoring phase: ms[0..5] = k_hyp_sample, k_kabsch,
+ * k_prep_fast(+_fine), k_score_split, k_score_resolve, and the tail
+ * (k_score overflow + k_score_exits + k_score_finalists). */
+lk_status lk_reg_ctx_phase_times(lk_reg_ctx* ctx, double* ms, int32_t n_phases, int64_t* runs, int32_t reset);
 /* copy the prepared context back to the host (any pointer may be NULL) */
 lk_status lk_reg_ctx_download(const lk_reg_ctx* ctx, double* src_xyz, double* src_n, double* tgt_xyz, double* tgt_n,
                               int32_t* cache, float* src_features, float* tgt_features);

@@ -122,6 +122,7 @@ SIGNATURES = {
     "lk_reg_ctx_set_stream": (C.c_int, [C.c_void_p, C.c_void_p]),
     "lk_reg_ctx_set_profiling": (C.c_int, [C.c_void_p, C.c_int32]),
     "lk_reg_ctx_kernel_times": (C.c_int, [C.c_void_p, dptr, i64ptr, C.c_int32]),
+    "lk_reg_ctx_phase_times": (C.c_int, [C.c_void_p, dptr, C.c_int32, i64ptr, C.c_int32]),
     "lk_reg_ctx_sizes": (C.c_int, [C.c_void_p, i64ptr, i64ptr]),
     "lk_reg_ctx_download": (C.c_int, [C.c_void_p, dptr, dptr, dptr, dptr, i32ptr, fptr, fptr]),
     "lk_reg_run_hypotheses": (C.c_int, [C.c_void_p, C.POINTER(lk_reg_params), C.POINTER(lk_reg_result),

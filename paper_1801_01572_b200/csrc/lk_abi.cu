@@ -290,14 +290,14 @@ struct lk_reg_ctx {
     lk_reg_record* d_record = nullptr;
     double prepare_seconds = 0.0;
     bool profile = false;
-    std::vector<std::array<cudaEvent_t, 4>> pending;
-    double kernel_ms[3] = {0, 0, 0};
+    std::vector<std::array<cudaEvent_t, lkk::kPhaseEvents>> pending;
+    double kernel_ms[lkk::kPhaseEvents - 1] = {};
     int64_t profiled_runs = 0;
     std::mutex mu;
     void drain_events() {
         for (auto& ev : pending) {
-            cudaEventSynchronize(ev[3]);
-            for (int k = 0; k < 3; ++k) {
+            cudaEventSynchronize(ev[lkk::kPhaseEvents - 1]);
+            for (int k = 0; k < lkk::kPhaseEvents - 1; ++k) {
                 float ms = 0.f;
                 cudaEventElapsedTime(&ms, ev[k], ev[k + 1]);
                 kernel_ms[k] += ms;
@@ -490,7 +490,7 @@ lk_status run_range_impl(lk_reg_ctx* c, const lk_reg_params& p, int64_t begin, i
     if (fast_path_enabled()) lkk::configure_fast_path(sp, c->grid.view, c->src_max_norm);
     cudaEvent_t* ev = nullptr;
     if (c->profile) {
-        std::array<cudaEvent_t, 4> e4;
+        std::array<cudaEvent_t, lkk::kPhaseEvents> e4;
         for (auto& e : e4) CK(cudaEventCreate(&e));
         c->pending.push_back(e4);
         ev = c->pending.back().data();
@@ -575,8 +575,27 @@ lk_status lk_reg_ctx_kernel_times(lk_reg_ctx* ctx, double* ms3, int64_t* runs, i
     std::lock_guard<std::mutex> lock(ctx->mu);
     cudaSetDevice(ctx->device);
     ctx->drain_events();
-    if (ms3)
-        for (int k = 0; k < 3; ++k) ms3[k] = ctx->kernel_ms[k];
+    if (ms3) {
+        ms3[0] = ctx->kernel_ms[0];
+        ms3[1] = ctx->kernel_ms[1];
+        ms3[2] = 0.0;
+        for (int k = 2; k < lkk::kPhaseEvents - 1; ++k) ms3[2] += ctx->kernel_ms[k];
+    }
+    if (runs) *runs = ctx->profiled_runs;
+    if (reset) {
+        for (double& v : ctx->kernel_ms) v = 0.0;
+        ctx->profiled_runs = 0;
+    }
+    return LK_OK;
+}
+
+lk_status lk_reg_ctx_phase_times(lk_reg_ctx* ctx, double* ms, int32_t n_phases, int64_t* runs, int32_t reset) {
+    if (!ctx) return fail(LK_INVALID_ARGUMENT, "null context");
+    if (n_phases < 0 || (n_phases > 0 && !ms)) return fail(LK_INVALID_ARGUMENT, "null argument");
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    cudaSetDevice(ctx->device);
+    ctx->drain_events();
+    for (int k = 0; k < n_phases; ++k) ms[k] = k < lkk::kPhaseEvents - 1 ? ctx->kernel_ms[k] : 0.0;
     if (runs) *runs = ctx->profiled_runs;
     if (reset) {
         for (double& v : ctx->kernel_ms) v = 0.0;

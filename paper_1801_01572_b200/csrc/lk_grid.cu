@@ -653,6 +653,10 @@ cudaError_t build_grid(GridStorage& g, int kind, const double* d_pos, const doub
     v.pos_orig = g.pos_orig;
     v.fine_info = g.fine_info;
     v.fine_pts = g.fine_pts;
+    v.n_points = g.npoints;
+    v.n_cells = g.ncells;
+    v.n_fine = g.nfine;
+    v.n_fine_entries = g.fine_pts ? g.nfine_entries : 0;
     g.view = v;
     return cudaStreamSynchronize(stream);
 }

@@ -13,10 +13,11 @@
 //                   reference's visit count from the miss ballots; inliers and a
 //                   tree sum of d2 with a rigorous order bound decide qualification
 //                   (the sequential chain only when the bound straddles max_fitness).
-//   k_score_finalists one CTA: global max inliers / min fitness, the finalists
-//                   whose bounds overlap, their exact sequential sums in point
-//                   order; the strict total order (registration.cpp:272-276) picks
-//                   the winner and the rank record is written.
+//   k_score_finalists 32 CTAs: global max inliers / min fitness, the finalists
+//                   whose bounds overlap (spread over the CTAs), their exact
+//                   sequential sums in point order; the strict total order
+//                   (registration.cpp:272-276) picks the winner and the last CTA
+//                   writes the rank record.
 //   k_score         warp per candidate streaming its points in order (explicit
 //                   candidate lists, and candidates beyond the split capacity).
 //
@@ -26,6 +27,7 @@
 // recovered from the ordered miss ballots. Sums are added lane by lane in
 // point order, so every fitness is bit-identical to the reference's.
 #include <cstdint>
+#include <cstdlib>
 
 #include "lk_device_math.cuh"
 #include "lk_kernels.cuh"
@@ -63,12 +65,37 @@ __device__ __forceinline__ unsigned long long warp_atomic_add(unsigned long long
     return base + __popc(mask & ((1u << lane) - 1u));
 }
 
+// Byte ranges the scoring phase gathers from (grid lists, target and source
+// arrays). k_hyp_sample pulls them into L2 with bulk prefetches as it starts,
+// so the scoring kernel's dependent gathers hit L2 instead of DRAM.
+struct PrefetchList {
+    static constexpr int kMax = 8;
+    const char* ptr[kMax];
+    unsigned long long bytes[kMax];
+    int n;
+};
+constexpr unsigned kPrefetchChunk = 64 << 10;
+
+__device__ __forceinline__ void l2_prefetch_bulk(const void* p, unsigned bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 __global__ void __launch_bounds__(256) k_hyp_sample(int64_t begin, int64_t count, uint64_t seed_mix, uint32_t ns,
                                                     uint32_t thresh, const int32_t* __restrict__ cache,
                                                     const double* __restrict__ spos,
                                                     const double* __restrict__ tpos, double tau,
                                                     int64_t* __restrict__ surv_index, int32_t* __restrict__ surv_ids,
-                                                    Counters* __restrict__ ctr) {
+                                                    Counters* __restrict__ ctr, const __grid_constant__ PrefetchList pf) {
+    if (blockIdx.x < pf.n) {
+        // range blockIdx.x, 64 KB per thread-step (16-byte granules)
+        const char* p = pf.ptr[blockIdx.x];
+        const unsigned long long nb = pf.bytes[blockIdx.x] & ~15ull;
+        for (unsigned long long o = static_cast<unsigned long long>(threadIdx.x) * kPrefetchChunk; o < nb;
+             o += static_cast<unsigned long long>(blockDim.x) * kPrefetchChunk) {
+            const unsigned long long left = nb - o;
+            l2_prefetch_bulk(p + o, static_cast<unsigned>(left < kPrefetchChunk ? left : kPrefetchChunk));
+        }
+    }
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     // uniform trip count per warp so the warp-wide ballots stay convergent
     const int64_t rounds = (count + stride - 1) / stride;
@@ -101,9 +128,9 @@ __global__ void __launch_bounds__(256) k_hyp_sample(int64_t begin, int64_t count
             }
             survive = !prerejected(sp, dp, tau);
         }
+        // prerejected = sampled - survivors (every live hypothesis is one or
+        // the other), so only the survivors touch a counter
         unsigned long long slot = warp_atomic_add(&ctr->n_survivors, survive);
-        unsigned rej = __ballot_sync(kFull, live && !survive);
-        if ((threadIdx.x & 31) == 0 && rej) atomicAdd(&ctr->prerejected, static_cast<unsigned long long>(__popc(rej)));
         if (survive) {
             surv_index[slot] = begin + j;
             int4* ids = reinterpret_cast<int4*>(surv_ids + 8 * slot);
@@ -404,19 +431,31 @@ struct WarpTally {
 // Returns true in the CTA that finishes last (it then owns the final reduce).
 __device__ bool publish_cta(const WarpTally& wt, Counters* ctr, BestRec* block_best, int slot, bool want_ticket) {
     __shared__ BestRec s_best[kScoreWarps];
+    __shared__ unsigned long long s_tally[kScoreWarps][3];
     __shared__ unsigned long long s_ticket;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (lane == 0) {
-        if (wt.qualified) atomicAdd(&ctr->qualified, wt.qualified);
-        if (wt.w_ref) atomicAdd(&ctr->w_ref, wt.w_ref);
-        if (wt.executed) atomicAdd(&ctr->evals_executed, wt.executed);
+        s_tally[warp][0] = wt.qualified;
+        s_tally[warp][1] = wt.w_ref;
+        s_tally[warp][2] = wt.executed;
         s_best[warp] = wt.best;
     }
     __syncthreads();
+    // one thread per CTA touches the global counters (same-address atomics
+    // from every warp serialise in one L2 slice)
     if (threadIdx.x == 0) {
+        unsigned long long q = 0, w = 0, x = 0;
+        for (int k = 0; k < kScoreWarps; ++k) {
+            q += s_tally[k][0];
+            w += s_tally[k][1];
+            x += s_tally[k][2];
+        }
+        if (q) atomicAdd(&ctr->qualified, q);
+        if (w) atomicAdd(&ctr->w_ref, w);
+        if (x) atomicAdd(&ctr->evals_executed, x);
         BestRec b = s_best[0];
-        for (int w = 1; w < kScoreWarps; ++w)
-            if (better(s_best[w], b)) b = s_best[w];
+        for (int k = 1; k < kScoreWarps; ++k)
+            if (better(s_best[k], b)) b = s_best[k];
         block_best[slot] = b;
         __threadfence();
         s_ticket = want_ticket ? atomicAdd(&ctr->blocks_done, 1ull) : 0ull;
@@ -891,6 +930,8 @@ __global__ void __launch_bounds__(kScoreThreads) k_score_exits(int64_t ns, Score
                                                                CandInfo* __restrict__ info,
                                                                Counters* __restrict__ ctr,
                                                                BestRec* __restrict__ block_best, int best_offset) {
+    constexpr int kGroups = 8;  // 8 x 32 miss ballots (8192 points) in flight per pass
+    constexpr int kBatch = 8;   // addend loads in flight per lane
     __shared__ double s_chain[kScoreWarps][256];
     const int lane = threadIdx.x & 31;
     const int64_t n_all = static_cast<int64_t>(ctr->n_candidates);
@@ -900,44 +941,68 @@ __global__ void __launch_bounds__(kScoreThreads) k_score_exits(int64_t ns, Score
     for (int64_t cand = blockIdx.x * static_cast<int64_t>(blockDim.x >> 5) + (threadIdx.x >> 5); cand < n_cand;
          cand += nwarps) {
         const uint32_t* mm = miss_masks + cand * n_chunks;
-        // exact miss-budget decision and the reference's visit count
+        // exact miss-budget decision and the reference's visit count: the
+        // ballots of 256 chunks are loaded at once, then scanned in order
         int64_t misses = 0, visited = ns;
         bool exited = false;
-        for (int32_t g0 = 0; g0 < n_chunks && !exited; g0 += 32) {
-            const int32_t c = g0 + lane;
-            const int cnt = c < n_chunks ? __popc(__ldg(mm + c)) : 0;
-            int incl = cnt;
+        for (int32_t s0 = 0; s0 < n_chunks && !exited; s0 += 32 * kGroups) {
+            uint32_t mreg[kGroups];
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                int y = __shfl_up_sync(kFull, incl, o);
-                if (lane >= o) incl += y;
+            for (int g = 0; g < kGroups; ++g) {
+                const int32_t c = s0 + g * 32 + lane;
+                mreg[g] = c < n_chunks ? __ldg(mm + c) : 0u;
             }
-            const unsigned over = __ballot_sync(kFull, misses + incl > sp.miss_budget);
-            if (over) {
-                const int L = __ffs(over) - 1;
-                const int64_t before = misses + __shfl_sync(kFull, incl - cnt, L);
-                unsigned m = __ldg(mm + g0 + L);
-                const int need = static_cast<int>(sp.miss_budget - before);
-                for (int q = 0; q < need; ++q) m &= m - 1;
-                visited = static_cast<int64_t>(g0 + L) * 32 + (__ffs(m) - 1) + 1;
-                exited = true;
+#pragma unroll
+            for (int g = 0; g < kGroups; ++g) {
+                if (exited) continue;  // warp-uniform
+                const int cnt = __popc(mreg[g]);
+                int incl = cnt;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    int y = __shfl_up_sync(kFull, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                const unsigned over = __ballot_sync(kFull, misses + incl > sp.miss_budget);
+                if (over) {
+                    const int L = __ffs(over) - 1;
+                    const int64_t before = misses + __shfl_sync(kFull, incl - cnt, L);
+                    unsigned m = __shfl_sync(kFull, mreg[g], L);
+                    const int need = static_cast<int>(sp.miss_budget - before);
+                    for (int q = 0; q < need; ++q) m &= m - 1;
+                    visited = static_cast<int64_t>(s0 + g * 32 + L) * 32 + (__ffs(m) - 1) + 1;
+                    exited = true;
+                }
+                misses += __shfl_sync(kFull, incl, 31);
             }
-            misses += __shfl_sync(kFull, incl, 31);
         }
         wt.w_ref += static_cast<unsigned long long>(visited);
         wt.executed += static_cast<unsigned long long>(ns);
         CandInfo ci{-1, 0.0, 0};
         if (!exited) {
-            // inliers and a lane-parallel sum of the inliers' d2 (any order)
+            // inliers and a lane-parallel sum of the inliers' d2 (any order;
+            // the zero fill of unset lanes adds exactly nothing)
             const uint32_t* im = inl_masks + cand * n_chunks;
             const double* ad = addends + cand * ns_pad;
-            int64_t inl = 0;
+            unsigned pop = 0;
             double part = 0.0;
-            for (int32_t c = 0; c < n_chunks; ++c) {
-                const uint32_t m = __ldg(im + c);
-                inl += __popc(m);
-                if ((m >> lane) & 1u) part += __ldg(ad + static_cast<int64_t>(c) * 32 + lane);
+            for (int32_t s0 = 0; s0 < n_chunks; s0 += 32) {
+                const uint32_t mine = s0 + lane < n_chunks ? __ldg(im + s0 + lane) : 0u;
+                pop += __popc(mine);
+                const int lim = n_chunks - s0 < 32 ? n_chunks - s0 : 32;
+                for (int j0 = 0; j0 < lim; j0 += kBatch) {
+                    double v[kBatch];
+#pragma unroll
+                    for (int j = 0; j < kBatch; ++j) {
+                        const uint32_t m = __shfl_sync(kFull, mine, j0 + j);
+                        v[j] = (j0 + j < lim && ((m >> lane) & 1u))
+                                   ? __ldg(ad + static_cast<int64_t>(s0 + j0 + j) * 32 + lane)
+                                   : 0.0;
+                    }
+#pragma unroll
+                    for (int j = 0; j < kBatch; ++j) part += v[j];
+                }
             }
+            const int64_t inl = static_cast<int64_t>(__reduce_add_sync(kFull, pop));
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(kFull, part, o);
             const double ratio = static_cast<double>(inl) / static_cast<double>(ns);
@@ -965,33 +1030,112 @@ __global__ void __launch_bounds__(kScoreThreads) k_score_exits(int64_t ns, Score
     publish_cta(wt, ctr, block_best, best_offset + blockIdx.x, false);
 }
 
-// Single CTA: the global (max inliers, min approximate fitness) from the
-// per-CTA bests; finalists = qualified candidates with that inlier count whose
-// fitness bound overlaps the minimum's; their exact sequential sums decide
-// under (fitness, hypothesis index) (registration.cpp:272-276); record out.
+// ---- finalists -------------------------------------------------------------
+constexpr int kFinalCtas = 32;
+constexpr int kChainChunks = 128;  // 4096 addends per shared-memory window
+
+// Block-wide exclusive scan of one int per thread (kScoreThreads threads).
+__device__ __forceinline__ int block_exclusive_scan(int v, int* s_warp, int* total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    int base = 0, all = 0;
+#pragma unroll
+    for (int w = 0; w < kScoreWarps; ++w) {
+        const int t = s_warp[w];
+        base += w < warp ? t : 0;
+        all += t;
+    }
+    __syncthreads();
+    *total = all;
+    return base + incl - v;
+}
+
+// Sequential FP64 sum of one candidate's inliers' d2 in point order
+// (registration.cpp:206) by a whole CTA: the CTA compacts a window of 128
+// chunks' addends into shared memory in point order (one scan over the
+// ballots, coalesced gathers by all warps), then thread 0 runs the dependent
+// add chain from shared memory. Result valid in thread 0.
+__device__ double cta_exact_chain(const uint32_t* __restrict__ im, const double* __restrict__ ad, int32_t n_chunks,
+                                  double* buf, uint32_t* s_mask, int* s_off, int* s_warp) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned below = (1u << lane) - 1u;
+    double sum = 0.0;
+    for (int32_t c0 = 0; c0 < n_chunks; c0 += kChainChunks) {
+        const int nc = n_chunks - c0 < kChainChunks ? n_chunks - c0 : kChainChunks;
+        const uint32_t m = threadIdx.x < nc ? __ldg(im + c0 + threadIdx.x) : 0u;
+        int total = 0;
+        const int off = block_exclusive_scan(__popc(m), s_warp, &total);
+        if (threadIdx.x < kChainChunks) {
+            s_mask[threadIdx.x] = m;
+            s_off[threadIdx.x] = off;
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int q = warp; q < nc; q += kScoreWarps) {
+            const uint32_t mq = s_mask[q];
+            if ((mq >> lane) & 1u) buf[s_off[q] + __popc(mq & below)] = __ldg(ad + static_cast<int64_t>(c0 + q) * 32 + lane);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int k = 0;
+            for (; k + 4 <= total; k += 4) {
+                const double x0 = buf[k], x1 = buf[k + 1], x2 = buf[k + 2], x3 = buf[k + 3];
+                sum += x0;
+                sum += x1;
+                sum += x2;
+                sum += x3;
+            }
+            for (; k < total; ++k) sum += buf[k];
+        }
+        __syncthreads();
+    }
+    return sum;
+}
+
+__device__ __forceinline__ bool approx_better(const BestRec& c, const BestRec& g) {
+    return c.valid && (!g.valid || c.inliers > g.inliers || (c.inliers == g.inliers && c.fitness < g.fitness));
+}
+
+// kFinalCtas CTAs. Each one reduces the per-CTA bests to the global (max
+// inliers, min approximate fitness), enumerates the finalists -- qualified
+// candidates with that inlier count whose fitness bound overlaps the
+// minimum's -- in candidate order and takes every kFinalCtas-th; their exact
+// sequential sums decide under (fitness, hypothesis index)
+// (registration.cpp:272-276). The last CTA to finish merges the CTA winners
+// (and the overflow candidates' bests) and writes the rank record.
 __global__ void __launch_bounds__(kScoreThreads) k_score_finalists(int32_t n_chunks, int64_t ns_pad,
                                                                    const uint32_t* __restrict__ inl_masks,
                                                                    const double* __restrict__ addends,
                                                                    const CandInfo* __restrict__ info, int64_t cap,
                                                                    const double* __restrict__ cand_rt,
                                                                    const int64_t* __restrict__ cand_index,
-                                                                   const BestRec* __restrict__ block_best,
+                                                                   BestRec* __restrict__ block_best,
                                                                    int n_best, int64_t sampled,
                                                                    Counters* __restrict__ ctr,
                                                                    RecordDev* __restrict__ rec) {
+    __shared__ double s_buf[kChainChunks * 32];
+    __shared__ uint32_t s_mask[kChainChunks];
+    __shared__ int s_off[kChainChunks];
+    __shared__ int s_warp[kScoreWarps];
     __shared__ BestRec s_red[kScoreWarps];
-    __shared__ int64_t s_final[256];
-    __shared__ int s_nfinal;
-    __shared__ BestRec s_win[kScoreWarps];
-    __shared__ double s_chain[kScoreWarps][256];
+    __shared__ int64_t s_list[kScoreThreads];
+    __shared__ unsigned long long s_ticket;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t n_all = static_cast<int64_t>(ctr->n_candidates);
     const int64_t n_split = n_all < cap ? n_all : cap;
-    // 1. global (max inliers, min fitness) over the per-CTA bests
+    const int64_t prerej = sampled - static_cast<int64_t>(ctr->n_survivors);
+    // 1. global (max inliers, min approximate fitness) over the per-CTA bests
     BestRec g{0, 0, 0.0, INT64_MAX, -1};
     for (int b = threadIdx.x; b < n_best; b += blockDim.x) {
         const BestRec c = block_best[b];
-        if (c.valid && (!g.valid || c.inliers > g.inliers || (c.inliers == g.inliers && c.fitness < g.fitness))) g = c;
+        if (approx_better(c, g)) g = c;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -1001,74 +1145,103 @@ __global__ void __launch_bounds__(kScoreThreads) k_score_finalists(int32_t n_chu
         c.fitness = __shfl_down_sync(kFull, g.fitness, o);
         c.index = __shfl_down_sync(kFull, g.index, o);
         c.slot = __shfl_down_sync(kFull, g.slot, o);
-        if (c.valid && (!g.valid || c.inliers > g.inliers || (c.inliers == g.inliers && c.fitness < g.fitness))) g = c;
+        if (approx_better(c, g)) g = c;
     }
     if (lane == 0) s_red[warp] = g;
-    if (threadIdx.x == 0) s_nfinal = 0;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int w = 1; w < kScoreWarps; ++w) {
-            const BestRec c = s_red[w];
-            if (c.valid && (!g.valid || c.inliers > g.inliers || (c.inliers == g.inliers && c.fitness < g.fitness)))
-                g = c;
-        }
-        s_red[0] = g;
-    }
     __syncthreads();
     g = s_red[0];
-    RecordDev* out = rec;
+    for (int w = 1; w < kScoreWarps; ++w)
+        if (approx_better(s_red[w], g)) g = s_red[w];
+    __syncthreads();
     if (!g.valid) {
-        if (threadIdx.x == 0) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
             RecordDev r{};
             r.index = -1;
             r.sampled = sampled;
-            r.prerejected = static_cast<int64_t>(ctr->prerejected);
+            r.prerejected = prerej;
             r.degenerate = static_cast<int64_t>(ctr->degenerate);
             r.evaluated = n_all;
             r.qualified = static_cast<int64_t>(ctr->qualified);
             r.w_ref = static_cast<int64_t>(ctr->w_ref);
             r.evals_executed = static_cast<int64_t>(ctr->evals_executed);
-            *out = r;
+            *rec = r;
         }
         return;
     }
-    // 2. finalists: same inlier count, fitness within the combined bounds
+    // 2. ordered finalist enumeration; this CTA takes ranks r = blockIdx (mod gridDim)
     const double lim = g.fitness * (1.0 + 2.0 * order_bound(g.inliers)) + 1e-300;
-    for (int64_t k = threadIdx.x; k < n_split; k += blockDim.x) {
-        const CandInfo ci = info[k];
-        if (ci.inliers == g.inliers && ci.fitness <= lim) {
-            const int slot = atomicAdd(&s_nfinal, 1);
-            if (slot < 256) s_final[slot] = k;
+    BestRec mine{0, 0, 0.0, INT64_MAX, -1};
+    int64_t rank0 = 0;
+    for (int64_t k0 = 0; k0 < n_split; k0 += kScoreThreads) {
+        const int64_t k = k0 + threadIdx.x;
+        bool fin = false;
+        if (k < n_split) {
+            const CandInfo ci = info[k];
+            fin = ci.inliers == g.inliers && ci.fitness <= lim;
         }
+        int n_here = 0;
+        const int r = block_exclusive_scan(fin ? 1 : 0, s_warp, &n_here);
+        const int64_t rank = rank0 + r;
+        // compact this CTA's share of the finalists in candidate order
+        int take = 0;
+        const bool my = fin && (rank % gridDim.x) == blockIdx.x;
+        const int pos = block_exclusive_scan(my ? 1 : 0, s_warp, &take);
+        if (my) s_list[pos] = k;
+        __syncthreads();
+        for (int f = 0; f < take; ++f) {
+            const int64_t kk = s_list[f];
+            const CandInfo ci = info[kk];
+            double fit = ci.fitness;
+            if (!ci.exact)
+                fit = cta_exact_chain(inl_masks + kk * n_chunks, addends + kk * ns_pad, n_chunks, s_buf, s_mask, s_off,
+                                      s_warp) /
+                      static_cast<double>(ci.inliers);
+            if (threadIdx.x == 0) {
+                BestRec c{1, ci.inliers, fit, __ldg(cand_index + kk), kk};
+                if (better(c, mine)) mine = c;
+            }
+        }
+        __syncthreads();
+        rank0 += n_here;
+    }
+    // 3. publish; the last CTA merges
+    if (threadIdx.x == 0) {
+        block_best[n_best + blockIdx.x] = mine;
+        __threadfence();
+        s_ticket = atomicAdd(&ctr->fin_done, 1ull);
     }
     __syncthreads();
-    const int nf = s_nfinal;
-    // 3. exact fitness of every finalist (warp per finalist), pick the best
-    BestRec wbest{0, 0, 0.0, INT64_MAX, -1};
-    const bool listed = nf <= 256;  // else (massive ties) rescan the candidates
-    const int64_t n_iter = listed ? nf : n_split;
-    for (int64_t f = warp; f < n_iter; f += kScoreWarps) {
-        const int64_t k = listed ? s_final[f] : f;
-        const CandInfo ci = info[k];
-        if (!listed && !(ci.inliers == g.inliers && ci.fitness <= lim)) continue;
-        double fit = ci.fitness;
-        if (!ci.exact)
-            fit = exact_chain(inl_masks + k * n_chunks, addends + k * ns_pad, n_chunks, s_chain[warp]) /
-                  static_cast<double>(ci.inliers);
-        BestRec c{1, ci.inliers, fit, __ldg(cand_index + k), k};
-        if (better(c, wbest)) wbest = c;
+    if (s_ticket != gridDim.x - 1) return;
+    __threadfence();
+    // the last CTA: CTA winners and the overflow candidates (k_score, exact
+    // already, slot >= cap) in parallel, then a warp / CTA reduction
+    BestRec b{0, 0, 0.0, INT64_MAX, -1};
+    for (int i = threadIdx.x; i < static_cast<int>(gridDim.x) + n_best; i += blockDim.x) {
+        const BestRec* src = i < static_cast<int>(gridDim.x) ? block_best + n_best + i : block_best + (i - gridDim.x);
+        BestRec c;
+        c.valid = __ldcg(&src->valid);
+        c.inliers = __ldcg(&src->inliers);
+        c.fitness = __ldcg(&src->fitness);
+        c.index = __ldcg(&src->index);
+        c.slot = __ldcg(&src->slot);
+        if (i >= static_cast<int>(gridDim.x) && c.slot < cap) continue;
+        if (better(c, b)) b = c;
     }
-    if (lane == 0) s_win[warp] = wbest;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        BestRec c;
+        c.valid = __shfl_down_sync(kFull, b.valid, o);
+        c.inliers = __shfl_down_sync(kFull, b.inliers, o);
+        c.fitness = __shfl_down_sync(kFull, b.fitness, o);
+        c.index = __shfl_down_sync(kFull, b.index, o);
+        c.slot = __shfl_down_sync(kFull, b.slot, o);
+        if (better(c, b)) b = c;
+    }
+    if (lane == 0) s_red[warp] = b;
     __syncthreads();
     if (threadIdx.x != 0) return;
-    BestRec b = s_win[0];
     for (int w = 1; w < kScoreWarps; ++w)
-        if (better(s_win[w], b)) b = s_win[w];
-    // the overflow candidates (k_score, exact already) compete through block_best
-    for (int i = 0; i < n_best; ++i) {
-        const BestRec c = block_best[i];
-        if (c.valid && c.slot >= cap && better(c, b)) b = c;
-    }
+        if (better(s_red[w], b)) b = s_red[w];
     RecordDev r{};
     r.valid = b.valid;
     r.inliers = b.valid ? b.inliers : 0;
@@ -1077,15 +1250,434 @@ __global__ void __launch_bounds__(kScoreThreads) k_score_finalists(int32_t n_chu
     for (int q = 0; q < 9; ++q) r.R[q] = b.valid ? cand_rt[12 * b.slot + q] : 0.0;
     for (int q = 0; q < 3; ++q) r.t[q] = b.valid ? cand_rt[12 * b.slot + 9 + q] : 0.0;
     r.sampled = sampled;
-    r.prerejected = static_cast<int64_t>(ctr->prerejected);
+    r.prerejected = prerej;
     r.degenerate = static_cast<int64_t>(ctr->degenerate);
     r.evaluated = n_all;
     r.qualified = static_cast<int64_t>(ctr->qualified);
     r.w_ref = static_cast<int64_t>(ctr->w_ref);
     r.evals_executed = static_cast<int64_t>(ctr->evals_executed);
-    *out = r;
+    *rec = r;
 }
 
+
+// ---- candidate-CTA scoring ------------------------------------------------
+// One CTA owns one candidate at a time (persistent grid, candidates taken from
+// a ticket counter) and walks its source points in rounds of kCtaPts:
+//   A. every thread transforms its points in FP32 (fine-cell units), settles
+//      the certain misses and appends the rest to a shared-memory queue with
+//      their fine-list (offset, count), or the exact FP64 tag;
+//   B. the queue is resolved densely by all threads (resolve_fine /
+//      eval_point_slow); results land as bits of the round's ballots (double
+//      buffered by round parity); the inliers' d2 go to the CTA's scratch slot
+//      in point order and into per-thread partial sums;
+//   C. every warp applies the reference's miss budget to the round's ballots
+//      (exit => the visited count from the ordered ballots, warp 0).
+// At the end of a candidate the partial sums give its fitness within a
+// rigorous order bound; qualification and the comparison with the CTA's best
+// are decided by the bound, and only when it straddles a decision is the
+// reference's own sequential sum (registration.cpp:206) run from the scratch
+// slot. Each CTA's best ends with its exact sequential sum, so the strict
+// total order (registration.cpp:272-276) across CTAs is exact; the last CTA
+// writes the rank record. Two scratch slots per CTA (current, best) swap
+// instead of copying.
+constexpr int kCtaThreads = 256;
+constexpr int kCtaWarps = kCtaThreads / 32;
+constexpr int kCtaPer = 8;                         // points per thread per round
+constexpr int kCtaPts = kCtaThreads * kCtaPer;     // 2048 points per round
+constexpr int kCtaWords = kCtaPts / 32;            // 64 ballot words per round
+constexpr int kCtaSlow = 0xffff;                   // queue count tag: exact FP64 fallback
+constexpr int kCtaChainChunks = kCtaPts / 32;      // chain window: the queue's 16 KB as doubles
+
+struct CtaSmem {
+    union {
+        int2 q[kCtaPts];            // A/B: (local | count << 16, fine-list offset)
+        double chain[kCtaPts];      // exact chains: compacted addends of 64 chunks
+    };
+    uint32_t inl[2][kCtaWords];
+    uint32_t miss[2][kCtaWords];
+    uint32_t cmask[kCtaChainChunks];
+    int coff[kCtaChainChunks];
+    double R[9], t[3];
+    FastRT F;
+    double red[kCtaWarps];
+    int scan[kCtaWarps];
+    int nq;
+    int flag;
+    int swap;
+    double exact[2];
+    int64_t cand;
+};
+
+// Sequential FP64 sum of one candidate's inliers' d2 in point order
+// (registration.cpp:206) by a whole CTA from its ballot words `im` and
+// addends `ad` (global scratch): 64 chunks at a time are compacted in point
+// order into shared memory, then thread 0 runs the dependent add chain.
+// Result valid in thread 0. All threads must call it.
+__device__ double cta_chain(const uint32_t* im, const double* ad, int32_t n_chunks, CtaSmem& S) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned below = (1u << lane) - 1u;
+    double sum = 0.0;
+    for (int32_t c0 = 0; c0 < n_chunks; c0 += kCtaChainChunks) {
+        const int nc = n_chunks - c0 < kCtaChainChunks ? n_chunks - c0 : kCtaChainChunks;
+        const uint32_t m = threadIdx.x < nc ? __ldcg(im + c0 + threadIdx.x) : 0u;
+        // block exclusive scan of the popcounts
+        const int v = __popc(m);
+        int incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) S.scan[warp] = incl;
+        __syncthreads();
+        int base = 0, total = 0;
+#pragma unroll
+        for (int w = 0; w < kCtaWarps; ++w) {
+            base += w < warp ? S.scan[w] : 0;
+            total += S.scan[w];
+        }
+        if (threadIdx.x < kCtaChainChunks) {
+            S.cmask[threadIdx.x] = m;
+            S.coff[threadIdx.x] = base + incl - v;
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int q = warp; q < nc; q += kCtaWarps) {
+            const uint32_t mq = S.cmask[q];
+            if ((mq >> lane) & 1u) S.chain[S.coff[q] + __popc(mq & below)] = __ldcg(ad + static_cast<int64_t>(c0 + q) * 32 + lane);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int k = 0;
+            for (; k + 4 <= total; k += 4) {
+                const double x0 = S.chain[k], x1 = S.chain[k + 1], x2 = S.chain[k + 2], x3 = S.chain[k + 3];
+                sum += x0;
+                sum += x1;
+                sum += x2;
+                sum += x3;
+            }
+            for (; k < total; ++k) sum += S.chain[k];
+        }
+        __syncthreads();
+    }
+    return sum;
+}
+
+__global__ void __launch_bounds__(kCtaThreads, 4) k_score_cta(SourceView src, const __grid_constant__ GridView g,
+                                                               const __grid_constant__ ScoreParams sp,
+                                                               const double* __restrict__ cand_rt,
+                                                               const int64_t* __restrict__ cand_index,
+                                                               int64_t sampled, int64_t ns_pad,
+                                                               double* __restrict__ scr_add,
+                                                               uint32_t* __restrict__ scr_inl,
+                                                               Counters* __restrict__ ctr,
+                                                               BestRec* __restrict__ block_best,
+                                                               RecordDev* __restrict__ rec) {
+    __shared__ CtaSmem S;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t n_cand = static_cast<int64_t>(ctr->n_candidates);
+    const int64_t ns = src.n;
+    const int32_t n_chunks = static_cast<int32_t>(ns_pad / 32);
+    // the CTA's two scratch slots: addends (ns_pad) and ballot words (n_chunks)
+    double* slot_add[2] = {scr_add + (2 * static_cast<int64_t>(blockIdx.x)) * ns_pad,
+                           scr_add + (2 * static_cast<int64_t>(blockIdx.x) + 1) * ns_pad};
+    uint32_t* slot_inl[2] = {scr_inl + (2 * static_cast<int64_t>(blockIdx.x)) * n_chunks,
+                             scr_inl + (2 * static_cast<int64_t>(blockIdx.x) + 1) * n_chunks};
+    int cur = 0;  // slot of the candidate in progress; the best lives in 1 - cur
+    // thread 0's books: the CTA best (fitness exact when best_eb == 0)
+    BestRec best{0, 0, 0.0, INT64_MAX, -1};
+    double best_eb = 0.0;
+    unsigned long long t_qual = 0, t_wref = 0, t_exec = 0;
+    for (;;) {
+        if (threadIdx.x == 0) S.cand = static_cast<int64_t>(atomicAdd(&ctr->work_next, 1ull));
+        if (threadIdx.x < 2 * kCtaWords) {
+            (&S.inl[0][0])[threadIdx.x] = 0u;
+            (&S.miss[0][0])[threadIdx.x] = 0u;
+        }
+        __syncthreads();
+        const int64_t cand = S.cand;
+        if (cand >= n_cand) break;
+        if (threadIdx.x < 12) {
+            const double v = __ldg(cand_rt + 12 * cand + threadIdx.x);
+            if (threadIdx.x < 9) S.R[threadIdx.x] = v;
+            else S.t[threadIdx.x - 9] = v;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            S.F = make_fast_fine(S.R, S.t, g, sp);
+            S.nq = 0;
+        }
+        __syncthreads();
+        const FastRT& F = S.F;
+        double* add = slot_add[cur];
+        uint32_t* inlw = slot_inl[cur];
+        double part = 0.0;
+        int64_t misses = 0, inliers = 0, visited = ns, done = ns;
+        bool exited = false;
+        for (int64_t base = 0, r = 0; base < ns; base += kCtaPts, ++r) {
+            const int b = static_cast<int>(r & 1);
+            // A. FP32 location of the round's points
+#pragma unroll
+            for (int u = 0; u < kCtaPer; ++u) {
+                const int local = u * kCtaThreads + threadIdx.x;
+                const int64_t i = base + local;
+                int state = 0;  // 0 certain miss, 1 exact fallback, 2 fine-list scan
+                int2 bi = make_int2(0, 0);
+                if (i < ns) {
+                    if (F.ok == 0.0f) {
+                        state = 1;
+                    } else {
+                        const float4 P = __ldg(src.pos32 + i);
+                        const float qx = fmaf(F.r[0], P.x, fmaf(F.r[1], P.y, fmaf(F.r[2], P.z, F.t[0])));
+                        const float qy = fmaf(F.r[3], P.x, fmaf(F.r[4], P.y, fmaf(F.r[5], P.z, F.t[1])));
+                        const float qz = fmaf(F.r[6], P.x, fmaf(F.r[7], P.y, fmaf(F.r[8], P.z, F.t[2])));
+                        const float eps = F.eps;
+                        if (!(qx < -eps || qy < -eps || qz < -eps || qx >= g.fnx + eps || qy >= g.fny + eps ||
+                              qz >= g.fnz + eps)) {
+                            const float fx = floorf(qx), fy = floorf(qy), fz = floorf(qz);
+                            const float rx = qx - fx, ry = qy - fy, rz = qz - fz;
+                            if (rx < eps || rx > 1.0f - eps || ry < eps || ry > 1.0f - eps || rz < eps ||
+                                rz > 1.0f - eps) {
+                                state = 1;
+                            } else {
+                                const int ix = static_cast<int>(fx), iy = static_cast<int>(fy),
+                                          iz = static_cast<int>(fz);
+                                if (ix >= 0 && iy >= 0 && iz >= 0 && ix < g.fnx && iy < g.fny && iz < g.fnz) {
+                                    bi = __ldg(g.fine_info + (static_cast<int64_t>(ix) * g.fny + iy) * g.fnz + iz);
+                                    if (bi.y > 0) state = bi.y < kCtaSlow ? 2 : 1;
+                                }
+                            }
+                        }
+                    }
+                }
+                const unsigned mm = __ballot_sync(kFull, i < ns && state == 0);
+                if (lane == 0) S.miss[b][local >> 5] = mm;
+                const unsigned m = __ballot_sync(kFull, state != 0);
+                int slot = 0;
+                if (m) {
+                    const int leader = __ffs(m) - 1;
+                    if (lane == leader) slot = atomicAdd(&S.nq, __popc(m));
+                    slot = __shfl_sync(kFull, slot, leader) + __popc(m & ((1u << lane) - 1u));
+                }
+                if (state != 0) S.q[slot] = make_int2(local | ((state == 1 ? kCtaSlow : bi.y) << 16), bi.x);
+            }
+            __syncthreads();
+            // B. dense resolution of the queue; the next round's ballots are cleared
+            const int nq = S.nq;
+            if (threadIdx.x < kCtaWords) {
+                S.inl[b ^ 1][threadIdx.x] = 0u;
+                S.miss[b ^ 1][threadIdx.x] = 0u;
+            }
+            for (int e = threadIdx.x; e < nq; e += kCtaThreads) {
+                const int2 qe = S.q[e];
+                const int local = qe.x & 0xffff;
+                const int cnt = static_cast<int>(static_cast<unsigned>(qe.x) >> 16);
+                const int64_t i = base + local;
+                double addend = 0.0;
+                bool inl;
+                if (cnt == kCtaSlow) {
+                    inl = eval_point_slow(g, cand_rt + 12 * cand, src, i, sp, &addend);
+                } else {
+                    const float4 P = __ldg(src.pos32 + i);
+                    const float qx = fmaf(F.r[0], P.x, fmaf(F.r[1], P.y, fmaf(F.r[2], P.z, F.t[0])));
+                    const float qy = fmaf(F.r[3], P.x, fmaf(F.r[4], P.y, fmaf(F.r[5], P.z, F.t[1])));
+                    const float qz = fmaf(F.r[6], P.x, fmaf(F.r[7], P.y, fmaf(F.r[8], P.z, F.t[2])));
+                    inl = resolve_fine(g, S.R, S.t, F, ld3(src.pos, i), ld3(src.nrm, i), qx, qy, qz, qe.y, cnt, sp,
+                                       addend);
+                }
+                const int word = local >> 5;  // ballot word w covers points base + 32 w ..
+                const uint32_t bit = 1u << (local & 31);
+                if (inl) {
+                    atomicOr(&S.inl[b][word], bit);
+                    add[i] = addend;
+                    part += addend;
+                } else {
+                    atomicOr(&S.miss[b][word], bit);
+                }
+            }
+            __syncthreads();
+            // C. the miss budget in point order (word w covers points base + 32 w ..)
+            if (threadIdx.x == 0) S.nq = 0;
+            const uint32_t m0 = S.miss[b][lane], m1 = S.miss[b][32 + lane];
+            const int c0 = __popc(m0), c1 = __popc(m1);
+            const int round_misses = __reduce_add_sync(kFull, static_cast<unsigned>(c0 + c1));
+            if (misses + round_misses > sp.miss_budget) {
+                exited = true;
+                if (warp == 0) {
+                    int64_t before = misses;
+                    for (int h = 0; h < 2; ++h) {
+                        const uint32_t mw = h ? m1 : m0;
+                        const int cnt = h ? c1 : c0;
+                        int incl = cnt;
+#pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const int y = __shfl_up_sync(kFull, incl, o);
+                            if (lane >= o) incl += y;
+                        }
+                        const unsigned over = __ballot_sync(kFull, before + incl > sp.miss_budget);
+                        if (over) {
+                            const int L = __ffs(over) - 1;
+                            const int64_t bef = before + __shfl_sync(kFull, incl - cnt, L);
+                            unsigned m = __shfl_sync(kFull, mw, L);
+                            const int need = static_cast<int>(sp.miss_budget - bef);
+                            for (int q = 0; q < need; ++q) m &= m - 1;
+                            visited = base + static_cast<int64_t>(h * 32 + L) * 32 + (__ffs(m) - 1) + 1;
+                            break;
+                        }
+                        before += __shfl_sync(kFull, incl, 31);
+                    }
+                }
+                const int64_t end = base + kCtaPts;
+                done = end < ns ? end : ns;
+                break;
+            }
+            misses += round_misses;
+            if (warp == 0) {
+                const uint32_t i0 = S.inl[b][lane], i1 = S.inl[b][32 + lane];
+                const int64_t w0 = base / 32 + lane;
+                if (w0 < n_chunks) inlw[w0] = i0;
+                if (w0 + 32 < n_chunks) inlw[w0 + 32] = i1;
+                inliers += __reduce_add_sync(kFull, static_cast<unsigned>(__popc(i0) + __popc(i1)));
+            }
+        }
+        // the candidate's verdict (thread 0 decides, the CTA runs exact chains on demand)
+        if (!exited) {
+            double v = part;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+            if (lane == 0) S.red[warp] = v;
+        }
+        __syncthreads();
+        int need = 0;  // bit 0: chain the candidate, bit 1: chain the best
+        double fit = 0.0, eb = 0.0;
+        bool qual_sure = false;
+        if (threadIdx.x == 0) {
+            t_wref += static_cast<unsigned long long>(visited);
+            t_exec += static_cast<unsigned long long>(done);
+            if (!exited) {
+                const double ratio = static_cast<double>(inliers) / static_cast<double>(ns);
+                if (!(ratio < sp.min_ratio)) {
+                    double s = 0.0;
+                    for (int w = 0; w < kCtaWarps; ++w) s += S.red[w];
+                    fit = inliers > 0 ? s / static_cast<double>(inliers) : 0.0;
+                    eb = inliers > 0 ? order_bound(inliers) * fit : 0.0;
+                    const bool may = !(fit - eb > sp.max_fitness);
+                    qual_sure = fit + eb <= sp.max_fitness;
+                    if (may) {
+                        need |= 16;
+                        if (!qual_sure) need |= 1;
+                        if (best.valid && inliers == best.inliers && fabs(fit - best.fitness) <= eb + best_eb) {
+                            need |= 1;
+                            if (best_eb != 0.0) need |= 2;
+                        }
+                    }
+                }
+            }
+            S.flag = need;
+            S.swap = 0;
+        }
+        __syncthreads();
+        need = S.flag;
+        if (need & 1) {
+            const double s = cta_chain(inlw, add, n_chunks, S);
+            if (threadIdx.x == 0) S.exact[0] = s;
+        }
+        if (need & 2) {
+            const double s = cta_chain(slot_inl[1 - cur], slot_add[1 - cur], n_chunks, S);
+            if (threadIdx.x == 0) S.exact[1] = s;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && (need & 16)) {
+            if (need & 2) {
+                best.fitness = S.exact[1] / static_cast<double>(best.inliers);
+                best_eb = 0.0;
+            }
+            bool qual = qual_sure;
+            if (need & 1) {
+                fit = S.exact[0] / static_cast<double>(inliers);
+                eb = 0.0;
+                qual = !(fit > sp.max_fitness);
+            }
+            if (qual) {
+                t_qual += 1;
+                const BestRec c{1, inliers, fit, __ldg(cand_index + cand), cand};
+                bool take;
+                if (!best.valid || inliers != best.inliers) take = !best.valid || inliers > best.inliers;
+                else if (eb == 0.0 && best_eb == 0.0) take = better(c, best);
+                else take = fit < best.fitness;  // bounds disjoint (else both were chained)
+                if (take) {
+                    best = c;
+                    best_eb = eb;
+                    S.swap = 1;  // the candidate's slot becomes the best's
+                }
+            }
+        }
+        __syncthreads();
+        if (S.swap) cur = 1 - cur;
+        __syncthreads();
+    }
+    // the CTA best's exact sum
+    if (threadIdx.x == 0) S.flag = (best.valid && best_eb != 0.0) ? 1 : 0;
+    __syncthreads();
+    if (S.flag) {
+        const double s = cta_chain(slot_inl[1 - cur], slot_add[1 - cur], n_chunks, S);
+        if (threadIdx.x == 0) best.fitness = s / static_cast<double>(best.inliers);
+    }
+    // publish the CTA's tallies and best; the last CTA writes the record
+    __shared__ unsigned long long s_ticket;
+    if (threadIdx.x == 0) {
+        if (t_qual) atomicAdd(&ctr->qualified, t_qual);
+        if (t_wref) atomicAdd(&ctr->w_ref, t_wref);
+        if (t_exec) atomicAdd(&ctr->evals_executed, t_exec);
+        block_best[blockIdx.x] = best;
+        __threadfence();
+        s_ticket = atomicAdd(&ctr->fin_done, 1ull);
+    }
+    __syncthreads();
+    if (s_ticket != gridDim.x - 1) return;
+    __threadfence();
+    BestRec b{0, 0, 0.0, INT64_MAX, -1};
+    for (int i = threadIdx.x; i < static_cast<int>(gridDim.x); i += blockDim.x) {
+        BestRec c;
+        c.valid = __ldcg(&block_best[i].valid);
+        c.inliers = __ldcg(&block_best[i].inliers);
+        c.fitness = __ldcg(&block_best[i].fitness);
+        c.index = __ldcg(&block_best[i].index);
+        c.slot = __ldcg(&block_best[i].slot);
+        if (better(c, b)) b = c;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        BestRec c;
+        c.valid = __shfl_down_sync(kFull, b.valid, o);
+        c.inliers = __shfl_down_sync(kFull, b.inliers, o);
+        c.fitness = __shfl_down_sync(kFull, b.fitness, o);
+        c.index = __shfl_down_sync(kFull, b.index, o);
+        c.slot = __shfl_down_sync(kFull, b.slot, o);
+        if (better(c, b)) b = c;
+    }
+    __shared__ BestRec s_red[kCtaWarps];
+    if (lane == 0) s_red[warp] = b;
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    for (int w = 1; w < kCtaWarps; ++w)
+        if (better(s_red[w], b)) b = s_red[w];
+    RecordDev r{};
+    r.valid = b.valid;
+    r.inliers = b.valid ? b.inliers : 0;
+    r.fitness = b.valid ? b.fitness : 0.0;
+    r.index = b.valid ? b.index : -1;
+    for (int q = 0; q < 9; ++q) r.R[q] = b.valid ? cand_rt[12 * b.slot + q] : 0.0;
+    for (int q = 0; q < 3; ++q) r.t[q] = b.valid ? cand_rt[12 * b.slot + 9 + q] : 0.0;
+    r.sampled = sampled;
+    r.prerejected = sampled - static_cast<int64_t>(__ldcg(&ctr->n_survivors));
+    r.degenerate = static_cast<int64_t>(__ldcg(&ctr->degenerate));
+    r.evaluated = n_cand;
+    r.qualified = static_cast<int64_t>(__ldcg(&ctr->qualified));
+    r.w_ref = static_cast<int64_t>(__ldcg(&ctr->w_ref));
+    r.evals_executed = static_cast<int64_t>(__ldcg(&ctr->evals_executed));
+    *rec = r;
+}
 
 int blocks_per_sm(const void* fn) {
     int b = 0;
@@ -1102,6 +1694,23 @@ int split_blocks_per_sm() {
     static int cached = 0;
     if (!cached) cached = blocks_per_sm(reinterpret_cast<const void*>(k_score_split));
     return cached;
+}
+
+int cand_blocks_per_sm() {
+    static int cached = 0;
+    if (!cached) cached = blocks_per_sm(reinterpret_cast<const void*>(k_score_cta));
+    return cached;
+}
+
+// LK_SCORE_SPLIT=1 selects the (candidate x chunk) split scorer instead of the
+// candidate-CTA scorer (both exact; kept for comparison).
+bool split_scoring() {
+    static int cached = -1;
+    if (cached < 0) {
+        const char* v = std::getenv("LK_SCORE_SPLIT");
+        cached = (v && v[0] == '1') ? 1 : 0;
+    }
+    return cached == 1;
 }
 
 int resolve_blocks_per_sm() {
@@ -1127,6 +1736,12 @@ void RunBuffers::release() {
     pool_free(cand_fine, stream);
     pool_free(queue, stream);
     pool_free(queue_counts, stream);
+    pool_free(cta_add, stream);
+    pool_free(cta_inl, stream);
+    cta_add = nullptr;
+    cta_inl = nullptr;
+    cta_slots = 0;
+    cta_ns_pad = 0;
     queue_counts = nullptr;
     full_list = nullptr;
     cand_fast = nullptr;
@@ -1172,6 +1787,25 @@ cudaError_t RunBuffers::ensure(int64_t cap, int32_t score_blocks) {
         if ((e = pool_alloc(&cand_rt, cap * 12 * sizeof(double), stream)) != cudaSuccess) return e;
         capacity = cap;
     }
+    return cudaSuccess;
+}
+
+cudaError_t RunBuffers::ensure_cta(int64_t ns, int32_t n_ctas) {
+    const int64_t ns_pad = (ns + 31) / 32 * 32;
+    if (n_ctas <= cta_slots && ns_pad == cta_ns_pad) return cudaSuccess;
+    pool_free(cta_add, stream);
+    pool_free(cta_inl, stream);
+    cta_add = nullptr;
+    cta_inl = nullptr;
+    cta_slots = 0;
+    cudaError_t e;
+    if ((e = pool_alloc(&cta_add, 2 * static_cast<int64_t>(n_ctas) * ns_pad * sizeof(double), stream)) != cudaSuccess)
+        return e;
+    if ((e = pool_alloc(&cta_inl, 2 * static_cast<int64_t>(n_ctas) * (ns_pad / 32) * sizeof(uint32_t), stream)) !=
+        cudaSuccess)
+        return e;
+    cta_slots = n_ctas;
+    cta_ns_pad = ns_pad;
     return cudaSuccess;
 }
 
@@ -1234,19 +1868,26 @@ cudaError_t run_hypotheses_range(const SourceView& src, const double* d_tgt_pos,
     const int split_blocks = sm_count * split_blocks_per_sm();
     const int exit_blocks = sm_count * 2;
     const int over_blocks = sm_count;
-    cudaError_t e = rb.ensure(count > 0 ? count : 1, exit_blocks + over_blocks);
+    const int cand_blocks = sm_count * cand_blocks_per_sm();
+    const int n_best_slots = exit_blocks + over_blocks + kFinalCtas;
+    cudaError_t e = rb.ensure(count > 0 ? count : 1, n_best_slots > cand_blocks ? n_best_slots : cand_blocks);
     if (e != cudaSuccess) return e;
-    // split capacity: a few percent of the hypotheses survive pre-rejection in
-    // practice; any excess is scored by the streaming k_score (exact too)
-    const int64_t want_split = count / 64 > 4096 ? count / 64 : 4096;
-    if ((e = rb.ensure_split(src.n, want_split < count ? want_split : (count > 0 ? count : 1))) != cudaSuccess)
+    const bool split = split_scoring();
+    if (split) {
+        // split capacity: a few percent of the hypotheses survive pre-rejection in
+        // practice; any excess is scored by the streaming k_score (exact too)
+        const int64_t want_split = count / 64 > 4096 ? count / 64 : 4096;
+        if ((e = rb.ensure_split(src.n, want_split < count ? want_split : (count > 0 ? count : 1))) != cudaSuccess)
+            return e;
+        if ((e = rb.ensure_fast(count > 0 ? count : 1)) != cudaSuccess) return e;
+        if ((e = cudaMemsetAsync(rb.queue_counts, 0, kQueueParts * kQueueStride * sizeof(unsigned long long),
+                                 stream)) != cudaSuccess)
+            return e;
+    } else if ((e = rb.ensure_cta(src.n, cand_blocks)) != cudaSuccess) {
         return e;
-    if ((e = rb.ensure_fast(count > 0 ? count : 1)) != cudaSuccess) return e;
+    }
     FastRT* cand_fast = static_cast<FastRT*>(rb.cand_fast);
     if ((e = cudaMemsetAsync(rb.counters, 0, sizeof(Counters), stream)) != cudaSuccess) return e;
-    if ((e = cudaMemsetAsync(rb.queue_counts, 0, kQueueParts * kQueueStride * sizeof(unsigned long long), stream)) !=
-        cudaSuccess)
-        return e;
     const uint32_t ns = static_cast<uint32_t>(src.n);
     const uint32_t thresh = static_cast<uint32_t>(0x100000000ull % ns);
     const int32_t n_chunks = static_cast<int32_t>((src.n + 31) / 32);
@@ -1254,8 +1895,25 @@ cudaError_t run_hypotheses_range(const SourceView& src, const double* d_tgt_pos,
     if (count > 0) {
         int64_t want = (count + 255) / 256;
         unsigned gs = static_cast<unsigned>(want < sm_count * 16 ? want : sm_count * 16);
+        PrefetchList pf{};
+        auto add = [&](const void* ptr, int64_t bytes) {
+            // 16-byte aligned start (allocations are), whole 16-byte granules
+            if (ptr && bytes >= 16 && pf.n < PrefetchList::kMax) {
+                pf.ptr[pf.n] = static_cast<const char*>(ptr);
+                pf.bytes[pf.n] = static_cast<unsigned long long>(bytes);
+                ++pf.n;
+            }
+        };
+        add(grid.fine_info, grid.n_fine * static_cast<int64_t>(sizeof(int2)));
+        add(grid.fine_pts, grid.n_fine_entries * static_cast<int64_t>(sizeof(float4)));
+        add(grid.pos_orig, grid.n_points * 24);
+        add(grid.nrm_orig, grid.n_points * 24);
+        add(src.pos32, src.n * static_cast<int64_t>(sizeof(float4)));
+        add(src.pos, src.n * 24);
+        add(src.nrm, src.n * 24);
+        if (static_cast<int64_t>(gs) < pf.n) pf.n = static_cast<int>(gs);
         k_hyp_sample<<<gs, 256, 0, stream>>>(begin, count, splitmix64(seed), ns, thresh, d_cache, src.pos, d_tgt_pos,
-                                             tau, rb.surv_index, rb.surv_ids, rb.counters);
+                                             tau, rb.surv_index, rb.surv_ids, rb.counters, pf);
     }
     if (events) cudaEventRecord(events[1], stream);
     if (count > 0) {
@@ -1263,17 +1921,33 @@ cudaError_t run_hypotheses_range(const SourceView& src, const double* d_tgt_pos,
                                                    rb.cand_rt, rb.counters);
     }
     if (events) cudaEventRecord(events[2], stream);
+    if (!split) {
+        // candidate-CTA scoring: one persistent kernel, record included
+        if (events) cudaEventRecord(events[3], stream);
+        k_score_cta<<<cand_blocks, kCtaThreads, 0, stream>>>(src, grid, sp, rb.cand_rt, rb.cand_index, count,
+                                                            rb.cta_ns_pad, rb.cta_add, rb.cta_inl, rb.counters,
+                                                            rb.block_best, static_cast<RecordDev*>(d_record));
+        if (events) {
+            cudaEventRecord(events[4], stream);
+            cudaEventRecord(events[5], stream);
+            cudaEventRecord(events[6], stream);
+        }
+        return cudaGetLastError();
+    }
     FastRT* cand_fine = static_cast<FastRT*>(rb.cand_fine);
     k_prep_fast<<<sm_count * 2, 128, 0, stream>>>(rb.cand_rt, -1, rb.counters, grid, sp, cand_fast);
     k_prep_fast_fine<<<sm_count * 2, 128, 0, stream>>>(rb.cand_rt, rb.counters, grid, sp, cand_fine);
+    if (events) cudaEventRecord(events[3], stream);
     const int64_t part_cap = rb.queue_cap / kQueueParts;
     k_score_split<<<split_blocks, kScoreThreads, 0, stream>>>(src, grid, sp, rb.cand_rt, cand_fine, rb.split_cap,
                                                               n_chunks, rb.split_ns_pad, rb.inl_masks, rb.miss_masks,
                                                               rb.addends, rb.queue, part_cap, rb.queue_counts,
                                                               rb.counters);
+    if (events) cudaEventRecord(events[4], stream);
     k_score_resolve<<<sm_count * resolve_blocks_per_sm(), kScoreThreads, 0, stream>>>(
         src, grid, sp, rb.cand_rt, cand_fine, n_chunks, rb.split_ns_pad, rb.queue, part_cap, rb.queue_counts,
         rb.inl_masks, rb.miss_masks, rb.addends);
+    if (events) cudaEventRecord(events[5], stream);
     // candidates beyond the split capacity (normally none): streamed warp per candidate
     k_score<<<over_blocks, kScoreThreads, 0, stream>>>(src, grid, sp, rb.cand_rt, cand_fast, rb.cand_index,
                                                        rb.split_cap, -1,
@@ -1283,11 +1957,11 @@ cudaError_t run_hypotheses_range(const SourceView& src, const double* d_tgt_pos,
     k_score_exits<<<exit_blocks, kScoreThreads, 0, stream>>>(src.n, sp, rb.split_cap, n_chunks, rb.split_ns_pad,
                                                              rb.miss_masks, rb.inl_masks, rb.addends, info,
                                                              rb.counters, rb.block_best, 0);
-    k_score_finalists<<<1, kScoreThreads, 0, stream>>>(n_chunks, rb.split_ns_pad, rb.inl_masks, rb.addends, info,
+    k_score_finalists<<<kFinalCtas, kScoreThreads, 0, stream>>>(n_chunks, rb.split_ns_pad, rb.inl_masks, rb.addends, info,
                                                        rb.split_cap, rb.cand_rt, rb.cand_index, rb.block_best,
                                                        exit_blocks + over_blocks, count, rb.counters,
                                                        static_cast<RecordDev*>(d_record));
-    if (events) cudaEventRecord(events[3], stream);
+    if (events) cudaEventRecord(events[6], stream);
     return cudaGetLastError();
 }
 

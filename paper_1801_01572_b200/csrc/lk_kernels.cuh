@@ -57,6 +57,8 @@ struct GridView {
     double fine_dmax;
     const int2* fine_info;
     const float4* fine_pts;
+    // sizes (elements) of the arrays above, for L2 prefetching
+    int64_t n_points, n_cells, n_fine, n_fine_entries;
 };
 
 struct GridStorage {
@@ -99,7 +101,8 @@ struct Counters {  // device-side, zeroed per run
     unsigned long long work_next;   // work queue head for k_score
     unsigned long long blocks_done; // last-block-done ticket
     unsigned long long n_full;      // split candidates that were fully scored
-    unsigned long long _pad[6];
+    unsigned long long fin_done;    // k_score_finalists last-CTA ticket
+    unsigned long long _pad[5];
 };
 
 struct BestRec {  // per-block best, then the final record
@@ -139,6 +142,11 @@ struct RunBuffers {
     cudaError_t ensure(int64_t cap, int32_t score_blocks);
     cudaError_t ensure_split(int64_t ns, int64_t max_candidates);
     cudaError_t ensure_fast(int64_t n);
+    // candidate-CTA scoring: two scratch slots per CTA (addends + ballot words)
+    double* cta_add = nullptr;
+    uint32_t* cta_inl = nullptr;
+    int64_t cta_slots = 0, cta_ns_pad = 0;
+    cudaError_t ensure_cta(int64_t ns, int32_t n_ctas);
 };
 
 struct SourceView {
@@ -172,8 +180,10 @@ cudaError_t make_source32(const double* d_pos, int64_t n, float4* d_out, cudaStr
 
 // Samples, pre-rejects and fits hypotheses [begin, end); scores the
 // candidates; reduces the per-run best into `record` (an lk_reg_record, device).
-// `events` (nullable): 4 events recorded before k_hyp_sample, k_kabsch,
-// k_score and after k_score, for per-kernel timing on the launch stream.
+// `events` (nullable): kPhaseEvents events on the launch stream bracketing the
+// phases k_hyp_sample | k_kabsch | k_prep_fast(_fine) | k_score_split |
+// k_score_resolve | k_score + k_score_exits + k_score_finalists.
+constexpr int kPhaseEvents = 7;
 cudaError_t run_hypotheses_range(const SourceView& src, const double* d_tgt_pos, const int32_t* d_cache,
                                  const GridView& grid, const ScoreParams& sp, uint64_t seed, double tau, int64_t begin,
                                  int64_t end, RunBuffers& rb, void* d_record, cudaStream_t stream, int sm_count,

@@ -198,6 +198,16 @@ class RegistrationContext:
         check(abi.lib().lk_reg_ctx_kernel_times(self._h, ms, C.byref(runs), 1 if reset else 0))
         return dict(zip(("k_hyp_sample", "k_kabsch", "k_score"), ms[:])), runs.value
 
+    PHASES = ("k_hyp_sample", "k_kabsch", "k_prep_fast", "k_score_split", "k_score_resolve", "score_tail")
+
+    def phase_times(self, reset: bool = False):
+        """({phase: ms}, runs): the same events split per scoring phase
+        (score_tail = k_score overflow + k_score_exits + k_score_finalists)."""
+        ms = (C.c_double * len(self.PHASES))()
+        runs = C.c_int64()
+        check(abi.lib().lk_reg_ctx_phase_times(self._h, ms, len(self.PHASES), C.byref(runs), 1 if reset else 0))
+        return dict(zip(self.PHASES, ms[:])), runs.value
+
     def download(self):
         """(source, target, cache, source_features, target_features) on the host."""
         ns, nt = self.n_source, self.n_target
