@@ -283,6 +283,8 @@ struct lk_reg_ctx {
     double *d_spos = nullptr, *d_snrm = nullptr, *d_tpos = nullptr, *d_tnrm = nullptr;
     float *d_sfeat = nullptr, *d_tfeat = nullptr;  // FPFH (prepare_registration only)
     float4* d_spos32 = nullptr;  // FP32 copy of the source for the guard-band scan
+    double4* d_spos4 = nullptr;  // (x, y, z, 0) FP64 source records
+    float4* d_snrm32 = nullptr;  // FP32 source normals (guarded normal gate)
     double src_max_norm = 0.0;
     int32_t* d_cache = nullptr;
     lkk::GridStorage grid;
@@ -314,6 +316,8 @@ struct lk_reg_ctx {
         cudaStream_t s = own_stream;
         lkk::pool_free(d_spos, s);
         lkk::pool_free(d_spos32, s);
+        lkk::pool_free(d_spos4, s);
+        lkk::pool_free(d_snrm32, s);
         lkk::pool_free(d_snrm, s);
         lkk::pool_free(d_tpos, s);
         lkk::pool_free(d_tnrm, s);
@@ -338,6 +342,9 @@ void ctx_finish_source(lk_reg_ctx* c) {
     cudaStream_t s = c->stream;
     CK(lkk::pool_alloc(&c->d_spos32, std::max<int64_t>(c->ns, 1) * sizeof(float4), s));
     CK(lkk::make_source32(c->d_spos, c->ns, c->d_spos32, s));
+    CK(lkk::pool_alloc(&c->d_spos4, std::max<int64_t>(c->ns, 1) * sizeof(double4), s));
+    CK(lkk::pool_alloc(&c->d_snrm32, std::max<int64_t>(c->ns, 1) * sizeof(float4), s));
+    CK(lkk::make_records(c->d_spos, c->d_snrm, c->ns, c->d_spos4, c->d_snrm32, s));
     CK(lkk::pool_alloc(&c->d_record, sizeof(lk_reg_record), s));
 }
 
@@ -485,7 +492,7 @@ lk_status run_range_impl(lk_reg_ctx* c, const lk_reg_params& p, int64_t begin, i
     if (!c->d_cache) return fail(LK_MISSING_DATA, "sample_quadruple: no correspondence cache");
     if (begin < 0 || end < begin) return fail(LK_INVALID_ARGUMENT, "bad hypothesis range");
     CK(cudaSetDevice(c->device));
-    lkk::SourceView sv{c->d_spos, c->d_snrm, c->d_spos32, c->ns};
+    lkk::SourceView sv{c->d_spos, c->d_snrm, c->d_spos32, c->ns, c->d_spos4, c->d_snrm32};
     lkk::ScoreParams sp = score_params(p, c->ns, true, false);
     if (fast_path_enabled()) lkk::configure_fast_path(sp, c->grid.view, c->src_max_norm);
     cudaEvent_t* ev = nullptr;

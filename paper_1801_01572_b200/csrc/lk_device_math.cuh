@@ -25,6 +25,13 @@ __device__ __forceinline__ V3 ld3(const double* __restrict__ p, int64_t i) {
     return V3{__ldg(p + 3 * i), __ldg(p + 3 * i + 1), __ldg(p + 3 * i + 2)};
 }
 
+// (x, y, z, 0) records: one 32-byte sector per point, two 16-byte loads
+__device__ __forceinline__ V3 ld4(const double4* __restrict__ p, int64_t i) {
+    const double2* q = reinterpret_cast<const double2*>(p + i);
+    const double2 a = __ldg(q), b = __ldg(q + 1);
+    return V3{a.x, a.y, b.x};
+}
+
 // Matrix3d * Vector3d: rows 0-1 ((a0 + a1) + a2), row 2 a0 + (a1 + a2).
 // R is row-major r[9].
 __device__ __forceinline__ V3 rot(const double* r, V3 v) {

@@ -500,6 +500,10 @@ void GridStorage::release() {
     pool_free(nrm_orig, stream);
     pool_free(block_f32, stream);
     pool_free(pos_orig, stream);
+    pool_free(pos4_orig, stream);
+    pool_free(nrm32_orig, stream);
+    pos4_orig = nullptr;
+    nrm32_orig = nullptr;
     pool_free(fine_info, stream);
     pool_free(fine_pts, stream);
     fine_info = nullptr;
@@ -653,12 +657,35 @@ cudaError_t build_grid(GridStorage& g, int kind, const double* d_pos, const doub
     v.pos_orig = g.pos_orig;
     v.fine_info = g.fine_info;
     v.fine_pts = g.fine_pts;
+    if (g.pos_orig && g.nrm_orig && n > 0) {
+        LK_TRY(pool_alloc(&g.pos4_orig, n * sizeof(double4), stream));
+        LK_TRY(pool_alloc(&g.nrm32_orig, n * sizeof(float4), stream));
+        LK_TRY(make_records(g.pos_orig, g.nrm_orig, n, g.pos4_orig, g.nrm32_orig, stream));
+    }
+    v.pos4_orig = g.pos4_orig;
+    v.nrm32_orig = g.nrm32_orig;
     v.n_points = g.npoints;
     v.n_cells = g.ncells;
     v.n_fine = g.nfine;
     v.n_fine_entries = g.fine_pts ? g.nfine_entries : 0;
     g.view = v;
     return cudaStreamSynchronize(stream);
+}
+
+__global__ void k_records(const double* __restrict__ pos, const double* __restrict__ nrm, int64_t n,
+                          double4* __restrict__ pos4, float4* __restrict__ nrm32) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    if (pos4) pos4[i] = make_double4(pos[3 * i], pos[3 * i + 1], pos[3 * i + 2], 0.0);
+    if (nrm32)
+        nrm32[i] = make_float4(static_cast<float>(nrm[3 * i]), static_cast<float>(nrm[3 * i + 1]),
+                               static_cast<float>(nrm[3 * i + 2]), 0.0f);
+}
+
+cudaError_t make_records(const double* d_pos, const double* d_nrm, int64_t n, double4* d_pos4, float4* d_nrm32,
+                         cudaStream_t stream) {
+    if (n > 0) k_records<<<blocks_for(n, 256), 256, 0, stream>>>(d_pos, d_nrm, n, d_pos4, d_nrm32);
+    return cudaGetLastError();
 }
 
 cudaError_t make_source32(const double* d_pos, int64_t n, float4* d_out, cudaStream_t stream) {

@@ -646,8 +646,12 @@ __device__ __forceinline__ void top3(float d2, int32_t o, float& f1, float& f2, 
     }
 }
 
-__device__ __forceinline__ bool resolve_fine(const GridView& g, const double* R, const double* t, const FastRT& F,
-                                             V3 p, V3 ns,
+// Guard of the FP32 normal gate, relative to |ns|_1 |nt|_1: the FP32 value of
+// (R ns) . nt is within ~14 u |ns|_1 |nt|_1 (u = 2^-24) of the exact one.
+constexpr float kGateGuard = 1e-5f;
+
+__device__ __forceinline__ bool resolve_fine(const GridView& g, const double* R, const double* t, const float* Rf,
+                                             const FastRT& F, const SourceView& src, int64_t i, V3 p, float4 ns32,
                                              float qx, float qy, float qz, int32_t off, int32_t cnt,
                                              const ScoreParams& sp, double& addend) {
     const float inf = __int_as_float(0x7f800000);
@@ -655,14 +659,20 @@ __device__ __forceinline__ bool resolve_fine(const GridView& g, const double* R,
     int32_t o1 = -1, o2 = -1;
     int32_t e = off;
     const int32_t end = off + cnt;
-    for (; e + 1 < end; e += 2) {  // two independent loads in flight
+    for (; e + 3 < end; e += 4) {  // four independent loads in flight
         const float4 A = __ldg(g.fine_pts + e), B = __ldg(g.fine_pts + e + 1);
-        const float ax = qx - A.x, ay = qy - A.y, az = qz - A.z;
-        const float bx = qx - B.x, by = qy - B.y, bz = qz - B.z;
-        top3(fmaf(ax, ax, fmaf(ay, ay, az * az)), __float_as_int(A.w), f1, f2, f3, o1, o2);
-        top3(fmaf(bx, bx, fmaf(by, by, bz * bz)), __float_as_int(B.w), f1, f2, f3, o1, o2);
+        const float4 C = __ldg(g.fine_pts + e + 2), D = __ldg(g.fine_pts + e + 3);
+        float x, y, z;
+        x = qx - A.x; y = qy - A.y; z = qz - A.z;
+        top3(fmaf(x, x, fmaf(y, y, z * z)), __float_as_int(A.w), f1, f2, f3, o1, o2);
+        x = qx - B.x; y = qy - B.y; z = qz - B.z;
+        top3(fmaf(x, x, fmaf(y, y, z * z)), __float_as_int(B.w), f1, f2, f3, o1, o2);
+        x = qx - C.x; y = qy - C.y; z = qz - C.z;
+        top3(fmaf(x, x, fmaf(y, y, z * z)), __float_as_int(C.w), f1, f2, f3, o1, o2);
+        x = qx - D.x; y = qy - D.y; z = qz - D.z;
+        top3(fmaf(x, x, fmaf(y, y, z * z)), __float_as_int(D.w), f1, f2, f3, o1, o2);
     }
-    if (e < end) {
+    for (; e < end; ++e) {
         const float4 A = __ldg(g.fine_pts + e);
         const float ax = qx - A.x, ay = qy - A.y, az = qz - A.z;
         top3(fmaf(ax, ax, fmaf(ay, ay, az * az)), __float_as_int(A.w), f1, f2, f3, o1, o2);
@@ -673,7 +683,8 @@ __device__ __forceinline__ bool resolve_fine(const GridView& g, const double* R,
     double best_d2 = __longlong_as_double(0x7ff0000000000000ll);
     int32_t best_orig = INT32_MAX;
     auto consider = [&](int32_t o) {
-        const double d2 = sqnorm(sub(ld3(g.pos_orig, o), y));
+        const V3 q = g.pos4_orig ? ld4(g.pos4_orig, o) : ld3(g.pos_orig, o);
+        const double d2 = sqnorm(sub(q, y));
         if (d2 > sp.d2_max) return;
         if (d2 < best_d2 || (d2 == best_d2 && o < best_orig)) {
             best_d2 = d2;
@@ -692,9 +703,29 @@ __device__ __forceinline__ bool resolve_fine(const GridView& g, const double* R,
         if (f2 <= lim) consider(o2);
     }
     if (best_orig == INT32_MAX) return false;
-    const V3 nt = ld3(g.nrm_orig, best_orig);
-    if (is_zero(ns) || is_zero(nt)) return false;
-    if (!(dot(rot(R, ns), nt) >= sp.cos_max)) return false;
+    bool gate_done = false;
+    if (Rf && g.nrm32_orig) {
+        // FP32 normal gate; only a value within the guard of cos_max (or a zero
+        // FP32 normal) is decided by the reference's FP64 expression below
+        const float4 nt = __ldg(g.nrm32_orig + best_orig);
+        const float ns1 = fabsf(ns32.x) + fabsf(ns32.y) + fabsf(ns32.z);
+        const float nt1 = fabsf(nt.x) + fabsf(nt.y) + fabsf(nt.z);
+        if (ns1 > 0.0f && nt1 > 0.0f) {
+            const float ax = fmaf(Rf[0], ns32.x, fmaf(Rf[1], ns32.y, Rf[2] * ns32.z));
+            const float ay = fmaf(Rf[3], ns32.x, fmaf(Rf[4], ns32.y, Rf[5] * ns32.z));
+            const float az = fmaf(Rf[6], ns32.x, fmaf(Rf[7], ns32.y, Rf[8] * ns32.z));
+            const double d = static_cast<double>(fmaf(ax, nt.x, fmaf(ay, nt.y, az * nt.z)));
+            const double guard = static_cast<double>(kGateGuard * ns1 * nt1);
+            if (d < sp.cos_max - guard) return false;
+            gate_done = d > sp.cos_max + guard;
+        }
+    }
+    if (!gate_done) {
+        const V3 ns = ld3(src.nrm, i);
+        const V3 nt = ld3(g.nrm_orig, best_orig);
+        if (is_zero(ns) || is_zero(nt)) return false;
+        if (!(dot(rot(R, ns), nt) >= sp.cos_max)) return false;
+    }
     if (sp.fitness_from_distance) {
         const double dist = sqrt(best_d2);
         addend = dist * dist;
@@ -851,13 +882,14 @@ __global__ void __launch_bounds__(kScoreThreads, 4) k_score_resolve(SourceView s
         } else {
             double R[9], t[3];
             load_rt(cand_rt + 12 * cand, R, t);
-            const V3 p = ld3(src.pos, i), ns = ld3(src.nrm, i);
+            const V3 p = src.pos4 ? ld4(src.pos4, i) : ld3(src.pos, i);
             const FastRT F = load_fast(cand_fine + cand);
             const float4 P = __ldg(src.pos32 + i);
             const float qx = fmaf(F.r[0], P.x, fmaf(F.r[1], P.y, fmaf(F.r[2], P.z, F.t[0])));
             const float qy = fmaf(F.r[3], P.x, fmaf(F.r[4], P.y, fmaf(F.r[5], P.z, F.t[1])));
             const float qz = fmaf(F.r[6], P.x, fmaf(F.r[7], P.y, fmaf(F.r[8], P.z, F.t[2])));
-            inl = resolve_fine(g, R, t, F, p, ns, qx, qy, qz, q.z, q.w, sp, addend);
+            inl = resolve_fine(g, R, t, nullptr, F, src, i, p, make_float4(0, 0, 0, 0), qx, qy, qz, q.z, q.w, sp,
+                               addend);
         }
         const int64_t word = cand * n_chunks + (i >> 5);
         const uint32_t bit = 1u << (i & 31);
@@ -1283,8 +1315,9 @@ __global__ void __launch_bounds__(kScoreThreads) k_score_finalists(int32_t n_chu
 constexpr int kCtaThreads = 256;
 constexpr int kCtaWarps = kCtaThreads / 32;
 constexpr int kCtaPer = 8;                         // points per thread per round
-constexpr int kCtaPts = kCtaThreads * kCtaPer;     // 2048 points per round
-constexpr int kCtaWords = kCtaPts / 32;            // 64 ballot words per round
+constexpr int kCtaPts = kCtaThreads * kCtaPer;     // points per round
+constexpr int kCtaWords = kCtaPts / 32;            // ballot words per round (32 or 64)
+static_assert(kCtaWords == 32 || kCtaWords == 64, "the books read one or two ballot words per lane");
 constexpr int kCtaSlow = 0xffff;                   // queue count tag: exact FP64 fallback
 constexpr int kCtaChainChunks = kCtaPts / 32;      // chain window: the queue's 16 KB as doubles
 
@@ -1298,6 +1331,7 @@ struct CtaSmem {
     uint32_t cmask[kCtaChainChunks];
     int coff[kCtaChainChunks];
     double R[9], t[3];
+    float Rf[9];
     FastRT F;
     double red[kCtaWarps];
     int scan[kCtaWarps];
@@ -1399,8 +1433,12 @@ __global__ void __launch_bounds__(kCtaThreads, 4) k_score_cta(SourceView src, co
         if (cand >= n_cand) break;
         if (threadIdx.x < 12) {
             const double v = __ldg(cand_rt + 12 * cand + threadIdx.x);
-            if (threadIdx.x < 9) S.R[threadIdx.x] = v;
-            else S.t[threadIdx.x - 9] = v;
+            if (threadIdx.x < 9) {
+                S.R[threadIdx.x] = v;
+                S.Rf[threadIdx.x] = static_cast<float>(v);
+            } else {
+                S.t[threadIdx.x - 9] = v;
+            }
         }
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -1482,8 +1520,11 @@ __global__ void __launch_bounds__(kCtaThreads, 4) k_score_cta(SourceView src, co
                     const float qx = fmaf(F.r[0], P.x, fmaf(F.r[1], P.y, fmaf(F.r[2], P.z, F.t[0])));
                     const float qy = fmaf(F.r[3], P.x, fmaf(F.r[4], P.y, fmaf(F.r[5], P.z, F.t[1])));
                     const float qz = fmaf(F.r[6], P.x, fmaf(F.r[7], P.y, fmaf(F.r[8], P.z, F.t[2])));
-                    inl = resolve_fine(g, S.R, S.t, F, ld3(src.pos, i), ld3(src.nrm, i), qx, qy, qz, qe.y, cnt, sp,
-                                       addend);
+                    const bool rec = src.pos4 != nullptr && src.nrm32 != nullptr;
+                    const V3 p = rec ? ld4(src.pos4, i) : ld3(src.pos, i);
+                    const float4 n32 = rec ? __ldg(src.nrm32 + i) : make_float4(0, 0, 0, 0);
+                    inl = resolve_fine(g, S.R, S.t, rec ? S.Rf : nullptr, F, src, i, p, n32, qx, qy, qz, qe.y, cnt,
+                                       sp, addend);
                 }
                 const int word = local >> 5;  // ballot word w covers points base + 32 w ..
                 const uint32_t bit = 1u << (local & 31);
@@ -1498,7 +1539,7 @@ __global__ void __launch_bounds__(kCtaThreads, 4) k_score_cta(SourceView src, co
             __syncthreads();
             // C. the miss budget in point order (word w covers points base + 32 w ..)
             if (threadIdx.x == 0) S.nq = 0;
-            const uint32_t m0 = S.miss[b][lane], m1 = S.miss[b][32 + lane];
+            const uint32_t m0 = S.miss[b][lane], m1 = kCtaWords > 32 ? S.miss[b][(32 + lane) % kCtaWords] : 0u;
             const int c0 = __popc(m0), c1 = __popc(m1);
             const int round_misses = __reduce_add_sync(kFull, static_cast<unsigned>(c0 + c1));
             if (misses + round_misses > sp.miss_budget) {
@@ -1533,10 +1574,10 @@ __global__ void __launch_bounds__(kCtaThreads, 4) k_score_cta(SourceView src, co
             }
             misses += round_misses;
             if (warp == 0) {
-                const uint32_t i0 = S.inl[b][lane], i1 = S.inl[b][32 + lane];
+                const uint32_t i0 = S.inl[b][lane], i1 = kCtaWords > 32 ? S.inl[b][(32 + lane) % kCtaWords] : 0u;
                 const int64_t w0 = base / 32 + lane;
                 if (w0 < n_chunks) inlw[w0] = i0;
-                if (w0 + 32 < n_chunks) inlw[w0 + 32] = i1;
+                if (kCtaWords > 32 && w0 + 32 < n_chunks) inlw[w0 + 32] = i1;
                 inliers += __reduce_add_sync(kFull, static_cast<unsigned>(__popc(i0) + __popc(i1)));
             }
         }
@@ -1906,12 +1947,15 @@ cudaError_t run_hypotheses_range(const SourceView& src, const double* d_tgt_pos,
         };
         add(grid.fine_info, grid.n_fine * static_cast<int64_t>(sizeof(int2)));
         add(grid.fine_pts, grid.n_fine_entries * static_cast<int64_t>(sizeof(float4)));
-        add(grid.pos_orig, grid.n_points * 24);
-        add(grid.nrm_orig, grid.n_points * 24);
+        add(grid.pos4_orig, grid.n_points * static_cast<int64_t>(sizeof(double4)));
+        add(grid.nrm32_orig, grid.n_points * static_cast<int64_t>(sizeof(float4)));
         add(src.pos32, src.n * static_cast<int64_t>(sizeof(float4)));
-        add(src.pos, src.n * 24);
-        add(src.nrm, src.n * 24);
+        add(src.pos4, src.n * static_cast<int64_t>(sizeof(double4)));
+        add(src.nrm32, src.n * static_cast<int64_t>(sizeof(float4)));
         if (static_cast<int64_t>(gs) < pf.n) pf.n = static_cast<int>(gs);
+        // measured on B1: the scoring gathers hit L2 without it and the bulk
+        // DRAM reads slow k_hyp_sample, so it is opt-in (LK_PREFETCH=1)
+        if (const char* v = std::getenv("LK_PREFETCH"); !(v && v[0] == '1')) pf.n = 0;
         k_hyp_sample<<<gs, 256, 0, stream>>>(begin, count, splitmix64(seed), ns, thresh, d_cache, src.pos, d_tgt_pos,
                                              tau, rb.surv_index, rb.surv_ids, rb.counters, pf);
     }

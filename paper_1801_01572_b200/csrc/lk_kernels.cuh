@@ -59,6 +59,9 @@ struct GridView {
     const float4* fine_pts;
     // sizes (elements) of the arrays above, for L2 prefetching
     int64_t n_points, n_cells, n_fine, n_fine_entries;
+    // resolution records in original point order (radius-1 grids with blocks)
+    const double4* pos4_orig;  // (x, y, z, 0) FP64
+    const float4* nrm32_orig;  // FP32 normals for the guarded normal gate
 };
 
 struct GridStorage {
@@ -79,6 +82,8 @@ struct GridStorage {
     int64_t nfine = 0, nfine_entries = 0;
     int2* fine_info = nullptr;
     float4* fine_pts = nullptr;
+    double4* pos4_orig = nullptr;
+    float4* nrm32_orig = nullptr;
     cudaStream_t stream = nullptr;  // allocation stream
     void release();
 };
@@ -154,6 +159,9 @@ struct SourceView {
     const double* nrm;    // 3 * ns
     const float4* pos32;  // ns float copies (x, y, z, 0) for the fast path; null -> FP64 only
     int64_t n;
+    // resolution records of the fast path (null -> FP64 arrays above):
+    const double4* pos4 = nullptr;  // (x, y, z, 0) FP64, one sector per point
+    const float4* nrm32 = nullptr;  // FP32 normals for the guarded normal gate
 };
 
 struct ScoreParams {
@@ -177,6 +185,9 @@ struct ScoreParams {
 void configure_fast_path(ScoreParams& sp, const GridView& g, double max_abs_source);
 
 cudaError_t make_source32(const double* d_pos, int64_t n, float4* d_out, cudaStream_t stream);
+// (x, y, z, 0) FP64 records and FP32 copies of 3 * n FP64 arrays (either output may be null)
+cudaError_t make_records(const double* d_pos, const double* d_nrm, int64_t n, double4* d_pos4, float4* d_nrm32,
+                         cudaStream_t stream);
 
 // Samples, pre-rejects and fits hypotheses [begin, end); scores the
 // candidates; reduces the per-run best into `record` (an lk_reg_record, device).

@@ -109,6 +109,25 @@ def test_run_hypotheses_matches_oracle(prepared1, oracle, seed, H):
     assert st.evals_executed >= st.w_ref
 
 
+@pytest.mark.parametrize("kw", [
+    dict(normal_angle_max=8.0 * math.pi / 180.0, min_inlier_ratio=0.05),   # many gate decisions near cos_max
+    dict(normal_angle_max=75.0 * math.pi / 180.0),
+    dict(max_fitness=0.0009, min_inlier_ratio=0.1),                        # qualification near the fitness bar
+    dict(min_inlier_ratio=0.0),                                            # zero-inlier candidates qualify
+])
+def test_run_hypotheses_params_match_oracle(prepared1, oracle, kw):
+    # the scorer's FP32 normal gate, the order-bound qualification and the
+    # exact chains on demand must reproduce the reference's decisions
+    octx, c = prepared1
+    params = lk.RegistrationParams(hypothesis_count=60_000, seed=5, **kw)
+    ctx = lk.registration_context(lk.PointCloud(c["src"], c["src_n"]), lk.PointCloud(c["tgt"], c["tgt_n"]),
+                                  c["cache"], params)
+    st = lk.HypothesisStats()
+    dev = lk.run_hypotheses(ctx, params, st)
+    orc, ost = octx.run(oracle.params_from(params))
+    _assert_same_result(dev, orc, st, ost)
+
+
 def test_prepare_and_register_global_match_oracle(pair1, oracle):
     params = lk.RegistrationParams(hypothesis_count=100_000, seed=1)
     ctx = lk.prepare_registration(pair1.source, pair1.target, params)
