@@ -279,6 +279,7 @@ struct lk_reg_ctx {
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
     cudaStream_t aux_stream = nullptr;  // target-side preparation, concurrent with the source side
+    cudaStream_t grid_stream = nullptr; // EvalGrid build, concurrent with the target's FPFH
     int64_t ns = 0, nt = 0;
     double *d_spos = nullptr, *d_snrm = nullptr, *d_tpos = nullptr, *d_tnrm = nullptr;
     float *d_sfeat = nullptr, *d_tfeat = nullptr;  // FPFH (prepare_registration only)
@@ -329,8 +330,10 @@ struct lk_reg_ctx {
         lkk::pool_free(d_record, s);
         if (own_stream) cudaStreamSynchronize(own_stream);
         if (aux_stream) cudaStreamSynchronize(aux_stream);
+        if (grid_stream) cudaStreamSynchronize(grid_stream);
         release_stream(device, own_stream);
         release_stream(device, aux_stream);
+        release_stream(device, grid_stream);
     }
 };
 
@@ -355,6 +358,7 @@ lk_reg_ctx* ctx_new(int32_t device) {
         c->sm_count = sm_count_of(c->device);
         c->own_stream = acquire_stream(c->device);
         c->aux_stream = acquire_stream(c->device);
+        c->grid_stream = acquire_stream(c->device);
         c->stream = c->own_stream;
         c->rb.stream = c->own_stream;
     } catch (...) {
@@ -382,7 +386,7 @@ struct CloudSide {
 };
 
 void prepare_side(CloudSide& cs, double feature_radius, double leaf, lkk::GridStorage* grid, double d_max,
-                  int device, double t0, const char* tag) {
+                  int device, double t0, const char* tag, cudaStream_t grid_stream = nullptr) {
     auto mark = [&](const char* what) {
         if (!trace_on()) return;
         cudaStreamSynchronize(cs.s);
@@ -404,11 +408,41 @@ void prepare_side(CloudSide& cs, double feature_radius, double leaf, lkk::GridSt
         if (cs.status != 0 || cs.n < 4) return;
         CK(lkk::cloud_stats(cs.pos, cs.nrm, cs.n, &cs.usable, &cs.max_norm, cs.s));
         if (cs.usable < 4) return;
-        CK(lkk::pool_alloc(&cs.feat, 33 * cs.n * sizeof(float), cs.s));
-        CK(lkk::compute_fpfh(cs.pos, cs.nrm, cs.n, feature_radius, cs.feat, cs.s));
-        mark("fpfh");
+        // the EvalGrid (registration.cpp:249) only needs the downsampled
+        // cloud: it is built on its own stream and host thread while this
+        // one runs the FPFH
+        Worker* gw = nullptr;
+        cudaError_t grid_err = cudaSuccess;
         if (grid) {
-            CK(lkk::build_grid(*grid, 0, cs.pos, cs.nrm, cs.n, d_max, d_max, cs.s));
+            cudaEvent_t ready;
+            CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+            CK(cudaEventRecord(ready, cs.s));
+            CK(cudaStreamWaitEvent(grid_stream, ready, 0));
+            cudaEventDestroy(ready);
+            gw = acquire_worker();
+            const double* pos = cs.pos;
+            const double* nrm = cs.nrm;
+            const int64_t n = cs.n;
+            gw->post([grid, pos, nrm, n, d_max, grid_stream, device, &grid_err] {
+                cudaSetDevice(device);
+                grid_err = lkk::build_grid(*grid, 0, pos, nrm, n, d_max, d_max, grid_stream);
+            });
+        }
+        try {
+            CK(lkk::pool_alloc(&cs.feat, 33 * cs.n * sizeof(float), cs.s));
+            CK(lkk::compute_fpfh(cs.pos, cs.nrm, cs.n, feature_radius, cs.feat, cs.s));
+        } catch (...) {
+            if (gw) {
+                gw->wait();
+                release_worker(gw);
+            }
+            throw;
+        }
+        mark("fpfh");
+        if (gw) {
+            gw->wait();
+            release_worker(gw);
+            CK(grid_err);
             mark("eval grid");
         }
     } catch (...) {
@@ -446,7 +480,8 @@ lk_status prepare_impl(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_pa
         const double fr = params->feature_radius, leaf = params->leaf, dm = params->d_max;
         const int dev = c->device;
         lkk::GridStorage* grid = &c->grid;
-        worker->post([&T, fr, leaf, grid, dm, dev, t0] { prepare_side(T, fr, leaf, grid, dm, dev, t0, "tgt"); });
+        cudaStream_t gs = c->grid_stream;
+        worker->post([&T, fr, leaf, grid, dm, dev, t0, gs] { prepare_side(T, fr, leaf, grid, dm, dev, t0, "tgt", gs); });
         prepare_side(S, fr, leaf, nullptr, 0.0, dev, t0, "src");
         worker->wait();
         release_worker(worker);
