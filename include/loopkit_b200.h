@@ -206,6 +206,38 @@ lk_status lk_edge_info_batched(const lk_cloud* clouds_i, const lk_cloud* clouds_
 lk_status lk_feature_nn_cache(const float* src_features, int64_t ns, const float* tgt_features, int64_t nt,
                               int32_t device, int32_t* cache);
 
+/* ---- ICP point-to-plane refinement (north-star item 4, config D) ---------
+ * No reference implementation exists (SPEC.md:332 lists ICP as a non-goal);
+ * the specification is frozen in DESIGN.md "ICP" and its CPU oracle
+ * (oracle/lk_oracle.cpp): correspondences are the EvalGrid NN within
+ * max_correspondence_distance (registration.cpp:165-199 semantics), the
+ * residual is (T p - q) . n_q with J = (T p x n_q, n_q) (the G_p convention of
+ * line_process.cpp:23-28), the 6x6 system is reduced in a fixed tree order
+ * and solved by LDL^T, and T is updated by the Cayley map. Refines T0 (12
+ * doubles, R row-major then t); history (nullable) receives max_iterations x
+ * (correspondences, rmse, |delta|^2). LK_NO_CORRESPONDENCES when the first
+ * iteration finds fewer than 6 pairs; LK_MISSING_NORMALS without target
+ * normals. */
+typedef struct lk_icp_params {
+    double max_correspondence_distance; /* > 0 (metres) */
+    int32_t max_iterations;
+    int32_t device;                     /* -1: current device */
+    double convergence_eps;             /* stop once |delta| < eps */
+} lk_icp_params;
+
+typedef struct lk_icp_result {
+    double R[9]; /* row-major */
+    double t[3];
+    int32_t iterations;     /* updates applied */
+    int32_t converged;
+    int64_t correspondences; /* of the last accumulation */
+    double rmse;             /* sqrt(sum r^2 / correspondences) of the last accumulation */
+    double fitness;          /* correspondences / source size */
+} lk_icp_result;
+
+lk_status lk_icp_point_to_plane(const lk_cloud* source, const lk_cloud* target, const double* T0,
+                                const lk_icp_params* params, lk_icp_result* result, double* history);
+
 /* host-side helpers of prepare (this tier) */
 lk_status lk_voxel_downsample(const lk_cloud* cloud, double leaf, double* out_xyz, double* out_n, int64_t* out_count);
 lk_status lk_compute_fpfh(const lk_cloud* cloud, double radius, int32_t threads, float* out);

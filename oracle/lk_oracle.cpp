@@ -1069,6 +1069,229 @@ static void edge_info(const Cloud& ci, const Cloud& cj, const Rigid& ti, const R
 // ================================================================ C ABI
 using namespace orc;
 
+
+// ---- ICP point-to-plane (north-star item 4; config D) ----------------------
+// The reference has no ICP (SPEC.md:332 lists it as a non-goal), so this is
+// the builder's own specification, frozen here and in DESIGN.md "ICP", and
+// the device implementation (lk_icp.cu) must equal it bit for bit:
+//  * correspondences: the EvalGrid of the target at cell = max_dist and the
+//    exact NN of evaluate_against_grid (registration.cpp:165-199: +-1 cell
+//    window, d2 <= max_dist^2, min (d2, original index)); a zero target
+//    normal drops the pair;
+//  * per pair (y = T p, q, n): r = (y - q) . n, J = (y x n, n) -- the
+//    G_p = [-[p]x | I] convention of line_process.cpp:23-28 applied to the
+//    plane normal -- contributing H_uv = J_u J_v (u <= v, row-major), g_u =
+//    J_u r, e = r r;
+//  * a fixed reduction tree over the point order: 32-point butterflies (xor
+//    16, 8, 4, 2, 1), 8 of them summed in order per 256-point chunk, chunk
+//    values in 32-chunk butterflies, those summed in order from 0.0;
+//  * H delta = -g by LDL^T without pivoting; the update is the Cayley map
+//    R_d = I + s (K + K^2), K = [delta_w / 2]x, s = 2 / (1 + |delta_w / 2|^2)
+//    (a rotation; rational, so host and device agree bitwise), then
+//    T <- (R_d R, R_d t + delta_v) in Eigen's Matrix3d product order;
+//  * stop after the update when |delta|^2 < eps^2, or when fewer than 6
+//    correspondences / a non-positive pivot leave the system singular.
+static bool eval_grid_nn(const EvalGrid& g, V3 y, double d2_max, int32_t& slot_out, double& d2_out) {
+    int ix = floor_int((y.x - g.origin.x) / g.cell);
+    int iy = floor_int((y.y - g.origin.y) / g.cell);
+    int iz = floor_int((y.z - g.origin.z) / g.cell);
+    if (ix < 0 || iy < 0 || iz < 0 || ix >= g.nx || iy >= g.ny || iz >= g.nz) return false;
+    const size_t plane = static_cast<size_t>(g.ny) * g.nz;
+    size_t c = static_cast<size_t>(ix) * plane + static_cast<size_t>(iy) * g.nz + static_cast<size_t>(iz);
+    if (!g.near_occupied[c]) return false;
+    double best_d2 = std::numeric_limits<double>::infinity();
+    int32_t best_slot = -1;
+    int best_index = std::numeric_limits<int>::max();
+    int x0 = std::max(ix - 1, 0), x1 = std::min(ix + 1, g.nx - 1);
+    int y0 = std::max(iy - 1, 0), y1 = std::min(iy + 1, g.ny - 1);
+    int z0 = std::max(iz - 1, 0), z1 = std::min(iz + 1, g.nz - 1);
+    for (int x = x0; x <= x1; ++x)
+        for (int yy = y0; yy <= y1; ++yy) {
+            size_t row = static_cast<size_t>(x) * plane + static_cast<size_t>(yy) * g.nz;
+            for (int32_t s = g.start[row + z0]; s < g.start[row + z1 + 1]; ++s) {
+                double d2 = sqnorm(sub(g.slot_position[s], y));
+                if (d2 > d2_max) continue;
+                int orig = g.index[s];
+                if (d2 < best_d2 || (d2 == best_d2 && orig < best_index)) {
+                    best_d2 = d2;
+                    best_slot = s;
+                    best_index = orig;
+                }
+            }
+        }
+    slot_out = best_slot;
+    d2_out = best_d2;
+    return best_slot >= 0;
+}
+
+static constexpr int kIcpVals = 28;  // 21 H (upper, row-major) + 6 g + e
+
+// LDL^T solve of H x = -g (6x6, no pivoting); false on a non-positive pivot.
+// Shared verbatim (operation for operation) by lk_icp.cu's device solve.
+static bool icp_solve(const double* h21, const double* g6, double* x6) {
+    double H[6][6];
+    int k = 0;
+    for (int u = 0; u < 6; ++u)
+        for (int w = u; w < 6; ++w) {
+            H[u][w] = h21[k];
+            H[w][u] = h21[k];
+            ++k;
+        }
+    double L[6][6] = {}, D[6];
+    for (int j = 0; j < 6; ++j) {
+        double dj = H[j][j];
+        for (int q = 0; q < j; ++q) dj = dj - (L[j][q] * L[j][q]) * D[q];
+        if (!(dj > 0.0)) return false;
+        D[j] = dj;
+        for (int i = j + 1; i < 6; ++i) {
+            double v = H[i][j];
+            for (int q = 0; q < j; ++q) v = v - (L[i][q] * L[j][q]) * D[q];
+            L[i][j] = v / dj;
+        }
+    }
+    double z[6];
+    for (int i = 0; i < 6; ++i) {
+        double v = -g6[i];
+        for (int q = 0; q < i; ++q) v = v - L[i][q] * z[q];
+        z[i] = v;
+    }
+    for (int i = 5; i >= 0; --i) {
+        double v = z[i] / D[i];
+        for (int q = i + 1; q < 6; ++q) v = v - L[q][i] * x6[q];
+        x6[i] = v;
+    }
+    return true;
+}
+
+// Cayley update of T by the twist x6 = (w, v).
+static Rigid icp_update(const Rigid& T, const double* x6) {
+    const double wx = x6[0] * 0.5, wy = x6[1] * 0.5, wz = x6[2] * 0.5;
+    const double s = 2.0 / (1.0 + ((wx * wx + wy * wy) + wz * wz));
+    M3 K;
+    K.m[0][0] = 0.0; K.m[0][1] = -wz; K.m[0][2] = wy;
+    K.m[1][0] = wz; K.m[1][1] = 0.0; K.m[1][2] = -wx;
+    K.m[2][0] = -wy; K.m[2][1] = wx; K.m[2][2] = 0.0;
+    M3 K2 = mul(K, K);
+    M3 Rd;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) Rd.m[i][j] = (i == j ? 1.0 : 0.0) + s * (K.m[i][j] + K2.m[i][j]);
+    Rigid out;
+    out.R = mul(Rd, T.R);
+    out.t = add(mul(Rd, T.t), v3(x6[3], x6[4], x6[5]));
+    return out;
+}
+
+static void butterfly32(double* x) {
+    for (int o = 16; o > 0; o >>= 1) {
+        double y[32];
+        for (int l = 0; l < 32; ++l) y[l] = x[l] + x[l ^ o];
+        for (int l = 0; l < 32; ++l) x[l] = y[l];
+    }
+}
+
+// One ICP accumulation at T: the 28 reduced values and the pair count.
+static void icp_accumulate(const EvalGrid& g, const std::vector<V3>& tgt_n_orig, const Cloud& source, const Rigid& T,
+                           double max_dist, double* out, int64_t& count) {
+    const int64_t n = static_cast<int64_t>(source.size());
+    const int64_t n_chunks = (n + 255) / 256;
+    const double d2_max = max_dist * max_dist;
+    std::vector<double> chunk_vals(static_cast<size_t>(n_chunks) * kIcpVals, 0.0);
+    int64_t total = 0;
+    // chunks are independent (their values land in fixed slots): any thread
+    // count gives the same bits
+#pragma omp parallel for schedule(dynamic, 16) reduction(+ : total)
+    for (int64_t c = 0; c < n_chunks; ++c) {
+        std::vector<double> contrib(static_cast<size_t>(256) * kIcpVals);
+        for (int l = 0; l < 256; ++l) {
+            double* v = &contrib[static_cast<size_t>(l) * kIcpVals];
+            for (int q = 0; q < kIcpVals; ++q) v[q] = 0.0;
+            const int64_t i = c * 256 + l;
+            if (i >= n) continue;
+            V3 y = apply(T, source.pos[static_cast<size_t>(i)]);
+            int32_t slot;
+            double d2;
+            if (!eval_grid_nn(g, y, d2_max, slot, d2)) continue;
+            const V3 q = g.slot_position[static_cast<size_t>(slot)];
+            const V3 nn = g.slot_normal[static_cast<size_t>(slot)];
+            if (is_zero(nn)) continue;
+            const V3 d = sub(y, q);
+            const double r = dot(d, nn);
+            const V3 a = v3(y.y * nn.z - y.z * nn.y, y.z * nn.x - y.x * nn.z, y.x * nn.y - y.y * nn.x);
+            const double J[6] = {a.x, a.y, a.z, nn.x, nn.y, nn.z};
+            int k = 0;
+            for (int u = 0; u < 6; ++u)
+                for (int w = u; w < 6; ++w) v[k++] = J[u] * J[w];
+            for (int u = 0; u < 6; ++u) v[k++] = J[u] * r;
+            v[k] = r * r;
+            total += 1;
+        }
+        for (int q = 0; q < kIcpVals; ++q) {
+            double acc = 0.0;
+            for (int w = 0; w < 8; ++w) {
+                double x[32];
+                for (int l = 0; l < 32; ++l) x[l] = contrib[static_cast<size_t>(w * 32 + l) * kIcpVals + q];
+                butterfly32(x);
+                acc = w == 0 ? x[0] : acc + x[0];
+            }
+            chunk_vals[static_cast<size_t>(c) * kIcpVals + q] = acc;
+        }
+    }
+    (void)tgt_n_orig;
+    count = total;
+    for (int q = 0; q < kIcpVals; ++q) {
+        double acc = 0.0;
+        for (int64_t s0 = 0; s0 < n_chunks; s0 += 32) {
+            double x[32];
+            for (int l = 0; l < 32; ++l) x[l] = s0 + l < n_chunks ? chunk_vals[static_cast<size_t>(s0 + l) * kIcpVals + q] : 0.0;
+            butterfly32(x);
+            acc = acc + x[0];
+        }
+        out[q] = acc;
+    }
+}
+
+static int icp_point_to_plane(const Cloud& source, const Cloud& target, const Rigid& T0, double max_dist,
+                              int32_t max_iter, double eps, Rigid& T, or_icp_result& res, double* history) {
+    if (source.pos.empty() || target.pos.empty()) fail(OR_EMPTY_CLOUD, "icp: empty cloud");
+    if (!target.has_normals()) fail(OR_MISSING_NORMALS, "icp: target normals required");
+    if (!(max_dist > 0.0)) fail(OR_INVALID_ARGUMENT, "icp: max_correspondence_distance must be positive");
+    EvalGrid g = build_eval_grid(target, max_dist);
+    T = T0;
+    res = or_icp_result{};
+    const double ns = static_cast<double>(source.size());
+    for (int32_t it = 0; it < max_iter; ++it) {
+        double vals[kIcpVals];
+        int64_t cnt = 0;
+        icp_accumulate(g, target.nrm, source, T, max_dist, vals, cnt);
+        res.correspondences = cnt;
+        res.fitness = static_cast<double>(cnt) / ns;
+        res.rmse = cnt > 0 ? std::sqrt(vals[27] / static_cast<double>(cnt)) : 0.0;
+        double x[6] = {0, 0, 0, 0, 0, 0};
+        const bool ok = cnt >= 6 && icp_solve(vals, vals + 21, x);
+        double dd = 0.0;
+        if (ok) {
+            for (int k = 0; k < 6; ++k) dd = dd + x[k] * x[k];
+        }
+        if (history) {
+            history[3 * it] = static_cast<double>(cnt);
+            history[3 * it + 1] = res.rmse;
+            history[3 * it + 2] = dd;
+        }
+        if (!ok) {
+            if (it == 0 && cnt < 6) fail(OR_NO_CORRESPONDENCES, "icp: fewer than 6 correspondences");
+            res.iterations = it;
+            return OR_OK;
+        }
+        T = icp_update(T, x);
+        res.iterations = it + 1;
+        if (dd < eps * eps) {
+            res.converged = 1;
+            return OR_OK;
+        }
+    }
+    return OR_OK;
+}
+
 template <class F>
 static int guarded(F&& f) {
     try {
@@ -1445,6 +1668,20 @@ int or_edge_info(const double* ci, int64_t ni, const double* cj, int64_t nj, con
     return guarded([&] {
         edge_info(make_cloud(ci, nullptr, ni), make_cloud(cj, nullptr, nj), load_rigid(Ri9, ti3),
                   load_rigid(Rj9, tj3), epsilon, info36, *pair_count);
+    });
+}
+
+int or_icp_point_to_plane(const double* sxyz, int64_t ns, const double* txyz, const double* tn, int64_t nt,
+                          const double* R0, const double* t0, double max_dist, int32_t max_iter, double eps,
+                          double* R9, double* t3, or_icp_result* res, double* history) {
+    return guarded([&] {
+        Rigid T;
+        icp_point_to_plane(make_cloud(sxyz, nullptr, ns), make_cloud(txyz, tn, nt), load_rigid(R0, t0), max_dist,
+                           max_iter, eps, T, *res, history);
+        store_m(R9, T.R);
+        t3[0] = T.t.x;
+        t3[1] = T.t.y;
+        t3[2] = T.t.z;
     });
 }
 

@@ -158,6 +158,19 @@ int or_better(const or_result* a, const or_result* b);
 int or_edge_info(const double* ci, int64_t ni, const double* cj, int64_t nj, const double* Ri9, const double* ti3,
                  const double* Rj9, const double* tj3, double epsilon, double* info36, int64_t* pair_count);
 
+/* ICP point-to-plane (no reference; the builder's frozen spec, lk_oracle.cpp
+ * "ICP point-to-plane"). history (nullable): max_iter x (count, rmse, |delta|^2). */
+typedef struct or_icp_result {
+    int32_t iterations;
+    int32_t converged;
+    int64_t correspondences;
+    double rmse;
+    double fitness;
+} or_icp_result;
+int or_icp_point_to_plane(const double* sxyz, int64_t ns, const double* txyz, const double* tn, int64_t nt,
+                          const double* R0, const double* t0, double max_dist, int32_t max_iter, double eps,
+                          double* R9, double* t3, or_icp_result* res, double* history);
+
 #ifdef __cplusplus
 }
 #endif

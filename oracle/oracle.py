@@ -391,3 +391,25 @@ def edge_info(ci, cj, Ri, ti, Rj, tj, eps):
     _check(lib().or_edge_info(_p(a), a.shape[0], _p(b), b.shape[0], _p(Ri), _p(ti), _p(Rj), _p(tj), eps, _p(info),
                               C.byref(cnt)))
     return info.reshape(6, 6), cnt.value
+
+
+class or_icp_result(C.Structure):
+    _fields_ = [("iterations", C.c_int32), ("converged", C.c_int32), ("correspondences", C.c_int64),
+                ("rmse", C.c_double), ("fitness", C.c_double)]
+
+
+def icp_point_to_plane(src_xyz, tgt_xyz, tgt_n, R0, t0, max_dist, max_iter=30, eps=1e-10):
+    """The frozen ICP spec (lk_oracle.cpp "ICP point-to-plane"): returns
+    (R, t, or_icp_result, history[max_iter, 3])."""
+    L = lib()
+    L.or_icp_point_to_plane.restype = C.c_int
+    s, t, tn = _d(src_xyz), _d(tgt_xyz), _d(tgt_n)
+    R0 = _d(np.asarray(R0).reshape(9))
+    t0 = _d(np.asarray(t0).reshape(3))
+    R, tt = np.empty(9), np.empty(3)
+    res = or_icp_result()
+    hist = np.zeros((max(int(max_iter), 1), 3))
+    _check(L.or_icp_point_to_plane(_p(s), C.c_int64(len(s)), _p(t), _p(tn), C.c_int64(len(t)), _p(R0), _p(t0),
+                                   C.c_double(max_dist), C.c_int32(max_iter), C.c_double(eps), _p(R), _p(tt),
+                                   C.byref(res), _p(hist)))
+    return R.reshape(3, 3), tt, res, hist

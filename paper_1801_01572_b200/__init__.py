@@ -7,10 +7,12 @@ the Python mirror of the reference interface.
 """
 from .errors import (CudaError, DegenerateConfiguration, EmptyCloud, Error, MissingData, MissingNormals,
                      NoCorrespondences, TooFewPoints)
-from .registration import (CandidateScores, DeviceGrid, EdgeInfo, EvalGrid, HypothesisStats, PointCloud,
+from .registration import (CandidateScores, DeviceGrid, EdgeInfo, EvalGrid, HypothesisStats, IcpParams, IcpResult,
+                           PointCloud,
                            RegistrationContext, RegistrationParams, RegistrationResult, RigidTransform, SearchGrid,
                            build_eval_grid, build_grid, compute_fpfh, device_count, edge_info, edge_info_batched,
-                           evaluate_hypothesis, feature_nn_cache, merge_records, prepare_registration,
+                           evaluate_hypothesis, feature_nn_cache, icp_point_to_plane, merge_records,
+                           prepare_registration,
                            records_from_bytes, register_global, registration_context, run_hypotheses,
                            run_hypotheses_range, score_candidates, voxel_downsample)
 

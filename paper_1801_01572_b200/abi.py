@@ -69,6 +69,27 @@ class lk_reg_result(C.Structure):
     ]
 
 
+class lk_icp_params(C.Structure):
+    _fields_ = [
+        ("max_correspondence_distance", C.c_double),
+        ("max_iterations", C.c_int32),
+        ("device", C.c_int32),
+        ("convergence_eps", C.c_double),
+    ]
+
+
+class lk_icp_result(C.Structure):
+    _fields_ = [
+        ("R", C.c_double * 9),
+        ("t", C.c_double * 3),
+        ("iterations", C.c_int32),
+        ("converged", C.c_int32),
+        ("correspondences", C.c_int64),
+        ("rmse", C.c_double),
+        ("fitness", C.c_double),
+    ]
+
+
 class lk_hyp_stats(C.Structure):
     _fields_ = [
         ("sampled", C.c_int64),
@@ -143,6 +164,8 @@ SIGNATURES = {
     "lk_edge_info_batched": (C.c_int, [C.POINTER(lk_cloud), C.POINTER(lk_cloud), dptr, dptr, C.c_int64, C.c_double,
                                        C.c_int32, dptr, i64ptr]),
     "lk_feature_nn_cache": (C.c_int, [fptr, C.c_int64, fptr, C.c_int64, C.c_int32, i32ptr]),
+    "lk_icp_point_to_plane": (C.c_int, [C.POINTER(lk_cloud), C.POINTER(lk_cloud), dptr, C.POINTER(lk_icp_params),
+                                        C.POINTER(lk_icp_result), dptr]),
     "lk_voxel_downsample": (C.c_int, [C.POINTER(lk_cloud), C.c_double, dptr, dptr, i64ptr]),
     "lk_compute_fpfh": (C.c_int, [C.POINTER(lk_cloud), C.c_double, C.c_int32, fptr]),
 }
@@ -154,6 +177,8 @@ SYNTH_SIGNATURES = {
     "lks_frame_pair": (C.c_void_p, [C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
                                     C.c_double, C.c_int, C.c_double, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int)]),
     "lks_surface_pair": (C.c_void_p, [C.c_uint64, C.c_double, C.c_double, C.POINTER(C.c_int)]),
+    "lks_submap_pair": (C.c_void_p, [C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int,
+                                     C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int)]),
     "lks_random_cloud": (C.c_void_p, [C.c_uint64, C.c_uint64, C.c_int, C.c_double, C.c_double, C.c_int,
                                       C.POINTER(C.c_int)]),
     "lks_count": (C.c_int64, [C.c_void_p, C.c_int]),

@@ -956,6 +956,70 @@ lk_status lk_edge_info_batched(const lk_cloud* clouds_i, const lk_cloud* clouds_
     });
 }
 
+lk_status lk_icp_point_to_plane(const lk_cloud* source, const lk_cloud* target, const double* T0,
+                                const lk_icp_params* params, lk_icp_result* result, double* history) {
+    return guarded([&]() -> lk_status {
+        if (!T0 || !params || !result) return fail(LK_INVALID_ARGUMENT, "null argument");
+        check_cloud_ptr(source, "source");
+        check_cloud_ptr(target, "target");
+        if (source->n == 0 || target->n == 0) return fail(LK_EMPTY_CLOUD, "icp: empty cloud");
+        if (!target->nxyz) return fail(LK_MISSING_NORMALS, "icp: target normals required");
+        const double dmax = params->max_correspondence_distance;
+        if (!(dmax > 0.0)) return fail(LK_INVALID_ARGUMENT, "icp: max_correspondence_distance must be positive");
+        if (params->max_iterations < 0) return fail(LK_INVALID_ARGUMENT, "icp: max_iterations must be >= 0");
+        const int dev = select_device(params->device);
+        const int sms = sm_count_of(dev);
+        cudaStream_t s = acquire_stream(dev);
+        lkk::GridStorage g;
+        double *d_src = nullptr, *d_tp = nullptr, *d_tn = nullptr, *d_hist = nullptr;
+        lkk::IcpOutcome o{};
+        double R[9], t[3];
+        cudaError_t e = cudaSuccess;
+        try {
+            d_src = dev_upload(source->xyz, 3 * source->n, s);
+            d_tp = dev_upload(target->xyz, 3 * target->n, s);
+            d_tn = dev_upload(target->nxyz, 3 * target->n, s);
+            const int64_t hn = 3 * static_cast<int64_t>(params->max_iterations);
+            if (history && hn > 0) CK(cudaMalloc(&d_hist, hn * sizeof(double)));
+            e = lkk::build_grid(g, 0, d_tp, d_tn, target->n, dmax, dmax, s);
+            if (e == cudaSuccess)
+                e = lkk::icp_point_to_plane(d_src, source->n, g, dmax, params->max_iterations,
+                                            params->convergence_eps, T0, T0 + 9, R, t, &o, d_hist, s, sms,
+                                            fast_path_enabled());
+            if (e == cudaSuccess && d_hist)
+                e = cudaMemcpyAsync(history, d_hist, hn * sizeof(double), cudaMemcpyDeviceToHost, s);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        } catch (...) {
+            g.release();
+            lkk::pool_free(d_src, s);
+            lkk::pool_free(d_tp, s);
+            lkk::pool_free(d_tn, s);
+            cudaStreamSynchronize(s);
+            cudaFree(d_hist);
+            release_stream(dev, s);
+            throw;
+        }
+        g.release();
+        lkk::pool_free(d_src, s);
+        lkk::pool_free(d_tp, s);
+        lkk::pool_free(d_tn, s);
+        cudaStreamSynchronize(s);
+        cudaFree(d_hist);
+        release_stream(dev, s);
+        CK(e);
+        if (o.status == LK_NO_CORRESPONDENCES)
+            return fail(LK_NO_CORRESPONDENCES, "icp: fewer than 6 correspondences");
+        for (int k = 0; k < 9; ++k) result->R[k] = R[k];
+        for (int k = 0; k < 3; ++k) result->t[k] = t[k];
+        result->iterations = o.iterations;
+        result->converged = o.converged;
+        result->correspondences = o.correspondences;
+        result->rmse = o.rmse;
+        result->fitness = o.fitness;
+        return LK_OK;
+    });
+}
+
 lk_status lk_feature_nn_cache(const float* src_features, int64_t ns, const float* tgt_features, int64_t nt,
                               int32_t device, int32_t* cache) {
     return guarded([&]() -> lk_status {

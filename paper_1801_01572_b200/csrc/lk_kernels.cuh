@@ -88,6 +88,32 @@ struct GridStorage {
     void release();
 };
 
+// Ring grid (lk_ring.cu): dense CSR of small cells for exact NN on dense
+// targets, with the reference EvalGrid's frame for the window check.
+struct RingGrid {
+    double ox, oy, oz, cell;  // ring cells: origin = bbox_lo
+    int nx, ny, nz;
+    int rmax;                 // shells beyond which nothing lies within d_max
+    int64_t ncells, npoints;
+    float delta;              // FP32 coordinate error (cells, both sides)
+    float band;               // guard on FP32 d2 (squared cells)
+    float thr;                // d_max^2 in squared cells
+    const int32_t* start;     // ncells + 1
+    const float4* pts;        // CSR order: ring-cell coordinates, original index in w
+    const double4* pos4;      // original order FP64 (x, y, z, 0)
+    double eox, eoy, eoz, ecell;  // the reference EvalGrid at cell = d_max
+    int enx, eny, enz;
+};
+struct RingStorage {
+    RingGrid view{};
+    int32_t* start = nullptr;
+    float4* pts = nullptr;
+    double4* pos4 = nullptr;
+    cudaStream_t stream = nullptr;
+    void release();
+};
+cudaError_t build_ring_grid(RingStorage& rs, const double* d_pos, int64_t n, double d_max, cudaStream_t stream);
+
 // Builds a grid of the given kind from device arrays pos/nrm (nrm may be null).
 // Returns cudaSuccess or the first CUDA error; throws nothing.
 // with_blocks = false skips the 3x3x3 block lists (neighbour grids of FPFH).
@@ -199,6 +225,18 @@ cudaError_t run_hypotheses_range(const SourceView& src, const double* d_tgt_pos,
                                  const GridView& grid, const ScoreParams& sp, uint64_t seed, double tau, int64_t begin,
                                  int64_t end, RunBuffers& rb, void* d_record, cudaStream_t stream, int sm_count,
                                  cudaEvent_t* events = nullptr);
+
+// ICP point-to-plane (lk_icp.cu; spec frozen in oracle/lk_oracle.cpp "ICP").
+// `grid` is the target's EvalGrid at cell = max_dist; d_src is 3 * n FP64.
+struct IcpOutcome {
+    int32_t iterations, converged, status;
+    int64_t correspondences;
+    double rmse, fitness;
+};
+cudaError_t icp_point_to_plane(const double* d_src, int64_t n, const GridStorage& grid, double max_dist,
+                               int32_t max_iter, double eps, const double* R0, const double* t0, double* R9,
+                               double* t3, IcpOutcome* out, double* d_history, cudaStream_t stream, int sm_count,
+                               bool fast = true);
 
 // Scores an explicit candidate list (Rt on device, C x 12) and reduces the best.
 cudaError_t score_candidates(const SourceView& src, const GridView& grid, const ScoreParams& sp, const double* d_rt,

@@ -1,0 +1,190 @@
+// lk_ring.cu -- exact nearest neighbour for dense targets (ICP, config D).
+//
+// The EvalGrid's 3x3x3 block lists grow with the square of the target density
+// (a 640x480-rendered submap puts ~150 points in a 5 cm cell, ~4000 in its
+// block). The ring grid instead bins the target into small cells (dense CSR
+// over the bounding box, cell ~ d_max / 4 within a memory cap) and answers a
+// query by scanning cube shells of cells around it in FP32, stopping as soon
+// as no unscanned entry can be nearer (or tie), then deciding in FP64:
+//   * FP32 keeps the three smallest d2; the stop test and the FP64 re-check
+//     use guard bands sized from the conversion error of both coordinates;
+//   * the winner (and every entry within the band) is re-evaluated with the
+//     FP64 d2 and the (d2, original index) order;
+//   * the result is the reference's EvalGrid neighbour
+//     (registration.cpp:165-199): the query's EvalGrid cell must be inside the
+//     grid, and a global nearest point outside the query's +-1 EvalGrid
+//     window (possible only when a division rounds across a cell face) sends
+//     the query to an exact scan of that window.
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+
+#include "lk_device_math.cuh"
+#include "lk_kernels.cuh"
+
+namespace lkk {
+
+using namespace lkd;
+
+namespace {
+
+inline unsigned nblocks(int64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
+
+__device__ __forceinline__ unsigned long long order_key(double d) {
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(d));
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__host__ __device__ inline double from_key(unsigned long long k) {
+    const unsigned long long b = (k >> 63) ? (k & 0x7fffffffffffffffull) : ~k;
+    double d;
+    memcpy(&d, &b, sizeof(d));
+    return d;
+}
+
+// keys[0..2] = min, keys[3..5] = max (orderable encodings)
+__global__ void k_ring_bbox(const double* __restrict__ p, int64_t n, unsigned long long* keys) {
+    unsigned long long lo[3] = {~0ull, ~0ull, ~0ull}, hi[3] = {0ull, 0ull, 0ull};
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        for (int a = 0; a < 3; ++a) {
+            const unsigned long long k = order_key(p[3 * i + a]);
+            lo[a] = k < lo[a] ? k : lo[a];
+            hi[a] = k > hi[a] ? k : hi[a];
+        }
+    for (int a = 0; a < 3; ++a) {
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long x = __shfl_xor_sync(0xffffffffu, lo[a], o);
+            const unsigned long long y = __shfl_xor_sync(0xffffffffu, hi[a], o);
+            lo[a] = x < lo[a] ? x : lo[a];
+            hi[a] = y > hi[a] ? y : hi[a];
+        }
+        if ((threadIdx.x & 31) == 0) {
+            atomicMin(keys + a, lo[a]);
+            atomicMax(keys + 3 + a, hi[a]);
+        }
+    }
+}
+
+__device__ __forceinline__ int ring_cell_axis(double v, double o, double cell, int n) {
+    int c = static_cast<int>(floor((v - o) / cell));
+    return c < 0 ? 0 : (c >= n ? n - 1 : c);
+}
+
+__global__ void k_ring_count(const double* __restrict__ p, int64_t n, RingGrid rg, int32_t* __restrict__ cell_of,
+                             int32_t* __restrict__ counts) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const int cx = ring_cell_axis(p[3 * i], rg.ox, rg.cell, rg.nx);
+    const int cy = ring_cell_axis(p[3 * i + 1], rg.oy, rg.cell, rg.ny);
+    const int cz = ring_cell_axis(p[3 * i + 2], rg.oz, rg.cell, rg.nz);
+    const int64_t c = (static_cast<int64_t>(cx) * rg.ny + cy) * rg.nz + cz;
+    cell_of[i] = static_cast<int32_t>(c);
+    atomicAdd(counts + c, 1);
+}
+
+__global__ void k_ring_scatter(const double* __restrict__ p, int64_t n, RingGrid rg,
+                               const int32_t* __restrict__ cell_of, int32_t* __restrict__ cursor,
+                               float4* __restrict__ pts) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const int32_t s = rg.start[cell_of[i]] + atomicAdd(cursor + cell_of[i], 1);
+    pts[s] = make_float4(static_cast<float>((p[3 * i] - rg.ox) / rg.cell),
+                         static_cast<float>((p[3 * i + 1] - rg.oy) / rg.cell),
+                         static_cast<float>((p[3 * i + 2] - rg.oz) / rg.cell), __int_as_float(static_cast<int>(i)));
+}
+
+}  // namespace
+
+void RingStorage::release() {
+    pool_free(start, stream);
+    pool_free(pts, stream);
+    pool_free(pos4, stream);
+    start = nullptr;
+    pts = nullptr;
+    pos4 = nullptr;
+    view = RingGrid{};
+}
+
+cudaError_t build_ring_grid(RingStorage& rs, const double* d_pos, int64_t n, double d_max, cudaStream_t stream) {
+#define RG_TRY(x)                         \
+    do {                                  \
+        cudaError_t e_ = (x);             \
+        if (e_ != cudaSuccess) return e_; \
+    } while (0)
+    rs.stream = stream;
+    if (n <= 0 || n > INT32_MAX || !(d_max > 0.0)) return cudaErrorInvalidValue;
+    unsigned long long* keys = nullptr;
+    RG_TRY(cudaMallocAsync(&keys, 6 * sizeof(unsigned long long), stream));
+    const unsigned long long init[6] = {~0ull, ~0ull, ~0ull, 0ull, 0ull, 0ull};
+    RG_TRY(cudaMemcpyAsync(keys, init, sizeof(init), cudaMemcpyHostToDevice, stream));
+    k_ring_bbox<<<std::min<unsigned>(nblocks(n, 256), 296), 256, 0, stream>>>(d_pos, n, keys);
+    unsigned long long hk[6];
+    RG_TRY(cudaMemcpyAsync(hk, keys, sizeof(hk), cudaMemcpyDeviceToHost, stream));
+    RG_TRY(cudaStreamSynchronize(stream));
+    cudaFreeAsync(keys, stream);
+    double lo[3], hi[3];
+    for (int a = 0; a < 3; ++a) {
+        lo[a] = from_key(hk[a]);
+        hi[a] = from_key(hk[3 + a]);
+    }
+    RingGrid v{};
+    // the reference's EvalGrid over the same cloud (registration.cpp:82-97)
+    v.ecell = d_max;
+    v.eox = lo[0] - d_max;
+    v.eoy = lo[1] - d_max;
+    v.eoz = lo[2] - d_max;
+    v.enx = static_cast<int>(std::floor(((hi[0] - v.eox) + d_max) / d_max)) + 2;
+    v.eny = static_cast<int>(std::floor(((hi[1] - v.eoy) + d_max) / d_max)) + 2;
+    v.enz = static_cast<int>(std::floor(((hi[2] - v.eoz) + d_max) / d_max)) + 2;
+    // ring cells: d_max / 4, coarsened until the dense CSR stays under 2^27 cells
+    double cell = d_max / 4.0;
+    int64_t nc = 0;
+    int dims[3];
+    for (int guard = 0; guard < 64; ++guard) {
+        for (int a = 0; a < 3; ++a) dims[a] = static_cast<int>(std::floor((hi[a] - lo[a]) / cell)) + 1;
+        nc = static_cast<int64_t>(dims[0]) * dims[1] * dims[2];
+        if (nc <= (int64_t(1) << 27)) break;
+        cell *= 1.25;
+    }
+    v.ox = lo[0];
+    v.oy = lo[1];
+    v.oz = lo[2];
+    v.cell = cell;
+    v.nx = dims[0];
+    v.ny = dims[1];
+    v.nz = dims[2];
+    v.ncells = nc;
+    v.rmax = static_cast<int>(std::ceil(d_max / cell)) + 2;
+    // FP32 conversion error of a coordinate (cells), both sides, plus slack
+    const double nmax = std::max(v.nx, std::max(v.ny, v.nz)) + v.rmax + 2.0;
+    v.delta = static_cast<float>(2.0 * nmax * 5.9604644775390625e-8 + 1e-6);
+    const double thr = (d_max / cell) * (d_max / cell);
+    v.thr = static_cast<float>(thr);
+    // |d2_fp32 - d2| <= 2 sqrt3 |d| delta + 3 delta^2 + 4 u d2 over |d| <= rmax cells; 4x margin
+    const double R = v.rmax + 1.0;
+    v.band = static_cast<float>(4.0 * (2.0 * 1.7320508 * R * v.delta + 3.0 * v.delta * v.delta +
+                                       4.0 * 5.9604644775390625e-8 * R * R) + 1e-6);
+    int32_t *cell_of = nullptr, *counts = nullptr;
+    RG_TRY(cudaMallocAsync(&cell_of, n * sizeof(int32_t), stream));
+    RG_TRY(cudaMallocAsync(&counts, nc * sizeof(int32_t), stream));
+    RG_TRY(pool_alloc(&rs.start, (nc + 1) * sizeof(int32_t), stream));
+    RG_TRY(pool_alloc(&rs.pts, n * sizeof(float4), stream));
+    RG_TRY(cudaMemsetAsync(counts, 0, nc * sizeof(int32_t), stream));
+    k_ring_count<<<nblocks(n, 256), 256, 0, stream>>>(d_pos, n, v, cell_of, counts);
+    RG_TRY(exclusive_scan(counts, nc, rs.start, stream));
+    RG_TRY(cudaMemsetAsync(counts, 0, nc * sizeof(int32_t), stream));
+    v.start = rs.start;
+    k_ring_scatter<<<nblocks(n, 256), 256, 0, stream>>>(d_pos, n, v, cell_of, counts, rs.pts);
+    RG_TRY(pool_alloc(&rs.pos4, n * sizeof(double4), stream));
+    RG_TRY(make_records(d_pos, nullptr, n, rs.pos4, nullptr, stream));
+    cudaFreeAsync(cell_of, stream);
+    cudaFreeAsync(counts, stream);
+    v.pts = rs.pts;
+    v.pos4 = rs.pos4;
+    v.npoints = n;
+    rs.view = v;
+    return cudaGetLastError();
+#undef RG_TRY
+}
+
+}  // namespace lkk

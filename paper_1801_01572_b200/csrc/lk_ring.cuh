@@ -1,0 +1,159 @@
+// lk_ring.cuh -- device query of the ring grid (lk_ring.cu): the reference
+// EvalGrid's nearest neighbour within d_max (registration.cpp:165-199
+// semantics) for dense targets. See lk_ring.cu for the exactness argument.
+#pragma once
+
+#include <cstdint>
+
+#include "lk_device_math.cuh"
+#include "lk_kernels.cuh"
+
+namespace lkk {
+
+// visits the entries of the cube shell of radius r around (cx, cy, cz)
+template <class F>
+__device__ __forceinline__ void ring_shell(const RingGrid& rg, int cx, int cy, int cz, int r, F&& f) {
+    for (int dx = -r; dx <= r; ++dx) {
+        const int x = cx + dx;
+        if (x < 0 || x >= rg.nx) continue;
+        for (int dy = -r; dy <= r; ++dy) {
+            const int y = cy + dy;
+            if (y < 0 || y >= rg.ny) continue;
+            const int64_t row = (static_cast<int64_t>(x) * rg.ny + y) * rg.nz;
+            const bool edge = dx == -r || dx == r || dy == -r || dy == r;
+            for (int pass = 0; pass < (edge ? 1 : 2); ++pass) {
+                int z0, z1;
+                if (edge) {
+                    z0 = cz - r;
+                    z1 = cz + r;
+                } else {
+                    z0 = z1 = pass == 0 ? cz - r : cz + r;
+                }
+                z0 = z0 < 0 ? 0 : z0;
+                z1 = z1 >= rg.nz ? rg.nz - 1 : z1;
+                if (z0 > z1) continue;
+                const int32_t s0 = __ldg(rg.start + row + z0), s1 = __ldg(rg.start + row + z1 + 1);
+                for (int32_t e = s0; e < s1; ++e) f(e);
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ int ecell_axis(double v, double o, double c) { return static_cast<int>(floor((v - o) / c)); }
+
+// exact scan of the reference window (the +-1 EvalGrid cells of y's cell)
+__device__ __noinline__ int32_t ring_window_scan(const RingGrid& rg, lkd::V3 y, double d2_max, int ex, int ey,
+                                                 int ez) {
+    using namespace lkd;
+    const double lx = rg.eox + (ex - 1) * rg.ecell, hx = rg.eox + (ex + 2) * rg.ecell;
+    const double ly = rg.eoy + (ey - 1) * rg.ecell, hy = rg.eoy + (ey + 2) * rg.ecell;
+    const double lz = rg.eoz + (ez - 1) * rg.ecell, hz = rg.eoz + (ez + 2) * rg.ecell;
+    auto clampc = [](int c, int n) { return c < 0 ? 0 : (c >= n ? n - 1 : c); };
+    const int x0 = clampc(static_cast<int>(floor((lx - rg.ox) / rg.cell)) - 1, rg.nx);
+    const int x1 = clampc(static_cast<int>(floor((hx - rg.ox) / rg.cell)) + 1, rg.nx);
+    const int y0 = clampc(static_cast<int>(floor((ly - rg.oy) / rg.cell)) - 1, rg.ny);
+    const int y1 = clampc(static_cast<int>(floor((hy - rg.oy) / rg.cell)) + 1, rg.ny);
+    const int z0 = clampc(static_cast<int>(floor((lz - rg.oz) / rg.cell)) - 1, rg.nz);
+    const int z1 = clampc(static_cast<int>(floor((hz - rg.oz) / rg.cell)) + 1, rg.nz);
+    double best_d2 = __longlong_as_double(0x7ff0000000000000ll);
+    int32_t best = INT32_MAX;
+    for (int x = x0; x <= x1; ++x)
+        for (int yy = y0; yy <= y1; ++yy) {
+            const int64_t row = (static_cast<int64_t>(x) * rg.ny + yy) * rg.nz;
+            for (int32_t e = rg.start[row + z0]; e < rg.start[row + z1 + 1]; ++e) {
+                const int32_t o = __float_as_int(rg.pts[e].w);
+                const V3 q = ld4(rg.pos4, o);
+                const int qx = ecell_axis(q.x, rg.eox, rg.ecell), qy = ecell_axis(q.y, rg.eoy, rg.ecell),
+                          qz = ecell_axis(q.z, rg.eoz, rg.ecell);
+                if (qx < ex - 1 || qx > ex + 1 || qy < ey - 1 || qy > ey + 1 || qz < ez - 1 || qz > ez + 1) continue;
+                const double d2 = sqnorm(sub(q, y));
+                if (d2 > d2_max) continue;
+                if (d2 < best_d2 || (d2 == best_d2 && o < best)) {
+                    best_d2 = d2;
+                    best = o;
+                }
+            }
+        }
+    return best == INT32_MAX ? -1 : best;
+}
+
+__device__ __forceinline__ void ring_top3(float d2, int32_t o, float& f1, float& f2, float& f3, int32_t& o1,
+                                          int32_t& o2) {
+    if (d2 < f1) {
+        f3 = f2;
+        f2 = f1;
+        o2 = o1;
+        f1 = d2;
+        o1 = o;
+    } else if (d2 < f2) {
+        f3 = f2;
+        f2 = d2;
+        o2 = o;
+    } else if (d2 < f3) {
+        f3 = d2;
+    }
+}
+
+// Original index of the reference EvalGrid neighbour of y within d_max, or -1.
+__device__ __forceinline__ int32_t ring_nn(const RingGrid& rg, lkd::V3 y, double d2_max) {
+    using namespace lkd;
+    // the reference's cell of y (registration.cpp:167-172): outside the grid => miss
+    const double fx = floor((y.x - rg.eox) / rg.ecell), fy = floor((y.y - rg.eoy) / rg.ecell),
+                 fz = floor((y.z - rg.eoz) / rg.ecell);
+    if (!(fx >= 0.0 && fy >= 0.0 && fz >= 0.0 && fx < rg.enx && fy < rg.eny && fz < rg.enz)) return -1;
+    const float qx = static_cast<float>((y.x - rg.ox) / rg.cell);
+    const float qy = static_cast<float>((y.y - rg.oy) / rg.cell);
+    const float qz = static_cast<float>((y.z - rg.oz) / rg.cell);
+    const int cx = static_cast<int>(floorf(qx)), cy = static_cast<int>(floorf(qy)), cz = static_cast<int>(floorf(qz));
+    const float inf = __int_as_float(0x7f800000);
+    float f1 = inf, f2 = inf, f3 = inf;
+    int32_t o1 = -1, o2 = -1;
+    int r_end = 0;
+    for (int r = 0; r <= rg.rmax; ++r) {
+        ring_shell(rg, cx, cy, cz, r, [&](int32_t e) {
+            const float4 A = __ldg(rg.pts + e);
+            const float dx = qx - A.x, dy = qy - A.y, dz = qz - A.z;
+            ring_top3(fmaf(dx, dx, fmaf(dy, dy, dz * dz)), __float_as_int(A.w), f1, f2, f3, o1, o2);
+        });
+        r_end = r;
+        // every entry outside the scanned cube lies >= r - delta cells away
+        const float m = static_cast<float>(r) - rg.delta;
+        if (m > 0.0f && m * m > fminf(f1 + 2.0f * rg.band, rg.thr + rg.band)) break;
+    }
+    if (f1 > rg.thr + rg.band) return -1;
+    double best_d2 = __longlong_as_double(0x7ff0000000000000ll);
+    int32_t best = INT32_MAX;
+    auto consider = [&](int32_t o) {
+        const V3 q = ld4(rg.pos4, o);
+        const double d2 = sqnorm(sub(q, y));
+        if (d2 > d2_max) return;
+        if (d2 < best_d2 || (d2 == best_d2 && o < best)) {
+            best_d2 = d2;
+            best = o;
+        }
+    };
+    const float lim = f1 + 2.0f * rg.band;
+    if (f3 <= lim) {
+        for (int r = 0; r <= r_end; ++r)
+            ring_shell(rg, cx, cy, cz, r, [&](int32_t e) {
+                const float4 A = __ldg(rg.pts + e);
+                const float dx = qx - A.x, dy = qy - A.y, dz = qz - A.z;
+                if (fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= lim) consider(__float_as_int(A.w));
+            });
+    } else {
+        consider(o1);
+        if (f2 <= lim) consider(o2);
+    }
+    if (best == INT32_MAX) return -1;
+    // the reference only sees its +-1 window: a nearest point outside it (a
+    // division rounded across a face) sends the query to the exact window scan
+    const V3 q = ld4(rg.pos4, best);
+    const int ex = static_cast<int>(fx), ey = static_cast<int>(fy), ez = static_cast<int>(fz);
+    const int wx = ecell_axis(q.x, rg.eox, rg.ecell), wy = ecell_axis(q.y, rg.eoy, rg.ecell),
+              wz = ecell_axis(q.z, rg.eoz, rg.ecell);
+    if (wx < ex - 1 || wx > ex + 1 || wy < ey - 1 || wy > ey + 1 || wz < ez - 1 || wz > ez + 1)
+        return ring_window_scan(rg, y, d2_max, ex, ey, ez);
+    return best;
+}
+
+}  // namespace lkk

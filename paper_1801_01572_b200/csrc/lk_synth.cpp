@@ -405,6 +405,36 @@ Fixture frame_pair(uint64_t seed, int boxes, int width, int height, double fx, d
     return f;
 }
 
+// Config D: two submaps of make_room_scene(seed), each the
+// world-frame union of `views` full renders along an orbit arc (frames
+// a0 + step k and b0 + step k of the synth_scene orbit), not downsampled;
+// the source is displaced by synth_random_transform(pi/3, 1 m) from
+// RngStream(seed, 0xD00); truth maps the source back onto the target.
+Fixture submap_pair(uint64_t seed, int boxes, int views, int width, int height, int stride, double noise, int frames,
+                    int a0, int b0, int step) {
+    Scene scene = make_room_scene(seed, boxes);
+    Intrinsics k{525.0, 525.0, 319.5 * width / 640.0, 239.5 * height / 480.0, width, height};
+    auto submap = [&](int f0) {
+        Cloud world;
+        for (int v = 0; v < views; ++v) {
+            const int fr = f0 + step * v;
+            Rigid pose = orbit_pose(frames, fr);
+            RngStream r(seed, 0xD10 + static_cast<uint64_t>(fr));
+            append(world, transformed(render_view(scene, pose, k, stride, noise, r), pose));
+        }
+        return world;
+    };
+    Cloud a = submap(a0), b = submap(b0);
+    RngStream rng(seed, 0xD00);
+    Rigid displace = synth_random_transform(rng, M_PI / 3.0, 1.0);
+    Fixture f;
+    f.clouds.push_back(transformed(a, displace));
+    f.clouds.push_back(std::move(b));
+    f.transforms.push_back(inverse(displace));
+    f.scalars.push_back(0.0);
+    return f;
+}
+
 // Config A: Q = sample_surface(scatter scene), P = T^-1 (Q + noise).
 Fixture surface_pair(uint64_t seed, double density, double noise) {
     Scene scene = make_scatter_scene(seed);
@@ -470,6 +500,11 @@ void* lks_frame_pair(uint64_t seed, int boxes, int width, int height, double fx,
     return guard(status, [&] {
         return frame_pair(seed, boxes, width, height, fx, fy, cx, cy, stride, noise, frames, frame_a, frame_b);
     });
+}
+void* lks_submap_pair(uint64_t seed, int boxes, int views, int width, int height, int stride, double noise,
+                      int frames, int a0, int b0, int step, int* status) {
+    return guard(status,
+                 [&] { return submap_pair(seed, boxes, views, width, height, stride, noise, frames, a0, b0, step); });
 }
 void* lks_surface_pair(uint64_t seed, double density, double noise, int* status) {
     return guard(status, [&] { return surface_pair(seed, density, noise); });

@@ -483,6 +483,48 @@ def edge_info(cloud_i: PointCloud, cloud_j: PointCloud, t_i: RigidTransform, t_j
     return e
 
 
+# ------------------------------------------------------- ICP (north-star item 4)
+@dataclass
+class IcpParams:
+    """Point-to-plane ICP (no reference: SPEC.md:332; spec in DESIGN.md "ICP")."""
+
+    max_correspondence_distance: float = 0.05
+    max_iterations: int = 30
+    convergence_eps: float = 1e-10
+    device: int = -1
+
+
+@dataclass
+class IcpResult:
+    transform: RigidTransform
+    iterations: int
+    converged: bool
+    correspondences: int
+    rmse: float
+    fitness: float
+    history: np.ndarray  # (iterations evaluated, 3): correspondences, rmse, |delta|^2
+
+
+def icp_point_to_plane(source: PointCloud, target: PointCloud, init: RigidTransform,
+                       params: Optional[IcpParams] = None) -> IcpResult:
+    """Refines `init` (source -> target) by point-to-plane ICP on the device.
+    Raises EmptyCloud / MissingNormals / NoCorrespondences."""
+    p = params or IcpParams()
+    cp = abi.lk_icp_params(max_correspondence_distance=float(p.max_correspondence_distance),
+                           max_iterations=int(p.max_iterations), device=int(p.device),
+                           convergence_eps=float(p.convergence_eps))
+    res = abi.lk_icp_result()
+    T0 = np.ascontiguousarray(init.packed())
+    hist = np.zeros((max(int(p.max_iterations), 1), 3))
+    s, t = source.as_c(), target.as_c()
+    check(abi.lib().lk_icp_point_to_plane(C.byref(s), C.byref(t), T0.ctypes.data_as(abi.dptr), C.byref(cp),
+                                          C.byref(res), hist.ctypes.data_as(abi.dptr)))
+    evaluated = min(int(res.iterations) + (0 if res.converged else 1), int(p.max_iterations))
+    return IcpResult(RigidTransform(np.array(res.R[:]).reshape(3, 3), np.array(res.t[:])), int(res.iterations),
+                     bool(res.converged), int(res.correspondences), float(res.rmse), float(res.fitness),
+                     hist[:evaluated].copy())
+
+
 # ------------------------------------------------------- prepare helpers
 def feature_nn_cache(source_features: np.ndarray, target_features: np.ndarray, device: int = -1) -> np.ndarray:
     """grid.cpp:176-213 semantics pinned to the FP64 exhaustive matcher (reference.hpp:56-76)."""

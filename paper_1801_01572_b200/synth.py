@@ -75,6 +75,18 @@ def depth_frame_pair(seed: int = 1, boxes: int = 6, width: int = 640, height: in
     return _take(h, st)
 
 
+def submap_pair(seed: int = 2, boxes: int = 6, views: int = 8, width: int = 640, height: int = 480, stride: int = 1,
+                noise: float = 0.005, frames: int = 90, a0: int = 0, b0: int = 8, step: int = 2) -> RegistrationPair:
+    """Config D: world-frame unions of `views` renders of
+    make_room_scene(seed) along two overlapping orbit arcs (~2.4M points each
+    at 640x480, stride 1), no downsample; the source is displaced by
+    random_transform(pi/3, 1 m) and truth maps it back onto the target."""
+    st = C.c_int()
+    h = abi.synth_lib().lks_submap_pair(seed, boxes, views, width, height, stride, noise, frames, a0, b0, step,
+                                        C.byref(st))
+    return _take(h, st)
+
+
 def surface_pair(seed: int = 1, density: float = 1000.0, noise: float = 0.005) -> RegistrationPair:
     """Config A: Q = sample_surface(make_scatter_scene(seed)),
     P = T^-1 (Q + N(0, noise^2)); truth T = random_transform(RngStream(seed, 0xA110))."""
