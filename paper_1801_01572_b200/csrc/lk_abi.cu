@@ -970,7 +970,7 @@ lk_status lk_icp_point_to_plane(const lk_cloud* source, const lk_cloud* target, 
         const int dev = select_device(params->device);
         const int sms = sm_count_of(dev);
         cudaStream_t s = acquire_stream(dev);
-        lkk::GridStorage g;
+        lkk::RingStorage g;
         double *d_src = nullptr, *d_tp = nullptr, *d_tn = nullptr, *d_hist = nullptr;
         lkk::IcpOutcome o{};
         double R[9], t[3];
@@ -981,11 +981,10 @@ lk_status lk_icp_point_to_plane(const lk_cloud* source, const lk_cloud* target, 
             d_tn = dev_upload(target->nxyz, 3 * target->n, s);
             const int64_t hn = 3 * static_cast<int64_t>(params->max_iterations);
             if (history && hn > 0) CK(cudaMalloc(&d_hist, hn * sizeof(double)));
-            e = lkk::build_grid(g, 0, d_tp, d_tn, target->n, dmax, dmax, s);
+            e = lkk::build_ring_grid(g, d_tp, target->n, dmax, s, fast_path_enabled());
             if (e == cudaSuccess)
-                e = lkk::icp_point_to_plane(d_src, source->n, g, dmax, params->max_iterations,
-                                            params->convergence_eps, T0, T0 + 9, R, t, &o, d_hist, s, sms,
-                                            fast_path_enabled());
+                e = lkk::icp_point_to_plane(d_src, source->n, g, d_tn, dmax, params->max_iterations,
+                                            params->convergence_eps, T0, T0 + 9, R, t, &o, d_hist, s, sms);
             if (e == cudaSuccess && d_hist)
                 e = cudaMemcpyAsync(history, d_hist, hn * sizeof(double), cudaMemcpyDeviceToHost, s);
             if (e == cudaSuccess) e = cudaStreamSynchronize(s);

@@ -112,7 +112,8 @@ struct RingStorage {
     cudaStream_t stream = nullptr;
     void release();
 };
-cudaError_t build_ring_grid(RingStorage& rs, const double* d_pos, int64_t n, double d_max, cudaStream_t stream);
+cudaError_t build_ring_grid(RingStorage& rs, const double* d_pos, int64_t n, double d_max, cudaStream_t stream,
+                            bool fast = true);
 
 // Builds a grid of the given kind from device arrays pos/nrm (nrm may be null).
 // Returns cudaSuccess or the first CUDA error; throws nothing.
@@ -227,16 +228,17 @@ cudaError_t run_hypotheses_range(const SourceView& src, const double* d_tgt_pos,
                                  cudaEvent_t* events = nullptr);
 
 // ICP point-to-plane (lk_icp.cu; spec frozen in oracle/lk_oracle.cpp "ICP").
-// `grid` is the target's EvalGrid at cell = max_dist; d_src is 3 * n FP64.
+// `ring` is the target's ring grid at d_max = max_dist, d_tnrm its normals
+// (3 * nt FP64, original order); d_src is 3 * n FP64.
 struct IcpOutcome {
     int32_t iterations, converged, status;
     int64_t correspondences;
     double rmse, fitness;
 };
-cudaError_t icp_point_to_plane(const double* d_src, int64_t n, const GridStorage& grid, double max_dist,
-                               int32_t max_iter, double eps, const double* R0, const double* t0, double* R9,
-                               double* t3, IcpOutcome* out, double* d_history, cudaStream_t stream, int sm_count,
-                               bool fast = true);
+cudaError_t icp_point_to_plane(const double* d_src, int64_t n, const RingStorage& ring, const double* d_tnrm,
+                               double max_dist, int32_t max_iter, double eps, const double* R0, const double* t0,
+                               double* R9, double* t3, IcpOutcome* out, double* d_history, cudaStream_t stream,
+                               int sm_count);
 
 // Scores an explicit candidate list (Rt on device, C x 12) and reduces the best.
 cudaError_t score_candidates(const SourceView& src, const GridView& grid, const ScoreParams& sp, const double* d_rt,

@@ -3,7 +3,7 @@
 // The EvalGrid's 3x3x3 block lists grow with the square of the target density
 // (a 640x480-rendered submap puts ~150 points in a 5 cm cell, ~4000 in its
 // block). The ring grid instead bins the target into small cells (dense CSR
-// over the bounding box, cell ~ d_max / 4 within a memory cap) and answers a
+// over the bounding box, cell ~ d_max / 6 within a memory cap) and answers a
 // query by scanning cube shells of cells around it in FP32, stopping as soon
 // as no unscanned entry can be nearer (or tie), then deciding in FP64:
 //   * FP32 keeps the three smallest d2; the stop test and the FP64 re-check
@@ -105,7 +105,8 @@ void RingStorage::release() {
     view = RingGrid{};
 }
 
-cudaError_t build_ring_grid(RingStorage& rs, const double* d_pos, int64_t n, double d_max, cudaStream_t stream) {
+cudaError_t build_ring_grid(RingStorage& rs, const double* d_pos, int64_t n, double d_max, cudaStream_t stream,
+                            bool fast) {
 #define RG_TRY(x)                         \
     do {                                  \
         cudaError_t e_ = (x);             \
@@ -136,14 +137,14 @@ cudaError_t build_ring_grid(RingStorage& rs, const double* d_pos, int64_t n, dou
     v.enx = static_cast<int>(std::floor(((hi[0] - v.eox) + d_max) / d_max)) + 2;
     v.eny = static_cast<int>(std::floor(((hi[1] - v.eoy) + d_max) / d_max)) + 2;
     v.enz = static_cast<int>(std::floor(((hi[2] - v.eoz) + d_max) / d_max)) + 2;
-    // ring cells: d_max / 4, coarsened until the dense CSR stays under 2^27 cells
-    double cell = d_max / 4.0;
+    // ring cells: d_max / 6, coarsened until the dense CSR stays under 2^28 cells
+    double cell = d_max / 6.0;
     int64_t nc = 0;
     int dims[3];
     for (int guard = 0; guard < 64; ++guard) {
         for (int a = 0; a < 3; ++a) dims[a] = static_cast<int>(std::floor((hi[a] - lo[a]) / cell)) + 1;
         nc = static_cast<int64_t>(dims[0]) * dims[1] * dims[2];
-        if (nc <= (int64_t(1) << 27)) break;
+        if (nc <= (int64_t(1) << 28)) break;
         cell *= 1.25;
     }
     v.ox = lo[0];
@@ -164,6 +165,9 @@ cudaError_t build_ring_grid(RingStorage& rs, const double* d_pos, int64_t n, dou
     const double R = v.rmax + 1.0;
     v.band = static_cast<float>(4.0 * (2.0 * 1.7320508 * R * v.delta + 3.0 * v.delta * v.delta +
                                        4.0 * 5.9604644775390625e-8 * R * R) + 1e-6);
+    // FP64-only mode: an infinite band scans every shell within d_max and
+    // decides every entry in FP64 (the tests' exhaustive reference path)
+    if (!fast) v.band = 1e30f;
     int32_t *cell_of = nullptr, *counts = nullptr;
     RG_TRY(cudaMallocAsync(&cell_of, n * sizeof(int32_t), stream));
     RG_TRY(cudaMallocAsync(&counts, nc * sizeof(int32_t), stream));

@@ -10,29 +10,38 @@
 
 namespace lkk {
 
-// visits the entries of the cube shell of radius r around (cx, cy, cz)
-template <class F>
-__device__ __forceinline__ void ring_shell(const RingGrid& rg, int cx, int cy, int cz, int r, F&& f) {
+// Visits the entries of the cells of the cube shell of radius r around
+// (cx, cy, cz) that can hold a point within sqrt(bound()) cells of q: a
+// cell's entries lie within [c - delta, c + 1 + delta] per axis, so a cell
+// whose box is farther than that from q is skipped without loading it. The
+// bound is re-read as entries are visited (it shrinks as the best improves).
+template <class B, class F>
+__device__ __forceinline__ void ring_shell(const RingGrid& rg, float qx, float qy, float qz, int cx, int cy, int cz,
+                                           int r, B&& bound, F&& f) {
+    const float dl = rg.delta;
+    auto gap = [dl](float q, int c) {  // distance from q to [c - dl, c + 1 + dl]
+        const float lo = static_cast<float>(c) - dl, hi = static_cast<float>(c + 1) + dl;
+        return q < lo ? lo - q : (q > hi ? q - hi : 0.0f);
+    };
     for (int dx = -r; dx <= r; ++dx) {
         const int x = cx + dx;
         if (x < 0 || x >= rg.nx) continue;
+        const float gx = gap(qx, x);
+        if (gx * gx > bound()) continue;
         for (int dy = -r; dy <= r; ++dy) {
             const int y = cy + dy;
             if (y < 0 || y >= rg.ny) continue;
+            const float gy = gap(qy, y);
+            const float gxy = gx * gx + gy * gy;
+            if (gxy > bound()) continue;
             const int64_t row = (static_cast<int64_t>(x) * rg.ny + y) * rg.nz;
             const bool edge = dx == -r || dx == r || dy == -r || dy == r;
-            for (int pass = 0; pass < (edge ? 1 : 2); ++pass) {
-                int z0, z1;
-                if (edge) {
-                    z0 = cz - r;
-                    z1 = cz + r;
-                } else {
-                    z0 = z1 = pass == 0 ? cz - r : cz + r;
-                }
-                z0 = z0 < 0 ? 0 : z0;
-                z1 = z1 >= rg.nz ? rg.nz - 1 : z1;
-                if (z0 > z1) continue;
-                const int32_t s0 = __ldg(rg.start + row + z0), s1 = __ldg(rg.start + row + z1 + 1);
+            const int step = edge ? 1 : (r > 0 ? 2 * r : 1);
+            for (int z = cz - r; z <= cz + r; z += step) {
+                if (z < 0 || z >= rg.nz) continue;
+                const float gz = gap(qz, z);
+                if (gxy + gz * gz > bound()) continue;
+                const int32_t s0 = __ldg(rg.start + row + z), s1 = __ldg(rg.start + row + z + 1);
                 for (int32_t e = s0; e < s1; ++e) f(e);
             }
         }
@@ -109,8 +118,11 @@ __device__ __forceinline__ int32_t ring_nn(const RingGrid& rg, lkd::V3 y, double
     float f1 = inf, f2 = inf, f3 = inf;
     int32_t o1 = -1, o2 = -1;
     int r_end = 0;
+    // entries farther than this (squared cells) can be neither the nearest,
+    // nor tied with it, nor within d_max
+    auto bound = [&]() { return fminf(f1 + 2.0f * rg.band, rg.thr + rg.band); };
     for (int r = 0; r <= rg.rmax; ++r) {
-        ring_shell(rg, cx, cy, cz, r, [&](int32_t e) {
+        ring_shell(rg, qx, qy, qz, cx, cy, cz, r, bound, [&](int32_t e) {
             const float4 A = __ldg(rg.pts + e);
             const float dx = qx - A.x, dy = qy - A.y, dz = qz - A.z;
             ring_top3(fmaf(dx, dx, fmaf(dy, dy, dz * dz)), __float_as_int(A.w), f1, f2, f3, o1, o2);
@@ -118,7 +130,7 @@ __device__ __forceinline__ int32_t ring_nn(const RingGrid& rg, lkd::V3 y, double
         r_end = r;
         // every entry outside the scanned cube lies >= r - delta cells away
         const float m = static_cast<float>(r) - rg.delta;
-        if (m > 0.0f && m * m > fminf(f1 + 2.0f * rg.band, rg.thr + rg.band)) break;
+        if (m > 0.0f && m * m > bound()) break;
     }
     if (f1 > rg.thr + rg.band) return -1;
     double best_d2 = __longlong_as_double(0x7ff0000000000000ll);
@@ -134,8 +146,9 @@ __device__ __forceinline__ int32_t ring_nn(const RingGrid& rg, lkd::V3 y, double
     };
     const float lim = f1 + 2.0f * rg.band;
     if (f3 <= lim) {
+        auto lim_bound = [&]() { return lim; };
         for (int r = 0; r <= r_end; ++r)
-            ring_shell(rg, cx, cy, cz, r, [&](int32_t e) {
+            ring_shell(rg, qx, qy, qz, cx, cy, cz, r, lim_bound, [&](int32_t e) {
                 const float4 A = __ldg(rg.pts + e);
                 const float dx = qx - A.x, dy = qy - A.y, dz = qz - A.z;
                 if (fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= lim) consider(__float_as_int(A.w));

@@ -37,7 +37,7 @@ def _check_same(oracle, pair, T0, dmax, iters, eps):
     return dev
 
 
-@pytest.mark.parametrize("fp64_only", [False, True])
+@pytest.mark.parametrize("fp64_only", [False, True])  # True: infinite band, every shell in FP64
 def test_icp_submaps_match_oracle(oracle, monkeypatch, fp64_only):
     if fp64_only:
         monkeypatch.setenv("LK_FP64_ONLY", "1")
