@@ -201,6 +201,41 @@ lk_status lk_score_candidates(lk_grid* grid, const lk_cloud* src, const double* 
 lk_status lk_edge_info_batched(const lk_cloud* clouds_i, const lk_cloud* clouds_j, const double* Ti, const double* Tj,
                                int64_t n_pairs, double epsilon, int32_t device, double* info, int64_t* pair_count);
 
+/* ---- batched loop verification (north-star item 5, config E) -------------
+ * Per pair k, with Q = clouds_i[k] (the earlier fragment, pose Ti[k]),
+ * P = clouds_j[k] (the later fragment, pose Tj[k]) and the measurement
+ * T[k] mapping P into Q's frame, all bit-exact against the reference:
+ *   info / pair_count  edge_info(Q, P, Ti, Tj, epsilon)   line_process.cpp:11-33
+ *   overlap            propose_loops' overlap of the pair  fragments.cpp:80-100
+ *                      (Tj P points within overlap_radius of Ti Q)
+ *   inliers / ratio / fitness
+ *                      evaluate_hypothesis(T, P, Q, SearchGrid(Q, grid_cell))
+ *                                                          registration.cpp:53-78
+ * A pair without edge correspondences reports pair_count 0 (the reference
+ * throws NoCorrespondences); clouds must be non-empty and carry normals. */
+typedef struct lk_verify_params {
+    double epsilon;          /* edge_info radius */
+    double overlap_radius;   /* LoopParams::overlap_radius (fragments.hpp) */
+    double d_max;            /* RegistrationParams::d_max */
+    double grid_cell;        /* SearchGrid cell of evaluate_hypothesis's target grid; <= 0 -> d_max */
+    double normal_angle_max; /* RegistrationParams::normal_angle_max (radians) */
+    int32_t device;          /* -1: current device */
+    int32_t reserved;
+} lk_verify_params;
+
+typedef struct lk_verify_result {
+    double info[36];      /* row-major 6x6 */
+    int64_t pair_count;
+    int64_t overlap_hits;
+    double overlap;       /* overlap_hits / |P| */
+    int64_t inliers;
+    double inlier_ratio;  /* inliers / |P| */
+    double fitness;       /* sum of distance^2 / inliers (0 without inliers) */
+} lk_verify_result;
+
+lk_status lk_verify_batch(const lk_cloud* clouds_i, const lk_cloud* clouds_j, const double* Ti, const double* Tj,
+                          const double* T, int64_t n_pairs, const lk_verify_params* params, lk_verify_result* out);
+
 /* ---- feature pre-match (registration.cpp:248 -> grid.cpp:176-213) ---------
  * argmin_j ||F(p_i) - F(q_j)||^2 in FP64, ties -> lowest j. */
 lk_status lk_feature_nn_cache(const float* src_features, int64_t ns, const float* tgt_features, int64_t nt,

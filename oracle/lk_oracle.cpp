@@ -1685,4 +1685,24 @@ int or_icp_point_to_plane(const double* sxyz, int64_t ns, const double* txyz, co
     });
 }
 
+// propose_loops' overlap of one pair (fragments.cpp:67-100): the later cloud
+// posed by T_later, hits within r of the earlier cloud posed by T_earlier
+// (SearchGrid at cell r, center 0).
+int or_overlap_hits(const double* later, int64_t nl, const double* Rl9, const double* tl3, const double* earlier,
+                    int64_t ne, const double* Re9, const double* te3, double r, int64_t* hits) {
+    return guarded([&] {
+        const Rigid Tl = load_rigid(Rl9, tl3), Te = load_rigid(Re9, te3);
+        std::vector<V3> pe;
+        pe.reserve(static_cast<size_t>(ne));
+        for (int64_t i = 0; i < ne; ++i) pe.push_back(apply(Te, load3(earlier, i)));
+        SearchGrid grid = build_grid(pe, r, V3{});
+        int64_t h = 0;
+        for (int64_t i = 0; i < nl; ++i) {
+            Nn nn;
+            if (nn_within(grid, apply(Tl, load3(later, i)), r, &nn)) h += 1;
+        }
+        *hits = h;
+    });
+}
+
 }  // extern "C"

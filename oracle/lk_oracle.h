@@ -171,6 +171,10 @@ int or_icp_point_to_plane(const double* sxyz, int64_t ns, const double* txyz, co
                           const double* R0, const double* t0, double max_dist, int32_t max_iter, double eps,
                           double* R9, double* t3, or_icp_result* res, double* history);
 
+/* propose_loops' overlap hit count of one pair (fragments.cpp:67-100) */
+int or_overlap_hits(const double* later, int64_t nl, const double* Rl9, const double* tl3, const double* earlier,
+                    int64_t ne, const double* Re9, const double* te3, double r, int64_t* hits);
+
 #ifdef __cplusplus
 }
 #endif

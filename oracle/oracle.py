@@ -413,3 +413,16 @@ def icp_point_to_plane(src_xyz, tgt_xyz, tgt_n, R0, t0, max_dist, max_iter=30, e
                                    C.c_double(max_dist), C.c_int32(max_iter), C.c_double(eps), _p(R), _p(tt),
                                    C.byref(res), _p(hist)))
     return R.reshape(3, 3), tt, res, hist
+
+
+def overlap_hits(later, T_later_R, T_later_t, earlier, T_earlier_R, T_earlier_t, r):
+    """propose_loops' overlap hit count of one pair (fragments.cpp:67-100)."""
+    L = lib()
+    L.or_overlap_hits.restype = C.c_int
+    a, b = _d(later), _d(earlier)
+    Rl, tl = _d(np.asarray(T_later_R).reshape(9)), _d(np.asarray(T_later_t).reshape(3))
+    Re, te = _d(np.asarray(T_earlier_R).reshape(9)), _d(np.asarray(T_earlier_t).reshape(3))
+    h = C.c_int64()
+    _check(L.or_overlap_hits(_p(a), C.c_int64(len(a)), _p(Rl), _p(tl), _p(b), C.c_int64(len(b)), _p(Re), _p(te),
+                             C.c_double(r), C.byref(h)))
+    return h.value

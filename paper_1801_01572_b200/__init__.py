@@ -14,6 +14,7 @@ from .registration import (CandidateScores, DeviceGrid, EdgeInfo, EvalGrid, Hypo
                            evaluate_hypothesis, feature_nn_cache, icp_point_to_plane, merge_records,
                            prepare_registration,
                            records_from_bytes, register_global, registration_context, run_hypotheses,
-                           run_hypotheses_range, score_candidates, voxel_downsample)
+                           run_hypotheses_range, score_candidates, verify_batch, voxel_downsample)
+from .registration import VerifyParams, VerifyResult
 
 __all__ = [name for name in dir() if not name.startswith("_")]

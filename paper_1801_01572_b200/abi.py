@@ -90,6 +90,30 @@ class lk_icp_result(C.Structure):
     ]
 
 
+class lk_verify_params(C.Structure):
+    _fields_ = [
+        ("epsilon", C.c_double),
+        ("overlap_radius", C.c_double),
+        ("d_max", C.c_double),
+        ("grid_cell", C.c_double),
+        ("normal_angle_max", C.c_double),
+        ("device", C.c_int32),
+        ("reserved", C.c_int32),
+    ]
+
+
+class lk_verify_result(C.Structure):
+    _fields_ = [
+        ("info", C.c_double * 36),
+        ("pair_count", C.c_int64),
+        ("overlap_hits", C.c_int64),
+        ("overlap", C.c_double),
+        ("inliers", C.c_int64),
+        ("inlier_ratio", C.c_double),
+        ("fitness", C.c_double),
+    ]
+
+
 class lk_hyp_stats(C.Structure):
     _fields_ = [
         ("sampled", C.c_int64),
@@ -164,6 +188,8 @@ SIGNATURES = {
     "lk_edge_info_batched": (C.c_int, [C.POINTER(lk_cloud), C.POINTER(lk_cloud), dptr, dptr, C.c_int64, C.c_double,
                                        C.c_int32, dptr, i64ptr]),
     "lk_feature_nn_cache": (C.c_int, [fptr, C.c_int64, fptr, C.c_int64, C.c_int32, i32ptr]),
+    "lk_verify_batch": (C.c_int, [C.POINTER(lk_cloud), C.POINTER(lk_cloud), dptr, dptr, dptr, C.c_int64,
+                                  C.POINTER(lk_verify_params), C.POINTER(lk_verify_result)]),
     "lk_icp_point_to_plane": (C.c_int, [C.POINTER(lk_cloud), C.POINTER(lk_cloud), dptr, C.POINTER(lk_icp_params),
                                         C.POINTER(lk_icp_result), dptr]),
     "lk_voxel_downsample": (C.c_int, [C.POINTER(lk_cloud), C.c_double, dptr, dptr, i64ptr]),

@@ -891,68 +891,122 @@ lk_status lk_score_candidates(lk_grid* grid, const lk_cloud* src, const double* 
     });
 }
 
+// Packs the pairs' clouds into contiguous host arrays with point offsets.
+struct PackedPairs {
+    std::vector<double> qpos, qnrm, ppos, pnrm;
+    std::vector<int64_t> offq, offp;
+};
+
+PackedPairs pack_pairs(const lk_cloud* ci, const lk_cloud* cj, int64_t K, bool normals) {
+    PackedPairs pk;
+    pk.offq.assign(static_cast<size_t>(K) + 1, 0);
+    pk.offp.assign(static_cast<size_t>(K) + 1, 0);
+    for (int64_t k = 0; k < K; ++k) {
+        check_cloud_ptr(&ci[k], "cloud_i");
+        check_cloud_ptr(&cj[k], "cloud_j");
+        if (ci[k].n == 0 || cj[k].n == 0) throw lk::Status(LK_EMPTY_CLOUD, "edge_info: empty cloud");
+        if (normals && (!ci[k].nxyz || !cj[k].nxyz))
+            throw lk::Status(LK_MISSING_NORMALS, "evaluate_hypothesis: both clouds need normals");
+        pk.offq[k + 1] = pk.offq[k] + ci[k].n;
+        pk.offp[k + 1] = pk.offp[k] + cj[k].n;
+    }
+    if (pk.offq[K] > INT32_MAX / 2 || pk.offp[K] > INT32_MAX / 2)
+        throw lk::Status(LK_INVALID_ARGUMENT, "verify: batch too large");
+    pk.qpos.resize(3 * static_cast<size_t>(pk.offq[K]));
+    pk.ppos.resize(3 * static_cast<size_t>(pk.offp[K]));
+    if (normals) {
+        pk.qnrm.resize(pk.qpos.size());
+        pk.pnrm.resize(pk.ppos.size());
+    }
+    for (int64_t k = 0; k < K; ++k) {
+        std::memcpy(pk.qpos.data() + 3 * pk.offq[k], ci[k].xyz, 3 * ci[k].n * sizeof(double));
+        std::memcpy(pk.ppos.data() + 3 * pk.offp[k], cj[k].xyz, 3 * cj[k].n * sizeof(double));
+        if (normals) {
+            std::memcpy(pk.qnrm.data() + 3 * pk.offq[k], ci[k].nxyz, 3 * ci[k].n * sizeof(double));
+            std::memcpy(pk.pnrm.data() + 3 * pk.offp[k], cj[k].nxyz, 3 * cj[k].n * sizeof(double));
+        }
+    }
+    return pk;
+}
+
 lk_status lk_edge_info_batched(const lk_cloud* clouds_i, const lk_cloud* clouds_j, const double* Ti, const double* Tj,
                                int64_t n_pairs, double epsilon, int32_t device, double* info, int64_t* pair_count) {
     return guarded([&]() -> lk_status {
         if (n_pairs < 0 || (n_pairs > 0 && (!clouds_i || !clouds_j || !Ti || !Tj || !info || !pair_count)))
             return fail(LK_INVALID_ARGUMENT, "null argument");
         if (!(epsilon > 0.0)) return fail(LK_INVALID_ARGUMENT, "build_grid: cell_length must be positive");
-        int dev = select_device(device);
-        int sms = sm_count_of(dev);
-        cudaStream_t s;
-        CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-        const int nb = sms * 2;
-        double *d_part = nullptr, *d_info = nullptr;
-        unsigned long long* d_count = nullptr;
-        lk_status result = LK_OK;
-        try {
-            CK(cudaMalloc(&d_part, nb * 9 * sizeof(double)));
-            CK(cudaMalloc(&d_info, 36 * sizeof(double)));
-            CK(cudaMalloc(&d_count, sizeof(unsigned long long)));
-            for (int64_t k = 0; k < n_pairs; ++k) {
-                const lk_cloud& ci = clouds_i[k];
-                const lk_cloud& cj = clouds_j[k];
-                check_cloud_ptr(&ci, "cloud_i");
-                check_cloud_ptr(&cj, "cloud_j");
-                if (ci.n == 0 || cj.n == 0) {
-                    result = fail(LK_EMPTY_CLOUD, "edge_info: empty cloud");
-                    break;
-                }
-                double* d_ci = dev_upload(ci.xyz, 3 * ci.n, s);
-                double* d_cj = dev_upload(cj.xyz, 3 * cj.n, s);
-                double* d_posed = nullptr;
-                CK(cudaMalloc(&d_posed, 3 * cj.n * sizeof(double)));
-                CK(lkk::transform_points(d_cj, cj.n, Tj + 12 * k, d_posed, s));
-                lkk::GridStorage g;
-                cudaError_t e = lkk::build_grid(g, 1, d_posed, nullptr, cj.n, epsilon, epsilon, s);
-                if (e == cudaSuccess)
-                    e = lkk::edge_info(d_ci, ci.n, Ti + 12 * k, g.view, epsilon, d_part, nb, d_info, d_count, s);
-                unsigned long long cnt = 0;
-                if (e == cudaSuccess)
-                    e = cudaMemcpyAsync(info + 36 * k, d_info, 36 * sizeof(double), cudaMemcpyDeviceToHost, s);
-                if (e == cudaSuccess) e = cudaMemcpyAsync(&cnt, d_count, sizeof(cnt), cudaMemcpyDeviceToHost, s);
-                if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-                g.release();
-                cudaFree(d_ci);
-                cudaFree(d_cj);
-                cudaFree(d_posed);
-                CK(e);
-                pair_count[k] = static_cast<int64_t>(cnt);
-                if (cnt == 0)
-                    for (int q = 0; q < 36; ++q) info[36 * k + q] = 0.0;
-            }
-        } catch (...) {
-            cudaFree(d_part);
-            cudaFree(d_info);
-            cudaFree(d_count);
-            cudaStreamDestroy(s);
-            throw;
+        if (n_pairs == 0) return LK_OK;
+        if (n_pairs > INT32_MAX) return fail(LK_INVALID_ARGUMENT, "edge_info: batch too large");
+        PackedPairs pk = pack_pairs(clouds_i, clouds_j, n_pairs, false);
+        const int dev = select_device(device);
+        cudaStream_t s = acquire_stream(dev);
+        lkk::VerifyInput in{};
+        in.n_pairs = static_cast<int32_t>(n_pairs);
+        in.qpos = pk.qpos.data();
+        in.ppos = pk.ppos.data();
+        in.offq = pk.offq.data();
+        in.offp = pk.offp.data();
+        in.Ti = Ti;
+        in.Tj = Tj;
+        in.epsilon = epsilon;
+        in.full = 0;
+        std::vector<lkk::VerifyOutput> o(static_cast<size_t>(n_pairs));
+        cudaError_t e = lkk::verify_batch(in, o.data(), s);
+        release_stream(dev, s);
+        CK(e);
+        for (int64_t k = 0; k < n_pairs; ++k) {
+            for (int q = 0; q < 36; ++q) info[36 * k + q] = o[k].info[q];
+            pair_count[k] = o[k].pair_count;
         }
-        cudaFree(d_part);
-        cudaFree(d_info);
-        cudaFree(d_count);
-        cudaStreamDestroy(s);
-        return result;
+        return LK_OK;
+    });
+}
+
+lk_status lk_verify_batch(const lk_cloud* clouds_i, const lk_cloud* clouds_j, const double* Ti, const double* Tj,
+                          const double* T, int64_t n_pairs, const lk_verify_params* params, lk_verify_result* out) {
+    return guarded([&]() -> lk_status {
+        if (!params || n_pairs < 0 || (n_pairs > 0 && (!clouds_i || !clouds_j || !Ti || !Tj || !T || !out)))
+            return fail(LK_INVALID_ARGUMENT, "null argument");
+        if (!(params->epsilon > 0.0) || !(params->overlap_radius > 0.0) || !(params->d_max > 0.0))
+            return fail(LK_INVALID_ARGUMENT, "build_grid: cell_length must be positive");
+        if (n_pairs == 0) return LK_OK;
+        if (n_pairs > INT32_MAX) return fail(LK_INVALID_ARGUMENT, "verify: batch too large");
+        PackedPairs pk = pack_pairs(clouds_i, clouds_j, n_pairs, true);
+        const int dev = select_device(params->device);
+        cudaStream_t s = acquire_stream(dev);
+        lkk::VerifyInput in{};
+        in.n_pairs = static_cast<int32_t>(n_pairs);
+        in.qpos = pk.qpos.data();
+        in.qnrm = pk.qnrm.data();
+        in.ppos = pk.ppos.data();
+        in.pnrm = pk.pnrm.data();
+        in.offq = pk.offq.data();
+        in.offp = pk.offp.data();
+        in.Ti = Ti;
+        in.Tj = Tj;
+        in.T = T;
+        in.epsilon = params->epsilon;
+        in.overlap_radius = params->overlap_radius;
+        in.d_max = params->d_max;
+        in.grid_cell = params->grid_cell > 0.0 ? params->grid_cell : params->d_max;
+        in.cos_max = std::cos(params->normal_angle_max);  // registration.cpp:61
+        in.full = 1;
+        std::vector<lkk::VerifyOutput> o(static_cast<size_t>(n_pairs));
+        cudaError_t e = lkk::verify_batch(in, o.data(), s);
+        release_stream(dev, s);
+        CK(e);
+        for (int64_t k = 0; k < n_pairs; ++k) {
+            lk_verify_result& r = out[k];
+            for (int q = 0; q < 36; ++q) r.info[q] = o[k].info[q];
+            r.pair_count = o[k].pair_count;
+            r.overlap_hits = o[k].overlap_hits;
+            const double np = static_cast<double>(clouds_j[k].n);
+            r.overlap = static_cast<double>(o[k].overlap_hits) / np;
+            r.inliers = o[k].inliers;
+            r.inlier_ratio = static_cast<double>(o[k].inliers) / np;
+            r.fitness = o[k].inliers > 0 ? o[k].sq_sum / static_cast<double>(o[k].inliers) : 0.0;
+        }
+        return LK_OK;
     });
 }
 

@@ -101,9 +101,17 @@ struct RingGrid {
     const int32_t* start;     // ncells + 1
     const float4* pts;        // CSR order: ring-cell coordinates, original index in w
     const double4* pos4;      // original order FP64 (x, y, z, 0)
-    double eox, eoy, eoz, ecell;  // the reference EvalGrid at cell = d_max
+    // the reference grid whose window the answer must come from: the
+    // EvalGrid (origin bbox_lo - d_max, cell d_max, +-1 cells, queries outside
+    // [0, en) miss; registration.cpp:82-97,165-199) or a SearchGrid (center 0,
+    // cell length, +-ceil(d_max / cell) cells, unbounded; grid.cpp:26-30,78-109)
+    double eox, eoy, eoz, ecell;
     int enx, eny, enz;
+    int ewin;      // window half-width in reference cells
+    int ebounded;  // 1: EvalGrid range check on the query cell
 };
+RingGrid ring_frame(const double* lo, const double* hi, double d_max, double search_cell, int64_t max_cells,
+                    bool fast);
 struct RingStorage {
     RingGrid view{};
     int32_t* start = nullptr;
@@ -114,6 +122,20 @@ struct RingStorage {
 };
 cudaError_t build_ring_grid(RingStorage& rs, const double* d_pos, int64_t n, double d_max, cudaStream_t stream,
                             bool fast = true);
+// K ring grids in one pass over K concatenated clouds (h_offsets: K + 1 point
+// offsets into d_pos). Grid k answers radius h_dmax[k] in the window of an
+// EvalGrid (h_cell[k] <= 0) or of a SearchGrid with cell length h_cell[k].
+// d_views (K RingGrid on the device) and the storage stay valid until release.
+struct RingBatch {
+    int32_t* start = nullptr;
+    float4* pts = nullptr;
+    double4* pos4 = nullptr;
+    RingGrid* d_views = nullptr;
+    cudaStream_t stream = nullptr;
+    void release();
+};
+cudaError_t build_ring_grids(RingBatch& rb, const double* d_pos, const int64_t* h_offsets, int32_t K,
+                             const double* h_dmax, const double* h_cell, cudaStream_t stream);
 
 // Builds a grid of the given kind from device arrays pos/nrm (nrm may be null).
 // Returns cudaSuccess or the first CUDA error; throws nothing.
@@ -239,6 +261,24 @@ cudaError_t icp_point_to_plane(const double* d_src, int64_t n, const RingStorage
                                double max_dist, int32_t max_iter, double eps, const double* R0, const double* t0,
                                double* R9, double* t3, IcpOutcome* out, double* d_history, cudaStream_t stream,
                                int sm_count);
+
+// Batched loop verification (lk_verify.cu). Host arrays: clouds concatenated
+// with K + 1 point offsets; T_i, T_j, T as 12 doubles per pair. `full` = 0
+// computes edge_info only (normals and T unused).
+struct VerifyInput {
+    int32_t n_pairs;
+    const double *qpos, *qnrm, *ppos, *pnrm;  // Q = cloud_i (earlier), P = cloud_j (later)
+    const int64_t *offq, *offp;
+    const double *Ti, *Tj, *T;
+    double epsilon, overlap_radius, d_max, grid_cell, cos_max;
+    int32_t full;
+};
+struct VerifyOutput {
+    double info[36];
+    int64_t pair_count, overlap_hits, inliers;
+    double sq_sum;  // evaluate_hypothesis's sequential sum of distance^2
+};
+cudaError_t verify_batch(const VerifyInput& in, VerifyOutput* out, cudaStream_t stream);
 
 // Scores an explicit candidate list (Rt on device, C x 12) and reduces the best.
 cudaError_t score_candidates(const SourceView& src, const GridView& grid, const ScoreParams& sp, const double* d_rt,

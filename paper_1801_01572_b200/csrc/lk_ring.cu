@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <vector>
 
 #include "lk_device_math.cuh"
 #include "lk_kernels.cuh"
@@ -93,7 +94,133 @@ __global__ void k_ring_scatter(const double* __restrict__ p, int64_t n, RingGrid
                          static_cast<float>((p[3 * i + 2] - rg.oz) / rg.cell), __int_as_float(static_cast<int>(i)));
 }
 
+
+// ---- batched build (K clouds concatenated) ---------------------------------
+__device__ __forceinline__ int cloud_of(const int64_t* __restrict__ off, int K, int64_t i) {
+    int lo = 0, hi = K;  // off[lo] <= i < off[hi]
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(off + mid) <= i) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// CTA per cloud: keys[6k..6k+2] = min, [6k+3..6k+5] = max
+__global__ void k_ring_bbox_batched(const double* __restrict__ p, const int64_t* __restrict__ off,
+                                    unsigned long long* __restrict__ keys) {
+    const int k = blockIdx.x;
+    unsigned long long lo[3] = {~0ull, ~0ull, ~0ull}, hi[3] = {0ull, 0ull, 0ull};
+    for (int64_t i = off[k] + threadIdx.x; i < off[k + 1]; i += blockDim.x)
+        for (int a = 0; a < 3; ++a) {
+            const unsigned long long q = order_key(p[3 * i + a]);
+            lo[a] = q < lo[a] ? q : lo[a];
+            hi[a] = q > hi[a] ? q : hi[a];
+        }
+    for (int a = 0; a < 3; ++a) {
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long x = __shfl_xor_sync(0xffffffffu, lo[a], o);
+            const unsigned long long y = __shfl_xor_sync(0xffffffffu, hi[a], o);
+            lo[a] = x < lo[a] ? x : lo[a];
+            hi[a] = y > hi[a] ? y : hi[a];
+        }
+        if ((threadIdx.x & 31) == 0) {
+            atomicMin(keys + 6 * k + a, lo[a]);
+            atomicMax(keys + 6 * k + 3 + a, hi[a]);
+        }
+    }
+}
+
+__global__ void k_ring_count_batched(const double* __restrict__ p, int64_t n, const int64_t* __restrict__ off,
+                                     int K, const RingGrid* __restrict__ views, const int64_t* __restrict__ cell_off,
+                                     int64_t* __restrict__ cell_of, int32_t* __restrict__ counts) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const int k = cloud_of(off, K, i);
+    const RingGrid& rg = views[k];
+    const int cx = ring_cell_axis(p[3 * i], rg.ox, rg.cell, rg.nx);
+    const int cy = ring_cell_axis(p[3 * i + 1], rg.oy, rg.cell, rg.ny);
+    const int cz = ring_cell_axis(p[3 * i + 2], rg.oz, rg.cell, rg.nz);
+    const int64_t c = cell_off[k] + (static_cast<int64_t>(cx) * rg.ny + cy) * rg.nz + cz;
+    cell_of[i] = c;
+    atomicAdd(counts + c, 1);
+}
+
+__global__ void k_ring_scatter_batched(const double* __restrict__ p, int64_t n, const int64_t* __restrict__ off,
+                                       int K, const RingGrid* __restrict__ views, const int32_t* __restrict__ start,
+                                       const int64_t* __restrict__ cell_of, int32_t* __restrict__ cursor,
+                                       float4* __restrict__ pts) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const int k = cloud_of(off, K, i);
+    const RingGrid& rg = views[k];
+    const int64_t c = cell_of[i];
+    const int32_t s = start[c] + atomicAdd(cursor + c, 1);
+    pts[s] = make_float4(static_cast<float>((p[3 * i] - rg.ox) / rg.cell),
+                         static_cast<float>((p[3 * i + 1] - rg.oy) / rg.cell),
+                         static_cast<float>((p[3 * i + 2] - rg.oz) / rg.cell),
+                         __int_as_float(static_cast<int>(i - off[k])));
+}
+
 }  // namespace
+
+// Frame of one ring grid over a cloud with bounding box [lo, hi] answering
+// radius d_max: ring cells of d_max / 6 (coarsened under max_cells), guard
+// bands, and the reference window -- the EvalGrid at cell d_max when
+// search_cell <= 0, else a SearchGrid of that cell length.
+RingGrid ring_frame(const double* lo, const double* hi, double d_max, double search_cell, int64_t max_cells,
+                    bool fast) {
+    RingGrid v{};
+    if (search_cell <= 0.0) {
+        // the reference's EvalGrid over the same cloud (registration.cpp:82-97)
+        v.ecell = d_max;
+        v.eox = lo[0] - d_max;
+        v.eoy = lo[1] - d_max;
+        v.eoz = lo[2] - d_max;
+        v.enx = static_cast<int>(std::floor(((hi[0] - v.eox) + d_max) / d_max)) + 2;
+        v.eny = static_cast<int>(std::floor(((hi[1] - v.eoy) + d_max) / d_max)) + 2;
+        v.enz = static_cast<int>(std::floor(((hi[2] - v.eoz) + d_max) / d_max)) + 2;
+        v.ewin = 1;
+        v.ebounded = 1;
+    } else {
+        // SearchGrid (grid.cpp:26-30, 101-109): center 0, block radius ceil(d / cell)
+        v.ecell = search_cell;
+        v.eox = v.eoy = v.eoz = 0.0;
+        v.ewin = static_cast<int>(std::ceil(d_max / search_cell));
+        v.ebounded = 0;
+    }
+    double cell = d_max / 6.0;
+    int dims[3] = {1, 1, 1};
+    int64_t nc = 1;
+    for (int guard = 0; guard < 200; ++guard) {
+        for (int a = 0; a < 3; ++a) dims[a] = static_cast<int>(std::floor((hi[a] - lo[a]) / cell)) + 1;
+        nc = static_cast<int64_t>(dims[0]) * dims[1] * dims[2];
+        if (nc <= max_cells) break;
+        cell *= 1.25;
+    }
+    v.ox = lo[0];
+    v.oy = lo[1];
+    v.oz = lo[2];
+    v.cell = cell;
+    v.nx = dims[0];
+    v.ny = dims[1];
+    v.nz = dims[2];
+    v.ncells = nc;
+    v.rmax = static_cast<int>(std::ceil(d_max / cell)) + 2;
+    // FP32 conversion error of a coordinate (cells), both sides, plus slack
+    const double nmax = std::max(v.nx, std::max(v.ny, v.nz)) + v.rmax + 2.0;
+    v.delta = static_cast<float>(2.0 * nmax * 5.9604644775390625e-8 + 1e-6);
+    const double thr = (d_max / cell) * (d_max / cell);
+    v.thr = static_cast<float>(thr);
+    // |d2_fp32 - d2| <= 2 sqrt3 |d| delta + 3 delta^2 + 4 u d2 over |d| <= rmax cells; 4x margin
+    const double R = v.rmax + 1.0;
+    v.band = static_cast<float>(4.0 * (2.0 * 1.7320508 * R * v.delta + 3.0 * v.delta * v.delta +
+                                       4.0 * 5.9604644775390625e-8 * R * R) + 1e-6);
+    // FP64-only mode: an infinite band scans every shell within d_max and
+    // decides every entry in FP64 (the tests' exhaustive reference path)
+    if (!fast) v.band = 1e30f;
+    return v;
+}
 
 void RingStorage::release() {
     pool_free(start, stream);
@@ -128,46 +255,8 @@ cudaError_t build_ring_grid(RingStorage& rs, const double* d_pos, int64_t n, dou
         lo[a] = from_key(hk[a]);
         hi[a] = from_key(hk[3 + a]);
     }
-    RingGrid v{};
-    // the reference's EvalGrid over the same cloud (registration.cpp:82-97)
-    v.ecell = d_max;
-    v.eox = lo[0] - d_max;
-    v.eoy = lo[1] - d_max;
-    v.eoz = lo[2] - d_max;
-    v.enx = static_cast<int>(std::floor(((hi[0] - v.eox) + d_max) / d_max)) + 2;
-    v.eny = static_cast<int>(std::floor(((hi[1] - v.eoy) + d_max) / d_max)) + 2;
-    v.enz = static_cast<int>(std::floor(((hi[2] - v.eoz) + d_max) / d_max)) + 2;
-    // ring cells: d_max / 6, coarsened until the dense CSR stays under 2^28 cells
-    double cell = d_max / 6.0;
-    int64_t nc = 0;
-    int dims[3];
-    for (int guard = 0; guard < 64; ++guard) {
-        for (int a = 0; a < 3; ++a) dims[a] = static_cast<int>(std::floor((hi[a] - lo[a]) / cell)) + 1;
-        nc = static_cast<int64_t>(dims[0]) * dims[1] * dims[2];
-        if (nc <= (int64_t(1) << 28)) break;
-        cell *= 1.25;
-    }
-    v.ox = lo[0];
-    v.oy = lo[1];
-    v.oz = lo[2];
-    v.cell = cell;
-    v.nx = dims[0];
-    v.ny = dims[1];
-    v.nz = dims[2];
-    v.ncells = nc;
-    v.rmax = static_cast<int>(std::ceil(d_max / cell)) + 2;
-    // FP32 conversion error of a coordinate (cells), both sides, plus slack
-    const double nmax = std::max(v.nx, std::max(v.ny, v.nz)) + v.rmax + 2.0;
-    v.delta = static_cast<float>(2.0 * nmax * 5.9604644775390625e-8 + 1e-6);
-    const double thr = (d_max / cell) * (d_max / cell);
-    v.thr = static_cast<float>(thr);
-    // |d2_fp32 - d2| <= 2 sqrt3 |d| delta + 3 delta^2 + 4 u d2 over |d| <= rmax cells; 4x margin
-    const double R = v.rmax + 1.0;
-    v.band = static_cast<float>(4.0 * (2.0 * 1.7320508 * R * v.delta + 3.0 * v.delta * v.delta +
-                                       4.0 * 5.9604644775390625e-8 * R * R) + 1e-6);
-    // FP64-only mode: an infinite band scans every shell within d_max and
-    // decides every entry in FP64 (the tests' exhaustive reference path)
-    if (!fast) v.band = 1e30f;
+    RingGrid v = ring_frame(lo, hi, d_max, -1.0, int64_t(1) << 28, fast);
+    int64_t nc = v.ncells;
     int32_t *cell_of = nullptr, *counts = nullptr;
     RG_TRY(cudaMallocAsync(&cell_of, n * sizeof(int32_t), stream));
     RG_TRY(cudaMallocAsync(&counts, nc * sizeof(int32_t), stream));
@@ -187,6 +276,94 @@ cudaError_t build_ring_grid(RingStorage& rs, const double* d_pos, int64_t n, dou
     v.pos4 = rs.pos4;
     v.npoints = n;
     rs.view = v;
+    return cudaGetLastError();
+#undef RG_TRY
+}
+
+void RingBatch::release() {
+    pool_free(start, stream);
+    pool_free(pts, stream);
+    pool_free(pos4, stream);
+    pool_free(d_views, stream);
+    start = nullptr;
+    pts = nullptr;
+    pos4 = nullptr;
+    d_views = nullptr;
+}
+
+cudaError_t build_ring_grids(RingBatch& rb, const double* d_pos, const int64_t* h_offsets, int32_t K,
+                             const double* h_dmax, const double* h_cell, cudaStream_t stream) {
+#define RG_TRY(x)                         \
+    do {                                  \
+        cudaError_t e_ = (x);             \
+        if (e_ != cudaSuccess) return e_; \
+    } while (0)
+    rb.stream = stream;
+    if (K <= 0) return cudaErrorInvalidValue;
+    const int64_t n = h_offsets[K];
+    if (n <= 0 || n > INT32_MAX) return cudaErrorInvalidValue;
+    for (int k = 0; k < K; ++k)
+        if (h_offsets[k + 1] <= h_offsets[k] || !(h_dmax[k] > 0.0)) return cudaErrorInvalidValue;
+    int64_t* d_off = nullptr;
+    unsigned long long* keys = nullptr;
+    RG_TRY(cudaMallocAsync(&d_off, (K + 1) * sizeof(int64_t), stream));
+    RG_TRY(cudaMallocAsync(&keys, 6 * static_cast<size_t>(K) * sizeof(unsigned long long), stream));
+    std::vector<unsigned long long> hk(6 * static_cast<size_t>(K));
+    for (int k = 0; k < K; ++k)
+        for (int a = 0; a < 3; ++a) {
+            hk[6 * k + a] = ~0ull;
+            hk[6 * k + 3 + a] = 0ull;
+        }
+    RG_TRY(cudaMemcpyAsync(d_off, h_offsets, (K + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, stream));
+    RG_TRY(cudaMemcpyAsync(keys, hk.data(), hk.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice, stream));
+    k_ring_bbox_batched<<<K, 256, 0, stream>>>(d_pos, d_off, keys);
+    RG_TRY(cudaMemcpyAsync(hk.data(), keys, hk.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream));
+    RG_TRY(cudaStreamSynchronize(stream));
+    cudaFreeAsync(keys, stream);
+    std::vector<RingGrid> views(static_cast<size_t>(K));
+    std::vector<int64_t> cell_off(static_cast<size_t>(K) + 1, 0);
+    for (int k = 0; k < K; ++k) {
+        double lo[3], hi[3];
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = from_key(hk[6 * k + a]);
+            hi[a] = from_key(hk[6 * k + 3 + a]);
+        }
+        views[k] = ring_frame(lo, hi, h_dmax[k], h_cell ? h_cell[k] : -1.0, int64_t(1) << 24, true);
+        cell_off[k + 1] = cell_off[k] + views[k].ncells;
+    }
+    const int64_t nc = cell_off[K];
+    if (nc > INT32_MAX) return cudaErrorInvalidValue;
+    int64_t *d_cell_off = nullptr, *cell_of = nullptr;
+    int32_t* counts = nullptr;
+    RG_TRY(cudaMallocAsync(&d_cell_off, (K + 1) * sizeof(int64_t), stream));
+    RG_TRY(cudaMallocAsync(&cell_of, n * sizeof(int64_t), stream));
+    RG_TRY(cudaMallocAsync(&counts, nc * sizeof(int32_t), stream));
+    RG_TRY(pool_alloc(&rb.start, (nc + 1) * sizeof(int32_t), stream));
+    RG_TRY(pool_alloc(&rb.pts, n * sizeof(float4), stream));
+    RG_TRY(pool_alloc(&rb.pos4, n * sizeof(double4), stream));
+    RG_TRY(pool_alloc(&rb.d_views, K * sizeof(RingGrid), stream));
+    for (int k = 0; k < K; ++k) {
+        views[k].start = rb.start + cell_off[k];
+        views[k].pts = rb.pts;
+        views[k].pos4 = rb.pos4 + h_offsets[k];
+        views[k].npoints = h_offsets[k + 1] - h_offsets[k];
+    }
+    RG_TRY(cudaMemcpyAsync(d_cell_off, cell_off.data(), (K + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, stream));
+    RG_TRY(cudaMemcpyAsync(rb.d_views, views.data(), K * sizeof(RingGrid), cudaMemcpyHostToDevice, stream));
+    RG_TRY(cudaMemsetAsync(counts, 0, nc * sizeof(int32_t), stream));
+    k_ring_count_batched<<<nblocks(n, 256), 256, 0, stream>>>(d_pos, n, d_off, K, rb.d_views, d_cell_off, cell_of,
+                                                              counts);
+    RG_TRY(exclusive_scan(counts, nc, rb.start, stream));
+    RG_TRY(cudaMemsetAsync(counts, 0, nc * sizeof(int32_t), stream));
+    k_ring_scatter_batched<<<nblocks(n, 256), 256, 0, stream>>>(d_pos, n, d_off, K, rb.d_views, rb.start, cell_of,
+                                                                counts, rb.pts);
+    RG_TRY(make_records(d_pos, nullptr, n, rb.pos4, nullptr, stream));
+    // the host vectors above are read by async copies: finish before returning
+    RG_TRY(cudaStreamSynchronize(stream));
+    cudaFreeAsync(d_off, stream);
+    cudaFreeAsync(d_cell_off, stream);
+    cudaFreeAsync(cell_of, stream);
+    cudaFreeAsync(counts, stream);
     return cudaGetLastError();
 #undef RG_TRY
 }

@@ -50,20 +50,23 @@ __device__ __forceinline__ void ring_shell(const RingGrid& rg, float qx, float q
 
 __device__ __forceinline__ int ecell_axis(double v, double o, double c) { return static_cast<int>(floor((v - o) / c)); }
 
-// exact scan of the reference window (the +-1 EvalGrid cells of y's cell)
-__device__ __noinline__ int32_t ring_window_scan(const RingGrid& rg, lkd::V3 y, double d2_max, int ex, int ey,
+// exact scan of the reference window (the +-ewin reference cells of y's cell)
+static __device__ __noinline__ int32_t ring_window_scan(const RingGrid& rg, lkd::V3 y, double d2_max, int ex, int ey,
                                                  int ez) {
     using namespace lkd;
-    const double lx = rg.eox + (ex - 1) * rg.ecell, hx = rg.eox + (ex + 2) * rg.ecell;
-    const double ly = rg.eoy + (ey - 1) * rg.ecell, hy = rg.eoy + (ey + 2) * rg.ecell;
-    const double lz = rg.eoz + (ez - 1) * rg.ecell, hz = rg.eoz + (ez + 2) * rg.ecell;
-    auto clampc = [](int c, int n) { return c < 0 ? 0 : (c >= n ? n - 1 : c); };
-    const int x0 = clampc(static_cast<int>(floor((lx - rg.ox) / rg.cell)) - 1, rg.nx);
-    const int x1 = clampc(static_cast<int>(floor((hx - rg.ox) / rg.cell)) + 1, rg.nx);
-    const int y0 = clampc(static_cast<int>(floor((ly - rg.oy) / rg.cell)) - 1, rg.ny);
-    const int y1 = clampc(static_cast<int>(floor((hy - rg.oy) / rg.cell)) + 1, rg.ny);
-    const int z0 = clampc(static_cast<int>(floor((lz - rg.oz) / rg.cell)) - 1, rg.nz);
-    const int z1 = clampc(static_cast<int>(floor((hz - rg.oz) / rg.cell)) + 1, rg.nz);
+    const int w = rg.ewin;
+    const double lx = rg.eox + (ex - w) * rg.ecell, hx = rg.eox + (ex + w + 1) * rg.ecell;
+    const double ly = rg.eoy + (ey - w) * rg.ecell, hy = rg.eoy + (ey + w + 1) * rg.ecell;
+    const double lz = rg.eoz + (ez - w) * rg.ecell, hz = rg.eoz + (ez + w + 1) * rg.ecell;
+    auto clampc = [](double v, int n) {
+        return v < 0.0 ? 0 : (v >= static_cast<double>(n) ? n - 1 : static_cast<int>(v));
+    };
+    const int x0 = clampc(floor((lx - rg.ox) / rg.cell) - 1.0, rg.nx);
+    const int x1 = clampc(floor((hx - rg.ox) / rg.cell) + 1.0, rg.nx);
+    const int y0 = clampc(floor((ly - rg.oy) / rg.cell) - 1.0, rg.ny);
+    const int y1 = clampc(floor((hy - rg.oy) / rg.cell) + 1.0, rg.ny);
+    const int z0 = clampc(floor((lz - rg.oz) / rg.cell) - 1.0, rg.nz);
+    const int z1 = clampc(floor((hz - rg.oz) / rg.cell) + 1.0, rg.nz);
     double best_d2 = __longlong_as_double(0x7ff0000000000000ll);
     int32_t best = INT32_MAX;
     for (int x = x0; x <= x1; ++x)
@@ -74,7 +77,7 @@ __device__ __noinline__ int32_t ring_window_scan(const RingGrid& rg, lkd::V3 y, 
                 const V3 q = ld4(rg.pos4, o);
                 const int qx = ecell_axis(q.x, rg.eox, rg.ecell), qy = ecell_axis(q.y, rg.eoy, rg.ecell),
                           qz = ecell_axis(q.z, rg.eoz, rg.ecell);
-                if (qx < ex - 1 || qx > ex + 1 || qy < ey - 1 || qy > ey + 1 || qz < ez - 1 || qz > ez + 1) continue;
+                if (qx < ex - w || qx > ex + w || qy < ey - w || qy > ey + w || qz < ez - w || qz > ez + w) continue;
                 const double d2 = sqnorm(sub(q, y));
                 if (d2 > d2_max) continue;
                 if (d2 < best_d2 || (d2 == best_d2 && o < best)) {
@@ -106,10 +109,12 @@ __device__ __forceinline__ void ring_top3(float d2, int32_t o, float& f1, float&
 // Original index of the reference EvalGrid neighbour of y within d_max, or -1.
 __device__ __forceinline__ int32_t ring_nn(const RingGrid& rg, lkd::V3 y, double d2_max) {
     using namespace lkd;
-    // the reference's cell of y (registration.cpp:167-172): outside the grid => miss
+    // the reference's cell of y; an EvalGrid query outside the grid misses
+    // (registration.cpp:167-172)
     const double fx = floor((y.x - rg.eox) / rg.ecell), fy = floor((y.y - rg.eoy) / rg.ecell),
                  fz = floor((y.z - rg.eoz) / rg.ecell);
-    if (!(fx >= 0.0 && fy >= 0.0 && fz >= 0.0 && fx < rg.enx && fy < rg.eny && fz < rg.enz)) return -1;
+    if (rg.ebounded && !(fx >= 0.0 && fy >= 0.0 && fz >= 0.0 && fx < rg.enx && fy < rg.eny && fz < rg.enz))
+        return -1;
     const float qx = static_cast<float>((y.x - rg.ox) / rg.cell);
     const float qy = static_cast<float>((y.y - rg.oy) / rg.cell);
     const float qz = static_cast<float>((y.z - rg.oz) / rg.cell);
@@ -158,13 +163,14 @@ __device__ __forceinline__ int32_t ring_nn(const RingGrid& rg, lkd::V3 y, double
         if (f2 <= lim) consider(o2);
     }
     if (best == INT32_MAX) return -1;
-    // the reference only sees its +-1 window: a nearest point outside it (a
+    // the reference only sees its window: a nearest point outside it (a
     // division rounded across a face) sends the query to the exact window scan
     const V3 q = ld4(rg.pos4, best);
     const int ex = static_cast<int>(fx), ey = static_cast<int>(fy), ez = static_cast<int>(fz);
     const int wx = ecell_axis(q.x, rg.eox, rg.ecell), wy = ecell_axis(q.y, rg.eoy, rg.ecell),
               wz = ecell_axis(q.z, rg.eoz, rg.ecell);
-    if (wx < ex - 1 || wx > ex + 1 || wy < ey - 1 || wy > ey + 1 || wz < ez - 1 || wz > ez + 1)
+    const int w = rg.ewin;
+    if (wx < ex - w || wx > ex + w || wy < ey - w || wy > ey + w || wz < ez - w || wz > ez + w)
         return ring_window_scan(rg, y, d2_max, ex, ey, ez);
     return best;
 }

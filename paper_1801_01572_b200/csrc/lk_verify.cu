@@ -1,0 +1,266 @@
+// lk_verify.cu -- batched loop verification (north-star item 5, config E).
+//
+// For a batch of loop pairs (cloud_i = the earlier fragment Q with pose T_i,
+// cloud_j = the later fragment P with pose T_j, measurement T mapping P into
+// Q's frame) one pass computes, per pair:
+//   * edge_info(Q, P, T_i, T_j, eps)         proj/src/line_process.cpp:11-33
+//   * the overlap hit count of propose_loops  proj/src/fragments.cpp:61-109
+//     (posed later points within r of the posed earlier cloud)
+//   * evaluate_hypothesis(T, P, Q, SearchGrid(Q, cell), d_max, angle)
+//                                             proj/src/registration.cpp:53-78
+// Every nearest-neighbour question goes to a ring grid (lk_ring.cuh) that
+// answers with the reference SearchGrid's window semantics; all 3K grids are
+// built in one batched pass. The per-pair sums are the reference's own
+// sequential sums in point order (one lane per accumulator), so the
+// information matrix, the fitness and every count are bit-exact.
+#include <cmath>
+#include <cstdint>
+#include <vector>
+
+#include "lk_device_math.cuh"
+#include "lk_kernels.cuh"
+#include "lk_ring.cuh"
+
+namespace lkk {
+
+using namespace lkd;
+
+namespace {
+
+inline unsigned nblocks(int64_t n, int t) { return static_cast<unsigned>((n + t - 1) / t); }
+
+__device__ __forceinline__ int pair_of(const int64_t* __restrict__ off, int K, int64_t i) {
+    int lo = 0, hi = K;
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(off + mid) <= i) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// out[i] = T_k p_i for the cloud k that holds point i (RigidTransform::operator*)
+__global__ void k_pose_batched(const double* __restrict__ in, int64_t n, const int64_t* __restrict__ off, int K,
+                               const double* __restrict__ T12, double* __restrict__ out) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    const int k = pair_of(off, K, i);
+    const double* T = T12 + 12 * k;
+    const V3 y = xform(T, T + 9, ld3(in, i));
+    out[3 * i] = y.x;
+    out[3 * i + 1] = y.y;
+    out[3 * i + 2] = y.z;
+}
+
+// edge_info queries: q in Q_k under T_i[k] against the grid over T_j[k] P_k
+__global__ void k_verify_edge(const double* __restrict__ q, int64_t nq, const int64_t* __restrict__ offq, int K,
+                              const double* __restrict__ Ti12, const RingGrid* __restrict__ grids, double eps2,
+                              uint8_t* __restrict__ hit) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= nq) return;
+    const int k = pair_of(offq, K, i);
+    const double* T = Ti12 + 12 * k;
+    const V3 y = xform(T, T + 9, ld3(q, i));
+    hit[i] = ring_nn(grids[k], y, eps2) >= 0 ? 1 : 0;
+}
+
+// source-side queries: p in P_k posed by T_j[k] against the grid over
+// T_i[k] Q_k (overlap), and T[k] p against the grid over Q_k with the normal
+// gate (evaluate_hypothesis); addend = distance^2 with distance = sqrt(d2)
+__global__ void k_verify_src(const double* __restrict__ p, const double* __restrict__ pn, int64_t np,
+                             const int64_t* __restrict__ offp, int K, const double* __restrict__ qn,
+                             const int64_t* __restrict__ offq, const double* __restrict__ Tj12,
+                             const double* __restrict__ T12, const RingGrid* __restrict__ grids_o,
+                             const RingGrid* __restrict__ grids_h, double r2, double d2_max, double cos_max,
+                             uint8_t* __restrict__ overlap_hit, uint8_t* __restrict__ inlier,
+                             double* __restrict__ addend) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= np) return;
+    const int k = pair_of(offp, K, i);
+    const V3 x = ld3(p, i);
+    const double* Tj = Tj12 + 12 * k;
+    overlap_hit[i] = ring_nn(grids_o[k], xform(Tj, Tj + 9, x), r2) >= 0 ? 1 : 0;
+    const double* T = T12 + 12 * k;
+    const V3 y = xform(T, T + 9, x);
+    const RingGrid& gh = grids_h[k];
+    const int32_t j = ring_nn(gh, y, d2_max);
+    uint8_t ok = 0;
+    double add = 0.0;
+    if (j >= 0) {
+        const V3 ns = ld3(pn, i);
+        const V3 nt = ld3(qn, offq[k] + j);
+        if (!is_zero(ns) && !is_zero(nt) && !(dot(rot(T, ns), nt) < cos_max)) {
+            const double dist = sqrt(sqnorm(sub(ld4(gh.pos4, j), y)));
+            add = dist * dist;
+            ok = 1;
+        }
+    }
+    inlier[i] = ok;
+    addend[i] = add;
+}
+
+// One warp per pair, one accumulator per lane, each summed in point order:
+// lanes 0-5 the a^T a entries (0,0) (0,1) (0,2) (1,1) (1,2) (2,2) with
+// a = -[q]x, lanes 6-8 sum q.x, q.y, q.z, lane 9 the evaluate_hypothesis
+// sq_sum; lane 10 counts the edge hits, 11 the overlap hits, 12 the inliers.
+// out per pair: 10 doubles then 3 int64 (as doubles' bits).
+__global__ void k_verify_sums(const double* __restrict__ q, const int64_t* __restrict__ offq,
+                              const uint8_t* __restrict__ edge_hit, const int64_t* __restrict__ offp,
+                              const uint8_t* __restrict__ overlap_hit, const uint8_t* __restrict__ inlier,
+                              const double* __restrict__ addend, double* __restrict__ out) {
+    const int k = blockIdx.x;
+    const int lane = threadIdx.x;
+    double acc = 0.0;
+    long long cnt = 0;
+    if (lane < 9 || lane == 10) {
+        const int r = lane < 3 ? 0 : (lane < 5 ? 1 : 2);
+        const int c = lane == 0 ? 0 : (lane == 1 || lane == 3) ? 1 : 2;
+        for (int64_t i = offq[k]; i < offq[k + 1]; ++i) {
+            if (!edge_hit[i]) continue;
+            if (lane == 10) {
+                ++cnt;
+                continue;
+            }
+            const V3 v = ld3(q, i);
+            if (lane < 6) {
+                const double a[3][3] = {{-0.0, v.z, -v.y}, {-v.z, -0.0, v.x}, {v.y, -v.x, -0.0}};
+                acc += (a[0][r] * a[0][c] + a[1][r] * a[1][c]) + a[2][r] * a[2][c];
+            } else {
+                acc += lane == 6 ? v.x : (lane == 7 ? v.y : v.z);
+            }
+        }
+    } else if (lane == 9 || lane == 11 || lane == 12) {
+        for (int64_t i = offp[k]; i < offp[k + 1]; ++i) {
+            if (lane == 11) {
+                cnt += overlap_hit[i];
+            } else if (inlier[i]) {
+                if (lane == 9) acc += addend[i];
+                else ++cnt;
+            }
+        }
+    }
+    double* o = out + 16 * k;
+    if (lane < 10) o[lane] = acc;
+    if (lane >= 10 && lane <= 12) reinterpret_cast<long long*>(o)[lane] = cnt;
+}
+
+}  // namespace
+
+cudaError_t verify_batch(const VerifyInput& in, VerifyOutput* out, cudaStream_t stream) {
+    const int K = in.n_pairs;
+    const int64_t nq = in.offq[K], np = in.offp[K];
+    cudaError_t e = cudaSuccess;
+    double *d_qpos = nullptr, *d_qn = nullptr, *d_ppos = nullptr, *d_pn = nullptr, *d_T = nullptr,
+           *d_grid_pts = nullptr, *d_addend = nullptr, *d_out = nullptr;
+    int64_t *d_offq = nullptr, *d_offp = nullptr;
+    uint8_t* d_flags = nullptr;
+    RingBatch rb;
+    auto cleanup = [&] {
+        rb.release();
+        for (void* p : {(void*)d_qpos, (void*)d_qn, (void*)d_ppos, (void*)d_pn, (void*)d_T, (void*)d_grid_pts,
+                        (void*)d_addend, (void*)d_out, (void*)d_offq, (void*)d_offp, (void*)d_flags})
+            pool_free(p, stream);
+    };
+#define VF_TRY(x)               \
+    do {                        \
+        e = (x);                \
+        if (e != cudaSuccess) { \
+            cleanup();          \
+            return e;           \
+        }                       \
+    } while (0)
+    VF_TRY(pool_alloc(&d_qpos, 3 * nq * sizeof(double), stream));
+    VF_TRY(pool_alloc(&d_ppos, 3 * np * sizeof(double), stream));
+    VF_TRY(pool_alloc(&d_offq, (K + 1) * sizeof(int64_t), stream));
+    VF_TRY(pool_alloc(&d_offp, (K + 1) * sizeof(int64_t), stream));
+    VF_TRY(pool_alloc(&d_T, 3 * 12 * K * sizeof(double), stream));
+    VF_TRY(cudaMemcpyAsync(d_qpos, in.qpos, 3 * nq * sizeof(double), cudaMemcpyHostToDevice, stream));
+    VF_TRY(cudaMemcpyAsync(d_ppos, in.ppos, 3 * np * sizeof(double), cudaMemcpyHostToDevice, stream));
+    VF_TRY(cudaMemcpyAsync(d_offq, in.offq, (K + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, stream));
+    VF_TRY(cudaMemcpyAsync(d_offp, in.offp, (K + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, stream));
+    const double* d_Ti = d_T;
+    const double* d_Tj = d_T + 12 * K;
+    const double* d_Tr = d_T + 24 * K;
+    VF_TRY(cudaMemcpyAsync(d_T, in.Ti, 12 * K * sizeof(double), cudaMemcpyHostToDevice, stream));
+    VF_TRY(cudaMemcpyAsync(d_T + 12 * K, in.Tj, 12 * K * sizeof(double), cudaMemcpyHostToDevice, stream));
+    if (in.full) {
+        VF_TRY(pool_alloc(&d_qn, 3 * nq * sizeof(double), stream));
+        VF_TRY(pool_alloc(&d_pn, 3 * np * sizeof(double), stream));
+        VF_TRY(cudaMemcpyAsync(d_qn, in.qnrm, 3 * nq * sizeof(double), cudaMemcpyHostToDevice, stream));
+        VF_TRY(cudaMemcpyAsync(d_pn, in.pnrm, 3 * np * sizeof(double), cudaMemcpyHostToDevice, stream));
+        VF_TRY(cudaMemcpyAsync(d_T + 24 * K, in.T, 12 * K * sizeof(double), cudaMemcpyHostToDevice, stream));
+    }
+    // grid clouds: [T_j P_k]_k for edge_info, then (full) [T_i Q_k]_k, [Q_k]_k
+    const int G = in.full ? 3 * K : K;
+    const int64_t ng = np + (in.full ? 2 * nq : 0);
+    VF_TRY(pool_alloc(&d_grid_pts, 3 * ng * sizeof(double), stream));
+    k_pose_batched<<<nblocks(np, 256), 256, 0, stream>>>(d_ppos, np, d_offp, K, d_Tj, d_grid_pts);
+    std::vector<int64_t> goff(static_cast<size_t>(G) + 1, 0);
+    std::vector<double> gd(static_cast<size_t>(G)), gc(static_cast<size_t>(G));
+    for (int k = 0; k < K; ++k) {
+        goff[k + 1] = in.offp[k + 1];
+        gd[k] = in.epsilon;
+        gc[k] = in.epsilon;  // build_grid(posed_j, epsilon): cell = epsilon
+    }
+    if (in.full) {
+        k_pose_batched<<<nblocks(nq, 256), 256, 0, stream>>>(d_qpos, nq, d_offq, K, d_Ti, d_grid_pts + 3 * np);
+        VF_TRY(cudaMemcpyAsync(d_grid_pts + 3 * (np + nq), d_qpos, 3 * nq * sizeof(double), cudaMemcpyDeviceToDevice,
+                               stream));
+        for (int k = 0; k < K; ++k) {
+            goff[K + k + 1] = np + in.offq[k + 1];
+            gd[K + k] = in.overlap_radius;
+            gc[K + k] = in.overlap_radius;  // build_grid(posed[j], overlap_radius)
+            goff[2 * K + k + 1] = np + nq + in.offq[k + 1];
+            gd[2 * K + k] = in.d_max;
+            gc[2 * K + k] = in.grid_cell;
+        }
+    }
+    VF_TRY(build_ring_grids(rb, d_grid_pts, goff.data(), G, gd.data(), gc.data(), stream));
+    VF_TRY(pool_alloc(&d_flags, (nq + 2 * np + 3) * sizeof(uint8_t), stream));
+    uint8_t* edge_hit = d_flags;
+    uint8_t* overlap_hit = d_flags + nq;
+    uint8_t* inl = d_flags + nq + np;
+    VF_TRY(pool_alloc(&d_addend, (np > 0 ? np : 1) * sizeof(double), stream));
+    VF_TRY(pool_alloc(&d_out, 16 * K * sizeof(double), stream));
+    VF_TRY(cudaMemsetAsync(d_flags, 0, nq + 2 * np + 3, stream));
+    k_verify_edge<<<nblocks(nq, 128), 128, 0, stream>>>(d_qpos, nq, d_offq, K, d_Ti, rb.d_views,
+                                                        in.epsilon * in.epsilon, edge_hit);
+    if (in.full)
+        k_verify_src<<<nblocks(np, 128), 128, 0, stream>>>(
+            d_ppos, d_pn, np, d_offp, K, d_qn, d_offq, d_Tj, d_Tr, rb.d_views + K, rb.d_views + 2 * K,
+            in.overlap_radius * in.overlap_radius, in.d_max * in.d_max, in.cos_max, overlap_hit, inl, d_addend);
+    k_verify_sums<<<K, 32, 0, stream>>>(d_qpos, d_offq, edge_hit, d_offp, overlap_hit, inl, d_addend, d_out);
+    std::vector<double> h(16 * static_cast<size_t>(K));
+    VF_TRY(cudaMemcpyAsync(h.data(), d_out, h.size() * sizeof(double), cudaMemcpyDeviceToHost, stream));
+    VF_TRY(cudaStreamSynchronize(stream));
+#undef VF_TRY
+    cleanup();
+    for (int k = 0; k < K; ++k) {
+        const double* o = h.data() + 16 * k;
+        const long long* c = reinterpret_cast<const long long*>(o);
+        VerifyOutput& r = out[k];
+        // the 6x6 of line_process.cpp:24-28 from the ordered sums
+        double L[6][6] = {};
+        const double ata[3][3] = {{o[0], o[1], o[2]}, {o[1], o[3], o[4]}, {o[2], o[4], o[5]}};
+        const double px = o[6], py = o[7], pz = o[8];
+        // TR += a^T, BL += a with a = -[p]x: +0.0 on the diagonals (sums of -0.0 from +0.0)
+        const double A[3][3] = {{0.0, pz, -py}, {-pz, 0.0, px}, {py, -px, 0.0}};
+        const double n_pairs = static_cast<double>(c[10]);
+        for (int a = 0; a < 3; ++a)
+            for (int b = 0; b < 3; ++b) {
+                L[a][b] = ata[a][b];
+                L[a][3 + b] = A[b][a];
+                L[3 + a][b] = A[a][b];
+                L[3 + a][3 + b] = a == b ? n_pairs : 0.0;
+            }
+        for (int a = 0; a < 6; ++a)
+            for (int b = 0; b < 6; ++b) r.info[6 * a + b] = c[10] > 0 ? L[a][b] : 0.0;
+        r.pair_count = c[10];
+        r.overlap_hits = c[11];
+        r.inliers = c[12];
+        r.sq_sum = o[9];
+    }
+    return cudaSuccess;
+}
+
+}  // namespace lkk

@@ -483,6 +483,51 @@ def edge_info(cloud_i: PointCloud, cloud_j: PointCloud, t_i: RigidTransform, t_j
     return e
 
 
+# ------------------------------------------------------- batched verification (north-star item 5)
+@dataclass
+class VerifyParams:
+    """Config E: edge_info radius, propose_loops overlap radius,
+    evaluate_hypothesis d_max / normal gate / SearchGrid cell."""
+
+    epsilon: float = 0.05
+    overlap_radius: float = 0.1
+    d_max: float = 0.075
+    grid_cell: float = 0.0  # <= 0 -> d_max
+    normal_angle_max: float = 30.0 * math.pi / 180.0
+    device: int = -1
+
+
+@dataclass
+class VerifyResult:
+    info: EdgeInfo            # edge_info(Q, P, T_i, T_j, epsilon); pair_count 0 = NoCorrespondences
+    overlap_hits: int         # propose_loops: posed later points within overlap_radius
+    overlap: float
+    inliers: int              # evaluate_hypothesis(T, P, Q)
+    inlier_ratio: float
+    fitness: float
+
+
+def verify_batch(earlier: Sequence[PointCloud], later: Sequence[PointCloud], pose_earlier: Sequence[RigidTransform],
+                 pose_later: Sequence[RigidTransform], measurement: Sequence[RigidTransform],
+                 params: Optional[VerifyParams] = None) -> List[VerifyResult]:
+    """Loop verification of a batch of pairs in one device pass (include/loopkit_b200.h lk_verify_batch)."""
+    p = params or VerifyParams()
+    n = len(earlier)
+    ci = (abi.lk_cloud * max(n, 1))(*[c.as_c() for c in earlier])
+    cj = (abi.lk_cloud * max(n, 1))(*[c.as_c() for c in later])
+    pack = lambda ts: np.ascontiguousarray(np.stack([t.packed() for t in ts]) if n else np.zeros((1, 12)))
+    ti, tj, tm = pack(pose_earlier), pack(pose_later), pack(measurement)
+    cp = abi.lk_verify_params(epsilon=float(p.epsilon), overlap_radius=float(p.overlap_radius), d_max=float(p.d_max),
+                              grid_cell=float(p.grid_cell), normal_angle_max=float(p.normal_angle_max),
+                              device=int(p.device), reserved=0)
+    out = (abi.lk_verify_result * max(n, 1))()
+    check(abi.lib().lk_verify_batch(ci, cj, ti.ctypes.data_as(abi.dptr), tj.ctypes.data_as(abi.dptr),
+                                    tm.ctypes.data_as(abi.dptr), n, C.byref(cp), out))
+    return [VerifyResult(EdgeInfo(np.array(out[k].info[:]).reshape(6, 6), int(out[k].pair_count)),
+                         int(out[k].overlap_hits), float(out[k].overlap), int(out[k].inliers),
+                         float(out[k].inlier_ratio), float(out[k].fitness)) for k in range(n)]
+
+
 # ------------------------------------------------------- ICP (north-star item 4)
 @dataclass
 class IcpParams:

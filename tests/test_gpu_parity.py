@@ -338,7 +338,7 @@ def test_edge_info_matches_oracle(oracle):
     info, cnt = oracle.edge_info(ci.positions, ci.positions, T.rotation, T.translation, T.rotation, T.translation,
                                  0.05)
     assert e.pair_count == cnt == 40
-    assert np.abs(e.info - info).max() <= 1e-9 * max(1.0, np.abs(info).max())
+    assert np.array_equal(e.info, info)  # the reference's sequential sums, bit for bit
     a = lk.PointCloud(np.array([[0, 0, 0], [1, 0, 0], [2, 0, 0]], float))
     b = lk.PointCloud(np.array([[0.01, 0, 0], [5, 0, 0]], float))
     I = lk.RigidTransform()
@@ -354,7 +354,7 @@ def test_edge_info_matches_oracle(oracle):
         info, cnt = oracle.edge_info(p.target.positions, p.source.positions, np.eye(3), np.zeros(3),
                                      p.truth.rotation, p.truth.translation, 0.05)
         assert e.pair_count == cnt
-        assert np.abs(e.info - info).max() <= 1e-9 * np.abs(info).max()
+        assert np.array_equal(e.info, info)
 
 
 def test_large_pair_b1_shape_parity(oracle):
