@@ -28,6 +28,8 @@ import sys
 import threading
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -50,6 +52,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true", help="skip the config D (ICP) and E (verification) legs")
+    ap.add_argument("--verify-pairs", type=int, default=256)
     return ap.parse_args()
 
 
@@ -218,6 +222,112 @@ def run_reference(args):
     return 0
 
 
+# ------------------------------------------------------------------ extras
+def _pool_map(fn, items):
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:  # ctypes calls release the GIL
+        return list(ex.map(fn, items))
+
+
+def bench_icp(args):
+    """Config D: ICP point-to-plane refinement of a 2.4M-point
+    submap pair from a perturbed truth, through the public API from host
+    buffers (upload, ring-grid build and every iteration inside the timing).
+    CPU baseline: one accumulation of the oracle on the full pair (all host
+    threads), scaled by the iteration count."""
+    import paper_1801_01572_b200 as lk
+    from paper_1801_01572_b200 import synth
+    pair = synth.submap_pair()
+    T0 = synth.compose(synth.transform_from_twist([0.02, -0.015, 0.01, 0.02, -0.01, 0.015]), pair.truth)
+    p = lk.IcpParams(max_correspondence_distance=0.05, max_iterations=30, convergence_eps=1e-10)
+    lk.icp_point_to_plane(pair.source, pair.target, T0, p)  # warm-up
+    times = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        r = lk.icp_point_to_plane(pair.source, pair.target, T0, p)
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * min(times)
+    evaluated = len(r.history)
+    out = {"workload": "D: submap_pair(seed 2, 8 views x 640x480 per submap, no downsample), ICP from truth "
+                       "perturbed by (0.02, -0.015, 0.01 rad; 0.02, -0.01, 0.015 m), d = 0.05 m",
+           "source_points": pair.source.size(), "target_points": pair.target.size(),
+           "iterations": r.iterations, "converged": r.converged, "correspondences": r.correspondences,
+           "rmse": r.rmse, "ms_per_icp": ms, "ms_per_iteration": ms / max(evaluated, 1),
+           "point_iterations_per_s": pair.source.size() * evaluated / (ms / 1e3),
+           "timing": "wall clock of lk_icp_point_to_plane from host buffers (H2D, ring grid, all iterations), best of 3"}
+    if not args.no_cpu_baseline:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle as O
+        t0 = time.perf_counter()
+        R1, t1, res1, h1 = O.icp_point_to_plane(pair.source.positions, pair.target.positions, pair.target.normals,
+                                                T0.rotation, T0.translation, 0.05, 1, 0.0)
+        cpu_it = time.perf_counter() - t0
+        out["cpu_baseline"] = {"kind": "port", "cores": os.cpu_count(),
+                               "sample": "one oracle ICP iteration (grid build + accumulation + solve) on the full "
+                                         "pair, scaled by the device's iteration count",
+                               "ms_per_iteration": 1e3 * cpu_it,
+                               "ms_per_icp_extrapolated": 1e3 * cpu_it * evaluated,
+                               "parity_first_iteration": bool(h1[0, 0] == r.history[0, 0]
+                                                              and h1[0, 1] == r.history[0, 1])}
+    return out
+
+
+def bench_verification(args):
+    """Config E: loop verification of synth_registration_pair
+    seeds 1..K with their truths as measurements: edge_info(Q, P, I, truth,
+    0.05), the propose_loops overlap within 0.1 m and evaluate_hypothesis(truth)
+    per pair, one lk_verify_batch call from host buffers."""
+    import paper_1801_01572_b200 as lk
+    from paper_1801_01572_b200 import synth
+    K = args.verify_pairs
+    pairs = _pool_map(synth.synth_registration_pair, range(1, K + 1))
+    Q = [p.target for p in pairs]
+    P = [p.source for p in pairs]
+    I = [lk.RigidTransform() for _ in pairs]
+    T = [p.truth for p in pairs]
+    vp = lk.VerifyParams()
+    lk.verify_batch(Q, P, I, T, T, vp)  # warm-up
+    times = []
+    for _ in range(5):
+        t0 = time.perf_counter()
+        out = lk.verify_batch(Q, P, I, T, T, vp)
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * min(times)
+    npts = sum(p.source.size() + p.target.size() for p in pairs)
+    res = {"workload": f"E: synth_registration_pair(1..{K}), measurement = truth; edge_info eps 0.05, overlap "
+                       "r 0.1, evaluate_hypothesis d_max 0.075 / 30 deg",
+           "pairs": K, "points": npts, "ms_per_batch": ms, "pairs_per_s": K / (ms / 1e3),
+           "mean_overlap": float(np.mean([o.overlap for o in out])),
+           "mean_inlier_ratio": float(np.mean([o.inlier_ratio for o in out])),
+           "timing": "wall clock of lk_verify_batch from host buffers (H2D, 3K ring grids, queries, sums), best of 5"}
+    if not args.no_cpu_baseline:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle as O
+        op = O.params()
+        sample = pairs[:32]
+
+        def one(p):
+            try:
+                O.edge_info(p.target.positions, p.source.positions, np.eye(3), np.zeros(3), p.truth.rotation,
+                            p.truth.translation, 0.05)
+            except O.OracleError:
+                pass
+            h = O.overlap_hits(p.source.positions, p.truth.rotation, p.truth.translation, p.target.positions,
+                               np.eye(3), np.zeros(3), 0.1)
+            e = O.evaluate_hypothesis(p.truth.rotation, p.truth.translation, p.source.positions, p.source.normals,
+                                      p.target.positions, p.target.normals, 0.075, op)
+            return h, e
+        t0 = time.perf_counter()
+        chk = _pool_map(one, sample)
+        cpu_s = time.perf_counter() - t0
+        res["cpu_baseline"] = {"kind": "port", "cores": os.cpu_count(),
+                               "sample": f"the oracle on the first {len(sample)} pairs, one pair per host thread",
+                               "pairs_per_s": len(sample) / cpu_s,
+                               "parity": all(h == o.overlap_hits and e[2] == o.inliers and e[1] == o.fitness
+                                             for (h, e), o in zip(chk, out[:len(sample)]))}
+    return res
+
+
 # ------------------------------------------------------------------ GPU
 def run_b200(args):
     import numpy as np
@@ -363,10 +473,11 @@ def run_b200(args):
             "gpu_launches": KERNELS_PER_STEP * args.steps,
             "clocks": clock_info,
         }
-        # roofline of the evaluation kernels (k_score_split + k_score_resolve:
-        # every candidate x point evaluation happens in one of the two),
-        # algorithmic bytes per SURVEY.md 8d, event-timed on the launch stream
-        score_ms = (ph["k_score_split"] + ph["k_score_resolve"]) / max(runs, 1)
+        # roofline of the scoring kernel (every candidate x point evaluation
+        # happens there), algorithmic bytes per SURVEY.md 8d, event-timed on
+        # the launch stream
+        score_kernels = [k for k in ph if k not in ("k_hyp_sample", "k_kabsch")]
+        score_ms = sum(ph[k] for k in score_kernels) / max(runs, 1)
         shape = None
         if world == 1 and not args.no_cpu_baseline:
             cpu = cpu_oracle_registration(pair, H, args.seed)
@@ -387,16 +498,19 @@ def run_b200(args):
         evals_per_launch = mstats.evals_executed / max(world, 1)
         if shape["bytes_per_eval"] and score_ms > 0:
             achieved = evals_per_launch * shape["bytes_per_eval"] / (score_ms / 1e3) / 1e9
-            traffic = ncu_traffic(("k_score_split", "k_score_resolve"))
+            traffic = ncu_traffic(score_kernels)
             line["roofline"] = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                                 "frac": achieved / hbm_peak, "traffic": traffic,
-                                "kernel": "k_score_split+k_score_resolve",
+                                "kernel": "+".join(score_kernels),
                                 "peak_kind": peak_kind, "evals_per_launch": evals_per_launch,
                                 "kernel_ms": score_ms, "work_shape": shape,
                                 "note": "achieved = evals executed per step x algorithmic bytes/eval "
-                                        "(1+72o+12k+12h, SURVEY.md 8d) / event time of the two evaluation "
-                                        "kernels; traffic = their DRAM bytes per launch from the committed ncu "
-                                        "capture (profiles/ncu_traffic.json): the working set is L2-resident"}
+                                        "(1+72o+12k+12h, SURVEY.md 8d) / event time of the scoring kernel; "
+                                        "traffic = its DRAM bytes per launch from the committed ncu capture "
+                                        "(profiles/ncu_traffic.json). The working set is L2-resident: the "
+                                        "binding limit is L2 gather latency (see profiles/ and DESIGN.md)"}
+        if world == 1 and not args.no_extras:
+            line["extras"] = {"icp_D": bench_icp(args), "verification_E": bench_verification(args)}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -255,7 +255,9 @@ cudaError_t build_ring_grid(RingStorage& rs, const double* d_pos, int64_t n, dou
         lo[a] = from_key(hk[a]);
         hi[a] = from_key(hk[3 + a]);
     }
-    RingGrid v = ring_frame(lo, hi, d_max, -1.0, int64_t(1) << 28, fast);
+    // at most 64 cells per point (and 2^28 overall)
+    const int64_t cap = std::min<int64_t>(std::max<int64_t>(64 * n, 4096), int64_t(1) << 28);
+    RingGrid v = ring_frame(lo, hi, d_max, -1.0, cap, fast);
     int64_t nc = v.ncells;
     int32_t *cell_of = nullptr, *counts = nullptr;
     RG_TRY(cudaMallocAsync(&cell_of, n * sizeof(int32_t), stream));
@@ -328,7 +330,10 @@ cudaError_t build_ring_grids(RingBatch& rb, const double* d_pos, const int64_t* 
             lo[a] = from_key(hk[6 * k + a]);
             hi[a] = from_key(hk[6 * k + 3 + a]);
         }
-        views[k] = ring_frame(lo, hi, h_dmax[k], h_cell ? h_cell[k] : -1.0, int64_t(1) << 24, true);
+        // the dense CSR is sized to the cloud: at most 16 cells per point
+        const int64_t npk = h_offsets[k + 1] - h_offsets[k];
+        const int64_t cap = std::min<int64_t>(std::max<int64_t>(16 * npk, 4096), int64_t(1) << 24);
+        views[k] = ring_frame(lo, hi, h_dmax[k], h_cell ? h_cell[k] : -1.0, cap, true);
         cell_off[k + 1] = cell_off[k] + views[k].ncells;
     }
     const int64_t nc = cell_off[K];
