@@ -223,6 +223,16 @@ def run_reference(args):
 
 
 # ------------------------------------------------------------------ extras
+def _pinned_cloud(c):
+    """The cloud's arrays copied into pinned host memory (the H2D inside the
+    timed calls then runs at full PCIe rate), and the tensors that own it."""
+    import torch
+    import paper_1801_01572_b200 as lk
+    tp = torch.from_numpy(np.ascontiguousarray(c.positions)).pin_memory()
+    tn = torch.from_numpy(np.ascontiguousarray(c.normals)).pin_memory() if c.normals is not None else None
+    return lk.PointCloud(tp.numpy(), tn.numpy() if tn is not None else None), (tp, tn)
+
+
 def _pool_map(fn, items):
     from concurrent.futures import ThreadPoolExecutor
     with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:  # ctypes calls release the GIL
@@ -240,11 +250,13 @@ def bench_icp(args):
     pair = synth.submap_pair()
     T0 = synth.compose(synth.transform_from_twist([0.02, -0.015, 0.01, 0.02, -0.01, 0.015]), pair.truth)
     p = lk.IcpParams(max_correspondence_distance=0.05, max_iterations=30, convergence_eps=1e-10)
-    lk.icp_point_to_plane(pair.source, pair.target, T0, p)  # warm-up
+    src, keep_s = _pinned_cloud(pair.source)
+    tgt, keep_t = _pinned_cloud(pair.target)
+    lk.icp_point_to_plane(src, tgt, T0, p)  # warm-up
     times = []
     for _ in range(3):
         t0 = time.perf_counter()
-        r = lk.icp_point_to_plane(pair.source, pair.target, T0, p)
+        r = lk.icp_point_to_plane(src, tgt, T0, p)
         times.append(time.perf_counter() - t0)
     ms = 1e3 * min(times)
     evaluated = len(r.history)
@@ -254,7 +266,9 @@ def bench_icp(args):
            "iterations": r.iterations, "converged": r.converged, "correspondences": r.correspondences,
            "rmse": r.rmse, "ms_per_icp": ms, "ms_per_iteration": ms / max(evaluated, 1),
            "point_iterations_per_s": pair.source.size() * evaluated / (ms / 1e3),
-           "timing": "wall clock of lk_icp_point_to_plane from host buffers (H2D, ring grid, all iterations), best of 3"}
+           "h2d_bytes": 24 * pair.source.size() + 48 * pair.target.size(),
+           "timing": "wall clock of lk_icp_point_to_plane from pinned host buffers (H2D, ring grid, all "
+                     "iterations), best of 3"}
     if not args.no_cpu_baseline:
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         import oracle as O
@@ -281,8 +295,9 @@ def bench_verification(args):
     from paper_1801_01572_b200 import synth
     K = args.verify_pairs
     pairs = _pool_map(synth.synth_registration_pair, range(1, K + 1))
-    Q = [p.target for p in pairs]
-    P = [p.source for p in pairs]
+    pinned = [(_pinned_cloud(p.target), _pinned_cloud(p.source)) for p in pairs]
+    Q = [q for (q, _), _ in pinned]
+    P = [s for _, (s, _) in pinned]
     I = [lk.RigidTransform() for _ in pairs]
     T = [p.truth for p in pairs]
     vp = lk.VerifyParams()
@@ -299,7 +314,9 @@ def bench_verification(args):
            "pairs": K, "points": npts, "ms_per_batch": ms, "pairs_per_s": K / (ms / 1e3),
            "mean_overlap": float(np.mean([o.overlap for o in out])),
            "mean_inlier_ratio": float(np.mean([o.inlier_ratio for o in out])),
-           "timing": "wall clock of lk_verify_batch from host buffers (H2D, 3K ring grids, queries, sums), best of 5"}
+           "h2d_bytes": 48 * npts,
+           "timing": "wall clock of lk_verify_batch from pinned host buffers (H2D, 3K ring grids, queries, "
+                     "sums), best of 5"}
     if not args.no_cpu_baseline:
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         import oracle as O

@@ -891,9 +891,9 @@ lk_status lk_score_candidates(lk_grid* grid, const lk_cloud* src, const double* 
     });
 }
 
-// Packs the pairs' clouds into contiguous host arrays with point offsets.
+// The pairs' clouds as per-pair host pointers with point offsets (validated).
 struct PackedPairs {
-    std::vector<double> qpos, qnrm, ppos, pnrm;
+    std::vector<const double*> qpos, qnrm, ppos, pnrm;
     std::vector<int64_t> offq, offp;
 };
 
@@ -909,23 +909,13 @@ PackedPairs pack_pairs(const lk_cloud* ci, const lk_cloud* cj, int64_t K, bool n
             throw lk::Status(LK_MISSING_NORMALS, "evaluate_hypothesis: both clouds need normals");
         pk.offq[k + 1] = pk.offq[k] + ci[k].n;
         pk.offp[k + 1] = pk.offp[k] + cj[k].n;
+        pk.qpos.push_back(ci[k].xyz);
+        pk.ppos.push_back(cj[k].xyz);
+        pk.qnrm.push_back(ci[k].nxyz);
+        pk.pnrm.push_back(cj[k].nxyz);
     }
     if (pk.offq[K] > INT32_MAX / 2 || pk.offp[K] > INT32_MAX / 2)
         throw lk::Status(LK_INVALID_ARGUMENT, "verify: batch too large");
-    pk.qpos.resize(3 * static_cast<size_t>(pk.offq[K]));
-    pk.ppos.resize(3 * static_cast<size_t>(pk.offp[K]));
-    if (normals) {
-        pk.qnrm.resize(pk.qpos.size());
-        pk.pnrm.resize(pk.ppos.size());
-    }
-    for (int64_t k = 0; k < K; ++k) {
-        std::memcpy(pk.qpos.data() + 3 * pk.offq[k], ci[k].xyz, 3 * ci[k].n * sizeof(double));
-        std::memcpy(pk.ppos.data() + 3 * pk.offp[k], cj[k].xyz, 3 * cj[k].n * sizeof(double));
-        if (normals) {
-            std::memcpy(pk.qnrm.data() + 3 * pk.offq[k], ci[k].nxyz, 3 * ci[k].n * sizeof(double));
-            std::memcpy(pk.pnrm.data() + 3 * pk.offp[k], cj[k].nxyz, 3 * cj[k].n * sizeof(double));
-        }
-    }
     return pk;
 }
 

@@ -267,7 +267,11 @@ cudaError_t icp_point_to_plane(const double* d_src, int64_t n, const RingStorage
 // computes edge_info only (normals and T unused).
 struct VerifyInput {
     int32_t n_pairs;
-    const double *qpos, *qnrm, *ppos, *pnrm;  // Q = cloud_i (earlier), P = cloud_j (later)
+    // per pair host pointers (3 * n doubles each); Q = cloud_i (earlier), P = cloud_j (later)
+    const double* const* qpos;
+    const double* const* qnrm;
+    const double* const* ppos;
+    const double* const* pnrm;
     const int64_t *offq, *offp;
     const double *Ti, *Tj, *T;
     double epsilon, overlap_radius, d_max, grid_cell, cos_max;

@@ -99,49 +99,82 @@ __global__ void k_verify_src(const double* __restrict__ p, const double* __restr
     addend[i] = add;
 }
 
-// One warp per pair, one accumulator per lane, each summed in point order:
-// lanes 0-5 the a^T a entries (0,0) (0,1) (0,2) (1,1) (1,2) (2,2) with
-// a = -[q]x, lanes 6-8 sum q.x, q.y, q.z, lane 9 the evaluate_hypothesis
-// sq_sum; lane 10 counts the edge hits, 11 the overlap hits, 12 the inliers.
-// out per pair: 10 doubles then 3 int64 (as doubles' bits).
-__global__ void k_verify_sums(const double* __restrict__ q, const int64_t* __restrict__ offq,
-                              const uint8_t* __restrict__ edge_hit, const int64_t* __restrict__ offp,
-                              const uint8_t* __restrict__ overlap_hit, const uint8_t* __restrict__ inlier,
-                              const double* __restrict__ addend, double* __restrict__ out) {
+// One warp per pair. The points are staged 32 at a time (coalesced): every
+// lane computes its point's nine contributions -- the a^T a entries (0,0)
+// (0,1) (0,2) (1,1) (1,2) (2,2) with a = -[q]x, then q.x, q.y, q.z -- into
+// shared memory, and lane j < 9 adds column j over the staged points in point
+// order: the reference's sequential sums (line_process.cpp:24-28), with the
+// loads off the dependent add chain. The same for the evaluate_hypothesis
+// sq_sum over the source points. Counts are popcounts of the hit ballots.
+// out per pair: 10 doubles (9 edge sums, sq_sum) then 3 int64 at [10..12].
+__global__ void __launch_bounds__(32) k_verify_sums(const double* __restrict__ q, const int64_t* __restrict__ offq,
+                                                    const uint8_t* __restrict__ edge_hit,
+                                                    const int64_t* __restrict__ offp,
+                                                    const uint8_t* __restrict__ overlap_hit,
+                                                    const uint8_t* __restrict__ inlier,
+                                                    const double* __restrict__ addend, double* __restrict__ out) {
+    __shared__ double s_c[9][33];
     const int k = blockIdx.x;
     const int lane = threadIdx.x;
-    double acc = 0.0;
-    long long cnt = 0;
-    if (lane < 9 || lane == 10) {
-        const int r = lane < 3 ? 0 : (lane < 5 ? 1 : 2);
-        const int c = lane == 0 ? 0 : (lane == 1 || lane == 3) ? 1 : 2;
-        for (int64_t i = offq[k]; i < offq[k + 1]; ++i) {
-            if (!edge_hit[i]) continue;
-            if (lane == 10) {
-                ++cnt;
-                continue;
-            }
+    double acc = 0.0, sq = 0.0;
+    long long n_edge = 0, n_over = 0, n_inl = 0;
+    for (int64_t base = offq[k]; base < offq[k + 1]; base += 32) {
+        const int64_t i = base + lane;
+        const bool hit = i < offq[k + 1] && edge_hit[i];
+        const unsigned m = __ballot_sync(0xffffffffu, hit);
+        n_edge += __popc(m);
+        if (hit) {
             const V3 v = ld3(q, i);
-            if (lane < 6) {
-                const double a[3][3] = {{-0.0, v.z, -v.y}, {-v.z, -0.0, v.x}, {v.y, -v.x, -0.0}};
-                acc += (a[0][r] * a[0][c] + a[1][r] * a[1][c]) + a[2][r] * a[2][c];
-            } else {
-                acc += lane == 6 ? v.x : (lane == 7 ? v.y : v.z);
+            const double a[3][3] = {{-0.0, v.z, -v.y}, {-v.z, -0.0, v.x}, {v.y, -v.x, -0.0}};
+            s_c[0][lane] = (a[0][0] * a[0][0] + a[1][0] * a[1][0]) + a[2][0] * a[2][0];
+            s_c[1][lane] = (a[0][0] * a[0][1] + a[1][0] * a[1][1]) + a[2][0] * a[2][1];
+            s_c[2][lane] = (a[0][0] * a[0][2] + a[1][0] * a[1][2]) + a[2][0] * a[2][2];
+            s_c[3][lane] = (a[0][1] * a[0][1] + a[1][1] * a[1][1]) + a[2][1] * a[2][1];
+            s_c[4][lane] = (a[0][1] * a[0][2] + a[1][1] * a[1][2]) + a[2][1] * a[2][2];
+            s_c[5][lane] = (a[0][2] * a[0][2] + a[1][2] * a[1][2]) + a[2][2] * a[2][2];
+            s_c[6][lane] = v.x;
+            s_c[7][lane] = v.y;
+            s_c[8][lane] = v.z;
+        }
+        __syncwarp();
+        if (lane < 9) {
+            unsigned mm = m;
+            while (mm) {
+                const int j = __ffs(mm) - 1;
+                mm &= mm - 1;
+                acc += s_c[lane][j];
             }
         }
-    } else if (lane == 9 || lane == 11 || lane == 12) {
-        for (int64_t i = offp[k]; i < offp[k + 1]; ++i) {
-            if (lane == 11) {
-                cnt += overlap_hit[i];
-            } else if (inlier[i]) {
-                if (lane == 9) acc += addend[i];
-                else ++cnt;
+        __syncwarp();
+    }
+    for (int64_t base = offp[k]; base < offp[k + 1]; base += 32) {
+        const int64_t i = base + lane;
+        const bool in = i < offp[k + 1];
+        n_over += __popc(__ballot_sync(0xffffffffu, in && overlap_hit[i]));
+        const bool inl = in && inlier[i];
+        const unsigned m = __ballot_sync(0xffffffffu, inl);
+        n_inl += __popc(m);
+        if (inl) s_c[0][lane] = addend[i];
+        __syncwarp();
+        if (lane == 9) {
+            unsigned mm = m;
+            while (mm) {
+                const int j = __ffs(mm) - 1;
+                mm &= mm - 1;
+                sq += s_c[0][j];
             }
         }
+        __syncwarp();
     }
     double* o = out + 16 * k;
-    if (lane < 10) o[lane] = acc;
-    if (lane >= 10 && lane <= 12) reinterpret_cast<long long*>(o)[lane] = cnt;
+    if (lane < 9) o[lane] = acc;
+    if (lane == 9) o[9] = sq;
+    if (lane == 0) {
+        long long* c = reinterpret_cast<long long*>(o);
+        c[10] = n_edge;
+        c[11] = n_over;
+        c[12] = n_inl;
+    }
 }
 
 }  // namespace
@@ -174,8 +207,19 @@ cudaError_t verify_batch(const VerifyInput& in, VerifyOutput* out, cudaStream_t 
     VF_TRY(pool_alloc(&d_offq, (K + 1) * sizeof(int64_t), stream));
     VF_TRY(pool_alloc(&d_offp, (K + 1) * sizeof(int64_t), stream));
     VF_TRY(pool_alloc(&d_T, 3 * 12 * K * sizeof(double), stream));
-    VF_TRY(cudaMemcpyAsync(d_qpos, in.qpos, 3 * nq * sizeof(double), cudaMemcpyHostToDevice, stream));
-    VF_TRY(cudaMemcpyAsync(d_ppos, in.ppos, 3 * np * sizeof(double), cudaMemcpyHostToDevice, stream));
+    // each cloud straight from the caller's buffer into its slot (pinned
+    // buffers go at full PCIe rate; no host-side packing)
+    std::vector<void*> dsts, srcs;
+    std::vector<size_t> sizes;
+    auto add_copies = [&](double* dst, const double* const* src, const int64_t* off) {
+        for (int k = 0; k < K; ++k) {
+            dsts.push_back(dst + 3 * off[k]);
+            srcs.push_back(const_cast<double*>(src[k]));
+            sizes.push_back(3 * (off[k + 1] - off[k]) * sizeof(double));
+        }
+    };
+    add_copies(d_qpos, in.qpos, in.offq);
+    add_copies(d_ppos, in.ppos, in.offp);
     VF_TRY(cudaMemcpyAsync(d_offq, in.offq, (K + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, stream));
     VF_TRY(cudaMemcpyAsync(d_offp, in.offp, (K + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, stream));
     const double* d_Ti = d_T;
@@ -186,10 +230,12 @@ cudaError_t verify_batch(const VerifyInput& in, VerifyOutput* out, cudaStream_t 
     if (in.full) {
         VF_TRY(pool_alloc(&d_qn, 3 * nq * sizeof(double), stream));
         VF_TRY(pool_alloc(&d_pn, 3 * np * sizeof(double), stream));
-        VF_TRY(cudaMemcpyAsync(d_qn, in.qnrm, 3 * nq * sizeof(double), cudaMemcpyHostToDevice, stream));
-        VF_TRY(cudaMemcpyAsync(d_pn, in.pnrm, 3 * np * sizeof(double), cudaMemcpyHostToDevice, stream));
+        add_copies(d_qn, in.qnrm, in.offq);
+        add_copies(d_pn, in.pnrm, in.offp);
         VF_TRY(cudaMemcpyAsync(d_T + 24 * K, in.T, 12 * K * sizeof(double), cudaMemcpyHostToDevice, stream));
     }
+    for (size_t c = 0; c < dsts.size(); ++c)
+        VF_TRY(cudaMemcpyAsync(dsts[c], srcs[c], sizes[c], cudaMemcpyHostToDevice, stream));
     // grid clouds: [T_j P_k]_k for edge_info, then (full) [T_i Q_k]_k, [Q_k]_k
     const int G = in.full ? 3 * K : K;
     const int64_t ng = np + (in.full ? 2 * nq : 0);
