@@ -205,4 +205,62 @@ std::pair<double, double> evaluate_hypothesis(const Transform& T, const Cloud& s
     return {sc.inlier_ratio, sc.fitness};
 }
 
+// edge_info (line_process.hpp:15-16 / line_process.cpp:11-33): the 6x6
+// information matrix (row-major) and pair count; throws NoCorrespondences.
+struct EdgeInfo {
+    double info[36];
+    std::int64_t pair_count = 0;
+};
+template <class E = DefaultErrors, class Cloud>
+EdgeInfo edge_info(const Cloud& cloud_i, const Cloud& cloud_j, const Transform& t_i, const Transform& t_j,
+                   double epsilon) {
+    lk_cloud ci = as_lk_cloud(cloud_i), cj = as_lk_cloud(cloud_j);
+    double ti[12], tj[12];
+    for (int k = 0; k < 9; ++k) {
+        ti[k] = t_i.R[k];
+        tj[k] = t_j.R[k];
+    }
+    for (int k = 0; k < 3; ++k) {
+        ti[9 + k] = t_i.t[k];
+        tj[9 + k] = t_j.t[k];
+    }
+    EdgeInfo out;
+    lk_status st = lk_edge_info_batched(&ci, &cj, ti, tj, 1, epsilon, -1, out.info, &out.pair_count);
+    if (st != LK_OK) throw_status<E>(st);
+    if (out.pair_count == 0) throw typename E::NoCorrespondencesT("edge_info: no points within epsilon");
+    return out;
+}
+
+// ICP point-to-plane refinement of `init` (source -> target); DESIGN.md "ICP".
+struct IcpResult {
+    Transform transform;
+    int iterations = 0;
+    bool converged = false;
+    std::int64_t correspondences = 0;
+    double rmse = 0.0;
+    double fitness = 0.0;
+};
+template <class E = DefaultErrors, class Cloud>
+IcpResult icp_point_to_plane(const Cloud& source, const Cloud& target, const Transform& init,
+                             double max_correspondence_distance = 0.05, int max_iterations = 30,
+                             double convergence_eps = 1e-10, int32_t device = -1) {
+    lk_cloud s = as_lk_cloud(source), t = as_lk_cloud(target);
+    double T0[12];
+    for (int k = 0; k < 9; ++k) T0[k] = init.R[k];
+    for (int k = 0; k < 3; ++k) T0[9 + k] = init.t[k];
+    lk_icp_params p{max_correspondence_distance, max_iterations, device, convergence_eps};
+    lk_icp_result r{};
+    lk_status st = lk_icp_point_to_plane(&s, &t, T0, &p, &r, nullptr);
+    if (st != LK_OK) throw_status<E>(st);
+    IcpResult o;
+    for (int k = 0; k < 9; ++k) o.transform.R[k] = r.R[k];
+    for (int k = 0; k < 3; ++k) o.transform.t[k] = r.t[k];
+    o.iterations = r.iterations;
+    o.converged = r.converged != 0;
+    o.correspondences = r.correspondences;
+    o.rmse = r.rmse;
+    o.fitness = r.fitness;
+    return o;
+}
+
 }  // namespace loopkit_b200

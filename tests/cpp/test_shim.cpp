@@ -84,5 +84,18 @@ int main(int argc, char** argv) {
                 r->transform.t[1], r->transform.t[2], (long long)st.sampled);
     auto ef = loopkit_b200::evaluate_hypothesis(r->transform, src, tgt, 0.075, params);
     std::printf("ok: evaluate_hypothesis ratio %.6f fitness %.3e\n", ef.first, ef.second);
+    loopkit_b200::Transform I{{1, 0, 0, 0, 1, 0, 0, 0, 1}, {0, 0, 0}};
+    auto ei = loopkit_b200::edge_info(tgt, src, I, r->transform, 0.05);
+    std::printf("ok: edge_info pair_count %lld\n", (long long)ei.pair_count);
+    try {
+        loopkit_b200::edge_info(tiny, tiny, I, loopkit_b200::Transform{{1, 0, 0, 0, 1, 0, 0, 0, 1}, {9, 9, 9}}, 0.05);
+        std::puts("FAIL: expected NoCorrespondences");
+        return 1;
+    } catch (const loopkit_b200::NoCorrespondences&) {
+        std::puts("ok: NoCorrespondences");
+    }
+    auto icp = loopkit_b200::icp_point_to_plane(src, tgt, r->transform, 0.05);
+    std::printf("ok: icp iterations %d converged %d rmse %.3e t = %.4f %.4f %.4f\n", icp.iterations,
+                icp.converged ? 1 : 0, icp.rmse, icp.transform.t[0], icp.transform.t[1], icp.transform.t[2]);
     return 0;
 }

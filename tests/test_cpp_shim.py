@@ -35,3 +35,4 @@ def test_shim_on_gpu(tmp_path):
     out = subprocess.run([exe, "gpu"], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "ok: TooFewPoints" in out.stdout and "ok: index" in out.stdout
+    assert "ok: NoCorrespondences" in out.stdout and "ok: icp iterations" in out.stdout
