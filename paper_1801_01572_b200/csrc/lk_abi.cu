@@ -174,6 +174,59 @@ void release_worker(Worker* w) {
     g_free_workers.push_back(w);
 }
 
+// LK_TRACE=2: device-event timeline of prepare_registration (no syncs added;
+// printed after the final sync): per mark the device time of the event on its
+// stream and the host time it was enqueued, both from the start of prepare.
+struct TraceMark {
+    std::string name;
+    cudaEvent_t ev;
+    double host_ms;
+};
+std::mutex g_trace_mu;
+std::vector<TraceMark> g_trace;
+cudaEvent_t g_trace_start = nullptr;
+
+int trace_level() {
+    static const int lvl = [] {
+        const char* v = std::getenv("LK_TRACE");
+        return v ? std::atoi(v) : 0;
+    }();
+    return lvl;
+}
+
+double now_ms_since(double t0) { return (now_s() - t0) * 1e3; }
+
+void tmark(const char* name, cudaStream_t s, double t0) {
+    if (trace_level() < 2) return;
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    cudaEventRecord(e, s);
+    std::lock_guard<std::mutex> lock(g_trace_mu);
+    g_trace.push_back({name, e, now_ms_since(t0)});
+}
+
+void tstart(cudaStream_t s) {
+    if (trace_level() < 2) return;
+    std::lock_guard<std::mutex> lock(g_trace_mu);
+    for (auto& m : g_trace) cudaEventDestroy(m.ev);
+    g_trace.clear();
+    if (!g_trace_start) cudaEventCreate(&g_trace_start);
+    cudaEventRecord(g_trace_start, s);
+}
+
+void tdump() {
+    if (trace_level() < 2) return;
+    std::lock_guard<std::mutex> lock(g_trace_mu);
+    for (auto& m : g_trace) {
+        float ms = -1.f;
+        cudaEventSynchronize(m.ev);
+        cudaEventElapsedTime(&ms, g_trace_start, m.ev);
+        std::fprintf(stderr, "[lk trace] %-26s device %8.3f ms   enqueued %8.3f ms\n", m.name.c_str(), ms, m.host_ms);
+        cudaEventDestroy(m.ev);
+    }
+    g_trace.clear();
+}
+
 bool trace_on() {
     static const bool on = std::getenv("LK_TRACE") != nullptr;
     return on;
@@ -388,6 +441,10 @@ struct CloudSide {
 void prepare_side(CloudSide& cs, double feature_radius, double leaf, lkk::GridStorage* grid, double d_max,
                   int device, double t0, const char* tag, cudaStream_t grid_stream = nullptr) {
     auto mark = [&](const char* what) {
+        if (trace_level() >= 2) {
+            tmark((std::string(tag) + " " + what).c_str(), cs.s, t0);
+            return;
+        }
         if (!trace_on()) return;
         cudaStreamSynchronize(cs.s);
         std::fprintf(stderr, "[lk prepare %s] %-14s %8.3f ms\n", tag, what, (now_s() - t0) * 1e3);
@@ -406,8 +463,10 @@ void prepare_side(CloudSide& cs, double feature_radius, double leaf, lkk::GridSt
         cs.raw_pos = cs.raw_nrm = nullptr;
         mark("downsample");
         if (cs.status != 0 || cs.n < 4) return;
-        CK(lkk::cloud_stats(cs.pos, cs.nrm, cs.n, &cs.usable, &cs.max_norm, cs.s));
-        if (cs.usable < 4) return;
+        // usable normals and |p|max come back with the side's final sync
+        thread_local unsigned long long* h_stats = nullptr;
+        if (!h_stats) CK(cudaHostAlloc(reinterpret_cast<void**>(&h_stats), 2 * sizeof(unsigned long long), 0));
+        CK(lkk::cloud_stats_async(cs.pos, cs.nrm, cs.n, h_stats, cs.s));
         // the EvalGrid (registration.cpp:249) only needs the downsampled
         // cloud: it is built on its own stream and host thread while this
         // one runs the FPFH
@@ -423,9 +482,10 @@ void prepare_side(CloudSide& cs, double feature_radius, double leaf, lkk::GridSt
             const double* pos = cs.pos;
             const double* nrm = cs.nrm;
             const int64_t n = cs.n;
-            gw->post([grid, pos, nrm, n, d_max, grid_stream, device, &grid_err] {
+            gw->post([grid, pos, nrm, n, d_max, grid_stream, device, &grid_err, t0] {
                 cudaSetDevice(device);
                 grid_err = lkk::build_grid(*grid, 0, pos, nrm, n, d_max, d_max, grid_stream);
+                tmark("tgt eval grid (own stream)", grid_stream, t0);
             });
         }
         try {
@@ -439,6 +499,10 @@ void prepare_side(CloudSide& cs, double feature_radius, double leaf, lkk::GridSt
             throw;
         }
         mark("fpfh");
+        // one wait for the side's stream: the stats above, the features
+        // (the feature match runs on another stream) and the FPFH staging
+        CK(cudaStreamSynchronize(cs.s));
+        lkk::cloud_stats_decode(h_stats, &cs.usable, &cs.max_norm);
         if (gw) {
             gw->wait();
             release_worker(gw);
@@ -463,6 +527,7 @@ lk_status prepare_impl(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_pa
         return fail(LK_MISSING_NORMALS,
                     "register_global: inputs without normals need estimate_normals (not in this tier)");
     lk_reg_ctx* c = ctx_new(params->device);
+    tstart(c->own_stream);
     CloudSide S, T;
     S.in = src;
     S.s = c->own_stream;
@@ -485,7 +550,8 @@ lk_status prepare_impl(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_pa
         prepare_side(S, fr, leaf, nullptr, 0.0, dev, t0, "src");
         worker->wait();
         release_worker(worker);
-        if (trace_on()) std::fprintf(stderr, "[lk prepare] joined %8.3f ms\n", (now_s() - t0) * 1e3);
+        if (trace_on() && trace_level() < 2)
+            std::fprintf(stderr, "[lk prepare] joined %8.3f ms\n", (now_s() - t0) * 1e3);
         c->d_spos = S.pos;
         c->d_snrm = S.nrm;
         c->d_tpos = T.pos;
@@ -508,8 +574,11 @@ lk_status prepare_impl(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_pa
         cudaStream_t s = c->stream;
         CK(lkk::pool_alloc(&c->d_cache, c->ns * sizeof(int32_t), s));
         CK(lkk::feature_nn(c->d_sfeat, c->ns, c->d_tfeat, c->nt, c->d_cache, s));
+        tmark("joined, feature nn start", s, t0);
         ctx_finish_source(c);
+        tmark("feature nn done", s, t0);
         CK(cudaStreamSynchronize(s));
+        tdump();
         if (trace_on()) std::fprintf(stderr, "[lk prepare] feature nn %8.3f ms\n", (now_s() - t0) * 1e3);
     } catch (...) {
         drop(S);
@@ -725,9 +794,11 @@ lk_status lk_reg_run_hypotheses(lk_reg_ctx* ctx, const lk_reg_params* params, lk
         double t0 = now_s();
         lk_status st = run_range_impl(ctx, *params, 0, params->hypothesis_count, ctx->d_record);
         if (st != LK_OK) return st;
-        lk_reg_record rec{};
-        CK(cudaMemcpyAsync(&rec, ctx->d_record, sizeof(rec), cudaMemcpyDeviceToHost, ctx->stream));
+        auto* hrec = static_cast<lk_reg_record*>(lkk::host_scratch(sizeof(lk_reg_record)));
+        if (!hrec) CK(cudaErrorMemoryAllocation);
+        CK(cudaMemcpyAsync(hrec, ctx->d_record, sizeof(lk_reg_record), cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
+        const lk_reg_record rec = *hrec;
         double t1 = now_s();
         lk_hyp_stats local{};
         lk_hyp_stats* sp = stats ? stats : &local;

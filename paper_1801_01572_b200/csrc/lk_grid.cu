@@ -536,8 +536,9 @@ cudaError_t build_grid(GridStorage& g, int kind, const double* d_pos, const doub
         double* d_box = nullptr;
         LK_TRY(cudaMallocAsync(&d_box, 6 * sizeof(double), stream));
         k_bbox<<<1, 1024, 0, stream>>>(d_pos, n, d_box);
-        double box[6];
-        LK_TRY(cudaMemcpyAsync(box, d_box, sizeof(box), cudaMemcpyDeviceToHost, stream));
+        double* box = static_cast<double*>(host_scratch(6 * sizeof(double)));
+        if (!box) return cudaErrorMemoryAllocation;
+        LK_TRY(cudaMemcpyAsync(box, d_box, 6 * sizeof(double), cudaMemcpyDeviceToHost, stream));
         LK_TRY(cudaStreamSynchronize(stream));
         cudaFreeAsync(d_box, stream);
         double origin[3];
@@ -562,8 +563,9 @@ cudaError_t build_grid(GridStorage& g, int kind, const double* d_pos, const doub
         int init[6] = {INT32_MAX, INT32_MAX, INT32_MAX, INT32_MIN, INT32_MIN, INT32_MIN};
         LK_TRY(cudaMemcpyAsync(d_b, init, sizeof(init), cudaMemcpyHostToDevice, stream));
         k_cell_bounds<<<std::min<unsigned>(blocks_for(n, 256), 592), 256, 0, stream>>>(d_pos, n, cell, d_b);
-        int b[6];
-        LK_TRY(cudaMemcpyAsync(b, d_b, sizeof(b), cudaMemcpyDeviceToHost, stream));
+        int* b = static_cast<int*>(host_scratch(6 * sizeof(int)));
+        if (!b) return cudaErrorMemoryAllocation;
+        LK_TRY(cudaMemcpyAsync(b, d_b, 6 * sizeof(int), cudaMemcpyDeviceToHost, stream));
         LK_TRY(cudaStreamSynchronize(stream));
         cudaFreeAsync(d_b, stream);
         int r = static_cast<int>(std::ceil(d_max / cell));
@@ -609,9 +611,11 @@ cudaError_t build_grid(GridStorage& g, int kind, const double* d_pos, const doub
         int32_t* d_off = nullptr;
         LK_TRY(cudaMallocAsync(&d_off, (ncells + 1) * sizeof(int32_t), stream));
         LK_TRY(exclusive_scan(d_counts, ncells, d_off, stream));
-        int32_t total = 0;
-        LK_TRY(cudaMemcpyAsync(&total, d_off + ncells, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
+        int32_t* h_total = static_cast<int32_t*>(host_scratch(sizeof(int32_t)));
+        if (!h_total) return cudaErrorMemoryAllocation;
+        LK_TRY(cudaMemcpyAsync(h_total, d_off + ncells, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
         LK_TRY(cudaStreamSynchronize(stream));
+        const int32_t total = *h_total;
         g.nblock = total;
         LK_TRY(pool_alloc(&g.block_info, ncells * sizeof(int2), stream));
         LK_TRY(pool_alloc(&g.block_pts, (total > 0 ? total : 1) * sizeof(double4), stream));

@@ -18,6 +18,30 @@ inline void pool_free(void* p, cudaStream_t s) {
     if (p) cudaFreeAsync(p, s);
 }
 
+// Pinned host scratch for small device->host readbacks (counts, bounding
+// boxes, records), one buffer per host thread. A readback into pageable
+// memory goes through the driver's staging path and queues behind in-flight
+// bulk copies (the other cloud's upload); a pinned one does not.
+inline void* host_scratch(size_t bytes) {
+    struct Buf {
+        void* p = nullptr;
+        size_t cap = 0;
+        ~Buf() {
+            if (p) cudaFreeHost(p);
+        }
+    };
+    thread_local Buf b;
+    if (bytes > b.cap) {
+        if (b.p) cudaFreeHost(b.p);
+        b.p = nullptr;
+        b.cap = 0;
+        const size_t cap = bytes < 65536 ? 65536 : bytes;
+        if (cudaHostAlloc(&b.p, cap, 0) != cudaSuccess) return nullptr;
+        b.cap = cap;
+    }
+    return b.p;
+}
+
 // Dense CSR cell grid over a target cloud.
 //  kind 0 = EvalGrid   (proj/src/registration.cpp:80-148): origin = bbox_lo - cell,
 //           cell = d_max, block radius 1, local cell = floor((y - origin) / cell).
@@ -304,6 +328,11 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
                          cudaStream_t stream);
 
 // Usable (non-zero) normal count and max |p| of a device cloud (synchronous).
+// usable-normal count and max |p| into h_out2 (pinned host, 2 x u64) without
+// waiting; cloud_stats_decode reads them once the stream has synchronised
+cudaError_t cloud_stats_async(const double* d_pos, const double* d_nrm, int64_t n, unsigned long long* h_out2,
+                              cudaStream_t stream);
+void cloud_stats_decode(const unsigned long long* h2, int64_t* usable, double* max_norm);
 cudaError_t cloud_stats(const double* d_pos, const double* d_nrm, int64_t n, int64_t* usable, double* max_norm,
                         cudaStream_t stream);
 

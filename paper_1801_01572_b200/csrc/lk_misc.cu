@@ -115,16 +115,38 @@ __global__ void __launch_bounds__(kFnnThreads) k_fnn_partial(const float4* __res
         __syncthreads();
         for (int q = threadIdx.x; q < tile * (kFnnPad / 4); q += kFnnThreads) s_t[q] = tf[j0 * (kFnnPad / 4) + q];
         __syncthreads();
-        for (int jj = 0; jj < tile; ++jj) {
-            const float d2 = feat_d2f(s, s_t + jj * (kFnnPad / 4));
+        auto take = [&](float d2, int64_t j) {
             if (d2 < f1) {
                 f2 = f1;
                 f1 = d2;
-                j1 = static_cast<int32_t>(j0 + jj);
+                j1 = static_cast<int32_t>(j);
             } else if (d2 < f2) {
                 f2 = d2;
             }
+        };
+        int jj = 0;
+        // four targets at a time, two partial sums each: eight independent
+        // FMA chains (any summation order stays within the 2.2e-6 bound the
+        // near-tie rescan assumes)
+        for (; jj + 4 <= tile; jj += 4) {
+            float a[4][2] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+#pragma unroll
+            for (int q = 0; q < kFnnPad / 4; ++q) {
+                const float4 x = s[q];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const float4 y = s_t[(jj + u) * (kFnnPad / 4) + q];
+                    float d;
+                    d = x.x - y.x; a[u][0] = fmaf(d, d, a[u][0]);
+                    d = x.y - y.y; a[u][1] = fmaf(d, d, a[u][1]);
+                    d = x.z - y.z; a[u][0] = fmaf(d, d, a[u][0]);
+                    d = x.w - y.w; a[u][1] = fmaf(d, d, a[u][1]);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) take(a[u][0] + a[u][1], j0 + jj + u);
         }
+        for (; jj < tile; ++jj) take(feat_d2f(s, s_t + jj * (kFnnPad / 4)), j0 + jj);
     }
     if (i < ns) partial[blockIdx.y * ns + i] = Best3{f1, j1, f2};
 }
@@ -302,7 +324,7 @@ cudaError_t feature_nn(const float* d_sf, int64_t ns, const float* d_tf, int64_t
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t src_blocks = (ns + kFnnThreads - 1) / kFnnThreads;
-    int64_t n_chunks = (2 * sms + src_blocks - 1) / src_blocks;
+    int64_t n_chunks = (8 * sms + src_blocks - 1) / src_blocks;
     if (n_chunks < 1) n_chunks = 1;
     if (n_chunks > (nt + kFnnTile - 1) / kFnnTile) n_chunks = (nt + kFnnTile - 1) / kFnnTile;
     const int64_t chunk = (nt + n_chunks - 1) / n_chunks;

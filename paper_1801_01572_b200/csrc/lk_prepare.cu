@@ -21,6 +21,7 @@
 //             neighbours in ascending order (the reference's summation order)
 #include <cmath>
 #include <cstdint>
+#include <algorithm>
 #include <cstring>
 #include <vector>
 
@@ -341,10 +342,11 @@ __global__ void __launch_bounds__(32 * kSortWarps) k_nbr_brute(const double* __r
                                                                const int4* __restrict__ cells, int64_t n, int rad,
                                                                double r2, int32_t* __restrict__ counts,
                                                                const int32_t* __restrict__ off,
-                                                               int32_t* __restrict__ nbr) {
+                                                               int32_t* __restrict__ nbr, int64_t cap) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t i = blockIdx.x * static_cast<int64_t>(kSortWarps) + warp;
     if (i >= n) return;
+    if (kFill && off[n] > cap) return;  // lists exceed the speculative capacity: the host redoes the fill
     const V3 p = ld3(pos, i);
     const int4 ci = cells[i];
     int32_t o = kFill ? off[i] : 0;
@@ -363,15 +365,62 @@ __global__ void __launch_bounds__(32 * kSortWarps) k_nbr_brute(const double* __r
     if (!kFill && lane == 0) counts[i] = o;
 }
 
+// One pass of k_nbr_brute that counts and keeps the first kNbrSlots
+// neighbours of each point in a fixed-stride table (ascending j); points with
+// more set *overflow (the host then runs the exact two-pass fill).
+constexpr int kNbrSlots = 192;
+
+__global__ void __launch_bounds__(32 * kSortWarps) k_nbr_brute_once(const double* __restrict__ pos,
+                                                                    const int4* __restrict__ cells, int64_t n,
+                                                                    int rad, double r2, int32_t* __restrict__ counts,
+                                                                    int32_t* __restrict__ slots,
+                                                                    int32_t* __restrict__ overflow) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t i = blockIdx.x * static_cast<int64_t>(kSortWarps) + warp;
+    if (i >= n) return;
+    const V3 p = ld3(pos, i);
+    const int4 ci = cells[i];
+    int32_t* row = slots + i * kNbrSlots;
+    int32_t o = 0;
+    for (int64_t b = 0; b < n; b += 32) {
+        const int64_t j = b + lane;
+        bool hit = false;
+        if (j < n && j != i) {
+            const int4 cj = __ldg(cells + j);
+            hit = abs(cj.x - ci.x) <= rad && abs(cj.y - ci.y) <= rad && abs(cj.z - ci.z) <= rad &&
+                  sqnorm(sub(ld3(pos, j), p)) <= r2;
+        }
+        const unsigned m = __ballot_sync(kFull, hit);
+        const int32_t at = o + __popc(m & ((1u << lane) - 1u));
+        if (hit && at < kNbrSlots) row[at] = static_cast<int32_t>(j);
+        o += __popc(m);
+    }
+    if (lane == 0) {
+        counts[i] = o;
+        if (o > kNbrSlots) atomicExch(overflow, 1);
+    }
+}
+
+// fixed-stride table -> CSR at the scanned offsets (warp per point)
+__global__ void k_nbr_compact(const int32_t* __restrict__ slots, const int32_t* __restrict__ off, int64_t n,
+                              const int32_t* __restrict__ overflow, int32_t* __restrict__ nbr, int64_t cap) {
+    const int lane = threadIdx.x & 31;
+    const int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+    if (i >= n || *overflow || off[n] > cap) return;
+    const int32_t o0 = off[i], k = off[i + 1] - o0;
+    for (int a = lane; a < k; a += 32) nbr[o0 + a] = slots[i * kNbrSlots + a];
+}
+
 // warp per point: gather the neighbours (row by row, lanes over slots,
 // ballot-compacted), then sort ascending (radius_search sorts its output)
 __global__ void __launch_bounds__(32 * kSortWarps) k_nbr_fill(const double* __restrict__ pos, int64_t n, GridView g,
                                                               double r2, const int32_t* __restrict__ off,
-                                                              int32_t* __restrict__ nbr) {
+                                                              int32_t* __restrict__ nbr, int64_t cap) {
     __shared__ int32_t s_buf[kSortWarps][kSortCap];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t i = blockIdx.x * static_cast<int64_t>(kSortWarps) + warp;
     if (i >= n) return;
+    if (off[n] > cap) return;  // lists exceed the speculative capacity: the host redoes the fill
     const V3 p = ld3(pos, i);
     const int kx = floor_cell((p.x - g.ox) / g.cell) - g.offx;
     const int ky = floor_cell((p.y - g.oy) / g.cell) - g.offy;
@@ -419,11 +468,13 @@ __global__ void __launch_bounds__(32 * kFpfhWarps) k_spfh(const double* __restri
                                                           const int32_t* __restrict__ off,
                                                           const int32_t* __restrict__ nbr, int32_t* __restrict__ counts,
                                                           int2* __restrict__ deferred, double2* __restrict__ deferred_x,
-                                                          int32_t* __restrict__ n_deferred) {
+                                                          int32_t* __restrict__ n_deferred, int64_t cap,
+                                                          const int32_t* __restrict__ skip) {
     __shared__ int hist[kFpfhWarps][34];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t i = blockIdx.x * static_cast<int64_t>(kFpfhWarps) + warp;
     if (i >= n) return;
+    if (off[n] > cap || (skip && *skip)) return;  // the neighbour lists overflowed: redone by the host
     for (int b = lane; b < 34; b += 32) hist[warp][b] = 0;
     __syncwarp();
     const V3 p = ld3(pos, i), np = ld3(nrm, i);
@@ -626,7 +677,8 @@ cudaError_t voxel_downsample(const double* d_pos, const double* d_nrm, int64_t n
     k_vox_insert<<<nblocks(n, 256), 256, 0, stream>>>(d_pos, n, leaf, keys, table - 1, point_slot, first, count);
     k_vox_mark<<<nblocks(table, 256), 256, 0, stream>>>(keys, first, table, flags);
     LK_TRY(exclusive_scan(flags, n, flag_scan, stream));
-    int32_t host[2] = {0, 0};
+    int32_t* host = static_cast<int32_t*>(host_scratch(2 * sizeof(int32_t)));
+    if (!host) return cudaErrorMemoryAllocation;
     LK_TRY(cudaMemcpyAsync(&host[0], flag_scan + n, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
     LK_TRY(cudaMemcpyAsync(&host[1], bad, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
     LK_TRY(cudaStreamSynchronize(stream));
@@ -678,9 +730,31 @@ cudaError_t voxel_downsample(const double* d_pos, const double* d_nrm, int64_t n
     return cudaGetLastError();
 }
 
+// Pinned host staging of compute_fpfh, one per host thread (each prepare side
+// runs on its own thread): the total neighbour count, the deferred count and
+// the first kStageX deferred pairs come back in one copy; the decisions go
+// back from here. Reused only after the caller's stream has synchronised.
+struct FpfhStage {
+    static constexpr int kStageX = 4096;
+    struct Head {
+        int32_t total, n_def, overflow, pad;
+        double2 x[kStageX];
+    };
+    Head* head = nullptr;
+    uint8_t* dec = nullptr;
+    size_t dec_cap = 0;
+    ~FpfhStage() {
+        if (head) cudaFreeHost(head);
+        if (dec) cudaFreeHost(dec);
+    }
+};
+thread_local FpfhStage t_stage;
+
 cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, double radius, float* d_out,
                          cudaStream_t stream) {
     if (n <= 0) return cudaErrorInvalidValue;
+    FpfhStage& st = t_stage;
+    if (!st.head) LK_TRY(cudaHostAlloc(reinterpret_cast<void**>(&st.head), sizeof(FpfhStage::Head), 0));
     GridStorage g;
     int32_t *counts = nullptr, *off = nullptr, *nbr = nullptr;
     int4* cells = nullptr;
@@ -689,88 +763,133 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
     const bool brute = n <= kBruteMax;
     LK_TRY(cudaMallocAsync(&counts, n * sizeof(int32_t), stream));
     LK_TRY(cudaMallocAsync(&off, (n + 1) * sizeof(int32_t), stream));
+    int32_t *slots = nullptr, *d_overflow = nullptr;
     if (brute) {
-        // SearchGrid(cell = radius): block radius ceil(radius / cell) = 1
+        // SearchGrid(cell = radius): block radius ceil(radius / cell) = 1;
+        // one pass counts and keeps the lists in a fixed-stride table
         LK_TRY(cudaMallocAsync(&cells, n * sizeof(int4), stream));
+        LK_TRY(cudaMallocAsync(&slots, n * kNbrSlots * sizeof(int32_t), stream));
+        LK_TRY(cudaMallocAsync(&d_overflow, sizeof(int32_t), stream));
+        LK_TRY(cudaMemsetAsync(d_overflow, 0, sizeof(int32_t), stream));
         k_search_cells<<<nblocks(n, 256), 256, 0, stream>>>(d_pos, n, radius, cells);
-        k_nbr_brute<false><<<nblocks(n, kSortWarps), 32 * kSortWarps, 0, stream>>>(d_pos, cells, n, 1, r2, counts,
-                                                                                   nullptr, nullptr);
+        k_nbr_brute_once<<<nblocks(n, kSortWarps), 32 * kSortWarps, 0, stream>>>(d_pos, cells, n, 1, r2, counts,
+                                                                                 slots, d_overflow);
     } else {
         LK_TRY(build_grid(g, 1, d_pos, nullptr, n, radius, radius, stream, false));
         k_nbr_count<<<nblocks(n, kSortWarps), 32 * kSortWarps, 0, stream>>>(d_pos, n, g.view, r2, counts);
     }
     LK_TRY(exclusive_scan(counts, n, off, stream));
-    int32_t total = 0;
-    LK_TRY(cudaMemcpyAsync(&total, off + n, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
-    LK_TRY(cudaStreamSynchronize(stream));
-    const int64_t cap = total > 0 ? total : 1;
+    // speculative capacity (no host round trip for the total): 192 neighbours
+    // per point; an overflow turns the fill and the votes into no-ops and is
+    // redone below with the exact size
+    int64_t cap = std::max<int64_t>(192 * n, 4096);
     int32_t *votes = nullptr, *n_def = nullptr;
     int2* deferred = nullptr;
     double2* deferred_x = nullptr;
     uint8_t* d_decision = nullptr;
-    LK_TRY(cudaMallocAsync(&nbr, cap * sizeof(int32_t), stream));
     LK_TRY(cudaMallocAsync(&spfh, 33 * n * sizeof(double), stream));
     LK_TRY(cudaMallocAsync(&votes, 34 * n * sizeof(int32_t), stream));
-    LK_TRY(cudaMallocAsync(&deferred, cap * sizeof(int2), stream));
-    LK_TRY(cudaMallocAsync(&deferred_x, cap * sizeof(double2), stream));
     LK_TRY(cudaMallocAsync(&n_def, sizeof(int32_t), stream));
-    LK_TRY(cudaMemsetAsync(n_def, 0, sizeof(int32_t), stream));
-    if (brute)
-        k_nbr_brute<true><<<nblocks(n, kSortWarps), 32 * kSortWarps, 0, stream>>>(d_pos, cells, n, 1, r2, nullptr, off,
-                                                                                  nbr);
-    else
-        k_nbr_fill<<<nblocks(n, kSortWarps), 32 * kSortWarps, 0, stream>>>(d_pos, n, g.view, r2, off, nbr);
-    k_spfh<<<nblocks(n, kFpfhWarps), 32 * kFpfhWarps, 0, stream>>>(d_pos, d_nrm, n, off, nbr, votes, deferred,
-                                                                   deferred_x, n_def);
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        LK_TRY(cudaMallocAsync(&nbr, cap * sizeof(int32_t), stream));
+        LK_TRY(cudaMallocAsync(&deferred, cap * sizeof(int2), stream));
+        LK_TRY(cudaMallocAsync(&deferred_x, cap * sizeof(double2), stream));
+        LK_TRY(cudaMemsetAsync(n_def, 0, sizeof(int32_t), stream));
+        if (brute && attempt == 0)
+            k_nbr_compact<<<nblocks(32 * n, 256), 256, 0, stream>>>(slots, off, n, d_overflow, nbr, cap);
+        else if (brute)
+            k_nbr_brute<true><<<nblocks(n, kSortWarps), 32 * kSortWarps, 0, stream>>>(d_pos, cells, n, 1, r2, nullptr,
+                                                                                      off, nbr, cap);
+        else
+            k_nbr_fill<<<nblocks(n, kSortWarps), 32 * kSortWarps, 0, stream>>>(d_pos, n, g.view, r2, off, nbr, cap);
+        // an overflowed slot table leaves nbr unfilled: the votes are skipped too
+        k_spfh<<<nblocks(n, kFpfhWarps), 32 * kFpfhWarps, 0, stream>>>(d_pos, d_nrm, n, off, nbr, votes, deferred,
+                                                                       deferred_x, n_def, cap,
+                                                                       (brute && attempt == 0) ? d_overflow : nullptr);
+        // one round trip: total, deferred count and the first deferred pairs
+        LK_TRY(cudaMemcpyAsync(&st.head->total, off + n, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
+        LK_TRY(cudaMemcpyAsync(&st.head->n_def, n_def, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
+        st.head->overflow = 0;
+        if (brute && attempt == 0)
+            LK_TRY(cudaMemcpyAsync(&st.head->overflow, d_overflow, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
+        LK_TRY(cudaMemcpyAsync(st.head->x, deferred_x, FpfhStage::kStageX * sizeof(double2), cudaMemcpyDeviceToHost,
+                               stream));
+        LK_TRY(cudaStreamSynchronize(stream));
+        if (st.head->total <= cap && !st.head->overflow) break;
+        cudaFreeAsync(nbr, stream);
+        cudaFreeAsync(deferred, stream);
+        cudaFreeAsync(deferred_x, stream);
+        cap = std::max<int64_t>(cap, st.head->total);
+    }
     // frame-source tests the device cannot decide: the host's libm decides
     // them exactly as the reference's std::acos comparison (fpfh.cpp:28)
-    int32_t m = 0;
-    LK_TRY(cudaMemcpyAsync(&m, n_def, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
-    LK_TRY(cudaStreamSynchronize(stream));
+    const int32_t m = st.head->n_def;
     if (m > 0) {
-        std::vector<double2> xs(m);
-        std::vector<uint8_t> dec(m);
-        LK_TRY(cudaMemcpyAsync(xs.data(), deferred_x, m * sizeof(double2), cudaMemcpyDeviceToHost, stream));
-        LK_TRY(cudaStreamSynchronize(stream));
+        std::vector<double2> more;
+        const double2* xs = st.head->x;
+        if (m > FpfhStage::kStageX) {
+            more.resize(m);
+            LK_TRY(cudaMemcpyAsync(more.data(), deferred_x, m * sizeof(double2), cudaMemcpyDeviceToHost, stream));
+            LK_TRY(cudaStreamSynchronize(stream));
+            xs = more.data();
+        }
+        if (static_cast<size_t>(m) > st.dec_cap) {
+            if (st.dec) cudaFreeHost(st.dec);
+            st.dec = nullptr;
+            st.dec_cap = 0;
+            LK_TRY(cudaHostAlloc(reinterpret_cast<void**>(&st.dec), m, 0));
+            st.dec_cap = m;
+        }
 #pragma omp parallel for schedule(static) if (m > 4096)
-        for (int32_t k = 0; k < m; ++k) dec[k] = std::acos(xs[k].x) > std::acos(xs[k].y) ? 1 : 0;
+        for (int32_t k = 0; k < m; ++k) st.dec[k] = std::acos(xs[k].x) > std::acos(xs[k].y) ? 1 : 0;
         LK_TRY(cudaMallocAsync(&d_decision, m, stream));
-        LK_TRY(cudaMemcpyAsync(d_decision, dec.data(), m, cudaMemcpyHostToDevice, stream));
+        LK_TRY(cudaMemcpyAsync(d_decision, st.dec, m, cudaMemcpyHostToDevice, stream));
         k_spfh_resolve<<<nblocks(m, 256), 256, 0, stream>>>(d_pos, d_nrm, deferred, d_decision, m, votes);
-        // the host vectors must outlive the async copy
-        LK_TRY(cudaStreamSynchronize(stream));
     }
     k_spfh_scale<<<nblocks(33 * n, 256), 256, 0, stream>>>(votes, n, spfh);
     k_fpfh<<<nblocks(n, kFpfhWarps), 32 * kFpfhWarps, 0, stream>>>(d_pos, d_nrm, n, off, nbr, spfh, d_out);
     LK_TRY(cudaGetLastError());
+    // stream-ordered frees: nothing here waits for the device (the pinned
+    // staging is reused only after the caller synchronises this stream)
     cudaFreeAsync(counts, stream);
     cudaFreeAsync(off, stream);
     cudaFreeAsync(nbr, stream);
     if (cells) cudaFreeAsync(cells, stream);
+    if (slots) cudaFreeAsync(slots, stream);
+    if (d_overflow) cudaFreeAsync(d_overflow, stream);
     cudaFreeAsync(spfh, stream);
     cudaFreeAsync(votes, stream);
     cudaFreeAsync(deferred, stream);
     cudaFreeAsync(deferred_x, stream);
     cudaFreeAsync(n_def, stream);
     if (d_decision) cudaFreeAsync(d_decision, stream);
-    cudaError_t e = cudaStreamSynchronize(stream);
     g.release();
-    return e;
+    return cudaGetLastError();
 }
 
-cudaError_t cloud_stats(const double* d_pos, const double* d_nrm, int64_t n, int64_t* usable, double* max_norm,
-                        cudaStream_t stream) {
+cudaError_t cloud_stats_async(const double* d_pos, const double* d_nrm, int64_t n, unsigned long long* h_out2,
+                              cudaStream_t stream) {
     unsigned long long* d = nullptr;
     LK_TRY(cudaMallocAsync(&d, 2 * sizeof(unsigned long long), stream));
     LK_TRY(cudaMemsetAsync(d, 0, 2 * sizeof(unsigned long long), stream));
     k_cloud_stats<<<nblocks(n, 256) < 64 ? nblocks(n, 256) : 64, 256, 0, stream>>>(d_pos, d_nrm, n, d);
-    unsigned long long h[2] = {0, 0};
-    LK_TRY(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, stream));
+    LK_TRY(cudaMemcpyAsync(h_out2, d, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream));
     cudaFreeAsync(d, stream);
-    LK_TRY(cudaStreamSynchronize(stream));
-    *usable = static_cast<int64_t>(h[0]);
-    const long long bits = static_cast<long long>(h[1]);
+    return cudaGetLastError();
+}
+
+void cloud_stats_decode(const unsigned long long* h2, int64_t* usable, double* max_norm) {
+    *usable = static_cast<int64_t>(h2[0]);
+    const long long bits = static_cast<long long>(h2[1]);
     std::memcpy(max_norm, &bits, sizeof(double));
+}
+
+cudaError_t cloud_stats(const double* d_pos, const double* d_nrm, int64_t n, int64_t* usable, double* max_norm,
+                        cudaStream_t stream) {
+    unsigned long long h[2] = {0, 0};
+    LK_TRY(cloud_stats_async(d_pos, d_nrm, n, h, stream));
+    LK_TRY(cudaStreamSynchronize(stream));
+    cloud_stats_decode(h, usable, max_norm);
     return cudaGetLastError();
 }
 

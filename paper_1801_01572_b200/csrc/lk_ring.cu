@@ -246,8 +246,9 @@ cudaError_t build_ring_grid(RingStorage& rs, const double* d_pos, int64_t n, dou
     const unsigned long long init[6] = {~0ull, ~0ull, ~0ull, 0ull, 0ull, 0ull};
     RG_TRY(cudaMemcpyAsync(keys, init, sizeof(init), cudaMemcpyHostToDevice, stream));
     k_ring_bbox<<<std::min<unsigned>(nblocks(n, 256), 296), 256, 0, stream>>>(d_pos, n, keys);
-    unsigned long long hk[6];
-    RG_TRY(cudaMemcpyAsync(hk, keys, sizeof(hk), cudaMemcpyDeviceToHost, stream));
+    unsigned long long* hk = static_cast<unsigned long long*>(host_scratch(6 * sizeof(unsigned long long)));
+    if (!hk) return cudaErrorMemoryAllocation;
+    RG_TRY(cudaMemcpyAsync(hk, keys, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream));
     RG_TRY(cudaStreamSynchronize(stream));
     cudaFreeAsync(keys, stream);
     double lo[3], hi[3];

@@ -162,6 +162,16 @@ def test_device_prepare_helpers_match_oracle(oracle):
         assert np.array_equal(f, fo)
 
 
+@pytest.mark.parametrize("n,half", [(1500, 0.2), (3000, 1.5)])
+def test_device_fpfh_dense_and_sparse_match_oracle(oracle, n, half):
+    # (1500 points in a 0.4 m box: > 192 neighbours within 0.25 m -- the
+    # slot table overflows and the exact two-pass fill runs) and a sparse cloud
+    c = synth.random_cloud(n, 77, 3, -half, half, with_normals=True)
+    f = lk.compute_fpfh(c, 0.25)
+    fo = oracle.compute_fpfh(c.positions, c.normals, 0.25)
+    assert np.array_equal(f, fo)
+
+
 def test_device_downsample_full_frame_matches_oracle(oracle):
     # 307k-point depth frame: dense voxels (hundreds of points each), zero normals mixed in
     pair = synth.depth_frame_pair()
