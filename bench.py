@@ -162,7 +162,7 @@ def cpu_oracle_registration(pair, hypotheses, seed, budget_s=12.0, min_reps=1, m
     workload until ~budget_s of CPU work; returns the best repetition."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
-    p = O.params(hypothesis_count=hypotheses, seed=seed, threads=0)
+    p = O.params(hypothesis_count=hypotheses, seed=seed, threads=os.cpu_count() or 0)
     best = None
     t_start = time.perf_counter()
     reps = 0
@@ -194,6 +194,8 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0  # N>1: rank 0 alone runs the host baseline
+    # torchrun sets OMP_NUM_THREADS=1 per rank; the baseline uses every host thread
+    os.environ["OMP_NUM_THREADS"] = str(os.cpu_count() or 1)
     pair = make_fixture()
     threads = os.cpu_count()
     times, wref = [], None
@@ -357,11 +359,19 @@ def run_b200(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook: LK_BENCH_ONE_DEVICE=1 runs every rank on cuda:0 over gloo
+    # (exercises the multi-rank path on a single-GPU box; not a bench mode)
+    one_dev = os.environ.get("LK_BENCH_ONE_DEVICE") == "1"
+    if one_dev:
+        local = 0
     if world != args.gpus:
         args.gpus = world
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_dev:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     # a dedicated stream: the library launches on it and the CUDA events are
     # recorded on it (torch's default stream is the legacy NULL stream)
