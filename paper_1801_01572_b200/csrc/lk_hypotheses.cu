@@ -144,7 +144,9 @@ __global__ void __launch_bounds__(256) k_hyp_sample(int64_t begin, int64_t count
 __global__ void __launch_bounds__(128) k_kabsch(const double* __restrict__ spos, const double* __restrict__ tpos,
                                                 const int64_t* __restrict__ surv_index,
                                                 const int32_t* __restrict__ surv_ids, int64_t* __restrict__ cand_index,
-                                                double* __restrict__ cand_rt, Counters* __restrict__ ctr) {
+                                                double* __restrict__ cand_rt, Counters* __restrict__ ctr,
+                                                double* __restrict__ u_sum = nullptr,
+                                                unsigned* __restrict__ u_done = nullptr, int64_t u_cap = 0) {
     const int64_t n = static_cast<int64_t>(ctr->n_survivors);
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     const int64_t rounds = (n + stride - 1) / stride;
@@ -164,6 +166,10 @@ __global__ void __launch_bounds__(128) k_kabsch(const double* __restrict__ spos,
         unsigned deg = __ballot_sync(kFull, live && !ok);
         if ((threadIdx.x & 31) == 0 && deg) atomicAdd(&ctr->degenerate, static_cast<unsigned long long>(__popc(deg)));
         if (ok) {
+            if (static_cast<int64_t>(slot) < u_cap) {  // the unit scorer's per-candidate sum and unit count
+                u_sum[slot] = 0.0;
+                u_done[slot] = 0u;
+            }
             cand_index[slot] = surv_index[j];
             double* o = cand_rt + 12 * slot;
 #pragma unroll
@@ -567,8 +573,9 @@ __global__ void __launch_bounds__(kScoreThreads) k_score(SourceView src, GridVie
 }
 
 __global__ void k_prep_fast_fine(const double* __restrict__ cand_rt, const Counters* __restrict__ ctr, GridView g,
-                                 ScoreParams sp, FastRT* __restrict__ out) {
-    const int64_t n = static_cast<int64_t>(ctr->n_candidates);
+                                 ScoreParams sp, FastRT* __restrict__ out, int64_t cap = INT64_MAX) {
+    const int64_t n_all = static_cast<int64_t>(ctr->n_candidates);
+    const int64_t n = n_all < cap ? n_all : cap;
     for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
          k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         double R[9], t[3];
@@ -1343,19 +1350,111 @@ __device__ double cta_chain(const uint32_t* im, const double* ad, int32_t n_chun
     return sum;
 }
 
-__global__ void __launch_bounds__(kCtaThreads, 4) k_score_cta(SourceView src, const __grid_constant__ GridView g,
-                                                               const __grid_constant__ ScoreParams sp,
-                                                               const double* __restrict__ cand_rt,
-                                                               const int64_t* __restrict__ cand_index,
-                                                               int64_t sampled, int64_t ns_pad,
-                                                               double* __restrict__ scr_add,
-                                                               uint32_t* __restrict__ scr_inl,
-                                                               Counters* __restrict__ ctr,
-                                                               BestRec* __restrict__ block_best,
-                                                               RecordDev* __restrict__ rec) {
-    __shared__ CtaSmem S;
+// Phases A and B of one round of kCtaPts points starting at `base` for the
+// candidate staged in S (R, t, Rf, F): FP32 location, the shared-memory queue
+// and its dense FP64-exact resolution. Leaves the round's ballots in S.inl[b] /
+// S.miss[b], the inliers' d2 in add[i] and their (any-order) sum in `part`;
+// clears the other parity's ballots; ends with a block barrier.
+__device__ __forceinline__ void score_round_ab(CtaSmem& S, const SourceView& src, const GridView& g,
+                                               const ScoreParams& sp, const double* cand_rt_c, int64_t base, int b,
+                                               int64_t ns, double* __restrict__ add, double& part) {
+    const int lane = threadIdx.x & 31;
+    const FastRT& F = S.F;
+    // A. FP32 location of the round's points
+#pragma unroll
+    for (int u = 0; u < kCtaPer; ++u) {
+        const int local = u * kCtaThreads + threadIdx.x;
+        const int64_t i = base + local;
+        int state = 0;  // 0 certain miss, 1 exact fallback, 2 fine-list scan
+        int2 bi = make_int2(0, 0);
+        if (i < ns) {
+            if (F.ok == 0.0f) {
+                state = 1;
+            } else {
+                const float4 P = __ldg(src.pos32 + i);
+                const float qx = fmaf(F.r[0], P.x, fmaf(F.r[1], P.y, fmaf(F.r[2], P.z, F.t[0])));
+                const float qy = fmaf(F.r[3], P.x, fmaf(F.r[4], P.y, fmaf(F.r[5], P.z, F.t[1])));
+                const float qz = fmaf(F.r[6], P.x, fmaf(F.r[7], P.y, fmaf(F.r[8], P.z, F.t[2])));
+                const float eps = F.eps;
+                if (!(qx < -eps || qy < -eps || qz < -eps || qx >= g.fnx + eps || qy >= g.fny + eps ||
+                      qz >= g.fnz + eps)) {
+                    const float fx = floorf(qx), fy = floorf(qy), fz = floorf(qz);
+                    const float rx = qx - fx, ry = qy - fy, rz = qz - fz;
+                    if (rx < eps || rx > 1.0f - eps || ry < eps || ry > 1.0f - eps || rz < eps ||
+                        rz > 1.0f - eps) {
+                        state = 1;
+                    } else {
+                        const int ix = static_cast<int>(fx), iy = static_cast<int>(fy),
+                                  iz = static_cast<int>(fz);
+                        if (ix >= 0 && iy >= 0 && iz >= 0 && ix < g.fnx && iy < g.fny && iz < g.fnz) {
+                            bi = __ldg(g.fine_info + (static_cast<int64_t>(ix) * g.fny + iy) * g.fnz + iz);
+                            if (bi.y > 0) state = bi.y < kCtaSlow ? 2 : 1;
+                        }
+                    }
+                }
+            }
+        }
+        const unsigned mm = __ballot_sync(kFull, i < ns && state == 0);
+        if (lane == 0) S.miss[b][local >> 5] = mm;
+        const unsigned m = __ballot_sync(kFull, state != 0);
+        int slot = 0;
+        if (m) {
+            const int leader = __ffs(m) - 1;
+            if (lane == leader) slot = atomicAdd(&S.nq, __popc(m));
+            slot = __shfl_sync(kFull, slot, leader) + __popc(m & ((1u << lane) - 1u));
+        }
+        if (state != 0) S.q[slot] = make_int2(local | ((state == 1 ? kCtaSlow : bi.y) << 16), bi.x);
+    }
+    __syncthreads();
+    // B. dense resolution of the queue; the next round's ballots are cleared
+    const int nq = S.nq;
+    if (threadIdx.x < kCtaWords) {
+        S.inl[b ^ 1][threadIdx.x] = 0u;
+        S.miss[b ^ 1][threadIdx.x] = 0u;
+    }
+    for (int e = threadIdx.x; e < nq; e += kCtaThreads) {
+        const int2 qe = S.q[e];
+        const int local = qe.x & 0xffff;
+        const int cnt = static_cast<int>(static_cast<unsigned>(qe.x) >> 16);
+        const int64_t i = base + local;
+        double addend = 0.0;
+        bool inl;
+        if (cnt == kCtaSlow) {
+            inl = eval_point_slow(g, cand_rt_c, src, i, sp, &addend);
+        } else {
+            const float4 P = __ldg(src.pos32 + i);
+            const float qx = fmaf(F.r[0], P.x, fmaf(F.r[1], P.y, fmaf(F.r[2], P.z, F.t[0])));
+            const float qy = fmaf(F.r[3], P.x, fmaf(F.r[4], P.y, fmaf(F.r[5], P.z, F.t[1])));
+            const float qz = fmaf(F.r[6], P.x, fmaf(F.r[7], P.y, fmaf(F.r[8], P.z, F.t[2])));
+            const bool rec = src.pos4 != nullptr && src.nrm32 != nullptr;
+            const V3 p = rec ? ld4(src.pos4, i) : ld3(src.pos, i);
+            const float4 n32 = rec ? __ldg(src.nrm32 + i) : make_float4(0, 0, 0, 0);
+            inl = resolve_fine(g, S.R, S.t, rec ? S.Rf : nullptr, F, src, i, p, n32, qx, qy, qz, qe.y, cnt,
+                               sp, addend);
+        }
+        const int word = local >> 5;  // ballot word w covers points base + 32 w ..
+        const uint32_t bit = 1u << (local & 31);
+        if (inl) {
+            atomicOr(&S.inl[b][word], bit);
+            add[i] = addend;
+            part += addend;
+        } else {
+            atomicOr(&S.miss[b][word], bit);
+        }
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ void cta_body(CtaSmem& S, const SourceView& src, const GridView& g, const ScoreParams& sp,
+                                         const double* __restrict__ cand_rt, const int64_t* __restrict__ cand_index,
+                                         int64_t sampled, int64_t ns_pad, double* __restrict__ scr_add,
+                                         uint32_t* __restrict__ scr_inl, Counters* __restrict__ ctr,
+                                         BestRec* __restrict__ block_best, RecordDev* __restrict__ rec,
+                                         int64_t unit_cap, int64_t unit_threshold, int n_prev_best) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t n_cand = static_cast<int64_t>(ctr->n_candidates);
+    // the candidates k_score_units did not take (same rule as there)
+    const int64_t cand_begin = n_cand >= unit_threshold ? 0 : (n_cand < unit_cap ? n_cand : unit_cap);
     const int64_t ns = src.n;
     const int32_t n_chunks = static_cast<int32_t>(ns_pad / 32);
     // the CTA's two scratch slots: addends (ns_pad) and ballot words (n_chunks)
@@ -1369,7 +1468,7 @@ __global__ void __launch_bounds__(kCtaThreads, 4) k_score_cta(SourceView src, co
     double best_eb = 0.0;
     unsigned long long t_qual = 0, t_wref = 0, t_exec = 0;
     for (;;) {
-        if (threadIdx.x == 0) S.cand = static_cast<int64_t>(atomicAdd(&ctr->work_next, 1ull));
+        if (threadIdx.x == 0) S.cand = cand_begin + static_cast<int64_t>(atomicAdd(&ctr->work_next2, 1ull));
         if (threadIdx.x < 2 * kCtaWords) {
             (&S.inl[0][0])[threadIdx.x] = 0u;
             (&S.miss[0][0])[threadIdx.x] = 0u;
@@ -1392,7 +1491,6 @@ __global__ void __launch_bounds__(kCtaThreads, 4) k_score_cta(SourceView src, co
             S.nq = 0;
         }
         __syncthreads();
-        const FastRT& F = S.F;
         double* add = slot_add[cur];
         uint32_t* inlw = slot_inl[cur];
         double part = 0.0;
@@ -1400,89 +1498,7 @@ __global__ void __launch_bounds__(kCtaThreads, 4) k_score_cta(SourceView src, co
         bool exited = false;
         for (int64_t base = 0, r = 0; base < ns; base += kCtaPts, ++r) {
             const int b = static_cast<int>(r & 1);
-            // A. FP32 location of the round's points
-#pragma unroll
-            for (int u = 0; u < kCtaPer; ++u) {
-                const int local = u * kCtaThreads + threadIdx.x;
-                const int64_t i = base + local;
-                int state = 0;  // 0 certain miss, 1 exact fallback, 2 fine-list scan
-                int2 bi = make_int2(0, 0);
-                if (i < ns) {
-                    if (F.ok == 0.0f) {
-                        state = 1;
-                    } else {
-                        const float4 P = __ldg(src.pos32 + i);
-                        const float qx = fmaf(F.r[0], P.x, fmaf(F.r[1], P.y, fmaf(F.r[2], P.z, F.t[0])));
-                        const float qy = fmaf(F.r[3], P.x, fmaf(F.r[4], P.y, fmaf(F.r[5], P.z, F.t[1])));
-                        const float qz = fmaf(F.r[6], P.x, fmaf(F.r[7], P.y, fmaf(F.r[8], P.z, F.t[2])));
-                        const float eps = F.eps;
-                        if (!(qx < -eps || qy < -eps || qz < -eps || qx >= g.fnx + eps || qy >= g.fny + eps ||
-                              qz >= g.fnz + eps)) {
-                            const float fx = floorf(qx), fy = floorf(qy), fz = floorf(qz);
-                            const float rx = qx - fx, ry = qy - fy, rz = qz - fz;
-                            if (rx < eps || rx > 1.0f - eps || ry < eps || ry > 1.0f - eps || rz < eps ||
-                                rz > 1.0f - eps) {
-                                state = 1;
-                            } else {
-                                const int ix = static_cast<int>(fx), iy = static_cast<int>(fy),
-                                          iz = static_cast<int>(fz);
-                                if (ix >= 0 && iy >= 0 && iz >= 0 && ix < g.fnx && iy < g.fny && iz < g.fnz) {
-                                    bi = __ldg(g.fine_info + (static_cast<int64_t>(ix) * g.fny + iy) * g.fnz + iz);
-                                    if (bi.y > 0) state = bi.y < kCtaSlow ? 2 : 1;
-                                }
-                            }
-                        }
-                    }
-                }
-                const unsigned mm = __ballot_sync(kFull, i < ns && state == 0);
-                if (lane == 0) S.miss[b][local >> 5] = mm;
-                const unsigned m = __ballot_sync(kFull, state != 0);
-                int slot = 0;
-                if (m) {
-                    const int leader = __ffs(m) - 1;
-                    if (lane == leader) slot = atomicAdd(&S.nq, __popc(m));
-                    slot = __shfl_sync(kFull, slot, leader) + __popc(m & ((1u << lane) - 1u));
-                }
-                if (state != 0) S.q[slot] = make_int2(local | ((state == 1 ? kCtaSlow : bi.y) << 16), bi.x);
-            }
-            __syncthreads();
-            // B. dense resolution of the queue; the next round's ballots are cleared
-            const int nq = S.nq;
-            if (threadIdx.x < kCtaWords) {
-                S.inl[b ^ 1][threadIdx.x] = 0u;
-                S.miss[b ^ 1][threadIdx.x] = 0u;
-            }
-            for (int e = threadIdx.x; e < nq; e += kCtaThreads) {
-                const int2 qe = S.q[e];
-                const int local = qe.x & 0xffff;
-                const int cnt = static_cast<int>(static_cast<unsigned>(qe.x) >> 16);
-                const int64_t i = base + local;
-                double addend = 0.0;
-                bool inl;
-                if (cnt == kCtaSlow) {
-                    inl = eval_point_slow(g, cand_rt + 12 * cand, src, i, sp, &addend);
-                } else {
-                    const float4 P = __ldg(src.pos32 + i);
-                    const float qx = fmaf(F.r[0], P.x, fmaf(F.r[1], P.y, fmaf(F.r[2], P.z, F.t[0])));
-                    const float qy = fmaf(F.r[3], P.x, fmaf(F.r[4], P.y, fmaf(F.r[5], P.z, F.t[1])));
-                    const float qz = fmaf(F.r[6], P.x, fmaf(F.r[7], P.y, fmaf(F.r[8], P.z, F.t[2])));
-                    const bool rec = src.pos4 != nullptr && src.nrm32 != nullptr;
-                    const V3 p = rec ? ld4(src.pos4, i) : ld3(src.pos, i);
-                    const float4 n32 = rec ? __ldg(src.nrm32 + i) : make_float4(0, 0, 0, 0);
-                    inl = resolve_fine(g, S.R, S.t, rec ? S.Rf : nullptr, F, src, i, p, n32, qx, qy, qz, qe.y, cnt,
-                                       sp, addend);
-                }
-                const int word = local >> 5;  // ballot word w covers points base + 32 w ..
-                const uint32_t bit = 1u << (local & 31);
-                if (inl) {
-                    atomicOr(&S.inl[b][word], bit);
-                    add[i] = addend;
-                    part += addend;
-                } else {
-                    atomicOr(&S.miss[b][word], bit);
-                }
-            }
-            __syncthreads();
+            score_round_ab(S, src, g, sp, cand_rt + 12 * cand, base, b, ns, add, part);
             // C. the miss budget in point order (word w covers points base + 32 w ..)
             if (threadIdx.x == 0) S.nq = 0;
             const uint32_t m0 = S.miss[b][lane], m1 = kCtaWords > 32 ? S.miss[b][(32 + lane) % kCtaWords] : 0u;
@@ -1616,15 +1632,16 @@ __global__ void __launch_bounds__(kCtaThreads, 4) k_score_cta(SourceView src, co
         if (t_qual) atomicAdd(&ctr->qualified, t_qual);
         if (t_wref) atomicAdd(&ctr->w_ref, t_wref);
         if (t_exec) atomicAdd(&ctr->evals_executed, t_exec);
-        block_best[blockIdx.x] = best;
+        block_best[n_prev_best + blockIdx.x] = best;
         __threadfence();
         s_ticket = atomicAdd(&ctr->fin_done, 1ull);
     }
     __syncthreads();
     if (s_ticket != gridDim.x - 1) return;
     __threadfence();
+    // every CTA best: the unit scorer's (before) and this kernel's
     BestRec b{0, 0, 0.0, INT64_MAX, -1};
-    for (int i = threadIdx.x; i < static_cast<int>(gridDim.x); i += blockDim.x) {
+    for (int i = threadIdx.x; i < n_prev_best + static_cast<int>(gridDim.x); i += blockDim.x) {
         BestRec c;
         c.valid = __ldcg(&block_best[i].valid);
         c.inliers = __ldcg(&block_best[i].inliers);
@@ -1664,6 +1681,256 @@ __global__ void __launch_bounds__(kCtaThreads, 4) k_score_cta(SourceView src, co
     r.w_ref = static_cast<int64_t>(__ldcg(&ctr->w_ref));
     r.evals_executed = static_cast<int64_t>(__ldcg(&ctr->evals_executed));
     *rec = r;
+}
+
+// ---- round-unit scoring ----------------------------------------------------
+// Work unit = (candidate, round of kCtaPts points), taken candidate-major from
+// a ticket counter by a persistent grid, so a heavy candidate (nearly every
+// point pending) spreads over many CTAs instead of serialising on one -- the
+// balance that strong scaling over ranks needs. A unit runs phases A and B of
+// the candidate-CTA scorer, then publishes its ballots (per candidate, per
+// 32-point word), its inliers' d2 and its partial sum (atomic, any order). The
+// CTA that completes a candidate's last unit applies the miss budget in point
+// order over the published ballots (exit => the reference's visit count), and
+// decides qualification and the comparison with its CTA best by the order
+// bound, running the reference's sequential sum (registration.cpp:206) on
+// demand; every CTA best ends exact (registration.cpp:272-276). Candidates
+// beyond the scratch capacity go to k_score_cta, which writes the record.
+__device__ __forceinline__ void units_body(CtaSmem& S, const SourceView& src, const GridView& g,
+                                           const ScoreParams& sp, const double* __restrict__ cand_rt,
+                                           const int64_t* __restrict__ cand_index, int64_t cap, int64_t ns_pad,
+                                           uint32_t* __restrict__ u_miss, uint32_t* __restrict__ u_inl,
+                                           double* __restrict__ u_add, double* __restrict__ u_sum,
+                                           unsigned* __restrict__ u_done, Counters* __restrict__ ctr,
+                                           BestRec* __restrict__ block_best, int64_t unit_threshold) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t n_all = static_cast<int64_t>(ctr->n_candidates);
+    // units only pay when candidates are too few to keep a CTA each busy
+    // (strong scaling over ranks); otherwise k_score_cta takes them all
+    const int64_t n_cand = n_all >= unit_threshold ? 0 : (n_all < cap ? n_all : cap);
+    const int64_t ns = src.n;
+    const int32_t n_chunks = static_cast<int32_t>(ns_pad / 32);
+    const int64_t R = (ns + kCtaPts - 1) / kCtaPts;
+    const int64_t n_units = n_cand * R;
+    // thread 0's books: the CTA best (fitness exact when best_eb == 0)
+    BestRec best{0, 0, 0.0, INT64_MAX, -1};
+    double best_eb = 0.0;
+    unsigned long long t_qual = 0, t_wref = 0, t_exec = 0;
+    for (;;) {
+        if (threadIdx.x == 0) {
+            S.cand = static_cast<int64_t>(atomicAdd(&ctr->work_next, 1ull));
+            S.nq = 0;
+        }
+        if (threadIdx.x < kCtaWords) {
+            S.inl[0][threadIdx.x] = 0u;
+            S.miss[0][threadIdx.x] = 0u;
+        }
+        __syncthreads();
+        const int64_t u = S.cand;
+        if (u >= n_units) break;
+        const int64_t c = u / R;
+        const int64_t base = (u - c * R) * kCtaPts;
+        if (threadIdx.x < 12) {
+            const double v = __ldg(cand_rt + 12 * c + threadIdx.x);
+            if (threadIdx.x < 9) {
+                S.R[threadIdx.x] = v;
+                S.Rf[threadIdx.x] = static_cast<float>(v);
+            } else {
+                S.t[threadIdx.x - 9] = v;
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) S.F = make_fast_fine(S.R, S.t, g, sp);
+        __syncthreads();
+        double part = 0.0;
+        double* add = u_add + c * ns_pad;
+        score_round_ab(S, src, g, sp, cand_rt + 12 * c, base, 0, ns, add, part);
+        // publish the round: ballots, the partial sum, then the unit count
+        const int32_t w0 = static_cast<int32_t>(base / 32);
+        if (threadIdx.x < kCtaWords && w0 + static_cast<int32_t>(threadIdx.x) < n_chunks) {
+            u_miss[c * n_chunks + w0 + threadIdx.x] = S.miss[0][threadIdx.x];
+            u_inl[c * n_chunks + w0 + threadIdx.x] = S.inl[0][threadIdx.x];
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(kFull, part, o);
+        if (lane == 0) S.red[warp] = part;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double sum = 0.0;
+            for (int w = 0; w < kCtaWarps; ++w) sum += S.red[w];
+            if (sum != 0.0) atomicAdd(u_sum + c, sum);
+        }
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) S.flag = atomicAdd(u_done + c, 1u) == static_cast<unsigned>(R - 1) ? 1 : 0;
+        __syncthreads();
+        if (!S.flag) continue;
+        // ---- the candidate's last unit: its verdict
+        __threadfence();
+        const uint32_t* mw_c = u_miss + c * n_chunks;
+        const uint32_t* iw_c = u_inl + c * n_chunks;
+        if (warp == 0) {
+            int64_t misses = 0, visited = ns;
+            unsigned pop = 0;
+            bool exited = false;
+            for (int32_t s0 = 0; s0 < n_chunks; s0 += 32) {
+                const int32_t w = s0 + lane;
+                const uint32_t mw = w < n_chunks ? __ldcg(mw_c + w) : 0u;
+                pop += w < n_chunks ? __popc(__ldcg(iw_c + w)) : 0u;
+                if (exited) continue;
+                const int cnt = __popc(mw);
+                int incl = cnt;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(kFull, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                const unsigned over = __ballot_sync(kFull, misses + incl > sp.miss_budget);
+                if (over) {
+                    const int L = __ffs(over) - 1;
+                    const int64_t before = misses + __shfl_sync(kFull, incl - cnt, L);
+                    unsigned m = __shfl_sync(kFull, mw, L);
+                    const int need = static_cast<int>(sp.miss_budget - before);
+                    for (int q = 0; q < need; ++q) m &= m - 1;
+                    visited = static_cast<int64_t>(s0 + L) * 32 + (__ffs(m) - 1) + 1;
+                    exited = true;
+                }
+                misses += __shfl_sync(kFull, incl, 31);
+            }
+            const int64_t inliers = static_cast<int64_t>(__reduce_add_sync(kFull, pop));
+            if (lane == 0) {
+                S.exact[0] = static_cast<double>(visited);
+                S.exact[1] = static_cast<double>(inliers);
+                S.swap = exited ? 1 : 0;
+            }
+        }
+        __syncthreads();
+        const bool exited = S.swap != 0;
+        const int64_t visited = static_cast<int64_t>(S.exact[0]);
+        const int64_t inliers = static_cast<int64_t>(S.exact[1]);
+        int need = 0;  // bit 0: chain the candidate, bit 1: chain the best, bit 4: a qualifying verdict
+        double fit = 0.0, eb = 0.0;
+        bool qual_sure = false;
+        if (threadIdx.x == 0) {
+            t_wref += static_cast<unsigned long long>(visited);
+            t_exec += static_cast<unsigned long long>(ns);
+            if (!exited) {
+                const double ratio = static_cast<double>(inliers) / static_cast<double>(ns);
+                if (!(ratio < sp.min_ratio)) {
+                    const double s = __ldcg(u_sum + c);
+                    fit = inliers > 0 ? s / static_cast<double>(inliers) : 0.0;
+                    eb = inliers > 0 ? order_bound(inliers) * fit : 0.0;
+                    const bool may = !(fit - eb > sp.max_fitness);
+                    qual_sure = fit + eb <= sp.max_fitness;
+                    if (may) {
+                        need |= 16;
+                        if (!qual_sure) need |= 1;
+                        if (best.valid && inliers == best.inliers && fabs(fit - best.fitness) <= eb + best_eb) {
+                            need |= 1;
+                            if (best_eb != 0.0) need |= 2;
+                        }
+                    }
+                }
+            }
+            S.flag = need;
+        }
+        __syncthreads();
+        need = S.flag;
+        if (need & 1) {
+            const double s = cta_chain(iw_c, u_add + c * ns_pad, n_chunks, S);
+            if (threadIdx.x == 0) S.exact[0] = s;
+        }
+        if (need & 2) {
+            const double s = cta_chain(u_inl + best.slot * n_chunks, u_add + best.slot * ns_pad, n_chunks, S);
+            if (threadIdx.x == 0) S.exact[1] = s;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && (need & 16)) {
+            if (need & 2) {
+                best.fitness = S.exact[1] / static_cast<double>(best.inliers);
+                best_eb = 0.0;
+            }
+            bool qual = qual_sure;
+            if (need & 1) {
+                fit = S.exact[0] / static_cast<double>(inliers);
+                eb = 0.0;
+                qual = !(fit > sp.max_fitness);
+            }
+            if (qual) {
+                t_qual += 1;
+                const BestRec cb{1, inliers, fit, __ldg(cand_index + c), c};
+                bool take;
+                if (!best.valid || inliers != best.inliers) take = !best.valid || inliers > best.inliers;
+                else if (eb == 0.0 && best_eb == 0.0) take = better(cb, best);
+                else take = fit < best.fitness;  // bounds disjoint (else both were chained)
+                if (take) {
+                    best = cb;
+                    best_eb = eb;
+                }
+            }
+        }
+        __syncthreads();
+    }
+    // the CTA best's exact sum (its scratch rows persist)
+    if (threadIdx.x == 0) {
+        S.flag = (best.valid && best_eb != 0.0) ? 1 : 0;
+        S.cand = best.slot;
+    }
+    __syncthreads();
+    if (S.flag) {
+        const int64_t bs = S.cand;
+        const double s = cta_chain(u_inl + bs * n_chunks, u_add + bs * ns_pad, n_chunks, S);
+        if (threadIdx.x == 0) best.fitness = s / static_cast<double>(best.inliers);
+    }
+    if (threadIdx.x == 0) {
+        if (t_qual) atomicAdd(&ctr->qualified, t_qual);
+        if (t_wref) atomicAdd(&ctr->w_ref, t_wref);
+        if (t_exec) atomicAdd(&ctr->evals_executed, t_exec);
+        block_best[blockIdx.x] = best;
+    }
+}
+
+// The scorer of run_hypotheses, two launches: k_score_units takes round units
+// while the candidates are too few to keep a CTA each busy (a rank's share
+// under strong scaling) and exits at once otherwise; k_score_cta then takes
+// one CTA per candidate for the rest and writes the rank record. Separate
+// kernels keep each body's register allocation.
+__global__ void __launch_bounds__(kCtaThreads, 4) k_score_units(SourceView src, const __grid_constant__ GridView g,
+                                                                 const __grid_constant__ ScoreParams sp,
+                                                                 const double* __restrict__ cand_rt,
+                                                                 const int64_t* __restrict__ cand_index,
+                                                                 int64_t unit_cap, int64_t unit_ns_pad,
+                                                                 uint32_t* __restrict__ u_miss,
+                                                                 uint32_t* __restrict__ u_inl,
+                                                                 double* __restrict__ u_add,
+                                                                 double* __restrict__ u_sum,
+                                                                 unsigned* __restrict__ u_done,
+                                                                 Counters* __restrict__ ctr,
+                                                                 BestRec* __restrict__ block_best,
+                                                                 int64_t unit_threshold) {
+    __shared__ CtaSmem S;
+    if (static_cast<int64_t>(ctr->n_candidates) >= unit_threshold) {
+        if (threadIdx.x == 0) block_best[blockIdx.x] = BestRec{0, 0, 0.0, INT64_MAX, -1};
+        return;
+    }
+    units_body(S, src, g, sp, cand_rt, cand_index, unit_cap, unit_ns_pad, u_miss, u_inl, u_add, u_sum, u_done, ctr,
+               block_best, unit_threshold);
+}
+
+__global__ void __launch_bounds__(kCtaThreads, 4) k_score_cta(SourceView src, const __grid_constant__ GridView g,
+                                                               const __grid_constant__ ScoreParams sp,
+                                                               const double* __restrict__ cand_rt,
+                                                               const int64_t* __restrict__ cand_index,
+                                                               int64_t sampled, int64_t cta_ns_pad,
+                                                               double* __restrict__ scr_add,
+                                                               uint32_t* __restrict__ scr_inl, int64_t unit_cap,
+                                                               Counters* __restrict__ ctr,
+                                                               BestRec* __restrict__ block_best,
+                                                               RecordDev* __restrict__ rec, int64_t unit_threshold,
+                                                               int n_unit_best) {
+    __shared__ CtaSmem S;
+    cta_body(S, src, g, sp, cand_rt, cand_index, sampled, cta_ns_pad, scr_add, scr_inl, ctr, block_best, rec,
+             unit_cap, unit_threshold, n_unit_best);
 }
 
 int blocks_per_sm(const void* fn) {
@@ -1725,6 +1992,15 @@ void RunBuffers::release() {
     pool_free(queue_counts, stream);
     pool_free(cta_add, stream);
     pool_free(cta_inl, stream);
+    pool_free(u_miss, stream);
+    pool_free(u_inl, stream);
+    pool_free(u_add, stream);
+    pool_free(u_sum, stream);
+    pool_free(u_done, stream);
+    u_miss = u_inl = nullptr;
+    u_add = u_sum = nullptr;
+    u_done = nullptr;
+    u_cap = u_ns_pad = 0;
     cta_add = nullptr;
     cta_inl = nullptr;
     cta_slots = 0;
@@ -1782,6 +2058,15 @@ cudaError_t RunBuffers::ensure_cta(int64_t ns, int32_t n_ctas) {
     if (n_ctas <= cta_slots && ns_pad == cta_ns_pad) return cudaSuccess;
     pool_free(cta_add, stream);
     pool_free(cta_inl, stream);
+    pool_free(u_miss, stream);
+    pool_free(u_inl, stream);
+    pool_free(u_add, stream);
+    pool_free(u_sum, stream);
+    pool_free(u_done, stream);
+    u_miss = u_inl = nullptr;
+    u_add = u_sum = nullptr;
+    u_done = nullptr;
+    u_cap = u_ns_pad = 0;
     cta_add = nullptr;
     cta_inl = nullptr;
     cta_slots = 0;
@@ -1793,6 +2078,30 @@ cudaError_t RunBuffers::ensure_cta(int64_t ns, int32_t n_ctas) {
         return e;
     cta_slots = n_ctas;
     cta_ns_pad = ns_pad;
+    return cudaSuccess;
+}
+
+cudaError_t RunBuffers::ensure_units(int64_t ns, int64_t cap) {
+    const int64_t ns_pad = (ns + 31) / 32 * 32;
+    if (cap <= u_cap && ns_pad == u_ns_pad) return cudaSuccess;
+    pool_free(u_miss, stream);
+    pool_free(u_inl, stream);
+    pool_free(u_add, stream);
+    pool_free(u_sum, stream);
+    pool_free(u_done, stream);
+    u_miss = u_inl = nullptr;
+    u_add = u_sum = nullptr;
+    u_done = nullptr;
+    u_cap = 0;
+    const int64_t words = cap * (ns_pad / 32);
+    cudaError_t e;
+    if ((e = pool_alloc(&u_miss, words * sizeof(uint32_t), stream)) != cudaSuccess) return e;
+    if ((e = pool_alloc(&u_inl, words * sizeof(uint32_t), stream)) != cudaSuccess) return e;
+    if ((e = pool_alloc(&u_add, cap * ns_pad * sizeof(double), stream)) != cudaSuccess) return e;
+    if ((e = pool_alloc(&u_sum, cap * sizeof(double), stream)) != cudaSuccess) return e;
+    if ((e = pool_alloc(&u_done, cap * sizeof(unsigned), stream)) != cudaSuccess) return e;
+    u_cap = cap;
+    u_ns_pad = ns_pad;
     return cudaSuccess;
 }
 
@@ -1857,7 +2166,7 @@ cudaError_t run_hypotheses_range(const SourceView& src, const double* d_tgt_pos,
     const int over_blocks = sm_count;
     const int cand_blocks = sm_count * cand_blocks_per_sm();
     const int n_best_slots = exit_blocks + over_blocks + kFinalCtas;
-    cudaError_t e = rb.ensure(count > 0 ? count : 1, n_best_slots > cand_blocks ? n_best_slots : cand_blocks);
+    cudaError_t e = rb.ensure(count > 0 ? count : 1, n_best_slots > 2 * cand_blocks ? n_best_slots : 2 * cand_blocks);
     if (e != cudaSuccess) return e;
     const bool split = split_scoring();
     if (split) {
@@ -1870,8 +2179,14 @@ cudaError_t run_hypotheses_range(const SourceView& src, const double* d_tgt_pos,
         if ((e = cudaMemsetAsync(rb.queue_counts, 0, kQueueParts * kQueueStride * sizeof(unsigned long long),
                                  stream)) != cudaSuccess)
             return e;
-    } else if ((e = rb.ensure_cta(src.n, cand_blocks)) != cudaSuccess) {
-        return e;
+    } else {
+        if ((e = rb.ensure_cta(src.n, cand_blocks)) != cudaSuccess) return e;
+        // unit scratch: a few percent of the hypotheses survive; at most 2 GiB of addends
+        const int64_t ns_pad = (src.n + 31) / 32 * 32;
+        int64_t ucap = count / 64 > 4096 ? count / 64 : 4096;
+        const int64_t byte_cap = (int64_t(2) << 30) / (ns_pad * static_cast<int64_t>(sizeof(double)));
+        if (ucap > byte_cap) ucap = byte_cap > 1 ? byte_cap : 1;
+        if ((e = rb.ensure_units(src.n, ucap)) != cudaSuccess) return e;
     }
     FastRT* cand_fast = static_cast<FastRT*>(rb.cand_fast);
     if ((e = cudaMemsetAsync(rb.counters, 0, sizeof(Counters), stream)) != cudaSuccess) return e;
@@ -1908,15 +2223,27 @@ cudaError_t run_hypotheses_range(const SourceView& src, const double* d_tgt_pos,
     if (events) cudaEventRecord(events[1], stream);
     if (count > 0) {
         k_kabsch<<<sm_count * 8, 128, 0, stream>>>(src.pos, d_tgt_pos, rb.surv_index, rb.surv_ids, rb.cand_index,
-                                                   rb.cand_rt, rb.counters);
+                                                   rb.cand_rt, rb.counters, rb.u_sum, rb.u_done,
+                                                   split ? 0 : rb.u_cap);
     }
     if (events) cudaEventRecord(events[2], stream);
     if (!split) {
         // candidate-CTA scoring: one persistent kernel, record included
         if (events) cudaEventRecord(events[3], stream);
+        // few candidates (a rank's share under strong scaling): units for the
+        // first u_cap, the candidate-CTA scorer for the rest; many: the
+        // candidate-CTA scorer for all. The latter writes the record.
+        int64_t unit_threshold = 2 * static_cast<int64_t>(cand_blocks);
+        if (const char* v = std::getenv("LK_SCORE_UNITS"); v && v[0] == '1') unit_threshold = INT64_MAX;
+        if (const char* v = std::getenv("LK_SCORE_UNITS"); v && v[0] == '0') unit_threshold = 0;
+        k_score_units<<<cand_blocks, kCtaThreads, 0, stream>>>(src, grid, sp, rb.cand_rt, rb.cand_index, rb.u_cap,
+                                                              rb.u_ns_pad, rb.u_miss, rb.u_inl, rb.u_add, rb.u_sum,
+                                                              rb.u_done, rb.counters, rb.block_best, unit_threshold);
         k_score_cta<<<cand_blocks, kCtaThreads, 0, stream>>>(src, grid, sp, rb.cand_rt, rb.cand_index, count,
-                                                            rb.cta_ns_pad, rb.cta_add, rb.cta_inl, rb.counters,
-                                                            rb.block_best, static_cast<RecordDev*>(d_record));
+                                                            rb.cta_ns_pad, rb.cta_add, rb.cta_inl, rb.u_cap,
+                                                            rb.counters, rb.block_best,
+                                                            static_cast<RecordDev*>(d_record), unit_threshold,
+                                                            cand_blocks);
         if (events) {
             cudaEventRecord(events[4], stream);
             cudaEventRecord(events[5], stream);

@@ -179,8 +179,9 @@ struct Counters {  // device-side, zeroed per run
     unsigned long long work_next;   // work queue head for k_score
     unsigned long long blocks_done; // last-block-done ticket
     unsigned long long n_full;      // split candidates that were fully scored
-    unsigned long long fin_done;    // k_score_finalists last-CTA ticket
-    unsigned long long _pad[5];
+    unsigned long long fin_done;    // last-CTA ticket of the record-writing scorer
+    unsigned long long work_next2;  // candidate ticket of k_score_cta (after the units)
+    unsigned long long _pad[4];
 };
 
 struct BestRec {  // per-block best, then the final record
@@ -225,6 +226,12 @@ struct RunBuffers {
     uint32_t* cta_inl = nullptr;
     int64_t cta_slots = 0, cta_ns_pad = 0;
     cudaError_t ensure_cta(int64_t ns, int32_t n_ctas);
+    // round-unit scoring: per candidate ballots, addends, sum and unit count
+    uint32_t *u_miss = nullptr, *u_inl = nullptr;
+    double *u_add = nullptr, *u_sum = nullptr;
+    unsigned* u_done = nullptr;
+    int64_t u_cap = 0, u_ns_pad = 0;
+    cudaError_t ensure_units(int64_t ns, int64_t cap);
 };
 
 struct SourceView {

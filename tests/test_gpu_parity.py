@@ -96,8 +96,11 @@ def test_eval_grid_build_matches_oracle(pair1, oracle):
         assert np.array_equal(a[k], b[k]), k
 
 
+@pytest.mark.parametrize("units", ["auto", "1", "0"])  # scorer: by candidate count / round units / CTA per candidate
 @pytest.mark.parametrize("seed,H", [(1, 100_000), (7, 20_000), (3, 50_000)])
-def test_run_hypotheses_matches_oracle(prepared1, oracle, seed, H):
+def test_run_hypotheses_matches_oracle(prepared1, oracle, monkeypatch, seed, H, units):
+    if units != "auto":
+        monkeypatch.setenv("LK_SCORE_UNITS", units)
     octx, c = prepared1
     params = lk.RegistrationParams(hypothesis_count=H, seed=seed)
     ctx = lk.registration_context(lk.PointCloud(c["src"], c["src_n"]), lk.PointCloud(c["tgt"], c["tgt_n"]),
