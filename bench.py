@@ -36,9 +36,9 @@ sys.path.insert(0, ROOT)
 METRIC = "candidate×point evals/sec"
 UNIT = "evals/s"
 # kernels of one hypothesis step (lk_hypotheses.cu run_hypotheses_range):
-# k_hyp_sample, k_kabsch, k_prep_fast, k_prep_fast_fine, k_score_split,
-# k_score_resolve, k_score (overflow), k_score_exits, k_score_finalists
-KERNELS_PER_STEP = 9
+# k_hyp_sample, k_kabsch, k_score_units (exits at once unless the candidates
+# are few), k_score_cta
+KERNELS_PER_STEP = 4
 PAPER_MS_PER_REGISTRATION = 20.50  # PAPER.md:161 (Titan X Pascal, redwood pairs) -- context only
 
 
