@@ -305,6 +305,9 @@ bool record_better(const lk_reg_record& a, const lk_reg_record& b) {
 
 }  // namespace
 
+// EvalGrid targets from this size on also get a ring grid (explicit candidates)
+constexpr int64_t kDenseTarget = 65536;
+
 struct lk_grid {
     int device = 0;
     int sm_count = 0;
@@ -313,6 +316,8 @@ struct lk_grid {
     bool has_normals = false;
     cudaStream_t stream = nullptr;
     lkk::GridStorage g;
+    lkk::RingStorage ring;  // dense EvalGrid targets: exact NN by ring shells
+    bool has_ring = false;
     lkk::RunBuffers rb;
     lk_reg_record* d_record = nullptr;
     std::mutex mu;
@@ -320,6 +325,7 @@ struct lk_grid {
         cudaSetDevice(device);
         if (stream) cudaStreamSynchronize(stream);
         g.release();
+        ring.release();
         rb.release();
         lkk::pool_free(d_record, stream);
         if (stream) cudaStreamDestroy(stream);
@@ -849,6 +855,13 @@ lk_status lk_grid_build(const lk_cloud* target, int32_t kind, double cell, doubl
             double* d_pos = dev_upload(target->xyz, 3 * target->n, g->stream);
             double* d_nrm = target->nxyz ? dev_upload(target->nxyz, 3 * target->n, g->stream) : nullptr;
             cudaError_t e = lkk::build_grid(g->g, kind, d_pos, d_nrm, target->n, cell, d_max, g->stream);
+            // a dense target (full-resolution frames: tens of points per
+            // EvalGrid cell) also gets a ring grid for explicit candidates
+            if (e == cudaSuccess && kind == 0 && target->n >= kDenseTarget && fast_path_enabled()) {
+                e = lkk::build_ring_grid(g->ring, d_pos, target->n, d_max, g->stream);
+                g->has_ring = e == cudaSuccess;
+            }
+            if (e == cudaSuccess) e = cudaStreamSynchronize(g->stream);
             cudaFree(d_pos);
             cudaFree(d_nrm);
             CK(e);
@@ -930,7 +943,7 @@ lk_status lk_score_candidates(lk_grid* grid, const lk_cloud* src, const double* 
         std::vector<int64_t> inl(C);
         std::vector<double> sum(C);
         cudaError_t e = lkk::score_candidates(sv, grid->g.view, sp, d_rt, C, grid->rb, d_inl, d_sum, grid->d_record,
-                                              s, grid->sm_count);
+                                              s, grid->sm_count, grid->has_ring ? &grid->ring.view : nullptr);
         if (e == cudaSuccess) e = cudaMemcpyAsync(&rec, grid->d_record, sizeof(rec), cudaMemcpyDeviceToHost, s);
         if (e == cudaSuccess && C)
             e = cudaMemcpyAsync(inl.data(), d_inl, C * sizeof(int64_t), cudaMemcpyDeviceToHost, s);

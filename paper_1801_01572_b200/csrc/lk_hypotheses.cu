@@ -32,6 +32,7 @@
 #include "lk_device_math.cuh"
 #include "lk_kernels.cuh"
 #include "lk_score_common.cuh"
+#include "lk_ring.cuh"
 
 namespace lkk {
 
@@ -1933,6 +1934,264 @@ __global__ void __launch_bounds__(kCtaThreads, 4) k_score_cta(SourceView src, co
              unit_cap, unit_threshold, n_unit_best);
 }
 
+// ---- explicit candidate lists (evaluate_hypothesis / evaluate_against_grid
+// per candidate, registration.cpp:53-78 / 155-219) over an EvalGrid with fine
+// lists: one CTA per candidate (persistent grid, ticket), rounds as in the
+// candidate-CTA scorer, and the candidate's sum run in point order by warp 0
+// round by round (every per-candidate fitness is the reference's own sum);
+// the last CTA writes the record of the best (registration.cpp:272-276).
+__global__ void __launch_bounds__(kCtaThreads, 4) k_score_list(SourceView src, const __grid_constant__ GridView g,
+                                                                const __grid_constant__ ScoreParams sp,
+                                                                const double* __restrict__ cand_rt, int64_t C,
+                                                                int64_t* __restrict__ out_inliers,
+                                                                double* __restrict__ out_sum,
+                                                                double* __restrict__ scratch,
+                                                                Counters* __restrict__ ctr,
+                                                                BestRec* __restrict__ block_best,
+                                                                RecordDev* __restrict__ rec) {
+    __shared__ CtaSmem S;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t ns = src.n;
+    double* my_add = scratch + static_cast<int64_t>(blockIdx.x) * kCtaPts;
+    WarpTally wt;  // thread 0's books
+    for (;;) {
+        if (threadIdx.x == 0) {
+            S.cand = static_cast<int64_t>(atomicAdd(&ctr->work_next, 1ull));
+            S.nq = 0;
+        }
+        if (threadIdx.x < 2 * kCtaWords) {
+            (&S.inl[0][0])[threadIdx.x] = 0u;
+            (&S.miss[0][0])[threadIdx.x] = 0u;
+        }
+        __syncthreads();
+        const int64_t cand = S.cand;
+        if (cand >= C) break;
+        if (threadIdx.x < 12) {
+            const double v = __ldg(cand_rt + 12 * cand + threadIdx.x);
+            if (threadIdx.x < 9) {
+                S.R[threadIdx.x] = v;
+                S.Rf[threadIdx.x] = static_cast<float>(v);
+            } else {
+                S.t[threadIdx.x - 9] = v;
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) S.F = make_fast_fine(S.R, S.t, g, sp);
+        __syncthreads();
+        double part = 0.0, sum = 0.0;
+        int64_t misses = 0, inliers = 0, visited = ns, done = ns;
+        bool exited = false;
+        for (int64_t base = 0, r = 0; base < ns; base += kCtaPts, ++r) {
+            const int b = static_cast<int>(r & 1);
+            score_round_ab(S, src, g, sp, cand_rt + 12 * cand, base, b, ns, my_add - base, part);
+            if (threadIdx.x == 0) S.nq = 0;
+            // the miss budget in point order (word w covers points base + 32 w ..)
+            const uint32_t m0 = S.miss[b][lane], m1 = kCtaWords > 32 ? S.miss[b][(32 + lane) % kCtaWords] : 0u;
+            const int c0 = __popc(m0), c1 = __popc(m1);
+            const int round_misses = __reduce_add_sync(kFull, static_cast<unsigned>(c0 + c1));
+            if (misses + round_misses > sp.miss_budget) {
+                exited = true;
+                if (warp == 0) {
+                    int64_t before = misses;
+                    for (int h = 0; h < 2; ++h) {
+                        const uint32_t mw = h ? m1 : m0;
+                        const int cnt = h ? c1 : c0;
+                        int incl = cnt;
+#pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const int y = __shfl_up_sync(kFull, incl, o);
+                            if (lane >= o) incl += y;
+                        }
+                        const unsigned over = __ballot_sync(kFull, before + incl > sp.miss_budget);
+                        if (over) {
+                            const int L = __ffs(over) - 1;
+                            const int64_t bef = before + __shfl_sync(kFull, incl - cnt, L);
+                            unsigned m = __shfl_sync(kFull, mw, L);
+                            const int need = static_cast<int>(sp.miss_budget - bef);
+                            for (int q = 0; q < need; ++q) m &= m - 1;
+                            visited = base + static_cast<int64_t>(h * 32 + L) * 32 + (__ffs(m) - 1) + 1;
+                            break;
+                        }
+                        before += __shfl_sync(kFull, incl, 31);
+                    }
+                }
+                const int64_t end = base + kCtaPts;
+                done = end < ns ? end : ns;
+                break;
+            }
+            misses += round_misses;
+            // this round's inliers' d2 in point order onto the candidate's sum
+            if (warp == 0) {
+                const unsigned below = (1u << lane) - 1u;
+                int off = 0;
+                for (int w = 0; w < kCtaWords; ++w) {
+                    const uint32_t m = S.inl[b][w];
+                    if ((m >> lane) & 1u) S.chain[off + __popc(m & below)] = my_add[w * 32 + lane];
+                    off += __popc(m);
+                }
+                inliers += off;
+                __syncwarp();
+                if (lane == 0) {
+                    int k = 0;
+                    for (; k + 4 <= off; k += 4) {
+                        const double x0 = S.chain[k], x1 = S.chain[k + 1], x2 = S.chain[k + 2], x3 = S.chain[k + 3];
+                        sum += x0;
+                        sum += x1;
+                        sum += x2;
+                        sum += x3;
+                    }
+                    for (; k < off; ++k) sum += S.chain[k];
+                }
+            }
+            __syncthreads();  // S.chain aliases the next round's queue
+        }
+        if (threadIdx.x == 0) {
+            out_inliers[cand] = exited ? -1 : inliers;
+            out_sum[cand] = exited ? 0.0 : sum;
+            wt.w_ref += static_cast<unsigned long long>(visited);
+            wt.executed += static_cast<unsigned long long>(done);
+            if (!exited) wt.candidate(inliers, sum, ns, sp, cand, cand);
+        }
+        __syncthreads();
+    }
+    // publish_cta folds lane 0 of every warp: only warp 0 carries the books
+    if (threadIdx.x != 0) wt = WarpTally{};
+    const bool last = publish_cta(wt, ctr, block_best, blockIdx.x, true);
+    if (last) write_record(block_best, gridDim.x, cand_rt, C, C, ctr, rec);
+}
+
+// Explicit lists on a dense EvalGrid target (its fine lists too long to scan):
+// the same per-candidate rounds, every point answered by the ring grid
+// (lk_ring.cuh: the reference EvalGrid's neighbour within d_max), then the
+// normal gate in FP64 (registration.cpp:200-210). Ballots come straight from
+// the warps; the sum runs in point order round by round.
+__global__ void __launch_bounds__(kCtaThreads, 4) k_score_list_ring(SourceView src, const __grid_constant__ RingGrid rg,
+                                                                     const double* __restrict__ tnrm,
+                                                                     const __grid_constant__ ScoreParams sp,
+                                                                     const double* __restrict__ cand_rt, int64_t C,
+                                                                     int64_t* __restrict__ out_inliers,
+                                                                     double* __restrict__ out_sum,
+                                                                     double* __restrict__ scratch,
+                                                                     Counters* __restrict__ ctr,
+                                                                     BestRec* __restrict__ block_best,
+                                                                     RecordDev* __restrict__ rec) {
+    __shared__ CtaSmem S;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t ns = src.n;
+    double* my_add = scratch + static_cast<int64_t>(blockIdx.x) * kCtaPts;
+    WarpTally wt;  // thread 0's books
+    for (;;) {
+        if (threadIdx.x == 0) S.cand = static_cast<int64_t>(atomicAdd(&ctr->work_next, 1ull));
+        __syncthreads();
+        const int64_t cand = S.cand;
+        if (cand >= C) break;
+        if (threadIdx.x < 12) {
+            const double v = __ldg(cand_rt + 12 * cand + threadIdx.x);
+            if (threadIdx.x < 9) S.R[threadIdx.x] = v;
+            else S.t[threadIdx.x - 9] = v;
+        }
+        __syncthreads();
+        double sum = 0.0;
+        int64_t misses = 0, inliers = 0, visited = ns, done = ns;
+        bool exited = false;
+        for (int64_t base = 0; base < ns; base += kCtaPts) {
+#pragma unroll 1
+            for (int u = 0; u < kCtaPer; ++u) {
+                const int local = u * kCtaThreads + threadIdx.x;
+                const int64_t i = base + local;
+                bool inl = false;
+                if (i < ns) {
+                    const V3 y = xform(S.R, S.t, src.pos4 ? ld4(src.pos4, i) : ld3(src.pos, i));
+                    const int32_t j = ring_nn(rg, y, sp.d2_max);
+                    if (j >= 0) {
+                        const V3 ns_ = ld3(src.nrm, i);
+                        const V3 nt = ld3(tnrm, j);
+                        if (!is_zero(ns_) && !is_zero(nt) && dot(rot(S.R, ns_), nt) >= sp.cos_max) {
+                            inl = true;
+                            my_add[local] = sqnorm(sub(ld4(rg.pos4, j), y));
+                        }
+                    }
+                }
+                const unsigned im = __ballot_sync(kFull, inl);
+                const unsigned mm = __ballot_sync(kFull, i < ns && !inl);
+                if (lane == 0) {
+                    S.inl[0][local >> 5] = im;
+                    S.miss[0][local >> 5] = mm;
+                }
+            }
+            __syncthreads();
+            const uint32_t m0 = S.miss[0][lane], m1 = kCtaWords > 32 ? S.miss[0][(32 + lane) % kCtaWords] : 0u;
+            const int c0 = __popc(m0), c1 = __popc(m1);
+            const int round_misses = __reduce_add_sync(kFull, static_cast<unsigned>(c0 + c1));
+            if (misses + round_misses > sp.miss_budget) {
+                exited = true;
+                if (warp == 0) {
+                    int64_t before = misses;
+                    for (int h = 0; h < 2; ++h) {
+                        const uint32_t mw = h ? m1 : m0;
+                        const int cnt = h ? c1 : c0;
+                        int incl = cnt;
+#pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const int yv = __shfl_up_sync(kFull, incl, o);
+                            if (lane >= o) incl += yv;
+                        }
+                        const unsigned over = __ballot_sync(kFull, before + incl > sp.miss_budget);
+                        if (over) {
+                            const int L = __ffs(over) - 1;
+                            const int64_t bef = before + __shfl_sync(kFull, incl - cnt, L);
+                            unsigned m = __shfl_sync(kFull, mw, L);
+                            const int need = static_cast<int>(sp.miss_budget - bef);
+                            for (int q = 0; q < need; ++q) m &= m - 1;
+                            visited = base + static_cast<int64_t>(h * 32 + L) * 32 + (__ffs(m) - 1) + 1;
+                            break;
+                        }
+                        before += __shfl_sync(kFull, incl, 31);
+                    }
+                }
+                const int64_t end = base + kCtaPts;
+                done = end < ns ? end : ns;
+                break;
+            }
+            misses += round_misses;
+            if (warp == 0) {
+                const unsigned below = (1u << lane) - 1u;
+                int off = 0;
+                for (int w = 0; w < kCtaWords; ++w) {
+                    const uint32_t m = S.inl[0][w];
+                    if ((m >> lane) & 1u) S.chain[off + __popc(m & below)] = my_add[w * 32 + lane];
+                    off += __popc(m);
+                }
+                inliers += off;
+                __syncwarp();
+                if (lane == 0) {
+                    int k = 0;
+                    for (; k + 4 <= off; k += 4) {
+                        const double x0 = S.chain[k], x1 = S.chain[k + 1], x2 = S.chain[k + 2], x3 = S.chain[k + 3];
+                        sum += x0;
+                        sum += x1;
+                        sum += x2;
+                        sum += x3;
+                    }
+                    for (; k < off; ++k) sum += S.chain[k];
+                }
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            out_inliers[cand] = exited ? -1 : inliers;
+            out_sum[cand] = exited ? 0.0 : sum;
+            wt.w_ref += static_cast<unsigned long long>(visited);
+            wt.executed += static_cast<unsigned long long>(done);
+            if (!exited) wt.candidate(inliers, sum, ns, sp, cand, cand);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x != 0) wt = WarpTally{};
+    const bool last = publish_cta(wt, ctr, block_best, blockIdx.x, true);
+    if (last) write_record(block_best, gridDim.x, cand_rt, C, C, ctr, rec);
+}
+
 int blocks_per_sm(const void* fn) {
     int b = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, kScoreThreads, 0) != cudaSuccess || b < 1) b = 1;
@@ -2284,7 +2543,31 @@ cudaError_t run_hypotheses_range(const SourceView& src, const double* d_tgt_pos,
 
 cudaError_t score_candidates(const SourceView& src, const GridView& grid, const ScoreParams& sp, const double* d_rt,
                              int64_t C, RunBuffers& rb, int64_t* d_out_inliers, double* d_out_sum, void* d_record,
-                             cudaStream_t stream, int sm_count) {
+                             cudaStream_t stream, int sm_count, const RingGrid* ring) {
+    if (ring && !sp.fitness_from_distance) {
+        // dense EvalGrid target: ring-grid queries, CTA per candidate
+        const int blocks = sm_count * blocks_per_sm(reinterpret_cast<const void*>(k_score_list_ring));
+        cudaError_t e = rb.ensure(1, blocks);
+        if (e != cudaSuccess) return e;
+        if ((e = rb.ensure_cta(kCtaPts, blocks)) != cudaSuccess) return e;
+        if ((e = cudaMemsetAsync(rb.counters, 0, sizeof(Counters), stream)) != cudaSuccess) return e;
+        k_score_list_ring<<<blocks, kCtaThreads, 0, stream>>>(src, *ring, grid.nrm_orig, sp, d_rt, C, d_out_inliers,
+                                                              d_out_sum, rb.cta_add, rb.counters, rb.block_best,
+                                                              static_cast<RecordDev*>(d_record));
+        return cudaGetLastError();
+    }
+    if (grid.fine_info && sp.fast && !sp.fitness_from_distance) {
+        // EvalGrid with fine lists: CTA per candidate over rounds
+        const int blocks = sm_count * cand_blocks_per_sm();
+        cudaError_t e = rb.ensure(1, blocks);
+        if (e != cudaSuccess) return e;
+        if ((e = rb.ensure_cta(kCtaPts, blocks)) != cudaSuccess) return e;  // kCtaPts doubles per CTA
+        if ((e = cudaMemsetAsync(rb.counters, 0, sizeof(Counters), stream)) != cudaSuccess) return e;
+        k_score_list<<<blocks, kCtaThreads, 0, stream>>>(src, grid, sp, d_rt, C, d_out_inliers, d_out_sum, rb.cta_add,
+                                                         rb.counters, rb.block_best,
+                                                         static_cast<RecordDev*>(d_record));
+        return cudaGetLastError();
+    }
     const int blocks = sm_count * score_blocks_per_sm();
     cudaError_t e = rb.ensure(1, blocks);
     if (e != cudaSuccess) return e;

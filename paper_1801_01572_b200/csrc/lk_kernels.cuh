@@ -318,7 +318,7 @@ cudaError_t verify_batch(const VerifyInput& in, VerifyOutput* out, cudaStream_t 
 // Scores an explicit candidate list (Rt on device, C x 12) and reduces the best.
 cudaError_t score_candidates(const SourceView& src, const GridView& grid, const ScoreParams& sp, const double* d_rt,
                              int64_t C, RunBuffers& rb, int64_t* d_out_inliers, double* d_out_sum,
-                             void* d_record, cudaStream_t stream, int sm_count);
+                             void* d_record, cudaStream_t stream, int sm_count, const RingGrid* ring = nullptr);
 
 // exclusive scan of n int32 into out[0..n] (out[n] = total), stream-ordered
 cudaError_t exclusive_scan(const int32_t* d_in, int64_t n, int32_t* d_out, cudaStream_t stream);

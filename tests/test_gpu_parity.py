@@ -306,6 +306,30 @@ def test_score_candidates_eval_grid_early_exit_matches_oracle(oracle):
             assert sc.best.hypothesis_index == ref["best"].hypothesis_index
 
 
+def test_score_candidates_dense_target_matches_oracle(oracle):
+    # config B2 shape: full-resolution depth frames (307k points, a ring grid
+    # answers the EvalGrid neighbour), lattice candidates around the truth plus
+    # misaligned ones, with and without the miss budget
+    pair = synth.depth_frame_pair()
+    rt, _ = synth.lattice_candidates(pair.truth, step_rad=math.pi / 180, step_m=0.01, half_rot=1, half_trans=0)
+    far, _ = synth.lattice_candidates(pair.truth, step_rad=25 * math.pi / 180, step_m=0.3, half_rot=0, half_trans=1)
+    rt = np.concatenate([rt, far[:6]])
+    params = lk.RegistrationParams()
+    grid = lk.build_eval_grid(pair.target, params.d_max)
+    for early in (False, True):
+        sc = lk.score_candidates(grid, pair.source, rt, params, early_exit=early)
+        ref = oracle.score_candidates(pair.source.positions, pair.source.normals, pair.target.positions,
+                                      pair.target.normals, rt, 0, int(early), 0.0, oracle.params_from(params))
+        scored = ref["scored"].astype(bool)
+        assert np.array_equal(sc.inliers >= 0, scored)
+        assert np.array_equal(sc.inliers[scored], ref["inliers"][scored])
+        assert np.array_equal(sc.fitness[scored], ref["fitness"][scored])
+        assert sc.qualified == ref["qualified"]
+        assert (sc.best is None) == (not ref["best"].found)
+        if sc.best:
+            assert sc.best.hypothesis_index == ref["best"].hypothesis_index
+
+
 @pytest.mark.parametrize("fp64_only", ["0", "1"])
 @pytest.mark.parametrize("kind", [0, 1])
 def test_fast_path_and_fp64_path_match_oracle(oracle, monkeypatch, fp64_only, kind):
