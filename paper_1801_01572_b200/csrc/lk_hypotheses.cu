@@ -1271,7 +1271,7 @@ constexpr int kCtaWarps = kCtaThreads / 32;
 constexpr int kCtaPer = 8;                         // points per thread per round
 constexpr int kCtaPts = kCtaThreads * kCtaPer;     // points per round
 constexpr int kCtaWords = kCtaPts / 32;            // ballot words per round (32 or 64)
-static_assert(kCtaWords == 32 || kCtaWords == 64, "the books read one or two ballot words per lane");
+static_assert(kCtaWords % 32 == 0, "ballot words come in warp-sized groups");
 constexpr int kCtaSlow = 0xffff;                   // queue count tag: exact FP64 fallback
 constexpr int kCtaChainChunks = kCtaPts / 32;      // chain window: the queue's 16 KB as doubles
 
@@ -1349,6 +1349,44 @@ __device__ double cta_chain(const uint32_t* im, const double* ad, int32_t n_chun
         __syncthreads();
     }
     return sum;
+}
+
+// The miss budget over one round's ballots (kCtaWords words, word w covering
+// points base + 32 w ..): returns the round's miss count (every thread); when
+// misses + count exceeds the budget, warp 0 sets `visited` to the reference's
+// visit count (its (budget + 1)-th miss, registration.cpp:211-214).
+__device__ __forceinline__ int round_misses(const uint32_t* __restrict__ words, int64_t base, int64_t misses,
+                                            const ScoreParams& sp, int64_t& visited) {
+    const int lane = threadIdx.x & 31;
+    unsigned c = 0;
+#pragma unroll
+    for (int w = lane; w < kCtaWords; w += 32) c += __popc(words[w]);
+    const int total = static_cast<int>(__reduce_add_sync(kFull, c));
+    if (misses + total > sp.miss_budget && (threadIdx.x >> 5) == 0) {
+        int64_t before = misses;
+        for (int h = 0; h < kCtaWords / 32; ++h) {
+            const uint32_t mw = words[h * 32 + lane];
+            const int cnt = __popc(mw);
+            int incl = cnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(kFull, incl, o);
+                if (lane >= o) incl += y;
+            }
+            const unsigned over = __ballot_sync(kFull, before + incl > sp.miss_budget);
+            if (over) {
+                const int L = __ffs(over) - 1;
+                const int64_t bef = before + __shfl_sync(kFull, incl - cnt, L);
+                unsigned m = __shfl_sync(kFull, mw, L);
+                const int need = static_cast<int>(sp.miss_budget - bef);
+                for (int q = 0; q < need; ++q) m &= m - 1;
+                visited = base + static_cast<int64_t>(h * 32 + L) * 32 + (__ffs(m) - 1) + 1;
+                break;
+            }
+            before += __shfl_sync(kFull, incl, 31);
+        }
+    }
+    return total;
 }
 
 // Phases A and B of one round of kCtaPts points starting at `base` for the
@@ -1502,46 +1540,23 @@ __device__ __forceinline__ void cta_body(CtaSmem& S, const SourceView& src, cons
             score_round_ab(S, src, g, sp, cand_rt + 12 * cand, base, b, ns, add, part);
             // C. the miss budget in point order (word w covers points base + 32 w ..)
             if (threadIdx.x == 0) S.nq = 0;
-            const uint32_t m0 = S.miss[b][lane], m1 = kCtaWords > 32 ? S.miss[b][(32 + lane) % kCtaWords] : 0u;
-            const int c0 = __popc(m0), c1 = __popc(m1);
-            const int round_misses = __reduce_add_sync(kFull, static_cast<unsigned>(c0 + c1));
-            if (misses + round_misses > sp.miss_budget) {
+            const int rm = round_misses(S.miss[b], base, misses, sp, visited);
+            if (misses + rm > sp.miss_budget) {
                 exited = true;
-                if (warp == 0) {
-                    int64_t before = misses;
-                    for (int h = 0; h < 2; ++h) {
-                        const uint32_t mw = h ? m1 : m0;
-                        const int cnt = h ? c1 : c0;
-                        int incl = cnt;
-#pragma unroll
-                        for (int o = 1; o < 32; o <<= 1) {
-                            const int y = __shfl_up_sync(kFull, incl, o);
-                            if (lane >= o) incl += y;
-                        }
-                        const unsigned over = __ballot_sync(kFull, before + incl > sp.miss_budget);
-                        if (over) {
-                            const int L = __ffs(over) - 1;
-                            const int64_t bef = before + __shfl_sync(kFull, incl - cnt, L);
-                            unsigned m = __shfl_sync(kFull, mw, L);
-                            const int need = static_cast<int>(sp.miss_budget - bef);
-                            for (int q = 0; q < need; ++q) m &= m - 1;
-                            visited = base + static_cast<int64_t>(h * 32 + L) * 32 + (__ffs(m) - 1) + 1;
-                            break;
-                        }
-                        before += __shfl_sync(kFull, incl, 31);
-                    }
-                }
                 const int64_t end = base + kCtaPts;
                 done = end < ns ? end : ns;
                 break;
             }
-            misses += round_misses;
+            misses += rm;
             if (warp == 0) {
-                const uint32_t i0 = S.inl[b][lane], i1 = kCtaWords > 32 ? S.inl[b][(32 + lane) % kCtaWords] : 0u;
-                const int64_t w0 = base / 32 + lane;
-                if (w0 < n_chunks) inlw[w0] = i0;
-                if (kCtaWords > 32 && w0 + 32 < n_chunks) inlw[w0 + 32] = i1;
-                inliers += __reduce_add_sync(kFull, static_cast<unsigned>(__popc(i0) + __popc(i1)));
+                unsigned pop = 0;
+#pragma unroll
+                for (int w = lane; w < kCtaWords; w += 32) {
+                    const uint32_t iw = S.inl[b][w];
+                    if (base / 32 + w < n_chunks) inlw[base / 32 + w] = iw;
+                    pop += __popc(iw);
+                }
+                inliers += __reduce_add_sync(kFull, pop);
             }
         }
         // the candidate's verdict (thread 0 decides, the CTA runs exact chains on demand)
@@ -1986,40 +2001,14 @@ __global__ void __launch_bounds__(kCtaThreads, 4) k_score_list(SourceView src, c
             score_round_ab(S, src, g, sp, cand_rt + 12 * cand, base, b, ns, my_add - base, part);
             if (threadIdx.x == 0) S.nq = 0;
             // the miss budget in point order (word w covers points base + 32 w ..)
-            const uint32_t m0 = S.miss[b][lane], m1 = kCtaWords > 32 ? S.miss[b][(32 + lane) % kCtaWords] : 0u;
-            const int c0 = __popc(m0), c1 = __popc(m1);
-            const int round_misses = __reduce_add_sync(kFull, static_cast<unsigned>(c0 + c1));
-            if (misses + round_misses > sp.miss_budget) {
+            const int rm = round_misses(S.miss[b], base, misses, sp, visited);
+            if (misses + rm > sp.miss_budget) {
                 exited = true;
-                if (warp == 0) {
-                    int64_t before = misses;
-                    for (int h = 0; h < 2; ++h) {
-                        const uint32_t mw = h ? m1 : m0;
-                        const int cnt = h ? c1 : c0;
-                        int incl = cnt;
-#pragma unroll
-                        for (int o = 1; o < 32; o <<= 1) {
-                            const int y = __shfl_up_sync(kFull, incl, o);
-                            if (lane >= o) incl += y;
-                        }
-                        const unsigned over = __ballot_sync(kFull, before + incl > sp.miss_budget);
-                        if (over) {
-                            const int L = __ffs(over) - 1;
-                            const int64_t bef = before + __shfl_sync(kFull, incl - cnt, L);
-                            unsigned m = __shfl_sync(kFull, mw, L);
-                            const int need = static_cast<int>(sp.miss_budget - bef);
-                            for (int q = 0; q < need; ++q) m &= m - 1;
-                            visited = base + static_cast<int64_t>(h * 32 + L) * 32 + (__ffs(m) - 1) + 1;
-                            break;
-                        }
-                        before += __shfl_sync(kFull, incl, 31);
-                    }
-                }
                 const int64_t end = base + kCtaPts;
                 done = end < ns ? end : ns;
                 break;
             }
-            misses += round_misses;
+            misses += rm;
             // this round's inliers' d2 in point order onto the candidate's sum
             if (warp == 0) {
                 const unsigned below = (1u << lane) - 1u;
@@ -2120,40 +2109,14 @@ __global__ void __launch_bounds__(kCtaThreads, 4) k_score_list_ring(SourceView s
                 }
             }
             __syncthreads();
-            const uint32_t m0 = S.miss[0][lane], m1 = kCtaWords > 32 ? S.miss[0][(32 + lane) % kCtaWords] : 0u;
-            const int c0 = __popc(m0), c1 = __popc(m1);
-            const int round_misses = __reduce_add_sync(kFull, static_cast<unsigned>(c0 + c1));
-            if (misses + round_misses > sp.miss_budget) {
+            const int rm = round_misses(S.miss[0], base, misses, sp, visited);
+            if (misses + rm > sp.miss_budget) {
                 exited = true;
-                if (warp == 0) {
-                    int64_t before = misses;
-                    for (int h = 0; h < 2; ++h) {
-                        const uint32_t mw = h ? m1 : m0;
-                        const int cnt = h ? c1 : c0;
-                        int incl = cnt;
-#pragma unroll
-                        for (int o = 1; o < 32; o <<= 1) {
-                            const int yv = __shfl_up_sync(kFull, incl, o);
-                            if (lane >= o) incl += yv;
-                        }
-                        const unsigned over = __ballot_sync(kFull, before + incl > sp.miss_budget);
-                        if (over) {
-                            const int L = __ffs(over) - 1;
-                            const int64_t bef = before + __shfl_sync(kFull, incl - cnt, L);
-                            unsigned m = __shfl_sync(kFull, mw, L);
-                            const int need = static_cast<int>(sp.miss_budget - bef);
-                            for (int q = 0; q < need; ++q) m &= m - 1;
-                            visited = base + static_cast<int64_t>(h * 32 + L) * 32 + (__ffs(m) - 1) + 1;
-                            break;
-                        }
-                        before += __shfl_sync(kFull, incl, 31);
-                    }
-                }
                 const int64_t end = base + kCtaPts;
                 done = end < ns ? end : ns;
                 break;
             }
-            misses += round_misses;
+            misses += rm;
             if (warp == 0) {
                 const unsigned below = (1u << lane) - 1u;
                 int off = 0;
