@@ -242,49 +242,68 @@ def _pool_map(fn, items):
 
 
 def bench_icp(args):
-    """Config D: ICP point-to-plane refinement of a 2.4M-point
-    submap pair from a perturbed truth, through the public API from host
-    buffers (upload, ring-grid build and every iteration inside the timing).
-    CPU baseline: one accumulation of the oracle on the full pair (all host
-    threads), scaled by the iteration count."""
+    """Config D: register_global (H = 10^6) on the 2.4M-point
+    submap pair, then ICP point-to-plane on the full clouds from the global
+    result, both through the public API from pinned host buffers (uploads,
+    prepare, grids and every ICP iteration inside the timing). CPU baseline:
+    the oracle's register_global on the same pair and one oracle ICP
+    iteration, scaled by the device's iteration count."""
+    import numpy as np
     import paper_1801_01572_b200 as lk
     from paper_1801_01572_b200 import synth
     pair = synth.submap_pair()
-    T0 = synth.compose(synth.transform_from_twist([0.02, -0.015, 0.01, 0.02, -0.01, 0.015]), pair.truth)
-    p = lk.IcpParams(max_correspondence_distance=0.05, max_iterations=30, convergence_eps=1e-10)
     src, keep_s = _pinned_cloud(pair.source)
     tgt, keep_t = _pinned_cloud(pair.target)
-    lk.icp_point_to_plane(src, tgt, T0, p)  # warm-up
-    times = []
+    params = lk.RegistrationParams(hypothesis_count=1_000_000, seed=1)
+    ip = lk.IcpParams(max_correspondence_distance=0.05, max_iterations=30, convergence_eps=1e-10)
+    reg = lk.register_global(src, tgt, params)  # warm-up
+    best = None
     for _ in range(3):
         t0 = time.perf_counter()
-        r = lk.icp_point_to_plane(src, tgt, T0, p)
-        times.append(time.perf_counter() - t0)
-    ms = 1e3 * min(times)
+        reg = lk.register_global(src, tgt, params)
+        t1 = time.perf_counter()
+        r = lk.icp_point_to_plane(src, tgt, reg.transform, ip)
+        t2 = time.perf_counter()
+        if best is None or (t2 - t0) < best[0] + best[1]:
+            best = (t1 - t0, t2 - t1)
+
+    def err(T):
+        R = pair.truth.rotation.T @ T.rotation
+        return (float(np.degrees(np.arccos(np.clip((np.trace(R) - 1) / 2, -1, 1)))),
+                float(np.linalg.norm(T.translation - pair.truth.translation)))
     evaluated = len(r.history)
-    out = {"workload": "D: submap_pair(seed 2, 8 views x 640x480 per submap, no downsample), ICP from truth "
-                       "perturbed by (0.02, -0.015, 0.01 rad; 0.02, -0.01, 0.015 m), d = 0.05 m",
+    out = {"workload": "D: submap_pair(seed 2, 8 views x 640x480 per submap, no downsample): register_global "
+                       "(H = 10^6, seed 1), then ICP point-to-plane (d = 0.05 m) from its result",
            "source_points": pair.source.size(), "target_points": pair.target.size(),
-           "iterations": r.iterations, "converged": r.converged, "correspondences": r.correspondences,
-           "rmse": r.rmse, "ms_per_icp": ms, "ms_per_iteration": ms / max(evaluated, 1),
-           "point_iterations_per_s": pair.source.size() * evaluated / (ms / 1e3),
-           "h2d_bytes": 24 * pair.source.size() + 48 * pair.target.size(),
-           "timing": "wall clock of lk_icp_point_to_plane from pinned host buffers (H2D, ring grid, all "
-                     "iterations), best of 3"}
+           "ms_register_global": 1e3 * best[0], "ms_icp": 1e3 * best[1], "ms_total": 1e3 * (best[0] + best[1]),
+           "global_error_deg_m": err(reg.transform), "icp_error_deg_m": err(r.transform),
+           "icp_iterations": r.iterations, "icp_converged": r.converged, "icp_correspondences": r.correspondences,
+           "icp_rmse": r.rmse, "icp_ms_per_iteration": 1e3 * best[1] / max(evaluated, 1),
+           "icp_point_iterations_per_s": pair.source.size() * evaluated / best[1],
+           "h2d_bytes": 2 * 48 * (pair.source.size() + pair.target.size()),
+           "timing": "wall clock of lk_register_global + lk_icp_point_to_plane from pinned host buffers, best of 3"}
     if not args.no_cpu_baseline:
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         import oracle as O
         t0 = time.perf_counter()
-        R1, t1, res1, h1 = O.icp_point_to_plane(pair.source.positions, pair.target.positions, pair.target.normals,
-                                                T0.rotation, T0.translation, 0.05, 1, 0.0)
+        p = O.params(hypothesis_count=1_000_000, seed=1, threads=os.cpu_count() or 0)
+        ctx = O.Context.prepare(pair.source.positions, pair.source.normals, pair.target.positions,
+                                pair.target.normals, p)
+        res, _ = ctx.run(p)
+        cpu_reg = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        R1, t1_, res1, h1 = O.icp_point_to_plane(pair.source.positions, pair.target.positions, pair.target.normals,
+                                                 reg.transform.rotation, reg.transform.translation, 0.05, 1, 0.0)
         cpu_it = time.perf_counter() - t0
         out["cpu_baseline"] = {"kind": "port", "cores": os.cpu_count(),
-                               "sample": "one oracle ICP iteration (grid build + accumulation + solve) on the full "
-                                         "pair, scaled by the device's iteration count",
-                               "ms_per_iteration": 1e3 * cpu_it,
-                               "ms_per_icp_extrapolated": 1e3 * cpu_it * evaluated,
-                               "parity_first_iteration": bool(h1[0, 0] == r.history[0, 0]
-                                                              and h1[0, 1] == r.history[0, 1])}
+                               "sample": "the oracle's register_global on the pair, and one oracle ICP iteration "
+                                         "(grid build + accumulation + solve) scaled by the device's iteration count",
+                               "ms_register_global": 1e3 * cpu_reg,
+                               "ms_icp_extrapolated": 1e3 * cpu_it * evaluated,
+                               "parity": {"hypothesis_index": bool(res.found and
+                                                                   res.hypothesis_index == reg.hypothesis_index),
+                                          "icp_first_iteration": bool(h1[0, 0] == r.history[0, 0]
+                                                                      and h1[0, 1] == r.history[0, 1])}}
     return out
 
 
