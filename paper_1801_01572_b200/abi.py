@@ -11,7 +11,7 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_DIR = os.path.join(_HERE, "_lib")
-LIB_PATH = os.path.join(LIB_DIR, "libloopkit_b200.so")
+LIB_PATH = os.environ.get("LK_LIB_OVERRIDE") or os.path.join(LIB_DIR, "libloopkit_b200.so")  # override: A/B experiments
 SYNTH_PATH = os.path.join(LIB_DIR, "libloopkit_synth.so")
 
 # lk_status (include/loopkit_b200.h), mirroring proj/include/loopkit/errors.hpp

@@ -1933,7 +1933,7 @@ __global__ void __launch_bounds__(kCtaThreads, 4) k_score_units(SourceView src, 
                block_best, unit_threshold);
 }
 
-__global__ void __launch_bounds__(kCtaThreads, 4) k_score_cta(SourceView src, const __grid_constant__ GridView g,
+__global__ void __launch_bounds__(kCtaThreads, 5) k_score_cta(SourceView src, const __grid_constant__ GridView g,
                                                                const __grid_constant__ ScoreParams sp,
                                                                const double* __restrict__ cand_rt,
                                                                const int64_t* __restrict__ cand_index,
