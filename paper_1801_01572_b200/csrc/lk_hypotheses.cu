@@ -633,6 +633,10 @@ __device__ __forceinline__ bool resolve_fine(const GridView& g, const double* R,
     }
     const float band = F.band;
     if (f1 > F.pad + band) return false;  // nothing within d_max of y
+    // the FP32 winner's normal is fetched with its position: it is the
+    // neighbour in all but near-tie cases, and saves a dependent round trip
+    const bool pre_nt = Rf && g.nrm32_orig;
+    const float4 nt1 = pre_nt ? __ldg(g.nrm32_orig + o1) : make_float4(0.f, 0.f, 0.f, 0.f);
     const V3 y = xform(R, t, p);
     double best_d2 = __longlong_as_double(0x7ff0000000000000ll);
     int32_t best_orig = INT32_MAX;
@@ -661,7 +665,7 @@ __device__ __forceinline__ bool resolve_fine(const GridView& g, const double* R,
     if (Rf && g.nrm32_orig) {
         // FP32 normal gate; only a value within the guard of cos_max (or a zero
         // FP32 normal) is decided by the reference's FP64 expression below
-        const float4 nt = __ldg(g.nrm32_orig + best_orig);
+        const float4 nt = best_orig == o1 ? nt1 : __ldg(g.nrm32_orig + best_orig);
         const float ns1 = fabsf(ns32.x) + fabsf(ns32.y) + fabsf(ns32.z);
         const float nt1 = fabsf(nt.x) + fabsf(nt.y) + fabsf(nt.z);
         if (ns1 > 0.0f && nt1 > 0.0f) {
