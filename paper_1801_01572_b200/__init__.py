@@ -6,7 +6,9 @@ CUDA kernels behind the C ABI in include/loopkit_b200.h, with this package as
 the Python mirror of the reference interface.
 """
 from .errors import (CudaError, DegenerateConfiguration, EmptyCloud, Error, MissingData, MissingNormals,
-                     NoCorrespondences, TooFewPoints)
+                     NoCorrespondences, ParseError, TooFewPoints)
+from .evaluation import (LogEntry, RegistrationScore, eval_registration, log_entry, read_registration_log,
+                         write_registration_log)
 from .registration import (CandidateScores, DeviceGrid, EdgeInfo, EvalGrid, HypothesisStats, IcpParams, IcpResult,
                            PointCloud,
                            RegistrationContext, RegistrationParams, RegistrationResult, RigidTransform, SearchGrid,

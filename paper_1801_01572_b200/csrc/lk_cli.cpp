@@ -10,6 +10,9 @@
 //       iterations, converged, correspondences, rmse and fitness.
 //   loopkit_b200 register-icp --source a.ply --target b.ply [register + icp options]
 //       global registration followed by ICP on the full clouds (config D).
+//   loopkit_b200 evaluate --mode registration --est e.log --truth t.log [--frags DIR] [--rmse-max M]
+//       cmd_evaluate_registration (loopkit_main.cpp:225-234): Table-I recall /
+//       precision of a registration log (metrics.cpp:112-156). Host-only.
 //
 // Errors print "error: <what>" and exit 1 (loopkit_main.cpp:405-408). PLY
 // input follows read_ply (proj/src/io.cpp:33-56, 66-190, 245-272): ascii or
@@ -204,6 +207,109 @@ PointCloud read_ply(const std::string& path) {
     return cloud;
 }
 
+// ---- registration log + Table-I scoring (proj/src/io.cpp, metrics.cpp) ------
+struct LogEntry {  // proj/include/loopkit/io.hpp:41-46
+    int i = 0, j = 0, n = 0;
+    double T[16] = {1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 1};  // row-major 4x4
+};
+
+std::vector<LogEntry> read_registration_log(const std::string& path) {  // io.cpp:341-369
+    std::ifstream f(path, std::ios::binary);
+    if (!f) throw CliError("cannot open " + path);
+    std::string text((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+    auto fail = [&](std::size_t line_no, const std::string& what) {
+        return CliError(path + ":" + std::to_string(line_no) + ": " + what);
+    };
+    std::vector<LogEntry> out;
+    std::size_t pos = 0, line_no = 0;
+    std::string line;
+    while (next_line(text, pos, line)) {
+        line_no += 1;
+        const std::size_t first = line.find_first_not_of(" \t");
+        if (first == std::string::npos || line[first] == '#') continue;
+        LogEntry e;
+        {
+            std::istringstream ss(line);
+            if (!(ss >> e.i >> e.j >> e.n)) throw fail(line_no, "expected header line 'i j n'");
+        }
+        for (int r = 0; r < 4; ++r) {
+            if (!next_line(text, pos, line)) throw fail(line_no, "truncated matrix block");
+            line_no += 1;
+            std::istringstream ss(line);
+            if (!(ss >> e.T[4 * r] >> e.T[4 * r + 1] >> e.T[4 * r + 2] >> e.T[4 * r + 3]))
+                throw fail(line_no, "expected 4 matrix values");
+        }
+        out.push_back(e);
+    }
+    return out;
+}
+
+struct RegistrationScore {  // proj/include/loopkit/metrics.hpp:39-45
+    double recall = 0.0, precision = 0.0;
+    int correct = 0, truth_count = 0, result_count = 0;
+};
+
+// eval_registration (metrics.cpp:112-156): a result is correct when its
+// (i, j) pair is in the truth log and the RMSE between the two transforms on
+// the probe points (fragment j's cloud, else the 8 corners of a unit cube)
+// is below rmse_max; each truth entry is credited at most once.
+RegistrationScore eval_registration(const std::vector<LogEntry>& results, const std::vector<LogEntry>& truth,
+                                    const std::vector<PointCloud>& probes, double rmse_max) {
+    RegistrationScore score;
+    score.truth_count = static_cast<int>(truth.size());
+    score.result_count = static_cast<int>(results.size());
+    if (truth.empty() || results.empty()) return score;
+    static const Vec3 cube[8] = {{-0.5, -0.5, -0.5}, {0.5, -0.5, -0.5}, {-0.5, 0.5, -0.5}, {0.5, 0.5, -0.5},
+                                 {-0.5, -0.5, 0.5},  {0.5, -0.5, 0.5},  {-0.5, 0.5, 0.5},  {0.5, 0.5, 0.5}};
+    auto apply = [](const double* T, const Vec3& p) {  // RigidTransform::operator*, geometry.hpp:26
+        return Vec3{((T[0] * p.x + T[1] * p.y) + T[2] * p.z) + T[3], ((T[4] * p.x + T[5] * p.y) + T[6] * p.z) + T[7],
+                    ((T[8] * p.x + T[9] * p.y) + T[10] * p.z) + T[11]};
+    };
+    auto pair_rmse = [&](const LogEntry& est, const LogEntry& gt) {
+        const Vec3* pts = cube;
+        std::size_t count = 8;
+        if (est.j >= 0 && static_cast<std::size_t>(est.j) < probes.size() &&
+            !probes[static_cast<std::size_t>(est.j)].positions.empty()) {
+            pts = probes[static_cast<std::size_t>(est.j)].positions.data();
+            count = probes[static_cast<std::size_t>(est.j)].positions.size();
+        }
+        double sq = 0.0;
+        for (std::size_t k = 0; k < count; ++k) {
+            const Vec3 a = apply(est.T, pts[k]), b = apply(gt.T, pts[k]);
+            const double dx = a.x - b.x, dy = a.y - b.y, dz = a.z - b.z;
+            sq += (dx * dx + dy * dy) + dz * dz;
+        }
+        return std::sqrt(sq / static_cast<double>(count));
+    };
+    std::vector<char> credited(truth.size(), 0);
+    for (const LogEntry& est : results) {
+        for (std::size_t t = 0; t < truth.size(); ++t) {
+            if (credited[t] || truth[t].i != est.i || truth[t].j != est.j) continue;
+            if (pair_rmse(est, truth[t]) < rmse_max) {
+                credited[t] = 1;
+                score.correct += 1;
+            }
+            break;
+        }
+    }
+    score.recall = static_cast<double>(score.correct) / static_cast<double>(truth.size());
+    score.precision = static_cast<double>(score.correct) / static_cast<double>(results.size());
+    return score;
+}
+
+std::vector<PointCloud> load_fragment_clouds(const std::string& dir) {  // loopkit_main.cpp:31-42
+    std::vector<PointCloud> clouds;
+    for (int i = 0;; ++i) {
+        char name[32];
+        std::snprintf(name, sizeof(name), "fragment_%04d.ply", i);
+        const std::string p = dir + "/" + name;
+        if (!std::ifstream(p).good()) break;
+        clouds.push_back(read_ply(p));
+    }
+    if (clouds.empty()) throw CliError("no fragment_%04d.ply files in " + dir);
+    return clouds;
+}
+
 // ---- arguments ---------------------------------------------------------------
 struct Args {
     std::map<std::string, std::string> opt;
@@ -298,7 +404,9 @@ int usage() {
                  "       loopkit_b200 icp --source A.ply --target B.ply --init \"m00 m01 ... m33\" [--max-dist D]\n"
                  "                     [--iterations N] [--eps E] [--device G]\n"
                  "       loopkit_b200 register-icp --source A.ply --target B.ply [register options]\n"
-                 "                     [--max-dist D] [--iterations N] [--eps E]\n");
+                 "                     [--max-dist D] [--iterations N] [--eps E]\n"
+                 "       loopkit_b200 evaluate --mode registration --est E.log --truth T.log [--frags DIR]\n"
+                 "                     [--rmse-max M]\n");
     return 1;
 }
 
@@ -348,6 +456,19 @@ int main(int argc, char** argv) {
             for (int k = 0; k < 9; ++k) T0[k] = result->transform.R[k];
             for (int k = 0; k < 3; ++k) T0[9 + k] = result->transform.t[k];
             return run_icp(source, target, T0, a);
+        }
+        if (cmd == "evaluate") {  // cmd_evaluate_registration, loopkit_main.cpp:225-234, flags :349-361
+            const Args a = parse(argc, argv, 2, {"mode", "est", "truth", "frags", "rmse-max"});
+            const std::string mode = a.str("mode");
+            if (mode != "registration")
+                throw CliError("--mode " + mode + ": only 'registration' is on the B200 path");
+            std::vector<PointCloud> probes;
+            if (a.has("frags") && !a.str("frags").empty()) probes = load_fragment_clouds(a.str("frags"));
+            const RegistrationScore s = eval_registration(read_registration_log(a.str("est")),
+                                                          read_registration_log(a.str("truth")), probes,
+                                                          a.num("rmse-max", 0.2));
+            std::printf("recall %.17g\nprecision %.17g\ncorrect %d\n", s.recall, s.precision, s.correct);
+            return 0;
         }
         if (cmd == "-h" || cmd == "--help") {
             usage();

@@ -44,6 +44,10 @@ class SingularSystem(Error):
     pass
 
 
+class ParseError(Error):
+    """A malformed input file; the message is "path:line: what" (errors.hpp:64-69)."""
+
+
 class CudaError(Error):
     """A CUDA failure on the device path (no CPU fallback exists)."""
 
