@@ -2058,7 +2058,12 @@ __global__ void __launch_bounds__(kCtaThreads, 4) k_score_list(SourceView src, c
 // (lk_ring.cuh: the reference EvalGrid's neighbour within d_max), then the
 // normal gate in FP64 (registration.cpp:200-210). Ballots come straight from
 // the warps; the sum runs in point order round by round.
-__global__ void __launch_bounds__(kCtaThreads, 4) k_score_list_ring(SourceView src, const __grid_constant__ RingGrid rg,
+// Each round's points are queried in their Morton order (order: per-round
+// permutation of the source, spatial_order_blocks) so that a warp's queries
+// share ring cells (ring_nn_warp); verdicts land in the round's bit words by
+// original index, so the round logic is unchanged.
+__global__ void __launch_bounds__(kCtaThreads, 3) k_score_list_ring(SourceView src, const __grid_constant__ RingGrid rg,
+                                                                     const int32_t* __restrict__ order,
                                                                      const double* __restrict__ tnrm,
                                                                      const __grid_constant__ ScoreParams sp,
                                                                      const double* __restrict__ cand_rt, int64_t C,
@@ -2069,6 +2074,7 @@ __global__ void __launch_bounds__(kCtaThreads, 4) k_score_list_ring(SourceView s
                                                                      BestRec* __restrict__ block_best,
                                                                      RecordDev* __restrict__ rec) {
     __shared__ CtaSmem S;
+    __shared__ float4 s_buf[kCtaWarps][32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t ns = src.n;
     double* my_add = scratch + static_cast<int64_t>(blockIdx.x) * kCtaPts;
@@ -2088,29 +2094,30 @@ __global__ void __launch_bounds__(kCtaThreads, 4) k_score_list_ring(SourceView s
         int64_t misses = 0, inliers = 0, visited = ns, done = ns;
         bool exited = false;
         for (int64_t base = 0; base < ns; base += kCtaPts) {
+            if (threadIdx.x < kCtaWords) {
+                S.inl[0][threadIdx.x] = 0u;
+                S.miss[0][threadIdx.x] = 0u;
+            }
+            __syncthreads();
 #pragma unroll 1
             for (int u = 0; u < kCtaPer; ++u) {
-                const int local = u * kCtaThreads + threadIdx.x;
-                const int64_t i = base + local;
+                const int64_t t = base + u * kCtaThreads + threadIdx.x;
+                const bool act = t < ns;
+                const int64_t i = act ? static_cast<int64_t>(__ldg(order + t)) : 0;
+                const int local = static_cast<int>(i - base);
+                V3 y = mk(0.0, 0.0, 0.0);
+                if (act) y = xform(S.R, S.t, src.pos4 ? ld4(src.pos4, i) : ld3(src.pos, i));
+                const int32_t j = ring_nn_warp(rg, y, sp.d2_max, act, s_buf[warp]);  // warp-uniform call
                 bool inl = false;
-                if (i < ns) {
-                    const V3 y = xform(S.R, S.t, src.pos4 ? ld4(src.pos4, i) : ld3(src.pos, i));
-                    const int32_t j = ring_nn(rg, y, sp.d2_max);
-                    if (j >= 0) {
-                        const V3 ns_ = ld3(src.nrm, i);
-                        const V3 nt = ld3(tnrm, j);
-                        if (!is_zero(ns_) && !is_zero(nt) && dot(rot(S.R, ns_), nt) >= sp.cos_max) {
-                            inl = true;
-                            my_add[local] = sqnorm(sub(ld4(rg.pos4, j), y));
-                        }
+                if (j >= 0) {
+                    const V3 ns_ = ld3(src.nrm, i);
+                    const V3 nt = ld3(tnrm, j);
+                    if (!is_zero(ns_) && !is_zero(nt) && dot(rot(S.R, ns_), nt) >= sp.cos_max) {
+                        inl = true;
+                        my_add[local] = sqnorm(sub(ld4(rg.pos4, j), y));
                     }
                 }
-                const unsigned im = __ballot_sync(kFull, inl);
-                const unsigned mm = __ballot_sync(kFull, i < ns && !inl);
-                if (lane == 0) {
-                    S.inl[0][local >> 5] = im;
-                    S.miss[0][local >> 5] = mm;
-                }
+                if (act) atomicOr(inl ? &S.inl[0][local >> 5] : &S.miss[0][local >> 5], 1u << (local & 31));
             }
             __syncthreads();
             const int rm = round_misses(S.miss[0], base, misses, sp, visited);
@@ -2518,10 +2525,18 @@ cudaError_t score_candidates(const SourceView& src, const GridView& grid, const 
         if (e != cudaSuccess) return e;
         if ((e = rb.ensure_cta(kCtaPts, blocks)) != cudaSuccess) return e;
         if ((e = cudaMemsetAsync(rb.counters, 0, sizeof(Counters), stream)) != cudaSuccess) return e;
-        k_score_list_ring<<<blocks, kCtaThreads, 0, stream>>>(src, *ring, grid.nrm_orig, sp, d_rt, C, d_out_inliers,
-                                                              d_out_sum, rb.cta_add, rb.counters, rb.block_best,
-                                                              static_cast<RecordDev*>(d_record));
-        return cudaGetLastError();
+        int32_t* order = nullptr;
+        if ((e = pool_alloc(&order, (src.n > 0 ? src.n : 1) * sizeof(int32_t), stream)) != cudaSuccess) return e;
+        if (src.n > 0 && (e = spatial_order_blocks(src.pos, src.n, kCtaPts, order, stream)) != cudaSuccess) {
+            pool_free(order, stream);
+            return e;
+        }
+        k_score_list_ring<<<blocks, kCtaThreads, 0, stream>>>(src, *ring, order, grid.nrm_orig, sp, d_rt, C,
+                                                              d_out_inliers, d_out_sum, rb.cta_add, rb.counters,
+                                                              rb.block_best, static_cast<RecordDev*>(d_record));
+        e = cudaGetLastError();
+        pool_free(order, stream);
+        return e;
     }
     if (grid.fine_info && sp.fast && !sp.fitness_from_distance) {
         // EvalGrid with fine lists: CTA per candidate over rounds

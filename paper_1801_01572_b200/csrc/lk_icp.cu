@@ -47,9 +47,29 @@ __device__ __forceinline__ double butterfly(double v) {
     return v;
 }
 
+// The nearest neighbours of one iteration, queries in the source's Morton
+// order (perm) so that a warp's walks share cells; nn[i] = -1 for no match.
+__global__ void __launch_bounds__(kIcpThreads) k_icp_nn(const double4* __restrict__ pos4,
+                                                        const int32_t* __restrict__ perm, int64_t n,
+                                                        const __grid_constant__ RingGrid rg, double d2_max,
+                                                        const IcpState* __restrict__ st, int32_t* __restrict__ nn) {
+    if (st->done) return;
+    __shared__ double s_R[12];
+    __shared__ float4 s_buf[kIcpThreads / 32][32];
+    if (threadIdx.x < 12) s_R[threadIdx.x] = threadIdx.x < 9 ? st->R[threadIdx.x] : st->t[threadIdx.x - 9];
+    __syncthreads();
+    const int64_t t = blockIdx.x * static_cast<int64_t>(kIcpThreads) + threadIdx.x;
+    const bool act = t < n;
+    const int32_t i = act ? __ldg(perm + t) : 0;
+    const V3 y = act ? xform(s_R, s_R + 9, ld4(pos4, i)) : mk(0.0, 0.0, 0.0);
+    const int32_t j = ring_nn_warp(rg, y, d2_max, act, s_buf[threadIdx.x >> 5]);  // warp-uniform call
+    if (act) nn[i] = j;
+}
+
 __global__ void __launch_bounds__(kIcpThreads) k_icp_accum(const double4* __restrict__ pos4, int64_t n,
                                                            const __grid_constant__ RingGrid rg,
-                                                           const double* __restrict__ tnrm, double d2_max,
+                                                           const double* __restrict__ tnrm,
+                                                           const int32_t* __restrict__ nn,
                                                            const IcpState* __restrict__ st,
                                                            double* __restrict__ partial,
                                                            unsigned long long* __restrict__ count) {
@@ -66,19 +86,19 @@ __global__ void __launch_bounds__(kIcpThreads) k_icp_accum(const double4* __rest
         double J[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
         double r = 0.0;
         if (i < n) {
-            const V3 y = xform(s_R, s_R + 9, ld4(pos4, i));
-            const int32_t j = ring_nn(rg, y, d2_max);
+            const int32_t j = __ldg(nn + i);
             if (j >= 0) {
-                const V3 nn = ld3(tnrm, j);
-                if (!is_zero(nn)) {
+                const V3 y = xform(s_R, s_R + 9, ld4(pos4, i));
+                const V3 nt = ld3(tnrm, j);
+                if (!is_zero(nt)) {
                     const V3 q = ld4(rg.pos4, j);
-                    r = dot(sub(y, q), nn);
-                    J[0] = y.y * nn.z - y.z * nn.y;
-                    J[1] = y.z * nn.x - y.x * nn.z;
-                    J[2] = y.x * nn.y - y.y * nn.x;
-                    J[3] = nn.x;
-                    J[4] = nn.y;
-                    J[5] = nn.z;
+                    r = dot(sub(y, q), nt);
+                    J[0] = y.y * nt.z - y.z * nt.y;
+                    J[1] = y.z * nt.x - y.x * nt.z;
+                    J[2] = y.x * nt.y - y.y * nt.x;
+                    J[3] = nt.x;
+                    J[4] = nt.y;
+                    J[5] = nt.z;
                     cnt += 1;
                 }
             }
@@ -169,10 +189,22 @@ __global__ void __launch_bounds__(kIcpVals * 32) k_icp_solve(const double* __res
     if (st->done) return;
     __shared__ double s_tot[kIcpVals];
     const int lane = threadIdx.x & 31, v = threadIdx.x >> 5;
+    // 32-chunk butterflies summed in order; eight groups' loads and
+    // butterflies in flight at once (the in-order sum is unchanged)
     double acc = 0.0;
-    for (int64_t s0 = 0; s0 < n_chunks; s0 += 32) {
-        const double x = s0 + lane < n_chunks ? partial[(s0 + lane) * kIcpVals + v] : 0.0;
-        acc = acc + butterfly(x);
+    constexpr int kU = 8;
+    for (int64_t s0 = 0; s0 < n_chunks; s0 += 32 * kU) {
+        double x[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int64_t c = s0 + 32 * u + lane;
+            x[u] = c < n_chunks ? partial[c * kIcpVals + v] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) x[u] = butterfly(x[u]);
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+            if (s0 + 32 * u < n_chunks) acc = acc + x[u];
     }
     if (lane == 0) s_tot[v] = acc;
     __syncthreads();
@@ -223,6 +255,7 @@ cudaError_t icp_point_to_plane(const double* d_src, int64_t n, const RingStorage
                                double* R9, double* t3, IcpOutcome* out, double* d_history, cudaStream_t stream,
                                int sm_count) {
     double4* pos4 = nullptr;
+    int32_t *perm = nullptr, *nn = nullptr;
     double* partial = nullptr;
     unsigned long long* counts = nullptr;
     IcpState* st = nullptr;
@@ -230,6 +263,8 @@ cudaError_t icp_point_to_plane(const double* d_src, int64_t n, const RingStorage
     cudaError_t e;
     auto cleanup = [&] {
         pool_free(pos4, stream);
+        pool_free(perm, stream);
+        pool_free(nn, stream);
         pool_free(partial, stream);
         pool_free(counts, stream);
         pool_free(st, stream);
@@ -247,7 +282,10 @@ cudaError_t icp_point_to_plane(const double* d_src, int64_t n, const RingStorage
     ICP_TRY(pool_alloc(&partial, n_chunks * kIcpVals * sizeof(double), stream));
     ICP_TRY(pool_alloc(&counts, (iters + 1) * sizeof(unsigned long long), stream));
     ICP_TRY(pool_alloc(&st, sizeof(IcpState), stream));
+    ICP_TRY(pool_alloc(&perm, n * sizeof(int32_t), stream));
+    ICP_TRY(pool_alloc(&nn, n * sizeof(int32_t), stream));
     ICP_TRY(make_records(d_src, nullptr, n, pos4, nullptr, stream));
+    ICP_TRY(spatial_order(d_src, n, perm, stream));
     ICP_TRY(cudaMemsetAsync(counts, 0, (iters + 1) * sizeof(unsigned long long), stream));
     IcpState h{};
     for (int k = 0; k < 9; ++k) h.R[k] = R0[k];
@@ -256,7 +294,8 @@ cudaError_t icp_point_to_plane(const double* d_src, int64_t n, const RingStorage
     const int blocks = static_cast<int>(n_chunks < sm_count * 8 ? n_chunks : sm_count * 8);
     const double d2_max = max_dist * max_dist;
     for (int32_t it = 0; it < iters; ++it) {
-        k_icp_accum<<<blocks, kIcpThreads, 0, stream>>>(pos4, n, ring.view, d_tnrm, d2_max, st, partial, counts + it);
+        k_icp_nn<<<static_cast<unsigned>(n_chunks), kIcpThreads, 0, stream>>>(pos4, perm, n, ring.view, d2_max, st, nn);
+        k_icp_accum<<<blocks, kIcpThreads, 0, stream>>>(pos4, n, ring.view, d_tnrm, nn, st, partial, counts + it);
         k_icp_solve<<<1, kIcpVals * 32, 0, stream>>>(partial, n_chunks, counts + it, st, d_history, it, eps * eps);
     }
     ICP_TRY(cudaGetLastError());

@@ -125,6 +125,9 @@ struct RingGrid {
     const int32_t* start;     // ncells + 1
     const float4* pts;        // CSR order: ring-cell coordinates, original index in w
     const double4* pos4;      // original order FP64 (x, y, z, 0)
+    // Chebyshev distance (cells, capped at rmax + 2) from each cell to the
+    // nearest occupied cell, or null: shells nearer than it hold no entries
+    const uint8_t* dt;
     // the reference grid whose window the answer must come from: the
     // EvalGrid (origin bbox_lo - d_max, cell d_max, +-1 cells, queries outside
     // [0, en) miss; registration.cpp:82-97,165-199) or a SearchGrid (center 0,
@@ -141,11 +144,17 @@ struct RingStorage {
     int32_t* start = nullptr;
     float4* pts = nullptr;
     double4* pos4 = nullptr;
+    uint8_t* dt = nullptr;
     cudaStream_t stream = nullptr;
     void release();
 };
 cudaError_t build_ring_grid(RingStorage& rs, const double* d_pos, int64_t n, double d_max, cudaStream_t stream,
                             bool fast = true);
+// Morton order of a cloud's points (d_perm: n indices), for coherent queries.
+cudaError_t spatial_order(const double* d_pos, int64_t n, int32_t* d_perm, cudaStream_t stream);
+// The same within each run of `block` consecutive points.
+cudaError_t spatial_order_blocks(const double* d_pos, int64_t n, int64_t block, int32_t* d_perm,
+                                 cudaStream_t stream);
 // K ring grids in one pass over K concatenated clouds (h_offsets: K + 1 point
 // offsets into d_pos). Grid k answers radius h_dmax[k] in the window of an
 // EvalGrid (h_cell[k] <= 0) or of a SearchGrid with cell length h_cell[k].

@@ -18,7 +18,10 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <vector>
+
+#include <cub/device/device_radix_sort.cuh>
 
 #include "lk_device_math.cuh"
 #include "lk_kernels.cuh"
@@ -94,6 +97,88 @@ __global__ void k_ring_scatter(const double* __restrict__ p, int64_t n, RingGrid
                          static_cast<float>((p[3 * i + 2] - rg.oz) / rg.cell), __int_as_float(static_cast<int>(i)));
 }
 
+
+// Chebyshev distance transform of the cell occupancy, one axis per pass
+// (the max-norm distance is separable): out = min over |d| <= K along the
+// axis of max(|d|, in[c + d]), with in = 0 / K + 1 for occupied / empty cells
+// on the first pass. Values saturate at K + 1 ("farther than K").
+template <int AX, bool FIRST>
+__global__ void k_ring_dt(const int32_t* __restrict__ start, const uint8_t* __restrict__ in, RingGrid rg, int K,
+                          uint8_t* __restrict__ out) {
+    const int64_t c = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (c >= rg.ncells) return;
+    const int64_t plane = static_cast<int64_t>(rg.ny) * rg.nz;
+    const int64_t stride = AX == 0 ? plane : (AX == 1 ? rg.nz : 1);
+    const int n = AX == 0 ? rg.nx : (AX == 1 ? rg.ny : rg.nz);
+    const int a = AX == 0 ? static_cast<int>(c / plane)
+                          : (AX == 1 ? static_cast<int>((c / rg.nz) % rg.ny) : static_cast<int>(c % rg.nz));
+    const int lo = a - K < 0 ? -a : -K, hi = a + K >= n ? n - 1 - a : K;
+    int best = K + 1;
+    for (int d = lo; d <= hi; ++d) {
+        const int64_t o = c + d * stride;
+        const int v = FIRST ? (__ldg(start + o + 1) > __ldg(start + o) ? 0 : K + 1) : static_cast<int>(__ldg(in + o));
+        const int ad = d < 0 ? -d : d;
+        const int m = v > ad ? v : ad;
+        best = m < best ? m : best;
+    }
+    out[c] = static_cast<uint8_t>(best);
+}
+
+cudaError_t ring_distance_transform(RingGrid& v, uint8_t** dt, cudaStream_t stream) {
+    const int K = std::min(v.rmax + 1, 254);
+    uint8_t* tmp = nullptr;
+    cudaError_t e = pool_alloc(dt, v.ncells, stream);
+    if (e != cudaSuccess) return e;
+    if ((e = cudaMallocAsync(&tmp, v.ncells, stream)) != cudaSuccess) return e;
+    const unsigned b = nblocks(v.ncells, 256);
+    k_ring_dt<0, true><<<b, 256, 0, stream>>>(v.start, nullptr, v, K, *dt);
+    k_ring_dt<1, false><<<b, 256, 0, stream>>>(nullptr, *dt, v, K, tmp);
+    k_ring_dt<2, false><<<b, 256, 0, stream>>>(nullptr, tmp, v, K, *dt);
+    cudaFreeAsync(tmp, stream);
+    v.dt = *dt;
+    return cudaGetLastError();
+}
+
+// 30-bit Morton code of a point in the cube of side `ext` at `lo` (10 bits per axis)
+__device__ __forceinline__ uint32_t spread10(uint32_t v) {
+    v &= 0x3ffu;
+    v = (v | (v << 16)) & 0x030000ffu;
+    v = (v | (v << 8)) & 0x0300f00fu;
+    v = (v | (v << 4)) & 0x030c30c3u;
+    v = (v | (v << 2)) & 0x09249249u;
+    return v;
+}
+
+__global__ void k_morton(const double* __restrict__ p, int64_t n, int64_t block,
+                         const unsigned long long* __restrict__ keys, unsigned long long* __restrict__ code,
+                         int32_t* __restrict__ idx) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    double lo[3], ext = 0.0;
+    for (int a = 0; a < 3; ++a) {
+        lo[a] = from_key(keys[a]);
+        ext = fmax(ext, from_key(keys[3 + a]) - lo[a]);
+    }
+    const double s = ext > 0.0 ? 1023.0 / ext : 0.0;
+    uint32_t c = 0;
+    for (int a = 0; a < 3; ++a) {
+        const double q = (p[3 * i + a] - lo[a]) * s;
+        const uint32_t v = q > 0.0 ? (q < 1023.0 ? static_cast<uint32_t>(q) : 1023u) : 0u;
+        c |= spread10(v) << a;
+    }
+    code[i] = (static_cast<unsigned long long>(i / block) << 30) | c;
+    idx[i] = static_cast<int32_t>(i);
+}
+
+// LK_RING_DT=0 disables the distance-transform shell skip (comparison runs)
+bool ring_dt_enabled() {
+    static int cached = -1;
+    if (cached < 0) {
+        const char* e = std::getenv("LK_RING_DT");
+        cached = (e && e[0] == '0') ? 0 : 1;
+    }
+    return cached == 1;
+}
 
 // ---- batched build (K clouds concatenated) ---------------------------------
 __device__ __forceinline__ int cloud_of(const int64_t* __restrict__ off, int K, int64_t i) {
@@ -226,10 +311,60 @@ void RingStorage::release() {
     pool_free(start, stream);
     pool_free(pts, stream);
     pool_free(pos4, stream);
+    pool_free(dt, stream);
     start = nullptr;
     pts = nullptr;
     pos4 = nullptr;
+    dt = nullptr;
     view = RingGrid{};
+}
+
+// A spatially coherent order of a cloud (Morton order of its own bounding
+// cube, 10 bits per axis): consecutive entries of perm lie close together,
+// and stay close under any rigid transform, so a warp walking queries in this
+// order visits the same ring cells (shared loop trip counts, L1 reuse).
+// spatial_order_blocks: the same inside each run of `block` consecutive
+// points (perm[b * block ...] is block b's points in Morton order).
+cudaError_t spatial_order_blocks(const double* d_pos, int64_t n, int64_t block, int32_t* d_perm,
+                                 cudaStream_t stream) {
+    if (n <= 0 || n > INT32_MAX || block <= 0) return cudaErrorInvalidValue;
+    int end_bit = 30;
+    for (int64_t nb = (n + block - 1) / block; nb > 1; nb = (nb + 1) / 2) ++end_bit;
+    unsigned long long* keys = nullptr;
+    unsigned long long *code = nullptr, *code_out = nullptr;
+    int32_t* idx = nullptr;
+    void* temp = nullptr;
+    size_t temp_bytes = 0;
+    cudaError_t e = cudaSuccess;
+    auto done = [&](cudaError_t r) {
+        cudaFreeAsync(keys, stream);
+        cudaFreeAsync(code, stream);
+        cudaFreeAsync(code_out, stream);
+        cudaFreeAsync(idx, stream);
+        if (temp) cudaFreeAsync(temp, stream);
+        return r;
+    };
+    if ((e = cudaMallocAsync(&keys, 6 * sizeof(unsigned long long), stream)) != cudaSuccess) return done(e);
+    if ((e = cudaMallocAsync(&code, n * sizeof(unsigned long long), stream)) != cudaSuccess) return done(e);
+    if ((e = cudaMallocAsync(&code_out, n * sizeof(unsigned long long), stream)) != cudaSuccess) return done(e);
+    if ((e = cudaMallocAsync(&idx, n * sizeof(int32_t), stream)) != cudaSuccess) return done(e);
+    // min keys start at all-ones, max keys at zero
+    if ((e = cudaMemsetAsync(keys, 0xff, 3 * sizeof(unsigned long long), stream)) != cudaSuccess) return done(e);
+    if ((e = cudaMemsetAsync(keys + 3, 0, 3 * sizeof(unsigned long long), stream)) != cudaSuccess) return done(e);
+    k_ring_bbox<<<std::min<unsigned>(nblocks(n, 256), 296), 256, 0, stream>>>(d_pos, n, keys);
+    k_morton<<<nblocks(n, 256), 256, 0, stream>>>(d_pos, n, block, keys, code, idx);
+    if ((e = cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, code, code_out, idx, d_perm, static_cast<int>(n), 0,
+                                             end_bit, stream)) != cudaSuccess)
+        return done(e);
+    if ((e = cudaMallocAsync(&temp, temp_bytes > 0 ? temp_bytes : 1, stream)) != cudaSuccess) return done(e);
+    if ((e = cub::DeviceRadixSort::SortPairs(temp, temp_bytes, code, code_out, idx, d_perm, static_cast<int>(n), 0,
+                                             end_bit, stream)) != cudaSuccess)
+        return done(e);
+    return done(cudaGetLastError());
+}
+
+cudaError_t spatial_order(const double* d_pos, int64_t n, int32_t* d_perm, cudaStream_t stream) {
+    return spatial_order_blocks(d_pos, n, n, d_perm, stream);
 }
 
 cudaError_t build_ring_grid(RingStorage& rs, const double* d_pos, int64_t n, double d_max, cudaStream_t stream,
@@ -275,6 +410,7 @@ cudaError_t build_ring_grid(RingStorage& rs, const double* d_pos, int64_t n, dou
     RG_TRY(make_records(d_pos, nullptr, n, rs.pos4, nullptr, stream));
     cudaFreeAsync(cell_of, stream);
     cudaFreeAsync(counts, stream);
+    if (ring_dt_enabled()) RG_TRY(ring_distance_transform(v, &rs.dt, stream));
     v.pts = rs.pts;
     v.pos4 = rs.pos4;
     v.npoints = n;

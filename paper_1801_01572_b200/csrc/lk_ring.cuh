@@ -119,14 +119,22 @@ __device__ __forceinline__ int32_t ring_nn(const RingGrid& rg, lkd::V3 y, double
     const float qy = static_cast<float>((y.y - rg.oy) / rg.cell);
     const float qz = static_cast<float>((y.z - rg.oz) / rg.cell);
     const int cx = static_cast<int>(floorf(qx)), cy = static_cast<int>(floorf(qy)), cz = static_cast<int>(floorf(qz));
+    // shells below the cell's distance to the nearest occupied cell are empty;
+    // every entry lies >= k0 - 1 - delta cells away on some axis
+    int k0 = 0;
+    if (rg.dt && cx >= 0 && cx < rg.nx && cy >= 0 && cy < rg.ny && cz >= 0 && cz < rg.nz) {
+        k0 = __ldg(rg.dt + (static_cast<int64_t>(cx) * rg.ny + cy) * rg.nz + cz);
+        const float m = static_cast<float>(k0 - 1) - rg.delta;
+        if (m > 0.0f && m * m > rg.thr + 2.0f * rg.band) return -1;
+    }
     const float inf = __int_as_float(0x7f800000);
     float f1 = inf, f2 = inf, f3 = inf;
     int32_t o1 = -1, o2 = -1;
-    int r_end = 0;
+    int r_end = k0;
     // entries farther than this (squared cells) can be neither the nearest,
     // nor tied with it, nor within d_max
     auto bound = [&]() { return fminf(f1 + 2.0f * rg.band, rg.thr + rg.band); };
-    for (int r = 0; r <= rg.rmax; ++r) {
+    for (int r = k0; r <= rg.rmax; ++r) {
         ring_shell(rg, qx, qy, qz, cx, cy, cz, r, bound, [&](int32_t e) {
             const float4 A = __ldg(rg.pts + e);
             const float dx = qx - A.x, dy = qy - A.y, dz = qz - A.z;
@@ -152,7 +160,7 @@ __device__ __forceinline__ int32_t ring_nn(const RingGrid& rg, lkd::V3 y, double
     const float lim = f1 + 2.0f * rg.band;
     if (f3 <= lim) {
         auto lim_bound = [&]() { return lim; };
-        for (int r = 0; r <= r_end; ++r)
+        for (int r = k0; r <= r_end; ++r)
             ring_shell(rg, qx, qy, qz, cx, cy, cz, r, lim_bound, [&](int32_t e) {
                 const float4 A = __ldg(rg.pts + e);
                 const float dx = qx - A.x, dy = qy - A.y, dz = qz - A.z;
@@ -165,6 +173,176 @@ __device__ __forceinline__ int32_t ring_nn(const RingGrid& rg, lkd::V3 y, double
     if (best == INT32_MAX) return -1;
     // the reference only sees its window: a nearest point outside it (a
     // division rounded across a face) sends the query to the exact window scan
+    const V3 q = ld4(rg.pos4, best);
+    const int ex = static_cast<int>(fx), ey = static_cast<int>(fy), ez = static_cast<int>(fz);
+    const int wx = ecell_axis(q.x, rg.eox, rg.ecell), wy = ecell_axis(q.y, rg.eoy, rg.ecell),
+              wz = ecell_axis(q.z, rg.eoz, rg.ecell);
+    const int w = rg.ewin;
+    if (wx < ex - w || wx > ex + w || wy < ey - w || wy > ey + w || wz < ez - w || wz > ez + w)
+        return ring_window_scan(rg, y, d2_max, ex, ey, ez);
+    return best;
+}
+
+// ---- warp-cooperative query ---------------------------------------------
+// All 32 lanes call ring_nn_warp together, each with its own query (active =
+// false: no query, -1). When the live queries' cells span at most
+// kWarpSpan cells per axis (queries in a spatially coherent order), the warp
+// scans cube shells around their common cell box instead of one walk per
+// lane: a cell is visited when any live lane's guard-banded bound reaches it,
+// its entries are loaded once (coalesced) and broadcast, and every lane keeps
+// its own FP32 top three. Scanning a superset of a lane's own walk keeps each
+// decision of ring_nn: the same stop rule per lane (every unscanned entry is
+// >= margin - delta cells away), the same band re-scan and FP64 choice, the
+// same window check. Wider warps fall back to ring_nn per lane.
+constexpr int kWarpSpan = 6;
+
+__device__ __forceinline__ void ring_top3_sel(float d2, int32_t o, float& f1, float& f2, float& f3, int32_t& o1,
+                                              int32_t& o2) {
+    const bool c1 = d2 < f1, c2 = d2 < f2, c3 = d2 < f3;
+    f3 = c2 ? f2 : (c3 ? d2 : f3);
+    o2 = c1 ? o1 : (c2 ? o : o2);
+    f2 = c1 ? f1 : (c2 ? d2 : f2);
+    o1 = c1 ? o : o1;
+    f1 = c1 ? d2 : f1;
+}
+
+// Visits the cells of shell r around the box [b0, b1] (r = 0: the box) that
+// some participating lane's bound reaches; visit(ax, ay, az, o) per entry.
+template <class B, class F>
+__device__ __forceinline__ void warp_shell(const RingGrid& rg, float qx, float qy, float qz, bool part, const int* b0,
+                                           const int* b1, int r, float4* wbuf, B&& bound, F&& visit) {
+    constexpr unsigned full = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const float dl = rg.delta;
+    auto gap = [dl](float q, int c) {
+        const float lo = static_cast<float>(c) - dl, hi = static_cast<float>(c + 1) + dl;
+        return q < lo ? lo - q : (q > hi ? q - hi : 0.0f);
+    };
+    const int X0 = b0[0] - r, X1 = b1[0] + r, Y0 = b0[1] - r, Y1 = b1[1] + r, Z0 = b0[2] - r, Z1 = b1[2] + r;
+    const int xa = X0 > 0 ? X0 : 0, xb = X1 < rg.nx - 1 ? X1 : rg.nx - 1;
+    const int ya = Y0 > 0 ? Y0 : 0, yb = Y1 < rg.ny - 1 ? Y1 : rg.ny - 1;
+    for (int x = xa; x <= xb; ++x) {
+        const float gx = gap(qx, x);
+        if (!__any_sync(full, part && gx * gx <= bound())) continue;
+        const bool xe = r == 0 || x == X0 || x == X1;
+        for (int y = ya; y <= yb; ++y) {
+            const float gy = gap(qy, y);
+            const float gxy = gx * gx + gy * gy;
+            if (!__any_sync(full, part && gxy <= bound())) continue;
+            const bool edge = xe || y == Y0 || y == Y1;
+            const int64_t row = (static_cast<int64_t>(x) * rg.ny + y) * rg.nz;
+            for (int z = Z0; z <= Z1; z = (edge || z == Z1) ? z + 1 : Z1) {
+                if (z < 0 || z >= rg.nz) continue;
+                const float gz = gap(qz, z);
+                if (!__any_sync(full, part && gxy + gz * gz <= bound())) continue;
+                const int32_t s0 = __ldg(rg.start + row + z), s1 = __ldg(rg.start + row + z + 1);
+                for (int32_t base = s0; base < s1; base += 32) {
+                    // stage 32 entries (one coalesced load), read back as broadcasts
+                    const int32_t e = base + lane;
+                    __syncwarp();
+                    if (e < s1) wbuf[lane] = __ldg(rg.pts + e);
+                    __syncwarp();
+                    const int cnt = s1 - base < 32 ? s1 - base : 32;
+                    for (int k = 0; k < cnt; ++k) {
+                        const float4 A = wbuf[k];
+                        visit(A.x, A.y, A.z, __float_as_int(A.w));
+                    }
+                }
+            }
+        }
+    }
+}
+
+// wbuf: 32 float4 of shared memory owned by the calling warp.
+__device__ __forceinline__ int32_t ring_nn_warp(const RingGrid& rg, lkd::V3 y, double d2_max, bool active,
+                                                float4* wbuf) {
+    using namespace lkd;
+    constexpr unsigned full = 0xffffffffu;
+    bool live = active;
+    double fx = 0.0, fy = 0.0, fz = 0.0;
+    if (live) {
+        fx = floor((y.x - rg.eox) / rg.ecell);
+        fy = floor((y.y - rg.eoy) / rg.ecell);
+        fz = floor((y.z - rg.eoz) / rg.ecell);
+        if (rg.ebounded && !(fx >= 0.0 && fy >= 0.0 && fz >= 0.0 && fx < rg.enx && fy < rg.eny && fz < rg.enz))
+            live = false;
+    }
+    float qx = 0.0f, qy = 0.0f, qz = 0.0f;
+    int c[3] = {0, 0, 0};
+    if (live) {
+        qx = static_cast<float>((y.x - rg.ox) / rg.cell);
+        qy = static_cast<float>((y.y - rg.oy) / rg.cell);
+        qz = static_cast<float>((y.z - rg.oz) / rg.cell);
+        c[0] = static_cast<int>(floorf(qx));
+        c[1] = static_cast<int>(floorf(qy));
+        c[2] = static_cast<int>(floorf(qz));
+        // every entry lies inside the grid's cells: a query more than rmax
+        // cells outside has nothing within d_max
+        if (c[0] < -rg.rmax || c[0] >= rg.nx + rg.rmax || c[1] < -rg.rmax || c[1] >= rg.ny + rg.rmax ||
+            c[2] < -rg.rmax || c[2] >= rg.nz + rg.rmax)
+            live = false;
+    }
+    if (live && rg.dt && c[0] >= 0 && c[0] < rg.nx && c[1] >= 0 && c[1] < rg.ny && c[2] >= 0 && c[2] < rg.nz) {
+        const int k0 = __ldg(rg.dt + (static_cast<int64_t>(c[0]) * rg.ny + c[1]) * rg.nz + c[2]);
+        const float m = static_cast<float>(k0 - 1) - rg.delta;
+        if (m > 0.0f && m * m > rg.thr + 2.0f * rg.band) live = false;
+    }
+    if (!__any_sync(full, live)) return -1;
+    int b0[3], b1[3];
+    bool wide = false;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        b0[a] = __reduce_min_sync(full, live ? c[a] : INT32_MAX);
+        b1[a] = __reduce_max_sync(full, live ? c[a] : INT32_MIN);
+        wide = wide || b1[a] - b0[a] > kWarpSpan;
+    }
+    if (wide) return live ? ring_nn(rg, y, d2_max) : -1;
+    const float inf = __int_as_float(0x7f800000);
+    float f1 = inf, f2 = inf, f3 = inf;
+    int32_t o1 = -1, o2 = -1;
+    auto bound = [&]() { return fminf(f1 + 2.0f * rg.band, rg.thr + rg.band); };
+    int r_end = 0;
+    // r = rmax covers every lane's own walk (its cell +- rmax)
+    for (int r = 0; r <= rg.rmax; ++r) {
+        warp_shell(rg, qx, qy, qz, live, b0, b1, r, wbuf, bound, [&](float ax, float ay, float az, int32_t o) {
+            const float dx = qx - ax, dy = qy - ay, dz = qz - az;
+            ring_top3_sel(fmaf(dx, dx, fmaf(dy, dy, dz * dz)), o, f1, f2, f3, o1, o2);
+        });
+        r_end = r;
+        // entries outside the scanned box lie >= m - delta cells from the query
+        const float mx = fminf(qx - static_cast<float>(b0[0] - r), static_cast<float>(b1[0] + r + 1) - qx);
+        const float my = fminf(qy - static_cast<float>(b0[1] - r), static_cast<float>(b1[1] + r + 1) - qy);
+        const float mz = fminf(qz - static_cast<float>(b0[2] - r), static_cast<float>(b1[2] + r + 1) - qz);
+        const float m = fminf(mx, fminf(my, mz)) - rg.delta;
+        if (__all_sync(full, !live || (m > 0.0f && m * m > bound()))) break;
+    }
+    const bool hit = live && f1 <= rg.thr + rg.band;
+    const float lim = f1 + 2.0f * rg.band;
+    double best_d2 = __longlong_as_double(0x7ff0000000000000ll);
+    int32_t best = INT32_MAX;
+    auto consider = [&](int32_t o) {
+        const V3 q = ld4(rg.pos4, o);
+        const double d2 = sqnorm(sub(q, y));
+        if (d2 > d2_max) return;
+        if (d2 < best_d2 || (d2 == best_d2 && o < best)) {
+            best_d2 = d2;
+            best = o;
+        }
+    };
+    const bool resc = hit && f3 <= lim;
+    if (__any_sync(full, resc)) {
+        auto lim_bound = [&]() { return lim; };
+        for (int r = 0; r <= r_end; ++r)
+            warp_shell(rg, qx, qy, qz, resc, b0, b1, r, wbuf, lim_bound, [&](float ax, float ay, float az, int32_t o) {
+                const float dx = qx - ax, dy = qy - ay, dz = qz - az;
+                if (resc && fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= lim) consider(o);
+            });
+    }
+    if (hit && !resc) {
+        consider(o1);
+        if (f2 <= lim) consider(o2);
+    }
+    if (!hit || best == INT32_MAX) return -1;
     const V3 q = ld4(rg.pos4, best);
     const int ex = static_cast<int>(fx), ey = static_cast<int>(fy), ez = static_cast<int>(fz);
     const int wx = ecell_axis(q.x, rg.eox, rg.ecell), wy = ecell_axis(q.y, rg.eoy, rg.ecell),
