@@ -138,7 +138,7 @@ struct RingGrid {
     int ebounded;  // 1: EvalGrid range check on the query cell
 };
 RingGrid ring_frame(const double* lo, const double* hi, double d_max, double search_cell, int64_t max_cells,
-                    bool fast);
+                    bool fast, double divisor = 6.0);
 struct RingStorage {
     RingGrid view{};
     int32_t* start = nullptr;

@@ -170,6 +170,17 @@ __global__ void k_morton(const double* __restrict__ p, int64_t n, int64_t block,
     idx[i] = static_cast<int32_t>(i);
 }
 
+// ring cells of d_max / LK_RING_DIV (default 5) for single dense grids
+double ring_divisor() {
+    static double cached = 0.0;
+    if (cached == 0.0) {
+        const char* e = std::getenv("LK_RING_DIV");
+        const double v = e ? std::atof(e) : 0.0;
+        cached = v >= 1.0 && v <= 64.0 ? v : 5.0;
+    }
+    return cached;
+}
+
 // LK_RING_DT=0 disables the distance-transform shell skip (comparison runs)
 bool ring_dt_enabled() {
     static int cached = -1;
@@ -254,7 +265,7 @@ __global__ void k_ring_scatter_batched(const double* __restrict__ p, int64_t n, 
 // bands, and the reference window -- the EvalGrid at cell d_max when
 // search_cell <= 0, else a SearchGrid of that cell length.
 RingGrid ring_frame(const double* lo, const double* hi, double d_max, double search_cell, int64_t max_cells,
-                    bool fast) {
+                    bool fast, double divisor) {
     RingGrid v{};
     if (search_cell <= 0.0) {
         // the reference's EvalGrid over the same cloud (registration.cpp:82-97)
@@ -274,7 +285,7 @@ RingGrid ring_frame(const double* lo, const double* hi, double d_max, double sea
         v.ewin = static_cast<int>(std::ceil(d_max / search_cell));
         v.ebounded = 0;
     }
-    double cell = d_max / 6.0;
+    double cell = d_max / divisor;
     int dims[3] = {1, 1, 1};
     int64_t nc = 1;
     for (int guard = 0; guard < 200; ++guard) {
@@ -393,7 +404,7 @@ cudaError_t build_ring_grid(RingStorage& rs, const double* d_pos, int64_t n, dou
     }
     // at most 64 cells per point (and 2^28 overall)
     const int64_t cap = std::min<int64_t>(std::max<int64_t>(64 * n, 4096), int64_t(1) << 28);
-    RingGrid v = ring_frame(lo, hi, d_max, -1.0, cap, fast);
+    RingGrid v = ring_frame(lo, hi, d_max, -1.0, cap, fast, ring_divisor());
     int64_t nc = v.ncells;
     int32_t *cell_of = nullptr, *counts = nullptr;
     RG_TRY(cudaMallocAsync(&cell_of, n * sizeof(int32_t), stream));
@@ -470,7 +481,7 @@ cudaError_t build_ring_grids(RingBatch& rb, const double* d_pos, const int64_t* 
         // the dense CSR is sized to the cloud: at most 16 cells per point
         const int64_t npk = h_offsets[k + 1] - h_offsets[k];
         const int64_t cap = std::min<int64_t>(std::max<int64_t>(16 * npk, 4096), int64_t(1) << 24);
-        views[k] = ring_frame(lo, hi, h_dmax[k], h_cell ? h_cell[k] : -1.0, cap, true);
+        views[k] = ring_frame(lo, hi, h_dmax[k], h_cell ? h_cell[k] : -1.0, cap, true, 6.0);
         cell_off[k + 1] = cell_off[k] + views[k].ncells;
     }
     const int64_t nc = cell_off[K];

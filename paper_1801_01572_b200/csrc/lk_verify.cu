@@ -13,8 +13,12 @@
 // built in one batched pass. The per-pair sums are the reference's own
 // sequential sums in point order (one lane per accumulator), so the
 // information matrix, the fitness and every count are bit-exact.
+#include <chrono>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "lk_device_math.cuh"
@@ -99,87 +103,159 @@ __global__ void k_verify_src(const double* __restrict__ p, const double* __restr
     addend[i] = add;
 }
 
-// One warp per pair. The points are staged 32 at a time (coalesced): every
-// lane computes its point's nine contributions -- the a^T a entries (0,0)
-// (0,1) (0,2) (1,1) (1,2) (2,2) with a = -[q]x, then q.x, q.y, q.z -- into
-// shared memory, and lane j < 9 adds column j over the staged points in point
-// order: the reference's sequential sums (line_process.cpp:24-28), with the
-// loads off the dependent add chain. The same for the evaluate_hypothesis
-// sq_sum over the source points. Counts are popcounts of the hit ballots.
+// One CTA of kSumThreads per pair. The points are staged kSumThreads at a
+// time (coalesced): every thread computes its point's nine contributions --
+// the a^T a entries (0,0) (0,1) (0,2) (1,1) (1,2) (2,2) with a = -[q]x, then
+// q.x, q.y, q.z -- into shared memory, and lane j < 9 of warp 0 adds column j
+// over the staged hits in point order: the reference's sequential sums
+// (line_process.cpp:24-28), with the loads off the dependent add chain. The
+// same for the evaluate_hypothesis sq_sum over the source points (lane 9).
+// Counts are popcounts of the hit ballots.
 // out per pair: 10 doubles (9 edge sums, sq_sum) then 3 int64 at [10..12].
-__global__ void __launch_bounds__(32) k_verify_sums(const double* __restrict__ q, const int64_t* __restrict__ offq,
-                                                    const uint8_t* __restrict__ edge_hit,
-                                                    const int64_t* __restrict__ offp,
-                                                    const uint8_t* __restrict__ overlap_hit,
-                                                    const uint8_t* __restrict__ inlier,
-                                                    const double* __restrict__ addend, double* __restrict__ out) {
-    __shared__ double s_c[9][33];
+constexpr int kSumThreads = 256;
+constexpr int kSumWarps = kSumThreads / 32;
+
+__global__ void __launch_bounds__(kSumThreads) k_verify_sums(const double* __restrict__ q,
+                                                             const int64_t* __restrict__ offq,
+                                                             const uint8_t* __restrict__ edge_hit,
+                                                             const int64_t* __restrict__ offp,
+                                                             const uint8_t* __restrict__ overlap_hit,
+                                                             const uint8_t* __restrict__ inlier,
+                                                             const double* __restrict__ addend,
+                                                             double* __restrict__ out) {
+    __shared__ double s_c[9][kSumThreads + 1];
+    __shared__ unsigned s_m[kSumWarps];
+    __shared__ unsigned long long s_cnt[3];
     const int k = blockIdx.x;
-    const int lane = threadIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (threadIdx.x < 3) s_cnt[threadIdx.x] = 0ull;
     double acc = 0.0, sq = 0.0;
-    long long n_edge = 0, n_over = 0, n_inl = 0;
-    for (int64_t base = offq[k]; base < offq[k + 1]; base += 32) {
-        const int64_t i = base + lane;
-        const bool hit = i < offq[k + 1] && edge_hit[i];
+    unsigned long long n_edge = 0, n_over = 0, n_inl = 0;
+    const int64_t q0 = offq[k], q1 = offq[k + 1], p0 = offp[k], p1 = offp[k + 1];
+    for (int64_t base = q0; base < q1; base += kSumThreads) {
+        const int64_t i = base + threadIdx.x;
+        const bool hit = i < q1 && edge_hit[i];
         const unsigned m = __ballot_sync(0xffffffffu, hit);
-        n_edge += __popc(m);
+        if (lane == 0) {
+            s_m[warp] = m;
+            n_edge += __popc(m);
+        }
         if (hit) {
             const V3 v = ld3(q, i);
             const double a[3][3] = {{-0.0, v.z, -v.y}, {-v.z, -0.0, v.x}, {v.y, -v.x, -0.0}};
-            s_c[0][lane] = (a[0][0] * a[0][0] + a[1][0] * a[1][0]) + a[2][0] * a[2][0];
-            s_c[1][lane] = (a[0][0] * a[0][1] + a[1][0] * a[1][1]) + a[2][0] * a[2][1];
-            s_c[2][lane] = (a[0][0] * a[0][2] + a[1][0] * a[1][2]) + a[2][0] * a[2][2];
-            s_c[3][lane] = (a[0][1] * a[0][1] + a[1][1] * a[1][1]) + a[2][1] * a[2][1];
-            s_c[4][lane] = (a[0][1] * a[0][2] + a[1][1] * a[1][2]) + a[2][1] * a[2][2];
-            s_c[5][lane] = (a[0][2] * a[0][2] + a[1][2] * a[1][2]) + a[2][2] * a[2][2];
-            s_c[6][lane] = v.x;
-            s_c[7][lane] = v.y;
-            s_c[8][lane] = v.z;
+            const int t = threadIdx.x;
+            s_c[0][t] = (a[0][0] * a[0][0] + a[1][0] * a[1][0]) + a[2][0] * a[2][0];
+            s_c[1][t] = (a[0][0] * a[0][1] + a[1][0] * a[1][1]) + a[2][0] * a[2][1];
+            s_c[2][t] = (a[0][0] * a[0][2] + a[1][0] * a[1][2]) + a[2][0] * a[2][2];
+            s_c[3][t] = (a[0][1] * a[0][1] + a[1][1] * a[1][1]) + a[2][1] * a[2][1];
+            s_c[4][t] = (a[0][1] * a[0][2] + a[1][1] * a[1][2]) + a[2][1] * a[2][2];
+            s_c[5][t] = (a[0][2] * a[0][2] + a[1][2] * a[1][2]) + a[2][2] * a[2][2];
+            s_c[6][t] = v.x;
+            s_c[7][t] = v.y;
+            s_c[8][t] = v.z;
         }
-        __syncwarp();
-        if (lane < 9) {
-            unsigned mm = m;
-            while (mm) {
-                const int j = __ffs(mm) - 1;
-                mm &= mm - 1;
-                acc += s_c[lane][j];
+        __syncthreads();
+        if (warp == 0 && lane < 9) {
+            for (int w = 0; w < kSumWarps; ++w) {
+                unsigned mm = s_m[w];
+                while (mm) {
+                    const int j = __ffs(mm) - 1;
+                    mm &= mm - 1;
+                    acc += s_c[lane][32 * w + j];
+                }
             }
         }
-        __syncwarp();
+        __syncthreads();
     }
-    for (int64_t base = offp[k]; base < offp[k + 1]; base += 32) {
-        const int64_t i = base + lane;
-        const bool in = i < offp[k + 1];
-        n_over += __popc(__ballot_sync(0xffffffffu, in && overlap_hit[i]));
+    for (int64_t base = p0; base < p1; base += kSumThreads) {
+        const int64_t i = base + threadIdx.x;
+        const bool in = i < p1;
+        const unsigned mo = __ballot_sync(0xffffffffu, in && overlap_hit[i]);
         const bool inl = in && inlier[i];
         const unsigned m = __ballot_sync(0xffffffffu, inl);
-        n_inl += __popc(m);
-        if (inl) s_c[0][lane] = addend[i];
-        __syncwarp();
-        if (lane == 9) {
-            unsigned mm = m;
-            while (mm) {
-                const int j = __ffs(mm) - 1;
-                mm &= mm - 1;
-                sq += s_c[0][j];
+        if (lane == 0) {
+            s_m[warp] = m;
+            n_over += __popc(mo);
+            n_inl += __popc(m);
+        }
+        if (inl) s_c[0][threadIdx.x] = addend[i];
+        __syncthreads();
+        if (warp == 0 && lane == 9) {
+            for (int w = 0; w < kSumWarps; ++w) {
+                unsigned mm = s_m[w];
+                while (mm) {
+                    const int j = __ffs(mm) - 1;
+                    mm &= mm - 1;
+                    sq += s_c[0][32 * w + j];
+                }
             }
         }
-        __syncwarp();
+        __syncthreads();
     }
-    double* o = out + 16 * k;
-    if (lane < 9) o[lane] = acc;
-    if (lane == 9) o[9] = sq;
     if (lane == 0) {
-        long long* c = reinterpret_cast<long long*>(o);
-        c[10] = n_edge;
-        c[11] = n_over;
-        c[12] = n_inl;
+        atomicAdd(&s_cnt[0], n_edge);
+        atomicAdd(&s_cnt[1], n_over);
+        atomicAdd(&s_cnt[2], n_inl);
     }
+    __syncthreads();
+    double* o = out + 16 * k;
+    if (warp == 0 && lane < 9) o[lane] = acc;
+    if (warp == 0 && lane == 9) o[9] = sq;
+    if (threadIdx.x == 0) {
+        long long* c = reinterpret_cast<long long*>(o);
+        c[10] = static_cast<long long>(s_cnt[0]);
+        c[11] = static_cast<long long>(s_cnt[1]);
+        c[12] = static_cast<long long>(s_cnt[2]);
+    }
+}
+
+// Zero-copy gather of many pinned host arrays into device slots: item k
+// copies count[k] doubles from src[k] (a device-mapped pinned host pointer)
+// to dst[k]; blockIdx.y picks the item, blockIdx.x strides inside it.
+struct GatherItem {
+    const double* src;
+    double* dst;
+    int64_t count;
+};
+
+__global__ void k_gather_host(const GatherItem* __restrict__ items) {
+    const GatherItem it = items[blockIdx.y];
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < it.count;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        it.dst[i] = it.src[i];
+}
+
+// LK_ZERO_COPY=0: always use one cudaMemcpyAsync per array
+bool zero_copy_enabled() {
+    static int cached = -1;
+    if (cached < 0) {
+        const char* e = std::getenv("LK_ZERO_COPY");
+        cached = (e && e[0] == '0') ? 0 : 1;
+    }
+    return cached == 1;
+}
+
+// Device-mapped address of a page-locked host pointer, or null (pageable).
+const double* mapped(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return a.type == cudaMemoryTypeHost ? static_cast<const double*>(a.devicePointer) : nullptr;
 }
 
 }  // namespace
 
 cudaError_t verify_batch(const VerifyInput& in, VerifyOutput* out, cudaStream_t stream) {
+    // LK_TRACE: host timestamps of the phases (diagnostic)
+    static const bool trace = std::getenv("LK_TRACE") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what) {
+        if (!trace) return;
+        const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        std::fprintf(stderr, "[lk verify] %-22s %8.3f ms\n", what, ms);
+    };
     const int K = in.n_pairs;
     const int64_t nq = in.offq[K], np = in.offp[K];
     cudaError_t e = cudaSuccess;
@@ -234,8 +310,39 @@ cudaError_t verify_batch(const VerifyInput& in, VerifyOutput* out, cudaStream_t 
         add_copies(d_pn, in.pnrm, in.offp);
         VF_TRY(cudaMemcpyAsync(d_T + 24 * K, in.T, 12 * K * sizeof(double), cudaMemcpyHostToDevice, stream));
     }
-    for (size_t c = 0; c < dsts.size(); ++c)
-        VF_TRY(cudaMemcpyAsync(dsts[c], srcs[c], sizes[c], cudaMemcpyHostToDevice, stream));
+    mark("allocs");
+    // page-locked callers' clouds are read straight over PCIe by one gather
+    // kernel (one launch instead of 4K copies); otherwise one copy per array
+    std::vector<GatherItem> items;
+    if (zero_copy_enabled()) {
+        items.reserve(dsts.size());
+        for (size_t c = 0; c < dsts.size(); ++c) {
+            const double* m = sizes[c] > 0 ? mapped(srcs[c]) : nullptr;
+            if (sizes[c] > 0 && !m) {
+                items.clear();
+                break;
+            }
+            if (sizes[c] > 0)
+                items.push_back(GatherItem{m, static_cast<double*>(dsts[c]),
+                                           static_cast<int64_t>(sizes[c] / sizeof(double))});
+        }
+    }
+    if (!items.empty() && items.size() <= 65535) {
+        GatherItem* d_items = nullptr;
+        const size_t bytes = items.size() * sizeof(GatherItem);
+        void* h_items = host_scratch(bytes);
+        if (!h_items) VF_TRY(cudaErrorMemoryAllocation);
+        std::memcpy(h_items, items.data(), bytes);
+        VF_TRY(cudaMallocAsync(&d_items, bytes, stream));
+        VF_TRY(cudaMemcpyAsync(d_items, h_items, bytes, cudaMemcpyHostToDevice, stream));
+        k_gather_host<<<dim3(8, static_cast<unsigned>(items.size())), 256, 0, stream>>>(d_items);
+        VF_TRY(cudaGetLastError());
+        cudaFreeAsync(d_items, stream);
+    } else {
+        for (size_t c = 0; c < dsts.size(); ++c)
+            VF_TRY(cudaMemcpyAsync(dsts[c], srcs[c], sizes[c], cudaMemcpyHostToDevice, stream));
+    }
+    mark("copies enqueued");
     // grid clouds: [T_j P_k]_k for edge_info, then (full) [T_i Q_k]_k, [Q_k]_k
     const int G = in.full ? 3 * K : K;
     const int64_t ng = np + (in.full ? 2 * nq : 0);
@@ -262,6 +369,7 @@ cudaError_t verify_batch(const VerifyInput& in, VerifyOutput* out, cudaStream_t 
         }
     }
     VF_TRY(build_ring_grids(rb, d_grid_pts, goff.data(), G, gd.data(), gc.data(), stream));
+    mark("ring grids");
     VF_TRY(pool_alloc(&d_flags, (nq + 2 * np + 3) * sizeof(uint8_t), stream));
     uint8_t* edge_hit = d_flags;
     uint8_t* overlap_hit = d_flags + nq;
@@ -275,10 +383,12 @@ cudaError_t verify_batch(const VerifyInput& in, VerifyOutput* out, cudaStream_t 
         k_verify_src<<<nblocks(np, 128), 128, 0, stream>>>(
             d_ppos, d_pn, np, d_offp, K, d_qn, d_offq, d_Tj, d_Tr, rb.d_views + K, rb.d_views + 2 * K,
             in.overlap_radius * in.overlap_radius, in.d_max * in.d_max, in.cos_max, overlap_hit, inl, d_addend);
-    k_verify_sums<<<K, 32, 0, stream>>>(d_qpos, d_offq, edge_hit, d_offp, overlap_hit, inl, d_addend, d_out);
+    k_verify_sums<<<K, kSumThreads, 0, stream>>>(d_qpos, d_offq, edge_hit, d_offp, overlap_hit, inl, d_addend, d_out);
     std::vector<double> h(16 * static_cast<size_t>(K));
     VF_TRY(cudaMemcpyAsync(h.data(), d_out, h.size() * sizeof(double), cudaMemcpyDeviceToHost, stream));
+    mark("kernels enqueued");
     VF_TRY(cudaStreamSynchronize(stream));
+    mark("done");
 #undef VF_TRY
     cleanup();
     for (int k = 0; k < K; ++k) {

@@ -524,19 +524,43 @@ def verify_batch(earlier: Sequence[PointCloud], later: Sequence[PointCloud], pos
     """Loop verification of a batch of pairs in one device pass (include/loopkit_b200.h lk_verify_batch)."""
     p = params or VerifyParams()
     n = len(earlier)
-    ci = (abi.lk_cloud * max(n, 1))(*[c.as_c() for c in earlier])
-    cj = (abi.lk_cloud * max(n, 1))(*[c.as_c() for c in later])
-    pack = lambda ts: np.ascontiguousarray(np.stack([t.packed() for t in ts]) if n else np.zeros((1, 12)))
-    ti, tj, tm = pack(pose_earlier), pack(pose_later), pack(measurement)
+    ci, cj = _cloud_table(earlier), _cloud_table(later)
+    ti, tj, tm = _pack_transforms(pose_earlier), _pack_transforms(pose_later), _pack_transforms(measurement)
     cp = abi.lk_verify_params(epsilon=float(p.epsilon), overlap_radius=float(p.overlap_radius), d_max=float(p.d_max),
                               grid_cell=float(p.grid_cell), normal_angle_max=float(p.normal_angle_max),
                               device=int(p.device), reserved=0)
     out = (abi.lk_verify_result * max(n, 1))()
-    check(abi.lib().lk_verify_batch(ci, cj, ti.ctypes.data_as(abi.dptr), tj.ctypes.data_as(abi.dptr),
-                                    tm.ctypes.data_as(abi.dptr), n, C.byref(cp), out))
-    return [VerifyResult(EdgeInfo(np.array(out[k].info[:]).reshape(6, 6), int(out[k].pair_count)),
-                         int(out[k].overlap_hits), float(out[k].overlap), int(out[k].inliers),
-                         float(out[k].inlier_ratio), float(out[k].fitness)) for k in range(n)]
+    check(abi.lib().lk_verify_batch(ci.ctypes.data_as(C.POINTER(abi.lk_cloud)),
+                                    cj.ctypes.data_as(C.POINTER(abi.lk_cloud)), ti.ctypes.data_as(abi.dptr),
+                                    tj.ctypes.data_as(abi.dptr), tm.ctypes.data_as(abi.dptr), n, C.byref(cp), out))
+    r = np.ctypeslib.as_array(out)[:n]
+    info = np.array(r["info"]).reshape(-1, 6, 6)
+    cols = [r[f].tolist() for f in ("pair_count", "overlap_hits", "overlap", "inliers", "inlier_ratio", "fitness")]
+    return [VerifyResult(EdgeInfo(info[k], pc), oh, ov, il, ir, ft)
+            for k, (pc, oh, ov, il, ir, ft) in enumerate(zip(*cols))]
+
+
+def _pack_transforms(ts) -> np.ndarray:
+    """(n, 12) row-major R then t per transform (RigidTransform.packed, batched)."""
+    if not len(ts):
+        return np.zeros((1, 12))
+    out = np.empty((len(ts), 12))
+    out[:, :9] = np.array([t.rotation for t in ts], dtype=np.float64).reshape(-1, 9)
+    out[:, 9:] = np.array([t.translation for t in ts], dtype=np.float64).reshape(-1, 3)
+    return out
+
+
+def _cloud_table(clouds) -> np.ndarray:
+    """lk_cloud[] as an (n, 3) int64 table (xyz, nxyz, n): one array instead
+    of a ctypes object per cloud."""
+    t = np.zeros((max(len(clouds), 1), 3), dtype=np.int64)
+    for k, c in enumerate(clouds):
+        m = c.positions.shape[0]
+        t[k, 0] = c.positions.ctypes.data if m else 0
+        nrm = c.normals
+        t[k, 1] = nrm.ctypes.data if nrm is not None and nrm.shape[0] > 0 else 0
+        t[k, 2] = m
+    return t
 
 
 # ------------------------------------------------------- ICP (north-star item 4)
