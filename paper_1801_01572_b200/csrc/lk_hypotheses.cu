@@ -1274,6 +1274,16 @@ constexpr int kCtaThreads = 256;
 constexpr int kCtaWarps = kCtaThreads / 32;
 constexpr int kCtaPer = 8;                         // points per thread per round
 constexpr int kCtaPts = kCtaThreads * kCtaPer;     // points per round
+// points per (candidate, unit) work item of k_score_units. Shorter units were
+// measured slower (125k / 250k / 500k hypotheses per rank: 256 points 0.213 /
+// 0.304 / 0.480 ms, 512: 0.189 / 0.250 / 0.371, 1024: 0.178 / 0.226 / 0.318,
+// 2048: 0.182 / 0.226 / 0.299): per-unit setup and the lost early exits cost
+// more than the shorter unit latency saves.
+#ifndef LK_UNIT_PTS
+#define LK_UNIT_PTS 2048
+#endif
+constexpr int kUnitPts = LK_UNIT_PTS;
+static_assert(kUnitPts % kCtaThreads == 0 && kUnitPts <= kCtaPts, "unit = whole thread rows of a round");
 constexpr int kCtaWords = kCtaPts / 32;            // ballot words per round (32 or 64)
 static_assert(kCtaWords % 32 == 0, "ballot words come in warp-sized groups");
 constexpr int kCtaSlow = 0xffff;                   // queue count tag: exact FP64 fallback
@@ -1730,7 +1740,7 @@ __device__ __forceinline__ void units_body(CtaSmem& S, const SourceView& src, co
     const int64_t n_cand = n_all >= unit_threshold ? 0 : (n_all < cap ? n_all : cap);
     const int64_t ns = src.n;
     const int32_t n_chunks = static_cast<int32_t>(ns_pad / 32);
-    const int64_t R = (ns + kCtaPts - 1) / kCtaPts;
+    const int64_t R = (ns + kUnitPts - 1) / kUnitPts;  // units per candidate
     const int64_t n_units = n_cand * R;
     // thread 0's books: the CTA best (fitness exact when best_eb == 0)
     BestRec best{0, 0, 0.0, INT64_MAX, -1};
@@ -1749,7 +1759,8 @@ __device__ __forceinline__ void units_body(CtaSmem& S, const SourceView& src, co
         const int64_t u = S.cand;
         if (u >= n_units) break;
         const int64_t c = u / R;
-        const int64_t base = (u - c * R) * kCtaPts;
+        const int64_t base = (u - c * R) * kUnitPts;
+        const int64_t ns_u = base + kUnitPts < ns ? base + kUnitPts : ns;  // the unit's end
         if (threadIdx.x < 12) {
             const double v = __ldg(cand_rt + 12 * c + threadIdx.x);
             if (threadIdx.x < 9) {
@@ -1764,10 +1775,10 @@ __device__ __forceinline__ void units_body(CtaSmem& S, const SourceView& src, co
         __syncthreads();
         double part = 0.0;
         double* add = u_add + c * ns_pad;
-        score_round_ab(S, src, g, sp, cand_rt + 12 * c, base, 0, ns, add, part);
+        score_round_ab(S, src, g, sp, cand_rt + 12 * c, base, 0, ns_u, add, part);
         // publish the round: ballots, the partial sum, then the unit count
         const int32_t w0 = static_cast<int32_t>(base / 32);
-        if (threadIdx.x < kCtaWords && w0 + static_cast<int32_t>(threadIdx.x) < n_chunks) {
+        if (threadIdx.x < kUnitPts / 32 && w0 + static_cast<int32_t>(threadIdx.x) < n_chunks) {
             u_miss[c * n_chunks + w0 + threadIdx.x] = S.miss[0][threadIdx.x];
             u_inl[c * n_chunks + w0 + threadIdx.x] = S.inl[0][threadIdx.x];
         }
