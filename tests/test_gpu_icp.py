@@ -66,3 +66,36 @@ def test_icp_errors():
                               lk.RigidTransform(np.eye(3), np.zeros(3)))
     with pytest.raises(lk.EmptyCloud):
         lk.icp_point_to_plane(lk.PointCloud(np.zeros((0, 3))), pair.target, lk.RigidTransform(np.eye(3), np.zeros(3)))
+
+
+def test_icp_exact_ties_take_the_lower_index(oracle):
+    """Every target point twice, the copy (higher index) with a different
+    normal: each query meets an exact distance tie, which the reference's
+    (d2, index) order gives to the original. Exercises the band re-scan of the
+    warp-cooperative ring walk."""
+    pair = synth.surface_pair(seed=4, density=600.0, noise=0.002)
+    P, N = pair.target.positions, pair.target.normals
+    tilt = synth.transform_from_twist([0.3, -0.2, 0.1, 0.0, 0.0, 0.0]).rotation
+    tgt = lk.PointCloud(np.vstack([P, P]), np.vstack([N, N @ tilt.T]))
+    dup = synth.RegistrationPair(pair.source, tgt, pair.truth)
+    T0 = _perturbed(pair.truth, [0.01, -0.012, 0.008, 0.01, -0.006, 0.008])
+    dev = _check_same(oracle, dup, T0, 0.05, 12, 1e-10)
+    ref = _check_same(oracle, pair, T0, 0.05, 12, 1e-10)  # the original normals decide
+    assert dev.iterations == ref.iterations and np.array_equal(dev.transform.rotation, ref.transform.rotation)
+
+
+def test_icp_scattered_queries_and_outliers(oracle):
+    """A source with a fifth of its points scattered far and wide (misses, and
+    queries many cells outside the grid) and in shuffled order: warps whose
+    queries span more than the cooperative window fall back to per-lane walks;
+    the result is still the oracle's bit for bit."""
+    pair = synth.surface_pair(seed=5, density=500.0, noise=0.003)
+    rng = np.random.default_rng(11)
+    src = pair.source.positions.copy()
+    k = len(src) // 5
+    idx = rng.choice(len(src), k, replace=False)
+    src[idx] = rng.uniform(-6.0, 6.0, size=(k, 3))
+    src = src[rng.permutation(len(src))]
+    scattered = synth.RegistrationPair(lk.PointCloud(src), pair.target, pair.truth)
+    T0 = _perturbed(pair.truth, [0.01, 0.01, -0.008, 0.005, 0.01, -0.004])
+    _check_same(oracle, scattered, T0, 0.05, 10, 1e-10)

@@ -330,6 +330,30 @@ def test_score_candidates_dense_target_matches_oracle(oracle):
             assert sc.best.hypothesis_index == ref["best"].hypothesis_index
 
 
+def test_score_candidates_dense_target_exact_ties(oracle):
+    # a dense target (ring grid) holding every point twice, the copy with a
+    # tilted normal: each neighbour query ties exactly and the reference's
+    # (d2, index) order picks the original, so the normal gate sees the
+    # original normal -- through the warp-cooperative walk's band re-scan
+    pair = synth.depth_frame_pair()
+    P, N = pair.target.positions[::3], pair.target.normals[::3]
+    tilt = synth.transform_from_twist([0.0, 0.9, 0.0, 0.0, 0.0, 0.0]).rotation
+    tgt = lk.PointCloud(np.vstack([P, P]), np.vstack([N, N @ tilt.T]))
+    assert tgt.size() >= 65536  # the ring-grid path
+    src = lk.PointCloud(pair.source.positions[::7], pair.source.normals[::7])
+    rt, _ = synth.lattice_candidates(pair.truth, step_rad=math.pi / 180, step_m=0.01, half_rot=1, half_trans=0)
+    params = lk.RegistrationParams()
+    grid = lk.build_eval_grid(tgt, params.d_max)
+    sc = lk.score_candidates(grid, src, rt, params, early_exit=False)
+    ref = oracle.score_candidates(src.positions, src.normals, tgt.positions, tgt.normals, rt, 0, 0, 0.0,
+                                  oracle.params_from(params))
+    assert np.array_equal(sc.inliers, ref["inliers"])
+    assert np.array_equal(sc.fitness, ref["fitness"])
+    assert sc.qualified == ref["qualified"]
+    if sc.best:
+        assert sc.best.hypothesis_index == ref["best"].hypothesis_index
+
+
 @pytest.mark.parametrize("fp64_only", ["0", "1"])
 @pytest.mark.parametrize("kind", [0, 1])
 def test_fast_path_and_fp64_path_match_oracle(oracle, monkeypatch, fp64_only, kind):
