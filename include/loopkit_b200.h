@@ -40,6 +40,7 @@ typedef enum lk_status {
     LK_INVALID_ARGUMENT = 8,    /* Error (bad cell length / leaf, null pointers) */
     LK_CUDA_ERROR = 9,
     LK_NCCL_ERROR = 10,
+    LK_ROTATION_TOO_LARGE = 11, /* RotationTooLarge (twist_from_transform at >= pi/2) */
     LK_INTERNAL_ERROR = 99
 } lk_status;
 
@@ -235,6 +236,27 @@ typedef struct lk_verify_result {
 
 lk_status lk_verify_batch(const lk_cloud* clouds_i, const lk_cloud* clouds_j, const double* Ti, const double* Tj,
                           const double* T, int64_t n_pairs, const lk_verify_params* params, lk_verify_result* out);
+
+/* ---- line-process weight of a loop edge (host; consumer of edge_info) -----
+ * Transforms are 12 doubles (row-major R, then t); info is the row-major 6x6
+ * of lk_verify_result / lk_edge_info_batched.
+ *   lk_edge_residual  f = xi^T Lambda xi, xi = twist(rel * T_j^-1 * T_i)
+ *                     line_process.cpp:35-40 (twist: geometry.cpp:28-40);
+ *                     LK_ROTATION_TOO_LARGE when the residual rotation
+ *                     reaches pi/2.
+ *   lk_update_weight  (mu / (mu + max(f, 0)))^2 clamped to [0, 1]; 0 when
+ *                     mu <= 0                         line_process.cpp:42-46
+ *   lk_loop_weights   per edge: mu = mu_tau * pair_count, the residual with
+ *                     the small-angle gate of loop_residual (weight 0 beyond
+ *                     pi/2), the weight, and accepted = weight >= threshold
+ *                     line_process.cpp:52-67, 100-103 (labels at given poses)
+ * Host-only arithmetic in the reference's evaluation order (libm asin /
+ * atan2 / acos); no device is used. */
+lk_status lk_edge_residual(const double* Ti, const double* Tj, const double* rel, const double* info36, double* f);
+double lk_update_weight(double f, double mu);
+lk_status lk_loop_weights(int64_t n, const double* Ti, const double* Tj, const double* rel, const double* info36,
+                          const int64_t* pair_count, double mu_tau, double threshold, double* weight,
+                          int32_t* accepted);
 
 /* ---- feature pre-match (registration.cpp:248 -> grid.cpp:176-213) ---------
  * argmin_j ||F(p_i) - F(q_j)||^2 in FP64, ties -> lowest j. */

@@ -231,6 +231,30 @@ EdgeInfo edge_info(const Cloud& cloud_i, const Cloud& cloud_j, const Transform& 
     return out;
 }
 
+// Line-process weight of a loop edge (line_process.cpp:35-46), host-only:
+// f = xi^T Lambda xi with xi = twist(rel * t_j^-1 * t_i) (a residual rotation
+// of pi/2 or more maps to E::Base via LK_ROTATION_TOO_LARGE), and the closed
+// form weight (mu / (mu + f))^2.
+template <class E = DefaultErrors>
+inline double edge_residual(const Transform& t_i, const Transform& t_j, const Transform& rel, const EdgeInfo& info) {
+    double a[12], b[12], r[12];
+    for (int k = 0; k < 9; ++k) {
+        a[k] = t_i.R[k];
+        b[k] = t_j.R[k];
+        r[k] = rel.R[k];
+    }
+    for (int k = 0; k < 3; ++k) {
+        a[9 + k] = t_i.t[k];
+        b[9 + k] = t_j.t[k];
+        r[9 + k] = rel.t[k];
+    }
+    double f = 0.0;
+    const lk_status st = lk_edge_residual(a, b, r, info.info, &f);
+    if (st != LK_OK) throw_status<E>(st);
+    return f;
+}
+inline double update_weight(double f, double mu) { return lk_update_weight(f, mu); }
+
 // ICP point-to-plane refinement of `init` (source -> target); DESIGN.md "ICP".
 struct IcpResult {
     Transform transform;

@@ -6,7 +6,8 @@ CUDA kernels behind the C ABI in include/loopkit_b200.h, with this package as
 the Python mirror of the reference interface.
 """
 from .errors import (CudaError, DegenerateConfiguration, EmptyCloud, Error, MissingData, MissingNormals,
-                     NoCorrespondences, ParseError, TooFewPoints)
+                     NoCorrespondences, ParseError, RotationTooLarge, TooFewPoints)
+from .line_process import edge_residual, loop_weights, update_weight
 from .evaluation import (LogEntry, RegistrationScore, eval_registration, log_entry, read_registration_log,
                          write_registration_log)
 from .registration import (CandidateScores, DeviceGrid, EdgeInfo, EvalGrid, HypothesisStats, IcpParams, IcpResult,

@@ -26,6 +26,7 @@ LK_DEGENERATE = 7
 LK_INVALID_ARGUMENT = 8
 LK_CUDA_ERROR = 9
 LK_NCCL_ERROR = 10
+LK_ROTATION_TOO_LARGE = 11
 LK_INTERNAL_ERROR = 99
 
 dptr = C.POINTER(C.c_double)
@@ -188,6 +189,10 @@ SIGNATURES = {
     "lk_edge_info_batched": (C.c_int, [C.POINTER(lk_cloud), C.POINTER(lk_cloud), dptr, dptr, C.c_int64, C.c_double,
                                        C.c_int32, dptr, i64ptr]),
     "lk_feature_nn_cache": (C.c_int, [fptr, C.c_int64, fptr, C.c_int64, C.c_int32, i32ptr]),
+    "lk_edge_residual": (C.c_int, [dptr, dptr, dptr, dptr, dptr]),
+    "lk_update_weight": (C.c_double, [C.c_double, C.c_double]),
+    "lk_loop_weights": (C.c_int, [C.c_int64, dptr, dptr, dptr, dptr, C.POINTER(C.c_int64), C.c_double, C.c_double,
+                                  dptr, C.POINTER(C.c_int32)]),
     "lk_verify_batch": (C.c_int, [C.POINTER(lk_cloud), C.POINTER(lk_cloud), dptr, dptr, dptr, C.c_int64,
                                   C.POINTER(lk_verify_params), C.POINTER(lk_verify_result)]),
     "lk_icp_point_to_plane": (C.c_int, [C.POINTER(lk_cloud), C.POINTER(lk_cloud), dptr, C.POINTER(lk_icp_params),

@@ -1233,4 +1233,90 @@ lk_status lk_compute_fpfh(const lk_cloud* cloud, double radius, int32_t threads,
     });
 }
 
+// ---- line-process weight (row a11; host) -----------------------------------
+namespace {
+
+lk::Rigid rigid12(const double* T) {
+    lk::Rigid r;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) r.R.m[i][j] = T[3 * i + j];
+    r.t = {T[9], T[10], T[11]};
+    return r;
+}
+
+// rotation_angle (geometry.cpp:23-26)
+double rotation_angle(const lk::Mat3& r) {
+    const double c = ((r.m[0][0] + r.m[1][1]) + r.m[2][2] - 1.0) / 2.0;
+    return std::acos(std::clamp(c, -1.0, 1.0));
+}
+
+// xi = twist(rel * T_j^-1 * T_i) (line_process.cpp:37-38, geometry.cpp:28-40);
+// false when the rotation angle reaches pi/2 (RotationTooLarge)
+bool residual_twist(const double* Ti, const double* Tj, const double* rel, double xi[6]) {
+    const lk::Rigid d = lk::compose(rigid12(rel), lk::compose(lk::inverse(rigid12(Tj)), rigid12(Ti)));
+    if (rotation_angle(d.R) >= M_PI / 2.0) return false;
+    xi[1] = std::asin(std::clamp(d.R.m[0][2], -1.0, 1.0));  // beta
+    xi[0] = std::atan2(-d.R.m[1][2], d.R.m[2][2]);          // alpha
+    xi[2] = std::atan2(-d.R.m[0][1], d.R.m[0][0]);          // gamma
+    xi[3] = d.t.x;
+    xi[4] = d.t.y;
+    xi[5] = d.t.z;
+    return true;
+}
+
+// xi . (Lambda xi): rows of Lambda xi accumulated in column order, then the
+// dot in index order (Eigen's packet order may differ in the last bits; the
+// accept decision l >= threshold is not that sensitive)
+double quad_form(const double* info36, const double xi[6]) {
+    double y[6];
+    for (int i = 0; i < 6; ++i) {
+        double a = info36[6 * i] * xi[0];
+        for (int k = 1; k < 6; ++k) a += info36[6 * i + k] * xi[k];
+        y[i] = a;
+    }
+    double f = xi[0] * y[0];
+    for (int k = 1; k < 6; ++k) f += xi[k] * y[k];
+    return f;
+}
+
+double update_weight(double f, double mu) {  // line_process.cpp:42-46
+    if (!(mu > 0.0)) return 0.0;
+    const double r = mu / (mu + std::max(f, 0.0));
+    return std::clamp(r * r, 0.0, 1.0);
+}
+
+}  // namespace
+
+lk_status lk_edge_residual(const double* Ti, const double* Tj, const double* rel, const double* info36, double* f) {
+    return guarded([&]() -> lk_status {
+        if (!Ti || !Tj || !rel || !info36 || !f) return fail(LK_INVALID_ARGUMENT, "null argument");
+        double xi[6];
+        if (!residual_twist(Ti, Tj, rel, xi))
+            return fail(LK_ROTATION_TOO_LARGE, "twist_from_transform: rotation angle >= pi/2");
+        *f = quad_form(info36, xi);
+        return LK_OK;
+    });
+}
+
+double lk_update_weight(double f, double mu) { return update_weight(f, mu); }
+
+lk_status lk_loop_weights(int64_t n, const double* Ti, const double* Tj, const double* rel, const double* info36,
+                          const int64_t* pair_count, double mu_tau, double threshold, double* weight,
+                          int32_t* accepted) {
+    return guarded([&]() -> lk_status {
+        if (n < 0 || (n > 0 && (!Ti || !Tj || !rel || !info36 || !pair_count || !weight)))
+            return fail(LK_INVALID_ARGUMENT, "null argument");
+        for (int64_t k = 0; k < n; ++k) {
+            const double mu = mu_tau * static_cast<double>(pair_count[k]);
+            double xi[6];
+            // loop_residual (line_process.cpp:52-60): outside the small-angle
+            // regime the edge gets weight 0
+            const bool ok = residual_twist(Ti + 12 * k, Tj + 12 * k, rel + 12 * k, xi);
+            weight[k] = ok ? update_weight(quad_form(info36 + 36 * k, xi), mu) : 0.0;
+            if (accepted) accepted[k] = weight[k] >= threshold ? 1 : 0;
+        }
+        return LK_OK;
+    });
+}
+
 }  // extern "C"

@@ -66,6 +66,7 @@ _BY_STATUS = {
     abi.LK_INVALID_ARGUMENT: Error,
     abi.LK_CUDA_ERROR: CudaError,
     abi.LK_NCCL_ERROR: NcclError,
+    abi.LK_ROTATION_TOO_LARGE: RotationTooLarge,
     abi.LK_INTERNAL_ERROR: Error,
 }
 

@@ -73,3 +73,21 @@ def test_verify_batch_errors():
     with pytest.raises(lk.MissingNormals):
         lk.verify_batch([lk.PointCloud(pair.target.positions)], [pair.source], [I], [I], [I])
     assert lk.verify_batch([], [], [], [], []) == []
+
+
+def test_verified_loops_weighted_by_the_line_process():
+    """Row a11 on top of the batch: the truth measurement of a pair is kept
+    (residual 0, weight 1), a measurement off by 0.5 rad / 0.6 m is rejected."""
+    pairs = [synth.synth_registration_pair(s) for s in (2, 3)]
+    Q = [p.target for p in pairs]
+    P = [p.source for p in pairs]
+    I = [lk.RigidTransform()] * 2
+    Tj = [p.truth for p in pairs]
+    out = lk.verify_batch(Q, P, I, Tj, Tj, lk.VerifyParams())
+    off = synth.compose(synth.transform_from_twist([0.5, 0.0, 0.0, 0.6, 0.0, 0.0]), pairs[1].truth)
+    # consistent measurement: rel = T_i^-1 T_j (residual rel T_j^-1 T_i = identity)
+    rel = [synth.compose(synth.inverse(I[0]), Tj[0]), synth.compose(off, synth.compose(synth.inverse(Tj[1]), Tj[1]))]
+    w, acc = lk.loop_weights(I, Tj, rel, [o.info for o in out])
+    assert out[0].info.pair_count > 0 and out[1].info.pair_count > 0
+    assert w[0] == pytest.approx(1.0, abs=1e-9) and acc[0]
+    assert w[1] < 0.25 and not acc[1]
