@@ -70,6 +70,24 @@ struct Best3 {
     float f2;
 };
 
+// packed FP32 pairs (sm_100a FADD2 / FFMA2): lo = first, hi = second
+__device__ __forceinline__ unsigned long long pack2(float lo, float hi) {
+    return (static_cast<unsigned long long>(__float_as_uint(hi)) << 32) | __float_as_uint(lo);
+}
+__device__ __forceinline__ float2 unpack2(unsigned long long v) {
+    return make_float2(__uint_as_float(static_cast<unsigned>(v)), __uint_as_float(static_cast<unsigned>(v >> 32)));
+}
+__device__ __forceinline__ unsigned long long sub2(unsigned long long a, unsigned long long b) {
+    unsigned long long r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ unsigned long long fma2(unsigned long long a, unsigned long long b, unsigned long long c) {
+    unsigned long long r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+
 __device__ __forceinline__ float feat_d2f(const float4* a, const float4* b) {
     float acc = 0.0f;
 #pragma unroll
@@ -125,26 +143,30 @@ __global__ void __launch_bounds__(kFnnThreads) k_fnn_partial(const float4* __res
             }
         };
         int jj = 0;
-        // four targets at a time, two partial sums each: eight independent
-        // FMA chains (any summation order stays within the 2.2e-6 bound the
-        // near-tie rescan assumes)
+        // four targets at a time, two partial sums each (bins x, z and y, w of
+        // every float4): eight independent FMA chains, run as packed FP32x2
+        // pairs (FADD2 / FFMA2: one instruction per two bins). Any summation
+        // order stays within the 2.2e-6 bound the near-tie rescan assumes.
         for (; jj + 4 <= tile; jj += 4) {
-            float a[4][2] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+            unsigned long long a[4] = {0ull, 0ull, 0ull, 0ull};  // (even, odd) partial sums
 #pragma unroll
             for (int q = 0; q < kFnnPad / 4; ++q) {
                 const float4 x = s[q];
+                const unsigned long long xlo = pack2(x.x, x.y), xhi = pack2(x.z, x.w);
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     const float4 y = s_t[(jj + u) * (kFnnPad / 4) + q];
-                    float d;
-                    d = x.x - y.x; a[u][0] = fmaf(d, d, a[u][0]);
-                    d = x.y - y.y; a[u][1] = fmaf(d, d, a[u][1]);
-                    d = x.z - y.z; a[u][0] = fmaf(d, d, a[u][0]);
-                    d = x.w - y.w; a[u][1] = fmaf(d, d, a[u][1]);
+                    const unsigned long long dlo = sub2(xlo, pack2(y.x, y.y));
+                    a[u] = fma2(dlo, dlo, a[u]);
+                    const unsigned long long dhi = sub2(xhi, pack2(y.z, y.w));
+                    a[u] = fma2(dhi, dhi, a[u]);
                 }
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) take(a[u][0] + a[u][1], j0 + jj + u);
+            for (int u = 0; u < 4; ++u) {
+                const float2 v = unpack2(a[u]);
+                take(v.x + v.y, j0 + jj + u);
+            }
         }
         for (; jj < tile; ++jj) take(feat_d2f(s, s_t + jj * (kFnnPad / 4)), j0 + jj);
     }
