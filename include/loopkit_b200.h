@@ -297,6 +297,13 @@ lk_status lk_icp_point_to_plane(const lk_cloud* source, const lk_cloud* target, 
 
 /* host-side helpers of prepare (this tier) */
 lk_status lk_voxel_downsample(const lk_cloud* cloud, double leaf, double* out_xyz, double* out_n, int64_t* out_count);
+/* estimate_normals (preprocess.hpp / preprocess.cpp:61-96): out_normals n x 3,
+ * oriented toward viewpoint (3 doubles; NULL = origin), zero where fewer than
+ * 3 points lie within radius. register_global / lk_reg_prepare call it with
+ * normal_radius and the origin for clouds given without normals
+ * (registration.cpp:232-237). */
+lk_status lk_estimate_normals(const lk_cloud* cloud, double radius, const double* viewpoint, int32_t device,
+                              double* out_normals);
 lk_status lk_compute_fpfh(const lk_cloud* cloud, double radius, int32_t threads, float* out);
 
 #ifdef __cplusplus

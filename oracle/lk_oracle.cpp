@@ -792,6 +792,186 @@ static int bin_index(double value, double lo, double hi) {
     return std::clamp(b, 0, 10);
 }
 // fpfh.cpp:57-141
+// ---- estimate_normals (proj/src/preprocess.cpp:61-96) ----------------------
+// Eigen::SelfAdjointEigenSolver<Matrix3d> restated (Eigen 3.4 source order;
+// Eigen is absent here, so this is the builder's statement of it -- the
+// normals' parity with the reference binary is unpinned):
+// SelfAdjointEigenSolver::compute, tridiagonalization_inplace_selector<3>,
+// computeFromTridiagonal_impl, tridiagonal_qr_step, JacobiRotation::makeGivens,
+// applyOnTheRight (rotation transposed), numext::hypot.
+namespace eig3 {
+static double eabs(double x) { return std::fabs(x); }
+static double ehypot(double x, double y) {
+    x = eabs(x);
+    y = eabs(y);
+    if (std::isinf(x) || std::isinf(y)) return HUGE_VAL;
+    if (std::isnan(x) || std::isnan(y)) return x + y;
+    const double p = std::max(x, y);
+    if (p == 0.0) return 0.0;
+    const double qp = std::min(y, x) / p;
+    return p * std::sqrt(1.0 + qp * qp);
+}
+static void givens(double p, double q, double& c, double& s) {
+    if (q == 0.0) {
+        c = p < 0.0 ? -1.0 : 1.0;
+        s = 0.0;
+    } else if (p == 0.0) {
+        c = 0.0;
+        s = q < 0.0 ? 1.0 : -1.0;
+    } else if (eabs(p) > eabs(q)) {
+        const double t = q / p;
+        double u = std::sqrt(1.0 + t * t);
+        if (p < 0.0) u = -u;
+        c = 1.0 / u;
+        s = -t * c;
+    } else {
+        const double t = p / q;
+        double u = std::sqrt(1.0 + t * t);
+        if (q < 0.0) u = -u;
+        s = -1.0 / u;
+        c = -t * s;
+    }
+}
+// eivec: column-major, e[col][row]
+static void qr_step(double* d, double* e, int start, int end, double ev[3][3]) {
+    const double td = (d[end - 1] - d[end]) * 0.5;
+    const double ee = e[end - 1];
+    double mu = d[end];
+    if (td == 0.0) {
+        mu -= eabs(ee);
+    } else if (ee != 0.0) {
+        const double e2 = ee * ee;
+        const double h = ehypot(td, ee);
+        if (e2 == 0.0) mu -= ee / ((td + (td > 0.0 ? h : -h)) / ee);
+        else mu -= e2 / (td + (td > 0.0 ? h : -h));
+    }
+    double x = d[start] - mu, z = e[start];
+    for (int k = start; k < end && z != 0.0; ++k) {
+        double c, s;
+        givens(x, z, c, s);
+        const double sdk = s * d[k] + c * e[k];
+        const double dkp1 = s * e[k] + c * d[k + 1];
+        d[k] = c * (c * d[k] - s * e[k]) - s * (c * e[k] - s * d[k + 1]);
+        d[k + 1] = s * sdk + c * dkp1;
+        e[k] = c * sdk - s * dkp1;
+        if (k > start) e[k - 1] = c * e[k - 1] - s * z;
+        x = e[k];
+        if (k < end - 1) {
+            z = -s * e[k + 1];
+            e[k + 1] = c * e[k + 1];
+        }
+        // Q = Q * G: applyOnTheRight(k, k+1, rot) = rotation in the plane with (c, -s)
+        for (int r = 0; r < 3; ++r) {
+            const double xi = ev[k][r], yi = ev[k + 1][r];
+            ev[k][r] = c * xi + -s * yi;
+            ev[k + 1][r] = -(-s) * xi + c * yi;
+        }
+    }
+}
+// column 0 of the eigenvector matrix of the symmetric A (lower triangle used)
+static V3 smallest_eigenvector(const double A[3][3]) {
+    double m[3][3];
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) m[r][c] = c <= r ? A[r][c] : 0.0;  // triangularView<Lower>
+    double scale = 0.0;
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c <= r; ++c) scale = std::max(scale, eabs(m[r][c]));
+    if (scale == 0.0) scale = 1.0;
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c <= r; ++c) m[r][c] /= scale;
+    double d[3], e[2], ev[3][3];
+    d[0] = m[0][0];
+    const double v1norm2 = m[2][0] * m[2][0];
+    if (v1norm2 <= std::numeric_limits<double>::min()) {
+        d[1] = m[1][1];
+        d[2] = m[2][2];
+        e[0] = m[1][0];
+        e[1] = m[2][1];
+        for (int c = 0; c < 3; ++c)
+            for (int r = 0; r < 3; ++r) ev[c][r] = r == c ? 1.0 : 0.0;
+    } else {
+        const double beta = std::sqrt(m[1][0] * m[1][0] + v1norm2);
+        const double inv = 1.0 / beta;
+        const double m01 = m[1][0] * inv, m02 = m[2][0] * inv;
+        const double q = 2.0 * m01 * m[2][1] + m02 * (m[2][2] - m[1][1]);
+        d[1] = m[1][1] + m02 * q;
+        d[2] = m[2][2] - m02 * q;
+        e[0] = beta;
+        e[1] = m[2][1] - m01 * q;
+        const double Q[3][3] = {{1, 0, 0}, {0, m01, m02}, {0, m02, -m01}};  // rows; symmetric
+        for (int c = 0; c < 3; ++c)
+            for (int r = 0; r < 3; ++r) ev[c][r] = Q[r][c];
+    }
+    const int n = 3;
+    int end = n - 1, start = 0, iter = 0;
+    const double considerAsZero = std::numeric_limits<double>::min();
+    const double precision_inv = 1.0 / std::numeric_limits<double>::epsilon();
+    while (end > 0) {
+        for (int i = start; i < end; ++i) {
+            if (eabs(e[i]) < considerAsZero) {
+                e[i] = 0.0;
+            } else {
+                const double sc = precision_inv * e[i];
+                if (sc * sc <= (eabs(d[i]) + eabs(d[i + 1]))) e[i] = 0.0;
+            }
+        }
+        while (end > 0 && e[end - 1] == 0.0) end--;
+        if (end <= 0) break;
+        iter++;
+        if (iter > 30 * n) break;
+        start = end - 1;
+        while (start > 0 && e[start - 1] != 0.0) start--;
+        qr_step(d, e, start, end, ev);
+    }
+    if (iter <= 30 * n) {
+        for (int i = 0; i < n - 1; ++i) {
+            int k = 0;
+            for (int j = 1; j < n - i; ++j)
+                if (d[i + j] < d[i + k]) k = j;
+            if (k > 0) {
+                std::swap(d[i], d[k + i]);
+                for (int r = 0; r < 3; ++r) std::swap(ev[i][r], ev[k + i][r]);
+            }
+        }
+    }
+    return V3{ev[0][0], ev[0][1], ev[0][2]};
+}
+}  // namespace eig3
+
+static Cloud estimate_normals(const Cloud& cloud, double radius, V3 viewpoint, int threads) {
+    if (cloud.pos.empty()) fail(OR_EMPTY_CLOUD, "estimate_normals: empty cloud");
+    if (!(radius > 0.0)) fail(OR_INVALID_ARGUMENT, "build_grid: cell_length must be positive");
+    SearchGrid grid = build_grid(cloud.pos, radius, V3{});
+    Cloud out;
+    out.pos = cloud.pos;
+    out.nrm.assign(cloud.size(), V3{});
+    const int n = static_cast<int>(cloud.size());
+    if (threads <= 0) threads = omp_get_max_threads();
+#pragma omp parallel for schedule(static) num_threads(threads)
+    for (int i = 0; i < n; ++i) {
+        const V3 p = cloud.pos[static_cast<size_t>(i)];
+        std::vector<int> nbrs = radius_search(grid, p, radius);
+        if (nbrs.size() < 3) continue;
+        V3 mean{};
+        for (int j : nbrs) mean = add(mean, cloud.pos[static_cast<size_t>(j)]);
+        mean = divs(mean, static_cast<double>(nbrs.size()));
+        double cov[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+        for (int j : nbrs) {
+            const V3 dd = sub(cloud.pos[static_cast<size_t>(j)], mean);
+            const double dv[3] = {dd.x, dd.y, dd.z};
+            for (int r = 0; r < 3; ++r)
+                for (int c = 0; c < 3; ++c) cov[r][c] = cov[r][c] + dv[r] * dv[c];
+        }
+        V3 normal = eig3::smallest_eigenvector(cov);
+        const double len = norm(normal);
+        if (!(len > 0.0) || !std::isfinite(len)) continue;
+        normal = divs(normal, len);
+        if (dot(normal, sub(viewpoint, p)) < 0.0) normal = neg(normal);
+        out.nrm[static_cast<size_t>(i)] = normal;
+    }
+    return out;
+}
+
 static std::vector<std::array<float, 33>> compute_fpfh(const Cloud& cloud, double radius, int threads) {
     if (cloud.pos.empty()) fail(OR_EMPTY_CLOUD, "compute_fpfh: empty cloud");
     if (!cloud.has_normals()) fail(OR_MISSING_NORMALS, "compute_fpfh: cloud has no normals");
@@ -902,10 +1082,8 @@ static Context* prepare(const Cloud& src_in, const Cloud& tgt_in, const or_param
     ctx->target = voxel_downsample(tgt_in, p.leaf);
     if (ctx->source.size() < 4 || ctx->target.size() < 4)
         fail(OR_TOO_FEW_POINTS, "register_global: fewer than 4 points after downsampling");
-    // estimate_normals (preprocess.cpp:61-96) is not restated: every fixture on
-    // this path carries normals; normal-less input is rejected.
-    if (!ctx->source.has_normals() || !ctx->target.has_normals())
-        fail(OR_MISSING_NORMALS, "oracle prepare: inputs without normals are not supported");
+    if (!ctx->source.has_normals()) ctx->source = estimate_normals(ctx->source, p.normal_radius, V3{}, p.threads);
+    if (!ctx->target.has_normals()) ctx->target = estimate_normals(ctx->target, p.normal_radius, V3{}, p.threads);
     auto usable = [](const Cloud& c) {
         size_t k = 0;
         for (const V3& nn : c.nrm) k += is_zero(nn) ? 0u : 1u;
@@ -1580,6 +1758,15 @@ int or_voxel_downsample(const double* xyz, const double* nxyz, int64_t n, double
             if (out_n && d.has_normals()) store3(out_n, static_cast<int64_t>(i), d.nrm[i]);
         }
         *out_count = static_cast<int64_t>(d.size());
+    });
+}
+
+int or_estimate_normals(const double* xyz, int64_t n, double radius, const double* viewpoint, int32_t threads,
+                        double* out) {
+    return guarded([&] {
+        Cloud c = estimate_normals(make_cloud(xyz, nullptr, n), radius, viewpoint ? load3(viewpoint, 0) : V3{},
+                                   threads);
+        for (size_t i = 0; i < c.nrm.size(); ++i) store3(out, static_cast<int64_t>(i), c.nrm[i]);
     });
 }
 

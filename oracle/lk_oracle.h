@@ -137,6 +137,8 @@ int or_score_candidates(const double* src_xyz, const double* src_n, int64_t ns, 
 /* ---- preprocessing (preprocess.cpp:14-59, fpfh.cpp:17-141, reference.hpp:56-76) ---- */
 int or_voxel_downsample(const double* xyz, const double* nxyz, int64_t n, double leaf, double* out_xyz,
                         double* out_n, int64_t* out_count);
+int or_estimate_normals(const double* xyz, int64_t n, double radius, const double* viewpoint, int32_t threads,
+                        double* out);
 int or_compute_fpfh(const double* xyz, const double* nxyz, int64_t n, double radius, int32_t threads, float* out);
 int or_feature_nn_cache(const float* sf, int64_t ns, const float* tf, int64_t nt, int32_t threads, int32_t* out);
 

@@ -82,6 +82,7 @@ _SIGS = {
                                       C.c_int32, C.c_double, C.POINTER(or_params), dptr, dptr, i64ptr, i32ptr,
                                       C.POINTER(or_result), i64ptr]),
     "or_voxel_downsample": (C.c_int, [dptr, dptr, C.c_int64, C.c_double, dptr, dptr, i64ptr]),
+    "or_estimate_normals": (C.c_int, [dptr, C.c_int64, C.c_double, dptr, C.c_int32, dptr]),
     "or_compute_fpfh": (C.c_int, [dptr, dptr, C.c_int64, C.c_double, C.c_int32, fptr]),
     "or_feature_nn_cache": (C.c_int, [fptr, C.c_int64, fptr, C.c_int64, C.c_int32, i32ptr]),
     "or_prepare": (C.c_void_p, [dptr, dptr, C.c_int64, dptr, dptr, C.c_int64, C.POINTER(or_params),
@@ -317,6 +318,15 @@ def voxel_downsample(xyz, nrm, leaf):
     _check(lib().or_voxel_downsample(_p(x), _p(n), N, leaf, _p(ox), _p(on), C.byref(cnt)))
     k = cnt.value
     return ox[:k].copy(), (on[:k].copy() if n is not None else None)
+
+
+def estimate_normals(xyz, radius, viewpoint=(0.0, 0.0, 0.0), threads=0):
+    """preprocess.cpp:61-96 (oracle restatement; Eigen's eigensolver restated)."""
+    x = _d(xyz)
+    v = _d(np.asarray(viewpoint, np.float64).reshape(1, 3))
+    out = np.zeros((x.shape[0], 3))
+    _check(lib().or_estimate_normals(_p(x), x.shape[0], radius, _p(v), threads, _p(out)))
+    return out
 
 
 def compute_fpfh(xyz, nrm, radius, threads=0):

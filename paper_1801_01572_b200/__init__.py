@@ -13,7 +13,7 @@ from .evaluation import (LogEntry, RegistrationScore, eval_registration, log_ent
 from .registration import (CandidateScores, DeviceGrid, EdgeInfo, EvalGrid, HypothesisStats, IcpParams, IcpResult,
                            PointCloud,
                            RegistrationContext, RegistrationParams, RegistrationResult, RigidTransform, SearchGrid,
-                           build_eval_grid, build_grid, compute_fpfh, device_count, edge_info, edge_info_batched,
+                           build_eval_grid, build_grid, compute_fpfh, estimate_normals, device_count, edge_info, edge_info_batched,
                            evaluate_hypothesis, feature_nn_cache, icp_point_to_plane, merge_records,
                            prepare_registration,
                            records_from_bytes, register_global, registration_context, run_hypotheses,

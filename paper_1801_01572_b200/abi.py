@@ -197,6 +197,7 @@ SIGNATURES = {
                                   C.POINTER(lk_verify_params), C.POINTER(lk_verify_result)]),
     "lk_icp_point_to_plane": (C.c_int, [C.POINTER(lk_cloud), C.POINTER(lk_cloud), dptr, C.POINTER(lk_icp_params),
                                         C.POINTER(lk_icp_result), dptr]),
+    "lk_estimate_normals": (C.c_int, [C.POINTER(lk_cloud), C.c_double, dptr, C.c_int32, dptr]),
     "lk_voxel_downsample": (C.c_int, [C.POINTER(lk_cloud), C.c_double, dptr, dptr, i64ptr]),
     "lk_compute_fpfh": (C.c_int, [C.POINTER(lk_cloud), C.c_double, C.c_int32, fptr]),
 }

@@ -444,8 +444,8 @@ struct CloudSide {
     std::exception_ptr err;
 };
 
-void prepare_side(CloudSide& cs, double feature_radius, double leaf, lkk::GridStorage* grid, double d_max,
-                  int device, double t0, const char* tag, cudaStream_t grid_stream = nullptr) {
+void prepare_side(CloudSide& cs, double feature_radius, double normal_radius, double leaf, lkk::GridStorage* grid,
+                  double d_max, int device, double t0, const char* tag, cudaStream_t grid_stream = nullptr) {
     auto mark = [&](const char* what) {
         if (trace_level() >= 2) {
             tmark((std::string(tag) + " " + what).c_str(), cs.s, t0);
@@ -459,7 +459,7 @@ void prepare_side(CloudSide& cs, double feature_radius, double leaf, lkk::GridSt
         CK(cudaSetDevice(device));
         const int64_t n = cs.in->n;
         cs.raw_pos = dev_upload(cs.in->xyz, 3 * n, cs.s);
-        cs.raw_nrm = dev_upload(cs.in->nxyz, 3 * n, cs.s);
+        cs.raw_nrm = cs.in->nxyz ? dev_upload(cs.in->nxyz, 3 * n, cs.s) : nullptr;
         mark("upload");
         CK(lkk::pool_alloc(&cs.pos, 3 * n * sizeof(double), cs.s));
         CK(lkk::pool_alloc(&cs.nrm, 3 * n * sizeof(double), cs.s));
@@ -469,6 +469,12 @@ void prepare_side(CloudSide& cs, double feature_radius, double leaf, lkk::GridSt
         cs.raw_pos = cs.raw_nrm = nullptr;
         mark("downsample");
         if (cs.status != 0 || cs.n < 4) return;
+        if (!cs.in->nxyz) {
+            // registration.cpp:232-237: estimate_normals(cloud, normal_radius, origin)
+            const double origin[3] = {0.0, 0.0, 0.0};
+            CK(lkk::estimate_normals(cs.pos, cs.n, normal_radius, origin, cs.nrm, cs.s));
+            mark("normals");
+        }
         // usable normals and |p|max come back with the side's final sync
         thread_local unsigned long long* h_stats = nullptr;
         if (!h_stats) CK(cudaHostAlloc(reinterpret_cast<void**>(&h_stats), 2 * sizeof(unsigned long long), 0));
@@ -528,10 +534,6 @@ lk_status prepare_impl(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_pa
     double t0 = now_s();
     if (src->n == 0 || tgt->n == 0) return fail(LK_EMPTY_CLOUD, "voxel_downsample: empty cloud");
     if (!(params->leaf > 0.0)) return fail(LK_INVALID_ARGUMENT, "voxel_downsample: leaf must be positive");
-    // estimate_normals (preprocess.cpp:61-96) is not part of this tier
-    if (!src->nxyz || !tgt->nxyz)
-        return fail(LK_MISSING_NORMALS,
-                    "register_global: inputs without normals need estimate_normals (not in this tier)");
     lk_reg_ctx* c = ctx_new(params->device);
     tstart(c->own_stream);
     CloudSide S, T;
@@ -548,12 +550,15 @@ lk_status prepare_impl(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_pa
         // side (H2D, downsample, FPFH, EvalGrid) runs on a second host thread
         // and stream while this thread does the source side
         Worker* worker = acquire_worker();
-        const double fr = params->feature_radius, leaf = params->leaf, dm = params->d_max;
+        const double fr = params->feature_radius, nr = params->normal_radius, leaf = params->leaf,
+                     dm = params->d_max;
         const int dev = c->device;
         lkk::GridStorage* grid = &c->grid;
         cudaStream_t gs = c->grid_stream;
-        worker->post([&T, fr, leaf, grid, dm, dev, t0, gs] { prepare_side(T, fr, leaf, grid, dm, dev, t0, "tgt", gs); });
-        prepare_side(S, fr, leaf, nullptr, 0.0, dev, t0, "src");
+        worker->post([&T, fr, nr, leaf, grid, dm, dev, t0, gs] {
+            prepare_side(T, fr, nr, leaf, grid, dm, dev, t0, "tgt", gs);
+        });
+        prepare_side(S, fr, nr, leaf, nullptr, 0.0, dev, t0, "src");
         worker->wait();
         release_worker(worker);
         if (trace_on() && trace_level() < 2)
@@ -1166,6 +1171,41 @@ lk_status lk_feature_nn_cache(const float* src_features, int64_t ns, const float
         cudaFree(d_tf);
         cudaFree(d_out);
         cudaStreamDestroy(s);
+        CK(e);
+        return LK_OK;
+    });
+}
+
+lk_status lk_estimate_normals(const lk_cloud* cloud, double radius, const double* viewpoint, int32_t device,
+                              double* out_normals) {
+    return guarded([&]() -> lk_status {
+        check_cloud_ptr(cloud, "cloud");
+        if (!out_normals) return fail(LK_INVALID_ARGUMENT, "null argument");
+        if (cloud->n == 0) return fail(LK_EMPTY_CLOUD, "estimate_normals: empty cloud");
+        if (!(radius > 0.0)) return fail(LK_INVALID_ARGUMENT, "build_grid: cell_length must be positive");
+        const double origin[3] = {0.0, 0.0, 0.0};
+        const int dev = select_device(device);
+        cudaStream_t s = acquire_stream(dev);
+        double* d_in = nullptr;
+        double* d_out = nullptr;
+        cudaError_t e = cudaSuccess;
+        try {
+            d_in = dev_upload(cloud->xyz, 3 * cloud->n, s);
+            CK(lkk::pool_alloc(&d_out, 3 * cloud->n * sizeof(double), s));
+            e = lkk::estimate_normals(d_in, cloud->n, radius, viewpoint ? viewpoint : origin, d_out, s);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(out_normals, d_out, 3 * cloud->n * sizeof(double), cudaMemcpyDeviceToHost, s);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        } catch (...) {
+            lkk::pool_free(d_in, s);
+            lkk::pool_free(d_out, s);
+            release_stream(dev, s);
+            throw;
+        }
+        lkk::pool_free(d_in, s);
+        lkk::pool_free(d_out, s);
+        cudaStreamSynchronize(s);
+        release_stream(dev, s);
         CK(e);
         return LK_OK;
     });

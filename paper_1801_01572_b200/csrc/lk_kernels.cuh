@@ -339,6 +339,11 @@ cudaError_t exclusive_scan(const int32_t* d_in, int64_t n, int32_t* d_out, cudaS
 // reported through cudaError_t.
 cudaError_t voxel_downsample(const double* d_pos, const double* d_nrm, int64_t n, double leaf, double* d_out_pos,
                              double* d_out_nrm, int64_t* out_count, int* status, cudaStream_t stream);
+// estimate_normals (proj/src/preprocess.cpp:61-96) on the device: n x 3 normals
+// oriented to `viewpoint` (3 doubles, host), zero where fewer than 3
+// neighbours lie within `radius`.
+cudaError_t estimate_normals(const double* d_pos, int64_t n, double radius, const double* viewpoint, double* d_out,
+                             cudaStream_t stream);
 // compute_fpfh (proj/src/fpfh.cpp:57-141) on the device: 33 floats per point.
 cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, double radius, float* d_out,
                          cudaStream_t stream);

@@ -28,6 +28,7 @@
 #include <cub/device/device_radix_sort.cuh>
 
 #include "lk_device_math.cuh"
+#include "lk_eig3.hpp"
 #include "lk_kernels.cuh"
 
 namespace lkk {
@@ -622,6 +623,80 @@ __global__ void __launch_bounds__(32 * kFpfhWarps) k_fpfh(const double* __restri
     }
 }
 
+// estimate_normals (proj/src/preprocess.cpp:61-96), warp per point: the
+// radius_search neighbours (grid.cpp:153-174 with cell = radius: the +-1 cell
+// window and d2 <= r^2, self included, ascending index) are found by a brute
+// scan in index order; the mean and then the covariance are the reference's
+// sequential sums (each hit broadcast to the warp in order); the eigenvector
+// of the smallest eigenvalue (lk_eig3.hpp) is normalised and oriented to the
+// viewpoint. Fewer than 3 neighbours or a non-finite length: zero normal.
+__global__ void __launch_bounds__(32 * kSortWarps) k_estimate_normals(const double* __restrict__ pos,
+                                                                      const int4* __restrict__ cells, int64_t n,
+                                                                      double r2, double vx, double vy, double vz,
+                                                                      double* __restrict__ out) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t i = blockIdx.x * static_cast<int64_t>(kSortWarps) + warp;
+    if (i >= n) return;
+    const V3 p = ld3(pos, i);
+    const int4 ci = cells[i];
+    auto scan = [&](auto&& use) {
+        for (int64_t b = 0; b < n; b += 32) {
+            const int64_t j = b + lane;
+            V3 q = mk(0.0, 0.0, 0.0);
+            bool hit = false;
+            if (j < n) {
+                const int4 cj = __ldg(cells + j);
+                if (abs(cj.x - ci.x) <= 1 && abs(cj.y - ci.y) <= 1 && abs(cj.z - ci.z) <= 1) {
+                    q = ld3(pos, j);
+                    hit = sqnorm(sub(q, p)) <= r2;
+                }
+            }
+            unsigned m = __ballot_sync(kFull, hit);
+            while (m) {
+                const int k = __ffs(m) - 1;
+                m &= m - 1;
+                use(mk(__shfl_sync(kFull, q.x, k), __shfl_sync(kFull, q.y, k), __shfl_sync(kFull, q.z, k)));
+            }
+        }
+    };
+    V3 mean = mk(0.0, 0.0, 0.0);
+    int64_t cnt = 0;
+    scan([&](V3 q) {
+        mean = mk(mean.x + q.x, mean.y + q.y, mean.z + q.z);
+        ++cnt;
+    });
+    double nv[3] = {0.0, 0.0, 0.0};
+    if (cnt >= 3) {
+        const double c = static_cast<double>(cnt);
+        mean = mk(mean.x / c, mean.y / c, mean.z / c);
+        double a00 = 0.0, a10 = 0.0, a20 = 0.0, a11 = 0.0, a21 = 0.0, a22 = 0.0;
+        scan([&](V3 q) {  // cov += d d^T (lower triangle)
+            const V3 d = sub(q, mean);
+            a00 = a00 + d.x * d.x;
+            a10 = a10 + d.y * d.x;
+            a20 = a20 + d.z * d.x;
+            a11 = a11 + d.y * d.y;
+            a21 = a21 + d.z * d.y;
+            a22 = a22 + d.z * d.z;
+        });
+        double v[3];
+        lkeig::smallest_eigenvector(a00, a10, a20, a11, a21, a22, v);
+        const double len = sqrt(sqnorm(mk(v[0], v[1], v[2])));
+        if (len > 0.0 && isfinite(len)) {
+            V3 nn = mk(v[0] / len, v[1] / len, v[2] / len);
+            if (dot(nn, mk(vx - p.x, vy - p.y, vz - p.z)) < 0.0) nn = mk(-nn.x, -nn.y, -nn.z);
+            nv[0] = nn.x;
+            nv[1] = nn.y;
+            nv[2] = nn.z;
+        }
+    }
+    if (lane == 0) {
+        out[3 * i] = nv[0];
+        out[3 * i + 1] = nv[1];
+        out[3 * i + 2] = nv[2];
+    }
+}
+
 // usable (non-zero) normals and max |p| of a cloud
 __global__ void k_cloud_stats(const double* __restrict__ pos, const double* __restrict__ nrm, int64_t n,
                               unsigned long long* __restrict__ out) {
@@ -645,6 +720,18 @@ __global__ void k_cloud_stats(const double* __restrict__ pos, const double* __re
     } while (0)
 
 }  // namespace
+
+cudaError_t estimate_normals(const double* d_pos, int64_t n, double radius, const double* viewpoint, double* d_out,
+                             cudaStream_t stream) {
+    if (n <= 0 || !(radius > 0.0)) return cudaErrorInvalidValue;
+    int4* cells = nullptr;
+    LK_TRY(cudaMallocAsync(&cells, n * sizeof(int4), stream));
+    k_search_cells<<<nblocks(n, 256), 256, 0, stream>>>(d_pos, n, radius, cells);
+    k_estimate_normals<<<nblocks(n, kSortWarps), 32 * kSortWarps, 0, stream>>>(
+        d_pos, cells, n, radius * radius, viewpoint[0], viewpoint[1], viewpoint[2], d_out);
+    cudaFreeAsync(cells, stream);
+    return cudaGetLastError();
+}
 
 cudaError_t voxel_downsample(const double* d_pos, const double* d_nrm, int64_t n, double leaf, double* d_out_pos,
                              double* d_out_nrm, int64_t* out_count, int* status, cudaStream_t stream) {

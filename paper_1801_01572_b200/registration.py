@@ -629,6 +629,17 @@ def voxel_downsample(cloud: PointCloud, leaf: float) -> PointCloud:
     return PointCloud(out[:k].copy(), outn[:k].copy() if cloud.has_normals() else None)
 
 
+def estimate_normals(cloud: PointCloud, radius: float, viewpoint=(0.0, 0.0, 0.0), device: int = -1) -> PointCloud:
+    """preprocess.cpp:61-96 on the device: the cloud with normals oriented toward
+    `viewpoint` (zero where fewer than 3 points lie within `radius`)."""
+    c = cloud.as_c()
+    out = np.zeros((max(cloud.size(), 1), 3))
+    v = np.ascontiguousarray(np.asarray(viewpoint, np.float64).reshape(3))
+    check(abi.lib().lk_estimate_normals(C.byref(c), float(radius), v.ctypes.data_as(abi.dptr), int(device),
+                                        out.ctypes.data_as(abi.dptr)))
+    return PointCloud(cloud.positions.copy(), out[:cloud.size()].copy())
+
+
 def compute_fpfh(cloud: PointCloud, radius: float, threads: int = 0) -> np.ndarray:
     """fpfh.cpp:57-141"""
     c = cloud.as_c()

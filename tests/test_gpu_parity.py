@@ -153,6 +153,42 @@ def test_prepare_and_register_global_match_oracle(pair1, oracle):
     assert st.prerejected + st.degenerate + st.evaluated == st.sampled == 100_000
 
 
+def test_device_estimate_normals_matches_oracle(oracle):
+    # estimate_normals (preprocess.cpp:61-96): radius_search neighbours, the
+    # sequential mean / covariance sums, the restated Eigen eigensolver, the
+    # viewpoint orientation -- bitwise against the oracle
+    rng = np.random.default_rng(32)
+    plane = np.array([[0.05 * i, 0.05 * j, 0.0] for i in range(20) for j in range(20)])
+    frame = lk.voxel_downsample(synth.depth_frame_pair().target, 0.02).positions
+    cases = [(rng.uniform(-1, 1, size=(400, 3)), 0.3, (0.0, 0.0, 0.0)), (plane, 0.12, (0.5, 0.5, 2.0)),
+             (plane, 0.12, (0.5, 0.5, -2.0)), (np.array([[0, 0, 0], [0.01, 0, 0], [0.02, 0, 0], [10, 10, 10.0]]), 0.05,
+                                                (0.0, 0.0, 1.0)), (frame, 0.1, (0.0, 0.0, 0.0))]
+    for xyz, r, vp in cases:
+        dev = lk.estimate_normals(lk.PointCloud(xyz), r, vp).normals
+        assert np.array_equal(dev, oracle.estimate_normals(xyz, r, vp)), (len(xyz), r)
+    assert np.allclose(lk.estimate_normals(lk.PointCloud(plane), 0.12, (0.5, 0.5, 2.0)).normals[:, 2], 1.0)
+    with pytest.raises(lk.EmptyCloud):
+        lk.estimate_normals(lk.PointCloud(np.zeros((0, 3))), 0.1)
+
+
+def test_normal_less_clouds_register_like_the_oracle(pair1, oracle):
+    # registration.cpp:232-237: clouds given without normals get
+    # estimate_normals(normal_radius, origin) after downsampling
+    params = lk.RegistrationParams(hypothesis_count=60_000, seed=2)
+    S, T = lk.PointCloud(pair1.source.positions), lk.PointCloud(pair1.target.positions)
+    ctx = lk.prepare_registration(S, T, params)
+    src, tgt, cache, sf, tf = ctx.download()
+    octx = oracle.Context.prepare(S.positions, None, T.positions, None, oracle.params_from(params))
+    c = octx.get()
+    assert np.array_equal(src.normals, c["src_n"]) and np.array_equal(tgt.normals, c["tgt_n"])
+    assert np.array_equal(sf, c["src_feat"]) and np.array_equal(tf, c["tgt_feat"])
+    assert np.array_equal(cache, c["cache"])
+    st = lk.HypothesisStats()
+    dev = lk.register_global(S, T, params, st)
+    orc, ost = octx.run(oracle.params_from(params))
+    _assert_same_result(dev, orc, st, ost)
+
+
 def test_device_prepare_helpers_match_oracle(oracle):
     # device voxel_downsample (preprocess.cpp:14-59) and FPFH (fpfh.cpp:57-141), bitwise
     pair = synth.synth_registration_pair(4)

@@ -60,3 +60,31 @@ def test_icp_zero_iterations_is_identity(oracle):
     R, t, res, hist = oracle.icp_point_to_plane(pair.source.positions, pair.target.positions, pair.target.normals,
                                                 T0.rotation, T0.translation, 0.05, 0)
     assert res.iterations == 0 and np.array_equal(R, T0.rotation) and np.array_equal(t, T0.translation)
+
+
+def test_oracle_estimate_normals_reference_cases(oracle):
+    """preprocess.cpp:61-96 restated; the reference's own cases
+    (proj/tests/test_preprocess.cpp:77-122)."""
+    P = np.array([[0.05 * i, 0.05 * j, 0.0] for i in range(20) for j in range(20)])
+    N = oracle.estimate_normals(P, 0.12, (0.5, 0.5, 2.0))
+    assert np.allclose(np.linalg.norm(N, axis=1), 1.0, atol=1e-9)
+    assert np.allclose(N[:, 2], 1.0, atol=1e-6)
+    assert np.allclose(oracle.estimate_normals(P, 0.12, (0.5, 0.5, -2.0))[:, 2], -1.0, atol=1e-6)
+    c = np.array([[0, 0, 0], [0.01, 0, 0], [0.02, 0, 0], [10, 10, 10.0]])
+    N = oracle.estimate_normals(c, 0.05, (0, 0, 1))
+    assert np.linalg.norm(N[3]) == 0.0
+    assert abs(np.linalg.norm(N[0]) - 1.0) < 1e-9 and abs(N[0, 0]) < 1e-9
+    rng = np.random.default_rng(32)
+    R = rng.uniform(-1, 1, size=(400, 3))
+    base = oracle.estimate_normals(R, 0.3, threads=1)
+    for t in (2, 4, 16):
+        assert np.array_equal(oracle.estimate_normals(R, 0.3, threads=t), base)
+    # against a plain eigen-decomposition: same normal line (sign is the viewpoint's)
+    for i in range(0, 400, 37):
+        nb = np.where(np.sum((R - R[i]) ** 2, axis=1) <= 0.09)[0]
+        if len(nb) < 3:
+            continue
+        d = R[nb] - R[nb].mean(axis=0)
+        w, V = np.linalg.eigh(d.T @ d)
+        if w[1] - w[0] > 1e-6 * w[2]:
+            assert abs(abs(V[:, 0] @ base[i]) - 1.0) < 1e-9
