@@ -525,11 +525,13 @@ def run_b200(args):
         if k > 0:
             e2e_times.append(t1 - t0)
         ns2, nt2 = c2.n_source, c2.n_target
-        # bytes copied by the library this step: the raw clouds (positions +
-        # normals) in; downsampled clouds, features, cache, grid bounds and the
-        # record buffer out
+        # bytes copied this step: the raw clouds (positions + normals) in; out,
+        # the record buffer plus the library's control readbacks per cloud
+        # side (voxel count + normal check 8 B, FPFH staging head 12 B + 4096
+        # deferred pairs 64 KiB, cloud stats 16 B) and the EvalGrid's bounds
+        # and block total (28 B)
         h2d = 48 * (src_h.size() + tgt_h.size())
-        d2h = 48 * (ns2 + nt2) + 132 * (ns2 + nt2) + 4 * ns2 + 4 * 64 + host.nbytes
+        d2h = 2 * (8 + 12 + 4096 * 16 + 16) + 28 + host.nbytes
         c2.close()
     e2e_s = torch.tensor([statistics.mean(e2e_times)], dtype=torch.float64, device=dev)
     if world > 1:
