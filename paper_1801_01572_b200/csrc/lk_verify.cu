@@ -112,6 +112,27 @@ __global__ void k_verify_src(const double* __restrict__ p, const double* __restr
 // same for the evaluate_hypothesis sq_sum over the source points (lane 9).
 // Counts are popcounts of the hit ballots.
 // out per pair: 10 doubles (9 edge sums, sq_sum) then 3 int64 at [10..12].
+// acc + v[j] for the set bits j of m in ascending order (the sequential sum),
+// four shared-memory loads issued ahead of their dependent adds
+__device__ __forceinline__ double add_in_order(double acc, const double* v, unsigned m) {
+    while (m) {
+        double x[4];
+        int k = 0;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (m) {
+                x[u] = v[__ffs(m) - 1];
+                m &= m - 1;
+                k = u + 1;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (u < k) acc += x[u];
+    }
+    return acc;
+}
+
 constexpr int kSumThreads = 256;
 constexpr int kSumWarps = kSumThreads / 32;
 
@@ -155,16 +176,8 @@ __global__ void __launch_bounds__(kSumThreads) k_verify_sums(const double* __res
             s_c[8][t] = v.z;
         }
         __syncthreads();
-        if (warp == 0 && lane < 9) {
-            for (int w = 0; w < kSumWarps; ++w) {
-                unsigned mm = s_m[w];
-                while (mm) {
-                    const int j = __ffs(mm) - 1;
-                    mm &= mm - 1;
-                    acc += s_c[lane][32 * w + j];
-                }
-            }
-        }
+        if (warp == 0 && lane < 9)
+            for (int w = 0; w < kSumWarps; ++w) acc = add_in_order(acc, s_c[lane] + 32 * w, s_m[w]);
         __syncthreads();
     }
     for (int64_t base = p0; base < p1; base += kSumThreads) {
@@ -180,16 +193,8 @@ __global__ void __launch_bounds__(kSumThreads) k_verify_sums(const double* __res
         }
         if (inl) s_c[0][threadIdx.x] = addend[i];
         __syncthreads();
-        if (warp == 0 && lane == 9) {
-            for (int w = 0; w < kSumWarps; ++w) {
-                unsigned mm = s_m[w];
-                while (mm) {
-                    const int j = __ffs(mm) - 1;
-                    mm &= mm - 1;
-                    sq += s_c[0][32 * w + j];
-                }
-            }
-        }
+        if (warp == 0 && lane == 9)
+            for (int w = 0; w < kSumWarps; ++w) sq = add_in_order(sq, s_c[0] + 32 * w, s_m[w]);
         __syncthreads();
     }
     if (lane == 0) {
