@@ -112,6 +112,18 @@ class PointCloud:
     def has_normals(self) -> bool:
         return self.normals is not None and self.normals.shape[0] > 0
 
+    def pointers(self):
+        """(xyz address, normals address or 0, n), cached while the arrays are
+        the same objects (numpy's ctypes.data costs microseconds per call)."""
+        pos, nrm = self.positions, self.normals
+        cache = self.__dict__.get("_ptr_cache")
+        if cache is None or cache[0] is not pos or cache[1] is not nrm:
+            m = pos.shape[0]
+            cache = (pos, nrm, (pos.ctypes.data if m else 0,
+                                nrm.ctypes.data if nrm is not None and nrm.shape[0] > 0 else 0, m))
+            self.__dict__["_ptr_cache"] = cache
+        return cache[2]
+
     def as_c(self) -> abi.lk_cloud:
         nrm = self.normals if self.has_normals() else None
         return abi.lk_cloud(
@@ -553,14 +565,9 @@ def _pack_transforms(ts) -> np.ndarray:
 def _cloud_table(clouds) -> np.ndarray:
     """lk_cloud[] as an (n, 3) int64 table (xyz, nxyz, n): one array instead
     of a ctypes object per cloud."""
-    t = np.zeros((max(len(clouds), 1), 3), dtype=np.int64)
-    for k, c in enumerate(clouds):
-        m = c.positions.shape[0]
-        t[k, 0] = c.positions.ctypes.data if m else 0
-        nrm = c.normals
-        t[k, 1] = nrm.ctypes.data if nrm is not None and nrm.shape[0] > 0 else 0
-        t[k, 2] = m
-    return t
+    if not len(clouds):
+        return np.zeros((1, 3), dtype=np.int64)
+    return np.array([c.pointers() for c in clouds], dtype=np.int64)
 
 
 # ------------------------------------------------------- ICP (north-star item 4)
