@@ -1758,9 +1758,41 @@ __device__ __forceinline__ void units_body(CtaSmem& S, const SourceView& src, co
         __syncthreads();
         const int64_t u = S.cand;
         if (u >= n_units) break;
-        const int64_t c = u / R;
-        const int64_t base = (u - c * R) * kUnitPts;
+        // round-major tickets: every candidate's first unit, then the second,
+        // ... so a late round usually finds its candidate's earlier rounds done
+        const int64_t r = u / n_cand, c = u - r * n_cand;
+        const int64_t base = r * kUnitPts;
         const int64_t ns_u = base + kUnitPts < ns ? base + kUnitPts : ns;  // the unit's end
+        // u_done: unit count in bits 0-15, completed rounds (r < 16) above.
+        // When rounds 0..r-1 are complete and already hold more misses than the
+        // budget, the reference's exit lies before this unit: it is skipped
+        // (the verdict finds the exit in those rounds' ballots).
+        const unsigned inc = 1u + (r < 16 ? (1u << (16 + r)) : 0u);
+        if (warp == 0) {
+            int skip = 0;
+            if (r > 0 && r < 16 && sp.miss_budget != INT64_MAX) {
+                const unsigned need = ((1u << r) - 1u) << 16;
+                unsigned st = 0;
+                if (lane == 0) st = __ldcg(u_done + c);
+                st = __shfl_sync(kFull, st, 0);
+                if ((st & need) == need) {
+                    __threadfence();
+                    int64_t misses = 0;
+                    const int32_t wend = static_cast<int32_t>(base / 32);
+                    for (int32_t w = lane; w < wend; w += 32) misses += __popc(__ldcg(u_miss + c * n_chunks + w));
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) misses += __shfl_xor_sync(kFull, misses, o);
+                    skip = misses > sp.miss_budget ? 1 : 0;
+                }
+            }
+            if (lane == 0) S.swap = skip;
+        }
+        __syncthreads();
+        if (S.swap) {
+            if (threadIdx.x == 0) S.flag = (atomicAdd(u_done + c, inc) & 0xffffu) == static_cast<unsigned>(R - 1) ? 1 : 0;
+            __syncthreads();
+            if (!S.flag) continue;
+        } else {
         if (threadIdx.x < 12) {
             const double v = __ldg(cand_rt + 12 * c + threadIdx.x);
             if (threadIdx.x < 9) {
@@ -1791,11 +1823,13 @@ __device__ __forceinline__ void units_body(CtaSmem& S, const SourceView& src, co
             for (int w = 0; w < kCtaWarps; ++w) sum += S.red[w];
             if (sum != 0.0) atomicAdd(u_sum + c, sum);
         }
+        if (threadIdx.x == 0) t_exec += static_cast<unsigned long long>(ns_u - base);
         __threadfence();
         __syncthreads();
-        if (threadIdx.x == 0) S.flag = atomicAdd(u_done + c, 1u) == static_cast<unsigned>(R - 1) ? 1 : 0;
+        if (threadIdx.x == 0) S.flag = (atomicAdd(u_done + c, inc) & 0xffffu) == static_cast<unsigned>(R - 1) ? 1 : 0;
         __syncthreads();
         if (!S.flag) continue;
+        }
         // ---- the candidate's last unit: its verdict
         __threadfence();
         const uint32_t* mw_c = u_miss + c * n_chunks;
@@ -1844,7 +1878,6 @@ __device__ __forceinline__ void units_body(CtaSmem& S, const SourceView& src, co
         bool qual_sure = false;
         if (threadIdx.x == 0) {
             t_wref += static_cast<unsigned long long>(visited);
-            t_exec += static_cast<unsigned long long>(ns);
             if (!exited) {
                 const double ratio = static_cast<double>(inliers) / static_cast<double>(ns);
                 if (!(ratio < sp.min_ratio)) {
