@@ -630,35 +630,11 @@ __global__ void __launch_bounds__(32 * kFpfhWarps) k_fpfh(const double* __restri
 // sequential sums (each hit broadcast to the warp in order); the eigenvector
 // of the smallest eigenvalue (lk_eig3.hpp) is normalised and oriented to the
 // viewpoint. Fewer than 3 neighbours or a non-finite length: zero normal.
-__global__ void __launch_bounds__(32 * kSortWarps) k_estimate_normals(const double* __restrict__ pos,
-                                                                      const int4* __restrict__ cells, int64_t n,
-                                                                      double r2, double vx, double vy, double vz,
-                                                                      double* __restrict__ out) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t i = blockIdx.x * static_cast<int64_t>(kSortWarps) + warp;
-    if (i >= n) return;
-    const V3 p = ld3(pos, i);
-    const int4 ci = cells[i];
-    auto scan = [&](auto&& use) {
-        for (int64_t b = 0; b < n; b += 32) {
-            const int64_t j = b + lane;
-            V3 q = mk(0.0, 0.0, 0.0);
-            bool hit = false;
-            if (j < n) {
-                const int4 cj = __ldg(cells + j);
-                if (abs(cj.x - ci.x) <= 1 && abs(cj.y - ci.y) <= 1 && abs(cj.z - ci.z) <= 1) {
-                    q = ld3(pos, j);
-                    hit = sqnorm(sub(q, p)) <= r2;
-                }
-            }
-            unsigned m = __ballot_sync(kFull, hit);
-            while (m) {
-                const int k = __ffs(m) - 1;
-                m &= m - 1;
-                use(mk(__shfl_sync(kFull, q.x, k), __shfl_sync(kFull, q.y, k), __shfl_sync(kFull, q.z, k)));
-            }
-        }
-    };
+// The normal of one point from a warp-uniform scan(use) that calls use(q) for
+// each radius_search neighbour q in ascending index order (self included).
+template <class Scan>
+__device__ __forceinline__ void normal_of(V3 p, double vx, double vy, double vz, Scan&& scan, double* out3) {
+    const int lane = threadIdx.x & 31;
     V3 mean = mk(0.0, 0.0, 0.0);
     int64_t cnt = 0;
     scan([&](V3 q) {
@@ -691,10 +667,79 @@ __global__ void __launch_bounds__(32 * kSortWarps) k_estimate_normals(const doub
         }
     }
     if (lane == 0) {
-        out[3 * i] = nv[0];
-        out[3 * i + 1] = nv[1];
-        out[3 * i + 2] = nv[2];
+        out3[0] = nv[0];
+        out3[1] = nv[1];
+        out3[2] = nv[2];
     }
+}
+
+// estimate_normals (proj/src/preprocess.cpp:61-96), warp per point: the
+// radius_search neighbours (grid.cpp:153-174 with cell = radius: the +-1 cell
+// window and d2 <= r^2, self included, ascending index) are found by a brute
+// scan in index order; the mean and then the covariance are the reference's
+// sequential sums (each hit broadcast to the warp in order); the eigenvector
+// of the smallest eigenvalue (lk_eig3.hpp) is normalised and oriented to the
+// viewpoint. Fewer than 3 neighbours or a non-finite length: zero normal.
+__global__ void __launch_bounds__(32 * kSortWarps) k_estimate_normals(const double* __restrict__ pos,
+                                                                      const int4* __restrict__ cells, int64_t n,
+                                                                      double r2, double vx, double vy, double vz,
+                                                                      double* __restrict__ out) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t i = blockIdx.x * static_cast<int64_t>(kSortWarps) + warp;
+    if (i >= n) return;
+    const V3 p = ld3(pos, i);
+    const int4 ci = cells[i];
+    auto scan = [&](auto&& use) {
+        for (int64_t b = 0; b < n; b += 32) {
+            const int64_t j = b + lane;
+            V3 q = mk(0.0, 0.0, 0.0);
+            bool hit = false;
+            if (j < n) {
+                const int4 cj = __ldg(cells + j);
+                if (abs(cj.x - ci.x) <= 1 && abs(cj.y - ci.y) <= 1 && abs(cj.z - ci.z) <= 1) {
+                    q = ld3(pos, j);
+                    hit = sqnorm(sub(q, p)) <= r2;
+                }
+            }
+            unsigned m = __ballot_sync(kFull, hit);
+            while (m) {
+                const int k = __ffs(m) - 1;
+                m &= m - 1;
+                use(mk(__shfl_sync(kFull, q.x, k), __shfl_sync(kFull, q.y, k), __shfl_sync(kFull, q.z, k)));
+            }
+        }
+    };
+    normal_of(p, vx, vy, vz, scan, out + 3 * i);
+}
+
+// The same from the SearchGrid neighbour lists of the FPFH path (sorted
+// ascending, self excluded; self is visited at its place in the order).
+__global__ void __launch_bounds__(32 * kSortWarps) k_estimate_normals_lists(const double* __restrict__ pos,
+                                                                            int64_t n,
+                                                                            const int32_t* __restrict__ off,
+                                                                            const int32_t* __restrict__ nbr,
+                                                                            double vx, double vy, double vz,
+                                                                            double* __restrict__ out) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t i = blockIdx.x * static_cast<int64_t>(kSortWarps) + warp;
+    if (i >= n) return;
+    const V3 p = ld3(pos, i);
+    const int32_t o0 = off[i], k = off[i + 1] - o0;
+    // self's place: the number of listed neighbours below i
+    int below = 0;
+    for (int a = lane; a < k; a += 32) below += nbr[o0 + a] < i ? 1 : 0;
+    below = __reduce_add_sync(kFull, below);
+    auto scan = [&](auto&& use) {
+        for (int b = 0; b <= k; b += 32) {
+            const int v = b + lane;  // position in the list with self inserted
+            V3 q = mk(0.0, 0.0, 0.0);
+            if (v <= k) q = ld3(pos, v < below ? nbr[o0 + v] : (v == below ? static_cast<int32_t>(i) : nbr[o0 + v - 1]));
+            const int cnt = k + 1 - b < 32 ? k + 1 - b : 32;
+            for (int t = 0; t < cnt; ++t)
+                use(mk(__shfl_sync(kFull, q.x, t), __shfl_sync(kFull, q.y, t), __shfl_sync(kFull, q.z, t)));
+        }
+    };
+    normal_of(p, vx, vy, vz, scan, out + 3 * i);
 }
 
 // usable (non-zero) normals and max |p| of a cloud
@@ -724,12 +769,38 @@ __global__ void k_cloud_stats(const double* __restrict__ pos, const double* __re
 cudaError_t estimate_normals(const double* d_pos, int64_t n, double radius, const double* viewpoint, double* d_out,
                              cudaStream_t stream) {
     if (n <= 0 || !(radius > 0.0)) return cudaErrorInvalidValue;
-    int4* cells = nullptr;
-    LK_TRY(cudaMallocAsync(&cells, n * sizeof(int4), stream));
-    k_search_cells<<<nblocks(n, 256), 256, 0, stream>>>(d_pos, n, radius, cells);
-    k_estimate_normals<<<nblocks(n, kSortWarps), 32 * kSortWarps, 0, stream>>>(
-        d_pos, cells, n, radius * radius, viewpoint[0], viewpoint[1], viewpoint[2], d_out);
-    cudaFreeAsync(cells, stream);
+    const double r2 = radius * radius;
+    if (n <= kBruteMax) {
+        int4* cells = nullptr;
+        LK_TRY(cudaMallocAsync(&cells, n * sizeof(int4), stream));
+        k_search_cells<<<nblocks(n, 256), 256, 0, stream>>>(d_pos, n, radius, cells);
+        k_estimate_normals<<<nblocks(n, kSortWarps), 32 * kSortWarps, 0, stream>>>(
+            d_pos, cells, n, r2, viewpoint[0], viewpoint[1], viewpoint[2], d_out);
+        cudaFreeAsync(cells, stream);
+        return cudaGetLastError();
+    }
+    // larger clouds: the FPFH path's SearchGrid lists (exact size, one readback)
+    GridStorage g;
+    int32_t *counts = nullptr, *off = nullptr, *nbr = nullptr;
+    LK_TRY(build_grid(g, 1, d_pos, nullptr, n, radius, radius, stream, false));
+    LK_TRY(cudaMallocAsync(&counts, n * sizeof(int32_t), stream));
+    LK_TRY(cudaMallocAsync(&off, (n + 1) * sizeof(int32_t), stream));
+    k_nbr_count<<<nblocks(n, kSortWarps), 32 * kSortWarps, 0, stream>>>(d_pos, n, g.view, r2, counts);
+    LK_TRY(exclusive_scan(counts, n, off, stream));
+    int32_t* h_total = static_cast<int32_t*>(host_scratch(sizeof(int32_t)));
+    if (!h_total) return cudaErrorMemoryAllocation;
+    LK_TRY(cudaMemcpyAsync(h_total, off + n, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
+    LK_TRY(cudaStreamSynchronize(stream));
+    const int64_t total = *h_total;
+    LK_TRY(cudaMallocAsync(&nbr, (total > 0 ? total : 1) * sizeof(int32_t), stream));
+    k_nbr_fill<<<nblocks(n, kSortWarps), 32 * kSortWarps, 0, stream>>>(d_pos, n, g.view, r2, off, nbr,
+                                                                       total > 0 ? total : 1);
+    k_estimate_normals_lists<<<nblocks(n, kSortWarps), 32 * kSortWarps, 0, stream>>>(
+        d_pos, n, off, nbr, viewpoint[0], viewpoint[1], viewpoint[2], d_out);
+    cudaFreeAsync(counts, stream);
+    cudaFreeAsync(off, stream);
+    cudaFreeAsync(nbr, stream);
+    g.release();
     return cudaGetLastError();
 }
 

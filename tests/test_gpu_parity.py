@@ -163,6 +163,10 @@ def test_device_estimate_normals_matches_oracle(oracle):
     cases = [(rng.uniform(-1, 1, size=(400, 3)), 0.3, (0.0, 0.0, 0.0)), (plane, 0.12, (0.5, 0.5, 2.0)),
              (plane, 0.12, (0.5, 0.5, -2.0)), (np.array([[0, 0, 0], [0.01, 0, 0], [0.02, 0, 0], [10, 10, 10.0]]), 0.05,
                                                 (0.0, 0.0, 1.0)), (frame, 0.1, (0.0, 0.0, 0.0))]
+    # above the brute-force size the SearchGrid neighbour lists are used
+    big = lk.voxel_downsample(synth.depth_frame_pair().target, 0.008).positions
+    assert len(big) > 24576
+    cases.append((big, 0.03, (0.0, 0.0, 0.0)))
     for xyz, r, vp in cases:
         dev = lk.estimate_normals(lk.PointCloud(xyz), r, vp).normals
         assert np.array_equal(dev, oracle.estimate_normals(xyz, r, vp)), (len(xyz), r)
