@@ -95,6 +95,27 @@ def test_cli_register_matches_oracle(tmp_path, oracle, binary):
 
 
 @pytest.mark.gpu
+def test_cli_register_without_normals(tmp_path, oracle):
+    # PLY files with positions only: register_global estimates the normals
+    # (registration.cpp:232-237) -- the same output as the oracle's path
+    from paper_1801_01572_b200 import synth
+    pair = synth.synth_registration_pair(3)
+    sp, _ = write_ply(tmp_path / "s.ply", pair.source.positions)
+    tp, _ = write_ply(tmp_path / "t.ply", pair.target.positions)
+    r = run("register", "--source", str(tmp_path / "s.ply"), "--target", str(tmp_path / "t.ply"),
+            "--hypotheses", "40000", "--seed", "5")
+    p = oracle.params(hypothesis_count=40_000, seed=5)
+    ctx = oracle.Context.prepare(sp, None, tp, None, p)
+    res, _ = ctx.run(p)
+    if not res.found:
+        assert r.returncode == 2 and r.stdout.strip() == "no-alignment"
+        return
+    assert r.returncode == 0, r.stderr
+    want = _fmt_matrix(res.R, res.t) + [f"inlier_ratio {res.inlier_ratio:.17g}", f"fitness {res.fitness:.17g}"]
+    assert r.stdout.strip().splitlines() == want
+
+
+@pytest.mark.gpu
 def test_cli_no_alignment_and_icp(tmp_path, oracle):
     from paper_1801_01572_b200 import synth
     neg = synth.synth_negative_pair(1)
