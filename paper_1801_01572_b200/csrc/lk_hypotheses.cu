@@ -120,15 +120,33 @@ __global__ void __launch_bounds__(256) k_hyp_sample(int64_t begin, int64_t count
                         break;
                     }
                 }
-                d[k] = __ldg(cache + s[k]);
             }
+            // prerejected (registration.cpp:42-51) edge by edge, loading the
+            // corners as the edges need them: most quadruples fail on the
+            // first edge, so most skip half of the gathers
             V3 sp[4], dp[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
+            auto corner = [&](int k) {
+                d[k] = __ldg(cache + s[k]);
                 sp[k] = ld3(spos, s[k]);
                 dp[k] = ld3(tpos, d[k]);
+            };
+            auto edge_fails = [&](int a, int b) {
+                const double es = sqrt(sqnorm(sub(sp[a], sp[b])));
+                const double ed = sqrt(sqnorm(sub(dp[a], dp[b])));
+                return es < tau * ed || ed < tau * es;
+            };
+            corner(0);
+            corner(1);
+            bool rej = edge_fails(0, 1);
+            if (!rej) {
+                corner(2);
+                rej = edge_fails(1, 2);
+                if (!rej) {
+                    corner(3);
+                    rej = edge_fails(2, 3) || edge_fails(3, 0);
+                }
             }
-            survive = !prerejected(sp, dp, tau);
+            survive = !rej;
         }
         // prerejected = sampled - survivors (every live hypothesis is one or
         // the other), so only the survivors touch a counter
