@@ -383,18 +383,27 @@ __global__ void __launch_bounds__(32 * kSortWarps) k_nbr_brute_once(const double
     const int4 ci = cells[i];
     int32_t* row = slots + i * kNbrSlots;
     int32_t o = 0;
-    for (int64_t b = 0; b < n; b += 32) {
-        const int64_t j = b + lane;
-        bool hit = false;
-        if (j < n && j != i) {
-            const int4 cj = __ldg(cells + j);
-            hit = abs(cj.x - ci.x) <= rad && abs(cj.y - ci.y) <= rad && abs(cj.z - ci.z) <= rad &&
-                  sqnorm(sub(ld3(pos, j), p)) <= r2;
+    // four 32-point chunks per step: their cell loads are issued together
+    constexpr int kU = 4;
+    for (int64_t b0 = 0; b0 < n; b0 += 32 * kU) {
+        int4 cj[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int64_t j = b0 + 32 * u + lane;
+            cj[u] = j < n ? __ldg(cells + j) : make_int4(INT32_MIN, INT32_MIN, INT32_MIN, 0);
         }
-        const unsigned m = __ballot_sync(kFull, hit);
-        const int32_t at = o + __popc(m & ((1u << lane) - 1u));
-        if (hit && at < kNbrSlots) row[at] = static_cast<int32_t>(j);
-        o += __popc(m);
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int64_t j = b0 + 32 * u + lane;
+            bool hit = false;
+            if (j < n && j != i && abs(cj[u].x - ci.x) <= rad && abs(cj[u].y - ci.y) <= rad &&
+                abs(cj[u].z - ci.z) <= rad)
+                hit = sqnorm(sub(ld3(pos, j), p)) <= r2;
+            const unsigned m = __ballot_sync(kFull, hit);
+            const int32_t at = o + __popc(m & ((1u << lane) - 1u));
+            if (hit && at < kNbrSlots) row[at] = static_cast<int32_t>(j);
+            o += __popc(m);
+        }
     }
     if (lane == 0) {
         counts[i] = o;
