@@ -191,7 +191,9 @@ __global__ void __launch_bounds__(32 * kSortWarps) k_vox_reduce(const int32_t* _
             }
         }
     };
-    V3 ps = mk(0.0, 0.0, 0.0), nsum = mk(0.0, 0.0, 0.0);
+    // lane q < 6 runs component q's sequential chain (x, y, z of the
+    // positions, then of the normals): six chains side by side
+    double acc = 0.0;
     V3 p, nv;
     fetch(0, p, nv);
     for (int c0 = 0; c0 < k; c0 += 32) {
@@ -203,20 +205,16 @@ __global__ void __launch_bounds__(32 * kSortWarps) k_vox_reduce(const int32_t* _
         s_v[warp][5][lane] = nv.z;
         __syncwarp();
         if (c0 + 32 < k) fetch(c0 + 32, p, nv);
-        if (lane == 0) {
+        if (lane < 6) {
             const int m = k - c0 < 32 ? k - c0 : 32;
-#pragma unroll 4
-            for (int L = 0; L < m; ++L) {
-                ps.x += s_v[warp][0][L];
-                ps.y += s_v[warp][1][L];
-                ps.z += s_v[warp][2][L];
-                nsum.x += s_v[warp][3][L];
-                nsum.y += s_v[warp][4][L];
-                nsum.z += s_v[warp][5][L];
-            }
+            const double* col = s_v[warp][lane];
+#pragma unroll 8
+            for (int L = 0; L < m; ++L) acc += col[L];
         }
         __syncwarp();
     }
+    const V3 ps = mk(__shfl_sync(kFull, acc, 0), __shfl_sync(kFull, acc, 1), __shfl_sync(kFull, acc, 2));
+    const V3 nsum = mk(__shfl_sync(kFull, acc, 3), __shfl_sync(kFull, acc, 4), __shfl_sync(kFull, acc, 5));
     if (lane != 0) return;
     const double cnt = static_cast<double>(k);
     out_pos[3 * o] = ps.x / cnt;
