@@ -456,6 +456,7 @@ __global__ void __launch_bounds__(32 * kSortWarps) k_nbr_fill(const double* __re
 }
 
 constexpr int kFpfhWarps = 4;
+constexpr int kRows = 8;  // spfh rows in flight per step of k_fpfh
 
 // a / b correctly rounded from r = RN(1 / b): q = RN(a r) is within one ulp,
 // the residual a - b q is exact in one FMA, and RN(q + residual * r) is the
@@ -590,19 +591,19 @@ __global__ void __launch_bounds__(32 * kFpfhWarps) k_fpfh(const double* __restri
         }
         unsigned m = __ballot_sync(kFull, ok);
         k_count += __popc(m);
-        // the usable ones in neighbour order, four rows of spfh in flight
+        // the usable ones in neighbour order, kRows rows of spfh in flight
         while (m) {
-            int src[4];
-            bool use[4];
+            int src[kRows];
+            bool use[kRows];
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
+            for (int t = 0; t < kRows; ++t) {
                 use[t] = m != 0;
                 src[t] = use[t] ? __ffs(m) - 1 : 0;
                 if (use[t]) m &= m - 1;
             }
-            double sv[4], wv[4], rv[4], q32v[4];
+            double sv[kRows], wv[kRows], rv[kRows], q32v[kRows];
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
+            for (int t = 0; t < kRows; ++t) {
                 const int32_t jt = __shfl_sync(kFull, j, src[t]);
                 wv[t] = __shfl_sync(kFull, w, src[t]);
                 rv[t] = __shfl_sync(kFull, r, src[t]);
@@ -610,7 +611,7 @@ __global__ void __launch_bounds__(32 * kFpfhWarps) k_fpfh(const double* __restri
                 sv[t] = use[t] ? spfh[33 * static_cast<int64_t>(jt) + lane] : 0.0;
             }
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
+            for (int t = 0; t < kRows; ++t) {
                 if (use[t]) {
                     acc0 += div_by(sv[t], wv[t], rv[t]);
                     acc1 += q32v[t];  // lane 0's value is the one used
