@@ -70,18 +70,6 @@ struct Rng {
     }
 };
 
-// ---- pre-rejection (proj/src/registration.cpp:42-51) ---------------------
-__device__ __forceinline__ bool prerejected(const V3 (&s)[4], const V3 (&d)[4], double tau) {
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-        int b = (a + 1) & 3;
-        double es = sqrt(sqnorm(sub(s[a], s[b])));
-        double ed = sqrt(sqnorm(sub(d[a], d[b])));
-        if (es < tau * ed || ed < tau * es) return true;
-    }
-    return false;
-}
-
 // ---- 3x3 Jacobi SVD (Eigen 3.4 JacobiSVD<Matrix3d>, full U/V) ------------
 // Matrices are row-major m[3*r + c].
 struct Rot {
