@@ -99,3 +99,16 @@ def test_icp_scattered_queries_and_outliers(oracle):
     scattered = synth.RegistrationPair(lk.PointCloud(src), pair.target, pair.truth)
     T0 = _perturbed(pair.truth, [0.01, 0.01, -0.008, 0.005, 0.01, -0.004])
     _check_same(oracle, scattered, T0, 0.05, 10, 1e-10)
+
+
+def test_icp_singular_plane_stops_like_the_oracle(oracle):
+    """A plane against a plane (every normal +z): in-plane translation and the
+    rotation about z are unobservable, the LDL^T meets a zero pivot and the
+    run stops where the oracle stops, with the same history."""
+    g = np.array([[0.02 * a, 0.02 * b, 0.0] for a in range(40) for b in range(40)])
+    n = np.tile([0.0, 0.0, 1.0], (len(g), 1))
+    src = lk.PointCloud(g + np.array([0.003, -0.002, 0.01]))
+    tgt = lk.PointCloud(g, n)
+    pair = synth.RegistrationPair(src, tgt, lk.RigidTransform())
+    dev = _check_same(oracle, pair, lk.RigidTransform(), 0.05, 10, 1e-12)
+    assert not dev.converged

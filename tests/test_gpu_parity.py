@@ -163,6 +163,12 @@ def test_device_estimate_normals_matches_oracle(oracle):
     cases = [(rng.uniform(-1, 1, size=(400, 3)), 0.3, (0.0, 0.0, 0.0)), (plane, 0.12, (0.5, 0.5, 2.0)),
              (plane, 0.12, (0.5, 0.5, -2.0)), (np.array([[0, 0, 0], [0.01, 0, 0], [0.02, 0, 0], [10, 10, 10.0]]), 0.05,
                                                 (0.0, 0.0, 1.0)), (frame, 0.1, (0.0, 0.0, 0.0))]
+    # degenerate neighbourhoods: coincident points (zero covariance), a line
+    # (two zero eigenvalues), exact ties in the eigenvalues of a regular grid
+    dup = np.vstack([np.zeros((5, 3)), np.array([[0.5, 0.0, 0.0], [0.0, 0.0, 3.0]])])
+    line = np.array([[0.01 * k, 0.0, 0.0] for k in range(12)])
+    cube = np.array([[0.05 * a, 0.05 * b, 0.05 * c] for a in range(4) for b in range(4) for c in range(4)])
+    cases += [(dup, 0.1, (1.0, 2.0, 3.0)), (line, 0.05, (0.0, 1.0, 0.0)), (cube, 0.06, (0.0, 0.0, 0.0))]
     # above the brute-force size the SearchGrid neighbour lists are used
     big = lk.voxel_downsample(synth.depth_frame_pair().target, 0.008).positions
     assert len(big) > 24576
