@@ -1322,6 +1322,7 @@ struct CtaSmem {
     double red[kCtaWarps];
     int scan[kCtaWarps];
     int nq;
+    int next;  // B: next queue entry a warp takes (dynamic, 32 at a time)
     int flag;
     int swap;
     double exact[2];
@@ -1431,6 +1432,7 @@ __device__ __forceinline__ void score_round_ab(CtaSmem& S, const SourceView& src
                                                int64_t ns, double* __restrict__ add, double& part) {
     const int lane = threadIdx.x & 31;
     const FastRT& F = S.F;
+    if (threadIdx.x == 0) S.next = 0;
     // A. FP32 location of the round's points
 #pragma unroll
     for (int u = 0; u < kCtaPer; ++u) {
@@ -1483,7 +1485,16 @@ __device__ __forceinline__ void score_round_ab(CtaSmem& S, const SourceView& src
         S.inl[b ^ 1][threadIdx.x] = 0u;
         S.miss[b ^ 1][threadIdx.x] = 0u;
     }
-    for (int e = threadIdx.x; e < nq; e += kCtaThreads) {
+    // warps take the queue 32 entries at a time: a warp with slow entries
+    // (long lists, the exact fallback) takes fewer chunks, so the round's
+    // barrier waits less for the slowest thread
+    for (;;) {
+        int e0 = 0;
+        if (lane == 0) e0 = atomicAdd(&S.next, 32);
+        e0 = __shfl_sync(kFull, e0, 0);
+        if (e0 >= nq) break;
+        const int e = e0 + lane;
+        if (e >= nq) continue;
         const int2 qe = S.q[e];
         const int local = qe.x & 0xffff;
         const int cnt = static_cast<int>(static_cast<unsigned>(qe.x) >> 16);
