@@ -1964,6 +1964,8 @@ __device__ __forceinline__ void units_body(CtaSmem& S, const SourceView& src, co
         }
         __syncthreads();
     }
+    // every warp has read the final ticket from S.cand before it is reused
+    __syncthreads();
     // the CTA best's exact sum (its scratch rows persist)
     if (threadIdx.x == 0) {
         S.flag = (best.valid && best_eb != 0.0) ? 1 : 0;
