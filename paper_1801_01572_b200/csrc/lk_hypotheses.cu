@@ -1322,6 +1322,7 @@ struct CtaSmem {
     double red[kCtaWarps];
     int scan[kCtaWarps];
     int nq;
+    int nslow;  // A: exact-fallback entries, queued from the back of q
     int next;  // B: next queue entry a warp takes (dynamic, 32 at a time)
     int flag;
     int swap;
@@ -1469,18 +1470,28 @@ __device__ __forceinline__ void score_round_ab(CtaSmem& S, const SourceView& src
         }
         const unsigned mm = __ballot_sync(kFull, i < ns && state == 0);
         if (lane == 0) S.miss[b][local >> 5] = mm;
-        const unsigned m = __ballot_sync(kFull, state != 0);
+        // list scans from the front of q, exact fallbacks from the back; B
+        // hands out the (rare, slow) fallbacks first and together, so they
+        // share warp chunks with each other and do not end up in the tail
+        const unsigned mf = __ballot_sync(kFull, state == 2), ms = __ballot_sync(kFull, state == 1);
         int slot = 0;
-        if (m) {
-            const int leader = __ffs(m) - 1;
-            if (lane == leader) slot = atomicAdd(&S.nq, __popc(m));
-            slot = __shfl_sync(kFull, slot, leader) + __popc(m & ((1u << lane) - 1u));
+        if (mf) {
+            const int leader = __ffs(mf) - 1;
+            if (lane == leader) slot = atomicAdd(&S.nq, __popc(mf));
+            slot = __shfl_sync(kFull, slot, leader) + __popc(mf & ((1u << lane) - 1u));
+        }
+        if (ms) {
+            const int leader = __ffs(ms) - 1;
+            int sl = 0;
+            if (lane == leader) sl = atomicAdd(&S.nslow, __popc(ms));
+            sl = __shfl_sync(kFull, sl, leader) + __popc(ms & ((1u << lane) - 1u));
+            if (state == 1) slot = kCtaPts - 1 - sl;
         }
         if (state != 0) S.q[slot] = make_int2(local | ((state == 1 ? kCtaSlow : bi.y) << 16), bi.x);
     }
     __syncthreads();
     // B. dense resolution of the queue; the next round's ballots are cleared
-    const int nq = S.nq;
+    const int nslow = S.nslow, nq = S.nq + nslow;
     if (threadIdx.x < kCtaWords) {
         S.inl[b ^ 1][threadIdx.x] = 0u;
         S.miss[b ^ 1][threadIdx.x] = 0u;
@@ -1495,7 +1506,7 @@ __device__ __forceinline__ void score_round_ab(CtaSmem& S, const SourceView& src
         if (e0 >= nq) break;
         const int e = e0 + lane;
         if (e >= nq) continue;
-        const int2 qe = S.q[e];
+        const int2 qe = S.q[e < nslow ? kCtaPts - 1 - e : e - nslow];
         const int local = qe.x & 0xffff;
         const int cnt = static_cast<int>(static_cast<unsigned>(qe.x) >> 16);
         const int64_t i = base + local;
@@ -1571,6 +1582,7 @@ __device__ __forceinline__ void cta_body(CtaSmem& S, const SourceView& src, cons
         if (threadIdx.x == 0) {
             S.F = make_fast_fine(S.R, S.t, g, sp);
             S.nq = 0;
+            S.nslow = 0;
         }
         __syncthreads();
         double* add = slot_add[cur];
@@ -1582,7 +1594,10 @@ __device__ __forceinline__ void cta_body(CtaSmem& S, const SourceView& src, cons
             const int b = static_cast<int>(r & 1);
             score_round_ab(S, src, g, sp, cand_rt + 12 * cand, base, b, ns, add, part);
             // C. the miss budget in point order (word w covers points base + 32 w ..)
-            if (threadIdx.x == 0) S.nq = 0;
+            if (threadIdx.x == 0) {
+                S.nq = 0;
+                S.nslow = 0;
+            }
             const int rm = round_misses(S.miss[b], base, misses, sp, visited);
             if (misses + rm > sp.miss_budget) {
                 exited = true;
@@ -1779,6 +1794,7 @@ __device__ __forceinline__ void units_body(CtaSmem& S, const SourceView& src, co
         if (threadIdx.x == 0) {
             S.cand = static_cast<int64_t>(atomicAdd(&ctr->work_next, 1ull));
             S.nq = 0;
+            S.nslow = 0;
         }
         if (threadIdx.x < kCtaWords) {
             S.inl[0][threadIdx.x] = 0u;
@@ -2052,6 +2068,7 @@ __global__ void __launch_bounds__(kCtaThreads, 4) k_score_list(SourceView src, c
         if (threadIdx.x == 0) {
             S.cand = static_cast<int64_t>(atomicAdd(&ctr->work_next, 1ull));
             S.nq = 0;
+            S.nslow = 0;
         }
         if (threadIdx.x < 2 * kCtaWords) {
             (&S.inl[0][0])[threadIdx.x] = 0u;
@@ -2078,7 +2095,10 @@ __global__ void __launch_bounds__(kCtaThreads, 4) k_score_list(SourceView src, c
         for (int64_t base = 0, r = 0; base < ns; base += kCtaPts, ++r) {
             const int b = static_cast<int>(r & 1);
             score_round_ab(S, src, g, sp, cand_rt + 12 * cand, base, b, ns, my_add - base, part);
-            if (threadIdx.x == 0) S.nq = 0;
+            if (threadIdx.x == 0) {
+                S.nq = 0;
+                S.nslow = 0;
+            }
             // the miss budget in point order (word w covers points base + 32 w ..)
             const int rm = round_misses(S.miss[b], base, misses, sp, visited);
             if (misses + rm > sp.miss_budget) {
