@@ -1499,10 +1499,14 @@ __device__ __forceinline__ void score_round_ab(CtaSmem& S, const SourceView& src
     // warps take the queue 32 entries at a time: a warp with slow entries
     // (long lists, the exact fallback) takes fewer chunks, so the round's
     // barrier waits less for the slowest thread
-    for (;;) {
-        int e0 = 0;
-        if (lane == 0) e0 = atomicAdd(&S.next, 32);
-        e0 = __shfl_sync(kFull, e0, 0);
+    for (int first = 1;; first = 0) {
+        // each warp's first chunk is its own (no atomic round trip), the rest
+        // are handed out in order of demand
+        int e0 = (threadIdx.x >> 5) * 32;
+        if (!first) {
+            if (lane == 0) e0 = kCtaThreads + atomicAdd(&S.next, 32);
+            e0 = __shfl_sync(kFull, e0, 0);
+        }
         if (e0 >= nq) break;
         const int e = e0 + lane;
         if (e >= nq) continue;
