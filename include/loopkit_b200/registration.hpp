@@ -72,9 +72,14 @@ inline bool check(lk_status s) {  // true: found; false: no alignment
     throw_status<E>(s);
 }
 
-// View of a cloud with contiguous xyz triples (no copy).
-template <class Cloud>
+// View of a cloud with contiguous xyz triples (no copy). lk_cloud carries one
+// count for both arrays, so a normals array that is neither empty nor
+// parallel to the positions throws MissingNormals here, as validate_cloud
+// does (geometry.cpp:93-96), instead of letting the library read past it.
+template <class E = DefaultErrors, class Cloud>
 inline lk_cloud as_lk_cloud(const Cloud& c) {
+    if (!c.normals.empty() && c.normals.size() != c.positions.size())
+        throw typename E::MissingNormalsT("normals array must be empty or match positions");
     lk_cloud out{};
     out.n = static_cast<int64_t>(c.positions.size());
     out.xyz = out.n ? reinterpret_cast<const double*>(c.positions.data()) : nullptr;
@@ -150,7 +155,7 @@ private:
 // prepare_registration (registration.hpp:105-107)
 template <class E = DefaultErrors, class Cloud, class Params>
 RegistrationContext<E> prepare_registration(const Cloud& source, const Cloud& target, const Params& params) {
-    lk_cloud s = as_lk_cloud(source), t = as_lk_cloud(target);
+    lk_cloud s = as_lk_cloud<E>(source), t = as_lk_cloud<E>(target);
     lk_reg_params p = to_lk_params(params);
     lk_reg_ctx* h = nullptr;
     lk_status st = lk_reg_prepare(&s, &t, &p, &h);
@@ -173,7 +178,7 @@ std::optional<RegistrationResult> run_hypotheses(const RegistrationContext<E>& c
 template <class E = DefaultErrors, class Cloud, class Params>
 std::optional<RegistrationResult> register_global(const Cloud& source, const Cloud& target, const Params& params,
                                                   HypothesisStats* stats = nullptr) {
-    lk_cloud s = as_lk_cloud(source), t = as_lk_cloud(target);
+    lk_cloud s = as_lk_cloud<E>(source), t = as_lk_cloud<E>(target);
     lk_reg_params p = to_lk_params(params);
     lk_reg_result r{};
     lk_hyp_stats local{};
@@ -190,7 +195,7 @@ std::pair<double, double> evaluate_hypothesis(const Transform& T, const Cloud& s
         throw typename E::EmptyCloudT("evaluate_hypothesis: empty cloud");
     if (source.normals.empty() || target.normals.empty())
         throw typename E::MissingNormalsT("evaluate_hypothesis: both clouds need normals");
-    lk_cloud s = as_lk_cloud(source), t = as_lk_cloud(target);
+    lk_cloud s = as_lk_cloud<E>(source), t = as_lk_cloud<E>(target);
     lk_reg_params p = to_lk_params(params);
     lk_grid* g = nullptr;
     lk_status st = lk_grid_build(&t, 1, grid_cell, params.d_max, -1, &g);
@@ -214,7 +219,7 @@ struct EdgeInfo {
 template <class E = DefaultErrors, class Cloud>
 EdgeInfo edge_info(const Cloud& cloud_i, const Cloud& cloud_j, const Transform& t_i, const Transform& t_j,
                    double epsilon) {
-    lk_cloud ci = as_lk_cloud(cloud_i), cj = as_lk_cloud(cloud_j);
+    lk_cloud ci = as_lk_cloud<E>(cloud_i), cj = as_lk_cloud<E>(cloud_j);
     double ti[12], tj[12];
     for (int k = 0; k < 9; ++k) {
         ti[k] = t_i.R[k];
@@ -268,7 +273,7 @@ template <class E = DefaultErrors, class Cloud>
 IcpResult icp_point_to_plane(const Cloud& source, const Cloud& target, const Transform& init,
                              double max_correspondence_distance = 0.05, int max_iterations = 30,
                              double convergence_eps = 1e-10, int32_t device = -1) {
-    lk_cloud s = as_lk_cloud(source), t = as_lk_cloud(target);
+    lk_cloud s = as_lk_cloud<E>(source), t = as_lk_cloud<E>(target);
     double T0[12];
     for (int k = 0; k < 9; ++k) T0[k] = init.R[k];
     for (int k = 0; k < 3; ++k) T0[9 + k] = init.t[k];

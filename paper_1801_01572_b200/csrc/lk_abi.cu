@@ -385,6 +385,7 @@ struct lk_reg_ctx {
         lkk::pool_free(d_sfeat, s);
         lkk::pool_free(d_tfeat, s);
         grid.release();
+        rb.stream = s;  // the caller's stream (synchronised above) may be gone
         rb.release();
         lkk::pool_free(d_record, s);
         if (own_stream) cudaStreamSynchronize(own_stream);
@@ -681,7 +682,14 @@ void lk_reg_ctx_destroy(lk_reg_ctx* ctx) { delete ctx; }
 lk_status lk_reg_ctx_set_stream(lk_reg_ctx* ctx, void* stream) {
     if (!ctx) return fail(LK_INVALID_ARGUMENT, "null context");
     std::lock_guard<std::mutex> lock(ctx->mu);
+    cudaSetDevice(ctx->device);
+    // the run buffers are (re)allocated and freed stream-ordered: finish the
+    // old stream's work and move the buffers' stream with the kernels, so a
+    // buffer freed on growth is ordered after every kernel that read it
+    const cudaError_t e = cudaStreamSynchronize(ctx->stream);
     ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+    ctx->rb.stream = ctx->stream;
+    if (e != cudaSuccess) return fail(LK_CUDA_ERROR, cudaGetErrorString(e));
     return LK_OK;
 }
 

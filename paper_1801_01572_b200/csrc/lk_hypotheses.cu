@@ -1321,8 +1321,11 @@ struct CtaSmem {
     FastRT F;
     double red[kCtaWarps];
     int scan[kCtaWarps];
-    int nq;
-    int nslow;  // A: exact-fallback entries, queued from the back of q
+    // per round parity b: queue counts of round b (list scans / exact-fallback
+    // entries, the latter queued from the back of q). Round r's phase B clears
+    // parity b ^ 1, so no reset ever races the next round's phase-A atomics.
+    int nq[2];
+    int nslow[2];
     int next;  // B: next queue entry a warp takes (dynamic, 32 at a time)
     int flag;
     int swap;
@@ -1477,13 +1480,13 @@ __device__ __forceinline__ void score_round_ab(CtaSmem& S, const SourceView& src
         int slot = 0;
         if (mf) {
             const int leader = __ffs(mf) - 1;
-            if (lane == leader) slot = atomicAdd(&S.nq, __popc(mf));
+            if (lane == leader) slot = atomicAdd(&S.nq[b], __popc(mf));
             slot = __shfl_sync(kFull, slot, leader) + __popc(mf & ((1u << lane) - 1u));
         }
         if (ms) {
             const int leader = __ffs(ms) - 1;
             int sl = 0;
-            if (lane == leader) sl = atomicAdd(&S.nslow, __popc(ms));
+            if (lane == leader) sl = atomicAdd(&S.nslow[b], __popc(ms));
             sl = __shfl_sync(kFull, sl, leader) + __popc(ms & ((1u << lane) - 1u));
             if (state == 1) slot = kCtaPts - 1 - sl;
         }
@@ -1491,7 +1494,11 @@ __device__ __forceinline__ void score_round_ab(CtaSmem& S, const SourceView& src
     }
     __syncthreads();
     // B. dense resolution of the queue; the next round's ballots are cleared
-    const int nslow = S.nslow, nq = S.nq + nslow;
+    const int nslow = S.nslow[b], nq = S.nq[b] + nslow;
+    if (threadIdx.x == 0) {
+        S.nq[b ^ 1] = 0;
+        S.nslow[b ^ 1] = 0;
+    }
     if (threadIdx.x < kCtaWords) {
         S.inl[b ^ 1][threadIdx.x] = 0u;
         S.miss[b ^ 1][threadIdx.x] = 0u;
@@ -1585,8 +1592,8 @@ __device__ __forceinline__ void cta_body(CtaSmem& S, const SourceView& src, cons
         __syncthreads();
         if (threadIdx.x == 0) {
             S.F = make_fast_fine(S.R, S.t, g, sp);
-            S.nq = 0;
-            S.nslow = 0;
+            S.nq[0] = S.nq[1] = 0;
+            S.nslow[0] = S.nslow[1] = 0;
         }
         __syncthreads();
         double* add = slot_add[cur];
@@ -1598,10 +1605,6 @@ __device__ __forceinline__ void cta_body(CtaSmem& S, const SourceView& src, cons
             const int b = static_cast<int>(r & 1);
             score_round_ab(S, src, g, sp, cand_rt + 12 * cand, base, b, ns, add, part);
             // C. the miss budget in point order (word w covers points base + 32 w ..)
-            if (threadIdx.x == 0) {
-                S.nq = 0;
-                S.nslow = 0;
-            }
             const int rm = round_misses(S.miss[b], base, misses, sp, visited);
             if (misses + rm > sp.miss_budget) {
                 exited = true;
@@ -1797,8 +1800,8 @@ __device__ __forceinline__ void units_body(CtaSmem& S, const SourceView& src, co
     for (;;) {
         if (threadIdx.x == 0) {
             S.cand = static_cast<int64_t>(atomicAdd(&ctr->work_next, 1ull));
-            S.nq = 0;
-            S.nslow = 0;
+            S.nq[0] = S.nq[1] = 0;
+            S.nslow[0] = S.nslow[1] = 0;
         }
         if (threadIdx.x < kCtaWords) {
             S.inl[0][threadIdx.x] = 0u;
@@ -2071,8 +2074,8 @@ __global__ void __launch_bounds__(kCtaThreads, 4) k_score_list(SourceView src, c
     for (;;) {
         if (threadIdx.x == 0) {
             S.cand = static_cast<int64_t>(atomicAdd(&ctr->work_next, 1ull));
-            S.nq = 0;
-            S.nslow = 0;
+            S.nq[0] = S.nq[1] = 0;
+            S.nslow[0] = S.nslow[1] = 0;
         }
         if (threadIdx.x < 2 * kCtaWords) {
             (&S.inl[0][0])[threadIdx.x] = 0u;
@@ -2099,10 +2102,6 @@ __global__ void __launch_bounds__(kCtaThreads, 4) k_score_list(SourceView src, c
         for (int64_t base = 0, r = 0; base < ns; base += kCtaPts, ++r) {
             const int b = static_cast<int>(r & 1);
             score_round_ab(S, src, g, sp, cand_rt + 12 * cand, base, b, ns, my_add - base, part);
-            if (threadIdx.x == 0) {
-                S.nq = 0;
-                S.nslow = 0;
-            }
             // the miss budget in point order (word w covers points base + 32 w ..)
             const int rm = round_misses(S.miss[b], base, misses, sp, visited);
             if (misses + rm > sp.miss_budget) {

@@ -99,6 +99,11 @@ class PointCloud:
         self.positions = np.ascontiguousarray(np.asarray(self.positions, dtype=np.float64).reshape(-1, 3))
         if self.normals is not None:
             self.normals = np.ascontiguousarray(np.asarray(self.normals, dtype=np.float64).reshape(-1, 3))
+            # lk_cloud has one count for both arrays: validate_cloud's size rule
+            # (geometry.cpp:93-96) is enforced before any pointer crosses the ABI
+            if self.normals.shape[0] not in (0, self.positions.shape[0]):
+                from .errors import MissingNormals
+                raise MissingNormals("normals array must be empty or match positions")
 
     def size(self) -> int:
         return int(self.positions.shape[0])
