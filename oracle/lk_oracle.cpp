@@ -1033,28 +1033,58 @@ static std::vector<std::array<float, 33>> compute_fpfh(const Cloud& cloud, doubl
     return out;
 }
 
-// Feature pre-match. The reference's float GEMV (grid.cpp:176-213) has an
-// Eigen-dependent summation order; its own test pins it to the FP64
-// exhaustive matcher (reference.hpp:56-76, test_grid.cpp:113-125), which is
-// the semantics restated here: strict < over ascending j (ties -> lowest j).
+// Feature pre-match: the reference binary's float matcher (grid.cpp:176-213),
+// score_j = |q_j|^2 - 2 (Q^T f)_j in FP32, argmin with strict < over ascending j
+// (ties -> lowest j). The reference's own test pins it only against the FP64
+// exhaustive matcher on random features (test_grid.cpp:113-125); on FPFH
+// near-ties the two differ (56 of 5,309 sources on B1), and the drop-in must
+// match the binary, so this restates Eigen 3.4's float evaluation order
+// (SSE2, no FMA; the same rules as oracle/ref_shim/Eigen/Dense, against which
+// tests/test_ref_parity.py checks it bit for bit):
+//   |q|^2: colwise().squaredNorm() -- redux over 33 floats: two 4-lane packet
+//     accumulators r0 (packets 0,2,4,6) and r1 (packets 1,3,5,7), r0 + r1,
+//     predux (l0 + l2) + (l1 + l3), then + q32^2;
+//   Q^T f: row-major GEMV -- 4 lane accumulators over the 8 whole packets in
+//     order (0 + a b, then + a b), predux, then + a32 b32; times alpha = 2
+//     (exact).
+static inline float eigen_qnorm33(const float* q) {
+    float r0[4], r1[4];
+    for (int l = 0; l < 4; ++l) {
+        r0[l] = q[l] * q[l];
+        r1[l] = q[4 + l] * q[4 + l];
+    }
+    for (int idx = 8; idx < 32; idx += 8)
+        for (int l = 0; l < 4; ++l) {
+            r0[l] = r0[l] + q[idx + l] * q[idx + l];
+            r1[l] = r1[l] + q[idx + 4 + l] * q[idx + 4 + l];
+        }
+    for (int l = 0; l < 4; ++l) r0[l] = r0[l] + r1[l];
+    float res = (r0[0] + r0[2]) + (r0[1] + r0[3]);
+    return res + q[32] * q[32];
+}
+static inline float eigen_dot33(const float* a, const float* b) {
+    float c[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    for (int k = 0; k < 32; k += 4)
+        for (int l = 0; l < 4; ++l) c[l] = a[k + l] * b[k + l] + c[l];
+    float cc = (c[0] + c[2]) + (c[1] + c[3]);
+    cc += a[32] * b[32];
+    return 0.0f + 2.0f * cc;
+}
 static std::vector<int32_t> feature_nn_cache(const float* sf, int64_t ns, const float* tf, int64_t nt, int threads) {
     if (ns <= 0 || nt <= 0) fail(OR_MISSING_DATA, "feature_nn_cache: empty feature set");
+    std::vector<float> q2(static_cast<size_t>(nt));
+    for (int64_t j = 0; j < nt; ++j) q2[static_cast<size_t>(j)] = eigen_qnorm33(tf + 33 * j);
     std::vector<int32_t> cache(ns, -1);
     if (threads <= 0) threads = omp_get_max_threads();
 #pragma omp parallel for schedule(static) num_threads(threads)
     for (int64_t i = 0; i < ns; ++i) {
-        double best_d2 = std::numeric_limits<double>::infinity();
-        int best = -1;
-        const float* s = sf + 33 * i;
-        for (int64_t j = 0; j < nt; ++j) {
-            const float* t = tf + 33 * j;
-            double d2 = 0.0;
-            for (int b = 0; b < 33; ++b) {
-                double diff = static_cast<double>(s[b]) - static_cast<double>(t[b]);
-                d2 += diff * diff;
-            }
-            if (d2 < best_d2) {
-                best_d2 = d2;
+        const float* f = sf + 33 * i;
+        int best = 0;
+        float best_s = q2[0] - eigen_dot33(tf, f);
+        for (int64_t j = 1; j < nt; ++j) {
+            float s = q2[static_cast<size_t>(j)] - eigen_dot33(tf + 33 * j, f);
+            if (s < best_s) {
+                best_s = s;
                 best = static_cast<int>(j);
             }
         }

@@ -23,8 +23,8 @@
 #include <vector>
 
 #include "../../include/loopkit_b200.h"
+#include "lk_host_math.hpp"
 #include "lk_kernels.cuh"
-#include "lk_prepare_host.hpp"
 
 namespace {
 
@@ -1261,7 +1261,13 @@ lk_status lk_compute_fpfh(const lk_cloud* cloud, double radius, int32_t threads,
         if (cloud->n == 0) return fail(LK_EMPTY_CLOUD, "compute_fpfh: empty cloud");
         if (!cloud->nxyz) return fail(LK_MISSING_NORMALS, "compute_fpfh: cloud has no normals");
         if (!(radius > 0.0)) return fail(LK_INVALID_ARGUMENT, "build_grid: cell_length must be positive");
-        lk::validate_cloud(lk::make_cloud(cloud->xyz, cloud->nxyz, cloud->n));
+        // validate_cloud (proj/src/geometry.cpp:93-103): unit length (1e-6) or exactly zero
+        for (int64_t i = 0; i < cloud->n; ++i) {
+            const double* q = cloud->nxyz + 3 * i;
+            const double len = std::sqrt((q[0] * q[0] + q[1] * q[1]) + q[2] * q[2]);
+            if (len != 0.0 && std::abs(len - 1.0) > 1e-6)
+                return fail(LK_MISSING_NORMALS, "normals must be unit length or exactly zero");
+        }
         select_device(-1);
         cudaStream_t s;
         CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));

@@ -6,10 +6,19 @@
 // lk_device_math.cuh. Compiled with -ffp-contract=off (no FMA).
 #pragma once
 
+#include <stdexcept>
+#include <string>
+
 #include <cmath>
 #include <cstdint>
 
 namespace lk {
+
+// Error carrying an lk_status code (include/loopkit_b200.h).
+struct Status : std::runtime_error {
+    int code;
+    Status(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
 
 struct Vec3 {
     double x = 0, y = 0, z = 0;

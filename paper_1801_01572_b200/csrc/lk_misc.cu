@@ -1,4 +1,4 @@
-// lk_misc.cu -- feature pre-match (K1), edge_info (K8), point transforms.
+// lk_misc.cu -- feature pre-match (K1, the reference binary's float matcher), edge_info (K8), point transforms.
 #include <cstdint>
 #include <cstdlib>
 
@@ -13,93 +13,107 @@ namespace {
 
 constexpr int kFeatDim = 33;
 constexpr int kFeatThreads = 128;
-constexpr int kFeatTile = 128;
 
-// argmin_j sum_b (double(s_b) - double(t_b))^2, strict < over ascending j
-// (proj/include/loopkit/reference.hpp:56-76). One thread per source feature;
-// target features are staged through shared memory tile by tile and read as
-// broadcasts.
-__global__ void __launch_bounds__(kFeatThreads) k_feature_nn(const float* __restrict__ sf, int64_t ns,
-                                                             const float* __restrict__ tf, int64_t nt,
-                                                             int32_t* __restrict__ out) {
-    __shared__ float s_t[kFeatTile * kFeatDim];
-    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    float f[kFeatDim];
-#pragma unroll
-    for (int b = 0; b < kFeatDim; ++b) f[b] = i < ns ? sf[i * kFeatDim + b] : 0.0f;
-    double best_d2 = __longlong_as_double(0x7ff0000000000000ll);
-    int32_t best = -1;
-    for (int64_t j0 = 0; j0 < nt; j0 += kFeatTile) {
-        const int64_t tile = nt - j0 < kFeatTile ? nt - j0 : kFeatTile;
-        __syncthreads();
-        for (int64_t q = threadIdx.x; q < tile * kFeatDim; q += blockDim.x) s_t[q] = tf[j0 * kFeatDim + q];
-        __syncthreads();
-        for (int jj = 0; jj < tile; ++jj) {
-            const float* t = s_t + jj * kFeatDim;
-            double d2 = 0.0;
-#pragma unroll
-            for (int b = 0; b < kFeatDim; ++b) {
-                double diff = static_cast<double>(f[b]) - static_cast<double>(t[b]);
-                d2 += diff * diff;
-            }
-            if (d2 < best_d2) {
-                best_d2 = d2;
-                best = static_cast<int32_t>(j0 + jj);
-            }
-        }
-    }
-    if (i < ns) out[i] = best;
-}
-
-// ---- FP32 pre-match with exact FP64 resolution of near-ties ---------------
-// d2f = sum_b fl(s_b - t_b)^2 via fmaf is within (2 + 33 + 1) * 2^-24 < 2.2e-6
-// relative of the exact d2 (all terms are non-negative). Every (source,
-// target-chunk) keeps its FP32 best (value, lowest index) and runner-up;
-// chunks merge in ascending order. A source whose runner-up lies within
-// kTieRel of the best is resolved exactly in FP64 over all targets within
-// that band (ties -> lowest index, as reference.hpp:56-76). d2f == 0 implies
-// identical features, hence an exact zero: no resolution needed.
+// ---- feature pre-match (K1): the reference binary's float matcher ---------
+// proj/src/grid.cpp:176-213: score_j = |q_j|^2 - 2 (Q^T f)_j in FP32 through
+// Eigen (x86-64 SSE2, no FMA), argmin with strict < over ascending j (ties ->
+// lowest j). Every score is reproduced bit for bit (the order below is Eigen
+// 3.4's, restated in oracle/lk_oracle.cpp and oracle/ref_shim/Eigen/Dense and
+// checked against the reference build there), so the argmin needs no
+// tie-band rescan:
+//   |q|^2 (colwise().squaredNorm(), redux_impl LinearVectorized): 4-lane
+//     accumulators r0 = packets 0,2,4,6 and r1 = packets 1,3,5,7 (adds in
+//     order), r0 + r1, predux (l0 + l2) + (l1 + l3), + q32^2;
+//   (Q^T f)_j (row-major general_matrix_vector_product): lanes
+//     c_l = (((0 + a_l b_l) + a_{4+l} b_{4+l}) + ...) over the 8 whole
+//     packets, predux (c0 + c2) + (c1 + c3), + a32 b32, times alpha 2 (exact).
+// Products and sums are separately rounded (mul/add .rn, packed FP32x2 where
+// two lanes run the same chain), never fused.
 constexpr int kFnnThreads = 128;
 constexpr int kFnnTile = 64;
 constexpr int kFnnPad = 36;  // 33 bins padded to 9 float4
-constexpr float kTieRel = 1e-5f;
 
-struct Best3 {
-    float f1;
-    int32_t j1;
-    float f2;
+struct BestF {
+    float s;
+    int32_t j;
 };
 
-// packed FP32 pairs (sm_100a FADD2 / FFMA2): lo = first, hi = second
+// packed FP32 pairs (sm_100a FMUL2 / FADD2): lo = first, hi = second
 __device__ __forceinline__ unsigned long long pack2(float lo, float hi) {
     return (static_cast<unsigned long long>(__float_as_uint(hi)) << 32) | __float_as_uint(lo);
 }
 __device__ __forceinline__ float2 unpack2(unsigned long long v) {
     return make_float2(__uint_as_float(static_cast<unsigned>(v)), __uint_as_float(static_cast<unsigned>(v >> 32)));
 }
-__device__ __forceinline__ unsigned long long sub2(unsigned long long a, unsigned long long b) {
+__device__ __forceinline__ unsigned long long add2(unsigned long long a, unsigned long long b) {
     unsigned long long r;
-    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
     return r;
 }
-__device__ __forceinline__ unsigned long long fma2(unsigned long long a, unsigned long long b, unsigned long long c) {
+__device__ __forceinline__ unsigned long long mul2(unsigned long long a, unsigned long long b) {
     unsigned long long r;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
     return r;
 }
 
-__device__ __forceinline__ float feat_d2f(const float4* a, const float4* b) {
-    float acc = 0.0f;
+// colwise().squaredNorm() of one 33-bin feature, Eigen's order
+__device__ __forceinline__ float eigen_qnorm33(const float* q) {
+    float r0[4], r1[4];
 #pragma unroll
-    for (int q = 0; q < kFnnPad / 4; ++q) {
-        const float4 x = a[q], y = b[q];
-        float d;
-        d = x.x - y.x; acc = fmaf(d, d, acc);
-        d = x.y - y.y; acc = fmaf(d, d, acc);
-        d = x.z - y.z; acc = fmaf(d, d, acc);
-        d = x.w - y.w; acc = fmaf(d, d, acc);
+    for (int l = 0; l < 4; ++l) {
+        r0[l] = __fmul_rn(q[l], q[l]);
+        r1[l] = __fmul_rn(q[4 + l], q[4 + l]);
     }
-    return acc;
+#pragma unroll
+    for (int idx = 8; idx < 32; idx += 8)
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+            r0[l] = __fadd_rn(r0[l], __fmul_rn(q[idx + l], q[idx + l]));
+            r1[l] = __fadd_rn(r1[l], __fmul_rn(q[idx + 4 + l], q[idx + 4 + l]));
+        }
+#pragma unroll
+    for (int l = 0; l < 4; ++l) r0[l] = __fadd_rn(r0[l], r1[l]);
+    const float res = __fadd_rn(__fadd_rn(r0[0], r0[2]), __fadd_rn(r0[1], r0[3]));
+    return __fadd_rn(res, __fmul_rn(q[32], q[32]));
+}
+
+// one score, scalar: the exhaustive path (LK_FP64_ONLY=1) and the reference
+// for the packed kernel below
+__device__ __forceinline__ float eigen_score(float q2, const float* a, const float* b) {
+    float c[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+    for (int k = 0; k < 32; k += 4)
+#pragma unroll
+        for (int l = 0; l < 4; ++l) c[l] = __fadd_rn(__fmul_rn(a[k + l], b[k + l]), c[l]);
+    float cc = __fadd_rn(__fadd_rn(c[0], c[2]), __fadd_rn(c[1], c[3]));
+    cc = __fadd_rn(cc, __fmul_rn(a[32], b[32]));
+    return __fsub_rn(q2, __fmul_rn(2.0f, cc));
+}
+
+__global__ void k_fnn_qnorm(const float* __restrict__ tf, int64_t nt, float* __restrict__ q2) {
+    const int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (j < nt) q2[j] = eigen_qnorm33(tf + j * kFeatDim);
+}
+
+// exhaustive: one thread per source over every target in order
+__global__ void __launch_bounds__(kFeatThreads) k_feature_nn_exact(const float* __restrict__ sf, int64_t ns,
+                                                                   const float* __restrict__ tf, int64_t nt,
+                                                                   const float* __restrict__ q2,
+                                                                   int32_t* __restrict__ out) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= ns) return;
+    float f[kFeatDim];
+    for (int b = 0; b < kFeatDim; ++b) f[b] = sf[i * kFeatDim + b];
+    int32_t best = 0;
+    float best_s = eigen_score(q2[0], tf, f);
+    for (int64_t j = 1; j < nt; ++j) {
+        const float s = eigen_score(q2[j], tf + j * kFeatDim, f);
+        if (s < best_s) {
+            best_s = s;
+            best = static_cast<int32_t>(j);
+        }
+    }
+    out[i] = best;
 }
 
 __global__ void k_pad_features(const float* __restrict__ f, int64_t n, float4* __restrict__ out) {
@@ -115,103 +129,86 @@ __global__ void k_pad_features(const float* __restrict__ f, int64_t n, float4* _
     out[t] = make_float4(v[0], v[1], v[2], v[3]);
 }
 
-// grid (source blocks, target chunks): FP32 best / runner-up per pair
+// grid (source blocks, target chunks): the chunk's best (score, lowest j) per
+// source. Target tiles staged in shared memory and read as broadcasts; four
+// targets at a time, the lane pairs (0,1) and (2,3) of Eigen's 4-lane
+// accumulators as packed FP32x2 chains (one FMUL2 + one FADD2 per two bins).
 __global__ void __launch_bounds__(kFnnThreads) k_fnn_partial(const float4* __restrict__ sf, int64_t ns,
-                                                             const float4* __restrict__ tf, int64_t nt,
-                                                             int64_t chunk, Best3* __restrict__ partial) {
+                                                             const float4* __restrict__ tf,
+                                                             const float* __restrict__ q2, int64_t nt,
+                                                             int64_t chunk, BestF* __restrict__ partial) {
     __shared__ float4 s_t[kFnnTile * (kFnnPad / 4)];
+    __shared__ float s_q2[kFnnTile];
     const int64_t i = blockIdx.x * static_cast<int64_t>(kFnnThreads) + threadIdx.x;
     float4 s[kFnnPad / 4];
 #pragma unroll
     for (int q = 0; q < kFnnPad / 4; ++q) s[q] = i < ns ? sf[i * (kFnnPad / 4) + q] : make_float4(0, 0, 0, 0);
+    unsigned long long x01[8], x23[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        x01[q] = pack2(s[q].x, s[q].y);
+        x23[q] = pack2(s[q].z, s[q].w);
+    }
+    const float x32 = s[8].x;
     const int64_t j_begin = blockIdx.y * chunk;
     const int64_t j_end = j_begin + chunk < nt ? j_begin + chunk : nt;
-    float f1 = __int_as_float(0x7f800000), f2 = f1;
-    int32_t j1 = -1;
+    float best_s = __int_as_float(0x7f800000);
+    int32_t best_j = -1;
     for (int64_t j0 = j_begin; j0 < j_end; j0 += kFnnTile) {
         const int tile = static_cast<int>(j_end - j0 < kFnnTile ? j_end - j0 : kFnnTile);
         __syncthreads();
         for (int q = threadIdx.x; q < tile * (kFnnPad / 4); q += kFnnThreads) s_t[q] = tf[j0 * (kFnnPad / 4) + q];
+        for (int q = threadIdx.x; q < tile; q += kFnnThreads) s_q2[q] = q2[j0 + q];
         __syncthreads();
-        auto take = [&](float d2, int64_t j) {
-            if (d2 < f1) {
-                f2 = f1;
-                f1 = d2;
-                j1 = static_cast<int32_t>(j);
-            } else if (d2 < f2) {
-                f2 = d2;
+        auto take = [&](float sc, int jj) {
+            if (sc < best_s || best_j < 0) {
+                best_s = sc;
+                best_j = static_cast<int32_t>(j0 + jj);
             }
         };
         int jj = 0;
-        // four targets at a time, two partial sums each (bins x, z and y, w of
-        // every float4): eight independent FMA chains, run as packed FP32x2
-        // pairs (FADD2 / FFMA2: one instruction per two bins). Any summation
-        // order stays within the 2.2e-6 bound the near-tie rescan assumes.
         for (; jj + 4 <= tile; jj += 4) {
-            unsigned long long a[4] = {0ull, 0ull, 0ull, 0ull};  // (even, odd) partial sums
+            unsigned long long c01[4], c23[4];
 #pragma unroll
-            for (int q = 0; q < kFnnPad / 4; ++q) {
-                const float4 x = s[q];
-                const unsigned long long xlo = pack2(x.x, x.y), xhi = pack2(x.z, x.w);
+            for (int u = 0; u < 4; ++u) {
+                const float4 y = s_t[(jj + u) * (kFnnPad / 4)];
+                c01[u] = mul2(pack2(y.x, y.y), x01[0]);  // 0 + a b == a b (features are >= 0)
+                c23[u] = mul2(pack2(y.z, y.w), x23[0]);
+            }
+#pragma unroll
+            for (int q = 1; q < 8; ++q)
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     const float4 y = s_t[(jj + u) * (kFnnPad / 4) + q];
-                    const unsigned long long dlo = sub2(xlo, pack2(y.x, y.y));
-                    a[u] = fma2(dlo, dlo, a[u]);
-                    const unsigned long long dhi = sub2(xhi, pack2(y.z, y.w));
-                    a[u] = fma2(dhi, dhi, a[u]);
+                    c01[u] = add2(mul2(pack2(y.x, y.y), x01[q]), c01[u]);
+                    c23[u] = add2(mul2(pack2(y.z, y.w), x23[q]), c23[u]);
                 }
-            }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const float2 v = unpack2(a[u]);
-                take(v.x + v.y, j0 + jj + u);
+                const float2 p = unpack2(add2(c01[u], c23[u]));  // (c0 + c2, c1 + c3)
+                float cc = __fadd_rn(p.x, p.y);
+                cc = __fadd_rn(cc, __fmul_rn(s_t[(jj + u) * (kFnnPad / 4) + 8].x, x32));
+                take(__fsub_rn(s_q2[jj + u], __fmul_rn(2.0f, cc)), jj + u);
             }
         }
-        for (; jj < tile; ++jj) take(feat_d2f(s, s_t + jj * (kFnnPad / 4)), j0 + jj);
+        for (; jj < tile; ++jj) {
+            const float* t = reinterpret_cast<const float*>(s_t + jj * (kFnnPad / 4));
+            take(eigen_score(s_q2[jj], t, reinterpret_cast<const float*>(s)), jj);
+        }
     }
-    if (i < ns) partial[blockIdx.y * ns + i] = Best3{f1, j1, f2};
+    if (i < ns) partial[blockIdx.y * ns + i] = BestF{best_s, best_j};
 }
 
-__global__ void k_fnn_merge(const float4* __restrict__ sf, const float* __restrict__ sraw, int64_t ns,
-                            const float4* __restrict__ tf, const float* __restrict__ traw, int64_t nt,
-                            const Best3* __restrict__ partial, int n_chunks, int32_t* __restrict__ out) {
+// chunks in ascending j order, strict <: the lowest index wins ties
+__global__ void k_fnn_merge(int64_t ns, const BestF* __restrict__ partial, int n_chunks, int32_t* __restrict__ out) {
     const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (i >= ns) return;
-    Best3 b = partial[i];
+    BestF b = partial[i];
     for (int c = 1; c < n_chunks; ++c) {
-        const Best3 p = partial[c * ns + i];
-        if (p.f1 < b.f1) {
-            b.f2 = fminf(b.f1, p.f2);
-            b.f1 = p.f1;
-            b.j1 = p.j1;
-        } else {
-            b.f2 = fminf(b.f2, p.f1);  // equal values keep the earlier (lower) index
-        }
+        const BestF p = partial[c * ns + i];
+        if (p.s < b.s) b = p;
     }
-    int32_t best = b.j1;
-    if (b.f1 > 0.0f && b.f2 <= b.f1 * (1.0f + kTieRel)) {
-        // near-tie: exact FP64 distances for every target within the band
-        const float lim = b.f1 * (1.0f + kTieRel);
-        float4 s[kFnnPad / 4];
-#pragma unroll
-        for (int q = 0; q < kFnnPad / 4; ++q) s[q] = sf[i * (kFnnPad / 4) + q];
-        double best_d2 = __longlong_as_double(0x7ff0000000000000ll);
-        best = -1;
-        for (int64_t j = 0; j < nt; ++j) {
-            if (feat_d2f(s, tf + j * (kFnnPad / 4)) > lim) continue;
-            double d2 = 0.0;
-            for (int q = 0; q < kFeatDim; ++q) {
-                const double diff = static_cast<double>(sraw[i * kFeatDim + q]) - static_cast<double>(traw[j * kFeatDim + q]);
-                d2 += diff * diff;
-            }
-            if (d2 < best_d2) {
-                best_d2 = d2;
-                best = static_cast<int32_t>(j);
-            }
-        }
-    }
-    out[i] = best;
+    out[i] = b.j;
 }
 
 struct Xf {
@@ -337,9 +334,14 @@ __global__ void k_info_final(const double* __restrict__ partials, int nb, const 
 
 cudaError_t feature_nn(const float* d_sf, int64_t ns, const float* d_tf, int64_t nt, int32_t* d_out,
                        cudaStream_t stream) {
+    float* q2 = nullptr;
+    cudaError_t e;
+    if ((e = pool_alloc(&q2, nt * sizeof(float), stream)) != cudaSuccess) return e;
+    k_fnn_qnorm<<<static_cast<unsigned>((nt + 255) / 256), 256, 0, stream>>>(d_tf, nt, q2);
     if (const char* v = std::getenv("LK_FP64_ONLY"); v && v[0] == '1') {
         const unsigned blocks = static_cast<unsigned>((ns + kFeatThreads - 1) / kFeatThreads);
-        k_feature_nn<<<blocks, kFeatThreads, 0, stream>>>(d_sf, ns, d_tf, nt, d_out);
+        k_feature_nn_exact<<<blocks, kFeatThreads, 0, stream>>>(d_sf, ns, d_tf, nt, q2, d_out);
+        pool_free(q2, stream);
         return cudaGetLastError();
     }
     int dev = 0, sms = 148;
@@ -352,20 +354,20 @@ cudaError_t feature_nn(const float* d_sf, int64_t ns, const float* d_tf, int64_t
     const int64_t chunk = (nt + n_chunks - 1) / n_chunks;
     n_chunks = (nt + chunk - 1) / chunk;
     float4 *sp = nullptr, *tp = nullptr;
-    Best3* partial = nullptr;
-    cudaError_t e;
+    BestF* partial = nullptr;
     if ((e = pool_alloc(&sp, ns * kFnnPad * sizeof(float), stream)) != cudaSuccess) return e;
     if ((e = pool_alloc(&tp, nt * kFnnPad * sizeof(float), stream)) != cudaSuccess) return e;
-    if ((e = pool_alloc(&partial, n_chunks * ns * sizeof(Best3), stream)) != cudaSuccess) return e;
+    if ((e = pool_alloc(&partial, n_chunks * ns * sizeof(BestF), stream)) != cudaSuccess) return e;
     k_pad_features<<<static_cast<unsigned>((ns * 9 + 255) / 256), 256, 0, stream>>>(d_sf, ns, sp);
     k_pad_features<<<static_cast<unsigned>((nt * 9 + 255) / 256), 256, 0, stream>>>(d_tf, nt, tp);
     k_fnn_partial<<<dim3(static_cast<unsigned>(src_blocks), static_cast<unsigned>(n_chunks)), kFnnThreads, 0,
-                    stream>>>(sp, ns, tp, nt, chunk, partial);
-    k_fnn_merge<<<static_cast<unsigned>((ns + 255) / 256), 256, 0, stream>>>(sp, d_sf, ns, tp, d_tf, nt, partial,
-                                                                            static_cast<int>(n_chunks), d_out);
+                    stream>>>(sp, ns, tp, q2, nt, chunk, partial);
+    k_fnn_merge<<<static_cast<unsigned>((ns + 255) / 256), 256, 0, stream>>>(ns, partial, static_cast<int>(n_chunks),
+                                                                            d_out);
     pool_free(sp, stream);
     pool_free(tp, stream);
     pool_free(partial, stream);
+    pool_free(q2, stream);
     return cudaGetLastError();
 }
 

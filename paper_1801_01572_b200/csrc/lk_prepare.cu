@@ -15,7 +15,8 @@
 //   neighbour lists within r (SearchGrid cell = r, ascending, self excluded),
 //   k_spfh    warp per point: pair-angle votes as integer counts; pairs whose
 //             frame-source test (std::acos comparison) the device cannot
-//             decide are deferred to the host's libm (k_spfh_resolve), then
+//             decide, or whose theta (atan2) lies at a bin edge, are deferred
+//             to the host's libm (host_pair_bins, k_spfh_resolve), then
 //             k_spfh_scale applies fl(100 / votes) like `v *= 100.0 / votes`
 //   k_fpfh    warp per point, lane per bin: acc_b += spfh_j[b] / w_j over the
 //             neighbours in ascending order (the reference's summation order)
@@ -273,7 +274,13 @@ __device__ __forceinline__ bool pair_setup(V3 p1, V3 n1, V3 p2, V3 n2, PairSetup
     s.a2 = dot(n2, s.d) / s.dist;
     return true;
 }
-__device__ __forceinline__ bool pair_bins(const PairSetup& s, V3 n1, V3 n2, int swap, int3& bins) {
+// theta = atan2(w.nt, u.nt) comes from CUDA's atan2 (<= 2 ulp) where the
+// reference uses glibc's; its bin floor(11 (theta + pi) / 2 pi) is decided
+// here only when that value is more than 1e-12 from an inner bin edge (the
+// two libms put it within ~1e-14 of each other); otherwise theta_edge is set
+// and the pair goes to the host (k_spfh's deferred list). alpha and phi are
+// plain IEEE arithmetic, identical on both sides.
+__device__ __forceinline__ bool pair_bins(const PairSetup& s, V3 n1, V3 n2, int swap, int3& bins, bool& theta_edge) {
     V3 ns = n1, nt = n2, line = s.d;
     double cos_line = s.a1;
     if (swap == 1) {
@@ -285,12 +292,16 @@ __device__ __forceinline__ bool pair_bins(const PairSetup& s, V3 n1, V3 n2, int 
     V3 u = ns;
     V3 v = cross(line, u);
     double v_len = sqrt(sqnorm(v));
+    theta_edge = false;
     if (v_len <= 1e-12 * s.dist) return false;
     v = mk(v.x / v_len, v.y / v_len, v.z / v_len);
     V3 w = cross(u, v);
     const double alpha = dot(v, nt);
     const double phi = cos_line;
     const double theta = atan2(dot(w, nt), dot(u, nt));
+    const double tv = 11 * (theta - -M_PI) / (M_PI - -M_PI);
+    const double edge = rint(tv);
+    theta_edge = edge >= 1.0 && edge <= 10.0 && fabs(tv - edge) < 1e-12;
     bins = make_int3(bin_index(alpha, -1.0, 1.0), 11 + bin_index(phi, -1.0, 1.0),
                      22 + bin_index(theta, -M_PI, M_PI));
     return true;
@@ -472,13 +483,22 @@ __device__ __forceinline__ double div_by(double a, double b, double r) {
 // pass 1 (proj/src/fpfh.cpp:76-100): warp per point, integer vote counts in
 // counts[i][0..32], votes in counts[i][33]. Pairs whose frame-source test the
 // device cannot decide are appended to the deferred list (k_spfh_resolve).
+// A pair the device cannot settle (frame-source acos test undecided and
+// deciding, or theta at a bin edge) is appended to the deferred list with its
+// two points and normals; the host evaluates pair_angles with the reference's
+// libm and returns its three bins (k_spfh_resolve).
+struct DeferredPair {
+    double v[12];  // p1, n1, p2, n2
+};
+
 __global__ void __launch_bounds__(32 * kFpfhWarps) k_spfh(const double* __restrict__ pos,
                                                           const double* __restrict__ nrm, int64_t n,
                                                           const int32_t* __restrict__ off,
                                                           const int32_t* __restrict__ nbr, int32_t* __restrict__ counts,
-                                                          int2* __restrict__ deferred, double2* __restrict__ deferred_x,
+                                                          int2* __restrict__ deferred,
+                                                          DeferredPair* __restrict__ deferred_x,
                                                           int32_t* __restrict__ n_deferred, int64_t cap,
-                                                          const int32_t* __restrict__ skip) {
+                                                          int64_t dcap, const int32_t* __restrict__ skip) {
     __shared__ int hist[kFpfhWarps][34];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t i = blockIdx.x * static_cast<int64_t>(kFpfhWarps) + warp;
@@ -493,24 +513,33 @@ __global__ void __launch_bounds__(32 * kFpfhWarps) k_spfh(const double* __restri
             const int32_t j = nbr[k];
             const V3 nq = ld3(nrm, j);
             if (is_zero(nq)) continue;
+            const V3 q = ld3(pos, j);
             PairSetup s;
-            if (!pair_setup(p, np, ld3(pos, j), nq, s)) continue;
+            if (!pair_setup(p, np, q, nq, s)) continue;
             const int dec = swap_decision(fabs(s.a1), fabs(s.a2));
             int3 bins;
-            bool valid;
+            bool valid, edge;
+            bool defer = false;
             if (dec == 2) {
                 // undecidable here: settle it only if the outcome depends on it
                 int3 b1;
-                valid = pair_bins(s, np, nq, 0, bins);
-                const bool valid1 = pair_bins(s, np, nq, 1, b1);
-                if (valid != valid1 || (valid && (bins.x != b1.x || bins.y != b1.y || bins.z != b1.z))) {
-                    const int32_t slot = atomicAdd(n_deferred, 1);
-                    deferred[slot] = make_int2(static_cast<int32_t>(i), j);
-                    deferred_x[slot] = make_double2(fabs(s.a1), fabs(s.a2));
-                    continue;
-                }
+                bool edge1;
+                valid = pair_bins(s, np, nq, 0, bins, edge);
+                const bool valid1 = pair_bins(s, np, nq, 1, b1, edge1);
+                defer = edge || edge1 || valid != valid1 ||
+                        (valid && (bins.x != b1.x || bins.y != b1.y || bins.z != b1.z));
             } else {
-                valid = pair_bins(s, np, nq, dec, bins);
+                valid = pair_bins(s, np, nq, dec, bins, edge);
+                defer = edge;
+            }
+            if (defer) {
+                const int32_t slot = atomicAdd(n_deferred, 1);
+                if (slot >= dcap) continue;  // list full: the host sees n_deferred > dcap and redoes the pass
+                deferred[slot] = make_int2(static_cast<int32_t>(i), j);
+                DeferredPair& d = deferred_x[slot];
+                d.v[0] = p.x, d.v[1] = p.y, d.v[2] = p.z, d.v[3] = np.x, d.v[4] = np.y, d.v[5] = np.z;
+                d.v[6] = q.x, d.v[7] = q.y, d.v[8] = q.z, d.v[9] = nq.x, d.v[10] = nq.y, d.v[11] = nq.z;
+                continue;
             }
             if (!valid) continue;
             atomicAdd(&hist[warp][bins.x], 1);
@@ -525,21 +554,18 @@ __global__ void __launch_bounds__(32 * kFpfhWarps) k_spfh(const double* __restri
     if (lane == 0) counts[34 * i + 33] = votes;
 }
 
-// deferred pairs with the host's decisions (0/1) of the frame-source test
-__global__ void k_spfh_resolve(const double* __restrict__ pos, const double* __restrict__ nrm,
-                               const int2* __restrict__ deferred, const uint8_t* __restrict__ decision, int32_t m,
+// deferred pairs with the host's bins: (alpha bin, 11 + phi bin, 22 + theta
+// bin) packed as bytes 0-2, byte 3 = 1 for a vote (0: the pair casts none)
+__global__ void k_spfh_resolve(const int2* __restrict__ deferred, const uint32_t* __restrict__ decision, int32_t m,
                                int32_t* __restrict__ counts) {
     const int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= m) return;
-    const int2 ij = deferred[k];
-    const V3 n1 = ld3(nrm, ij.x), n2 = ld3(nrm, ij.y);
-    PairSetup s;
-    int3 bins;
-    if (!pair_setup(ld3(pos, ij.x), n1, ld3(pos, ij.y), n2, s) || !pair_bins(s, n1, n2, decision[k], bins)) return;
-    int32_t* c = counts + 34 * static_cast<int64_t>(ij.x);
-    atomicAdd(c + bins.x, 1);
-    atomicAdd(c + bins.y, 1);
-    atomicAdd(c + bins.z, 1);
+    const uint32_t d = decision[k];
+    if (!(d >> 24)) return;
+    int32_t* c = counts + 34 * static_cast<int64_t>(deferred[k].x);
+    atomicAdd(c + (d & 0xff), 1);
+    atomicAdd(c + ((d >> 8) & 0xff), 1);
+    atomicAdd(c + ((d >> 16) & 0xff), 1);
     atomicAdd(c + 33, 1);
 }
 
@@ -896,18 +922,61 @@ cudaError_t voxel_downsample(const double* d_pos, const double* d_nrm, int64_t n
     return cudaGetLastError();
 }
 
+// proj/src/fpfh.cpp:17-53 on the host with the reference's libm (std::acos,
+// std::atan2) for the pairs k_spfh defers. Same IEEE operation order as the
+// device (-ffp-contract=off), so everything but the two libm calls agrees
+// bit for bit. Returns the packed bins of k_spfh_resolve.
+static uint32_t host_pair_bins(const double* v) {
+    struct H {
+        double x, y, z;
+    };
+    auto sub3 = [](H a, H b) { return H{a.x - b.x, a.y - b.y, a.z - b.z}; };
+    auto dot3 = [](H a, H b) { return (a.x * b.x + a.y * b.y) + a.z * b.z; };
+    auto cross3 = [](H a, H b) { return H{a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x}; };
+    auto bin = [](double value, double lo, double hi) {
+        int b = static_cast<int>(std::floor(11 * (value - lo) / (hi - lo)));
+        return std::clamp(b, 0, 10);
+    };
+    const H p1{v[0], v[1], v[2]}, n1{v[3], v[4], v[5]}, p2{v[6], v[7], v[8]}, n2{v[9], v[10], v[11]};
+    const H d = sub3(p2, p1);
+    const double dist = std::sqrt(dot3(d, d));
+    if (dist <= 0.0) return 0;
+    const double angle1 = dot3(n1, d) / dist;
+    const double angle2 = dot3(n2, d) / dist;
+    H ns = n1, nt = n2, line = d;
+    double cos_line = angle1;
+    if (std::acos(std::abs(angle1)) > std::acos(std::abs(angle2))) {
+        ns = n2;
+        nt = n1;
+        line = H{-d.x, -d.y, -d.z};
+        cos_line = -angle2;
+    }
+    const H u = ns;
+    H w3 = cross3(line, u);
+    const double v_len = std::sqrt(dot3(w3, w3));
+    if (v_len <= 1e-12 * dist) return 0;
+    const H vv{w3.x / v_len, w3.y / v_len, w3.z / v_len};
+    const H w = cross3(u, vv);
+    const double alpha = dot3(vv, nt);
+    const double theta = std::atan2(dot3(w, nt), dot3(u, nt));
+    const uint32_t b0 = static_cast<uint32_t>(bin(alpha, -1.0, 1.0));
+    const uint32_t b1 = 11u + static_cast<uint32_t>(bin(cos_line, -1.0, 1.0));
+    const uint32_t b2 = 22u + static_cast<uint32_t>(bin(theta, -M_PI, M_PI));
+    return b0 | (b1 << 8) | (b2 << 16) | (1u << 24);
+}
+
 // Pinned host staging of compute_fpfh, one per host thread (each prepare side
 // runs on its own thread): the total neighbour count, the deferred count and
 // the first kStageX deferred pairs come back in one copy; the decisions go
 // back from here. Reused only after the caller's stream has synchronised.
 struct FpfhStage {
-    static constexpr int kStageX = 4096;
+    static constexpr int kStageX = 1024;
     struct Head {
         int32_t total, n_def, overflow, pad;
-        double2 x[kStageX];
+        DeferredPair x[kStageX];
     };
     Head* head = nullptr;
-    uint8_t* dec = nullptr;
+    uint32_t* dec = nullptr;
     size_t dec_cap = 0;
     ~FpfhStage() {
         if (head) cudaFreeHost(head);
@@ -949,17 +1018,18 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
     // per point; an overflow turns the fill and the votes into no-ops and is
     // redone below with the exact size
     int64_t cap = std::max<int64_t>(192 * n, 4096);
+    int64_t dcap = std::max<int64_t>(4 * n, 65536);  // deferred pairs are rare (acos ties, theta bin edges)
     int32_t *votes = nullptr, *n_def = nullptr;
     int2* deferred = nullptr;
-    double2* deferred_x = nullptr;
-    uint8_t* d_decision = nullptr;
+    DeferredPair* deferred_x = nullptr;
+    uint32_t* d_decision = nullptr;
     LK_TRY(cudaMallocAsync(&spfh, 33 * n * sizeof(double), stream));
     LK_TRY(cudaMallocAsync(&votes, 34 * n * sizeof(int32_t), stream));
     LK_TRY(cudaMallocAsync(&n_def, sizeof(int32_t), stream));
     for (int attempt = 0; attempt < 2; ++attempt) {
         LK_TRY(cudaMallocAsync(&nbr, cap * sizeof(int32_t), stream));
-        LK_TRY(cudaMallocAsync(&deferred, cap * sizeof(int2), stream));
-        LK_TRY(cudaMallocAsync(&deferred_x, cap * sizeof(double2), stream));
+        LK_TRY(cudaMallocAsync(&deferred, dcap * sizeof(int2), stream));
+        LK_TRY(cudaMallocAsync(&deferred_x, dcap * sizeof(DeferredPair), stream));
         LK_TRY(cudaMemsetAsync(n_def, 0, sizeof(int32_t), stream));
         if (brute && attempt == 0)
             k_nbr_compact<<<nblocks(32 * n, 256), 256, 0, stream>>>(slots, off, n, d_overflow, nbr, cap);
@@ -970,7 +1040,7 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
             k_nbr_fill<<<nblocks(n, kSortWarps), 32 * kSortWarps, 0, stream>>>(d_pos, n, g.view, r2, off, nbr, cap);
         // an overflowed slot table leaves nbr unfilled: the votes are skipped too
         k_spfh<<<nblocks(n, kFpfhWarps), 32 * kFpfhWarps, 0, stream>>>(d_pos, d_nrm, n, off, nbr, votes, deferred,
-                                                                       deferred_x, n_def, cap,
+                                                                       deferred_x, n_def, cap, dcap,
                                                                        (brute && attempt == 0) ? d_overflow : nullptr);
         // one round trip: total, deferred count and the first deferred pairs
         LK_TRY(cudaMemcpyAsync(&st.head->total, off + n, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
@@ -978,24 +1048,25 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
         st.head->overflow = 0;
         if (brute && attempt == 0)
             LK_TRY(cudaMemcpyAsync(&st.head->overflow, d_overflow, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
-        LK_TRY(cudaMemcpyAsync(st.head->x, deferred_x, FpfhStage::kStageX * sizeof(double2), cudaMemcpyDeviceToHost,
-                               stream));
+        LK_TRY(cudaMemcpyAsync(st.head->x, deferred_x, FpfhStage::kStageX * sizeof(DeferredPair),
+                               cudaMemcpyDeviceToHost, stream));
         LK_TRY(cudaStreamSynchronize(stream));
-        if (st.head->total <= cap && !st.head->overflow) break;
+        if (st.head->total <= cap && !st.head->overflow && st.head->n_def <= dcap) break;
         cudaFreeAsync(nbr, stream);
         cudaFreeAsync(deferred, stream);
         cudaFreeAsync(deferred_x, stream);
         cap = std::max<int64_t>(cap, st.head->total);
+        dcap = std::max<int64_t>(dcap, st.head->n_def);
     }
-    // frame-source tests the device cannot decide: the host's libm decides
-    // them exactly as the reference's std::acos comparison (fpfh.cpp:28)
+    // pairs the device cannot settle: the host evaluates pair_angles with the
+    // reference's libm (fpfh.cpp:17-53, host_pair_bins)
     const int32_t m = st.head->n_def;
     if (m > 0) {
-        std::vector<double2> more;
-        const double2* xs = st.head->x;
+        std::vector<DeferredPair> more;
+        const DeferredPair* xs = st.head->x;
         if (m > FpfhStage::kStageX) {
             more.resize(m);
-            LK_TRY(cudaMemcpyAsync(more.data(), deferred_x, m * sizeof(double2), cudaMemcpyDeviceToHost, stream));
+            LK_TRY(cudaMemcpyAsync(more.data(), deferred_x, m * sizeof(DeferredPair), cudaMemcpyDeviceToHost, stream));
             LK_TRY(cudaStreamSynchronize(stream));
             xs = more.data();
         }
@@ -1003,14 +1074,14 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
             if (st.dec) cudaFreeHost(st.dec);
             st.dec = nullptr;
             st.dec_cap = 0;
-            LK_TRY(cudaHostAlloc(reinterpret_cast<void**>(&st.dec), m, 0));
+            LK_TRY(cudaHostAlloc(reinterpret_cast<void**>(&st.dec), m * sizeof(uint32_t), 0));
             st.dec_cap = m;
         }
 #pragma omp parallel for schedule(static) if (m > 4096)
-        for (int32_t k = 0; k < m; ++k) st.dec[k] = std::acos(xs[k].x) > std::acos(xs[k].y) ? 1 : 0;
-        LK_TRY(cudaMallocAsync(&d_decision, m, stream));
-        LK_TRY(cudaMemcpyAsync(d_decision, st.dec, m, cudaMemcpyHostToDevice, stream));
-        k_spfh_resolve<<<nblocks(m, 256), 256, 0, stream>>>(d_pos, d_nrm, deferred, d_decision, m, votes);
+        for (int32_t k = 0; k < m; ++k) st.dec[k] = host_pair_bins(xs[k].v);
+        LK_TRY(cudaMallocAsync(&d_decision, m * sizeof(uint32_t), stream));
+        LK_TRY(cudaMemcpyAsync(d_decision, st.dec, m * sizeof(uint32_t), cudaMemcpyHostToDevice, stream));
+        k_spfh_resolve<<<nblocks(m, 256), 256, 0, stream>>>(deferred, d_decision, m, votes);
     }
     k_spfh_scale<<<nblocks(33 * n, 256), 256, 0, stream>>>(votes, n, spfh);
     k_fpfh<<<nblocks(n, kFpfhWarps), 32 * kFpfhWarps, 0, stream>>>(d_pos, d_nrm, n, off, nbr, spfh, d_out);

@@ -1,9 +1,7 @@
-// lk_prepare_host.hpp -- host side of prepare_registration for this tier.
-//
-// voxel_downsample (proj/src/preprocess.cpp:14-59) and compute_fpfh
-// (proj/src/fpfh.cpp:17-141) run once per cloud pair on the host with
-// OpenMP; the per-pair feature pre-match and the target grid are built on
-// the device (lk_kernels.cu). SURVEY.md 8f row f1 moves the rest on-device.
+// lk_prepare_host.hpp -- host restatements used by the FIXTURE library only
+// (libloopkit_synth.so: voxel_downsample, transformed, centroid, a SearchGrid
+// for the synth_registration_pair overlap test). The product library never
+// links them: prepare_registration runs on the device (lk_prepare.cu).
 #pragma once
 
 #include <array>
@@ -16,12 +14,6 @@
 #include "lk_host_math.hpp"
 
 namespace lk {
-
-// Error carrying an lk_status code (include/loopkit_b200.h).
-struct Status : std::runtime_error {
-    int code;
-    Status(int c, const std::string& m) : std::runtime_error(m), code(c) {}
-};
 
 struct Cloud {
     std::vector<Vec3> pos;
