@@ -12,9 +12,10 @@ range, sharded contiguously over ranks, plus the cross-rank record exchange.
   e2e    the same metric through the public API from pinned host clouds:
          prepare_registration + run + exchange + merge, every step.
 
-`python bench.py --impl reference` times the reference's algorithm on the
-host cores (the CPU oracle restatement -- the reference itself cannot be
-compiled here) on the same workload and metric.
+`python bench.py --impl reference` times the reference itself on the host
+cores: its own registration sources compiled unmodified into oracle/_ref
+(oracle/Makefile.ref, Eigen/doctest shim; OpenMP on every host thread), or the
+oracle restatement where that build is absent, on the same workload and metric.
 """
 from __future__ import annotations
 
@@ -35,10 +36,6 @@ sys.path.insert(0, ROOT)
 
 METRIC = "candidate×point evals/sec"
 UNIT = "evals/s"
-# kernels of one hypothesis step (lk_hypotheses.cu run_hypotheses_range):
-# k_hyp_sample, k_kabsch, k_score_units (exits at once unless the candidates
-# are few), k_score_cta
-KERNELS_PER_STEP = 4
 PAPER_MS_PER_REGISTRATION = 20.50  # PAPER.md:161 (Titan X Pascal, redwood pairs) -- context only
 
 
@@ -85,6 +82,20 @@ def peaks():
         return float(p["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+def onchip_peaks():
+    """The ceilings of an L2-resident gather (tools/peaks.cu, run on this pool's
+    B200s, committed as profiles/peaks.json): L2 random 32-B sector gather GB/s
+    (best working set), FP32 FMA TFLOP/s, or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "peaks.json")) as f:
+            p = json.load(f)
+        l2 = max(x["gbs"] for x in p["l2_random_sector"])
+        return {"l2_random_gbs": l2, "l2_stream_gbs": p["l2_stream"]["gbs"], "smem_gbs": p["smem"]["gbs"],
+                "fp32_tflops": p["fp32_fma"]["tflops"], "fp64_tflops": p["fp64_fma"]["tflops"]}
+    except Exception:
+        return None
 
 
 def ncu_traffic(kernels):
@@ -156,24 +167,55 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU
-def cpu_oracle_registration(pair, hypotheses, seed, budget_s=12.0, min_reps=1, max_reps=8):
-    """The reference algorithm on the host cores (oracle restatement, OpenMP
-    schedule(dynamic,256), all threads). Repeats full registrations of the
-    workload until ~budget_s of CPU work; returns the best repetition."""
+def _ref_module():
+    """oracle/_ref (the reference's own sources, prebuilt) when present, else None."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import ref as RF
+    return RF if os.path.exists(RF.LIB_PATH) else None
+
+
+_W_REF = {}
+
+
+def oracle_work(pair, hypotheses, seed):
+    """The oracle's run of the workload: its work counters (W_ref = the points
+    the reference loop visits, o / k / h of SURVEY.md 8d) are the metric's
+    numerator; the reference does not count them."""
+    key = (id(pair), hypotheses, seed)
+    if key not in _W_REF:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle as O
+        p = O.params(hypothesis_count=hypotheses, seed=seed, threads=os.cpu_count() or 0)
+        ctx = O.Context.prepare(pair.source.positions, pair.source.normals, pair.target.positions,
+                                pair.target.normals, p)
+        res, st = ctx.run(p)
+        _W_REF[key] = dict(stats=st, result=res, ns=ctx.ns, nt=ctx.nt)
+    return _W_REF[key]
+
+
+def cpu_reference_registration(pair, hypotheses, seed, budget_s=12.0, min_reps=1, max_reps=8):
+    """The reference on the host cores: register_global's prepare + run_hypotheses
+    from oracle/_ref (OpenMP schedule(dynamic,256), all threads), or the oracle
+    restatement when _ref is absent. Repeats full registrations until ~budget_s
+    of CPU work; returns the best repetition (kind "reference" or "port")."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
+    RF = _ref_module()
+    mod, kind = (RF, "reference") if RF is not None else (O, "port")
     p = O.params(hypothesis_count=hypotheses, seed=seed, threads=os.cpu_count() or 0)
+    work = oracle_work(pair, hypotheses, seed)
     best = None
     t_start = time.perf_counter()
     reps = 0
     while reps < min_reps or (time.perf_counter() - t_start < budget_s and reps < max_reps):
         t0 = time.perf_counter()
-        ctx = O.Context.prepare(pair.source.positions, pair.source.normals, pair.target.positions,
-                                pair.target.normals, p)
+        ctx = mod.Context.prepare(pair.source.positions, pair.source.normals, pair.target.positions,
+                                  pair.target.normals, p)
         t1 = time.perf_counter()
         res, st = ctx.run(p)
         t2 = time.perf_counter()
-        rec = dict(prepare_s=t1 - t0, run_s=t2 - t1, stats=st, result=res, ns=ctx.ns, nt=ctx.nt)
+        rec = dict(prepare_s=t1 - t0, run_s=t2 - t1, stats=dict(work["stats"]), result=res, ns=ctx.ns, nt=ctx.nt,
+                   kind=kind, parity=(res.hypothesis_index == work["result"].hypothesis_index))
         if best is None or rec["prepare_s"] + rec["run_s"] < best["prepare_s"] + best["run_s"]:
             best = rec
         reps += 1
@@ -200,7 +242,7 @@ def run_reference(args):
     threads = os.cpu_count()
     times, wref = [], None
     for step in range(args.warmup + args.steps):
-        rec = cpu_oracle_registration(pair, args.hypotheses, args.seed, budget_s=0.0)
+        rec = cpu_reference_registration(pair, args.hypotheses, args.seed, budget_s=0.0)
         if step >= args.warmup:
             times.append(rec)
         wref = rec["stats"]["w_ref"]
@@ -213,9 +255,11 @@ def run_reference(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": workload_config(args, pair.source.size(), pair.target.size(), times[0]["ns"], times[0]["nt"]),
         "ms_per_registration": reg_s * 1e3,
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": times[0]["kind"],
                          "sample": f"full B1 registration per step (prepare + {args.hypotheses:,} hypotheses), "
-                                   "oracle restatement, OpenMP dynamic,256 on all host threads"},
+                                   + ("the reference's own sources (oracle/_ref, -O3, Eigen shim)"
+                                      if times[0]["kind"] == "reference" else "oracle restatement")
+                                   + ", OpenMP dynamic,256 on all host threads; W_ref from the oracle's counters"},
         "e2e": {"value": wref / reg_s, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
                 "ms_per_registration": reg_s * 1e3},
         "gpu_launches": 0,
@@ -344,6 +388,75 @@ def bench_b2(args):
     return out
 
 
+def bench_config_a(args):
+    """configs[0]: the ~10k-point scatter-scene surface
+    pair (density 150, noise 0.005): all 9,261 lattice candidates scored with
+    evaluate_hypothesis semantics (SearchGrid cell 0.075, no early exit), and
+    register_global H = 10^4 seed 1, through the public API from host arrays.
+    Parity against the committed reference golden file (oracle/_ref output)."""
+    import paper_1801_01572_b200 as lk
+    from paper_1801_01572_b200 import synth
+    g = json.load(open(os.path.join(ROOT, "tests", "golden", "ref_golden.json")))
+    pair = synth.surface_pair(1, density=150.0)
+    rt, ti = synth.lattice_candidates(pair.truth)
+    params = lk.RegistrationParams()
+    grid = lk.build_grid(pair.target, 0.075)
+    lk.score_candidates(grid, pair.source, rt[:64], params)  # warm-up
+    times = []
+    for _ in range(5):
+        t0 = time.perf_counter()
+        sc = lk.score_candidates(grid, pair.source, rt, params)
+        times.append(time.perf_counter() - t0)
+    lat_s = min(times)
+    evals = rt.shape[0] * pair.source.size()
+    rp = lk.RegistrationParams(hypothesis_count=10_000, seed=1)
+    lk.register_global(pair.source, pair.target, rp)  # warm-up
+    rtimes, st = [], lk.HypothesisStats()
+    for _ in range(5):
+        t0 = time.perf_counter()
+        res = lk.register_global(pair.source, pair.target, rp, st)
+        rtimes.append(time.perf_counter() - t0)
+    out = {"workload": "A: surface_pair(make_scatter_scene(1), density 150, noise 0.005): 9,261-candidate lattice "
+                       "(2 deg / 2 cm around truth, evaluate_hypothesis semantics) + register_global H=1e4 seed 1",
+           "source_points": pair.source.size(), "target_points": pair.target.size(),
+           "lattice_candidates": int(rt.shape[0]), "lattice_evals": evals, "lattice_ms": 1e3 * lat_s,
+           "lattice_evals_per_s": evals / lat_s,
+           "register_ms": 1e3 * min(rtimes), "register_index": res.hypothesis_index if res else -1,
+           "parity_vs_reference_golden": {
+               "lattice_inliers": sc.inliers.tolist() == g["a_lattice"]["inliers"],
+               "register_index": bool(res and res.hypothesis_index == g["a_register"]["index"]),
+               "register_stats": {k: getattr(st, k) for k in ("sampled", "prerejected", "degenerate", "evaluated",
+                                                              "qualified")} == g["a_register"]["stats"]},
+           "timing": "wall clock of lk_score_candidates (candidates H2D, scoring, per-candidate results D2H) and of "
+                     "lk_register_global from pageable numpy arrays, best of 5"}
+    if not args.no_cpu_baseline:
+        RF = _ref_module()
+        if RF is not None:
+            sys.path.insert(0, os.path.join(ROOT, "oracle"))
+            import oracle as O
+            op = O.params()
+            sample = list(range(0, rt.shape[0], 97))
+
+            def one(k):
+                return RF.evaluate_hypothesis(rt[k, :9].reshape(3, 3), rt[k, 9:], pair.source.positions,
+                                              pair.source.normals, pair.target.positions, pair.target.normals,
+                                              0.075, op)
+            t0 = time.perf_counter()
+            _pool_map(one, sample)
+            cpu_s = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            RF.register_global(pair.source.positions, pair.source.normals, pair.target.positions,
+                               pair.target.normals, O.params(hypothesis_count=10_000, seed=1,
+                                                             threads=os.cpu_count() or 0))
+            cpu_reg = time.perf_counter() - t0
+            out["cpu_baseline"] = {"kind": "reference", "cores": os.cpu_count(),
+                                   "sample": f"oracle/_ref evaluate_hypothesis on {len(sample)} of the lattice "
+                                             "candidates (one per host thread), and its register_global",
+                                   "lattice_evals_per_s": len(sample) * pair.source.size() / cpu_s,
+                                   "register_ms": 1e3 * cpu_reg}
+    return out
+
+
 def bench_verification(args):
     """Config E: loop verification of synth_registration_pair
     seeds 1..K with their truths as measurements: edge_info(Q, P, I, truth,
@@ -404,6 +517,25 @@ def bench_verification(args):
 
 
 # ------------------------------------------------------------------ GPU
+def count_kernel_launches(step, torch):
+    """Kernels of this library launched by one (untimed) step, counted from a
+    CUPTI trace (torch.profiler); library kernels live in namespace lkk."""
+    try:
+        from torch.profiler import ProfilerActivity, profile
+        torch.cuda.synchronize()
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            step()
+            torch.cuda.synchronize()
+        names = [e.name for e in prof.events() if "lkk::" in e.name]
+        per = {}
+        for n in names:
+            k = n.split("(")[0].split("::")[-1]
+            per[k] = per.get(k, 0) + 1
+        return len(names), per
+    except Exception as e:  # profiler unavailable: report it, do not guess
+        return None, {"error": str(e)[:200]}
+
+
 def run_b200(args):
     import numpy as np
     import torch
@@ -492,6 +624,7 @@ def run_b200(args):
     clock_info = clocks.stop() if rank == 0 else None
     ctx.set_profiling(False)
     step_ms = [a.elapsed_time(b) for a, b in ev]
+    launches_per_step, launch_kinds = count_kernel_launches(step, torch)
     total_ms = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(total_ms, op=dist.ReduceOp.MAX)
@@ -538,6 +671,32 @@ def run_b200(args):
         dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
     e2e_s = float(e2e_s.item())
 
+    # the same leg from pageable host arrays, as the drop-in register_global
+    # receives them (std::vector / numpy; registration.hpp:121-124)
+    src_p = lk.PointCloud(np.array(pair.source.positions), np.array(pair.source.normals))
+    tgt_p = lk.PointCloud(np.array(pair.target.positions), np.array(pair.target.normals))
+    pg_times = []
+    for k in range(e2e_steps + 1):
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        c3 = lk.prepare_registration(src_p, tgt_p, params)
+        c3.set_stream(stream.cuda_stream)
+        xbuf.zero_()
+        lk.run_hypotheses_range(c3, params, begin, end, slot_ptr)
+        if world > 1:
+            dist.all_reduce(xbuf)
+        lk.merge_records(lk.records_from_bytes(xbuf.cpu().numpy()), c3.n_source)
+        t1 = time.perf_counter()
+        if k > 0:
+            pg_times.append(t1 - t0)
+        c3.close()
+    pg_s = torch.tensor([statistics.mean(pg_times)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(pg_s, op=dist.ReduceOp.MAX)
+    pg_s = float(pg_s.item())
+
     if rank == 0:
         hbm_peak, peak_kind = peaks()
         line = {
@@ -554,8 +713,13 @@ def run_b200(args):
                     "d2h_bytes_per_step": int(d2h), "ms_per_registration": e2e_s * 1e3,
                     "note": "prepare_registration on the device (H2D of the raw pinned clouds, voxel "
                             "downsample, FPFH, feature match, EvalGrid) + hypotheses + exchange + merge"},
+            "e2e_pageable": {"value": w_step / pg_s, "unit": UNIT, "ms_per_registration": pg_s * 1e3,
+                             "h2d_bytes_per_step": int(h2d),
+                             "note": "the e2e leg from pageable numpy arrays (what a drop-in register_global "
+                                     "caller passes), H2D staged by the driver"},
             "paper_ms_per_registration": PAPER_MS_PER_REGISTRATION,
-            "gpu_launches": KERNELS_PER_STEP * args.steps,
+            "gpu_launches": launches_per_step * args.steps if launches_per_step is not None else None,
+            "gpu_launches_per_step": launch_kinds,
             "clocks": clock_info,
         }
         # roofline of the scoring kernel (every candidate x point evaluation
@@ -565,16 +729,18 @@ def run_b200(args):
         score_ms = sum(ph[k] for k in score_kernels) / max(runs, 1)
         shape = None
         if world == 1 and not args.no_cpu_baseline:
-            cpu = cpu_oracle_registration(pair, H, args.seed)
+            cpu = cpu_reference_registration(pair, H, args.seed)
             shape = work_shape(cpu["stats"])
             line["cpu_baseline"] = {
                 "value": cpu["stats"]["w_ref"] / cpu["run_s"], "unit": UNIT, "cores": os.cpu_count(),
-                "kind": "port",
-                "sample": f"{cpu['reps']} full B1 registration(s) on the oracle (prepare + {H:,} hypotheses); "
+                "kind": cpu["kind"],
+                "sample": f"{cpu['reps']} full B1 registration(s) on "
+                          + ("the reference's own sources (oracle/_ref)" if cpu["kind"] == "reference"
+                             else "the oracle") + f" (prepare + {H:,} hypotheses); "
                           f"best {1e3 * (cpu['prepare_s'] + cpu['run_s']):.1f} ms/registration, "
-                          f"hypothesis stage {1e3 * cpu['run_s']:.1f} ms",
+                          f"hypothesis stage {1e3 * cpu['run_s']:.1f} ms; W_ref from the oracle's counters",
                 "ms_per_registration": 1e3 * (cpu["prepare_s"] + cpu["run_s"]),
-                "parity": {"oracle_index": cpu["result"].hypothesis_index,
+                "parity": {"reference_index": cpu["result"].hypothesis_index,
                            "b200_index": merged.hypothesis_index if merged else -1,
                            "oracle_w_ref": cpu["stats"]["w_ref"], "b200_w_ref": w_step},
             }
@@ -583,20 +749,31 @@ def run_b200(args):
         evals_per_launch = mstats.evals_executed / max(world, 1)
         if shape["bytes_per_eval"] and score_ms > 0:
             achieved = evals_per_launch * shape["bytes_per_eval"] / (score_ms / 1e3) / 1e9
+            flops = evals_per_launch * shape["flop_per_eval"] / (score_ms / 1e3) / 1e12
             traffic = ncu_traffic(score_kernels)
-            line["roofline"] = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                                "frac": achieved / hbm_peak, "traffic": traffic,
-                                "kernel": "+".join(score_kernels),
-                                "peak_kind": peak_kind, "evals_per_launch": evals_per_launch,
-                                "kernel_ms": score_ms, "work_shape": shape,
-                                "note": "achieved = evals executed per step x algorithmic bytes/eval "
-                                        "(1+72o+12k+12h, SURVEY.md 8d) / event time of the scoring kernel; "
-                                        "traffic = its DRAM bytes per launch from the committed ncu capture "
-                                        "(profiles/ncu_traffic.json). The working set is L2-resident: the "
-                                        "binding limit is L2 gather latency (see profiles/ and DESIGN.md)"}
+            oc = onchip_peaks()
+            if oc:
+                peak, unit, kind = oc["l2_random_gbs"], "GB/s", "measured (tools/peaks.cu -> profiles/peaks.json)"
+            else:
+                peak, unit, kind = hbm_peak, "GB/s", peak_kind + " HBM (profiles/peaks.json absent)"
+            line["roofline"] = {"bound": "l2_gather" if oc else "hbm", "achieved": achieved, "peak": peak,
+                                "unit": unit, "frac": achieved / peak, "traffic": traffic,
+                                "kernel": "+".join(score_kernels), "peak_kind": kind,
+                                "evals_per_launch": evals_per_launch, "kernel_ms": score_ms, "work_shape": shape,
+                                "fp32": {"achieved_tflops": flops,
+                                         "peak_tflops": oc["fp32_tflops"] if oc else None,
+                                         "frac": flops / oc["fp32_tflops"] if oc else None},
+                                "hbm": {"dram_gbs": traffic / (score_ms / 1e3) / 1e9 if traffic else None,
+                                        "peak_gbs": hbm_peak,
+                                        "frac": traffic / (score_ms / 1e3) / 1e9 / hbm_peak if traffic else None},
+                                "note": "achieved = evals executed per step x algorithmic on-chip bytes/eval "
+                                        "(1+72o+12k+12h, SURVEY.md 8d) / event time of the scoring kernel on its "
+                                        "launch stream; peak = the measured L2 random 32-B sector gather rate "
+                                        "(the working set is L2-resident: DRAM traffic per launch is `traffic`, "
+                                        "from the committed ncu capture profiles/ncu_traffic.json)"}
         if world == 1 and not args.no_extras:
-            line["extras"] = {"icp_D": bench_icp(args), "verification_E": bench_verification(args),
-                              "explicit_B2": bench_b2(args)}
+            line["extras"] = {"config_A": bench_config_a(args), "icp_D": bench_icp(args),
+                              "verification_E": bench_verification(args), "explicit_B2": bench_b2(args)}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

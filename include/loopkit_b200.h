@@ -126,9 +126,11 @@ const char* lk_last_error(void);
 int lk_device_count(void);
 
 /* ---- RegistrationContext --------------------------------------------------
- * prepare_registration (registration.hpp:105-107, registration.cpp:223-251):
- * downsample + FPFH (host, this tier), feature pre-match and EvalGrid
- * (device). Throws-equivalents: LK_TOO_FEW_POINTS, LK_MISSING_DATA. */
+ * prepare_registration (registration.hpp:105-107, registration.cpp:223-251),
+ * all on the device: voxel downsample, estimate_normals for clouds given
+ * without normals, FPFH, the feature pre-match (the binary's float matcher,
+ * grid.cpp:176-213) and the EvalGrid. Throws-equivalents: LK_TOO_FEW_POINTS,
+ * LK_MISSING_DATA, LK_MISSING_NORMALS. */
 lk_status lk_reg_prepare(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_params* params, lk_reg_ctx** out);
 /* A RegistrationContext from already-prepared parts (downsampled clouds with
  * normals + the feature match cache), as when the reference's caller fills
@@ -145,9 +147,8 @@ lk_status lk_reg_ctx_sizes(const lk_reg_ctx* ctx, int64_t* n_source, int64_t* n_
  * the three kernels (ms3) and the number of runs (synchronises the events). */
 lk_status lk_reg_ctx_set_profiling(lk_reg_ctx* ctx, int32_t enable);
 lk_status lk_reg_ctx_kernel_times(lk_reg_ctx* ctx, double* ms3, int64_t* runs, int32_t reset);
-/* The same events, per scoring phase: ms[0..5] = k_hyp_sample, k_kabsch,
- * k_prep_fast(+_fine), k_score_split, k_score_resolve, and the tail
- * (k_score overflow + k_score_exits + k_score_finalists). */
+/* The same events, per phase: ms[0..5] = k_hyp_sample, k_kabsch, then the
+ * scorer (k_score_units + k_score_cta) in ms[2] with ms[3..5] = 0. */
 lk_status lk_reg_ctx_phase_times(lk_reg_ctx* ctx, double* ms, int32_t n_phases, int64_t* runs, int32_t reset);
 /* copy the prepared context back to the host (any pointer may be NULL) */
 lk_status lk_reg_ctx_download(const lk_reg_ctx* ctx, double* src_xyz, double* src_n, double* tgt_xyz, double* tgt_n,
@@ -295,7 +296,8 @@ typedef struct lk_icp_result {
 lk_status lk_icp_point_to_plane(const lk_cloud* source, const lk_cloud* target, const double* T0,
                                 const lk_icp_params* params, lk_icp_result* result, double* history);
 
-/* host-side helpers of prepare (this tier) */
+/* the pieces of prepare_registration as separate device calls */
+/* voxel_downsample (preprocess.hpp / preprocess.cpp:14-59) */
 lk_status lk_voxel_downsample(const lk_cloud* cloud, double leaf, double* out_xyz, double* out_n, int64_t* out_count);
 /* estimate_normals (preprocess.hpp / preprocess.cpp:61-96): out_normals n x 3,
  * oriented toward viewpoint (3 doubles; NULL = origin), zero where fewer than

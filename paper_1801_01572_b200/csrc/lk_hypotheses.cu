@@ -5,21 +5,18 @@
 //                   with warp-aggregated atomics (Algorithm 1 "stream compact").
 //   k_kabsch        FP64 Kabsch + restated Jacobi SVD per survivor
 //                   (proj/src/geometry.cpp:62-91); degenerate ones counted.
-//   k_score_split   scoring of (candidate, 32-point chunk) work items spread over
-//                   every warp of the GPU: transform, exact NN within d_max over
-//                   the cell block, normal gate (registration.cpp:165-210). Each
-//                   item leaves its inlier / miss ballots and the inliers' d2.
-//   k_score_exits   warp per candidate: exact miss-budget decision and the
-//                   reference's visit count from the miss ballots; inliers and a
-//                   tree sum of d2 with a rigorous order bound decide qualification
-//                   (the sequential chain only when the bound straddles max_fitness).
-//   k_score_finalists 32 CTAs: global max inliers / min fitness, the finalists
-//                   whose bounds overlap (spread over the CTAs), their exact
-//                   sequential sums in point order; the strict total order
-//                   (registration.cpp:272-276) picks the winner and the last CTA
-//                   writes the rank record.
-//   k_score         warp per candidate streaming its points in order (explicit
-//                   candidate lists, and candidates beyond the split capacity).
+//   k_score_cta     persistent CTA per candidate (the default scorer): rounds of
+//                   2,048 source points -- FP32 fine-cell lookups settle the
+//                   certain misses, a shared-memory queue sends the rest to the
+//                   exact FP64 resolution (guard bands), ballots and
+//                   the reference's miss budget in point order; order-bounded
+//                   sums with the sequential chain on demand; the last CTA
+//                   writes the rank record (registration.cpp:155-219, 253-332).
+//   k_score_units   the same work split into (candidate, round) units when a
+//                   rank has fewer candidates than CTAs (strong scaling).
+//   k_score_list / k_score_list_ring / k_score
+//                   explicit candidate lists (EvalGrid with fine lists, dense
+//                   targets through the ring grid, SearchGrid semantics).
 //
 // Parity: disqualification by the miss budget depends only on the total miss
 // count (misses only grow), so evaluating every point and deciding afterwards
@@ -526,7 +523,7 @@ __device__ __forceinline__ void load_rt(const double* __restrict__ crt, double* 
 }
 
 // Warp per candidate, points streamed in order (explicit candidate lists and
-// the overflow beyond the split capacity).
+// SearchGrid targets: evaluate_hypothesis semantics).
 __global__ void __launch_bounds__(kScoreThreads) k_score(SourceView src, GridView g, ScoreParams sp,
                                                          const double* __restrict__ cand_rt,
                                                          const FastRT* __restrict__ cand_fast,
@@ -589,21 +586,6 @@ __global__ void __launch_bounds__(kScoreThreads) k_score(SourceView src, GridVie
     }
     const bool last = publish_cta(wt, ctr, block_best, best_offset + blockIdx.x, rec != nullptr);
     if (last) write_record(block_best, best_offset + gridDim.x, cand_rt, n_cand, sampled, ctr, rec);
-}
-
-__global__ void k_prep_fast_fine(const double* __restrict__ cand_rt, const Counters* __restrict__ ctr, GridView g,
-                                 ScoreParams sp, FastRT* __restrict__ out, int64_t cap = INT64_MAX) {
-    const int64_t n_all = static_cast<int64_t>(ctr->n_candidates);
-    const int64_t n = n_all < cap ? n_all : cap;
-    for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
-         k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        double R[9], t[3];
-#pragma unroll
-        for (int q = 0; q < 9; ++q) R[q] = cand_rt[12 * k + q];
-#pragma unroll
-        for (int q = 0; q < 3; ++q) t[q] = cand_rt[12 * k + 9 + q];
-        out[k] = make_fast_fine(R, t, g, sp);
-    }
 }
 
 // Exact resolution of one query over its fine list: FP32 top-3 with the guard
@@ -711,561 +693,7 @@ __device__ __forceinline__ bool resolve_fine(const GridView& g, const double* R,
     return true;
 }
 
-// The resolve queue is split into kQueueParts partitions, each with its own
-// counter on its own 128-byte line, so the warps' reservations spread over L2
-// slices instead of serialising on one address.
-constexpr int kQueueParts = 64;
-constexpr int kQueueStride = 16;  // u64 per counter line
-
-// Pass A: (candidate, chunk) items, chunk-major so neighbouring warps share
-// the source chunk in L1. Each lane locates its point's fine cell in FP32:
-// certain misses are settled here; points with a non-empty fine list (or a
-// coordinate near a fine-cell face) go to the dense queue for pass B, so no
-// lane idles through another lane's scan. No early exit: every point of a
-// split candidate is evaluated; k_score_exits decides from the ballots.
-__global__ void __launch_bounds__(kScoreThreads, 4) k_score_split(SourceView src, const __grid_constant__ GridView g,
-    const __grid_constant__ ScoreParams sp,
-                                                               const double* __restrict__ cand_rt,
-                                                               const FastRT* __restrict__ cand_fine, int64_t cap,
-                                                               int32_t n_chunks, int64_t ns_pad,
-                                                               uint32_t* __restrict__ inl_masks,
-                                                               uint32_t* __restrict__ miss_masks,
-                                                               double* __restrict__ addends, int4* __restrict__ queue,
-                                                               int64_t part_cap,
-                                                               unsigned long long* __restrict__ part_count,
-                                                               const Counters* __restrict__ ctr) {
-    const int lane = threadIdx.x & 31;
-    const int64_t n_all = static_cast<int64_t>(ctr->n_candidates);
-    const int64_t n_cand = n_all < cap ? n_all : cap;
-    if (n_cand == 0) return;
-    const int64_t total = n_cand * n_chunks;
-    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
-    const int64_t ns = src.n;
-    const int part = blockIdx.x % kQueueParts;
-    unsigned long long* counter = part_count + part * kQueueStride;
-    int4* pq = queue + part * part_cap;
-    int64_t w = blockIdx.x * static_cast<int64_t>(blockDim.x >> 5) + (threadIdx.x >> 5);
-    // (chunk, cand) of w, advanced without dividing in the loop
-    int64_t chunk = w / n_cand, cand = w - (w / n_cand) * n_cand;
-    const int64_t dq = nwarps / n_cand, dr = nwarps - dq * n_cand;
-    for (; w < total; w += nwarps) {
-        const FastRT F = load_fast(cand_fine + cand);
-        const int64_t i = chunk * 32 + lane;
-        const bool valid = i < ns;
-        int state = 0;  // 0 certain miss, 1 exact fallback, 2 fine-list scan
-        int2 bi = make_int2(0, 0);
-        if (valid) {
-            if (F.ok == 0.0f) {
-                state = 1;
-            } else {
-                const float4 P = __ldg(src.pos32 + i);
-                const float qx = fmaf(F.r[0], P.x, fmaf(F.r[1], P.y, fmaf(F.r[2], P.z, F.t[0])));
-                const float qy = fmaf(F.r[3], P.x, fmaf(F.r[4], P.y, fmaf(F.r[5], P.z, F.t[1])));
-                const float qz = fmaf(F.r[6], P.x, fmaf(F.r[7], P.y, fmaf(F.r[8], P.z, F.t[2])));
-                const float eps = F.eps;
-                if (!(qx < -eps || qy < -eps || qz < -eps || qx >= g.fnx + eps || qy >= g.fny + eps ||
-                      qz >= g.fnz + eps)) {
-                    const float fx = floorf(qx), fy = floorf(qy), fz = floorf(qz);
-                    const float rx = qx - fx, ry = qy - fy, rz = qz - fz;
-                    if (rx < eps || rx > 1.0f - eps || ry < eps || ry > 1.0f - eps || rz < eps || rz > 1.0f - eps) {
-                        state = 1;
-                    } else {
-                        const int ix = static_cast<int>(fx), iy = static_cast<int>(fy), iz = static_cast<int>(fz);
-                        if (ix >= 0 && iy >= 0 && iz >= 0 && ix < g.fnx && iy < g.fny && iz < g.fnz) {
-                            bi = __ldg(g.fine_info + (static_cast<int64_t>(ix) * g.fny + iy) * g.fnz + iz);
-                            if (bi.y > 0) state = 2;
-                        }
-                    }
-                }
-            }
-        }
-        const bool need = state != 0;
-        const unsigned long long slot = warp_atomic_add(counter, need);
-        bool inl = false, inline_done = false;
-        double addend = 0.0;
-        if (need) {
-            if (static_cast<int64_t>(slot) < part_cap) {
-                pq[slot] = make_int4(static_cast<int32_t>(cand), static_cast<int32_t>(i), bi.x,
-                                     state == 1 ? -1 : bi.y);
-            } else {  // partition full: evaluate here (exact, slow, never on the bench inputs)
-                inl = eval_point_slow(g, cand_rt + 12 * cand, src, i, sp, &addend);
-                inline_done = true;
-            }
-        }
-        const unsigned im = __ballot_sync(kFull, inl);
-        const unsigned mm = __ballot_sync(kFull, (valid && state == 0) || (inline_done && !inl));
-        if (lane == 0) {
-            inl_masks[cand * n_chunks + chunk] = im;
-            miss_masks[cand * n_chunks + chunk] = mm;
-        }
-        if (inl) addends[cand * ns_pad + i] = addend;
-        cand += dr;
-        chunk += dq;
-        if (cand >= n_cand) {
-            cand -= n_cand;
-            chunk += 1;
-        }
-    }
-}
-
-// Pass B: thread per queued (candidate, point) over the concatenated
-// partitions: the fine-list scan and the exact decisions; results are OR-ed
-// into the chunk ballots.
-__global__ void __launch_bounds__(kScoreThreads, 4) k_score_resolve(SourceView src, const __grid_constant__ GridView g,
-    const __grid_constant__ ScoreParams sp,
-                                                                 const double* __restrict__ cand_rt,
-                                                                 const FastRT* __restrict__ cand_fine,
-                                                                 int32_t n_chunks, int64_t ns_pad,
-                                                                 const int4* __restrict__ queue, int64_t part_cap,
-                                                                 const unsigned long long* __restrict__ part_count,
-                                                                 uint32_t* __restrict__ inl_masks,
-                                                                 uint32_t* __restrict__ miss_masks,
-                                                                 double* __restrict__ addends) {
-    __shared__ int64_t s_start[kQueueParts + 1];
-    if (threadIdx.x < 32) {
-        // inclusive scan of the clamped partition counts, two per lane
-        const int lane = threadIdx.x;
-        int64_t a = static_cast<int64_t>(part_count[(2 * lane) * kQueueStride]);
-        int64_t b = static_cast<int64_t>(part_count[(2 * lane + 1) * kQueueStride]);
-        a = a < part_cap ? a : part_cap;
-        b = b < part_cap ? b : part_cap;
-        int64_t v = a + b;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int64_t u = __shfl_up_sync(kFull, v, o);
-            if (lane >= o) v += u;
-        }
-        s_start[2 * lane + 1] = v - b;
-        s_start[2 * lane + 2] = v;
-        if (lane == 0) s_start[0] = 0;
-    }
-    __syncthreads();
-    const int64_t n = s_start[kQueueParts];
-    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
-         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        int lo = 0, hi = kQueueParts;  // s_start[lo] <= e < s_start[hi]
-        while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (s_start[mid] <= e) lo = mid;
-            else hi = mid;
-        }
-        const int4 q = __ldg(queue + lo * part_cap + (e - s_start[lo]));
-        const int64_t cand = q.x, i = q.y;
-        double addend = 0.0;
-        bool inl;
-        if (q.w < 0) {
-            inl = eval_point_slow(g, cand_rt + 12 * cand, src, i, sp, &addend);
-        } else {
-            double R[9], t[3];
-            load_rt(cand_rt + 12 * cand, R, t);
-            const V3 p = src.pos4 ? ld4(src.pos4, i) : ld3(src.pos, i);
-            const FastRT F = load_fast(cand_fine + cand);
-            const float4 P = __ldg(src.pos32 + i);
-            const float qx = fmaf(F.r[0], P.x, fmaf(F.r[1], P.y, fmaf(F.r[2], P.z, F.t[0])));
-            const float qy = fmaf(F.r[3], P.x, fmaf(F.r[4], P.y, fmaf(F.r[5], P.z, F.t[1])));
-            const float qz = fmaf(F.r[6], P.x, fmaf(F.r[7], P.y, fmaf(F.r[8], P.z, F.t[2])));
-            inl = resolve_fine(g, R, t, nullptr, F, src, i, p, make_float4(0, 0, 0, 0), qx, qy, qz, q.z, q.w, sp,
-                               addend);
-        }
-        const int64_t word = cand * n_chunks + (i >> 5);
-        const uint32_t bit = 1u << (i & 31);
-        if (inl) {
-            atomicOr(inl_masks + word, bit);
-            addends[cand * ns_pad + i] = addend;
-        } else {
-            atomicOr(miss_masks + word, bit);
-        }
-    }
-}
-
-
-// Per fully scored split candidate, what the final selection needs.
-struct CandInfo {
-    int64_t inliers;  // -1: exited or not qualified
-    double fitness;   // exact when exact != 0, else the tree-sum approximation
-    int64_t exact;
-};
-
-// Sequential FP64 sum of the inliers' d2 in point order (registration.cpp:206),
-// warp-cooperative: each round the lanes compact 8 chunks' inlier addends in
-// point order into `buf` (256 doubles of shared memory), then lane 0 adds them
-// in that order -- a pure dependent-add chain fed by shared-memory loads.
-__device__ double exact_chain(const uint32_t* __restrict__ im, const double* __restrict__ ad, int32_t n_chunks,
-                              double* buf) {
-    const int lane = threadIdx.x & 31;
-    const unsigned below = (1u << lane) - 1u;
-    double sum = 0.0;
-    for (int32_t c0 = 0; c0 < n_chunks; c0 += 8) {
-        int base = 0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const uint32_t m = (c0 + j < n_chunks) ? __ldg(im + c0 + j) : 0u;
-            if ((m >> lane) & 1u) buf[base + __popc(m & below)] = __ldg(ad + static_cast<int64_t>(c0 + j) * 32 + lane);
-            base += __popc(m);
-        }
-        __syncwarp();
-        if (lane == 0) {
-            int k = 0;
-            for (; k + 4 <= base; k += 4) {
-                const double x0 = buf[k], x1 = buf[k + 1], x2 = buf[k + 2], x3 = buf[k + 3];
-                sum += x0;
-                sum += x1;
-                sum += x2;
-                sum += x3;
-            }
-            for (; k < base; ++k) sum += buf[k];
-        }
-        __syncwarp();
-    }
-    return __shfl_sync(kFull, sum, 0);
-}
-
-// Relative bound between any two summation orders of n non-negative terms
-// (each within (n - 1) u of the exact sum), plus the final division.
 __device__ __forceinline__ double order_bound(int64_t n) { return 2.0 * static_cast<double>(n + 1) * 1.1102230246251565e-16 + 4.5e-16; }
-
-// Warp per split candidate: the exact miss-budget decision and the
-// reference's visit count from the ordered miss ballots; for fully scored
-// candidates the inlier count, a tree-reduced sum with a rigorous bound, and
-// the qualification (the sequential chain only when the bound straddles
-// max_fitness). Publishes per-CTA (max inliers, min fitness) for the
-// finalist pass.
-__global__ void __launch_bounds__(kScoreThreads) k_score_exits(int64_t ns, ScoreParams sp, int64_t cap,
-                                                               int32_t n_chunks, int64_t ns_pad,
-                                                               const uint32_t* __restrict__ miss_masks,
-                                                               const uint32_t* __restrict__ inl_masks,
-                                                               const double* __restrict__ addends,
-                                                               CandInfo* __restrict__ info,
-                                                               Counters* __restrict__ ctr,
-                                                               BestRec* __restrict__ block_best, int best_offset) {
-    constexpr int kGroups = 8;  // 8 x 32 miss ballots (8192 points) in flight per pass
-    constexpr int kBatch = 8;   // addend loads in flight per lane
-    __shared__ double s_chain[kScoreWarps][256];
-    const int lane = threadIdx.x & 31;
-    const int64_t n_all = static_cast<int64_t>(ctr->n_candidates);
-    const int64_t n_cand = n_all < cap ? n_all : cap;
-    const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
-    WarpTally wt;
-    for (int64_t cand = blockIdx.x * static_cast<int64_t>(blockDim.x >> 5) + (threadIdx.x >> 5); cand < n_cand;
-         cand += nwarps) {
-        const uint32_t* mm = miss_masks + cand * n_chunks;
-        // exact miss-budget decision and the reference's visit count: the
-        // ballots of 256 chunks are loaded at once, then scanned in order
-        int64_t misses = 0, visited = ns;
-        bool exited = false;
-        for (int32_t s0 = 0; s0 < n_chunks && !exited; s0 += 32 * kGroups) {
-            uint32_t mreg[kGroups];
-#pragma unroll
-            for (int g = 0; g < kGroups; ++g) {
-                const int32_t c = s0 + g * 32 + lane;
-                mreg[g] = c < n_chunks ? __ldg(mm + c) : 0u;
-            }
-#pragma unroll
-            for (int g = 0; g < kGroups; ++g) {
-                if (exited) continue;  // warp-uniform
-                const int cnt = __popc(mreg[g]);
-                int incl = cnt;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    int y = __shfl_up_sync(kFull, incl, o);
-                    if (lane >= o) incl += y;
-                }
-                const unsigned over = __ballot_sync(kFull, misses + incl > sp.miss_budget);
-                if (over) {
-                    const int L = __ffs(over) - 1;
-                    const int64_t before = misses + __shfl_sync(kFull, incl - cnt, L);
-                    unsigned m = __shfl_sync(kFull, mreg[g], L);
-                    const int need = static_cast<int>(sp.miss_budget - before);
-                    for (int q = 0; q < need; ++q) m &= m - 1;
-                    visited = static_cast<int64_t>(s0 + g * 32 + L) * 32 + (__ffs(m) - 1) + 1;
-                    exited = true;
-                }
-                misses += __shfl_sync(kFull, incl, 31);
-            }
-        }
-        wt.w_ref += static_cast<unsigned long long>(visited);
-        wt.executed += static_cast<unsigned long long>(ns);
-        CandInfo ci{-1, 0.0, 0};
-        if (!exited) {
-            // inliers and a lane-parallel sum of the inliers' d2 (any order;
-            // the zero fill of unset lanes adds exactly nothing)
-            const uint32_t* im = inl_masks + cand * n_chunks;
-            const double* ad = addends + cand * ns_pad;
-            unsigned pop = 0;
-            double part = 0.0;
-            for (int32_t s0 = 0; s0 < n_chunks; s0 += 32) {
-                const uint32_t mine = s0 + lane < n_chunks ? __ldg(im + s0 + lane) : 0u;
-                pop += __popc(mine);
-                const int lim = n_chunks - s0 < 32 ? n_chunks - s0 : 32;
-                for (int j0 = 0; j0 < lim; j0 += kBatch) {
-                    double v[kBatch];
-#pragma unroll
-                    for (int j = 0; j < kBatch; ++j) {
-                        const uint32_t m = __shfl_sync(kFull, mine, j0 + j);
-                        v[j] = (j0 + j < lim && ((m >> lane) & 1u))
-                                   ? __ldg(ad + static_cast<int64_t>(s0 + j0 + j) * 32 + lane)
-                                   : 0.0;
-                    }
-#pragma unroll
-                    for (int j = 0; j < kBatch; ++j) part += v[j];
-                }
-            }
-            const int64_t inl = static_cast<int64_t>(__reduce_add_sync(kFull, pop));
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(kFull, part, o);
-            const double ratio = static_cast<double>(inl) / static_cast<double>(ns);
-            if (!(ratio < sp.min_ratio)) {
-                double fit = inl > 0 ? part / static_cast<double>(inl) : 0.0;
-                int64_t exact = inl == 0 ? 1 : 0;
-                const double eb = order_bound(inl) * fit;
-                bool qualifies = fit + eb <= sp.max_fitness;
-                if (!exact && !qualifies && fit - eb <= sp.max_fitness) {
-                    // the bound straddles max_fitness: the reference's own sum decides
-                    fit = exact_chain(im, ad, n_chunks, s_chain[threadIdx.x >> 5]) / static_cast<double>(inl);
-                    exact = 1;
-                    qualifies = !(fit > sp.max_fitness);
-                }
-                if (qualifies) {
-                    ci = CandInfo{inl, fit, exact};
-                    wt.qualified += 1;
-                    BestRec c{1, inl, fit, cand, cand};
-                    if (better(c, wt.best)) wt.best = c;
-                }
-            }
-        }
-        if (lane == 0) info[cand] = ci;
-    }
-    publish_cta(wt, ctr, block_best, best_offset + blockIdx.x, false);
-}
-
-// ---- finalists -------------------------------------------------------------
-constexpr int kFinalCtas = 32;
-constexpr int kChainChunks = 128;  // 4096 addends per shared-memory window
-
-// Block-wide exclusive scan of one int per thread (kScoreThreads threads).
-__device__ __forceinline__ int block_exclusive_scan(int v, int* s_warp, int* total) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int incl = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(kFull, incl, o);
-        if (lane >= o) incl += y;
-    }
-    if (lane == 31) s_warp[warp] = incl;
-    __syncthreads();
-    int base = 0, all = 0;
-#pragma unroll
-    for (int w = 0; w < kScoreWarps; ++w) {
-        const int t = s_warp[w];
-        base += w < warp ? t : 0;
-        all += t;
-    }
-    __syncthreads();
-    *total = all;
-    return base + incl - v;
-}
-
-// Sequential FP64 sum of one candidate's inliers' d2 in point order
-// (registration.cpp:206) by a whole CTA: the CTA compacts a window of 128
-// chunks' addends into shared memory in point order (one scan over the
-// ballots, coalesced gathers by all warps), then thread 0 runs the dependent
-// add chain from shared memory. Result valid in thread 0.
-__device__ double cta_exact_chain(const uint32_t* __restrict__ im, const double* __restrict__ ad, int32_t n_chunks,
-                                  double* buf, uint32_t* s_mask, int* s_off, int* s_warp) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const unsigned below = (1u << lane) - 1u;
-    double sum = 0.0;
-    for (int32_t c0 = 0; c0 < n_chunks; c0 += kChainChunks) {
-        const int nc = n_chunks - c0 < kChainChunks ? n_chunks - c0 : kChainChunks;
-        const uint32_t m = threadIdx.x < nc ? __ldg(im + c0 + threadIdx.x) : 0u;
-        int total = 0;
-        const int off = block_exclusive_scan(__popc(m), s_warp, &total);
-        if (threadIdx.x < kChainChunks) {
-            s_mask[threadIdx.x] = m;
-            s_off[threadIdx.x] = off;
-        }
-        __syncthreads();
-#pragma unroll 4
-        for (int q = warp; q < nc; q += kScoreWarps) {
-            const uint32_t mq = s_mask[q];
-            if ((mq >> lane) & 1u) buf[s_off[q] + __popc(mq & below)] = __ldg(ad + static_cast<int64_t>(c0 + q) * 32 + lane);
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            int k = 0;
-            for (; k + 4 <= total; k += 4) {
-                const double x0 = buf[k], x1 = buf[k + 1], x2 = buf[k + 2], x3 = buf[k + 3];
-                sum += x0;
-                sum += x1;
-                sum += x2;
-                sum += x3;
-            }
-            for (; k < total; ++k) sum += buf[k];
-        }
-        __syncthreads();
-    }
-    return sum;
-}
-
-__device__ __forceinline__ bool approx_better(const BestRec& c, const BestRec& g) {
-    return c.valid && (!g.valid || c.inliers > g.inliers || (c.inliers == g.inliers && c.fitness < g.fitness));
-}
-
-// kFinalCtas CTAs. Each one reduces the per-CTA bests to the global (max
-// inliers, min approximate fitness), enumerates the finalists -- qualified
-// candidates with that inlier count whose fitness bound overlaps the
-// minimum's -- in candidate order and takes every kFinalCtas-th; their exact
-// sequential sums decide under (fitness, hypothesis index)
-// (registration.cpp:272-276). The last CTA to finish merges the CTA winners
-// (and the overflow candidates' bests) and writes the rank record.
-__global__ void __launch_bounds__(kScoreThreads) k_score_finalists(int32_t n_chunks, int64_t ns_pad,
-                                                                   const uint32_t* __restrict__ inl_masks,
-                                                                   const double* __restrict__ addends,
-                                                                   const CandInfo* __restrict__ info, int64_t cap,
-                                                                   const double* __restrict__ cand_rt,
-                                                                   const int64_t* __restrict__ cand_index,
-                                                                   BestRec* __restrict__ block_best,
-                                                                   int n_best, int64_t sampled,
-                                                                   Counters* __restrict__ ctr,
-                                                                   RecordDev* __restrict__ rec) {
-    __shared__ double s_buf[kChainChunks * 32];
-    __shared__ uint32_t s_mask[kChainChunks];
-    __shared__ int s_off[kChainChunks];
-    __shared__ int s_warp[kScoreWarps];
-    __shared__ BestRec s_red[kScoreWarps];
-    __shared__ int64_t s_list[kScoreThreads];
-    __shared__ unsigned long long s_ticket;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t n_all = static_cast<int64_t>(ctr->n_candidates);
-    const int64_t n_split = n_all < cap ? n_all : cap;
-    const int64_t prerej = sampled - static_cast<int64_t>(ctr->n_survivors);
-    // 1. global (max inliers, min approximate fitness) over the per-CTA bests
-    BestRec g{0, 0, 0.0, INT64_MAX, -1};
-    for (int b = threadIdx.x; b < n_best; b += blockDim.x) {
-        const BestRec c = block_best[b];
-        if (approx_better(c, g)) g = c;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        BestRec c;
-        c.valid = __shfl_down_sync(kFull, g.valid, o);
-        c.inliers = __shfl_down_sync(kFull, g.inliers, o);
-        c.fitness = __shfl_down_sync(kFull, g.fitness, o);
-        c.index = __shfl_down_sync(kFull, g.index, o);
-        c.slot = __shfl_down_sync(kFull, g.slot, o);
-        if (approx_better(c, g)) g = c;
-    }
-    if (lane == 0) s_red[warp] = g;
-    __syncthreads();
-    g = s_red[0];
-    for (int w = 1; w < kScoreWarps; ++w)
-        if (approx_better(s_red[w], g)) g = s_red[w];
-    __syncthreads();
-    if (!g.valid) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
-            RecordDev r{};
-            r.index = -1;
-            r.sampled = sampled;
-            r.prerejected = prerej;
-            r.degenerate = static_cast<int64_t>(ctr->degenerate);
-            r.evaluated = n_all;
-            r.qualified = static_cast<int64_t>(ctr->qualified);
-            r.w_ref = static_cast<int64_t>(ctr->w_ref);
-            r.evals_executed = static_cast<int64_t>(ctr->evals_executed);
-            *rec = r;
-        }
-        return;
-    }
-    // 2. ordered finalist enumeration; this CTA takes ranks r = blockIdx (mod gridDim)
-    const double lim = g.fitness * (1.0 + 2.0 * order_bound(g.inliers)) + 1e-300;
-    BestRec mine{0, 0, 0.0, INT64_MAX, -1};
-    int64_t rank0 = 0;
-    for (int64_t k0 = 0; k0 < n_split; k0 += kScoreThreads) {
-        const int64_t k = k0 + threadIdx.x;
-        bool fin = false;
-        if (k < n_split) {
-            const CandInfo ci = info[k];
-            fin = ci.inliers == g.inliers && ci.fitness <= lim;
-        }
-        int n_here = 0;
-        const int r = block_exclusive_scan(fin ? 1 : 0, s_warp, &n_here);
-        const int64_t rank = rank0 + r;
-        // compact this CTA's share of the finalists in candidate order
-        int take = 0;
-        const bool my = fin && (rank % gridDim.x) == blockIdx.x;
-        const int pos = block_exclusive_scan(my ? 1 : 0, s_warp, &take);
-        if (my) s_list[pos] = k;
-        __syncthreads();
-        for (int f = 0; f < take; ++f) {
-            const int64_t kk = s_list[f];
-            const CandInfo ci = info[kk];
-            double fit = ci.fitness;
-            if (!ci.exact)
-                fit = cta_exact_chain(inl_masks + kk * n_chunks, addends + kk * ns_pad, n_chunks, s_buf, s_mask, s_off,
-                                      s_warp) /
-                      static_cast<double>(ci.inliers);
-            if (threadIdx.x == 0) {
-                BestRec c{1, ci.inliers, fit, __ldg(cand_index + kk), kk};
-                if (better(c, mine)) mine = c;
-            }
-        }
-        __syncthreads();
-        rank0 += n_here;
-    }
-    // 3. publish; the last CTA merges
-    if (threadIdx.x == 0) {
-        block_best[n_best + blockIdx.x] = mine;
-        __threadfence();
-        s_ticket = atomicAdd(&ctr->fin_done, 1ull);
-    }
-    __syncthreads();
-    if (s_ticket != gridDim.x - 1) return;
-    __threadfence();
-    // the last CTA: CTA winners and the overflow candidates (k_score, exact
-    // already, slot >= cap) in parallel, then a warp / CTA reduction
-    BestRec b{0, 0, 0.0, INT64_MAX, -1};
-    for (int i = threadIdx.x; i < static_cast<int>(gridDim.x) + n_best; i += blockDim.x) {
-        const BestRec* src = i < static_cast<int>(gridDim.x) ? block_best + n_best + i : block_best + (i - gridDim.x);
-        BestRec c;
-        c.valid = __ldcg(&src->valid);
-        c.inliers = __ldcg(&src->inliers);
-        c.fitness = __ldcg(&src->fitness);
-        c.index = __ldcg(&src->index);
-        c.slot = __ldcg(&src->slot);
-        if (i >= static_cast<int>(gridDim.x) && c.slot < cap) continue;
-        if (better(c, b)) b = c;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        BestRec c;
-        c.valid = __shfl_down_sync(kFull, b.valid, o);
-        c.inliers = __shfl_down_sync(kFull, b.inliers, o);
-        c.fitness = __shfl_down_sync(kFull, b.fitness, o);
-        c.index = __shfl_down_sync(kFull, b.index, o);
-        c.slot = __shfl_down_sync(kFull, b.slot, o);
-        if (better(c, b)) b = c;
-    }
-    if (lane == 0) s_red[warp] = b;
-    __syncthreads();
-    if (threadIdx.x != 0) return;
-    for (int w = 1; w < kScoreWarps; ++w)
-        if (better(s_red[w], b)) b = s_red[w];
-    RecordDev r{};
-    r.valid = b.valid;
-    r.inliers = b.valid ? b.inliers : 0;
-    r.fitness = b.valid ? b.fitness : 0.0;
-    r.index = b.valid ? b.index : -1;
-    for (int q = 0; q < 9; ++q) r.R[q] = b.valid ? cand_rt[12 * b.slot + q] : 0.0;
-    for (int q = 0; q < 3; ++q) r.t[q] = b.valid ? cand_rt[12 * b.slot + 9 + q] : 0.0;
-    r.sampled = sampled;
-    r.prerejected = prerej;
-    r.degenerate = static_cast<int64_t>(ctr->degenerate);
-    r.evaluated = n_all;
-    r.qualified = static_cast<int64_t>(ctr->qualified);
-    r.w_ref = static_cast<int64_t>(ctr->w_ref);
-    r.evals_executed = static_cast<int64_t>(ctr->evals_executed);
-    *rec = r;
-}
 
 
 // ---- candidate-CTA scoring ------------------------------------------------
@@ -2275,32 +1703,10 @@ int score_blocks_per_sm() {
     if (!cached) cached = blocks_per_sm(reinterpret_cast<const void*>(k_score));
     return cached;
 }
-int split_blocks_per_sm() {
-    static int cached = 0;
-    if (!cached) cached = blocks_per_sm(reinterpret_cast<const void*>(k_score_split));
-    return cached;
-}
 
 int cand_blocks_per_sm() {
     static int cached = 0;
     if (!cached) cached = blocks_per_sm(reinterpret_cast<const void*>(k_score_cta));
-    return cached;
-}
-
-// LK_SCORE_SPLIT=1 selects the (candidate x chunk) split scorer instead of the
-// candidate-CTA scorer (both exact; kept for comparison).
-bool split_scoring() {
-    static int cached = -1;
-    if (cached < 0) {
-        const char* v = std::getenv("LK_SCORE_SPLIT");
-        cached = (v && v[0] == '1') ? 1 : 0;
-    }
-    return cached == 1;
-}
-
-int resolve_blocks_per_sm() {
-    static int cached = 0;
-    if (!cached) cached = blocks_per_sm(reinterpret_cast<const void*>(k_score_resolve));
     return cached;
 }
 
@@ -2313,14 +1719,7 @@ void RunBuffers::release() {
     pool_free(cand_rt, stream);
     pool_free(counters, stream);
     pool_free(block_best, stream);
-    pool_free(inl_masks, stream);
-    pool_free(miss_masks, stream);
-    pool_free(addends, stream);
-    pool_free(full_list, stream);
     pool_free(cand_fast, stream);
-    pool_free(cand_fine, stream);
-    pool_free(queue, stream);
-    pool_free(queue_counts, stream);
     pool_free(cta_add, stream);
     pool_free(cta_inl, stream);
     pool_free(u_miss, stream);
@@ -2336,12 +1735,7 @@ void RunBuffers::release() {
     cta_inl = nullptr;
     cta_slots = 0;
     cta_ns_pad = 0;
-    queue_counts = nullptr;
-    full_list = nullptr;
     cand_fast = nullptr;
-    cand_fine = nullptr;
-    queue = nullptr;
-    queue_cap = 0;
     fast_capacity = 0;
     surv_index = nullptr;
     surv_ids = nullptr;
@@ -2349,12 +1743,8 @@ void RunBuffers::release() {
     cand_rt = nullptr;
     counters = nullptr;
     block_best = nullptr;
-    inl_masks = miss_masks = nullptr;
-    addends = nullptr;
     capacity = 0;
     n_blocks = 0;
-    split_cap = 0;
-    split_ns_pad = 0;
 }
 
 cudaError_t RunBuffers::ensure(int64_t cap, int32_t score_blocks) {
@@ -2439,52 +1829,11 @@ cudaError_t RunBuffers::ensure_units(int64_t ns, int64_t cap) {
 cudaError_t RunBuffers::ensure_fast(int64_t n) {
     if (n <= fast_capacity) return cudaSuccess;
     pool_free(cand_fast, stream);
-    pool_free(cand_fine, stream);
     cand_fast = nullptr;
-    cand_fine = nullptr;
     fast_capacity = 0;
     cudaError_t e = pool_alloc(&cand_fast, n * sizeof(FastRT), stream);
-    if (e == cudaSuccess) e = pool_alloc(&cand_fine, n * sizeof(FastRT), stream);
     if (e == cudaSuccess) fast_capacity = n;
     return e;
-}
-
-cudaError_t RunBuffers::ensure_split(int64_t ns, int64_t max_candidates) {
-    const int64_t n_chunks = (ns + 31) / 32;
-    const int64_t ns_pad = n_chunks * 32;
-    // addends are the big buffer: keep it under kSplitBytes
-    int64_t cap = kSplitBytes / (ns_pad * static_cast<int64_t>(sizeof(double)));
-    if (cap > max_candidates) cap = max_candidates;
-    if (cap < 1) cap = 1;
-    if (cap <= split_cap && ns_pad == split_ns_pad) return cudaSuccess;
-    pool_free(inl_masks, stream);
-    pool_free(miss_masks, stream);
-    pool_free(addends, stream);
-    pool_free(full_list, stream);
-    pool_free(queue, stream);
-    inl_masks = miss_masks = nullptr;
-    addends = nullptr;
-    full_list = nullptr;
-    queue = nullptr;
-    queue_cap = 0;
-    split_cap = 0;
-    cudaError_t e;
-    if ((e = pool_alloc(&full_list, cap * 3 * sizeof(int64_t), stream)) != cudaSuccess) return e;  // CandInfo
-    if ((e = pool_alloc(&inl_masks, cap * n_chunks * sizeof(uint32_t), stream)) != cudaSuccess) return e;
-    if ((e = pool_alloc(&miss_masks, cap * n_chunks * sizeof(uint32_t), stream)) != cudaSuccess) return e;
-    if ((e = pool_alloc(&addends, cap * ns_pad * sizeof(double), stream)) != cudaSuccess) return e;
-    // resolve queue: a quarter of all (candidate, point) pairs; overflow is
-    // evaluated inline by k_score_split
-    const int64_t qcap = (cap * ns_pad * 3 / 8 > 1024 ? cap * ns_pad * 3 / 8 : 1024) / kQueueParts * kQueueParts;
-    if ((e = pool_alloc(&queue, qcap * sizeof(int4), stream)) != cudaSuccess) return e;
-    if (!queue_counts &&
-        (e = pool_alloc(&queue_counts, kQueueParts * kQueueStride * sizeof(unsigned long long), stream)) !=
-            cudaSuccess)
-        return e;
-    queue_cap = qcap;
-    split_cap = cap;
-    split_ns_pad = ns_pad;
-    return cudaSuccess;
 }
 
 cudaError_t run_hypotheses_range(const SourceView& src, const double* d_tgt_pos, const int32_t* d_cache,
@@ -2492,26 +1841,11 @@ cudaError_t run_hypotheses_range(const SourceView& src, const double* d_tgt_pos,
                                  int64_t end, RunBuffers& rb, void* d_record, cudaStream_t stream, int sm_count,
                                  cudaEvent_t* events) {
     const int64_t count = end - begin;
-    const int split_blocks = sm_count * split_blocks_per_sm();
-    const int exit_blocks = sm_count * 2;
-    const int over_blocks = sm_count;
     const int cand_blocks = sm_count * cand_blocks_per_sm();
-    const int n_best_slots = exit_blocks + over_blocks + kFinalCtas;
-    cudaError_t e = rb.ensure(count > 0 ? count : 1, n_best_slots > 2 * cand_blocks ? n_best_slots : 2 * cand_blocks);
+    cudaError_t e = rb.ensure(count > 0 ? count : 1, 2 * cand_blocks);
     if (e != cudaSuccess) return e;
-    const bool split = split_scoring();
-    if (split) {
-        // split capacity: a few percent of the hypotheses survive pre-rejection in
-        // practice; any excess is scored by the streaming k_score (exact too)
-        const int64_t want_split = count / 64 > 4096 ? count / 64 : 4096;
-        if ((e = rb.ensure_split(src.n, want_split < count ? want_split : (count > 0 ? count : 1))) != cudaSuccess)
-            return e;
-        if ((e = rb.ensure_fast(count > 0 ? count : 1)) != cudaSuccess) return e;
-        if ((e = cudaMemsetAsync(rb.queue_counts, 0, kQueueParts * kQueueStride * sizeof(unsigned long long),
-                                 stream)) != cudaSuccess)
-            return e;
-    } else {
-        if ((e = rb.ensure_cta(src.n, cand_blocks)) != cudaSuccess) return e;
+    if ((e = rb.ensure_cta(src.n, cand_blocks)) != cudaSuccess) return e;
+    {
         // unit scratch: a few percent of the hypotheses survive; at most 2 GiB of addends
         const int64_t ns_pad = (src.n + 31) / 32 * 32;
         int64_t ucap = count / 64 > 4096 ? count / 64 : 4096;
@@ -2519,11 +1853,9 @@ cudaError_t run_hypotheses_range(const SourceView& src, const double* d_tgt_pos,
         if (ucap > byte_cap) ucap = byte_cap > 1 ? byte_cap : 1;
         if ((e = rb.ensure_units(src.n, ucap)) != cudaSuccess) return e;
     }
-    FastRT* cand_fast = static_cast<FastRT*>(rb.cand_fast);
     if ((e = cudaMemsetAsync(rb.counters, 0, sizeof(Counters), stream)) != cudaSuccess) return e;
     const uint32_t ns = static_cast<uint32_t>(src.n);
     const uint32_t thresh = static_cast<uint32_t>(0x100000000ull % ns);
-    const int32_t n_chunks = static_cast<int32_t>((src.n + 31) / 32);
     if (events) cudaEventRecord(events[0], stream);
     if (count > 0) {
         int64_t want = (count + 255) / 256;
@@ -2554,62 +1886,29 @@ cudaError_t run_hypotheses_range(const SourceView& src, const double* d_tgt_pos,
     if (events) cudaEventRecord(events[1], stream);
     if (count > 0) {
         k_kabsch<<<sm_count * 8, 128, 0, stream>>>(src.pos, d_tgt_pos, rb.surv_index, rb.surv_ids, rb.cand_index,
-                                                   rb.cand_rt, rb.counters, rb.u_sum, rb.u_done,
-                                                   split ? 0 : rb.u_cap);
+                                                   rb.cand_rt, rb.counters, rb.u_sum, rb.u_done, rb.u_cap);
     }
     if (events) cudaEventRecord(events[2], stream);
-    if (!split) {
-        // candidate-CTA scoring: one persistent kernel, record included
-        if (events) cudaEventRecord(events[3], stream);
-        // few candidates (a rank's share under strong scaling): units for the
-        // first u_cap, the candidate-CTA scorer for the rest; many: the
-        // candidate-CTA scorer for all. The latter writes the record.
-        int64_t unit_threshold = 2 * static_cast<int64_t>(cand_blocks);
-        if (const char* v = std::getenv("LK_SCORE_UNITS"); v && v[0] == '1') unit_threshold = INT64_MAX;
-        if (const char* v = std::getenv("LK_SCORE_UNITS"); v && v[0] == '0') unit_threshold = 0;
-        k_score_units<<<cand_blocks, kCtaThreads, 0, stream>>>(src, grid, sp, rb.cand_rt, rb.cand_index, rb.u_cap,
-                                                              rb.u_ns_pad, rb.u_miss, rb.u_inl, rb.u_add, rb.u_sum,
-                                                              rb.u_done, rb.counters, rb.block_best, unit_threshold);
-        k_score_cta<<<cand_blocks, kCtaThreads, 0, stream>>>(src, grid, sp, rb.cand_rt, rb.cand_index, count,
-                                                            rb.cta_ns_pad, rb.cta_add, rb.cta_inl, rb.u_cap,
-                                                            rb.counters, rb.block_best,
-                                                            static_cast<RecordDev*>(d_record), unit_threshold,
-                                                            cand_blocks);
-        if (events) {
-            cudaEventRecord(events[4], stream);
-            cudaEventRecord(events[5], stream);
-            cudaEventRecord(events[6], stream);
-        }
-        return cudaGetLastError();
-    }
-    FastRT* cand_fine = static_cast<FastRT*>(rb.cand_fine);
-    k_prep_fast<<<sm_count * 2, 128, 0, stream>>>(rb.cand_rt, -1, rb.counters, grid, sp, cand_fast);
-    k_prep_fast_fine<<<sm_count * 2, 128, 0, stream>>>(rb.cand_rt, rb.counters, grid, sp, cand_fine);
+    // candidate-CTA scoring: one persistent kernel, record included
     if (events) cudaEventRecord(events[3], stream);
-    const int64_t part_cap = rb.queue_cap / kQueueParts;
-    k_score_split<<<split_blocks, kScoreThreads, 0, stream>>>(src, grid, sp, rb.cand_rt, cand_fine, rb.split_cap,
-                                                              n_chunks, rb.split_ns_pad, rb.inl_masks, rb.miss_masks,
-                                                              rb.addends, rb.queue, part_cap, rb.queue_counts,
-                                                              rb.counters);
-    if (events) cudaEventRecord(events[4], stream);
-    k_score_resolve<<<sm_count * resolve_blocks_per_sm(), kScoreThreads, 0, stream>>>(
-        src, grid, sp, rb.cand_rt, cand_fine, n_chunks, rb.split_ns_pad, rb.queue, part_cap, rb.queue_counts,
-        rb.inl_masks, rb.miss_masks, rb.addends);
-    if (events) cudaEventRecord(events[5], stream);
-    // candidates beyond the split capacity (normally none): streamed warp per candidate
-    k_score<<<over_blocks, kScoreThreads, 0, stream>>>(src, grid, sp, rb.cand_rt, cand_fast, rb.cand_index,
-                                                       rb.split_cap, -1,
-                                                       count, nullptr, nullptr, rb.counters, rb.block_best,
-                                                       exit_blocks, nullptr);
-    CandInfo* info = reinterpret_cast<CandInfo*>(rb.full_list);
-    k_score_exits<<<exit_blocks, kScoreThreads, 0, stream>>>(src.n, sp, rb.split_cap, n_chunks, rb.split_ns_pad,
-                                                             rb.miss_masks, rb.inl_masks, rb.addends, info,
-                                                             rb.counters, rb.block_best, 0);
-    k_score_finalists<<<kFinalCtas, kScoreThreads, 0, stream>>>(n_chunks, rb.split_ns_pad, rb.inl_masks, rb.addends, info,
-                                                       rb.split_cap, rb.cand_rt, rb.cand_index, rb.block_best,
-                                                       exit_blocks + over_blocks, count, rb.counters,
-                                                       static_cast<RecordDev*>(d_record));
-    if (events) cudaEventRecord(events[6], stream);
+    // few candidates (a rank's share under strong scaling): units for the
+    // first u_cap, the candidate-CTA scorer for the rest; many: the
+    // candidate-CTA scorer for all. The latter writes the record.
+    int64_t unit_threshold = 2 * static_cast<int64_t>(cand_blocks);
+    if (const char* v = std::getenv("LK_SCORE_UNITS"); v && v[0] == '1') unit_threshold = INT64_MAX;
+    if (const char* v = std::getenv("LK_SCORE_UNITS"); v && v[0] == '0') unit_threshold = 0;
+    k_score_units<<<cand_blocks, kCtaThreads, 0, stream>>>(src, grid, sp, rb.cand_rt, rb.cand_index, rb.u_cap,
+                                                          rb.u_ns_pad, rb.u_miss, rb.u_inl, rb.u_add, rb.u_sum,
+                                                          rb.u_done, rb.counters, rb.block_best, unit_threshold);
+    k_score_cta<<<cand_blocks, kCtaThreads, 0, stream>>>(src, grid, sp, rb.cand_rt, rb.cand_index, count,
+                                                        rb.cta_ns_pad, rb.cta_add, rb.cta_inl, rb.u_cap, rb.counters,
+                                                        rb.block_best, static_cast<RecordDev*>(d_record),
+                                                        unit_threshold, cand_blocks);
+    if (events) {
+        cudaEventRecord(events[4], stream);
+        cudaEventRecord(events[5], stream);
+        cudaEventRecord(events[6], stream);
+    }
     return cudaGetLastError();
 }
 

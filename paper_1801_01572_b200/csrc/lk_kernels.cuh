@@ -210,25 +210,11 @@ struct RunBuffers {
     Counters* counters = nullptr;
     BestRec* block_best = nullptr;
     int32_t n_blocks = 0;
-    // split scoring: per (candidate, 32-point chunk) inlier / miss ballots and
-    // the inliers' d2, for up to split_cap candidates (addends <= kSplitBytes)
-    static constexpr int64_t kSplitBytes = int64_t(1) << 30;
-    uint32_t* inl_masks = nullptr;
-    uint32_t* miss_masks = nullptr;
-    double* addends = nullptr;
-    int64_t* full_list = nullptr;
-    void* cand_fast = nullptr;  // per-candidate FP32 transform + guard bands
+    void* cand_fast = nullptr;  // per-candidate FP32 transform + guard bands (explicit lists, k_score)
     int64_t fast_capacity = 0;
-    void* cand_fine = nullptr;  // per-candidate FastRT in fine-cell units
-    int4* queue = nullptr;      // (candidate, point, fine offset, count | -1) for k_score_resolve
-    int64_t queue_cap = 0;
-    unsigned long long* queue_counts = nullptr;  // per-partition queue lengths
-    int64_t split_cap = 0;
-    int64_t split_ns_pad = 0;
     cudaStream_t stream = nullptr;  // allocation stream (set by the owner)
     void release();
     cudaError_t ensure(int64_t cap, int32_t score_blocks);
-    cudaError_t ensure_split(int64_t ns, int64_t max_candidates);
     cudaError_t ensure_fast(int64_t n);
     // candidate-CTA scoring: two scratch slots per CTA (addends + ballot words)
     double* cta_add = nullptr;

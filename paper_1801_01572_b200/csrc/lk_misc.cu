@@ -38,22 +38,14 @@ struct BestF {
     int32_t j;
 };
 
-// packed FP32 pairs (sm_100a FMUL2 / FADD2): lo = first, hi = second
-__device__ __forceinline__ unsigned long long pack2(float lo, float hi) {
-    return (static_cast<unsigned long long>(__float_as_uint(hi)) << 32) | __float_as_uint(lo);
-}
-__device__ __forceinline__ float2 unpack2(unsigned long long v) {
-    return make_float2(__uint_as_float(static_cast<unsigned>(v)), __uint_as_float(static_cast<unsigned>(v >> 32)));
-}
-__device__ __forceinline__ unsigned long long add2(unsigned long long a, unsigned long long b) {
-    unsigned long long r;
-    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-    return r;
-}
-__device__ __forceinline__ unsigned long long mul2(unsigned long long a, unsigned long long b) {
-    unsigned long long r;
-    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-    return r;
+// Products as scalar FMUL, lane sums as packed FADD2 (.x = first lane, .y =
+// second). A packed product is not usable: ptxas contracts mul.rn.f32x2 ->
+// add.rn.f32x2 (also through __fmul2_rn / __fadd2_rn and with -fmad=false)
+// into FFMA2, which rounds once instead of twice. Scalar __fmul_rn feeding
+// __fadd2_rn stays two roundings (checked in the SASS: FMUL + FADD2, no FFMA2).
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 mul_pair(float a0, float b0, float a1, float b1) {
+    return make_float2(__fmul_rn(a0, b0), __fmul_rn(a1, b1));
 }
 
 // colwise().squaredNorm() of one 33-bin feature, Eigen's order
@@ -132,7 +124,7 @@ __global__ void k_pad_features(const float* __restrict__ f, int64_t n, float4* _
 // grid (source blocks, target chunks): the chunk's best (score, lowest j) per
 // source. Target tiles staged in shared memory and read as broadcasts; four
 // targets at a time, the lane pairs (0,1) and (2,3) of Eigen's 4-lane
-// accumulators as packed FP32x2 chains (one FMUL2 + one FADD2 per two bins).
+// accumulators as packed FP32x2 chains (two FMUL + one FADD2 per two bins).
 __global__ void __launch_bounds__(kFnnThreads) k_fnn_partial(const float4* __restrict__ sf, int64_t ns,
                                                              const float4* __restrict__ tf,
                                                              const float* __restrict__ q2, int64_t nt,
@@ -143,11 +135,11 @@ __global__ void __launch_bounds__(kFnnThreads) k_fnn_partial(const float4* __res
     float4 s[kFnnPad / 4];
 #pragma unroll
     for (int q = 0; q < kFnnPad / 4; ++q) s[q] = i < ns ? sf[i * (kFnnPad / 4) + q] : make_float4(0, 0, 0, 0);
-    unsigned long long x01[8], x23[8];
+    float2 x01[8], x23[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-        x01[q] = pack2(s[q].x, s[q].y);
-        x23[q] = pack2(s[q].z, s[q].w);
+        x01[q] = make_float2(s[q].x, s[q].y);
+        x23[q] = make_float2(s[q].z, s[q].w);
     }
     const float x32 = s[8].x;
     const int64_t j_begin = blockIdx.y * chunk;
@@ -168,24 +160,24 @@ __global__ void __launch_bounds__(kFnnThreads) k_fnn_partial(const float4* __res
         };
         int jj = 0;
         for (; jj + 4 <= tile; jj += 4) {
-            unsigned long long c01[4], c23[4];
+            float2 c01[4], c23[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const float4 y = s_t[(jj + u) * (kFnnPad / 4)];
-                c01[u] = mul2(pack2(y.x, y.y), x01[0]);  // 0 + a b == a b (features are >= 0)
-                c23[u] = mul2(pack2(y.z, y.w), x23[0]);
+                c01[u] = mul_pair(y.x, x01[0].x, y.y, x01[0].y);  // 0 + a b == a b (features are >= 0)
+                c23[u] = mul_pair(y.z, x23[0].x, y.w, x23[0].y);
             }
 #pragma unroll
             for (int q = 1; q < 8; ++q)
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     const float4 y = s_t[(jj + u) * (kFnnPad / 4) + q];
-                    c01[u] = add2(mul2(pack2(y.x, y.y), x01[q]), c01[u]);
-                    c23[u] = add2(mul2(pack2(y.z, y.w), x23[q]), c23[u]);
+                    c01[u] = add2(mul_pair(y.x, x01[q].x, y.y, x01[q].y), c01[u]);
+                    c23[u] = add2(mul_pair(y.z, x23[q].x, y.w, x23[q].y), c23[u]);
                 }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const float2 p = unpack2(add2(c01[u], c23[u]));  // (c0 + c2, c1 + c3)
+                const float2 p = add2(c01[u], c23[u]);  // (c0 + c2, c1 + c3)
                 float cc = __fadd_rn(p.x, p.y);
                 cc = __fadd_rn(cc, __fmul_rn(s_t[(jj + u) * (kFnnPad / 4) + 8].x, x32));
                 take(__fsub_rn(s_q2[jj + u], __fmul_rn(2.0f, cc)), jj + u);

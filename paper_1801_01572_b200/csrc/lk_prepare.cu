@@ -23,6 +23,8 @@
 #include <cmath>
 #include <cstdint>
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -970,7 +972,7 @@ static uint32_t host_pair_bins(const double* v) {
 // the first kStageX deferred pairs come back in one copy; the decisions go
 // back from here. Reused only after the caller's stream has synchronised.
 struct FpfhStage {
-    static constexpr int kStageX = 1024;
+    static constexpr int kStageX = 4096;
     struct Head {
         int32_t total, n_def, overflow, pad;
         DeferredPair x[kStageX];
@@ -1061,6 +1063,9 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
     // pairs the device cannot settle: the host evaluates pair_angles with the
     // reference's libm (fpfh.cpp:17-53, host_pair_bins)
     const int32_t m = st.head->n_def;
+    if (const char* tr = std::getenv("LK_TRACE"); tr && tr[0] == '1')
+        std::fprintf(stderr, "[lk fpfh] n %lld neighbours %d deferred pairs %d\n", static_cast<long long>(n),
+                     st.head->total, m);
     if (m > 0) {
         std::vector<DeferredPair> more;
         const DeferredPair* xs = st.head->x;

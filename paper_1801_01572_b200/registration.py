@@ -220,21 +220,14 @@ class RegistrationContext:
 
     def phase_times(self, reset: bool = False):
         """({kernel: ms}, runs) accumulated from CUDA events on the launch
-        stream: k_hyp_sample, k_kabsch and the scorer -- k_score_cta (the
-        default candidate-CTA scorer) or, with LK_SCORE_SPLIT=1, k_prep_fast,
-        k_score_split, k_score_resolve and the tail (k_score + k_score_exits +
-        k_score_finalists)."""
+        stream: k_hyp_sample, k_kabsch and the scorer (k_score_units +
+        k_score_cta, reported as k_score_cta)."""
         ms = (C.c_double * len(self._PHASES))()
         runs = C.c_int64()
         check(abi.lib().lk_reg_ctx_phase_times(self._h, ms, len(self._PHASES), C.byref(runs), 1 if reset else 0))
         t = dict(zip(self._PHASES, ms[:]))
-        out = {"k_hyp_sample": t["k_hyp_sample"], "k_kabsch": t["k_kabsch"]}
-        if os.environ.get("LK_SCORE_SPLIT") == "1":
-            out.update({"k_prep_fast": t["prep"], "k_score_split": t["score_a"], "k_score_resolve": t["score_b"],
-                        "score_tail": t["score_tail"]})
-        else:
-            out["k_score_cta"] = t["prep"] + t["score_a"] + t["score_b"] + t["score_tail"]
-        return out, runs.value
+        return {"k_hyp_sample": t["k_hyp_sample"], "k_kabsch": t["k_kabsch"],
+                "k_score_cta": t["prep"] + t["score_a"] + t["score_b"] + t["score_tail"]}, runs.value
 
     def download(self):
         """(source, target, cache, source_features, target_features) on the host."""
