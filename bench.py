@@ -526,10 +526,12 @@ def count_kernel_launches(step, torch):
         with profile(activities=[ProfilerActivity.CUDA]) as prof:
             step()
             torch.cuda.synchronize()
+        import re
         names = [e.name for e in prof.events() if "lkk::" in e.name]
         per = {}
         for n in names:
-            k = n.split("(")[0].split("::")[-1]
+            m = re.search(r"\b(k_\w+)", n)
+            k = m.group(1) if m else n[:60]
             per[k] = per.get(k, 0) + 1
         return len(names), per
     except Exception as e:  # profiler unavailable: report it, do not guess
@@ -660,11 +662,12 @@ def run_b200(args):
         ns2, nt2 = c2.n_source, c2.n_target
         # bytes copied this step: the raw clouds (positions + normals) in; out,
         # the record buffer plus the library's control readbacks per cloud
-        # side (voxel count + normal check 8 B, FPFH staging head 12 B + 4096
-        # deferred pairs 64 KiB, cloud stats 16 B) and the EvalGrid's bounds
-        # and block total (28 B)
+        # side (voxel count + normal check 8 B, FPFH staging head: 16 B of
+        # counts, 4096 acos-tie records of 16 B and 64 theta-edge records of
+        # 96 B, cloud stats 16 B) and the EvalGrid's bounds and block total
+        # (28 B); acos ties beyond the staged 4096 add 16 B each (not counted)
         h2d = 48 * (src_h.size() + tgt_h.size())
-        d2h = 2 * (8 + 12 + 4096 * 16 + 16) + 28 + host.nbytes
+        d2h = 2 * (8 + 16 + 4096 * 16 + 64 * 96 + 16) + 28 + host.nbytes
         c2.close()
     e2e_s = torch.tensor([statistics.mean(e2e_times)], dtype=torch.float64, device=dev)
     if world > 1:

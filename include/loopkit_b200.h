@@ -238,6 +238,32 @@ typedef struct lk_verify_result {
 lk_status lk_verify_batch(const lk_cloud* clouds_i, const lk_cloud* clouds_j, const double* Ti, const double* Tj,
                           const double* T, int64_t n_pairs, const lk_verify_params* params, lk_verify_result* out);
 
+/* ---- propose_loops (fragments.hpp:46-60, fragments.cpp:61-109) -----------
+ * Replaces loopkit::propose_loops(std::span<const Fragment>, const PoseGraph&,
+ * const LoopParams&). fragments[f] = Fragment::cloud (local frame; normals
+ * ignored), poses = PoseGraph::poses (n x 12: row-major R, t), loops =
+ * PoseGraph::loops as (i, j) pairs (either orientation suppresses a pair).
+ * Every pair (later i, earlier j) with i >= j + 2 whose overlap -- the
+ * fraction of i's posed points with a posed point of j within overlap_radius
+ * (the reference SearchGrid's nn_within) -- reaches min_overlap, sorted by
+ * overlap desc, then i, then j. Writes min(count, capacity) proposals and
+ * the full count to n_out. Throws-equivalents: LK_EMPTY_CLOUD (an empty
+ * fragment), LK_INVALID_ARGUMENT (overlap_radius <= 0). */
+typedef struct lk_loop_params {
+    double overlap_radius; /* LoopParams::overlap_radius (0.1) */
+    double min_overlap;    /* LoopParams::min_overlap (0.2) */
+    int32_t device;        /* -1 = current */
+    int32_t _pad;
+} lk_loop_params;
+typedef struct lk_loop_proposal {
+    int32_t i; /* later fragment */
+    int32_t j; /* earlier fragment */
+    double overlap;
+} lk_loop_proposal;
+lk_status lk_propose_loops(const lk_cloud* fragments, const double* poses, int32_t n, const int32_t* loops,
+                           int32_t n_loops, const lk_loop_params* params, lk_loop_proposal* out, int64_t capacity,
+                           int64_t* n_out);
+
 /* ---- line-process weight of a loop edge (host; consumer of edge_info) -----
  * Transforms are 12 doubles (row-major R, then t); info is the row-major 6x6
  * of lk_verify_result / lk_edge_info_batched.

@@ -15,6 +15,7 @@
 #pragma once
 
 #include <cstdint>
+#include <iterator>
 #include <optional>
 #include <stdexcept>
 #include <string>
@@ -259,6 +260,55 @@ inline double edge_residual(const Transform& t_i, const Transform& t_j, const Tr
     return f;
 }
 inline double update_weight(double f, double mu) { return lk_update_weight(f, mu); }
+
+// propose_loops (fragments.hpp:46-60, fragments.cpp:61-109) on the device.
+// Generic over the caller's types: fragments[f].cloud (a Cloud as above),
+// graph.poses[f] with rotation(r, c) / translation[k] (the reference's
+// RigidTransform) and graph.loops[e].i / .j; params has overlap_radius and
+// min_overlap (LoopParams). Throws MissingData when the pose count differs
+// (fragments.cpp:64-66) and EmptyCloud for an empty fragment.
+struct LoopProposal {
+    int i = 0;  // later fragment
+    int j = 0;  // earlier fragment
+    double overlap = 0.0;
+};
+template <class E = DefaultErrors, class Fragments, class Graph, class LoopParamsT>
+std::vector<LoopProposal> propose_loops(const Fragments& fragments, const Graph& graph, const LoopParamsT& params,
+                                        int32_t device = -1) {
+    const size_t n = std::size(fragments);
+    if (graph.poses.size() != n) throw typename E::MissingDataT("propose_loops: one graph pose per fragment required");
+    std::vector<lk_cloud> clouds;
+    std::vector<double> poses;
+    clouds.reserve(n);
+    poses.reserve(12 * n);
+    for (size_t f = 0; f < n; ++f) {
+        const auto& c = fragments[f].cloud;
+        lk_cloud lc{};
+        lc.n = static_cast<int64_t>(c.positions.size());
+        lc.xyz = lc.n ? reinterpret_cast<const double*>(c.positions.data()) : nullptr;
+        clouds.push_back(lc);
+        const auto& T = graph.poses[f];
+        for (int r = 0; r < 3; ++r)
+            for (int k = 0; k < 3; ++k) poses.push_back(T.rotation(r, k));
+        for (int k = 0; k < 3; ++k) poses.push_back(T.translation[k]);
+    }
+    std::vector<int32_t> loops;
+    for (const auto& e : graph.loops) {
+        loops.push_back(static_cast<int32_t>(e.i));
+        loops.push_back(static_cast<int32_t>(e.j));
+    }
+    lk_loop_params lp{params.overlap_radius, params.min_overlap, device, 0};
+    std::vector<lk_loop_proposal> out(n * n > 0 ? n * n : 1);
+    int64_t count = 0;
+    const lk_status st = lk_propose_loops(clouds.data(), poses.data(), static_cast<int32_t>(n), loops.data(),
+                                          static_cast<int32_t>(loops.size() / 2), &lp, out.data(),
+                                          static_cast<int64_t>(out.size()), &count);
+    if (st != LK_OK) throw_status<E>(st);
+    std::vector<LoopProposal> props;
+    props.reserve(static_cast<size_t>(count));
+    for (int64_t k = 0; k < count; ++k) props.push_back({out[k].i, out[k].j, out[k].overlap});
+    return props;
+}
 
 // ICP point-to-plane refinement of `init` (source -> target); DESIGN.md "ICP".
 struct IcpResult {

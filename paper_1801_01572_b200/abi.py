@@ -103,6 +103,15 @@ class lk_verify_params(C.Structure):
     ]
 
 
+class lk_loop_params(C.Structure):
+    _fields_ = [("overlap_radius", C.c_double), ("min_overlap", C.c_double), ("device", C.c_int32),
+                ("_pad", C.c_int32)]
+
+
+class lk_loop_proposal(C.Structure):
+    _fields_ = [("i", C.c_int32), ("j", C.c_int32), ("overlap", C.c_double)]
+
+
 class lk_verify_result(C.Structure):
     _fields_ = [
         ("info", C.c_double * 36),
@@ -195,6 +204,8 @@ SIGNATURES = {
                                   dptr, C.POINTER(C.c_int32)]),
     "lk_verify_batch": (C.c_int, [C.POINTER(lk_cloud), C.POINTER(lk_cloud), dptr, dptr, dptr, C.c_int64,
                                   C.POINTER(lk_verify_params), C.POINTER(lk_verify_result)]),
+    "lk_propose_loops": (C.c_int, [C.POINTER(lk_cloud), dptr, C.c_int32, i32ptr, C.c_int32, C.POINTER(lk_loop_params),
+                                   C.POINTER(lk_loop_proposal), C.c_int64, i64ptr]),
     "lk_icp_point_to_plane": (C.c_int, [C.POINTER(lk_cloud), C.POINTER(lk_cloud), dptr, C.POINTER(lk_icp_params),
                                         C.POINTER(lk_icp_result), dptr]),
     "lk_estimate_normals": (C.c_int, [C.POINTER(lk_cloud), C.c_double, dptr, C.c_int32, dptr]),

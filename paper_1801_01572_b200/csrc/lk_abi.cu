@@ -1016,6 +1016,65 @@ PackedPairs pack_pairs(const lk_cloud* ci, const lk_cloud* cj, int64_t K, bool n
     return pk;
 }
 
+lk_status lk_propose_loops(const lk_cloud* fragments, const double* poses, int32_t n, const int32_t* loops,
+                           int32_t n_loops, const lk_loop_params* params, lk_loop_proposal* out, int64_t capacity,
+                           int64_t* n_out) {
+    return guarded([&]() -> lk_status {
+        if (!params || !n_out || n < 0 || n_loops < 0 || (n > 0 && (!fragments || !poses)) ||
+            (n_loops > 0 && !loops) || (capacity > 0 && !out))
+            return fail(LK_INVALID_ARGUMENT, "null argument");
+        *n_out = 0;
+        if (n == 0) return LK_OK;
+        // grids in fragment order: build_grid throws EmptyCloud, then rejects the cell (grid.cpp:36-37)
+        for (int32_t f = 0; f < n; ++f) {
+            check_cloud_ptr(fragments + f, "fragment");
+            if (fragments[f].n == 0) return fail(LK_EMPTY_CLOUD, "build_grid: empty cloud");
+            if (!(params->overlap_radius > 0.0))
+                return fail(LK_INVALID_ARGUMENT, "build_grid: cell_length must be positive");
+        }
+        std::vector<int64_t> foff(static_cast<size_t>(n) + 1, 0);
+        for (int32_t f = 0; f < n; ++f) foff[f + 1] = foff[f] + fragments[f].n;
+        std::vector<double> xyz(static_cast<size_t>(3 * foff[n]));
+        for (int32_t f = 0; f < n; ++f)
+            std::memcpy(xyz.data() + 3 * foff[f], fragments[f].xyz, 3 * fragments[f].n * sizeof(double));
+        // pairs i >= j + 2 not joined by a loop edge in either orientation (fragments.cpp:79-84,89-92)
+        std::vector<int32_t> pairs;
+        for (int32_t i = 2; i < n; ++i)
+            for (int32_t j = 0; j + 2 <= i; ++j) {
+                bool linked = false;
+                for (int32_t e = 0; e < n_loops && !linked; ++e)
+                    linked = (loops[2 * e] == i && loops[2 * e + 1] == j) || (loops[2 * e] == j && loops[2 * e + 1] == i);
+                if (!linked) {
+                    pairs.push_back(i);
+                    pairs.push_back(j);
+                }
+            }
+        const int32_t K = static_cast<int32_t>(pairs.size() / 2);
+        std::vector<int64_t> hits(static_cast<size_t>(K > 0 ? K : 1));
+        const int dev = select_device(params->device);
+        cudaStream_t s = acquire_stream(dev);
+        cudaError_t e = lkk::propose_loops(xyz.data(), foff.data(), n, poses, pairs.data(), K,
+                                           params->overlap_radius, hits.data(), s);
+        release_stream(dev, s);
+        CK(e);
+        std::vector<lk_loop_proposal> props;
+        for (int32_t k = 0; k < K; ++k) {
+            const int32_t i = pairs[2 * k], j = pairs[2 * k + 1];
+            const double overlap = static_cast<double>(hits[k]) / static_cast<double>(fragments[i].n);
+            if (overlap >= params->min_overlap) props.push_back(lk_loop_proposal{i, j, overlap});
+        }
+        // fragments.cpp:102-107: overlap desc, then i, then j (a strict total order)
+        std::sort(props.begin(), props.end(), [](const lk_loop_proposal& a, const lk_loop_proposal& b) {
+            if (a.overlap != b.overlap) return a.overlap > b.overlap;
+            if (a.i != b.i) return a.i < b.i;
+            return a.j < b.j;
+        });
+        *n_out = static_cast<int64_t>(props.size());
+        for (int64_t k = 0; k < *n_out && k < capacity; ++k) out[k] = props[static_cast<size_t>(k)];
+        return LK_OK;
+    });
+}
+
 lk_status lk_edge_info_batched(const lk_cloud* clouds_i, const lk_cloud* clouds_j, const double* Ti, const double* Tj,
                                int64_t n_pairs, double epsilon, int32_t device, double* info, int64_t* pair_count) {
     return guarded([&]() -> lk_status {

@@ -309,6 +309,11 @@ struct VerifyOutput {
     double sq_sum;  // evaluate_hypothesis's sequential sum of distance^2
 };
 cudaError_t verify_batch(const VerifyInput& in, VerifyOutput* out, cudaStream_t stream);
+// propose_loops (proj/src/fragments.cpp:61-109): hit counts of the K pairs
+// (h_pairs[2k] = later i, [2k+1] = earlier j) over n fragments (h_xyz packed,
+// fragment f = points [h_foff[f], h_foff[f+1]) in its local frame, pose h_T12[12 f]).
+cudaError_t propose_loops(const double* h_xyz, const int64_t* h_foff, int32_t n, const double* h_T12,
+                          const int32_t* h_pairs, int32_t K, double radius, int64_t* h_hits, cudaStream_t stream);
 
 // Scores an explicit candidate list (Rt on device, C x 12) and reduces the best.
 cudaError_t score_candidates(const SourceView& src, const GridView& grid, const ScoreParams& sp, const double* d_rt,

@@ -485,22 +485,31 @@ __device__ __forceinline__ double div_by(double a, double b, double r) {
 // pass 1 (proj/src/fpfh.cpp:76-100): warp per point, integer vote counts in
 // counts[i][0..32], votes in counts[i][33]. Pairs whose frame-source test the
 // device cannot decide are appended to the deferred list (k_spfh_resolve).
-// A pair the device cannot settle (frame-source acos test undecided and
-// deciding, or theta at a bin edge) is appended to the deferred list with its
-// two points and normals; the host evaluates pair_angles with the reference's
-// libm and returns its three bins (k_spfh_resolve).
+// Pairs the device cannot settle go to the host's libm on two lists:
+//   A  the frame-source test acos(|a1|) > acos(|a2|) is undecided here and
+//      the bins depend on it (common on planar faces): (i, j) and (|a1|,
+//      |a2|); the host decides the swap, k_spfh_resolve_a recomputes the bins;
+//   B  theta (atan2) lies at a bin edge for an outcome the pair can take
+//      (astronomically rare): (i, j) and the two points and normals; the host
+//      evaluates pair_angles whole (host_pair_bins), k_spfh_resolve_b votes.
 struct DeferredPair {
     double v[12];  // p1, n1, p2, n2
+};
+struct DeferLists {
+    int2* a_ij;
+    double2* a_x;
+    int2* b_ij;
+    DeferredPair* b_x;
+    int32_t* n;  // n[0] = list A, n[1] = list B
+    int64_t a_cap, b_cap;
 };
 
 __global__ void __launch_bounds__(32 * kFpfhWarps) k_spfh(const double* __restrict__ pos,
                                                           const double* __restrict__ nrm, int64_t n,
                                                           const int32_t* __restrict__ off,
                                                           const int32_t* __restrict__ nbr, int32_t* __restrict__ counts,
-                                                          int2* __restrict__ deferred,
-                                                          DeferredPair* __restrict__ deferred_x,
-                                                          int32_t* __restrict__ n_deferred, int64_t cap,
-                                                          int64_t dcap, const int32_t* __restrict__ skip) {
+                                                          DeferLists dl, int64_t cap,
+                                                          const int32_t* __restrict__ skip) {
     __shared__ int hist[kFpfhWarps][34];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t i = blockIdx.x * static_cast<int64_t>(kFpfhWarps) + warp;
@@ -521,26 +530,37 @@ __global__ void __launch_bounds__(32 * kFpfhWarps) k_spfh(const double* __restri
             const int dec = swap_decision(fabs(s.a1), fabs(s.a2));
             int3 bins;
             bool valid, edge;
-            bool defer = false;
+            int list = -1;  // 0 = A, 1 = B
             if (dec == 2) {
                 // undecidable here: settle it only if the outcome depends on it
                 int3 b1;
                 bool edge1;
                 valid = pair_bins(s, np, nq, 0, bins, edge);
                 const bool valid1 = pair_bins(s, np, nq, 1, b1, edge1);
-                defer = edge || edge1 || valid != valid1 ||
-                        (valid && (bins.x != b1.x || bins.y != b1.y || bins.z != b1.z));
+                if ((valid && edge) || (valid1 && edge1))
+                    list = 1;
+                else if (valid != valid1 || (valid && (bins.x != b1.x || bins.y != b1.y || bins.z != b1.z)))
+                    list = 0;
             } else {
                 valid = pair_bins(s, np, nq, dec, bins, edge);
-                defer = edge;
+                if (valid && edge) list = 1;
             }
-            if (defer) {
-                const int32_t slot = atomicAdd(n_deferred, 1);
-                if (slot >= dcap) continue;  // list full: the host sees n_deferred > dcap and redoes the pass
-                deferred[slot] = make_int2(static_cast<int32_t>(i), j);
-                DeferredPair& d = deferred_x[slot];
-                d.v[0] = p.x, d.v[1] = p.y, d.v[2] = p.z, d.v[3] = np.x, d.v[4] = np.y, d.v[5] = np.z;
-                d.v[6] = q.x, d.v[7] = q.y, d.v[8] = q.z, d.v[9] = nq.x, d.v[10] = nq.y, d.v[11] = nq.z;
+            if (list == 0) {
+                const int32_t slot = atomicAdd(dl.n, 1);
+                if (slot < dl.a_cap) {  // full: the host sees the count over capacity and redoes the pass
+                    dl.a_ij[slot] = make_int2(static_cast<int32_t>(i), j);
+                    dl.a_x[slot] = make_double2(fabs(s.a1), fabs(s.a2));
+                }
+                continue;
+            }
+            if (list == 1) {
+                const int32_t slot = atomicAdd(dl.n + 1, 1);
+                if (slot < dl.b_cap) {
+                    dl.b_ij[slot] = make_int2(static_cast<int32_t>(i), j);
+                    DeferredPair& d = dl.b_x[slot];
+                    d.v[0] = p.x, d.v[1] = p.y, d.v[2] = p.z, d.v[3] = np.x, d.v[4] = np.y, d.v[5] = np.z;
+                    d.v[6] = q.x, d.v[7] = q.y, d.v[8] = q.z, d.v[9] = nq.x, d.v[10] = nq.y, d.v[11] = nq.z;
+                }
                 continue;
             }
             if (!valid) continue;
@@ -556,10 +576,31 @@ __global__ void __launch_bounds__(32 * kFpfhWarps) k_spfh(const double* __restri
     if (lane == 0) counts[34 * i + 33] = votes;
 }
 
-// deferred pairs with the host's bins: (alpha bin, 11 + phi bin, 22 + theta
-// bin) packed as bytes 0-2, byte 3 = 1 for a vote (0: the pair casts none)
-__global__ void k_spfh_resolve(const int2* __restrict__ deferred, const uint32_t* __restrict__ decision, int32_t m,
-                               int32_t* __restrict__ counts) {
+// list A with the host's decisions (0/1) of the frame-source test (no theta
+// edge for either outcome: checked in k_spfh)
+__global__ void k_spfh_resolve_a(const double* __restrict__ pos, const double* __restrict__ nrm,
+                                 const int2* __restrict__ deferred, const uint8_t* __restrict__ decision, int32_t m,
+                                 int32_t* __restrict__ counts) {
+    const int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= m) return;
+    const int2 ij = deferred[k];
+    const V3 n1 = ld3(nrm, ij.x), n2 = ld3(nrm, ij.y);
+    PairSetup s;
+    int3 bins;
+    bool edge;
+    if (!pair_setup(ld3(pos, ij.x), n1, ld3(pos, ij.y), n2, s) || !pair_bins(s, n1, n2, decision[k], bins, edge))
+        return;
+    int32_t* c = counts + 34 * static_cast<int64_t>(ij.x);
+    atomicAdd(c + bins.x, 1);
+    atomicAdd(c + bins.y, 1);
+    atomicAdd(c + bins.z, 1);
+    atomicAdd(c + 33, 1);
+}
+
+// list B with the host's bins: (alpha bin, 11 + phi bin, 22 + theta bin) as
+// bytes 0-2, byte 3 = 1 for a vote (0: the pair casts none)
+__global__ void k_spfh_resolve_b(const int2* __restrict__ deferred, const uint32_t* __restrict__ decision, int32_t m,
+                                 int32_t* __restrict__ counts) {
     const int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= m) return;
     const uint32_t d = decision[k];
@@ -972,17 +1013,24 @@ static uint32_t host_pair_bins(const double* v) {
 // the first kStageX deferred pairs come back in one copy; the decisions go
 // back from here. Reused only after the caller's stream has synchronised.
 struct FpfhStage {
-    static constexpr int kStageX = 4096;
+    static constexpr int kStageA = 4096;
+    static constexpr int kStageB = 64;
     struct Head {
-        int32_t total, n_def, overflow, pad;
-        DeferredPair x[kStageX];
+        int32_t total, n_a, n_b, overflow;
+        double2 a[kStageA];
+        DeferredPair b[kStageB];
     };
     Head* head = nullptr;
-    uint32_t* dec = nullptr;
-    size_t dec_cap = 0;
+    double2* more_a = nullptr;  // pinned: list A beyond the staged head
+    size_t more_cap = 0;
+    uint8_t* dec_a = nullptr;
+    uint32_t* dec_b = nullptr;
+    size_t dec_a_cap = 0, dec_b_cap = 0;
     ~FpfhStage() {
         if (head) cudaFreeHost(head);
-        if (dec) cudaFreeHost(dec);
+        if (more_a) cudaFreeHost(more_a);
+        if (dec_a) cudaFreeHost(dec_a);
+        if (dec_b) cudaFreeHost(dec_b);
     }
 };
 thread_local FpfhStage t_stage;
@@ -1020,19 +1068,31 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
     // per point; an overflow turns the fill and the votes into no-ops and is
     // redone below with the exact size
     int64_t cap = std::max<int64_t>(192 * n, 4096);
-    int64_t dcap = std::max<int64_t>(4 * n, 65536);  // deferred pairs are rare (acos ties, theta bin edges)
+    int64_t a_cap = std::max<int64_t>(8 * n, 65536);  // list A: acos ties (planar faces: ~4 per point)
+    int64_t b_cap = 4096;                            // list B: theta bin edges (essentially never)
     int32_t *votes = nullptr, *n_def = nullptr;
-    int2* deferred = nullptr;
-    DeferredPair* deferred_x = nullptr;
-    uint32_t* d_decision = nullptr;
+    DeferLists dl{};
+    uint8_t* d_dec_a = nullptr;
+    uint32_t* d_dec_b = nullptr;
     LK_TRY(cudaMallocAsync(&spfh, 33 * n * sizeof(double), stream));
     LK_TRY(cudaMallocAsync(&votes, 34 * n * sizeof(int32_t), stream));
-    LK_TRY(cudaMallocAsync(&n_def, sizeof(int32_t), stream));
+    LK_TRY(cudaMallocAsync(&n_def, 2 * sizeof(int32_t), stream));
+    auto free_lists = [&] {
+        cudaFreeAsync(dl.a_ij, stream);
+        cudaFreeAsync(dl.a_x, stream);
+        cudaFreeAsync(dl.b_ij, stream);
+        cudaFreeAsync(dl.b_x, stream);
+    };
     for (int attempt = 0; attempt < 2; ++attempt) {
         LK_TRY(cudaMallocAsync(&nbr, cap * sizeof(int32_t), stream));
-        LK_TRY(cudaMallocAsync(&deferred, dcap * sizeof(int2), stream));
-        LK_TRY(cudaMallocAsync(&deferred_x, dcap * sizeof(DeferredPair), stream));
-        LK_TRY(cudaMemsetAsync(n_def, 0, sizeof(int32_t), stream));
+        LK_TRY(cudaMallocAsync(&dl.a_ij, a_cap * sizeof(int2), stream));
+        LK_TRY(cudaMallocAsync(&dl.a_x, a_cap * sizeof(double2), stream));
+        LK_TRY(cudaMallocAsync(&dl.b_ij, b_cap * sizeof(int2), stream));
+        LK_TRY(cudaMallocAsync(&dl.b_x, b_cap * sizeof(DeferredPair), stream));
+        dl.n = n_def;
+        dl.a_cap = a_cap;
+        dl.b_cap = b_cap;
+        LK_TRY(cudaMemsetAsync(n_def, 0, 2 * sizeof(int32_t), stream));
         if (brute && attempt == 0)
             k_nbr_compact<<<nblocks(32 * n, 256), 256, 0, stream>>>(slots, off, n, d_overflow, nbr, cap);
         else if (brute)
@@ -1041,52 +1101,81 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
         else
             k_nbr_fill<<<nblocks(n, kSortWarps), 32 * kSortWarps, 0, stream>>>(d_pos, n, g.view, r2, off, nbr, cap);
         // an overflowed slot table leaves nbr unfilled: the votes are skipped too
-        k_spfh<<<nblocks(n, kFpfhWarps), 32 * kFpfhWarps, 0, stream>>>(d_pos, d_nrm, n, off, nbr, votes, deferred,
-                                                                       deferred_x, n_def, cap, dcap,
+        k_spfh<<<nblocks(n, kFpfhWarps), 32 * kFpfhWarps, 0, stream>>>(d_pos, d_nrm, n, off, nbr, votes, dl, cap,
                                                                        (brute && attempt == 0) ? d_overflow : nullptr);
-        // one round trip: total, deferred count and the first deferred pairs
+        // one round trip: total, list counts and the heads of both lists
         LK_TRY(cudaMemcpyAsync(&st.head->total, off + n, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
-        LK_TRY(cudaMemcpyAsync(&st.head->n_def, n_def, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
+        LK_TRY(cudaMemcpyAsync(&st.head->n_a, n_def, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
         st.head->overflow = 0;
         if (brute && attempt == 0)
             LK_TRY(cudaMemcpyAsync(&st.head->overflow, d_overflow, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
-        LK_TRY(cudaMemcpyAsync(st.head->x, deferred_x, FpfhStage::kStageX * sizeof(DeferredPair),
-                               cudaMemcpyDeviceToHost, stream));
+        LK_TRY(cudaMemcpyAsync(st.head->a, dl.a_x, FpfhStage::kStageA * sizeof(double2), cudaMemcpyDeviceToHost,
+                               stream));
+        LK_TRY(cudaMemcpyAsync(st.head->b, dl.b_x, FpfhStage::kStageB * sizeof(DeferredPair), cudaMemcpyDeviceToHost,
+                               stream));
         LK_TRY(cudaStreamSynchronize(stream));
-        if (st.head->total <= cap && !st.head->overflow && st.head->n_def <= dcap) break;
+        if (st.head->total <= cap && !st.head->overflow && st.head->n_a <= a_cap && st.head->n_b <= b_cap) break;
         cudaFreeAsync(nbr, stream);
-        cudaFreeAsync(deferred, stream);
-        cudaFreeAsync(deferred_x, stream);
+        free_lists();
         cap = std::max<int64_t>(cap, st.head->total);
-        dcap = std::max<int64_t>(dcap, st.head->n_def);
+        a_cap = std::max<int64_t>(a_cap, st.head->n_a);
+        b_cap = std::max<int64_t>(b_cap, st.head->n_b);
     }
-    // pairs the device cannot settle: the host evaluates pair_angles with the
-    // reference's libm (fpfh.cpp:17-53, host_pair_bins)
-    const int32_t m = st.head->n_def;
+    // pairs the device cannot settle, decided with the reference's libm:
+    // list A by its acos comparison (fpfh.cpp:28), list B whole (host_pair_bins)
+    const int32_t ma = st.head->n_a, mb = st.head->n_b;
     if (const char* tr = std::getenv("LK_TRACE"); tr && tr[0] == '1')
-        std::fprintf(stderr, "[lk fpfh] n %lld neighbours %d deferred pairs %d\n", static_cast<long long>(n),
-                     st.head->total, m);
-    if (m > 0) {
+        std::fprintf(stderr, "[lk fpfh] n %lld neighbours %d deferred: acos ties %d, theta edges %d\n",
+                     static_cast<long long>(n), st.head->total, ma, mb);
+    if (ma > 0) {
+        const double2* xs = st.head->a;
+        if (ma > FpfhStage::kStageA) {
+            if (static_cast<size_t>(ma) > st.more_cap) {
+                if (st.more_a) cudaFreeHost(st.more_a);
+                st.more_a = nullptr;
+                st.more_cap = 0;
+                LK_TRY(cudaHostAlloc(reinterpret_cast<void**>(&st.more_a), ma * sizeof(double2), 0));
+                st.more_cap = ma;
+            }
+            LK_TRY(cudaMemcpyAsync(st.more_a + FpfhStage::kStageA, dl.a_x + FpfhStage::kStageA,
+                                   (ma - FpfhStage::kStageA) * sizeof(double2), cudaMemcpyDeviceToHost, stream));
+            std::memcpy(st.more_a, st.head->a, FpfhStage::kStageA * sizeof(double2));
+            LK_TRY(cudaStreamSynchronize(stream));
+            xs = st.more_a;
+        }
+        if (static_cast<size_t>(ma) > st.dec_a_cap) {
+            if (st.dec_a) cudaFreeHost(st.dec_a);
+            st.dec_a = nullptr;
+            st.dec_a_cap = 0;
+            LK_TRY(cudaHostAlloc(reinterpret_cast<void**>(&st.dec_a), ma, 0));
+            st.dec_a_cap = ma;
+        }
+#pragma omp parallel for schedule(static) if (ma > 4096)
+        for (int32_t k = 0; k < ma; ++k) st.dec_a[k] = std::acos(xs[k].x) > std::acos(xs[k].y) ? 1 : 0;
+        LK_TRY(cudaMallocAsync(&d_dec_a, ma, stream));
+        LK_TRY(cudaMemcpyAsync(d_dec_a, st.dec_a, ma, cudaMemcpyHostToDevice, stream));
+        k_spfh_resolve_a<<<nblocks(ma, 256), 256, 0, stream>>>(d_pos, d_nrm, dl.a_ij, d_dec_a, ma, votes);
+    }
+    if (mb > 0) {
         std::vector<DeferredPair> more;
-        const DeferredPair* xs = st.head->x;
-        if (m > FpfhStage::kStageX) {
-            more.resize(m);
-            LK_TRY(cudaMemcpyAsync(more.data(), deferred_x, m * sizeof(DeferredPair), cudaMemcpyDeviceToHost, stream));
+        const DeferredPair* xs = st.head->b;
+        if (mb > FpfhStage::kStageB) {
+            more.resize(mb);
+            LK_TRY(cudaMemcpyAsync(more.data(), dl.b_x, mb * sizeof(DeferredPair), cudaMemcpyDeviceToHost, stream));
             LK_TRY(cudaStreamSynchronize(stream));
             xs = more.data();
         }
-        if (static_cast<size_t>(m) > st.dec_cap) {
-            if (st.dec) cudaFreeHost(st.dec);
-            st.dec = nullptr;
-            st.dec_cap = 0;
-            LK_TRY(cudaHostAlloc(reinterpret_cast<void**>(&st.dec), m * sizeof(uint32_t), 0));
-            st.dec_cap = m;
+        if (static_cast<size_t>(mb) > st.dec_b_cap) {
+            if (st.dec_b) cudaFreeHost(st.dec_b);
+            st.dec_b = nullptr;
+            st.dec_b_cap = 0;
+            LK_TRY(cudaHostAlloc(reinterpret_cast<void**>(&st.dec_b), mb * sizeof(uint32_t), 0));
+            st.dec_b_cap = mb;
         }
-#pragma omp parallel for schedule(static) if (m > 4096)
-        for (int32_t k = 0; k < m; ++k) st.dec[k] = host_pair_bins(xs[k].v);
-        LK_TRY(cudaMallocAsync(&d_decision, m * sizeof(uint32_t), stream));
-        LK_TRY(cudaMemcpyAsync(d_decision, st.dec, m * sizeof(uint32_t), cudaMemcpyHostToDevice, stream));
-        k_spfh_resolve<<<nblocks(m, 256), 256, 0, stream>>>(deferred, d_decision, m, votes);
+        for (int32_t k = 0; k < mb; ++k) st.dec_b[k] = host_pair_bins(xs[k].v);
+        LK_TRY(cudaMallocAsync(&d_dec_b, mb * sizeof(uint32_t), stream));
+        LK_TRY(cudaMemcpyAsync(d_dec_b, st.dec_b, mb * sizeof(uint32_t), cudaMemcpyHostToDevice, stream));
+        k_spfh_resolve_b<<<nblocks(mb, 256), 256, 0, stream>>>(dl.b_ij, d_dec_b, mb, votes);
     }
     k_spfh_scale<<<nblocks(33 * n, 256), 256, 0, stream>>>(votes, n, spfh);
     k_fpfh<<<nblocks(n, kFpfhWarps), 32 * kFpfhWarps, 0, stream>>>(d_pos, d_nrm, n, off, nbr, spfh, d_out);
@@ -1101,10 +1190,10 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
     if (d_overflow) cudaFreeAsync(d_overflow, stream);
     cudaFreeAsync(spfh, stream);
     cudaFreeAsync(votes, stream);
-    cudaFreeAsync(deferred, stream);
-    cudaFreeAsync(deferred_x, stream);
+    free_lists();
     cudaFreeAsync(n_def, stream);
-    if (d_decision) cudaFreeAsync(d_decision, stream);
+    if (d_dec_a) cudaFreeAsync(d_dec_a, stream);
+    if (d_dec_b) cudaFreeAsync(d_dec_b, stream);
     g.release();
     return cudaGetLastError();
 }

@@ -8,6 +8,8 @@
 //     (posed later points within r of the posed earlier cloud)
 //   * evaluate_hypothesis(T, P, Q, SearchGrid(Q, cell), d_max, angle)
 //                                             proj/src/registration.cpp:53-78
+// and, for the pose graph's all-pairs loop search, propose_loops' overlap hit
+// counts of every (later i, earlier j >= i + 2) fragment pair (propose_loops).
 // Every nearest-neighbour question goes to a ring grid (lk_ring.cuh) that
 // answers with the reference SearchGrid's window semantics; all 3K grids are
 // built in one batched pass. The per-pair sums are the reference's own
@@ -250,6 +252,32 @@ const double* mapped(const void* p) {
     return a.type == cudaMemoryTypeHost ? static_cast<const double*>(a.devicePointer) : nullptr;
 }
 
+// propose_loops overlap (proj/src/fragments.cpp:86-100): pair k = (later i,
+// earlier j); query q of pair k is point q - qoff[k] of posed fragment i,
+// hit iff the reference SearchGrid over posed fragment j (cell = r) finds a
+// point within r (nn_within existence). Warp-aggregated integer counts.
+__global__ void k_propose_hits(const double* __restrict__ posed, const int64_t* __restrict__ foff,
+                               const int32_t* __restrict__ pair_ij, const int64_t* __restrict__ qoff, int K,
+                               const RingGrid* __restrict__ grids, double r2, unsigned long long* __restrict__ hits) {
+    const int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    const bool live = q < qoff[K];
+    int k = 0;
+    bool hit = false;
+    if (live) {
+        k = pair_of(qoff, K, q);
+        const int fi = pair_ij[2 * k], fj = pair_ij[2 * k + 1];
+        const V3 y = ld3(posed, foff[fi] + (q - qoff[k]));
+        hit = ring_nn(grids[fj], y, r2) >= 0;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    if (!m) return;
+    // lanes of one pair (the common case) add once
+    const int lane = threadIdx.x & 31;
+    const unsigned same = __match_any_sync(0xffffffffu, live ? k : -1);
+    const unsigned mine = m & same;
+    if (hit && lane == __ffs(mine) - 1) atomicAdd(hits + k, static_cast<unsigned long long>(__popc(mine)));
+}
+
 }  // namespace
 
 cudaError_t verify_batch(const VerifyInput& in, VerifyOutput* out, cudaStream_t stream) {
@@ -421,6 +449,67 @@ cudaError_t verify_batch(const VerifyInput& in, VerifyOutput* out, cudaStream_t 
         r.inliers = c[12];
         r.sq_sum = o[9];
     }
+    return cudaSuccess;
+}
+
+// proj/src/fragments.cpp:61-109 on the device: pose every fragment
+// (RigidTransform::operator*), one ring grid per posed fragment with the
+// reference's build_grid(posed[f], overlap_radius) window, the hit counts of
+// every (i, j) pair in one launch. The caller filters and sorts.
+cudaError_t propose_loops(const double* h_xyz, const int64_t* h_foff, int32_t n, const double* h_T12,
+                          const int32_t* h_pairs, int32_t K, double radius, int64_t* h_hits, cudaStream_t stream) {
+    const int64_t np = h_foff[n];
+    cudaError_t e = cudaSuccess;
+    double *d_xyz = nullptr, *d_posed = nullptr, *d_T = nullptr;
+    int64_t *d_foff = nullptr, *d_qoff = nullptr;
+    int32_t* d_pairs = nullptr;
+    unsigned long long* d_hits = nullptr;
+    RingBatch rb;
+    auto cleanup = [&] {
+        rb.release();
+        for (void* p : {(void*)d_xyz, (void*)d_posed, (void*)d_T, (void*)d_foff, (void*)d_qoff, (void*)d_pairs,
+                        (void*)d_hits})
+            pool_free(p, stream);
+    };
+#define PL_TRY(x)               \
+    do {                        \
+        e = (x);                \
+        if (e != cudaSuccess) { \
+            cleanup();          \
+            return e;           \
+        }                       \
+    } while (0)
+    std::vector<int64_t> qoff(static_cast<size_t>(K) + 1, 0);
+    for (int k = 0; k < K; ++k) {
+        const int i = h_pairs[2 * k];
+        qoff[k + 1] = qoff[k] + (h_foff[i + 1] - h_foff[i]);
+    }
+    PL_TRY(pool_alloc(&d_xyz, 3 * np * sizeof(double), stream));
+    PL_TRY(pool_alloc(&d_posed, 3 * np * sizeof(double), stream));
+    PL_TRY(pool_alloc(&d_T, 12 * static_cast<int64_t>(n) * sizeof(double), stream));
+    PL_TRY(pool_alloc(&d_foff, (n + 1) * sizeof(int64_t), stream));
+    PL_TRY(pool_alloc(&d_qoff, (K + 1) * sizeof(int64_t), stream));
+    PL_TRY(pool_alloc(&d_pairs, 2 * static_cast<int64_t>(K > 0 ? K : 1) * sizeof(int32_t), stream));
+    PL_TRY(pool_alloc(&d_hits, (K > 0 ? K : 1) * sizeof(unsigned long long), stream));
+    PL_TRY(cudaMemcpyAsync(d_xyz, h_xyz, 3 * np * sizeof(double), cudaMemcpyHostToDevice, stream));
+    PL_TRY(cudaMemcpyAsync(d_T, h_T12, 12 * static_cast<int64_t>(n) * sizeof(double), cudaMemcpyHostToDevice, stream));
+    PL_TRY(cudaMemcpyAsync(d_foff, h_foff, (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, stream));
+    PL_TRY(cudaMemcpyAsync(d_qoff, qoff.data(), (K + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, stream));
+    if (K > 0) PL_TRY(cudaMemcpyAsync(d_pairs, h_pairs, 2 * K * sizeof(int32_t), cudaMemcpyHostToDevice, stream));
+    PL_TRY(cudaMemsetAsync(d_hits, 0, (K > 0 ? K : 1) * sizeof(unsigned long long), stream));
+    k_pose_batched<<<nblocks(np, 256), 256, 0, stream>>>(d_xyz, np, d_foff, n, d_T, d_posed);
+    std::vector<double> gd(static_cast<size_t>(n), radius), gc(static_cast<size_t>(n), radius);
+    PL_TRY(build_ring_grids(rb, d_posed, h_foff, n, gd.data(), gc.data(), stream));
+    if (qoff[K] > 0)
+        k_propose_hits<<<nblocks(qoff[K], 128), 128, 0, stream>>>(d_posed, d_foff, d_pairs, d_qoff, K, rb.d_views,
+                                                                 radius * radius, d_hits);
+    PL_TRY(cudaGetLastError());
+    std::vector<unsigned long long> h(static_cast<size_t>(K > 0 ? K : 1));
+    PL_TRY(cudaMemcpyAsync(h.data(), d_hits, h.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream));
+    PL_TRY(cudaStreamSynchronize(stream));
+#undef PL_TRY
+    cleanup();
+    for (int k = 0; k < K; ++k) h_hits[k] = static_cast<int64_t>(h[k]);
     return cudaSuccess;
 }
 

@@ -550,6 +550,48 @@ def verify_batch(earlier: Sequence[PointCloud], later: Sequence[PointCloud], pos
             for k, (pc, oh, ov, il, ir, ft) in enumerate(zip(*cols))]
 
 
+@dataclass
+class LoopParams:
+    """fragments.hpp LoopParams."""
+
+    overlap_radius: float = 0.1  # point-to-point distance counted as overlap
+    min_overlap: float = 0.2     # fraction of the source fragment's points
+    device: int = -1
+
+
+@dataclass
+class LoopProposal:
+    i: int  # later fragment
+    j: int  # earlier fragment
+    overlap: float
+
+
+def propose_loops(fragments: Sequence[PointCloud], poses: Sequence[RigidTransform],
+                  loops: Sequence[Tuple[int, int]] = (), params: Optional[LoopParams] = None) -> List[LoopProposal]:
+    """fragments.cpp:61-109 on the device: fragments = Fragment::cloud (local
+    frame), poses = PoseGraph::poses, loops = the (i, j) of PoseGraph::loops.
+    Raises MissingData when the counts differ (fragments.cpp:64-66), EmptyCloud
+    for an empty fragment."""
+    from .errors import MissingData
+    p = params or LoopParams()
+    n = len(fragments)
+    if len(poses) != n:
+        raise MissingData("propose_loops: one graph pose per fragment required")
+    tab = _cloud_table(fragments)
+    tp = _pack_transforms(poses)
+    lp = np.ascontiguousarray(np.asarray(list(loops), dtype=np.int32).reshape(-1, 2)) if len(loops) else \
+        np.zeros((1, 2), np.int32)
+    cp = abi.lk_loop_params(overlap_radius=float(p.overlap_radius), min_overlap=float(p.min_overlap),
+                            device=int(p.device), _pad=0)
+    cap = max(n * n, 1)
+    out = (abi.lk_loop_proposal * cap)()
+    cnt = C.c_int64()
+    check(abi.lib().lk_propose_loops(tab.ctypes.data_as(C.POINTER(abi.lk_cloud)), tp.ctypes.data_as(abi.dptr), n,
+                                     lp.ctypes.data_as(abi.i32ptr), len(loops), C.byref(cp), out, cap,
+                                     C.byref(cnt)))
+    return [LoopProposal(int(out[k].i), int(out[k].j), float(out[k].overlap)) for k in range(cnt.value)]
+
+
 def _pack_transforms(ts) -> np.ndarray:
     """(n, 12) row-major R then t per transform (RigidTransform.packed, batched)."""
     if not len(ts):

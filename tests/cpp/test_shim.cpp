@@ -19,6 +19,27 @@ struct PointCloud {  // proj/include/loopkit/geometry.hpp:92-99
     std::vector<Vec3> positions;
     std::vector<Vec3> normals;
 };
+struct Rigid {  // proj/include/loopkit/geometry.hpp:20-38 (rotation(r, c), translation[k])
+    struct M {
+        double m[3][3] = {{1, 0, 0}, {0, 1, 0}, {0, 0, 1}};
+        double operator()(int r, int c) const { return m[r][c]; }
+    } rotation;
+    std::array<double, 3> translation{0, 0, 0};
+};
+struct Fragment {  // proj/include/loopkit/fragments.hpp:18-25
+    PointCloud cloud;
+};
+struct LoopEdge {  // proj/include/loopkit/pose_graph.hpp (i, j)
+    int i = 0, j = 0;
+};
+struct PoseGraph {
+    std::vector<Rigid> poses;
+    std::vector<LoopEdge> loops;
+};
+struct LoopParams {  // proj/include/loopkit/fragments.hpp:39-42
+    double overlap_radius = 0.1;
+    double min_overlap = 0.2;
+};
 struct RegistrationParams {  // proj/include/loopkit/registration.hpp:17-32
     double leaf = 0.05;
     double normal_radius = 0.1;
@@ -94,6 +115,26 @@ int main(int argc, char** argv) {
     } catch (const loopkit_b200::NoCorrespondences&) {
         std::puts("ok: NoCorrespondences");
     }
+    // propose_loops: three copies of src at the identity -> only (2, 0) (test_fragments.cpp:183-200)
+    std::vector<Fragment> frags(3);
+    PoseGraph graph;
+    for (auto& f : frags) {
+        f.cloud.positions = src.positions;
+        graph.poses.emplace_back();
+    }
+    LoopParams lp;
+    lp.min_overlap = 0.0;
+    auto props = loopkit_b200::propose_loops(frags, graph, lp);
+    if (props.size() != 1 || props[0].i != 2 || props[0].j != 0 || props[0].overlap != 1.0) {
+        std::puts("FAIL: propose_loops");
+        return 1;
+    }
+    graph.loops.push_back({0, 2});
+    if (!loopkit_b200::propose_loops(frags, graph, lp).empty()) {
+        std::puts("FAIL: propose_loops linked pair");
+        return 1;
+    }
+    std::puts("ok: propose_loops (2, 0)");
     auto icp = loopkit_b200::icp_point_to_plane(src, tgt, r->transform, 0.05);
     std::printf("ok: icp iterations %d converged %d rmse %.3e t = %.4f %.4f %.4f\n", icp.iterations,
                 icp.converged ? 1 : 0, icp.rmse, icp.transform.t[0], icp.transform.t[1], icp.transform.t[2]);

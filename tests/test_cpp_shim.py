@@ -36,3 +36,4 @@ def test_shim_on_gpu(tmp_path):
     assert out.returncode == 0, out.stdout + out.stderr
     assert "ok: TooFewPoints" in out.stdout and "ok: index" in out.stdout
     assert "ok: NoCorrespondences" in out.stdout and "ok: icp iterations" in out.stdout
+    assert "ok: propose_loops (2, 0)" in out.stdout
