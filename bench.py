@@ -61,7 +61,8 @@ def workload_config(args, ns_raw, nt_raw, ns=None, nt=None):
         "source_points": ns_raw, "target_points": nt_raw,
         "hypotheses": args.hypotheses, "leaf": 0.05, "d_max": 0.075,
         "l2": "flushed before every timed step (256 MiB device write)",
-        "parallelism": f"hypotheses sharded contiguously over {args.gpus} rank(s), one record exchange",
+        "parallelism": f"hypotheses sharded contiguously over {args.gpus} rank(s) (one process per GPU), one NCCL "
+                       "all-reduce of the rank records inside the library (lk_reg_run_exchange)",
     }
     if ns is not None:
         cfg["source_downsampled"] = ns
@@ -594,8 +595,22 @@ def run_b200(args):
     # ---- device-resident leg
     ctx = lk.prepare_registration(src_h, tgt_h, params)
     ctx.set_stream(stream.cuda_stream)
+    # N > 1: the library's own exchange -- rank 0's NCCL unique id goes to every
+    # rank, each context joins the communicator, and lk_reg_run_exchange runs
+    # the rank's share and the ncclAllReduce of the rank records on the
+    # context stream (include/loopkit_b200.h). The one-device test hook (every
+    # rank on cuda:0, gloo) cannot host an NCCL communicator: it exchanges
+    # through torch.
+    lib_exchange = world > 1 and not one_dev
+    if lib_exchange:
+        box = [lk.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        ctx.attach_comm(box[0], world, rank)
 
     def step():
+        if lib_exchange:
+            ctx.run_exchange(params, xbuf.data_ptr())
+            return
         xbuf.zero_()
         lk.run_hypotheses_range(ctx, params, begin, end, slot_ptr)
         if world > 1:

@@ -25,7 +25,7 @@
 extern "C" {
 #endif
 
-#define LK_ABI_VERSION 1
+#define LK_ABI_VERSION 2
 
 /* proj/include/loopkit/errors.hpp:9-74 */
 typedef enum lk_status {
@@ -65,6 +65,16 @@ typedef struct lk_reg_params {
     uint64_t seed;           /* 0 */
     int32_t threads;         /* host threads for the host prepare stage; 0 = all */
     int32_t device;          /* CUDA device ordinal; -1 = current */
+    /* Devices one call uses (the reference's params.threads across GPUs,
+     * registration.cpp:280): 0 or 1 = `device` alone; G > 1 = devices
+     * device .. device + G - 1 (device -1 = from 0); -1 = every visible
+     * device. A G-device context is prepared once on the first device and
+     * broadcast over NCCL (ncclBroadcast); run_hypotheses gives device g the
+     * contiguous hypothesis range [g H / G, (g + 1) H / G) and merges the G
+     * rank records with one ncclAllReduce. Results are
+     * bitwise identical for every G. */
+    int32_t device_count;
+    int32_t _reserved;
 } lk_reg_params;
 
 /* proj/include/loopkit/registration.hpp:34-39 (RegistrationResult) + inlier count */
@@ -169,6 +179,22 @@ lk_status lk_reg_run_range(lk_reg_ctx* ctx, const lk_reg_params* params, int64_t
 lk_status lk_reg_merge_records(const lk_reg_record* records, int32_t count, int64_t n_source, lk_reg_result* result,
                                lk_hyp_stats* stats);
 
+/* ---- one process per GPU (torchrun / MPI style) ---------------------------
+ * Rank 0 creates an NCCL unique id and the caller broadcasts its 128 bytes to
+ * every rank by any means; each rank attaches it to its own context
+ * (ncclCommInitRank; the communicator belongs to the context). From then on
+ * lk_reg_run_hypotheses on that context runs the rank's contiguous share
+ * [rank H / nranks, (rank + 1) H / nranks), exchanges the rank records with
+ * one ncclAllReduce over NVLink and returns the merged result on every rank
+ * (identical to a 1-GPU run). lk_reg_run_exchange is the same without the
+ * host merge: asynchronous on the context stream, it leaves the nranks
+ * records in records_dev (device, nranks x lk_reg_record). */
+lk_status lk_nccl_unique_id(uint8_t id[128]);
+lk_status lk_reg_ctx_attach_comm(lk_reg_ctx* ctx, const uint8_t id[128], int32_t nranks, int32_t rank);
+lk_status lk_reg_run_exchange(lk_reg_ctx* ctx, const lk_reg_params* params, lk_reg_record* records_dev);
+/* number of devices (1 for a single-device context) and this context's rank */
+lk_status lk_reg_ctx_topology(const lk_reg_ctx* ctx, int32_t* n_devices, int32_t* nranks, int32_t* rank);
+
 /* ---- register_global (registration.hpp:121-124, registration.cpp:334-343) */
 lk_status lk_register_global(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_params* params,
                              lk_reg_result* result, lk_hyp_stats* stats);
@@ -222,7 +248,10 @@ typedef struct lk_verify_params {
     double grid_cell;        /* SearchGrid cell of evaluate_hypothesis's target grid; <= 0 -> d_max */
     double normal_angle_max; /* RegistrationParams::normal_angle_max (radians) */
     int32_t device;          /* -1: current device */
-    int32_t reserved;
+    /* 0 / 1: `device` alone; G > 1: the pairs split into G contiguous shares
+     * on devices device .. device + G - 1 (no exchange: pairs are
+     * independent); -1: every visible device */
+    int32_t device_count;
 } lk_verify_params;
 
 typedef struct lk_verify_result {

@@ -15,11 +15,13 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
 #include <iterator>
 #include <optional>
 #include <stdexcept>
 #include <string>
 #include <type_traits>
+#include <utility>
 #include <vector>
 
 #include "../loopkit_b200.h"
@@ -89,8 +91,25 @@ inline lk_cloud as_lk_cloud(const Cloud& c) {
     return out;
 }
 
+// GPUs per call: the caller's Params::device_count when it has one, else the
+// LK_DEVICE_COUNT environment variable (so the reference's own callers, whose
+// RegistrationParams have no such field, can opt in unchanged), else 1.
+template <class P, class = void>
+struct has_device_count : std::false_type {};
+template <class P>
+struct has_device_count<P, std::void_t<decltype(std::declval<const P&>().device_count)>> : std::true_type {};
 template <class Params>
-inline lk_reg_params to_lk_params(const Params& p, int32_t device = -1) {
+inline int32_t device_count_of(const Params& p) {
+    if constexpr (has_device_count<Params>::value) {
+        return static_cast<int32_t>(p.device_count);
+    } else {
+        const char* v = std::getenv("LK_DEVICE_COUNT");
+        return v ? static_cast<int32_t>(std::atoi(v)) : 0;
+    }
+}
+
+template <class Params>
+inline lk_reg_params to_lk_params(const Params& p, int32_t device = -1, int32_t device_count = -2) {
     lk_reg_params o{};
     o.leaf = p.leaf;
     o.normal_radius = p.normal_radius;
@@ -104,6 +123,7 @@ inline lk_reg_params to_lk_params(const Params& p, int32_t device = -1) {
     o.seed = p.seed;
     o.threads = p.threads;
     o.device = device;
+    o.device_count = device_count == -2 ? device_count_of(p) : device_count;  // GPUs of one call
     return o;
 }
 

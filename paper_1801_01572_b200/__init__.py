@@ -18,6 +18,6 @@ from .registration import (CandidateScores, DeviceGrid, EdgeInfo, EvalGrid, Hypo
                            prepare_registration,
                            records_from_bytes, register_global, registration_context, run_hypotheses,
                            run_hypotheses_range, score_candidates, verify_batch, voxel_downsample)
-from .registration import LoopParams, LoopProposal, VerifyParams, VerifyResult, propose_loops
+from .registration import LoopParams, LoopProposal, VerifyParams, VerifyResult, nccl_unique_id, propose_loops
 
 __all__ = [name for name in dir() if not name.startswith("_")]

@@ -54,6 +54,8 @@ class lk_reg_params(C.Structure):
         ("seed", C.c_uint64),
         ("threads", C.c_int32),
         ("device", C.c_int32),
+        ("device_count", C.c_int32),
+        ("_reserved", C.c_int32),
     ]
 
 
@@ -99,7 +101,7 @@ class lk_verify_params(C.Structure):
         ("grid_cell", C.c_double),
         ("normal_angle_max", C.c_double),
         ("device", C.c_int32),
-        ("reserved", C.c_int32),
+        ("device_count", C.c_int32),
     ]
 
 
@@ -204,6 +206,10 @@ SIGNATURES = {
                                   dptr, C.POINTER(C.c_int32)]),
     "lk_verify_batch": (C.c_int, [C.POINTER(lk_cloud), C.POINTER(lk_cloud), dptr, dptr, dptr, C.c_int64,
                                   C.POINTER(lk_verify_params), C.POINTER(lk_verify_result)]),
+    "lk_nccl_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
+    "lk_reg_ctx_attach_comm": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint8), C.c_int32, C.c_int32]),
+    "lk_reg_run_exchange": (C.c_int, [C.c_void_p, C.POINTER(lk_reg_params), C.c_void_p]),
+    "lk_reg_ctx_topology": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "lk_propose_loops": (C.c_int, [C.POINTER(lk_cloud), dptr, C.c_int32, i32ptr, C.c_int32, C.POINTER(lk_loop_params),
                                    C.POINTER(lk_loop_proposal), C.c_int64, i64ptr]),
     "lk_icp_point_to_plane": (C.c_int, [C.POINTER(lk_cloud), C.POINTER(lk_cloud), dptr, C.POINTER(lk_icp_params),

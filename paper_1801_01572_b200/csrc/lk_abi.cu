@@ -5,6 +5,7 @@
 // own their device buffers; calls on one context serialise on its mutex, so
 // concurrent calls on a shared context stay safe as in the reference.
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <array>
@@ -43,6 +44,11 @@ inline void ck(cudaError_t e, const char* where) {
     if (e != cudaSuccess) throw CudaFail{e, where};
 }
 #define CK(x) ck((x), #x)
+
+inline void nk(ncclResult_t r, const char* where) {
+    if (r != ncclSuccess) throw lk::Status(LK_NCCL_ERROR, std::string(where) + ": " + ncclGetErrorString(r));
+}
+#define NK(x) nk((x), #x)
 
 template <class F>
 lk_status guarded(F&& fn) {
@@ -350,6 +356,13 @@ struct lk_reg_ctx {
     lkk::GridStorage grid;
     lkk::RunBuffers rb;
     lk_reg_record* d_record = nullptr;
+    // multi-GPU: the NCCL communicator of this context's rank
+    // and the [nranks x record] exchange buffer; a single-process G-device
+    // context keeps the other devices' replicas in `peers` (rank g = peers[g-1])
+    ncclComm_t comm = nullptr;
+    int32_t nranks = 1, rank = 0;
+    lk_reg_record* d_xbuf = nullptr;
+    std::vector<lk_reg_ctx*> peers;
     double prepare_seconds = 0.0;
     bool profile = false;
     std::vector<std::array<cudaEvent_t, lkk::kPhaseEvents>> pending;
@@ -370,8 +383,11 @@ struct lk_reg_ctx {
         pending.clear();
     }
     ~lk_reg_ctx() {
+        for (lk_reg_ctx* p : peers) delete p;
+        peers.clear();
         cudaSetDevice(device);
         drain_events();
+        if (comm) ncclCommDestroy(comm);
         if (stream) cudaStreamSynchronize(stream);
         cudaStream_t s = own_stream;
         lkk::pool_free(d_spos, s);
@@ -388,6 +404,7 @@ struct lk_reg_ctx {
         rb.stream = s;  // the caller's stream (synchronised above) may be gone
         rb.release();
         lkk::pool_free(d_record, s);
+        lkk::pool_free(d_xbuf, s);
         if (own_stream) cudaStreamSynchronize(own_stream);
         if (aux_stream) cudaStreamSynchronize(aux_stream);
         if (grid_stream) cudaStreamSynchronize(grid_stream);
@@ -527,6 +544,74 @@ void prepare_side(CloudSide& cs, double feature_radius, double normal_radius, do
     }
 }
 
+// Devices of a call (lk_reg_params::device_count): `device` alone, or G
+// consecutive devices from it, or every visible device (-1).
+std::vector<int> call_devices(int32_t device, int32_t device_count) {
+    const int d0 = select_device(device);
+    int n = 0;
+    CK(cudaGetDeviceCount(&n));
+    int g = device_count < 0 ? n - d0 : device_count;
+    if (g <= 1) return {d0};
+    if (d0 + g > n) throw lk::Status(LK_INVALID_ARGUMENT, "device_count exceeds the visible CUDA devices");
+    std::vector<int> devs;
+    for (int k = 0; k < g; ++k) devs.push_back(d0 + k);
+    return devs;
+}
+
+// A single-process G-device context: NCCL communicators over the devices
+// (ncclCommInitAll), the prepared context broadcast from device 0
+// (ncclBroadcast of the downsampled clouds and the match cache), the source
+// records and the EvalGrid rebuilt on each replica from the broadcast target
+// (deterministic: bit-identical to device 0's), one exchange buffer per rank.
+void make_peers(lk_reg_ctx* c, const std::vector<int>& devs, double d_max) {
+    const int G = static_cast<int>(devs.size());
+    std::vector<ncclComm_t> comms(G);
+    NK(ncclCommInitAll(comms.data(), G, devs.data()));
+    c->comm = comms[0];
+    c->nranks = G;
+    c->rank = 0;
+    for (int g = 1; g < G; ++g) {
+        lk_reg_ctx* p = ctx_new(devs[g]);
+        c->peers.push_back(p);
+        p->comm = comms[g];
+        p->nranks = G;
+        p->rank = g;
+        p->ns = c->ns;
+        p->nt = c->nt;
+        p->src_max_norm = c->src_max_norm;
+        cudaStream_t s = p->stream;
+        CK(lkk::pool_alloc(&p->d_spos, 3 * p->ns * sizeof(double), s));
+        CK(lkk::pool_alloc(&p->d_snrm, 3 * p->ns * sizeof(double), s));
+        CK(lkk::pool_alloc(&p->d_tpos, 3 * p->nt * sizeof(double), s));
+        CK(lkk::pool_alloc(&p->d_tnrm, 3 * p->nt * sizeof(double), s));
+        CK(lkk::pool_alloc(&p->d_cache, p->ns * sizeof(int32_t), s));
+    }
+    std::vector<lk_reg_ctx*> all{c};
+    all.insert(all.end(), c->peers.begin(), c->peers.end());
+    auto bcast = [&](auto member, size_t count, ncclDataType_t type) {
+        NK(ncclGroupStart());
+        for (int g = 0; g < G; ++g)
+            NK(ncclBroadcast(all[0]->*member, all[g]->*member, count, type, 0, all[g]->comm, all[g]->stream));
+        NK(ncclGroupEnd());
+    };
+    bcast(&lk_reg_ctx::d_spos, 3 * c->ns, ncclFloat64);
+    bcast(&lk_reg_ctx::d_snrm, 3 * c->ns, ncclFloat64);
+    bcast(&lk_reg_ctx::d_tpos, 3 * c->nt, ncclFloat64);
+    bcast(&lk_reg_ctx::d_tnrm, 3 * c->nt, ncclFloat64);
+    bcast(&lk_reg_ctx::d_cache, c->ns, ncclInt32);
+    for (lk_reg_ctx* p : c->peers) {
+        CK(cudaSetDevice(p->device));
+        ctx_finish_source(p);
+        CK(lkk::build_grid(p->grid, 0, p->d_tpos, p->d_tnrm, p->nt, d_max, d_max, p->stream));
+    }
+    for (lk_reg_ctx* q : all) {
+        CK(cudaSetDevice(q->device));
+        CK(lkk::pool_alloc(&q->d_xbuf, G * sizeof(lk_reg_record), q->stream));
+        CK(cudaStreamSynchronize(q->stream));
+    }
+    CK(cudaSetDevice(c->device));
+}
+
 lk_status prepare_impl(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_params* params, lk_reg_ctx** out) {
     if (!params || !out) return fail(LK_INVALID_ARGUMENT, "null argument");
     check_cloud_ptr(src, "source");
@@ -535,7 +620,8 @@ lk_status prepare_impl(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_pa
     double t0 = now_s();
     if (src->n == 0 || tgt->n == 0) return fail(LK_EMPTY_CLOUD, "voxel_downsample: empty cloud");
     if (!(params->leaf > 0.0)) return fail(LK_INVALID_ARGUMENT, "voxel_downsample: leaf must be positive");
-    lk_reg_ctx* c = ctx_new(params->device);
+    const std::vector<int> devs = call_devices(params->device, params->device_count);
+    lk_reg_ctx* c = ctx_new(devs[0]);
     tstart(c->own_stream);
     CloudSide S, T;
     S.in = src;
@@ -592,6 +678,7 @@ lk_status prepare_impl(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_pa
         CK(cudaStreamSynchronize(s));
         tdump();
         if (trace_on()) std::fprintf(stderr, "[lk prepare] feature nn %8.3f ms\n", (now_s() - t0) * 1e3);
+        if (devs.size() > 1) make_peers(c, devs, params->d_max);
     } catch (...) {
         drop(S);
         drop(T);
@@ -620,6 +707,36 @@ lk_status run_range_impl(lk_reg_ctx* c, const lk_reg_params& p, int64_t begin, i
     }
     CK(lkk::run_hypotheses_range(sv, c->d_tpos, c->d_cache, c->grid.view, sp, p.seed, p.similarity_tau, begin, end,
                                  c->rb, d_record, c->stream, c->sm_count, ev));
+    return LK_OK;
+}
+
+// Every rank's share of [0, H) and one ncclAllReduce(sum) over the
+// zero-filled [nranks x record] buffers (an exact all-gather: each slot has
+// one writer); single-process G-device contexts drive all ranks from here,
+// a multi-process rank drives its own. Leaves the records on c's device.
+lk_status exchange_run(lk_reg_ctx* c, const lk_reg_params& p) {
+    const int G = c->nranks;
+    const int64_t H = p.hypothesis_count;
+    const size_t words = G * sizeof(lk_reg_record) / sizeof(int64_t);
+    std::vector<lk_reg_ctx*> all;
+    if (!c->peers.empty()) {
+        all.push_back(c);
+        all.insert(all.end(), c->peers.begin(), c->peers.end());
+    } else {
+        all.push_back(c);
+    }
+    for (lk_reg_ctx* q : all) {
+        CK(cudaSetDevice(q->device));
+        CK(cudaMemsetAsync(q->d_xbuf, 0, G * sizeof(lk_reg_record), q->stream));
+        const int64_t begin = q->rank * H / G, end = (q->rank + 1) * H / G;
+        const lk_status st = run_range_impl(q, p, begin, end, q->d_xbuf + q->rank);
+        if (st != LK_OK) return st;
+    }
+    NK(ncclGroupStart());
+    for (lk_reg_ctx* q : all)
+        NK(ncclAllReduce(q->d_xbuf, q->d_xbuf, words, ncclInt64, ncclSum, q->comm, q->stream));
+    NK(ncclGroupEnd());
+    CK(cudaSetDevice(c->device));
     return LK_OK;
 }
 
@@ -811,22 +928,99 @@ lk_status lk_reg_run_hypotheses(lk_reg_ctx* ctx, const lk_reg_params* params, lk
         if (params->hypothesis_count < 0) return fail(LK_INVALID_ARGUMENT, "negative hypothesis_count");
         std::lock_guard<std::mutex> lock(ctx->mu);
         double t0 = now_s();
-        lk_status st = run_range_impl(ctx, *params, 0, params->hypothesis_count, ctx->d_record);
-        if (st != LK_OK) return st;
-        auto* hrec = static_cast<lk_reg_record*>(lkk::host_scratch(sizeof(lk_reg_record)));
+        const int G = ctx->nranks;
+        std::vector<lk_reg_record> recs(static_cast<size_t>(G));
+        auto* hrec = static_cast<lk_reg_record*>(lkk::host_scratch(G * sizeof(lk_reg_record)));
         if (!hrec) CK(cudaErrorMemoryAllocation);
-        CK(cudaMemcpyAsync(hrec, ctx->d_record, sizeof(lk_reg_record), cudaMemcpyDeviceToHost, ctx->stream));
+        if (ctx->comm) {
+            lk_status st = exchange_run(ctx, *params);
+            if (st != LK_OK) return st;
+            CK(cudaMemcpyAsync(hrec, ctx->d_xbuf, G * sizeof(lk_reg_record), cudaMemcpyDeviceToHost, ctx->stream));
+            for (lk_reg_ctx* q : ctx->peers) {
+                CK(cudaSetDevice(q->device));
+                CK(cudaStreamSynchronize(q->stream));
+            }
+            CK(cudaSetDevice(ctx->device));
+        } else {
+            lk_status st = run_range_impl(ctx, *params, 0, params->hypothesis_count, ctx->d_record);
+            if (st != LK_OK) return st;
+            CK(cudaMemcpyAsync(hrec, ctx->d_record, sizeof(lk_reg_record), cudaMemcpyDeviceToHost, ctx->stream));
+        }
         CK(cudaStreamSynchronize(ctx->stream));
-        const lk_reg_record rec = *hrec;
+        std::memcpy(recs.data(), hrec, G * sizeof(lk_reg_record));
         double t1 = now_s();
         lk_hyp_stats local{};
         lk_hyp_stats* sp = stats ? stats : &local;
         double prep = sp->prepare_seconds;
-        lk_status ms = lk_reg_merge_records(&rec, 1, ctx->ns, result, sp);
+        lk_status ms = lk_reg_merge_records(recs.data(), G, ctx->ns, result, sp);
         sp->prepare_seconds = prep;
         sp->hypothesis_seconds = t1 - t0;
         return ms;
     });
+}
+
+lk_status lk_nccl_unique_id(uint8_t id[128]) {
+    return guarded([&]() -> lk_status {
+        if (!id) return fail(LK_INVALID_ARGUMENT, "null argument");
+        ncclUniqueId u;
+        static_assert(sizeof(u.internal) == 128, "NCCL unique id size");
+        NK(ncclGetUniqueId(&u));
+        std::memcpy(id, u.internal, 128);
+        return LK_OK;
+    });
+}
+
+lk_status lk_reg_ctx_attach_comm(lk_reg_ctx* ctx, const uint8_t id[128], int32_t nranks, int32_t rank) {
+    return guarded([&]() -> lk_status {
+        if (!ctx || !id) return fail(LK_INVALID_ARGUMENT, "null argument");
+        if (nranks < 1 || rank < 0 || rank >= nranks) return fail(LK_INVALID_ARGUMENT, "bad rank / nranks");
+        std::lock_guard<std::mutex> lock(ctx->mu);
+        if (ctx->comm) return fail(LK_INVALID_ARGUMENT, "context already has a communicator");
+        CK(cudaSetDevice(ctx->device));
+        ncclUniqueId u;
+        std::memcpy(u.internal, id, 128);
+        NK(ncclCommInitRank(&ctx->comm, nranks, u, rank));
+        ctx->nranks = nranks;
+        ctx->rank = rank;
+        CK(lkk::pool_alloc(&ctx->d_xbuf, nranks * sizeof(lk_reg_record), ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        return LK_OK;
+    });
+}
+
+lk_status lk_reg_run_exchange(lk_reg_ctx* ctx, const lk_reg_params* params, lk_reg_record* records_dev) {
+    return guarded([&]() -> lk_status {
+        if (!ctx || !params || !records_dev) return fail(LK_INVALID_ARGUMENT, "null argument");
+        if (params->hypothesis_count < 0) return fail(LK_INVALID_ARGUMENT, "negative hypothesis_count");
+        std::lock_guard<std::mutex> lock(ctx->mu);
+        if (ctx->comm) {
+            const lk_status st = exchange_run(ctx, *params);
+            if (st != LK_OK) return st;
+            CK(cudaMemcpyAsync(records_dev, ctx->d_xbuf, ctx->nranks * sizeof(lk_reg_record), cudaMemcpyDeviceToDevice,
+                               ctx->stream));
+            for (lk_reg_ctx* q : ctx->peers) {  // the caller waits on the context stream only
+                cudaEvent_t done;
+                CK(cudaSetDevice(q->device));
+                CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+                CK(cudaEventRecord(done, q->stream));
+                CK(cudaSetDevice(ctx->device));
+                CK(cudaStreamWaitEvent(ctx->stream, done, 0));
+                CK(cudaSetDevice(q->device));
+                cudaEventDestroy(done);
+            }
+            CK(cudaSetDevice(ctx->device));
+            return LK_OK;
+        }
+        return run_range_impl(ctx, *params, 0, params->hypothesis_count, records_dev);
+    });
+}
+
+lk_status lk_reg_ctx_topology(const lk_reg_ctx* ctx, int32_t* n_devices, int32_t* nranks, int32_t* rank) {
+    if (!ctx) return fail(LK_INVALID_ARGUMENT, "null context");
+    if (n_devices) *n_devices = 1 + static_cast<int32_t>(ctx->peers.size());
+    if (nranks) *nranks = ctx->nranks;
+    if (rank) *rank = ctx->rank;
+    return LK_OK;
 }
 
 lk_status lk_register_global(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_params* params,
@@ -1108,6 +1302,47 @@ lk_status lk_edge_info_batched(const lk_cloud* clouds_i, const lk_cloud* clouds_
     });
 }
 
+// One device's share of a verification batch (pairs [k0, k0 + K) of the call).
+void verify_share(const lk_cloud* clouds_i, const lk_cloud* clouds_j, const double* Ti, const double* Tj,
+                  const double* T, int64_t k0, int64_t K, const lk_verify_params* params, int dev,
+                  lk_verify_result* out) {
+    PackedPairs pk = pack_pairs(clouds_i + k0, clouds_j + k0, K, true);
+    CK(cudaSetDevice(dev));
+    cudaStream_t s = acquire_stream(dev);
+    lkk::VerifyInput in{};
+    in.n_pairs = static_cast<int32_t>(K);
+    in.qpos = pk.qpos.data();
+    in.qnrm = pk.qnrm.data();
+    in.ppos = pk.ppos.data();
+    in.pnrm = pk.pnrm.data();
+    in.offq = pk.offq.data();
+    in.offp = pk.offp.data();
+    in.Ti = Ti + 12 * k0;
+    in.Tj = Tj + 12 * k0;
+    in.T = T + 12 * k0;
+    in.epsilon = params->epsilon;
+    in.overlap_radius = params->overlap_radius;
+    in.d_max = params->d_max;
+    in.grid_cell = params->grid_cell > 0.0 ? params->grid_cell : params->d_max;
+    in.cos_max = std::cos(params->normal_angle_max);  // registration.cpp:61
+    in.full = 1;
+    std::vector<lkk::VerifyOutput> o(static_cast<size_t>(K));
+    cudaError_t e = lkk::verify_batch(in, o.data(), s);
+    release_stream(dev, s);
+    CK(e);
+    for (int64_t k = 0; k < K; ++k) {
+        lk_verify_result& r = out[k0 + k];
+        for (int q = 0; q < 36; ++q) r.info[q] = o[k].info[q];
+        r.pair_count = o[k].pair_count;
+        r.overlap_hits = o[k].overlap_hits;
+        const double np = static_cast<double>(clouds_j[k0 + k].n);
+        r.overlap = static_cast<double>(o[k].overlap_hits) / np;
+        r.inliers = o[k].inliers;
+        r.inlier_ratio = static_cast<double>(o[k].inliers) / np;
+        r.fitness = o[k].inliers > 0 ? o[k].sq_sum / static_cast<double>(o[k].inliers) : 0.0;
+    }
+}
+
 lk_status lk_verify_batch(const lk_cloud* clouds_i, const lk_cloud* clouds_j, const double* Ti, const double* Tj,
                           const double* T, int64_t n_pairs, const lk_verify_params* params, lk_verify_result* out) {
     return guarded([&]() -> lk_status {
@@ -1117,41 +1352,30 @@ lk_status lk_verify_batch(const lk_cloud* clouds_i, const lk_cloud* clouds_j, co
             return fail(LK_INVALID_ARGUMENT, "build_grid: cell_length must be positive");
         if (n_pairs == 0) return LK_OK;
         if (n_pairs > INT32_MAX) return fail(LK_INVALID_ARGUMENT, "verify: batch too large");
-        PackedPairs pk = pack_pairs(clouds_i, clouds_j, n_pairs, true);
-        const int dev = select_device(params->device);
-        cudaStream_t s = acquire_stream(dev);
-        lkk::VerifyInput in{};
-        in.n_pairs = static_cast<int32_t>(n_pairs);
-        in.qpos = pk.qpos.data();
-        in.qnrm = pk.qnrm.data();
-        in.ppos = pk.ppos.data();
-        in.pnrm = pk.pnrm.data();
-        in.offq = pk.offq.data();
-        in.offp = pk.offp.data();
-        in.Ti = Ti;
-        in.Tj = Tj;
-        in.T = T;
-        in.epsilon = params->epsilon;
-        in.overlap_radius = params->overlap_radius;
-        in.d_max = params->d_max;
-        in.grid_cell = params->grid_cell > 0.0 ? params->grid_cell : params->d_max;
-        in.cos_max = std::cos(params->normal_angle_max);  // registration.cpp:61
-        in.full = 1;
-        std::vector<lkk::VerifyOutput> o(static_cast<size_t>(n_pairs));
-        cudaError_t e = lkk::verify_batch(in, o.data(), s);
-        release_stream(dev, s);
-        CK(e);
-        for (int64_t k = 0; k < n_pairs; ++k) {
-            lk_verify_result& r = out[k];
-            for (int q = 0; q < 36; ++q) r.info[q] = o[k].info[q];
-            r.pair_count = o[k].pair_count;
-            r.overlap_hits = o[k].overlap_hits;
-            const double np = static_cast<double>(clouds_j[k].n);
-            r.overlap = static_cast<double>(o[k].overlap_hits) / np;
-            r.inliers = o[k].inliers;
-            r.inlier_ratio = static_cast<double>(o[k].inliers) / np;
-            r.fitness = o[k].inliers > 0 ? o[k].sq_sum / static_cast<double>(o[k].inliers) : 0.0;
+        pack_pairs(clouds_i, clouds_j, n_pairs, true);  // validation in pair order, before any device work
+        std::vector<int> devs = call_devices(params->device, params->device_count);
+        const int G = static_cast<int>(std::min<int64_t>(static_cast<int64_t>(devs.size()), n_pairs));
+        if (G <= 1) {
+            verify_share(clouds_i, clouds_j, Ti, Tj, T, 0, n_pairs, params, devs[0], out);
+            return LK_OK;
         }
+        // the pairs are independent: contiguous shares, one host thread per device, no exchange
+        std::vector<std::thread> th;
+        std::vector<std::exception_ptr> errs(static_cast<size_t>(G));
+        for (int g = 0; g < G; ++g) {
+            const int64_t k0 = g * n_pairs / G, k1 = (g + 1) * n_pairs / G;
+            th.emplace_back([&, g, k0, k1] {
+                try {
+                    verify_share(clouds_i, clouds_j, Ti, Tj, T, k0, k1 - k0, params, devs[g], out);
+                } catch (...) {
+                    errs[g] = std::current_exception();
+                }
+            });
+        }
+        for (auto& t : th) t.join();
+        for (auto& e : errs)
+            if (e) std::rethrow_exception(e);
+        CK(cudaSetDevice(devs[0]));
         return LK_OK;
     });
 }

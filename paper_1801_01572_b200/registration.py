@@ -46,6 +46,9 @@ class RegistrationParams:
     seed: int = 0
     threads: int = 0
     device: int = -1
+    # GPUs of one call (include/loopkit_b200.h lk_reg_params.device_count):
+    # 0/1 = `device` alone, G = G devices from it, -1 = all visible
+    device_count: int = 0
 
     def resolved_max_fitness(self) -> float:
         return self.max_fitness if self.max_fitness is not None else self.d_max * self.d_max / 2.0
@@ -57,7 +60,7 @@ class RegistrationParams:
             min_inlier_ratio=self.min_inlier_ratio,
             max_fitness=-1.0 if self.max_fitness is None else float(self.max_fitness),
             normal_angle_max=self.normal_angle_max, seed=int(self.seed) & 0xFFFFFFFFFFFFFFFF,
-            threads=int(self.threads), device=int(self.device))
+            threads=int(self.threads), device=int(self.device), device_count=int(self.device_count))
 
 
 @dataclass
@@ -229,6 +232,25 @@ class RegistrationContext:
         return {"k_hyp_sample": t["k_hyp_sample"], "k_kabsch": t["k_kabsch"],
                 "k_score_cta": t["prep"] + t["score_a"] + t["score_b"] + t["score_tail"]}, runs.value
 
+    def attach_comm(self, unique_id: bytes, nranks: int, rank: int) -> None:
+        """One process per GPU: join the NCCL communicator of `unique_id`
+        (lk_nccl_unique_id on rank 0, broadcast by the caller); run_hypotheses
+        then runs this rank's share and merges over NCCL."""
+        buf = (C.c_uint8 * 128).from_buffer_copy(bytes(unique_id))
+        check(abi.lib().lk_reg_ctx_attach_comm(self._h, buf, int(nranks), int(rank)))
+
+    def run_exchange(self, params: "RegistrationParams", records_dev_ptr: int) -> None:
+        """This rank's share + the NCCL record exchange, asynchronous on the
+        context stream; leaves nranks lk_reg_records at records_dev_ptr."""
+        p = params.to_c()
+        check(abi.lib().lk_reg_run_exchange(self._h, C.byref(p), C.c_void_p(records_dev_ptr)))
+
+    def topology(self):
+        """(devices of this context, nranks, rank)"""
+        a, b, c = C.c_int32(), C.c_int32(), C.c_int32()
+        check(abi.lib().lk_reg_ctx_topology(self._h, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
+
     def download(self):
         """(source, target, cache, source_features, target_features) on the host."""
         ns, nt = self.n_source, self.n_target
@@ -253,6 +275,13 @@ class RegistrationContext:
     @property
     def cache(self) -> np.ndarray:
         return self.download()[2]
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte NCCL unique id for RegistrationContext.attach_comm (rank 0)."""
+    buf = (C.c_uint8 * 128)()
+    check(abi.lib().lk_nccl_unique_id(buf))
+    return bytes(buf)
 
 
 def prepare_registration(source_cloud: PointCloud, target_cloud: PointCloud,
@@ -516,6 +545,7 @@ class VerifyParams:
     grid_cell: float = 0.0  # <= 0 -> d_max
     normal_angle_max: float = 30.0 * math.pi / 180.0
     device: int = -1
+    device_count: int = 0  # G > 1: the pairs split over G devices from `device`; -1 = all visible
 
 
 @dataclass
@@ -538,7 +568,7 @@ def verify_batch(earlier: Sequence[PointCloud], later: Sequence[PointCloud], pos
     ti, tj, tm = _pack_transforms(pose_earlier), _pack_transforms(pose_later), _pack_transforms(measurement)
     cp = abi.lk_verify_params(epsilon=float(p.epsilon), overlap_radius=float(p.overlap_radius), d_max=float(p.d_max),
                               grid_cell=float(p.grid_cell), normal_angle_max=float(p.normal_angle_max),
-                              device=int(p.device), reserved=0)
+                              device=int(p.device), device_count=int(p.device_count))
     out = (abi.lk_verify_result * max(n, 1))()
     check(abi.lib().lk_verify_batch(ci.ctypes.data_as(C.POINTER(abi.lk_cloud)),
                                     cj.ctypes.data_as(C.POINTER(abi.lk_cloud)), ti.ctypes.data_as(abi.dptr),

@@ -26,7 +26,7 @@ def test_header_symbols_exported_and_bound():
     for s in syms:
         assert hasattr(L, s), f"missing export {s}"
     assert set(syms) == set(abi.SIGNATURES), set(syms) ^ set(abi.SIGNATURES)
-    assert abi.lib().lk_abi_version() == 1
+    assert abi.lib().lk_abi_version() == 2
 
 
 def test_library_is_sm100a_cuda_code():
