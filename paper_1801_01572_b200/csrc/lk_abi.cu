@@ -252,6 +252,15 @@ T* dev_upload(const T* host, size_t count, cudaStream_t s) {
     return d;
 }
 
+bool is_pinned(const void* p) {
+    cudaPointerAttributes a{};
+    if (!p || cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
 void check_cloud_ptr(const lk_cloud* c, const char* what) {
     if (!c) throw lk::Status(LK_INVALID_ARGUMENT, std::string(what) + ": null cloud");
     if (c->n < 0) throw lk::Status(LK_INVALID_ARGUMENT, std::string(what) + ": negative size");
@@ -476,8 +485,10 @@ void prepare_side(CloudSide& cs, double feature_radius, double normal_radius, do
     try {
         CK(cudaSetDevice(device));
         const int64_t n = cs.in->n;
-        cs.raw_pos = dev_upload(cs.in->xyz, 3 * n, cs.s);
-        cs.raw_nrm = cs.in->nxyz ? dev_upload(cs.in->nxyz, 3 * n, cs.s) : nullptr;
+        if (!cs.raw_pos) {  // not already enqueued by prepare_impl (pageable callers)
+            cs.raw_pos = dev_upload(cs.in->xyz, 3 * n, cs.s);
+            cs.raw_nrm = cs.in->nxyz ? dev_upload(cs.in->nxyz, 3 * n, cs.s) : nullptr;
+        }
         mark("upload");
         CK(lkk::pool_alloc(&cs.pos, 3 * n * sizeof(double), cs.s));
         CK(lkk::pool_alloc(&cs.nrm, 3 * n * sizeof(double), cs.s));
@@ -633,6 +644,23 @@ lk_status prepare_impl(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_pa
         lkk::pool_free(cs.raw_nrm, cs.s);
     };
     try {
+        // page-locked callers: the two uploads are enqueued here back to back,
+        // the target's first and the source's after it (an event orders them),
+        // so each gets the whole PCIe link and its side starts as soon as its
+        // own cloud has landed (two concurrent copies share the link and both
+        // land late). Pageable callers: each side's thread stages its own.
+        if (is_pinned(src->xyz) && is_pinned(tgt->xyz) && (!src->nxyz || is_pinned(src->nxyz)) &&
+            (!tgt->nxyz || is_pinned(tgt->nxyz))) {
+            T.raw_pos = dev_upload(tgt->xyz, 3 * tgt->n, T.s);
+            T.raw_nrm = tgt->nxyz ? dev_upload(tgt->nxyz, 3 * tgt->n, T.s) : nullptr;
+            cudaEvent_t landed;
+            CK(cudaEventCreateWithFlags(&landed, cudaEventDisableTiming));
+            CK(cudaEventRecord(landed, T.s));
+            CK(cudaStreamWaitEvent(S.s, landed, 0));
+            cudaEventDestroy(landed);
+            S.raw_pos = dev_upload(src->xyz, 3 * src->n, S.s);
+            S.raw_nrm = src->nxyz ? dev_upload(src->nxyz, 3 * src->n, S.s) : nullptr;
+        }
         // the two clouds are independent until the feature match: the target
         // side (H2D, downsample, FPFH, EvalGrid) runs on a second host thread
         // and stream while this thread does the source side
