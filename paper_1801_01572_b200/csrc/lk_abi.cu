@@ -252,6 +252,69 @@ T* dev_upload(const T* host, size_t count, cudaStream_t s) {
     return d;
 }
 
+// Pageable uploads (the drop-in caller's std::vector clouds): chunks are
+// copied by a few host threads into this thread's page-locked staging ring
+// and DMA'd from there, the copy of chunk k + 1 overlapping the DMA of chunk
+// k. (cudaMemcpyAsync from pageable memory stages through the driver's
+// single-threaded bounce buffer and blocks the host for the whole copy.)
+struct StageRing {
+    static constexpr size_t kChunk = size_t(4) << 20;
+    static constexpr int kSlots = 3;
+    char* buf[kSlots] = {};
+    cudaEvent_t ev[kSlots] = {};
+    bool used[kSlots] = {};
+    int dev = -1;
+    void bind(int device) {
+        if (!buf[0])
+            for (auto& b : buf) CK(cudaHostAlloc(reinterpret_cast<void**>(&b), kChunk, cudaHostAllocPortable));
+        if (dev != device) {
+            for (int k = 0; k < kSlots; ++k) {
+                if (ev[k]) {
+                    if (used[k]) cudaEventSynchronize(ev[k]);
+                    cudaEventDestroy(ev[k]);
+                }
+                CK(cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming));
+                used[k] = false;
+            }
+            dev = device;
+        }
+    }
+    ~StageRing() {
+        for (int k = 0; k < kSlots; ++k) {
+            if (ev[k]) {
+                cudaEventSynchronize(ev[k]);
+                cudaEventDestroy(ev[k]);
+            }
+            if (buf[k]) cudaFreeHost(buf[k]);
+        }
+    }
+};
+thread_local StageRing t_ring;
+
+void staged_upload(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    int device = 0;
+    CK(cudaGetDevice(&device));
+    StageRing& r = t_ring;
+    r.bind(device);
+    size_t off = 0;
+    for (int k = 0; off < bytes; k = (k + 1) % StageRing::kSlots) {
+        const size_t len = std::min(StageRing::kChunk, bytes - off);
+        if (r.used[k]) CK(cudaEventSynchronize(r.ev[k]));
+        const char* from = static_cast<const char*>(src) + off;
+        char* to = r.buf[k];
+        const int parts = len >= (size_t(1) << 20) ? 4 : 1;  // 8 (16 threads for two sides) measured slower
+#pragma omp parallel for num_threads(parts) schedule(static)
+        for (int q = 0; q < parts; ++q) {
+            const size_t a = len * q / parts, b = len * (q + 1) / parts;
+            std::memcpy(to + a, from + a, b - a);
+        }
+        CK(cudaMemcpyAsync(static_cast<char*>(dst) + off, to, len, cudaMemcpyHostToDevice, s));
+        CK(cudaEventRecord(r.ev[k], s));
+        r.used[k] = true;
+        off += len;
+    }
+}
+
 bool is_pinned(const void* p) {
     cudaPointerAttributes a{};
     if (!p || cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -485,9 +548,18 @@ void prepare_side(CloudSide& cs, double feature_radius, double normal_radius, do
     try {
         CK(cudaSetDevice(device));
         const int64_t n = cs.in->n;
-        if (!cs.raw_pos) {  // not already enqueued by prepare_impl (pageable callers)
-            cs.raw_pos = dev_upload(cs.in->xyz, 3 * n, cs.s);
-            cs.raw_nrm = cs.in->nxyz ? dev_upload(cs.in->nxyz, 3 * n, cs.s) : nullptr;
+        if (!cs.raw_pos) {  // not already enqueued by prepare_impl: a pageable caller
+            auto up = [&](const double* h) {
+                double* d = nullptr;
+                CK(lkk::pool_alloc(&d, std::max<int64_t>(3 * n, 1) * sizeof(double), cs.s));
+                if (n) {
+                    if (is_pinned(h)) CK(cudaMemcpyAsync(d, h, 3 * n * sizeof(double), cudaMemcpyHostToDevice, cs.s));
+                    else staged_upload(d, h, 3 * n * sizeof(double), cs.s);
+                }
+                return d;
+            };
+            cs.raw_pos = up(cs.in->xyz);
+            cs.raw_nrm = cs.in->nxyz ? up(cs.in->nxyz) : nullptr;
         }
         mark("upload");
         CK(lkk::pool_alloc(&cs.pos, 3 * n * sizeof(double), cs.s));
