@@ -99,6 +99,32 @@ def onchip_peaks():
         return None
 
 
+def ncu_roofline(kernels, bound):
+    """Roofline of an extras leg's dominant kernels from the committed ncu
+    capture (profiles/ncu_kernels.json; cold-cache, serialised launches):
+    bound "l2_gather" = L2 sectors x 32 B / kernel time against the measured
+    random-sector rate; bound "issue" = warp instructions / kernel time
+    against 4 per SM per cycle at the measured clock."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_kernels.json")) as f:
+            k = json.load(f)
+        oc = onchip_peaks() or {}
+        t = sum(k[n]["gpu__time_duration.sum"] for n in kernels) * 1e-9
+        if bound == "l2_gather":
+            achieved = sum(k[n]["lts__t_sectors.sum"] for n in kernels) * 32 / t / 1e9
+            peak, unit = oc.get("l2_random_gbs"), "GB/s"
+        else:
+            achieved = sum(k[n]["smsp__inst_executed.sum"] for n in kernels) / t / 1e9
+            peak, unit = 148 * 4 * 1.965, "G warp-instructions/s"
+        dram = sum(k[n]["dram__bytes_read.sum"] + k[n]["dram__bytes_write.sum"] for n in kernels)
+        return {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
+                "frac": achieved / peak if peak else None, "traffic": dram / max(1, len(kernels)),
+                "kernel": "+".join(kernels), "kernel_ms_ncu": t * 1e3,
+                "source": "profiles/ncu_kernels.json (ncu --metrics, cold-cache serialised launches)"}
+    except Exception as e:
+        return {"unavailable": str(e)[:120]}
+
+
 def ncu_traffic(kernels):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernels`
     from the committed ncu --set full capture, or None."""
@@ -326,7 +352,8 @@ def bench_icp(args):
            "icp_rmse": r.rmse, "icp_ms_per_iteration": 1e3 * best[1] / max(evaluated, 1),
            "icp_point_iterations_per_s": pair.source.size() * evaluated / best[1],
            "h2d_bytes": 2 * 48 * (pair.source.size() + pair.target.size()),
-           "timing": "wall clock of lk_register_global + lk_icp_point_to_plane from pinned host buffers, best of 3"}
+           "timing": "wall clock of lk_register_global + lk_icp_point_to_plane from pinned host buffers, best of 3",
+           "roofline": ncu_roofline(["k_icp_nn"], "issue")}
     if not args.no_cpu_baseline:
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         import oracle as O
@@ -374,7 +401,9 @@ def bench_b2(args):
                        "rot +-2, trans +-1) = 3,375 of the 10^6-candidate lattice, early exit on",
            "candidates": int(rt.shape[0]), "source_points": pair.source.size(), "target_points": pair.target.size(),
            "evals": evals, "ms": 1e3 * dt, "evals_per_s": evals / dt, "qualified": sc.qualified,
-           "timing": "wall clock of lk_score_candidates (candidates H2D, scoring, per-candidate results D2H)"}
+           "timing": "wall clock of lk_score_candidates (candidates H2D, scoring, per-candidate results D2H)",
+           "full_lattice": "tools/b2_full.py: all 10^6 candidates device-side, profiles/r02_b2_full.json",
+           "roofline": ncu_roofline(["k_score_list_ring"], "issue")}
     if not args.no_cpu_baseline:
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         import oracle as O
@@ -488,7 +517,8 @@ def bench_verification(args):
            "mean_inlier_ratio": float(np.mean([o.inlier_ratio for o in out])),
            "h2d_bytes": 48 * npts,
            "timing": "wall clock of lk_verify_batch from pinned host buffers (H2D, 3K ring grids, queries, "
-                     "sums), best of 5"}
+                     "sums), best of 5",
+           "roofline": ncu_roofline(["k_verify_src", "k_verify_edge"], "l2_gather")}
     if not args.no_cpu_baseline:
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         import oracle as O

@@ -1701,19 +1701,22 @@ bool residual_twist(const double* Ti, const double* Tj, const double* rel, doubl
     return true;
 }
 
-// xi . (Lambda xi): rows of Lambda xi accumulated in column order, then the
-// dot in index order (Eigen's packet order may differ in the last bits; the
-// accept decision l >= threshold is not that sensitive)
+// xi.dot(info * xi) (line_process.cpp:39) in Eigen 3.4's SSE2 order (the rules
+// of oracle/ref_shim/Eigen/Dense, checked against the reference build in
+// tests/test_ref_parity.py): the Mat6 * Vec6 lazy product evaluates all six
+// rows as packets, k in order (m_i0 x0 + m_i1 x1) + ...; the Vec6 dot reduces
+// three packets by halving, lane-wise, then adds the two lanes:
+// (p0 + (p2 + p4)) + (p1 + (p3 + p5)) with p_k = xi_k y_k.
 double quad_form(const double* info36, const double xi[6]) {
     double y[6];
     for (int i = 0; i < 6; ++i) {
         double a = info36[6 * i] * xi[0];
-        for (int k = 1; k < 6; ++k) a += info36[6 * i + k] * xi[k];
+        for (int k = 1; k < 6; ++k) a = info36[6 * i + k] * xi[k] + a;
         y[i] = a;
     }
-    double f = xi[0] * y[0];
-    for (int k = 1; k < 6; ++k) f += xi[k] * y[k];
-    return f;
+    double p[6];
+    for (int k = 0; k < 6; ++k) p[k] = xi[k] * y[k];
+    return (p[0] + (p[2] + p[4])) + (p[1] + (p[3] + p[5]));
 }
 
 double update_weight(double f, double mu) {  // line_process.cpp:42-46

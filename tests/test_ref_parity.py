@@ -267,3 +267,30 @@ def test_propose_loops_golden_from_reference():
     got = RF.propose_loops(clouds, poses, loops=g["loops"], overlap_radius=g["overlap_radius"],
                            min_overlap=g["min_overlap"])
     assert [(i, j, float(o).hex()) for i, j, o in got] == [tuple(x) for x in g["proposals"]]
+
+
+def test_edge_residual_and_weight_equal_reference():
+    """line_process.cpp:35-46 (host side of the product, lk_edge_residual /
+    lk_update_weight) against the reference build bit for bit, including the
+    Eigen-order quadratic form xi.dot(info * xi)."""
+    import paper_1801_01572_b200 as lk
+    rng = np.random.default_rng(41)
+    n_cmp = 0
+    for k in range(400):
+        Ri, ti = RF.random_transform(1000 + k, 0, 0.6, 1.0)
+        Rj, tj = RF.random_transform(2000 + k, 0, 0.6, 1.0)
+        Rr, tr = RF.random_transform(3000 + k, 0, 0.6, 1.0)
+        A = rng.normal(size=(6, 6))
+        info = A @ A.T * rng.uniform(1, 1e4)
+        try:
+            want = RF.edge_residual(Ri, ti, Rj, tj, Rr, tr, info, 100)
+        except RF.RefError:
+            with pytest.raises(lk.Error):
+                lk.edge_residual(lk.RigidTransform(Ri, ti), lk.RigidTransform(Rj, tj), lk.RigidTransform(Rr, tr), info)
+            continue
+        got = lk.edge_residual(lk.RigidTransform(Ri, ti), lk.RigidTransform(Rj, tj), lk.RigidTransform(Rr, tr), info)
+        assert float(got).hex() == float(want).hex(), k
+        n_cmp += 1
+        mu = float(rng.uniform(0.1, 50))
+        assert lk.update_weight(got, mu) == RF.lib().rf_update_weight(want, mu)
+    assert n_cmp > 50
