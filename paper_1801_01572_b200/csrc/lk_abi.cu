@@ -6,6 +6,7 @@
 // concurrent calls on a shared context stay safe as in the reference.
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <array>
@@ -49,6 +50,16 @@ inline void nk(ncclResult_t r, const char* where) {
     if (r != ncclSuccess) throw lk::Status(LK_NCCL_ERROR, std::string(where) + ": " + ncclGetErrorString(r));
 }
 #define NK(x) nk((x), #x)
+
+// NVTX ranges around every ABI phase (header-only NVTX v3: free when no tool
+// is attached; nsys / ncu --nvtx show the prepare sides, the hypotheses and
+// the exchanges by name)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 template <class F>
 lk_status guarded(F&& fn) {
@@ -536,6 +547,7 @@ struct CloudSide {
 
 void prepare_side(CloudSide& cs, double feature_radius, double normal_radius, double leaf, lkk::GridStorage* grid,
                   double d_max, int device, double t0, const char* tag, cudaStream_t grid_stream = nullptr) {
+    NvtxRange range(tag[0] == 's' ? "lk prepare source side" : "lk prepare target side");
     auto mark = [&](const char* what) {
         if (trace_level() >= 2) {
             tmark((std::string(tag) + " " + what).c_str(), cs.s, t0);
@@ -647,6 +659,7 @@ std::vector<int> call_devices(int32_t device, int32_t device_count) {
 // records and the EvalGrid rebuilt on each replica from the broadcast target
 // (deterministic: bit-identical to device 0's), one exchange buffer per rank.
 void make_peers(lk_reg_ctx* c, const std::vector<int>& devs, double d_max) {
+    NvtxRange range("lk replicate context (ncclBroadcast)");
     const int G = static_cast<int>(devs.size());
     std::vector<ncclComm_t> comms(G);
     NK(ncclCommInitAll(comms.data(), G, devs.data()));
@@ -696,6 +709,7 @@ void make_peers(lk_reg_ctx* c, const std::vector<int>& devs, double d_max) {
 }
 
 lk_status prepare_impl(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_params* params, lk_reg_ctx** out) {
+    NvtxRange range("lk_reg_prepare");
     if (!params || !out) return fail(LK_INVALID_ARGUMENT, "null argument");
     check_cloud_ptr(src, "source");
     check_cloud_ptr(tgt, "target");
@@ -791,6 +805,7 @@ lk_status prepare_impl(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_pa
 }
 
 lk_status run_range_impl(lk_reg_ctx* c, const lk_reg_params& p, int64_t begin, int64_t end, void* d_record) {
+    NvtxRange range("lk run_hypotheses range");
     if (c->ns < 4) return fail(LK_TOO_FEW_POINTS, "sample_quadruple: need >= 4 source points");
     if (!c->d_cache) return fail(LK_MISSING_DATA, "sample_quadruple: no correspondence cache");
     if (begin < 0 || end < begin) return fail(LK_INVALID_ARGUMENT, "bad hypothesis range");
@@ -815,6 +830,7 @@ lk_status run_range_impl(lk_reg_ctx* c, const lk_reg_params& p, int64_t begin, i
 // one writer); single-process G-device contexts drive all ranks from here,
 // a multi-process rank drives its own. Leaves the records on c's device.
 lk_status exchange_run(lk_reg_ctx* c, const lk_reg_params& p) {
+    NvtxRange range("lk shares + ncclAllReduce of rank records");
     const int G = c->nranks;
     const int64_t H = p.hypothesis_count;
     const size_t words = G * sizeof(lk_reg_record) / sizeof(int64_t);
@@ -1326,6 +1342,7 @@ lk_status lk_propose_loops(const lk_cloud* fragments, const double* poses, int32
             if (!(params->overlap_radius > 0.0))
                 return fail(LK_INVALID_ARGUMENT, "build_grid: cell_length must be positive");
         }
+        NvtxRange range("lk_propose_loops");
         std::vector<int64_t> foff(static_cast<size_t>(n) + 1, 0);
         for (int32_t f = 0; f < n; ++f) foff[f + 1] = foff[f] + fragments[f].n;
         std::vector<double> xyz(static_cast<size_t>(3 * foff[n]));
@@ -1406,6 +1423,7 @@ lk_status lk_edge_info_batched(const lk_cloud* clouds_i, const lk_cloud* clouds_
 void verify_share(const lk_cloud* clouds_i, const lk_cloud* clouds_j, const double* Ti, const double* Tj,
                   const double* T, int64_t k0, int64_t K, const lk_verify_params* params, int dev,
                   lk_verify_result* out) {
+    NvtxRange range("lk verify share");
     PackedPairs pk = pack_pairs(clouds_i + k0, clouds_j + k0, K, true);
     CK(cudaSetDevice(dev));
     cudaStream_t s = acquire_stream(dev);
