@@ -206,8 +206,25 @@ __device__ __forceinline__ void ring_top3_sel(float d2, int32_t o, float& f1, fl
     f1 = c1 ? d2 : f1;
 }
 
+// Cells c along one axis whose entries ([c - delta, c + 1 + delta]) can lie
+// within h of q: c in [lo, hi]. h carries a relative and an absolute slack
+// over sqrt(rem) so that every cell the per-cell FP32 test
+// (gap^2 + rest <= bound) would pass is inside: the range is a superset.
+__device__ __forceinline__ void ring_reach(float q, float dl, float rem, float bnd, int& lo, int& hi) {
+    const float h = sqrtf(fmaxf(rem, 0.0f) * 1.0001f + bnd * 1e-5f) + 1e-3f;
+    lo = static_cast<int>(ceilf(q - dl - h - 1.0f));
+    hi = static_cast<int>(floorf(q + dl + h));
+}
+
 // Visits the cells of shell r around the box [b0, b1] (r = 0: the box) that
 // some participating lane's bound reaches; visit(ax, ay, az, o) per entry.
+// Row by row: each lane turns its bound into the z range of cells it can
+// reach in the (x, y) row, the warp takes the hull of those ranges, and the
+// hull's entries -- contiguous in the CSR -- are streamed with two start[]
+// reads per row instead of a box test and two reads per cell (empty cells
+// cost nothing). Rows strictly inside the shell only add their Z0 / Z1 cells.
+// The y range per x is pruned the same way. Hulls are supersets of the
+// per-cell test, which keeps every decision (see ring_nn_warp).
 template <class B, class F>
 __device__ __forceinline__ void warp_shell(const RingGrid& rg, float qx, float qy, float qz, bool part, const int* b0,
                                            const int* b1, int r, float4* wbuf, B&& bound, F&& visit) {
@@ -218,36 +235,54 @@ __device__ __forceinline__ void warp_shell(const RingGrid& rg, float qx, float q
         const float lo = static_cast<float>(c) - dl, hi = static_cast<float>(c + 1) + dl;
         return q < lo ? lo - q : (q > hi ? q - hi : 0.0f);
     };
+    auto scan = [&](int64_t row, int za, int zb) {
+        const int32_t s0 = __ldg(rg.start + row + za), s1 = __ldg(rg.start + row + zb + 1);
+        for (int32_t base = s0; base < s1; base += 32) {
+            // stage 32 entries (one coalesced load), read back as broadcasts
+            const int32_t e = base + lane;
+            __syncwarp();
+            if (e < s1) wbuf[lane] = __ldg(rg.pts + e);
+            __syncwarp();
+            const int cnt = s1 - base < 32 ? s1 - base : 32;
+            for (int k = 0; k < cnt; ++k) {
+                const float4 A = wbuf[k];
+                visit(A.x, A.y, A.z, __float_as_int(A.w));
+            }
+        }
+    };
     const int X0 = b0[0] - r, X1 = b1[0] + r, Y0 = b0[1] - r, Y1 = b1[1] + r, Z0 = b0[2] - r, Z1 = b1[2] + r;
     const int xa = X0 > 0 ? X0 : 0, xb = X1 < rg.nx - 1 ? X1 : rg.nx - 1;
     const int ya = Y0 > 0 ? Y0 : 0, yb = Y1 < rg.ny - 1 ? Y1 : rg.ny - 1;
+    const int za = Z0 > 0 ? Z0 : 0, zb = Z1 < rg.nz - 1 ? Z1 : rg.nz - 1;
+    if (za > zb) return;
     for (int x = xa; x <= xb; ++x) {
         const float gx = gap(qx, x);
-        if (!__any_sync(full, part && gx * gx <= bound())) continue;
+        const float bx = bound();
+        const bool okx = part && gx * gx <= bx;
+        if (!__any_sync(full, okx)) continue;
         const bool xe = r == 0 || x == X0 || x == X1;
-        for (int y = ya; y <= yb; ++y) {
+        int ly, hy;
+        ring_reach(qy, dl, bx - gx * gx, bx, ly, hy);
+        int y0 = __reduce_min_sync(full, okx ? ly : INT32_MAX), y1 = __reduce_max_sync(full, okx ? hy : INT32_MIN);
+        y0 = y0 > ya ? y0 : ya;
+        y1 = y1 < yb ? y1 : yb;
+        for (int y = y0; y <= y1; ++y) {
             const float gy = gap(qy, y);
             const float gxy = gx * gx + gy * gy;
-            if (!__any_sync(full, part && gxy <= bound())) continue;
-            const bool edge = xe || y == Y0 || y == Y1;
+            const float bxy = bound();
+            const bool ok = part && gxy <= bxy;
+            if (!__any_sync(full, ok)) continue;
+            int lz, hz;
+            ring_reach(qz, dl, bxy - gxy, bxy, lz, hz);
             const int64_t row = (static_cast<int64_t>(x) * rg.ny + y) * rg.nz;
-            for (int z = Z0; z <= Z1; z = (edge || z == Z1) ? z + 1 : Z1) {
-                if (z < 0 || z >= rg.nz) continue;
-                const float gz = gap(qz, z);
-                if (!__any_sync(full, part && gxy + gz * gz <= bound())) continue;
-                const int32_t s0 = __ldg(rg.start + row + z), s1 = __ldg(rg.start + row + z + 1);
-                for (int32_t base = s0; base < s1; base += 32) {
-                    // stage 32 entries (one coalesced load), read back as broadcasts
-                    const int32_t e = base + lane;
-                    __syncwarp();
-                    if (e < s1) wbuf[lane] = __ldg(rg.pts + e);
-                    __syncwarp();
-                    const int cnt = s1 - base < 32 ? s1 - base : 32;
-                    for (int k = 0; k < cnt; ++k) {
-                        const float4 A = wbuf[k];
-                        visit(A.x, A.y, A.z, __float_as_int(A.w));
-                    }
-                }
+            if (xe || y == Y0 || y == Y1) {
+                int z0 = __reduce_min_sync(full, ok ? lz : INT32_MAX), z1 = __reduce_max_sync(full, ok ? hz : INT32_MIN);
+                z0 = z0 > za ? z0 : za;
+                z1 = z1 < zb ? z1 : zb;
+                if (z0 <= z1) scan(row, z0, z1);
+            } else {
+                if (Z0 >= 0 && __any_sync(full, ok && lz <= Z0 && Z0 <= hz)) scan(row, Z0, Z0);
+                if (Z1 < rg.nz && __any_sync(full, ok && lz <= Z1 && Z1 <= hz)) scan(row, Z1, Z1);
             }
         }
     }
