@@ -65,3 +65,15 @@ for key in ("sec", "stall"):
         text = text_of(ln)
         print(f"  sec {100 * v['sec'] / max(tot['sec'], 1):5.1f}%  stall {100 * v['stall'] / max(tot['stall'], 1):5.1f}%"
               f"  inst {100 * v['inst'] / max(tot['inst'], 1):5.1f}%  {text}")
+
+# optional: LINE_RANGES="lk_ring.cuh:14-50,lk_ring.cuh:200-360" sums the
+# metrics of each source-line range
+for spec in filter(None, __import__("os").environ.get("LINE_RANGES", "").split(",")):
+    fname, rng = spec.split(":")
+    a, b = (int(x) for x in rng.split("-"))
+    s = collections.Counter()
+    for ln, v in agg.items():
+        if ln and ln[0].endswith(fname) and a <= ln[1] <= b:
+            s.update(v)
+    print(f"range {spec:28s} sec {100 * s['sec'] / max(tot['sec'], 1):5.1f}%  stall "
+          f"{100 * s['stall'] / max(tot['stall'], 1):5.1f}%  inst {100 * s['inst'] / max(tot['inst'], 1):5.1f}%")
