@@ -1624,10 +1624,17 @@ __global__ void __launch_bounds__(kCtaThreads, 3) k_score_list_ring(SourceView s
                 S.inl[0][threadIdx.x] = 0u;
                 S.miss[0][threadIdx.x] = 0u;
             }
+            if (threadIdx.x == 0) S.next = 0;
             __syncthreads();
+            // warps take the round's 32-point Morton runs dynamically: walk
+            // costs vary by run, so static shares leave warps at the barrier
 #pragma unroll 1
-            for (int u = 0; u < kCtaPer; ++u) {
-                const int64_t t = base + u * kCtaThreads + threadIdx.x;
+            for (;;) {
+                int run = 0;
+                if (lane == 0) run = atomicAdd(&S.next, 1);
+                run = __shfl_sync(0xffffffffu, run, 0);
+                if (run >= kCtaPts / 32) break;
+                const int64_t t = base + run * 32 + lane;
                 const bool act = t < ns;
                 const int64_t i = act ? static_cast<int64_t>(__ldg(order + t)) : 0;
                 const int local = static_cast<int>(i - base);
