@@ -3,8 +3,9 @@
 // The EvalGrid's 3x3x3 block lists grow with the square of the target density
 // (a 640x480-rendered submap puts ~150 points in a 5 cm cell, ~4000 in its
 // block). The ring grid instead bins the target into small cells (dense CSR
-// over the bounding box, cell ~ d_max / 6 within a memory cap) and answers a
-// query by scanning cube shells of cells around it in FP32, stopping as soon
+// over the bounding box, cell d_max / 5 coarsened for sparse targets, within a
+// memory cap) and answers a query by scanning cube shells of cells around it
+// in FP32, stopping as soon
 // as no unscanned entry can be nearer (or tie), then deciding in FP64:
 //   * FP32 keeps the three smallest d2; the stop test and the FP64 re-check
 //     use guard bands sized from the conversion error of both coordinates;
@@ -84,6 +85,17 @@ __global__ void k_ring_count(const double* __restrict__ p, int64_t n, RingGrid r
     const int64_t c = (static_cast<int64_t>(cx) * rg.ny + cy) * rg.nz + cz;
     cell_of[i] = static_cast<int32_t>(c);
     atomicAdd(counts + c, 1);
+}
+
+// sum over points of their cell's count (= sum over cells of count^2)
+__global__ void k_ring_occupancy(const int32_t* __restrict__ cell_of, int64_t n, const int32_t* __restrict__ counts,
+                                 unsigned long long* __restrict__ out) {
+    unsigned long long acc = 0;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        acc += static_cast<unsigned long long>(counts[cell_of[i]]);
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
 }
 
 __global__ void k_ring_scatter(const double* __restrict__ p, int64_t n, RingGrid rg,
@@ -170,13 +182,14 @@ __global__ void k_morton(const double* __restrict__ p, int64_t n, int64_t block,
     idx[i] = static_cast<int32_t>(i);
 }
 
-// ring cells of d_max / LK_RING_DIV (default 5) for single dense grids
+// ring cells of d_max / LK_RING_DIV for single dense grids; unset (0): d_max
+// / 5, coarsened to the occupancy target (build_ring_grid)
 double ring_divisor() {
-    static double cached = 0.0;
-    if (cached == 0.0) {
+    static double cached = -1.0;
+    if (cached < 0.0) {
         const char* e = std::getenv("LK_RING_DIV");
         const double v = e ? std::atof(e) : 0.0;
-        cached = v >= 1.0 && v <= 64.0 ? v : 5.0;
+        cached = v >= 1.0 && v <= 64.0 ? v : 0.0;
     }
     return cached;
 }
@@ -404,15 +417,46 @@ cudaError_t build_ring_grid(RingStorage& rs, const double* d_pos, int64_t n, dou
     }
     // at most 64 cells per point (and 2^28 overall)
     const int64_t cap = std::min<int64_t>(std::max<int64_t>(64 * n, 4096), int64_t(1) << 28);
-    RingGrid v = ring_frame(lo, hi, d_max, -1.0, cap, fast, ring_divisor());
+    const double fixed_div = ring_divisor();
+    RingGrid v = ring_frame(lo, hi, d_max, -1.0, cap, fast, fixed_div > 0.0 ? fixed_div : 5.0);
     int64_t nc = v.ncells;
     int32_t *cell_of = nullptr, *counts = nullptr;
     RG_TRY(cudaMallocAsync(&cell_of, n * sizeof(int32_t), stream));
     RG_TRY(cudaMallocAsync(&counts, nc * sizeof(int32_t), stream));
-    RG_TRY(pool_alloc(&rs.start, (nc + 1) * sizeof(int32_t), stream));
-    RG_TRY(pool_alloc(&rs.pts, n * sizeof(float4), stream));
     RG_TRY(cudaMemsetAsync(counts, 0, nc * sizeof(int32_t), stream));
     k_ring_count<<<nblocks(n, 256), 256, 0, stream>>>(d_pos, n, v, cell_of, counts);
+    if (fixed_div <= 0.0) {
+        // The walk's cost is a fixed cost per (x, y) row plus a cost per
+        // entry; sparse targets (few points per occupied cell) pay mostly
+        // rows. Coarsen until a point's cell holds ~kRingOccupancy entries
+        // (point-weighted mean, measured; surfaces scale it with the cell
+        // area), never beyond d_max / 2.5. Measured on B200: the B2 frame
+        // (13.7 at d_max / 5) runs 1.4x faster at d_max / 3 (43); the 2.4M
+        // submap of config D (51 at d_max / 5) is left alone.
+        constexpr double kRingOccupancy = 40.0;
+        unsigned long long* d_occ = nullptr;
+        RG_TRY(cudaMallocAsync(&d_occ, sizeof(unsigned long long), stream));
+        RG_TRY(cudaMemsetAsync(d_occ, 0, sizeof(unsigned long long), stream));
+        k_ring_occupancy<<<std::min<unsigned>(nblocks(n, 256), 592), 256, 0, stream>>>(cell_of, n, counts, d_occ);
+        auto* h_occ = static_cast<unsigned long long*>(host_scratch(sizeof(unsigned long long)));
+        if (!h_occ) return cudaErrorMemoryAllocation;
+        RG_TRY(cudaMemcpyAsync(h_occ, d_occ, sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream));
+        RG_TRY(cudaStreamSynchronize(stream));
+        cudaFreeAsync(d_occ, stream);
+        const double occ = static_cast<double>(*h_occ) / static_cast<double>(n);
+        if (occ < kRingOccupancy) {
+            const double div = std::max(2.5, (d_max / v.cell) / std::sqrt(kRingOccupancy / occ));
+            if (d_max / v.cell - div > 0.25) {
+                v = ring_frame(lo, hi, d_max, -1.0, cap, fast, div);
+                if (v.ncells > nc) return cudaErrorInvalidValue;  // coarser never has more cells
+                nc = v.ncells;
+                RG_TRY(cudaMemsetAsync(counts, 0, nc * sizeof(int32_t), stream));
+                k_ring_count<<<nblocks(n, 256), 256, 0, stream>>>(d_pos, n, v, cell_of, counts);
+            }
+        }
+    }
+    RG_TRY(pool_alloc(&rs.start, (nc + 1) * sizeof(int32_t), stream));
+    RG_TRY(pool_alloc(&rs.pts, n * sizeof(float4), stream));
     RG_TRY(exclusive_scan(counts, nc, rs.start, stream));
     RG_TRY(cudaMemsetAsync(counts, 0, nc * sizeof(int32_t), stream));
     v.start = rs.start;

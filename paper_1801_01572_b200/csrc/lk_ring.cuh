@@ -211,7 +211,10 @@ __device__ __forceinline__ void ring_top3_sel(float d2, int32_t o, float& f1, fl
 // over sqrt(rem) so that every cell the per-cell FP32 test
 // (gap^2 + rest <= bound) would pass is inside: the range is a superset.
 __device__ __forceinline__ void ring_reach(float q, float dl, float rem, float bnd, int& lo, int& hi) {
-    const float h = sqrtf(fmaxf(rem, 0.0f) * 1.0001f + bnd * 1e-5f) + 1e-3f;
+    // sqrt.approx (relative error ~2^-22) is far inside the slack
+    float h;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(h) : "f"(fmaxf(rem, 0.0f) * 1.0001f + bnd * 1e-5f));
+    h += 1e-3f;
     lo = static_cast<int>(ceilf(q - dl - h - 1.0f));
     hi = static_cast<int>(floorf(q + dl + h));
 }
