@@ -49,6 +49,7 @@ __device__ __forceinline__ double butterfly(double v) {
 
 // The nearest neighbours of one iteration, queries in the source's Morton
 // order (perm) so that a warp's walks share cells; nn[i] = -1 for no match.
+// nn holds the previous iteration's matches on entry (seeds of the walks).
 __global__ void __launch_bounds__(kIcpThreads) k_icp_nn(const double4* __restrict__ pos4,
                                                         const int32_t* __restrict__ perm, int64_t n,
                                                         const __grid_constant__ RingGrid rg, double d2_max,
@@ -62,7 +63,9 @@ __global__ void __launch_bounds__(kIcpThreads) k_icp_nn(const double4* __restric
     const bool act = t < n;
     const int32_t i = act ? __ldg(perm + t) : 0;
     const V3 y = act ? xform(s_R, s_R + 9, ld4(pos4, i)) : mk(0.0, 0.0, 0.0);
-    const int32_t j = ring_nn_warp(rg, y, d2_max, act, s_buf[threadIdx.x >> 5]);  // warp-uniform call
+    // seeded with the previous iteration's match (nn starts at -1)
+    const int32_t prev = act ? __ldg(nn + i) : -1;
+    const int32_t j = ring_nn_warp(rg, y, d2_max, act, s_buf[threadIdx.x >> 5], prev);  // warp-uniform call
     if (act) nn[i] = j;
 }
 
@@ -284,6 +287,7 @@ cudaError_t icp_point_to_plane(const double* d_src, int64_t n, const RingStorage
     ICP_TRY(pool_alloc(&st, sizeof(IcpState), stream));
     ICP_TRY(pool_alloc(&perm, n * sizeof(int32_t), stream));
     ICP_TRY(pool_alloc(&nn, n * sizeof(int32_t), stream));
+    ICP_TRY(cudaMemsetAsync(nn, 0xff, n * sizeof(int32_t), stream));  // no seeds in the first iteration
     ICP_TRY(make_records(d_src, nullptr, n, pos4, nullptr, stream));
     ICP_TRY(spatial_order(d_src, n, perm, stream));
     ICP_TRY(cudaMemsetAsync(counts, 0, (iters + 1) * sizeof(unsigned long long), stream));

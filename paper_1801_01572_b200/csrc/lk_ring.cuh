@@ -106,6 +106,19 @@ __device__ __forceinline__ void ring_top3(float d2, int32_t o, float& f1, float&
     }
 }
 
+// FP32 d2 up to which an entry may still be the FP64 nearest (or tie it),
+// given the FP32 best f1: the guard band of lk_ring.cu's ring_frame, but for
+// distances up to D = sqrt(f1 + band) (every such entry, and the FP32 best
+// itself, is within D) instead of the walk's worst case rmax + 1 cells -- so
+// the FP64 candidate set, and the re-scans when it exceeds two, stay small.
+__device__ __forceinline__ float ring_lim(const RingGrid& rg, float f1) {
+    if (!(rg.band < 1e29f)) return f1 + 2.0f * rg.band;  // FP64-only mode: every entry within d_max
+    const float D = sqrtf(f1 + rg.band) * 1.001f + 1e-4f;
+    const float e = 4.0f * (2.0f * 1.7320508f * D * rg.delta + 3.0f * rg.delta * rg.delta +
+                            4.0f * 5.9604645e-8f * D * D) + 1e-6f;
+    return f1 + 2.02f * e;
+}
+
 // Original index of the reference EvalGrid neighbour of y within d_max, or -1.
 __device__ __forceinline__ int32_t ring_nn(const RingGrid& rg, lkd::V3 y, double d2_max) {
     using namespace lkd;
@@ -157,7 +170,7 @@ __device__ __forceinline__ int32_t ring_nn(const RingGrid& rg, lkd::V3 y, double
             best = o;
         }
     };
-    const float lim = f1 + 2.0f * rg.band;
+    const float lim = ring_lim(rg, f1);
     if (f3 <= lim) {
         auto lim_bound = [&]() { return lim; };
         for (int r = k0; r <= r_end; ++r)
@@ -291,9 +304,13 @@ __device__ __forceinline__ void warp_shell(const RingGrid& rg, float qx, float q
     }
 }
 
-// wbuf: 32 float4 of shared memory owned by the calling warp.
+// wbuf: 32 float4 of shared memory owned by the calling warp. hint: an entry
+// (original index) likely near y -- e.g. the previous ICP iteration's match --
+// or -1. It seeds the top three, so the bound starts at its distance instead
+// of d_max and the box scan is pruned from the first row; any entry is a
+// valid seed (it is a real candidate, and the walk skips it once).
 __device__ __forceinline__ int32_t ring_nn_warp(const RingGrid& rg, lkd::V3 y, double d2_max, bool active,
-                                                float4* wbuf) {
+                                                float4* wbuf, int32_t hint = -1) {
     using namespace lkd;
     constexpr unsigned full = 0xffffffffu;
     bool live = active;
@@ -338,13 +355,23 @@ __device__ __forceinline__ int32_t ring_nn_warp(const RingGrid& rg, lkd::V3 y, d
     const float inf = __int_as_float(0x7f800000);
     float f1 = inf, f2 = inf, f3 = inf;
     int32_t o1 = -1, o2 = -1;
+    const int32_t seed = live && hint >= 0 && hint < rg.npoints ? hint : -1;
+    if (seed >= 0) {  // the same FP32 cell coordinates as the entry's (k_ring_scatter)
+        const V3 p = ld4(rg.pos4, seed);
+        const float dx = qx - static_cast<float>((p.x - rg.ox) / rg.cell);
+        const float dy = qy - static_cast<float>((p.y - rg.oy) / rg.cell);
+        const float dz = qz - static_cast<float>((p.z - rg.oz) / rg.cell);
+        f1 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+        o1 = seed;
+    }
     auto bound = [&]() { return fminf(f1 + 2.0f * rg.band, rg.thr + rg.band); };
     int r_end = 0;
     // r = rmax covers every lane's own walk (its cell +- rmax)
     for (int r = 0; r <= rg.rmax; ++r) {
         warp_shell(rg, qx, qy, qz, live, b0, b1, r, wbuf, bound, [&](float ax, float ay, float az, int32_t o) {
             const float dx = qx - ax, dy = qy - ay, dz = qz - az;
-            ring_top3_sel(fmaf(dx, dx, fmaf(dy, dy, dz * dz)), o, f1, f2, f3, o1, o2);
+            const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+            ring_top3_sel(o == seed ? inf : d2, o, f1, f2, f3, o1, o2);
         });
         r_end = r;
         // entries outside the scanned box lie >= m - delta cells from the query
@@ -355,7 +382,7 @@ __device__ __forceinline__ int32_t ring_nn_warp(const RingGrid& rg, lkd::V3 y, d
         if (__all_sync(full, !live || (m > 0.0f && m * m > bound()))) break;
     }
     const bool hit = live && f1 <= rg.thr + rg.band;
-    const float lim = f1 + 2.0f * rg.band;
+    const float lim = ring_lim(rg, f1);
     double best_d2 = __longlong_as_double(0x7ff0000000000000ll);
     int32_t best = INT32_MAX;
     auto consider = [&](int32_t o) {
