@@ -233,7 +233,8 @@ __device__ __forceinline__ void ring_reach(float q, float dl, float rem, float b
 }
 
 // Visits the cells of shell r around the box [b0, b1] (r = 0: the box) that
-// some participating lane's bound reaches; visit(ax, ay, az, o) per entry.
+// some participating lane's bound reaches; visit(chunk, cnt) per staged chunk
+// of up to 32 entries (chunk: x[32] y[32] z[32] index[32] in shared memory).
 // Row by row: each lane turns its bound into the z range of cells it can
 // reach in the (x, y) row, the warp takes the hull of those ranges, and the
 // hull's entries -- contiguous in the CSR -- are streamed with two start[]
@@ -251,19 +252,22 @@ __device__ __forceinline__ void warp_shell(const RingGrid& rg, float qx, float q
         const float lo = static_cast<float>(c) - dl, hi = static_cast<float>(c + 1) + dl;
         return q < lo ? lo - q : (q > hi ? q - hi : 0.0f);
     };
+    float* xs = reinterpret_cast<float*>(wbuf);  // staged chunk, SoA: x[32] y[32] z[32] index[32]
     auto scan = [&](int64_t row, int za, int zb) {
         const int32_t s0 = __ldg(rg.start + row + za), s1 = __ldg(rg.start + row + zb + 1);
         for (int32_t base = s0; base < s1; base += 32) {
             // stage 32 entries (one coalesced load), read back as broadcasts
             const int32_t e = base + lane;
             __syncwarp();
-            if (e < s1) wbuf[lane] = __ldg(rg.pts + e);
-            __syncwarp();
-            const int cnt = s1 - base < 32 ? s1 - base : 32;
-            for (int k = 0; k < cnt; ++k) {
-                const float4 A = wbuf[k];
-                visit(A.x, A.y, A.z, __float_as_int(A.w));
+            if (e < s1) {
+                const float4 A = __ldg(rg.pts + e);
+                xs[lane] = A.x;
+                xs[32 + lane] = A.y;
+                xs[64 + lane] = A.z;
+                xs[96 + lane] = A.w;
             }
+            __syncwarp();
+            visit(xs, s1 - base < 32 ? s1 - base : 32);
         }
     };
     const int X0 = b0[0] - r, X1 = b1[0] + r, Y0 = b0[1] - r, Y1 = b1[1] + r, Z0 = b0[2] - r, Z1 = b1[2] + r;
@@ -302,6 +306,16 @@ __device__ __forceinline__ void warp_shell(const RingGrid& rg, float qx, float q
             }
         }
     }
+}
+
+// FP32 d2 of staged entries k and k + 1 (chunk SoA) from the negated query:
+// fl(a - q) = -fl(q - a), so this is fmaf(dx, dx, fmaf(dy, dy, dz * dz)) bit
+// for bit, two lanes of FFMA2 / FADD2 / FMUL2 per instruction.
+__device__ __forceinline__ float2 ring_d2x2(const float2* nq, const float* ch, int k) {
+    const float2 dx = __fadd2_rn(*reinterpret_cast<const float2*>(ch + k), nq[0]);
+    const float2 dy = __fadd2_rn(*reinterpret_cast<const float2*>(ch + 32 + k), nq[1]);
+    const float2 dz = __fadd2_rn(*reinterpret_cast<const float2*>(ch + 64 + k), nq[2]);
+    return __ffma2_rn(dx, dx, __ffma2_rn(dy, dy, __fmul2_rn(dz, dz)));
 }
 
 // wbuf: 32 float4 of shared memory owned by the calling warp. hint: an entry
@@ -365,13 +379,28 @@ __device__ __forceinline__ int32_t ring_nn_warp(const RingGrid& rg, lkd::V3 y, d
         o1 = seed;
     }
     auto bound = [&]() { return fminf(f1 + 2.0f * rg.band, rg.thr + rg.band); };
+    const float2 nq[3] = {make_float2(-qx, -qx), make_float2(-qy, -qy), make_float2(-qz, -qz)};
     int r_end = 0;
     // r = rmax covers every lane's own walk (its cell +- rmax)
     for (int r = 0; r <= rg.rmax; ++r) {
-        warp_shell(rg, qx, qy, qz, live, b0, b1, r, wbuf, bound, [&](float ax, float ay, float az, int32_t o) {
-            const float dx = qx - ax, dy = qy - ay, dz = qz - az;
-            const float d2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
-            ring_top3_sel(o == seed ? inf : d2, o, f1, f2, f3, o1, o2);
+        warp_shell(rg, qx, qy, qz, live, b0, b1, r, wbuf, bound, [&](const float* ch, int cnt) {
+            // two entries per step in packed FP32 (the same roundings as the
+            // scalar fmaf(dx, dx, fmaf(dy, dy, dz * dz))); the top three are
+            // only touched when some live lane sees an entry below its third
+            int k = 0;
+            for (; k + 2 <= cnt; k += 2) {
+                const float2 d2 = ring_d2x2(nq, ch, k);
+                if (__any_sync(full, live && fminf(d2.x, d2.y) < f3)) {
+                    const int2 o = *reinterpret_cast<const int2*>(ch + 96 + k);
+                    ring_top3_sel(o.x == seed ? inf : d2.x, o.x, f1, f2, f3, o1, o2);
+                    ring_top3_sel(o.y == seed ? inf : d2.y, o.y, f1, f2, f3, o1, o2);
+                }
+            }
+            if (k < cnt) {
+                const float dx = qx - ch[k], dy = qy - ch[32 + k], dz = qz - ch[64 + k];
+                const int32_t o = __float_as_int(ch[96 + k]);
+                ring_top3_sel(o == seed ? inf : fmaf(dx, dx, fmaf(dy, dy, dz * dz)), o, f1, f2, f3, o1, o2);
+            }
         });
         r_end = r;
         // entries outside the scanned box lie >= m - delta cells from the query
@@ -398,9 +427,20 @@ __device__ __forceinline__ int32_t ring_nn_warp(const RingGrid& rg, lkd::V3 y, d
     if (__any_sync(full, resc)) {
         auto lim_bound = [&]() { return lim; };
         for (int r = 0; r <= r_end; ++r)
-            warp_shell(rg, qx, qy, qz, resc, b0, b1, r, wbuf, lim_bound, [&](float ax, float ay, float az, int32_t o) {
-                const float dx = qx - ax, dy = qy - ay, dz = qz - az;
-                if (resc && fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= lim) consider(o);
+            warp_shell(rg, qx, qy, qz, resc, b0, b1, r, wbuf, lim_bound, [&](const float* ch, int cnt) {
+                int k = 0;
+                for (; k + 2 <= cnt; k += 2) {
+                    const float2 d2 = ring_d2x2(nq, ch, k);
+                    if (__any_sync(full, resc && fminf(d2.x, d2.y) <= lim)) {
+                        const int2 o = *reinterpret_cast<const int2*>(ch + 96 + k);
+                        if (resc && d2.x <= lim) consider(o.x);
+                        if (resc && d2.y <= lim) consider(o.y);
+                    }
+                }
+                if (k < cnt) {
+                    const float dx = qx - ch[k], dy = qy - ch[32 + k], dz = qz - ch[64 + k];
+                    if (resc && fmaf(dx, dx, fmaf(dy, dy, dz * dz)) <= lim) consider(__float_as_int(ch[96 + k]));
+                }
             });
     }
     if (hit && !resc) {
