@@ -255,18 +255,21 @@ __device__ __forceinline__ void warp_shell(const RingGrid& rg, float qx, float q
     float* xs = reinterpret_cast<float*>(wbuf);  // staged chunk, SoA: x[32] y[32] z[32] index[32]
     auto scan = [&](int64_t row, int za, int zb) {
         const int32_t s0 = __ldg(rg.start + row + za), s1 = __ldg(rg.start + row + zb + 1);
+        // stage 32 entries (one coalesced load), read back as broadcasts; the
+        // next chunk's load is in flight while this one is visited
+        float4 A = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+        if (s0 + lane < s1) A = __ldg(rg.pts + s0 + lane);
         for (int32_t base = s0; base < s1; base += 32) {
-            // stage 32 entries (one coalesced load), read back as broadcasts
             const int32_t e = base + lane;
             __syncwarp();
             if (e < s1) {
-                const float4 A = __ldg(rg.pts + e);
                 xs[lane] = A.x;
                 xs[32 + lane] = A.y;
                 xs[64 + lane] = A.z;
                 xs[96 + lane] = A.w;
             }
             __syncwarp();
+            if (e + 32 < s1) A = __ldg(rg.pts + e + 32);
             visit(xs, s1 - base < 32 ? s1 - base : 32);
         }
     };
@@ -388,6 +391,16 @@ __device__ __forceinline__ int32_t ring_nn_warp(const RingGrid& rg, lkd::V3 y, d
             // scalar fmaf(dx, dx, fmaf(dy, dy, dz * dz))); the top three are
             // only touched when some live lane sees an entry below its third
             int k = 0;
+            for (; k + 4 <= cnt; k += 4) {
+                const float2 da = ring_d2x2(nq, ch, k), db = ring_d2x2(nq, ch, k + 2);
+                if (__any_sync(full, live && fminf(fminf(da.x, da.y), fminf(db.x, db.y)) < f3)) {
+                    const int4 o = *reinterpret_cast<const int4*>(ch + 96 + k);
+                    ring_top3_sel(o.x == seed ? inf : da.x, o.x, f1, f2, f3, o1, o2);
+                    ring_top3_sel(o.y == seed ? inf : da.y, o.y, f1, f2, f3, o1, o2);
+                    ring_top3_sel(o.z == seed ? inf : db.x, o.z, f1, f2, f3, o1, o2);
+                    ring_top3_sel(o.w == seed ? inf : db.y, o.w, f1, f2, f3, o1, o2);
+                }
+            }
             for (; k + 2 <= cnt; k += 2) {
                 const float2 d2 = ring_d2x2(nq, ch, k);
                 if (__any_sync(full, live && fminf(d2.x, d2.y) < f3)) {
