@@ -8,6 +8,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+
+#include <cub/device/device_scan.cuh>
 #include <vector>
 
 #include "lk_kernels.cuh"
@@ -15,10 +17,6 @@
 namespace lkk {
 
 namespace {
-
-constexpr int kScanThreads = 1024;
-constexpr int kScanItems = 4;
-constexpr int kScanTile = kScanThreads * kScanItems;
 
 __global__ void k_bbox(const double* __restrict__ pos, int64_t n, double* __restrict__ out6) {
     __shared__ double s_lo[3][32], s_hi[3][32];
@@ -105,93 +103,6 @@ __global__ void k_cell_of(const double* __restrict__ pos, int64_t n, GridView g,
     int32_t c = (kx * g.ny + ky) * g.nz + kz;
     cell_of[i] = c;
     atomicAdd(&counts[c], 1);
-}
-
-// Block-level exclusive scan of kScanTile counts; writes block totals.
-__global__ void k_scan_tiles(const int32_t* __restrict__ in, int64_t n, int32_t* __restrict__ out,
-                             int32_t* __restrict__ block_sums) {
-    __shared__ int32_t s_warp[32];
-    int64_t base = blockIdx.x * (int64_t)kScanTile + threadIdx.x * kScanItems;
-    int32_t v[kScanItems];
-    int32_t local = 0;
-#pragma unroll
-    for (int k = 0; k < kScanItems; ++k) {
-        v[k] = (base + k < n) ? in[base + k] : 0;
-        local += v[k];
-    }
-    int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int32_t incl = local;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
-    }
-    if (lane == 31) s_warp[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-        int32_t w = s_warp[lane];
-        int32_t wi = w;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            int32_t y = __shfl_up_sync(0xffffffffu, wi, o);
-            if (lane >= o) wi += y;
-        }
-        s_warp[lane] = wi - w;
-        if (lane == 31) block_sums[blockIdx.x] = wi;
-    }
-    __syncthreads();
-    int32_t run = s_warp[warp] + incl - local;
-#pragma unroll
-    for (int k = 0; k < kScanItems; ++k) {
-        if (base + k < n) out[base + k] = run;
-        run += v[k];
-    }
-}
-
-// Exclusive scan of the block totals in one block; writes the grand total.
-__global__ void k_scan_block_sums(int32_t* __restrict__ sums, int64_t nb, int32_t* __restrict__ total_out) {
-    __shared__ int32_t s_warp[32];
-    __shared__ int32_t s_carry;
-    if (threadIdx.x == 0) s_carry = 0;
-    __syncthreads();
-    int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int64_t base = 0; base < nb; base += blockDim.x) {
-        int64_t i = base + threadIdx.x;
-        int32_t v = i < nb ? sums[i] : 0;
-        int32_t incl = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
-        }
-        if (lane == 31) s_warp[warp] = incl;
-        __syncthreads();
-        if (warp == 0) {
-            int32_t w = s_warp[lane];
-            int32_t wi = w;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                int32_t y = __shfl_up_sync(0xffffffffu, wi, o);
-                if (lane >= o) wi += y;
-            }
-            s_warp[lane] = wi - w;
-        }
-        __syncthreads();
-        int32_t excl = s_carry + s_warp[warp] + incl - v;
-        if (i < nb) sums[i] = excl;
-        __syncthreads();
-        if (threadIdx.x == blockDim.x - 1) s_carry = excl + v;
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) *total_out = s_carry;
-}
-
-__global__ void k_scan_add(int32_t* __restrict__ out, int64_t n, const int32_t* __restrict__ block_offsets) {
-    int64_t base = blockIdx.x * (int64_t)kScanTile + threadIdx.x * kScanItems;
-    int32_t off = block_offsets[blockIdx.x];
-#pragma unroll
-    for (int k = 0; k < kScanItems; ++k)
-        if (base + k < n) out[base + k] += off;
 }
 
 __global__ void k_scatter(const int32_t* __restrict__ cell_of, int64_t n, const int32_t* __restrict__ start,
@@ -477,16 +388,21 @@ inline unsigned blocks_for(int64_t n, int t) { return static_cast<unsigned>((n +
 }  // namespace
 
 // exclusive scan of n int32 into out[0..n] (out[n] = total)
+// out[0..n] = exclusive prefix sums of in[0..n-1], out[n] = the total: one
+// single-pass (decoupled look-back) inclusive scan into out + 1
 cudaError_t exclusive_scan(const int32_t* in, int64_t n, int32_t* out, cudaStream_t stream) {
-    int64_t ntiles = (n + kScanTile - 1) / kScanTile;
-    int32_t* d_bsums = nullptr;
-    cudaError_t e = cudaMallocAsync(&d_bsums, (ntiles + 1) * sizeof(int32_t), stream);
+    cudaError_t e = cudaMemsetAsync(out, 0, sizeof(int32_t), stream);
+    if (e != cudaSuccess || n <= 0) return e;
+    if (n > INT32_MAX) return cudaErrorInvalidValue;
+    size_t temp_bytes = 0;
+    e = cub::DeviceScan::InclusiveSum(nullptr, temp_bytes, in, out + 1, static_cast<int>(n), stream);
     if (e != cudaSuccess) return e;
-    k_scan_tiles<<<static_cast<unsigned>(ntiles), kScanThreads, 0, stream>>>(in, n, out, d_bsums);
-    k_scan_block_sums<<<1, 1024, 0, stream>>>(d_bsums, ntiles, out + n);
-    k_scan_add<<<static_cast<unsigned>(ntiles), kScanThreads, 0, stream>>>(out, n, d_bsums);
-    cudaFreeAsync(d_bsums, stream);
-    return cudaGetLastError();
+    void* temp = nullptr;
+    e = cudaMallocAsync(&temp, temp_bytes > 0 ? temp_bytes : 1, stream);
+    if (e != cudaSuccess) return e;
+    e = cub::DeviceScan::InclusiveSum(temp, temp_bytes, in, out + 1, static_cast<int>(n), stream);
+    cudaFreeAsync(temp, stream);
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 void GridStorage::release() {
