@@ -389,16 +389,19 @@ def bench_b2(args):
     import paper_1801_01572_b200 as lk
     from paper_1801_01572_b200 import synth
     pair = synth.depth_frame_pair()
-    rt, _ = synth.lattice_candidates(pair.truth, math.pi / 180.0, 0.01, 2, 1)  # 125 x 27 = 3375 candidates
+    rt, _ = synth.lattice_candidates(pair.truth, math.pi / 180.0, 0.01, 2, 2)  # 125 x 125 = 15,625 candidates
     params = lk.RegistrationParams()
     grid = lk.build_eval_grid(pair.target, params.d_max)
-    lk.score_candidates(grid, pair.source, rt[:64], params, early_exit=True)  # warm-up
-    t0 = time.perf_counter()
-    sc = lk.score_candidates(grid, pair.source, rt, params, early_exit=True)
-    dt = time.perf_counter() - t0
+    lk.score_candidates(grid, pair.source, rt[:2048], params, early_exit=True)  # warm-up
+    times = []
+    for _ in range(2):
+        t0 = time.perf_counter()
+        sc = lk.score_candidates(grid, pair.source, rt, params, early_exit=True)
+        times.append(time.perf_counter() - t0)
+    dt = min(times)
     evals = rt.shape[0] * pair.source.size()
     out = {"workload": "B2: depth_frame_pair at full resolution, lattice_candidates(truth, 1 deg, 1 cm, "
-                       "rot +-2, trans +-1) = 3,375 of the 10^6-candidate lattice, early exit on",
+                       "rot +-2, trans +-2) = 15,625 of the 10^6-candidate lattice, early exit on, best of 2",
            "candidates": int(rt.shape[0]), "source_points": pair.source.size(), "target_points": pair.target.size(),
            "evals": evals, "ms": 1e3 * dt, "evals_per_s": evals / dt, "qualified": sc.qualified,
            "timing": "wall clock of lk_score_candidates (candidates H2D, scoring, per-candidate results D2H)",

@@ -32,6 +32,7 @@
 
 #include "lk_device_math.cuh"
 #include "lk_eig3.hpp"
+#include "lk_acos_cr.hpp"
 #include "lk_kernels.cuh"
 
 namespace lkk {
@@ -245,9 +246,12 @@ __device__ __forceinline__ V3 cross(V3 a, V3 b) {
 // the host libm's acos, which is not correctly rounded. When |a1| and |a2|
 // are more than 1e-15 apart the rounded values are certainly ordered like the
 // arguments (acos is decreasing with |slope| >= 1, ulp(acos) <= 2.3e-16 on
-// [0, pi/2], libm error < 1 ulp); closer pairs -- common on noisy planar
-// faces, where normals agree to the last bits -- are decided on the host with
-// the same libm (compute_fpfh below). Returns 0 no swap, 1 swap, 2 undecided.
+// [0, pi/2], libm error < 1 ulp). Closer pairs -- common on noisy planar
+// faces, where normals agree to the last bits -- go to list A: k_spfh_decide_a
+// settles those whose outcome does not depend on how glibc rounds near a
+// midpoint (lk_acos_cr.hpp), the rest (~5 % of the ties) are decided on the
+// host with the reference's libm (compute_fpfh below). Returns 0 no swap,
+// 1 swap, 2 undecided.
 __device__ __forceinline__ int swap_decision(double x1, double x2) {
     if (!(x1 <= 1.0 && x2 <= 1.0)) return 0;  // acos of |a| > 1 is NaN: never greater
     if (fabs(x1 - x2) > 1e-15) return x1 < x2 ? 1 : 0;
@@ -500,9 +504,34 @@ struct DeferLists {
     double2* a_x;
     int2* b_ij;
     DeferredPair* b_x;
-    int32_t* n;  // n[0] = list A, n[1] = list B
+    int32_t* n;  // n[0] = list A, n[1] = list B, n[2] = list A2
     int64_t a_cap, b_cap;
+    uint8_t* a_dec;  // list A decisions (k_spfh_decide_a; the host's for A2)
+    int32_t* a2_k;   // A2: list A entries the host decides
+    double2* a2_x;
 };
+
+// List A's frame-source tests settled on the device where glibc's outcome is
+// certain (lk_acos_cr.hpp acos_greater); the rest go to list A2 for the host.
+__global__ void k_spfh_decide_a(DeferLists dl) {
+    const int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= dl.n[0]) return;
+    const double2 x = dl.a_x[k];
+    const int g = lkacos::acos_greater(x.x, x.y);
+    if (g != 2) {
+        dl.a_dec[k] = static_cast<uint8_t>(g);
+        return;
+    }
+    const int32_t slot = atomicAdd(dl.n + 2, 1);
+    dl.a2_k[slot] = k;
+    dl.a2_x[slot] = x;
+}
+
+__global__ void k_spfh_scatter_a2(const int32_t* __restrict__ a2_k, const uint8_t* __restrict__ dec, int32_t m,
+                                  uint8_t* __restrict__ a_dec) {
+    const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < m) a_dec[a2_k[j]] = dec[j];
+}
 
 __global__ void __launch_bounds__(32 * kFpfhWarps) k_spfh(const double* __restrict__ pos,
                                                           const double* __restrict__ nrm, int64_t n,
@@ -1016,7 +1045,7 @@ struct FpfhStage {
     static constexpr int kStageA = 4096;
     static constexpr int kStageB = 64;
     struct Head {
-        int32_t total, n_a, n_b, overflow;
+        int32_t total, n_a, n_b, n_a2, overflow;
         double2 a[kStageA];
         DeferredPair b[kStageB];
     };
@@ -1076,12 +1105,15 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
     uint32_t* d_dec_b = nullptr;
     LK_TRY(cudaMallocAsync(&spfh, 33 * n * sizeof(double), stream));
     LK_TRY(cudaMallocAsync(&votes, 34 * n * sizeof(int32_t), stream));
-    LK_TRY(cudaMallocAsync(&n_def, 2 * sizeof(int32_t), stream));
+    LK_TRY(cudaMallocAsync(&n_def, 3 * sizeof(int32_t), stream));
     auto free_lists = [&] {
         cudaFreeAsync(dl.a_ij, stream);
         cudaFreeAsync(dl.a_x, stream);
         cudaFreeAsync(dl.b_ij, stream);
         cudaFreeAsync(dl.b_x, stream);
+        cudaFreeAsync(dl.a_dec, stream);
+        cudaFreeAsync(dl.a2_k, stream);
+        cudaFreeAsync(dl.a2_x, stream);
     };
     for (int attempt = 0; attempt < 2; ++attempt) {
         LK_TRY(cudaMallocAsync(&nbr, cap * sizeof(int32_t), stream));
@@ -1089,10 +1121,13 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
         LK_TRY(cudaMallocAsync(&dl.a_x, a_cap * sizeof(double2), stream));
         LK_TRY(cudaMallocAsync(&dl.b_ij, b_cap * sizeof(int2), stream));
         LK_TRY(cudaMallocAsync(&dl.b_x, b_cap * sizeof(DeferredPair), stream));
+        LK_TRY(cudaMallocAsync(&dl.a_dec, a_cap, stream));
+        LK_TRY(cudaMallocAsync(&dl.a2_k, a_cap * sizeof(int32_t), stream));
+        LK_TRY(cudaMallocAsync(&dl.a2_x, a_cap * sizeof(double2), stream));
         dl.n = n_def;
         dl.a_cap = a_cap;
         dl.b_cap = b_cap;
-        LK_TRY(cudaMemsetAsync(n_def, 0, 2 * sizeof(int32_t), stream));
+        LK_TRY(cudaMemsetAsync(n_def, 0, 3 * sizeof(int32_t), stream));
         if (brute && attempt == 0)
             k_nbr_compact<<<nblocks(32 * n, 256), 256, 0, stream>>>(slots, off, n, d_overflow, nbr, cap);
         else if (brute)
@@ -1103,13 +1138,14 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
         // an overflowed slot table leaves nbr unfilled: the votes are skipped too
         k_spfh<<<nblocks(n, kFpfhWarps), 32 * kFpfhWarps, 0, stream>>>(d_pos, d_nrm, n, off, nbr, votes, dl, cap,
                                                                        (brute && attempt == 0) ? d_overflow : nullptr);
-        // one round trip: total, list counts and the heads of both lists
+        k_spfh_decide_a<<<nblocks(a_cap, 256), 256, 0, stream>>>(dl);
+        // one round trip: total, list counts and the heads of lists A2 and B
         LK_TRY(cudaMemcpyAsync(&st.head->total, off + n, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
-        LK_TRY(cudaMemcpyAsync(&st.head->n_a, n_def, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
+        LK_TRY(cudaMemcpyAsync(&st.head->n_a, n_def, 3 * sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
         st.head->overflow = 0;
         if (brute && attempt == 0)
             LK_TRY(cudaMemcpyAsync(&st.head->overflow, d_overflow, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
-        LK_TRY(cudaMemcpyAsync(st.head->a, dl.a_x, FpfhStage::kStageA * sizeof(double2), cudaMemcpyDeviceToHost,
+        LK_TRY(cudaMemcpyAsync(st.head->a, dl.a2_x, FpfhStage::kStageA * sizeof(double2), cudaMemcpyDeviceToHost,
                                stream));
         LK_TRY(cudaMemcpyAsync(st.head->b, dl.b_x, FpfhStage::kStageB * sizeof(DeferredPair), cudaMemcpyDeviceToHost,
                                stream));
@@ -1122,11 +1158,11 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
         b_cap = std::max<int64_t>(b_cap, st.head->n_b);
     }
     // pairs the device cannot settle, decided with the reference's libm:
-    // list A by its acos comparison (fpfh.cpp:28), list B whole (host_pair_bins)
-    const int32_t ma = st.head->n_a, mb = st.head->n_b;
+    // list A2 by its acos comparison (fpfh.cpp:28), list B whole (host_pair_bins)
+    const int32_t na = st.head->n_a, ma = st.head->n_a2, mb = st.head->n_b;
     if (const char* tr = std::getenv("LK_TRACE"); tr && tr[0] == '1')
-        std::fprintf(stderr, "[lk fpfh] n %lld neighbours %d deferred: acos ties %d, theta edges %d\n",
-                     static_cast<long long>(n), st.head->total, ma, mb);
+        std::fprintf(stderr, "[lk fpfh] n %lld neighbours %d deferred: acos ties %d (host %d), theta edges %d\n",
+                     static_cast<long long>(n), st.head->total, na, ma, mb);
     if (ma > 0) {
         const double2* xs = st.head->a;
         if (ma > FpfhStage::kStageA) {
@@ -1137,7 +1173,7 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
                 LK_TRY(cudaHostAlloc(reinterpret_cast<void**>(&st.more_a), ma * sizeof(double2), 0));
                 st.more_cap = ma;
             }
-            LK_TRY(cudaMemcpyAsync(st.more_a + FpfhStage::kStageA, dl.a_x + FpfhStage::kStageA,
+            LK_TRY(cudaMemcpyAsync(st.more_a + FpfhStage::kStageA, dl.a2_x + FpfhStage::kStageA,
                                    (ma - FpfhStage::kStageA) * sizeof(double2), cudaMemcpyDeviceToHost, stream));
             std::memcpy(st.more_a, st.head->a, FpfhStage::kStageA * sizeof(double2));
             LK_TRY(cudaStreamSynchronize(stream));
@@ -1154,8 +1190,9 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
         for (int32_t k = 0; k < ma; ++k) st.dec_a[k] = std::acos(xs[k].x) > std::acos(xs[k].y) ? 1 : 0;
         LK_TRY(cudaMallocAsync(&d_dec_a, ma, stream));
         LK_TRY(cudaMemcpyAsync(d_dec_a, st.dec_a, ma, cudaMemcpyHostToDevice, stream));
-        k_spfh_resolve_a<<<nblocks(ma, 256), 256, 0, stream>>>(d_pos, d_nrm, dl.a_ij, d_dec_a, ma, votes);
+        k_spfh_scatter_a2<<<nblocks(ma, 256), 256, 0, stream>>>(dl.a2_k, d_dec_a, ma, dl.a_dec);
     }
+    if (na > 0) k_spfh_resolve_a<<<nblocks(na, 256), 256, 0, stream>>>(d_pos, d_nrm, dl.a_ij, dl.a_dec, na, votes);
     if (mb > 0) {
         std::vector<DeferredPair> more;
         const DeferredPair* xs = st.head->b;

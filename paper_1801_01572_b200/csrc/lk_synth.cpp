@@ -22,6 +22,7 @@
 
 #include "../../include/loopkit_b200.h"
 #include "lk_prepare_host.hpp"
+#include "lk_acos_cr.hpp"
 
 namespace lk {
 namespace {
@@ -486,6 +487,65 @@ void* guard(int* status, F&& fn) {
 using namespace lk;
 
 extern "C" {
+
+// Test hooks for lk_acos_cr.hpp (tests/test_acos_cr.py): acos_cr against this
+// machine's libm acos. check: the given arguments; sweep: n xorshift draws,
+// uniform on [0, 1) and cubed (more small arguments) alternately.
+void lks_acos_cr_check(const double* xs, int64_t n, int64_t* decided, int64_t* wrong) {
+    int64_t d = 0, w = 0;
+    for (int64_t k = 0; k < n; ++k) {
+        double c;
+        if (lkacos::acos_cr(xs[k], &c)) {
+            ++d;
+            if (c != std::acos(xs[k])) ++w;
+        }
+    }
+    *decided = d;
+    *wrong = w;
+}
+
+// acos_greater(x1, x2) against libm's acos(x1) > acos(x2) on pairs of
+// arguments a few ulps apart (the FPFH ties)
+void lks_acos_greater_sweep(uint64_t seed, int64_t n, int64_t* decided, int64_t* wrong) {
+    uint64_t s = seed | 1u;
+    int64_t d = 0, w = 0;
+    for (int64_t k = 0; k < n; ++k) {
+        s ^= s << 13;
+        s ^= s >> 7;
+        s ^= s << 17;
+        double x1 = static_cast<double>(s >> 11) * 0x1p-53;
+        if (k & 1) x1 = x1 * x1 * x1;
+        double x2 = x1;
+        for (int j = static_cast<int>(s & 7u); j >= 0; --j) x2 = std::nextafter(x2, 2.0);
+        if (k & 2) std::swap(x1, x2);
+        const int g = lkacos::acos_greater(x1, x2);
+        if (g != 2) {
+            ++d;
+            if (g != (std::acos(x1) > std::acos(x2) ? 1 : 0)) ++w;
+        }
+    }
+    *decided = d;
+    *wrong = w;
+}
+
+void lks_acos_cr_sweep(uint64_t seed, int64_t n, int64_t* decided, int64_t* wrong) {
+    uint64_t s = seed | 1u;
+    int64_t d = 0, w = 0;
+    for (int64_t k = 0; k < n; ++k) {
+        s ^= s << 13;
+        s ^= s >> 7;
+        s ^= s << 17;
+        double x = static_cast<double>(s >> 11) * 0x1p-53;
+        if (k & 1) x = x * x * x;
+        double c;
+        if (lkacos::acos_cr(x, &c)) {
+            ++d;
+            if (c != std::acos(x)) ++w;
+        }
+    }
+    *decided = d;
+    *wrong = w;
+}
 
 const char* lks_last_error(void) { return g_synth_err.c_str(); }
 
