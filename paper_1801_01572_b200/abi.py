@@ -280,3 +280,17 @@ def synth_lib():
 def last_error() -> str:
     msg = lib().lk_last_error()
     return msg.decode() if msg else ""
+
+
+def prefer_process_nccl() -> None:
+    """The library opens libnccl.so.2 on first NCCL use and reuses one already
+    in the process (lk_abi.cu nccl()). If PyTorch is installed but not yet
+    imported, import it first so that its bundled NCCL is the one loaded:
+    otherwise a later `import torch` would bind to the system NCCL already in
+    the process and fail on missing symbols."""
+    import sys
+    if "torch" not in sys.modules:
+        try:
+            import torch  # noqa: F401
+        except Exception:
+            pass

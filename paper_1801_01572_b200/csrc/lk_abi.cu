@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 #include <nvtx3/nvToolsExt.h>
+#include <dlfcn.h>
 
 #include <algorithm>
 #include <array>
@@ -22,6 +23,7 @@
 #include <condition_variable>
 #include <functional>
 #include <exception>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/loopkit_b200.h"
@@ -46,8 +48,58 @@ inline void ck(cudaError_t e, const char* where) {
 }
 #define CK(x) ck((x), #x)
 
+// NCCL is opened on first use (dlopen), not linked: a process that imports
+// PyTorch after this library must still get PyTorch's own libnccl.so.2 (the
+// dynamic linker reuses an already-loaded SONAME, and the system NCCL lacks
+// symbols PyTorch's build needs). An NCCL already in the process (PyTorch's)
+// is used as is; otherwise LK_NCCL_LIBRARY, otherwise libnccl.so.2 from the
+// loader's search path.
+struct NcclApi {
+    decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
+    decltype(&ncclCommInitRank) CommInitRank = nullptr;
+    decltype(&ncclCommInitAll) CommInitAll = nullptr;
+    decltype(&ncclCommDestroy) CommDestroy = nullptr;
+    decltype(&ncclBroadcast) Broadcast = nullptr;
+    decltype(&ncclAllReduce) AllReduce = nullptr;
+    decltype(&ncclGroupStart) GroupStart = nullptr;
+    decltype(&ncclGroupEnd) GroupEnd = nullptr;
+    decltype(&ncclGetErrorString) GetErrorString = nullptr;
+    std::string error;
+};
+const NcclApi& nccl() {
+    static const NcclApi api = [] {
+        NcclApi a;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h)
+            if (const char* path = std::getenv("LK_NCCL_LIBRARY")) h = dlopen(path, RTLD_NOW | RTLD_LOCAL);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+        if (!h) {
+            const char* why = dlerror();
+            a.error = std::string("cannot open libnccl.so.2: ") + (why ? why : "unknown");
+            return a;
+        }
+        auto sym = [&](auto& f, const char* name) {
+            f = reinterpret_cast<std::remove_reference_t<decltype(f)>>(dlsym(h, name));
+            if (!f && a.error.empty()) a.error = std::string("libnccl.so.2 has no ") + name;
+        };
+        sym(a.GetUniqueId, "ncclGetUniqueId");
+        sym(a.CommInitRank, "ncclCommInitRank");
+        sym(a.CommInitAll, "ncclCommInitAll");
+        sym(a.CommDestroy, "ncclCommDestroy");
+        sym(a.Broadcast, "ncclBroadcast");
+        sym(a.AllReduce, "ncclAllReduce");
+        sym(a.GroupStart, "ncclGroupStart");
+        sym(a.GroupEnd, "ncclGroupEnd");
+        sym(a.GetErrorString, "ncclGetErrorString");
+        return a;
+    }();
+    if (!api.error.empty()) throw lk::Status(LK_NCCL_ERROR, api.error);
+    return api;
+}
+
 inline void nk(ncclResult_t r, const char* where) {
-    if (r != ncclSuccess) throw lk::Status(LK_NCCL_ERROR, std::string(where) + ": " + ncclGetErrorString(r));
+    if (r != ncclSuccess)
+        throw lk::Status(LK_NCCL_ERROR, std::string(where) + ": " + nccl().GetErrorString(r));
 }
 #define NK(x) nk((x), #x)
 
@@ -470,7 +522,7 @@ struct lk_reg_ctx {
         peers.clear();
         cudaSetDevice(device);
         drain_events();
-        if (comm) ncclCommDestroy(comm);
+        if (comm) nccl().CommDestroy(comm);
         if (stream) cudaStreamSynchronize(stream);
         cudaStream_t s = own_stream;
         lkk::pool_free(d_spos, s);
@@ -662,7 +714,7 @@ void make_peers(lk_reg_ctx* c, const std::vector<int>& devs, double d_max) {
     NvtxRange range("lk replicate context (ncclBroadcast)");
     const int G = static_cast<int>(devs.size());
     std::vector<ncclComm_t> comms(G);
-    NK(ncclCommInitAll(comms.data(), G, devs.data()));
+    NK(nccl().CommInitAll(comms.data(), G, devs.data()));
     c->comm = comms[0];
     c->nranks = G;
     c->rank = 0;
@@ -685,10 +737,10 @@ void make_peers(lk_reg_ctx* c, const std::vector<int>& devs, double d_max) {
     std::vector<lk_reg_ctx*> all{c};
     all.insert(all.end(), c->peers.begin(), c->peers.end());
     auto bcast = [&](auto member, size_t count, ncclDataType_t type) {
-        NK(ncclGroupStart());
+        NK(nccl().GroupStart());
         for (int g = 0; g < G; ++g)
-            NK(ncclBroadcast(all[0]->*member, all[g]->*member, count, type, 0, all[g]->comm, all[g]->stream));
-        NK(ncclGroupEnd());
+            NK(nccl().Broadcast(all[0]->*member, all[g]->*member, count, type, 0, all[g]->comm, all[g]->stream));
+        NK(nccl().GroupEnd());
     };
     bcast(&lk_reg_ctx::d_spos, 3 * c->ns, ncclFloat64);
     bcast(&lk_reg_ctx::d_snrm, 3 * c->ns, ncclFloat64);
@@ -848,10 +900,10 @@ lk_status exchange_run(lk_reg_ctx* c, const lk_reg_params& p) {
         const lk_status st = run_range_impl(q, p, begin, end, q->d_xbuf + q->rank);
         if (st != LK_OK) return st;
     }
-    NK(ncclGroupStart());
+    NK(nccl().GroupStart());
     for (lk_reg_ctx* q : all)
-        NK(ncclAllReduce(q->d_xbuf, q->d_xbuf, words, ncclInt64, ncclSum, q->comm, q->stream));
-    NK(ncclGroupEnd());
+        NK(nccl().AllReduce(q->d_xbuf, q->d_xbuf, words, ncclInt64, ncclSum, q->comm, q->stream));
+    NK(nccl().GroupEnd());
     CK(cudaSetDevice(c->device));
     return LK_OK;
 }
@@ -1080,7 +1132,7 @@ lk_status lk_nccl_unique_id(uint8_t id[128]) {
         if (!id) return fail(LK_INVALID_ARGUMENT, "null argument");
         ncclUniqueId u;
         static_assert(sizeof(u.internal) == 128, "NCCL unique id size");
-        NK(ncclGetUniqueId(&u));
+        NK(nccl().GetUniqueId(&u));
         std::memcpy(id, u.internal, 128);
         return LK_OK;
     });
@@ -1095,7 +1147,7 @@ lk_status lk_reg_ctx_attach_comm(lk_reg_ctx* ctx, const uint8_t id[128], int32_t
         CK(cudaSetDevice(ctx->device));
         ncclUniqueId u;
         std::memcpy(u.internal, id, 128);
-        NK(ncclCommInitRank(&ctx->comm, nranks, u, rank));
+        NK(nccl().CommInitRank(&ctx->comm, nranks, u, rank));
         ctx->nranks = nranks;
         ctx->rank = rank;
         CK(lkk::pool_alloc(&ctx->d_xbuf, nranks * sizeof(lk_reg_record), ctx->stream));

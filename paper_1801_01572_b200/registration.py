@@ -54,6 +54,8 @@ class RegistrationParams:
         return self.max_fitness if self.max_fitness is not None else self.d_max * self.d_max / 2.0
 
     def to_c(self) -> abi.lk_reg_params:
+        if self.device_count not in (0, 1):
+            abi.prefer_process_nccl()  # G > 1 devices: NCCL inside the call
         return abi.lk_reg_params(
             leaf=self.leaf, normal_radius=self.normal_radius, feature_radius=self.feature_radius,
             hypothesis_count=int(self.hypothesis_count), similarity_tau=self.similarity_tau, d_max=self.d_max,
@@ -236,6 +238,7 @@ class RegistrationContext:
         """One process per GPU: join the NCCL communicator of `unique_id`
         (lk_nccl_unique_id on rank 0, broadcast by the caller); run_hypotheses
         then runs this rank's share and merges over NCCL."""
+        abi.prefer_process_nccl()
         buf = (C.c_uint8 * 128).from_buffer_copy(bytes(unique_id))
         check(abi.lib().lk_reg_ctx_attach_comm(self._h, buf, int(nranks), int(rank)))
 
@@ -279,6 +282,7 @@ class RegistrationContext:
 
 def nccl_unique_id() -> bytes:
     """128-byte NCCL unique id for RegistrationContext.attach_comm (rank 0)."""
+    abi.prefer_process_nccl()
     buf = (C.c_uint8 * 128)()
     check(abi.lib().lk_nccl_unique_id(buf))
     return bytes(buf)

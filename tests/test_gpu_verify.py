@@ -91,3 +91,39 @@ def test_verified_loops_weighted_by_the_line_process():
     assert out[0].info.pair_count > 0 and out[1].info.pair_count > 0
     assert w[0] == pytest.approx(1.0, abs=1e-9) and acc[0]
     assert w[1] < 0.25 and not acc[1]
+
+
+def test_verify_batch_large_batch_equals_small_batches(oracle):
+    """A 70-pair batch from page-locked clouds (the zero-copy gather path)
+    equals the same pairs verified in batches of 8, and a few are checked
+    against the oracle. torch is imported after the library: the library
+    must not have pulled a second NCCL into the process."""
+    import torch
+    pairs = [synth.synth_registration_pair(s) for s in range(1, 71)]
+    keep = []
+
+    def pin(c):  # page-locked clouds: the zero-copy gather path of the bench
+        tp = torch.from_numpy(np.ascontiguousarray(c.positions)).pin_memory()
+        tn = torch.from_numpy(np.ascontiguousarray(c.normals)).pin_memory()
+        keep.extend([tp, tn])
+        return lk.PointCloud(tp.numpy(), tn.numpy())
+
+    Q = [pin(p.target) for p in pairs]
+    P = [pin(p.source) for p in pairs]
+    Ti = [lk.RigidTransform() for _ in pairs]
+    Tj = [p.truth for p in pairs]
+    T = [p.truth if k % 5 else synth.compose(synth.transform_from_twist([0.1, 0, 0, 0.1, 0, 0]), p.truth)
+         for k, p in enumerate(pairs)]
+    vp = lk.VerifyParams()
+    big = lk.verify_batch(Q, P, Ti, Tj, T, vp)
+    for a in range(0, len(pairs), 8):
+        small = lk.verify_batch(Q[a:a + 8], P[a:a + 8], Ti[a:a + 8], Tj[a:a + 8], T[a:a + 8], vp)
+        for k, r in enumerate(small):
+            b = big[a + k]
+            assert b.info.pair_count == r.info.pair_count and np.array_equal(b.info.info, r.info.info), a + k
+            assert b.overlap_hits == r.overlap_hits and b.inliers == r.inliers and b.fitness == r.fitness, a + k
+    for k in (0, 17, 35, 69):
+        info, cnt, hits, ratio, fit, inl = _oracle_pair(oracle, Q[k], P[k], Ti[k], Tj[k], T[k], vp)
+        r = big[k]
+        assert r.info.pair_count == cnt and np.array_equal(r.info.info, info), k
+        assert r.overlap_hits == hits and r.inliers == inl and r.fitness == fit, k
