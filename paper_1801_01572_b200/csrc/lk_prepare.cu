@@ -508,7 +508,7 @@ struct DeferLists {
     int64_t a_cap, b_cap;
     uint8_t* a_dec;  // list A decisions (k_spfh_decide_a; the host's for A2)
     int32_t* a2_k;   // A2: list A entries the host decides
-    double2* a2_x;
+    double4* a2_x;   // (|a1|, |a2|, v1, v2): v = glibc's acos when certain, else NaN
 };
 
 // List A's frame-source tests settled on the device where glibc's outcome is
@@ -517,14 +517,17 @@ __global__ void k_spfh_decide_a(DeferLists dl) {
     const int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= dl.n[0]) return;
     const double2 x = dl.a_x[k];
-    const int g = lkacos::acos_greater(x.x, x.y);
-    if (g != 2) {
-        dl.a_dec[k] = static_cast<uint8_t>(g);
+    double l1, h1, l2, h2;
+    const int r1 = lkacos::acos_bracket(x.x, &l1, &h1), r2 = lkacos::acos_bracket(x.y, &l2, &h2);
+    if (r1 && r2 && (l1 > h2 || h1 <= l2)) {  // lkacos::acos_greater, certain
+        dl.a_dec[k] = l1 > h2 ? 1 : 0;
         return;
     }
+    // the host evaluates only the values whose rounding is in doubt
+    const double nan = __longlong_as_double(0x7ff8000000000000ll);
     const int32_t slot = atomicAdd(dl.n + 2, 1);
     dl.a2_k[slot] = k;
-    dl.a2_x[slot] = x;
+    dl.a2_x[slot] = make_double4(x.x, x.y, r1 == 1 ? l1 : nan, r2 == 1 ? l2 : nan);
 }
 
 __global__ void k_spfh_scatter_a2(const int32_t* __restrict__ a2_k, const uint8_t* __restrict__ dec, int32_t m,
@@ -1042,15 +1045,15 @@ static uint32_t host_pair_bins(const double* v) {
 // the first kStageX deferred pairs come back in one copy; the decisions go
 // back from here. Reused only after the caller's stream has synchronised.
 struct FpfhStage {
-    static constexpr int kStageA = 4096;
+    static constexpr int kStageA = 2048;
     static constexpr int kStageB = 64;
     struct Head {
         int32_t total, n_a, n_b, n_a2, overflow;
-        double2 a[kStageA];
+        double4 a[kStageA];
         DeferredPair b[kStageB];
     };
     Head* head = nullptr;
-    double2* more_a = nullptr;  // pinned: list A beyond the staged head
+    double4* more_a = nullptr;  // pinned: list A2 beyond the staged head
     size_t more_cap = 0;
     uint8_t* dec_a = nullptr;
     uint32_t* dec_b = nullptr;
@@ -1123,7 +1126,7 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
         LK_TRY(cudaMallocAsync(&dl.b_x, b_cap * sizeof(DeferredPair), stream));
         LK_TRY(cudaMallocAsync(&dl.a_dec, a_cap, stream));
         LK_TRY(cudaMallocAsync(&dl.a2_k, a_cap * sizeof(int32_t), stream));
-        LK_TRY(cudaMallocAsync(&dl.a2_x, a_cap * sizeof(double2), stream));
+        LK_TRY(cudaMallocAsync(&dl.a2_x, a_cap * sizeof(double4), stream));
         dl.n = n_def;
         dl.a_cap = a_cap;
         dl.b_cap = b_cap;
@@ -1145,7 +1148,7 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
         st.head->overflow = 0;
         if (brute && attempt == 0)
             LK_TRY(cudaMemcpyAsync(&st.head->overflow, d_overflow, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
-        LK_TRY(cudaMemcpyAsync(st.head->a, dl.a2_x, FpfhStage::kStageA * sizeof(double2), cudaMemcpyDeviceToHost,
+        LK_TRY(cudaMemcpyAsync(st.head->a, dl.a2_x, FpfhStage::kStageA * sizeof(double4), cudaMemcpyDeviceToHost,
                                stream));
         LK_TRY(cudaMemcpyAsync(st.head->b, dl.b_x, FpfhStage::kStageB * sizeof(DeferredPair), cudaMemcpyDeviceToHost,
                                stream));
@@ -1164,18 +1167,18 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
         std::fprintf(stderr, "[lk fpfh] n %lld neighbours %d deferred: acos ties %d (host %d), theta edges %d\n",
                      static_cast<long long>(n), st.head->total, na, ma, mb);
     if (ma > 0) {
-        const double2* xs = st.head->a;
+        const double4* xs = st.head->a;
         if (ma > FpfhStage::kStageA) {
             if (static_cast<size_t>(ma) > st.more_cap) {
                 if (st.more_a) cudaFreeHost(st.more_a);
                 st.more_a = nullptr;
                 st.more_cap = 0;
-                LK_TRY(cudaHostAlloc(reinterpret_cast<void**>(&st.more_a), ma * sizeof(double2), 0));
+                LK_TRY(cudaHostAlloc(reinterpret_cast<void**>(&st.more_a), ma * sizeof(double4), 0));
                 st.more_cap = ma;
             }
             LK_TRY(cudaMemcpyAsync(st.more_a + FpfhStage::kStageA, dl.a2_x + FpfhStage::kStageA,
-                                   (ma - FpfhStage::kStageA) * sizeof(double2), cudaMemcpyDeviceToHost, stream));
-            std::memcpy(st.more_a, st.head->a, FpfhStage::kStageA * sizeof(double2));
+                                   (ma - FpfhStage::kStageA) * sizeof(double4), cudaMemcpyDeviceToHost, stream));
+            std::memcpy(st.more_a, st.head->a, FpfhStage::kStageA * sizeof(double4));
             LK_TRY(cudaStreamSynchronize(stream));
             xs = st.more_a;
         }
@@ -1187,7 +1190,11 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
             st.dec_a_cap = ma;
         }
 #pragma omp parallel for schedule(static) if (ma > 4096)
-        for (int32_t k = 0; k < ma; ++k) st.dec_a[k] = std::acos(xs[k].x) > std::acos(xs[k].y) ? 1 : 0;
+        for (int32_t k = 0; k < ma; ++k) {
+            const double g1 = std::isnan(xs[k].z) ? std::acos(xs[k].x) : xs[k].z;
+            const double g2 = std::isnan(xs[k].w) ? std::acos(xs[k].y) : xs[k].w;
+            st.dec_a[k] = g1 > g2 ? 1 : 0;
+        }
         LK_TRY(cudaMallocAsync(&d_dec_a, ma, stream));
         LK_TRY(cudaMemcpyAsync(d_dec_a, st.dec_a, ma, cudaMemcpyHostToDevice, stream));
         k_spfh_scatter_a2<<<nblocks(ma, 256), 256, 0, stream>>>(dl.a2_k, d_dec_a, ma, dl.a_dec);
