@@ -163,18 +163,27 @@ int select_device(int32_t device) {
 std::mutex g_stream_mu;
 std::vector<std::pair<int, cudaStream_t>> g_free_streams;
 
-cudaStream_t acquire_stream(int dev) {
+// high = the device's greatest stream priority (the critical path of a
+// prepare: the side whose cloud lands last, then the hypotheses), else the
+// default priority. Pooled per (device, priority).
+cudaStream_t acquire_stream(int dev, bool high = false) {
+    int least = 0, greatest = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    const int prio = high ? greatest : 0;
     {
         std::lock_guard<std::mutex> lock(g_stream_mu);
-        for (size_t k = g_free_streams.size(); k-- > 0;)
-            if (g_free_streams[k].first == dev) {
+        for (size_t k = g_free_streams.size(); k-- > 0;) {
+            int p = 0;
+            if (g_free_streams[k].first == dev && cudaStreamGetPriority(g_free_streams[k].second, &p) == cudaSuccess &&
+                p == prio) {
                 cudaStream_t s = g_free_streams[k].second;
                 g_free_streams.erase(g_free_streams.begin() + static_cast<std::ptrdiff_t>(k));
                 return s;
             }
+        }
     }
     cudaStream_t s = nullptr;
-    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, prio));
     return s;
 }
 
@@ -568,7 +577,7 @@ lk_reg_ctx* ctx_new(int32_t device) {
     try {
         c->device = select_device(device);
         c->sm_count = sm_count_of(c->device);
-        c->own_stream = acquire_stream(c->device);
+        c->own_stream = acquire_stream(c->device, true);  // source side (lands last), then the run
         c->aux_stream = acquire_stream(c->device);
         c->grid_stream = acquire_stream(c->device);
         c->stream = c->own_stream;
