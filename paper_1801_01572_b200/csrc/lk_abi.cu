@@ -603,6 +603,8 @@ struct CloudSide {
     int status = 0;  // 5: invalid normals
     int64_t usable = 0;
     double max_norm = 0.0;
+    unsigned long long* stats = nullptr;  // pinned (the side thread's), decoded after the final sync
+    bool features = false;                 // feat is being computed on s
     std::exception_ptr err;
 };
 
@@ -649,10 +651,11 @@ void prepare_side(CloudSide& cs, double feature_radius, double normal_radius, do
             CK(lkk::estimate_normals(cs.pos, cs.n, normal_radius, origin, cs.nrm, cs.s));
             mark("normals");
         }
-        // usable normals and |p|max come back with the side's final sync
+        // usable normals and |p|max come back with prepare's final sync
         thread_local unsigned long long* h_stats = nullptr;
         if (!h_stats) CK(cudaHostAlloc(reinterpret_cast<void**>(&h_stats), 2 * sizeof(unsigned long long), 0));
         CK(lkk::cloud_stats_async(cs.pos, cs.nrm, cs.n, h_stats, cs.s));
+        cs.stats = h_stats;
         // the EvalGrid (registration.cpp:249) only needs the downsampled
         // cloud: it is built on its own stream and host thread while this
         // one runs the FPFH
@@ -685,10 +688,9 @@ void prepare_side(CloudSide& cs, double feature_radius, double normal_radius, do
             throw;
         }
         mark("fpfh");
-        // one wait for the side's stream: the stats above, the features
-        // (the feature match runs on another stream) and the FPFH staging
-        CK(cudaStreamSynchronize(cs.s));
-        lkk::cloud_stats_decode(h_stats, &cs.usable, &cs.max_norm);
+        // no wait here: the feature match is queued behind both sides'
+        // streams, and prepare's final sync brings the stats back
+        cs.features = true;
         if (gw) {
             gw->wait();
             release_worker(gw);
@@ -833,9 +835,32 @@ lk_status prepare_impl(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_pa
         c->d_tfeat = T.feat;
         c->ns = S.n;
         c->nt = T.n;
-        c->src_max_norm = S.max_norm;
         if (S.err) std::rethrow_exception(S.err);
         if (T.err) std::rethrow_exception(T.err);
+        // feature pre-match (registration.cpp:248) queued behind both sides'
+        // streams before any host wait; the checks below decide whether it
+        // counts (an error discards the context)
+        cudaStream_t s = c->stream;
+        if (S.features && T.features) {
+            for (CloudSide* cs : {&S, &T}) {
+                if (cs->s == s) continue;
+                cudaEvent_t done;
+                CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+                CK(cudaEventRecord(done, cs->s));
+                CK(cudaStreamWaitEvent(s, done, 0));
+                cudaEventDestroy(done);
+            }
+            CK(lkk::pool_alloc(&c->d_cache, c->ns * sizeof(int32_t), s));
+            CK(lkk::feature_nn(c->d_sfeat, c->ns, c->d_tfeat, c->nt, c->d_cache, s));
+            tmark("joined, feature nn start", s, t0);
+            ctx_finish_source(c);
+            tmark("feature nn done", s, t0);
+        }
+        CK(cudaStreamSynchronize(T.s));
+        CK(cudaStreamSynchronize(s));
+        for (CloudSide* cs : {&S, &T})
+            if (cs->stats) lkk::cloud_stats_decode(cs->stats, &cs->usable, &cs->max_norm);
+        c->src_max_norm = S.max_norm;
         // the reference's check order (registration.cpp:226-245)
         if (S.status == 5 || T.status == 5)
             throw lk::Status(LK_MISSING_NORMALS, "normals must be unit length or exactly zero");
@@ -843,14 +868,6 @@ lk_status prepare_impl(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_pa
             throw lk::Status(LK_TOO_FEW_POINTS, "register_global: fewer than 4 points after downsampling");
         if (S.usable < 4 || T.usable < 4)
             throw lk::Status(LK_MISSING_DATA, "register_global: fewer than 4 points with usable normals");
-        // feature pre-match (registration.cpp:248) once both sides are done
-        cudaStream_t s = c->stream;
-        CK(lkk::pool_alloc(&c->d_cache, c->ns * sizeof(int32_t), s));
-        CK(lkk::feature_nn(c->d_sfeat, c->ns, c->d_tfeat, c->nt, c->d_cache, s));
-        tmark("joined, feature nn start", s, t0);
-        ctx_finish_source(c);
-        tmark("feature nn done", s, t0);
-        CK(cudaStreamSynchronize(s));
         tdump();
         if (trace_on()) std::fprintf(stderr, "[lk prepare] feature nn %8.3f ms\n", (now_s() - t0) * 1e3);
         if (devs.size() > 1) make_peers(c, devs, params->d_max);
