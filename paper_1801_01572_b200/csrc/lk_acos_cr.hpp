@@ -2,11 +2,12 @@
 // away from a rounding boundary (host and device).
 //
 // The reference's FPFH frame-source test (proj/src/fpfh.cpp:28) compares
-// std::acos(|a1|) > std::acos(|a2|) with the host glibc, whose acos is not
-// correctly rounded: measured here on 2e7 uniform and cubed arguments, 0.079 %
-// of its results differ from the correctly rounded value, every one of them
-// with the exact value within 0.0212 ulp of a rounding midpoint (it returns
-// the other neighbour there). So wherever the exact acos lies farther than
+// std::acos(|a1|) > std::acos(|a2|) with the host glibc (2.39 here), whose
+// acos is not correctly rounded: measured against libquadmath's acosq on
+// 3.2e8 arguments (uniform, cubed, and 1 - cubed), 0.08-0.12 % of its results
+// differ from the correctly rounded value, every one of them with the exact
+// value within 0.0219 ulp of a rounding midpoint (it returns the other
+// neighbour there). So wherever the exact acos lies farther than
 // kAcosSafeUlp from every midpoint, glibc returns the correctly rounded value,
 // and the device can evaluate the comparison itself; only the rest goes to the
 // host's libm. tests/test_acos_cr.py re-checks this premise against the glibc
@@ -31,7 +32,7 @@
 
 namespace lkacos {
 
-constexpr double kAcosSafeUlp = 0.05;  // 2.4x the largest deviation measured
+constexpr double kAcosSafeUlp = 0.05;  // 2.3x the largest deviation measured
 
 struct DD {
     double hi, lo;
