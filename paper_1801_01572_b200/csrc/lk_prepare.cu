@@ -243,10 +243,11 @@ __device__ __forceinline__ V3 cross(V3 a, V3 b) {
 }
 
 // The reference's frame-source test is acos(|a1|) > acos(|a2|) evaluated with
-// the host libm's acos, which is not correctly rounded. When |a1| and |a2|
-// are more than 1e-15 apart the rounded values are certainly ordered like the
-// arguments (acos is decreasing with |slope| >= 1, ulp(acos) <= 2.3e-16 on
-// [0, pi/2], libm error < 1 ulp). Closer pairs -- common on noisy planar
+// the host libm's acos, which is not correctly rounded but within 0.522 ulp
+// (lk_acos_cr.hpp). When |a1| and |a2| are more than 2.5e-16 apart the libm
+// values are certainly ordered like the arguments (acos is decreasing with
+// |slope| >= 1 and ulp(acos) <= 2.22e-16 on [0, pi/2], so the exact values
+// are more than 2 x 0.522 ulp apart). Closer pairs -- common on noisy planar
 // faces, where normals agree to the last bits -- go to list A: k_spfh_decide_a
 // settles those whose outcome does not depend on how glibc rounds near a
 // midpoint (lk_acos_cr.hpp), the rest (~5 % of the ties) are decided on the
@@ -254,7 +255,7 @@ __device__ __forceinline__ V3 cross(V3 a, V3 b) {
 // 1 swap, 2 undecided.
 __device__ __forceinline__ int swap_decision(double x1, double x2) {
     if (!(x1 <= 1.0 && x2 <= 1.0)) return 0;  // acos of |a| > 1 is NaN: never greater
-    if (fabs(x1 - x2) > 1e-15) return x1 < x2 ? 1 : 0;
+    if (fabs(x1 - x2) > 2.5e-16) return x1 < x2 ? 1 : 0;
     if (x1 == x2) return 0;
     return 2;
 }

@@ -528,6 +528,29 @@ void lks_acos_greater_sweep(uint64_t seed, int64_t n, int64_t* decided, int64_t*
     *wrong = w;
 }
 
+// swap_decision's first rule (csrc/lk_prepare.cu): arguments more than
+// 2.5e-16 apart have libm acos values ordered like the exact ones
+void lks_acos_threshold_sweep(uint64_t seed, int64_t n, int64_t* checked, int64_t* wrong) {
+    uint64_t s = seed | 1u;
+    int64_t c = 0, w = 0;
+    for (int64_t k = 0; k < n; ++k) {
+        s ^= s << 13;
+        s ^= s >> 7;
+        s ^= s << 17;
+        double x1 = static_cast<double>(s >> 11) * 0x1p-53;
+        if (k % 3 == 1) x1 = x1 * x1 * x1;
+        if (k % 3 == 2) x1 = 1.0 - x1 * x1 * x1;
+        // the smallest step above 2.5e-16, plus a few ulps
+        double x2 = x1 + 2.5e-16;
+        for (int j = static_cast<int>(s & 3u); j >= 0; --j) x2 = std::nextafter(x2, 2.0);
+        if (!(x2 <= 1.0) || !(x2 - x1 > 2.5e-16)) continue;
+        ++c;
+        if (!(std::acos(x1) > std::acos(x2))) ++w;
+    }
+    *checked = c;
+    *wrong = w;
+}
+
 void lks_acos_cr_sweep(uint64_t seed, int64_t n, int64_t* decided, int64_t* wrong) {
     uint64_t s = seed | 1u;
     int64_t d = 0, w = 0;

@@ -33,6 +33,12 @@ def test_acos_greater_equals_libm_on_near_ties():
     assert decided > 0.9 * 4_000_000
 
 
+def test_acos_order_beyond_threshold():
+    # swap_decision settles |x1 - x2| > 2.5e-16 by the argument order alone
+    checked, wrong = _sweep("lks_acos_threshold_sweep", 11, 4_000_000)
+    assert wrong == 0 and checked > 3_900_000
+
+
 def test_acos_cr_edge_arguments():
     L = abi.synth_lib()
     xs = np.array([0.0, 1.0, 0.5, math.cos(1.0), 1e-300, 5e-324, 0.999999, 0.9999999, 1.0 - 2.0 ** -53,
