@@ -688,35 +688,42 @@ def run_b200(args):
     value = w_step * args.steps / (total_ms / 1e3)
 
     # ---- end-to-end leg through the public API from pinned host memory
-    e2e_steps = args.e2e_steps or max(3, min(args.steps, 5))
+    e2e_steps = args.e2e_steps or 20
+    e2e_warm = max(3, args.warmup)  # untimed: the first calls grow the memory pool and pinned staging
     e2e_times = []
     h2d = d2h = 0
-    for k in range(e2e_steps + 1):
+    rec_bytes = abi.C.sizeof(abi.lk_reg_record)
+    for k in range(e2e_steps + e2e_warm):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
-        c2 = lk.prepare_registration(src_h, tgt_h, params)
-        c2.set_stream(stream.cuda_stream)
-        xbuf.zero_()
-        lk.run_hypotheses_range(c2, params, begin, end, slot_ptr)
-        if world > 1:
+        if world == 1:
+            # one process, one GPU: the drop-in call itself (lk_register_global:
+            # prepare, hypotheses, record readback, merge)
+            res = lk.register_global(src_h, tgt_h, params)
+            out_bytes = rec_bytes
+        else:
+            c2 = lk.prepare_registration(src_h, tgt_h, params)
+            c2.set_stream(stream.cuda_stream)
+            xbuf.zero_()
+            lk.run_hypotheses_range(c2, params, begin, end, slot_ptr)
             dist.all_reduce(xbuf)
-        host = xbuf.cpu().numpy()
-        res = lk.merge_records(lk.records_from_bytes(host), c2.n_source)
+            host = xbuf.cpu().numpy()
+            res = lk.merge_records(lk.records_from_bytes(host), c2.n_source)
+            out_bytes = host.nbytes
+            c2.close()
         t1 = time.perf_counter()
-        if k > 0:
+        if k >= e2e_warm:
             e2e_times.append(t1 - t0)
-        ns2, nt2 = c2.n_source, c2.n_target
         # bytes copied this step: the raw clouds (positions + normals) in; out,
-        # the record buffer plus the library's control readbacks per cloud
-        # side (voxel count + normal check 8 B, FPFH staging head: 16 B of
-        # counts, 4096 acos-tie records of 16 B and 64 theta-edge records of
-        # 96 B, cloud stats 16 B) and the EvalGrid's bounds and block total
-        # (28 B); acos ties beyond the staged 4096 add 16 B each (not counted)
+        # the record(s) plus the library's control readbacks per cloud side
+        # (voxel count + normal check 8 B, FPFH staging head: 20 B of counts,
+        # 2048 acos records of 32 B and 64 theta-edge records of 96 B, cloud
+        # stats 16 B) and the EvalGrid's bounds and block total (28 B); acos
+        # records beyond the staged 2048 add 32 B each (not counted)
         h2d = 48 * (src_h.size() + tgt_h.size())
-        d2h = 2 * (8 + 16 + 4096 * 16 + 64 * 96 + 16) + 28 + host.nbytes
-        c2.close()
+        d2h = 2 * (8 + 20 + 2048 * 32 + 64 * 96 + 16) + 28 + out_bytes
     e2e_s = torch.tensor([statistics.mean(e2e_times)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
@@ -727,22 +734,24 @@ def run_b200(args):
     src_p = lk.PointCloud(np.array(pair.source.positions), np.array(pair.source.normals))
     tgt_p = lk.PointCloud(np.array(pair.target.positions), np.array(pair.target.normals))
     pg_times = []
-    for k in range(e2e_steps + 1):
+    for k in range(e2e_steps + e2e_warm):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
-        c3 = lk.prepare_registration(src_p, tgt_p, params)
-        c3.set_stream(stream.cuda_stream)
-        xbuf.zero_()
-        lk.run_hypotheses_range(c3, params, begin, end, slot_ptr)
-        if world > 1:
+        if world == 1:
+            lk.register_global(src_p, tgt_p, params)
+        else:
+            c3 = lk.prepare_registration(src_p, tgt_p, params)
+            c3.set_stream(stream.cuda_stream)
+            xbuf.zero_()
+            lk.run_hypotheses_range(c3, params, begin, end, slot_ptr)
             dist.all_reduce(xbuf)
-        lk.merge_records(lk.records_from_bytes(xbuf.cpu().numpy()), c3.n_source)
+            lk.merge_records(lk.records_from_bytes(xbuf.cpu().numpy()), c3.n_source)
+            c3.close()
         t1 = time.perf_counter()
-        if k > 0:
+        if k >= e2e_warm:
             pg_times.append(t1 - t0)
-        c3.close()
     pg_s = torch.tensor([statistics.mean(pg_times)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(pg_s, op=dist.ReduceOp.MAX)
@@ -762,8 +771,12 @@ def run_b200(args):
             "kernel_ms_per_step": {k: v / max(runs, 1) for k, v in ph.items()},
             "e2e": {"value": w_step / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h), "ms_per_registration": e2e_s * 1e3,
-                    "note": "prepare_registration on the device (H2D of the raw pinned clouds, voxel "
-                            "downsample, FPFH, feature match, EvalGrid) + hypotheses + exchange + merge"},
+                    "steps": len(e2e_times), "statistic": "mean",
+                    "note": ("lk_register_global from page-locked host clouds: H2D of the raw clouds, voxel "
+                             "downsample, FPFH, feature match, EvalGrid, hypotheses, record readback, merge"
+                             if world == 1 else
+                             "prepare_registration from page-locked host clouds + the rank's hypotheses + the "
+                             "record all-reduce + merge")},
             "e2e_pageable": {"value": w_step / pg_s, "unit": UNIT, "ms_per_registration": pg_s * 1e3,
                              "h2d_bytes_per_step": int(h2d),
                              "note": "the e2e leg from pageable numpy arrays (what a drop-in register_global "

@@ -33,7 +33,11 @@ def main():
         r = lk.register_global(clouds[0], clouds[1], params)
         ts.append(time.perf_counter() - t0)
         idx = r.hypothesis_index if r else -1
-    print(f"e2e median {1e3 * statistics.median(ts):.3f} ms  min {1e3 * min(ts):.3f} ms  index {idx}")
+    q = sorted(ts)
+    pct = {p: 1e3 * q[min(len(q) - 1, int(p / 100 * len(q)))] for p in (10, 50, 90, 99)}
+    print(f"e2e median {1e3 * statistics.median(ts):.3f} ms  mean {1e3 * statistics.mean(ts):.3f} ms  "
+          f"min {1e3 * min(ts):.3f} ms  p10/p50/p90/p99 {pct[10]:.3f}/{pct[50]:.3f}/{pct[90]:.3f}/{pct[99]:.3f}  "
+          f"index {idx}")
 
 
 if __name__ == "__main__":
