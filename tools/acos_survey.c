@@ -16,7 +16,8 @@ static uint64_t s = 0x9e3779b97f4a7c15ull;
 static uint64_t nx(void){ s ^= s << 13; s ^= s >> 7; s ^= s << 17; return s; }
 int main(int argc, char** argv) {
     long N = argc > 1 ? atol(argv[1]) : 10000000;
-    long mism = 0; double maxd = 0, mind_mis = 1;
+    long mism = 0;
+    double maxd = 0;
     for (long k = 0; k < N; ++k) {
         double x = (double)(nx() >> 11) * 0x1p-53;  // [0,1)
         if (k % 3 == 1) x = x * x * x; else if (k % 3 == 2) x = 1.0 - x * x * x;                    // more small values
