@@ -125,70 +125,102 @@ __global__ void k_pad_features(const float* __restrict__ f, int64_t n, float4* _
 // source. Target tiles staged in shared memory and read as broadcasts; four
 // targets at a time, the lane pairs (0,1) and (2,3) of Eigen's 4-lane
 // accumulators as packed FP32x2 chains (two FMUL + one FADD2 per two bins).
+// Two source points per thread (i and i + kFnnThreads of the block's
+// 2 * kFnnThreads): every staged target bin read from shared memory feeds
+// both, halving the loads per score.
 __global__ void __launch_bounds__(kFnnThreads) k_fnn_partial(const float4* __restrict__ sf, int64_t ns,
                                                              const float4* __restrict__ tf,
                                                              const float* __restrict__ q2, int64_t nt,
                                                              int64_t chunk, BestF* __restrict__ partial) {
     __shared__ float4 s_t[kFnnTile * (kFnnPad / 4)];
     __shared__ float s_q2[kFnnTile];
-    const int64_t i = blockIdx.x * static_cast<int64_t>(kFnnThreads) + threadIdx.x;
-    float4 s[kFnnPad / 4];
+    const int64_t i0 = blockIdx.x * static_cast<int64_t>(2 * kFnnThreads) + threadIdx.x;
+    const int64_t i1 = i0 + kFnnThreads;
+    float2 xa01[8], xa23[8], xb01[8], xb23[8];
+    float xa32, xb32;
+    {
+        float4 s[kFnnPad / 4];
 #pragma unroll
-    for (int q = 0; q < kFnnPad / 4; ++q) s[q] = i < ns ? sf[i * (kFnnPad / 4) + q] : make_float4(0, 0, 0, 0);
-    float2 x01[8], x23[8];
+        for (int q = 0; q < kFnnPad / 4; ++q) s[q] = i0 < ns ? sf[i0 * (kFnnPad / 4) + q] : make_float4(0, 0, 0, 0);
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-        x01[q] = make_float2(s[q].x, s[q].y);
-        x23[q] = make_float2(s[q].z, s[q].w);
+        for (int q = 0; q < 8; ++q) {
+            xa01[q] = make_float2(s[q].x, s[q].y);
+            xa23[q] = make_float2(s[q].z, s[q].w);
+        }
+        xa32 = s[8].x;
+#pragma unroll
+        for (int q = 0; q < kFnnPad / 4; ++q) s[q] = i1 < ns ? sf[i1 * (kFnnPad / 4) + q] : make_float4(0, 0, 0, 0);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            xb01[q] = make_float2(s[q].x, s[q].y);
+            xb23[q] = make_float2(s[q].z, s[q].w);
+        }
+        xb32 = s[8].x;
     }
-    const float x32 = s[8].x;
     const int64_t j_begin = blockIdx.y * chunk;
     const int64_t j_end = j_begin + chunk < nt ? j_begin + chunk : nt;
-    float best_s = __int_as_float(0x7f800000);
-    int32_t best_j = -1;
+    float best_a = __int_as_float(0x7f800000), best_b = best_a;
+    int32_t ja = -1, jb = -1;
     for (int64_t j0 = j_begin; j0 < j_end; j0 += kFnnTile) {
         const int tile = static_cast<int>(j_end - j0 < kFnnTile ? j_end - j0 : kFnnTile);
         __syncthreads();
         for (int q = threadIdx.x; q < tile * (kFnnPad / 4); q += kFnnThreads) s_t[q] = tf[j0 * (kFnnPad / 4) + q];
         for (int q = threadIdx.x; q < tile; q += kFnnThreads) s_q2[q] = q2[j0 + q];
         __syncthreads();
-        auto take = [&](float sc, int jj) {
-            if (sc < best_s || best_j < 0) {
-                best_s = sc;
-                best_j = static_cast<int32_t>(j0 + jj);
+        auto take = [&](float sc, int jj, float& bs, int32_t& bj) {
+            if (sc < bs || bj < 0) {
+                bs = sc;
+                bj = static_cast<int32_t>(j0 + jj);
             }
         };
         int jj = 0;
-        for (; jj + 4 <= tile; jj += 4) {
-            float2 c01[4], c23[4];
+        for (; jj + 2 <= tile; jj += 2) {
+            float2 a01[2], a23[2], b01[2], b23[2];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < 2; ++u) {
                 const float4 y = s_t[(jj + u) * (kFnnPad / 4)];
-                c01[u] = mul_pair(y.x, x01[0].x, y.y, x01[0].y);  // 0 + a b == a b (features are >= 0)
-                c23[u] = mul_pair(y.z, x23[0].x, y.w, x23[0].y);
+                a01[u] = mul_pair(y.x, xa01[0].x, y.y, xa01[0].y);  // 0 + a b == a b (features are >= 0)
+                a23[u] = mul_pair(y.z, xa23[0].x, y.w, xa23[0].y);
+                b01[u] = mul_pair(y.x, xb01[0].x, y.y, xb01[0].y);
+                b23[u] = mul_pair(y.z, xb23[0].x, y.w, xb23[0].y);
             }
 #pragma unroll
             for (int q = 1; q < 8; ++q)
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
+                for (int u = 0; u < 2; ++u) {
                     const float4 y = s_t[(jj + u) * (kFnnPad / 4) + q];
-                    c01[u] = add2(mul_pair(y.x, x01[q].x, y.y, x01[q].y), c01[u]);
-                    c23[u] = add2(mul_pair(y.z, x23[q].x, y.w, x23[q].y), c23[u]);
+                    a01[u] = add2(mul_pair(y.x, xa01[q].x, y.y, xa01[q].y), a01[u]);
+                    a23[u] = add2(mul_pair(y.z, xa23[q].x, y.w, xa23[q].y), a23[u]);
+                    b01[u] = add2(mul_pair(y.x, xb01[q].x, y.y, xb01[q].y), b01[u]);
+                    b23[u] = add2(mul_pair(y.z, xb23[q].x, y.w, xb23[q].y), b23[u]);
                 }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const float2 p = add2(c01[u], c23[u]);  // (c0 + c2, c1 + c3)
-                float cc = __fadd_rn(p.x, p.y);
-                cc = __fadd_rn(cc, __fmul_rn(s_t[(jj + u) * (kFnnPad / 4) + 8].x, x32));
-                take(__fsub_rn(s_q2[jj + u], __fmul_rn(2.0f, cc)), jj + u);
+            for (int u = 0; u < 2; ++u) {
+                const float y32 = s_t[(jj + u) * (kFnnPad / 4) + 8].x, qq = s_q2[jj + u];
+                const float2 pa = add2(a01[u], a23[u]), pb = add2(b01[u], b23[u]);  // (c0 + c2, c1 + c3)
+                float ca = __fadd_rn(pa.x, pa.y), cb = __fadd_rn(pb.x, pb.y);
+                ca = __fadd_rn(ca, __fmul_rn(y32, xa32));
+                cb = __fadd_rn(cb, __fmul_rn(y32, xb32));
+                take(__fsub_rn(qq, __fmul_rn(2.0f, ca)), jj + u, best_a, ja);
+                take(__fsub_rn(qq, __fmul_rn(2.0f, cb)), jj + u, best_b, jb);
             }
         }
         for (; jj < tile; ++jj) {
             const float* t = reinterpret_cast<const float*>(s_t + jj * (kFnnPad / 4));
-            take(eigen_score(s_q2[jj], t, reinterpret_cast<const float*>(s)), jj);
+            float fa[kFnnPad], fb[kFnnPad];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                fa[4 * q] = xa01[q].x, fa[4 * q + 1] = xa01[q].y, fa[4 * q + 2] = xa23[q].x, fa[4 * q + 3] = xa23[q].y;
+                fb[4 * q] = xb01[q].x, fb[4 * q + 1] = xb01[q].y, fb[4 * q + 2] = xb23[q].x, fb[4 * q + 3] = xb23[q].y;
+            }
+            fa[32] = xa32;
+            fb[32] = xb32;
+            take(eigen_score(s_q2[jj], t, fa), jj, best_a, ja);
+            take(eigen_score(s_q2[jj], t, fb), jj, best_b, jb);
         }
     }
-    if (i < ns) partial[blockIdx.y * ns + i] = BestF{best_s, best_j};
+    if (i0 < ns) partial[blockIdx.y * ns + i0] = BestF{best_a, ja};
+    if (i1 < ns) partial[blockIdx.y * ns + i1] = BestF{best_b, jb};
 }
 
 // chunks in ascending j order, strict <: the lowest index wins ties
@@ -339,7 +371,7 @@ cudaError_t feature_nn(const float* d_sf, int64_t ns, const float* d_tf, int64_t
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t src_blocks = (ns + kFnnThreads - 1) / kFnnThreads;
+    const int64_t src_blocks = (ns + 2 * kFnnThreads - 1) / (2 * kFnnThreads);
     int64_t n_chunks = (8 * sms + src_blocks - 1) / src_blocks;
     if (n_chunks < 1) n_chunks = 1;
     if (n_chunks > (nt + kFnnTile - 1) / kFnnTile) n_chunks = (nt + kFnnTile - 1) / kFnnTile;
