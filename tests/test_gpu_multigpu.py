@@ -6,6 +6,7 @@ strict total order, so any sharding gives the 1-GPU result bit for bit. These
 run on however many B200s the box has: with one GPU the G > 1 cases check the
 error path, and the NCCL code runs with one rank (ncclCommInitRank +
 ncclAllReduce over a 1-rank communicator)."""
+import json
 import multiprocessing as mp
 import os
 
@@ -129,3 +130,33 @@ def test_verify_batch_device_count(pair):
     if lk.device_count() < 2:
         with pytest.raises(lk.Error):
             lk.verify_batch(Q, P, I, T, T, lk.VerifyParams(device=0, device_count=2))
+
+
+def _free_port():
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_bench_multi_rank_product_path_one_device():
+    """bench.py's N > 1 path -- contiguous hypothesis shares per rank, the rank
+    records exchanged and merged -- with two ranks on cuda:0 (LK_BENCH_ONE_DEVICE:
+    gloo carries the exchange, since NCCL refuses two ranks on one device). The
+    merged result must be the reference's B1 result (tests/golden/ref_golden.json)."""
+    import json as _json
+    import subprocess
+    import sys
+    g = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "ref_golden.json")))["b1"]
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, LK_BENCH_ONE_DEVICE="1", OMP_NUM_THREADS="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", "bench.py", "--gpus", "2", "--steps", "3",
+           "--warmup", "3", "--e2e-steps", "2", "--no-extras", "--no-cpu-baseline"]
+    out = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = _json.loads([x for x in out.stdout.splitlines() if x.startswith("{")][-1])
+    assert line["n_gpus"] == 2
+    assert line["hypothesis_index"] == g["index"]
+    assert {k: line["stats_per_step"][k] for k in g["stats"]} == g["stats"]
+    assert line["stats_per_step"]["w_ref"] == g["oracle_w_ref"]
