@@ -1892,7 +1892,7 @@ cudaError_t run_hypotheses_range(const SourceView& src, const double* d_tgt_pos,
     }
     if (events) cudaEventRecord(events[1], stream);
     if (count > 0) {
-        k_kabsch<<<sm_count * 8, 128, 0, stream>>>(src.pos, d_tgt_pos, rb.surv_index, rb.surv_ids, rb.cand_index,
+        k_kabsch<<<sm_count * 8, 32, 0, stream>>>(src.pos, d_tgt_pos, rb.surv_index, rb.surv_ids, rb.cand_index,
                                                    rb.cand_rt, rb.counters, rb.u_sum, rb.u_done, rb.u_cap);
     }
     if (events) cudaEventRecord(events[2], stream);
