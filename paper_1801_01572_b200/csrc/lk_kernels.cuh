@@ -267,8 +267,8 @@ cudaError_t make_records(const double* d_pos, const double* d_nrm, int64_t n, do
 // Samples, pre-rejects and fits hypotheses [begin, end); scores the
 // candidates; reduces the per-run best into `record` (an lk_reg_record, device).
 // `events` (nullable): kPhaseEvents events on the launch stream bracketing the
-// phases k_hyp_sample | k_kabsch | k_prep_fast(_fine) | k_score_split |
-// k_score_resolve | k_score + k_score_exits + k_score_finalists.
+// phase events: [0] k_hyp_sample [1] k_kabsch [2] [3] the scorer
+// (k_score_units + k_score_cta) [4] [5] [6] (the last three coincide)
 constexpr int kPhaseEvents = 7;
 cudaError_t run_hypotheses_range(const SourceView& src, const double* d_tgt_pos, const int32_t* d_cache,
                                  const GridView& grid, const ScoreParams& sp, uint64_t seed, double tau, int64_t begin,
