@@ -106,35 +106,14 @@ __global__ void k_verify_src(const double* __restrict__ p, const double* __restr
 }
 
 // One CTA of kSumThreads per pair. The points are staged kSumThreads at a
-// time (coalesced): every thread computes its point's nine contributions --
-// the a^T a entries (0,0) (0,1) (0,2) (1,1) (1,2) (2,2) with a = -[q]x, then
-// q.x, q.y, q.z -- into shared memory, and lane j < 9 of warp 0 adds column j
-// over the staged hits in point order: the reference's sequential sums
-// (line_process.cpp:24-28), with the loads off the dependent add chain. The
-// same for the evaluate_hypothesis sq_sum over the source points (lane 9).
+// time (coalesced): every hit computes its nine contributions -- the a^T a
+// entries (0,0) (0,1) (0,2) (1,1) (1,2) (2,2) with a = -[q]x, then q.x, q.y,
+// q.z -- into shared memory at its rank among the chunk's hits, and lane j < 9
+// of warp 0 adds column j over them in point order: the reference's
+// sequential sums (line_process.cpp:24-28). The same for the
+// evaluate_hypothesis sq_sum over the source points (lane 9 of warp 1).
 // Counts are popcounts of the hit ballots.
 // out per pair: 10 doubles (9 edge sums, sq_sum) then 3 int64 at [10..12].
-// acc + v[j] for the set bits j of m in ascending order (the sequential sum),
-// four shared-memory loads issued ahead of their dependent adds
-__device__ __forceinline__ double add_in_order(double acc, const double* v, unsigned m) {
-    while (m) {
-        double x[4];
-        int k = 0;
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            if (m) {
-                x[u] = v[__ffs(m) - 1];
-                m &= m - 1;
-                k = u + 1;
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-            if (u < k) acc += x[u];
-    }
-    return acc;
-}
-
 constexpr int kSumThreads = 256;
 constexpr int kSumWarps = kSumThreads / 32;
 
@@ -146,8 +125,13 @@ __global__ void __launch_bounds__(kSumThreads) k_verify_sums(const double* __res
                                                              const uint8_t* __restrict__ inlier,
                                                              const double* __restrict__ addend,
                                                              double* __restrict__ out) {
+    // the chunk's hits compacted in point order (ballot prefix), so the
+    // sequential sums read consecutive shared-memory words, loads ahead of
+    // the dependent adds; lanes 0-8 of warp 0 run the nine edge sums, lane 9
+    // of warp 1 the sq_sum, each over the staged chunk
     __shared__ double s_c[9][kSumThreads + 1];
-    __shared__ unsigned s_m[kSumWarps];
+    __shared__ double s_a[kSumThreads + 1];
+    __shared__ int s_wq[kSumWarps + 1], s_wp[kSumWarps + 1];
     __shared__ unsigned long long s_cnt[3];
     const int k = blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -155,18 +139,40 @@ __global__ void __launch_bounds__(kSumThreads) k_verify_sums(const double* __res
     double acc = 0.0, sq = 0.0;
     unsigned long long n_edge = 0, n_over = 0, n_inl = 0;
     const int64_t q0 = offq[k], q1 = offq[k + 1], p0 = offp[k], p1 = offp[k + 1];
-    for (int64_t base = q0; base < q1; base += kSumThreads) {
-        const int64_t i = base + threadIdx.x;
+    const int64_t nq_c = (q1 - q0 + kSumThreads - 1) / kSumThreads, np_c = (p1 - p0 + kSumThreads - 1) / kSumThreads;
+    const int64_t chunks = nq_c > np_c ? nq_c : np_c;
+    const unsigned below = (1u << lane) - 1u;
+    for (int64_t c = 0; c < chunks; ++c) {
+        // edge_info chunk c of Q and evaluate_hypothesis chunk c of P, side by side
+        const int64_t i = q0 + c * kSumThreads + threadIdx.x;
         const bool hit = i < q1 && edge_hit[i];
         const unsigned m = __ballot_sync(0xffffffffu, hit);
+        const int64_t ip = p0 + c * kSumThreads + threadIdx.x;
+        const bool in = ip < p1;
+        const unsigned mo = __ballot_sync(0xffffffffu, in && overlap_hit[ip]);
+        const bool inl = in && inlier[ip];
+        const unsigned mi = __ballot_sync(0xffffffffu, inl);
         if (lane == 0) {
-            s_m[warp] = m;
+            s_wq[warp + 1] = __popc(m);
+            s_wp[warp + 1] = __popc(mi);
             n_edge += __popc(m);
+            n_over += __popc(mo);
+            n_inl += __popc(mi);
         }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            s_wq[0] = 0;
+            s_wp[0] = 0;
+            for (int w = 0; w < kSumWarps; ++w) {
+                s_wq[w + 1] += s_wq[w];
+                s_wp[w + 1] += s_wp[w];
+            }
+        }
+        __syncthreads();
         if (hit) {
+            const int t = s_wq[warp] + __popc(m & below);
             const V3 v = ld3(q, i);
             const double a[3][3] = {{-0.0, v.z, -v.y}, {-v.z, -0.0, v.x}, {v.y, -v.x, -0.0}};
-            const int t = threadIdx.x;
             s_c[0][t] = (a[0][0] * a[0][0] + a[1][0] * a[1][0]) + a[2][0] * a[2][0];
             s_c[1][t] = (a[0][0] * a[0][1] + a[1][0] * a[1][1]) + a[2][0] * a[2][1];
             s_c[2][t] = (a[0][0] * a[0][2] + a[1][0] * a[1][2]) + a[2][0] * a[2][2];
@@ -177,26 +183,33 @@ __global__ void __launch_bounds__(kSumThreads) k_verify_sums(const double* __res
             s_c[7][t] = v.y;
             s_c[8][t] = v.z;
         }
+        if (inl) s_a[s_wp[warp] + __popc(mi & below)] = addend[ip];
         __syncthreads();
-        if (warp == 0 && lane < 9)
-            for (int w = 0; w < kSumWarps; ++w) acc = add_in_order(acc, s_c[lane] + 32 * w, s_m[w]);
-        __syncthreads();
-    }
-    for (int64_t base = p0; base < p1; base += kSumThreads) {
-        const int64_t i = base + threadIdx.x;
-        const bool in = i < p1;
-        const unsigned mo = __ballot_sync(0xffffffffu, in && overlap_hit[i]);
-        const bool inl = in && inlier[i];
-        const unsigned m = __ballot_sync(0xffffffffu, inl);
-        if (lane == 0) {
-            s_m[warp] = m;
-            n_over += __popc(mo);
-            n_inl += __popc(m);
+        if (warp == 0 && lane < 9) {
+            const double* col = s_c[lane];
+            const int cnt = s_wq[kSumWarps];
+            int e = 0;
+            for (; e + 4 <= cnt; e += 4) {
+                const double x0 = col[e], x1 = col[e + 1], x2 = col[e + 2], x3 = col[e + 3];
+                acc += x0;
+                acc += x1;
+                acc += x2;
+                acc += x3;
+            }
+            for (; e < cnt; ++e) acc += col[e];
         }
-        if (inl) s_c[0][threadIdx.x] = addend[i];
-        __syncthreads();
-        if (warp == 0 && lane == 9)
-            for (int w = 0; w < kSumWarps; ++w) sq = add_in_order(sq, s_c[0] + 32 * w, s_m[w]);
+        if (warp == 1 && lane == 9) {
+            const int cnt = s_wp[kSumWarps];
+            int e = 0;
+            for (; e + 4 <= cnt; e += 4) {
+                const double x0 = s_a[e], x1 = s_a[e + 1], x2 = s_a[e + 2], x3 = s_a[e + 3];
+                sq += x0;
+                sq += x1;
+                sq += x2;
+                sq += x3;
+            }
+            for (; e < cnt; ++e) sq += s_a[e];
+        }
         __syncthreads();
     }
     if (lane == 0) {
@@ -207,7 +220,7 @@ __global__ void __launch_bounds__(kSumThreads) k_verify_sums(const double* __res
     __syncthreads();
     double* o = out + 16 * k;
     if (warp == 0 && lane < 9) o[lane] = acc;
-    if (warp == 0 && lane == 9) o[9] = sq;
+    if (warp == 1 && lane == 9) o[9] = sq;
     if (threadIdx.x == 0) {
         long long* c = reinterpret_cast<long long*>(o);
         c[10] = static_cast<long long>(s_cnt[0]);
