@@ -10,11 +10,25 @@
 
 namespace lkk {
 
+// Cells c along one axis whose entries ([c - delta, c + 1 + delta]) can lie
+// within h of q: c in [lo, hi]. h carries a relative and an absolute slack
+// over sqrt(rem) so that every cell the per-cell FP32 test
+// (gap^2 + rest <= bound) would pass is inside: the range is a superset.
+__device__ __forceinline__ void ring_reach(float q, float dl, float rem, float bnd, int& lo, int& hi) {
+    // sqrt.approx (relative error ~2^-22) is far inside the slack
+    float h;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(h) : "f"(fmaxf(rem, 0.0f) * 1.0001f + bnd * 1e-5f));
+    h += 1e-3f;
+    lo = static_cast<int>(ceilf(q - dl - h - 1.0f));
+    hi = static_cast<int>(floorf(q + dl + h));
+}
+
 // Visits the entries of the cells of the cube shell of radius r around
 // (cx, cy, cz) that can hold a point within sqrt(bound()) cells of q: a
-// cell's entries lie within [c - delta, c + 1 + delta] per axis, so a cell
-// whose box is farther than that from q is skipped without loading it. The
-// bound is re-read as entries are visited (it shrinks as the best improves).
+// cell's entries lie within [c - delta, c + 1 + delta] per axis, so a row or
+// cell whose box is farther than that from q is skipped without loading it;
+// a row's reachable cells are one contiguous CSR range. The bound is re-read
+// row by row (it shrinks as the best improves).
 template <class B, class F>
 __device__ __forceinline__ void ring_shell(const RingGrid& rg, float qx, float qy, float qz, int cx, int cy, int cz,
                                            int r, B&& bound, F&& f) {
@@ -36,13 +50,24 @@ __device__ __forceinline__ void ring_shell(const RingGrid& rg, float qx, float q
             if (gxy > bound()) continue;
             const int64_t row = (static_cast<int64_t>(x) * rg.ny + y) * rg.nz;
             const bool edge = dx == -r || dx == r || dy == -r || dy == r;
-            const int step = edge ? 1 : (r > 0 ? 2 * r : 1);
-            for (int z = cz - r; z <= cz + r; z += step) {
-                if (z < 0 || z >= rg.nz) continue;
-                const float gz = gap(qz, z);
-                if (gxy + gz * gz > bound()) continue;
-                const int32_t s0 = __ldg(rg.start + row + z), s1 = __ldg(rg.start + row + z + 1);
-                for (int32_t e = s0; e < s1; ++e) f(e);
+            // the cells of the row the bound reaches (a superset of the
+            // per-cell test): one contiguous CSR range per row
+            int lz, hz;
+            ring_reach(qz, dl, bound() - gxy, bound(), lz, hz);
+            if (edge) {
+                int z0 = cz - r > lz ? cz - r : lz, z1 = cz + r < hz ? cz + r : hz;
+                z0 = z0 > 0 ? z0 : 0;
+                z1 = z1 < rg.nz - 1 ? z1 : rg.nz - 1;
+                if (z0 <= z1) {
+                    const int32_t s0 = __ldg(rg.start + row + z0), s1 = __ldg(rg.start + row + z1 + 1);
+                    for (int32_t e = s0; e < s1; ++e) f(e);
+                }
+            } else {
+                for (int z = cz - r; z <= cz + r; z += 2 * r) {  // r > 0 here: the shell's two caps
+                    if (z < 0 || z >= rg.nz || z < lz || z > hz) continue;
+                    const int32_t s0 = __ldg(rg.start + row + z), s1 = __ldg(rg.start + row + z + 1);
+                    for (int32_t e = s0; e < s1; ++e) f(e);
+                }
             }
         }
     }
@@ -217,19 +242,6 @@ __device__ __forceinline__ void ring_top3_sel(float d2, int32_t o, float& f1, fl
     f2 = c1 ? f1 : (c2 ? d2 : f2);
     o1 = c1 ? o : o1;
     f1 = c1 ? d2 : f1;
-}
-
-// Cells c along one axis whose entries ([c - delta, c + 1 + delta]) can lie
-// within h of q: c in [lo, hi]. h carries a relative and an absolute slack
-// over sqrt(rem) so that every cell the per-cell FP32 test
-// (gap^2 + rest <= bound) would pass is inside: the range is a superset.
-__device__ __forceinline__ void ring_reach(float q, float dl, float rem, float bnd, int& lo, int& hi) {
-    // sqrt.approx (relative error ~2^-22) is far inside the slack
-    float h;
-    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(h) : "f"(fmaxf(rem, 0.0f) * 1.0001f + bnd * 1e-5f));
-    h += 1e-3f;
-    lo = static_cast<int>(ceilf(q - dl - h - 1.0f));
-    hi = static_cast<int>(floorf(q + dl + h));
 }
 
 // Visits the cells of shell r around the box [b0, b1] (r = 0: the box) that
