@@ -856,8 +856,14 @@ lk_status prepare_impl(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_pa
             ctx_finish_source(c);
             tmark("feature nn done", s, t0);
         }
-        CK(cudaStreamSynchronize(T.s));
-        CK(cudaStreamSynchronize(s));
+        // no wait for the match: each side's stats were copied ahead of its
+        // FPFH, whose list-head readback synchronised that side's stream; a
+        // side that stopped early (invalid normals, < 4 points) fails a check
+        // below before its stats are read
+        if (!(S.features && T.features)) {
+            CK(cudaStreamSynchronize(T.s));
+            CK(cudaStreamSynchronize(S.s));
+        }
         for (CloudSide* cs : {&S, &T})
             if (cs->stats) lkk::cloud_stats_decode(cs->stats, &cs->usable, &cs->max_norm);
         c->src_max_norm = S.max_norm;
@@ -868,8 +874,11 @@ lk_status prepare_impl(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_pa
             throw lk::Status(LK_TOO_FEW_POINTS, "register_global: fewer than 4 points after downsampling");
         if (S.usable < 4 || T.usable < 4)
             throw lk::Status(LK_MISSING_DATA, "register_global: fewer than 4 points with usable normals");
-        tdump();
-        if (trace_on()) std::fprintf(stderr, "[lk prepare] feature nn %8.3f ms\n", (now_s() - t0) * 1e3);
+        if (trace_on()) {
+            CK(cudaStreamSynchronize(s));
+            tdump();
+            std::fprintf(stderr, "[lk prepare] feature nn %8.3f ms\n", (now_s() - t0) * 1e3);
+        }
         if (devs.size() > 1) make_peers(c, devs, params->d_max);
     } catch (...) {
         drop(S);
