@@ -603,7 +603,7 @@ struct CloudSide {
     int status = 0;  // 5: invalid normals
     int64_t usable = 0;
     double max_norm = 0.0;
-    unsigned long long* stats = nullptr;  // pinned (the side thread's), decoded after the final sync
+    unsigned long long* stats = nullptr;  // 2 pinned words of the calling thread: usable normals, |p|max
     bool features = false;                 // feat is being computed on s
     std::exception_ptr err;
 };
@@ -651,11 +651,9 @@ void prepare_side(CloudSide& cs, double feature_radius, double normal_radius, do
             CK(lkk::estimate_normals(cs.pos, cs.n, normal_radius, origin, cs.nrm, cs.s));
             mark("normals");
         }
-        // usable normals and |p|max come back with prepare's final sync
-        thread_local unsigned long long* h_stats = nullptr;
-        if (!h_stats) CK(cudaHostAlloc(reinterpret_cast<void**>(&h_stats), 2 * sizeof(unsigned long long), 0));
-        CK(lkk::cloud_stats_async(cs.pos, cs.nrm, cs.n, h_stats, cs.s));
-        cs.stats = h_stats;
+        // usable normals and |p|max land in cs.stats (the calling thread's
+        // pinned words) ahead of the FPFH, whose readback synchronises
+        CK(lkk::cloud_stats_async(cs.pos, cs.nrm, cs.n, cs.stats, cs.s));
         // the EvalGrid (registration.cpp:249) only needs the downsampled
         // cloud: it is built on its own stream and host thread while this
         // one runs the FPFH
@@ -788,6 +786,12 @@ lk_status prepare_impl(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_pa
     S.s = c->own_stream;
     T.in = tgt;
     T.s = c->aux_stream;
+    // both sides' stats words belong to the calling thread (the target side's
+    // worker is released before they are read)
+    thread_local unsigned long long* t_stats = nullptr;
+    if (!t_stats) CK(cudaHostAlloc(reinterpret_cast<void**>(&t_stats), 4 * sizeof(unsigned long long), 0));
+    S.stats = t_stats;
+    T.stats = t_stats + 2;
     auto drop = [&](CloudSide& cs) {
         lkk::pool_free(cs.raw_pos, cs.s);
         lkk::pool_free(cs.raw_nrm, cs.s);
@@ -865,7 +869,7 @@ lk_status prepare_impl(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_pa
             CK(cudaStreamSynchronize(S.s));
         }
         for (CloudSide* cs : {&S, &T})
-            if (cs->stats) lkk::cloud_stats_decode(cs->stats, &cs->usable, &cs->max_norm);
+            if (cs->features) lkk::cloud_stats_decode(cs->stats, &cs->usable, &cs->max_norm);
         c->src_max_norm = S.max_norm;
         // the reference's check order (registration.cpp:226-245)
         if (S.status == 5 || T.status == 5)
