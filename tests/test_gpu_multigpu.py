@@ -160,3 +160,35 @@ def test_bench_multi_rank_product_path_one_device():
     assert line["hypothesis_index"] == g["index"]
     assert {k: line["stats_per_step"][k] for k in g["stats"]} == g["stats"]
     assert line["stats_per_step"]["w_ref"] == g["oracle_w_ref"]
+
+
+def test_concurrent_register_global_from_threads():
+    """Host threads calling lk_register_global at once (ctypes releases the
+    GIL): each call owns its context, streams, worker and pinned staging, so
+    every result equals the same call made alone."""
+    import threading
+    pairs = [synth.synth_registration_pair(s) for s in (1, 2, 3, 4)]
+    p = lk.RegistrationParams(hypothesis_count=60_000, seed=7)
+    alone = []
+    for pr in pairs:
+        st = lk.HypothesisStats()
+        alone.append((lk.register_global(pr.source, pr.target, p, st), st))
+    got = [None] * len(pairs)
+    errs = []
+
+    def work(k):
+        try:
+            for _ in range(3):
+                st = lk.HypothesisStats()
+                got[k] = (lk.register_global(pairs[k].source, pairs[k].target, p, st), st)
+        except Exception as e:  # reported below
+            errs.append(repr(e))
+
+    th = [threading.Thread(target=work, args=(k,)) for k in range(len(pairs))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for (ra, sa), (rb, sb) in zip(alone, got):
+        _same(ra, rb, sa, sb)
