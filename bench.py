@@ -490,6 +490,48 @@ def bench_config_a(args):
     return out
 
 
+def bench_propose_loops(args):
+    """Row f2, propose_loops (fragments.cpp:61-109): 32 fragments
+    of 4,000 random points in a 1 m cube under small random poses (every
+    pair overlaps), all (i, j <= i - 2) pairs = 465 pair overlaps of 4,000
+    queries each, one lk_propose_loops call from host arrays. Parity: the
+    proposals (i, j, overlap bits) against the reference's own propose_loops
+    (oracle/_ref) on the same input, which is also the CPU baseline."""
+    import paper_1801_01572_b200 as lk
+    from paper_1801_01572_b200 import synth
+    F, npts = 32, 4000
+    frags = [synth.random_cloud(npts, 100 + f, 0, -0.5, 0.5) for f in range(F)]
+    poses = [synth.random_transform(200 + f, 1, 0.3, 0.3) for f in range(F)]
+    lp = lk.LoopParams(overlap_radius=0.05, min_overlap=0.2)
+    lk.propose_loops(frags, poses, [], lp)  # warm-up
+    times = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        got = lk.propose_loops(frags, poses, [], lp)
+        times.append(time.perf_counter() - t0)
+    dt = min(times)
+    pairs = (F - 1) * (F - 2) // 2
+    out = {"workload": f"propose_loops: {F} fragments x {npts:,} random points (1 m cube), small random poses, "
+                       f"overlap radius 0.05, min_overlap 0.2: {pairs} pair overlaps",
+           "fragments": F, "points_per_fragment": npts, "pairs": pairs, "proposals": len(got), "ms": 1e3 * dt,
+           "pairs_per_s": pairs / dt, "queries_per_s": pairs * npts / dt,
+           "timing": "wall clock of lk_propose_loops from host arrays (H2D, posed ring grids, all pairs, host "
+                     "filter and sort), best of 3"}
+    if not args.no_cpu_baseline:
+        RF = _ref_module()
+        if RF is not None:
+            t0 = time.perf_counter()
+            ref = RF.propose_loops([f.positions for f in frags], [(T.rotation, T.translation) for T in poses], (),
+                                   0.05, 0.2)
+            cpu = time.perf_counter() - t0
+            out["parity_vs_reference"] = [(p.i, p.j, float(p.overlap).hex()) for p in got] == \
+                [(i, j, float(v).hex()) for i, j, v in ref]
+            out["cpu_baseline"] = {"kind": "reference", "cores": 1,
+                                   "sample": "oracle/_ref propose_loops on the same input (the reference loop, one "
+                                             "thread)", "ms": 1e3 * cpu, "pairs_per_s": pairs / cpu}
+    return out
+
+
 def bench_verification(args):
     """Config E: loop verification of synth_registration_pair
     seeds 1..K with their truths as measurements: edge_info(Q, P, I, truth,
@@ -837,7 +879,8 @@ def run_b200(args):
                                         "from the committed ncu capture profiles/ncu_traffic.json)"}
         if world == 1 and not args.no_extras:
             line["extras"] = {"config_A": bench_config_a(args), "icp_D": bench_icp(args),
-                              "verification_E": bench_verification(args), "explicit_B2": bench_b2(args)}
+                              "verification_E": bench_verification(args), "explicit_B2": bench_b2(args),
+                              "propose_loops_F2": bench_propose_loops(args)}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
