@@ -140,7 +140,10 @@ int lk_device_count(void);
  * all on the device: voxel downsample, estimate_normals for clouds given
  * without normals, FPFH, the feature pre-match (the binary's float matcher,
  * grid.cpp:176-213) and the EvalGrid. Throws-equivalents: LK_TOO_FEW_POINTS,
- * LK_MISSING_DATA, LK_MISSING_NORMALS. */
+ * LK_MISSING_DATA, LK_MISSING_NORMALS. Returns as soon as the checks are
+ * decided: the feature match may still run on the context's stream, which
+ * every later call on the context is ordered behind (lk_reg_ctx_set_stream
+ * first finishes the old stream's work). */
 lk_status lk_reg_prepare(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_params* params, lk_reg_ctx** out);
 /* A RegistrationContext from already-prepared parts (downsampled clouds with
  * normals + the feature match cache), as when the reference's caller fills
