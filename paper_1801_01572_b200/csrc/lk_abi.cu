@@ -23,6 +23,7 @@
 #include <condition_variable>
 #include <functional>
 #include <exception>
+#include <future>
 #include <type_traits>
 #include <vector>
 
@@ -593,7 +594,20 @@ lk_reg_ctx* ctx_new(int32_t device) {
 // (registration.cpp:226-228, 246-247); the target side also builds the
 // EvalGrid (:249). Runs on a host thread of its own; errors are kept, not
 // thrown, so both sides finish before the reference's check order decides.
+// Orders the two sides' host-staged (pageable) uploads: the target's first,
+// so that its side starts while the source's cloud is still being staged.
+struct UploadGate {
+    std::promise<void> p;
+    std::shared_future<void> f = p.get_future().share();
+    bool opened = false;
+    void open() {
+        if (!opened) p.set_value();
+        opened = true;
+    }
+};
 struct CloudSide {
+    UploadGate* wait_gate = nullptr;  // upload after this gate opens
+    UploadGate* open_gate = nullptr;  // opened once this side's upload is enqueued
     const lk_cloud* in = nullptr;
     cudaStream_t s = nullptr;
     double *raw_pos = nullptr, *raw_nrm = nullptr;
@@ -633,9 +647,11 @@ void prepare_side(CloudSide& cs, double feature_radius, double normal_radius, do
                 }
                 return d;
             };
+            if (cs.wait_gate) cs.wait_gate->f.wait();
             cs.raw_pos = up(cs.in->xyz);
             cs.raw_nrm = cs.in->nxyz ? up(cs.in->nxyz) : nullptr;
         }
+        if (cs.open_gate) cs.open_gate->open();
         mark("upload");
         CK(lkk::pool_alloc(&cs.pos, 3 * n * sizeof(double), cs.s));
         CK(lkk::pool_alloc(&cs.nrm, 3 * n * sizeof(double), cs.s));
@@ -698,6 +714,7 @@ void prepare_side(CloudSide& cs, double feature_radius, double normal_radius, do
     } catch (...) {
         cs.err = std::current_exception();
     }
+    if (cs.open_gate) cs.open_gate->open();  // never leave the other side waiting
 }
 
 // Devices of a call (lk_reg_params::device_count): `device` alone, or G
@@ -782,6 +799,7 @@ lk_status prepare_impl(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_pa
     lk_reg_ctx* c = ctx_new(devs[0]);
     tstart(c->own_stream);
     CloudSide S, T;
+    UploadGate gate;
     S.in = src;
     S.s = c->own_stream;
     T.in = tgt;
@@ -813,6 +831,11 @@ lk_status prepare_impl(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_pa
             cudaEventDestroy(landed);
             S.raw_pos = dev_upload(src->xyz, 3 * src->n, S.s);
             S.raw_nrm = src->nxyz ? dev_upload(src->nxyz, 3 * src->n, S.s) : nullptr;
+        } else {
+            // host-staged copies share the link and the host's memory
+            // bandwidth: the target's first, the source's after it
+            T.open_gate = &gate;
+            S.wait_gate = &gate;
         }
         // the two clouds are independent until the feature match: the target
         // side (H2D, downsample, FPFH, EvalGrid) runs on a second host thread

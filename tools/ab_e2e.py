@@ -1,7 +1,7 @@
 """Interleaved e2e A/B of two builds of the library (diagnostic): one worker
 process per .so (LK_LIB_OVERRIDE), each warmed up, then R rounds of K
 register_global calls alternating between the workers, so that both see the
-same box conditions. Prints per-build median / min and the paired median of
+same box conditions (LK_AB_PAGEABLE=1: from pageable numpy clouds). Prints per-build median / min and the paired median of
 per-round differences. usage: ab_e2e.py libA.so libB.so [rounds] [k]"""
 import multiprocessing as mp
 import os
@@ -19,7 +19,11 @@ def worker(lib, conn):
     from paper_1801_01572_b200 import synth
     pair = synth.depth_frame_pair()
     keep, clouds = [], []
+    pageable = os.environ.get("LK_AB_PAGEABLE") == "1"  # plain numpy clouds (the driver stages them)
     for c in (pair.source, pair.target):
+        if pageable:
+            clouds.append(lk.PointCloud(np.array(c.positions), np.array(c.normals)))
+            continue
         tp = torch.from_numpy(np.ascontiguousarray(c.positions)).pin_memory()
         tn = torch.from_numpy(np.ascontiguousarray(c.normals)).pin_memory()
         keep += [tp, tn]
