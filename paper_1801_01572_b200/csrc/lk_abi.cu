@@ -306,6 +306,9 @@ void tdump() {
     g_trace.clear();
 }
 
+double g_trace_t0 = 0.0;
+thread_local const char* t_trace_tag = "";
+
 bool trace_on() {
     static const bool on = std::getenv("LK_TRACE") != nullptr;
     return on;
@@ -455,6 +458,12 @@ bool record_better(const lk_reg_record& a, const lk_reg_record& b) {
 }
 
 }  // namespace
+
+void lkk::trace_point(const char* what, cudaStream_t s) {
+    if (trace_level() < 2) return;
+    tmark((std::string(t_trace_tag) + "   . " + what).c_str(), s, g_trace_t0);
+}
+
 
 // EvalGrid targets from this size on also get a ring grid (explicit candidates)
 constexpr int64_t kDenseTarget = 65536;
@@ -625,6 +634,7 @@ struct CloudSide {
 void prepare_side(CloudSide& cs, double feature_radius, double normal_radius, double leaf, lkk::GridStorage* grid,
                   double d_max, int device, double t0, const char* tag, cudaStream_t grid_stream = nullptr) {
     NvtxRange range(tag[0] == 's' ? "lk prepare source side" : "lk prepare target side");
+    t_trace_tag = tag;
     auto mark = [&](const char* what) {
         if (trace_level() >= 2) {
             tmark((std::string(tag) + " " + what).c_str(), cs.s, t0);
@@ -798,6 +808,7 @@ lk_status prepare_impl(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_pa
     const std::vector<int> devs = call_devices(params->device, params->device_count);
     lk_reg_ctx* c = ctx_new(devs[0]);
     tstart(c->own_stream);
+    g_trace_t0 = t0;
     CloudSide S, T;
     UploadGate gate;
     S.in = src;

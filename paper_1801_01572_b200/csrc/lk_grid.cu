@@ -9,6 +9,8 @@
 #include <cmath>
 #include <cstdint>
 
+#include <mutex>
+#include <unordered_map>
 #include <cub/device/device_scan.cuh>
 #include <vector>
 
@@ -404,6 +406,58 @@ cudaError_t exclusive_scan(const int32_t* in, int64_t n, int32_t* out, cudaStrea
     cudaFreeAsync(temp, stream);
     return e != cudaSuccess ? e : cudaGetLastError();
 }
+
+size_t scan_temp_bytes(int64_t n) {
+    size_t temp_bytes = 0;
+    if (n > 0 && n <= INT32_MAX)
+        cub::DeviceScan::InclusiveSum(nullptr, temp_bytes, static_cast<const int32_t*>(nullptr),
+                                      static_cast<int32_t*>(nullptr), static_cast<int>(n));
+    return temp_bytes > 0 ? temp_bytes : 1;
+}
+
+cudaError_t exclusive_scan(const int32_t* in, int64_t n, int32_t* out, cudaStream_t stream, void* temp,
+                           size_t temp_bytes, bool zero_first) {
+    if (zero_first) {
+        const cudaError_t e = cudaMemsetAsync(out, 0, sizeof(int32_t), stream);
+        if (e != cudaSuccess) return e;
+    }
+    if (n <= 0) return cudaSuccess;
+    if (n > INT32_MAX || temp_bytes < scan_temp_bytes(n)) return cudaErrorInvalidValue;
+    const cudaError_t e = cub::DeviceScan::InclusiveSum(temp, temp_bytes, in, out + 1, static_cast<int>(n), stream);
+    return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+struct Scratch::Entry {
+    std::mutex mu;
+    char* p = nullptr;
+    size_t cap = 0;
+};
+
+Scratch::Scratch(cudaStream_t s, size_t bytes) {
+    static std::mutex g_mu;
+    static std::unordered_map<cudaStream_t, Entry*> g_entries;
+    {
+        std::lock_guard<std::mutex> lock(g_mu);
+        Entry*& e = g_entries[s];
+        if (!e) e = new Entry();  // kept for the process (streams are pooled)
+        e_ = e;
+    }
+    e_->mu.lock();
+    if (e_->cap < bytes) {
+        // the old buffer's last users are ahead on s: a stream-ordered free
+        if (e_->p) cudaFreeAsync(e_->p, s);
+        e_->p = nullptr;
+        e_->cap = 0;
+        const size_t cap = bytes + bytes / 4;
+        err_ = cudaMallocAsync(reinterpret_cast<void**>(&e_->p), cap, s);
+        if (err_ == cudaSuccess) e_->cap = cap;
+        else e_->p = nullptr;
+    }
+    base_ = e_->p;
+    cap_ = e_->cap;
+}
+
+Scratch::~Scratch() { e_->mu.unlock(); }
 
 void GridStorage::release() {
     pool_free(start, stream);

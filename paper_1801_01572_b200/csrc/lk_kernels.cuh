@@ -18,6 +18,10 @@ inline void pool_free(void* p, cudaStream_t s) {
     if (p) cudaFreeAsync(p, s);
 }
 
+// LK_TRACE=2 only: a device-event mark on stream s inside a prepare phase
+// (defined in lk_abi.cu; a no-op otherwise).
+void trace_point(const char* what, cudaStream_t s);
+
 // Pinned host scratch for small device->host readbacks (counts, bounding
 // boxes, records), one buffer per host thread. A readback into pageable
 // memory goes through the driver's staging path and queues behind in-flight
@@ -322,6 +326,47 @@ cudaError_t score_candidates(const SourceView& src, const GridView& grid, const 
 
 // exclusive scan of n int32 into out[0..n] (out[n] = total), stream-ordered
 cudaError_t exclusive_scan(const int32_t* d_in, int64_t n, int32_t* d_out, cudaStream_t stream);
+// the same with caller-provided temporary storage (scan_temp_bytes(n)), and
+// d_out[0] left to the caller when zero_first is false: no allocation, no
+// memset, only the scan's two kernels go on the stream
+size_t scan_temp_bytes(int64_t n);
+cudaError_t exclusive_scan(const int32_t* d_in, int64_t n, int32_t* d_out, cudaStream_t stream, void* temp,
+                           size_t temp_bytes, bool zero_first);
+
+// Stream-ordered scratch for the prepare's temporaries: one device buffer per
+// stream, reused by every call on that stream (its earlier users are ordered
+// before on the stream, so reuse needs no wait), held by one host scope at a
+// time. Replaces the cudaMallocAsync / cudaFreeAsync pairs of a call: each is
+// a stream command, ~3 us of the device front end's time while the other
+// cloud's upload saturates PCIe (tools/launch_under_dma.cu).
+class Scratch {
+  public:
+    Scratch(cudaStream_t s, size_t bytes);  // locks the stream's buffer, grows it to `bytes`
+    ~Scratch();
+    Scratch(const Scratch&) = delete;
+    Scratch& operator=(const Scratch&) = delete;
+    static size_t round(size_t bytes) { return (bytes + 255) & ~size_t(255); }
+    // nullptr (and status() an error) past the reserved size
+    template <class T>
+    T* take(size_t count) {
+        const size_t b = round((count > 0 ? count : 1) * sizeof(T));
+        if (err_ != cudaSuccess || top_ + b > cap_) {
+            if (err_ == cudaSuccess) err_ = cudaErrorMemoryAllocation;
+            return nullptr;
+        }
+        T* p = reinterpret_cast<T*>(base_ + top_);
+        top_ += b;
+        return p;
+    }
+    cudaError_t status() const { return err_; }
+
+  private:
+    struct Entry;
+    Entry* e_ = nullptr;
+    char* base_ = nullptr;
+    size_t cap_ = 0, top_ = 0;
+    cudaError_t err_ = cudaSuccess;
+};
 
 // ---- device prepare_registration ---------------------
 // voxel_downsample (proj/src/preprocess.cpp:14-59) on the device: returns the

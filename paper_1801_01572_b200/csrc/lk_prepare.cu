@@ -20,6 +20,10 @@
 //             k_spfh_scale applies fl(100 / votes) like `v *= 100.0 / votes`
 //   k_fpfh    warp per point, lane per bin: acc_b += spfh_j[b] / w_j over the
 //             neighbours in ascending order (the reference's summation order)
+// Temporaries come from the stream's Scratch buffer and initialisation is
+// folded into the first kernel that runs: few stream commands per call (each
+// costs the device front end several us while the other cloud's upload holds
+// the PCIe link, tools/launch_under_dma.cu).
 #include <cmath>
 #include <cstdint>
 #include <algorithm>
@@ -70,19 +74,35 @@ __device__ __forceinline__ unsigned long long mix64(unsigned long long k) {
     return k;
 }
 
-// validate_cloud (proj/src/geometry.cpp:93-103): unit within 1e-6 or exactly zero
-__global__ void k_validate_normals(const double* __restrict__ nrm, int64_t n, int* __restrict__ bad) {
-    int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (i >= n) return;
-    V3 v = ld3(nrm, i);
-    double len = sqrt(sqnorm(v));
-    if (len != 0.0 && fabs(len - 1.0) > 1e-6) atomicOr(bad, 1);
+// the table and the flags to their empty state, the flag scan's leading 0
+__global__ void k_vox_init(uint32_t table, int64_t n, unsigned long long* __restrict__ keys,
+                           int32_t* __restrict__ first, int32_t* __restrict__ count, int32_t* __restrict__ flags,
+                           int32_t* __restrict__ flag_scan, int* __restrict__ bad) {
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < table; i += stride) {
+        keys[i] = kEmpty;
+        first[i] = 0x7f7f7f7f;
+        count[i] = 0;
+    }
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride) flags[i] = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        flag_scan[0] = 0;
+        *bad = 0;
+    }
 }
 
-__global__ void k_vox_insert(const double* __restrict__ pos, int64_t n, double leaf, unsigned long long* keys,
-                             uint32_t mask, int32_t* __restrict__ point_slot, int32_t* first, int32_t* count) {
+// nrm (optional): validate_cloud's normal check (proj/src/geometry.cpp:93-103:
+// unit within 1e-6 or exactly zero) on the same pass
+__global__ void k_vox_insert(const double* __restrict__ pos, const double* __restrict__ nrm, int64_t n, double leaf,
+                             unsigned long long* keys, uint32_t mask, int32_t* __restrict__ point_slot, int32_t* first,
+                             int32_t* count, int* __restrict__ bad) {
     int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (i >= n) return;
+    if (nrm) {
+        const V3 v = ld3(nrm, i);
+        const double len = sqrt(sqnorm(v));
+        if (len != 0.0 && fabs(len - 1.0) > 1e-6) atomicOr(bad, 1);
+    }
     const unsigned long long key = voxel_key(pos + 3 * i, leaf);
     uint32_t h = static_cast<uint32_t>(mix64(key)) & mask;
     while (true) {
@@ -103,12 +123,14 @@ __global__ void k_vox_mark(const unsigned long long* __restrict__ keys, const in
 
 __global__ void k_vox_out(const unsigned long long* __restrict__ keys, const int32_t* __restrict__ first,
                           const int32_t* __restrict__ count, uint32_t table, const int32_t* __restrict__ flag_scan,
-                          int32_t* __restrict__ slot_out, int32_t* __restrict__ cnt_out) {
+                          int32_t* __restrict__ slot_out, int32_t* __restrict__ cnt_out,
+                          int32_t* __restrict__ member_start) {
     uint32_t h = blockIdx.x * blockDim.x + threadIdx.x;
     if (h >= table || keys[h] == kEmpty) return;
     const int32_t o = flag_scan[first[h]];
     slot_out[h] = o;
     cnt_out[o] = count[h];
+    if (o == 0) member_start[0] = 0;  // the member scan's leading 0
 }
 
 // sort keys for the members: each point's output voxel, value = its index
@@ -347,8 +369,16 @@ __global__ void __launch_bounds__(32 * kSortWarps) k_nbr_count(const double* __r
 // the grid's to the bit even where rounding puts a point within r two cells away.
 constexpr int64_t kBruteMax = 24576;
 
-__global__ void k_search_cells(const double* __restrict__ pos, int64_t n, double cell, int4* __restrict__ out) {
+// zero (optional): off[0], the deferred-list counts and the overflow flag
+__global__ void k_search_cells(const double* __restrict__ pos, int64_t n, double cell, int4* __restrict__ out,
+                               int32_t* __restrict__ off = nullptr, int32_t* __restrict__ n_def = nullptr,
+                               int32_t* __restrict__ overflow = nullptr) {
     const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i == 0 && off) {
+        off[0] = 0;
+        n_def[0] = n_def[1] = n_def[2] = 0;
+        *overflow = 0;
+    }
     if (i >= n) return;
     out[i] = make_int4(floor_cell((pos[3 * i] - 0.0) / cell), floor_cell((pos[3 * i + 1] - 0.0) / cell),
                        floor_cell((pos[3 * i + 2] - 0.0) / cell), 0);
@@ -925,26 +955,45 @@ cudaError_t voxel_downsample(const double* d_pos, const double* d_nrm, int64_t n
     if (n > INT32_MAX / 2) return cudaErrorInvalidValue;
     uint32_t table = 1024;
     while (table < 2 * n) table <<= 1;
-    unsigned long long* keys = nullptr;
-    int32_t *point_slot = nullptr, *first = nullptr, *count = nullptr, *flags = nullptr, *flag_scan = nullptr;
-    int32_t *slot_out = nullptr, *cnt_out = nullptr, *member_start = nullptr, *members = nullptr, *bad = nullptr;
-    LK_TRY(cudaMallocAsync(&keys, table * sizeof(unsigned long long), stream));
-    LK_TRY(cudaMallocAsync(&point_slot, n * sizeof(int32_t), stream));
-    LK_TRY(cudaMallocAsync(&first, table * sizeof(int32_t), stream));
-    LK_TRY(cudaMallocAsync(&count, table * sizeof(int32_t), stream));
-    LK_TRY(cudaMallocAsync(&flags, n * sizeof(int32_t), stream));
-    LK_TRY(cudaMallocAsync(&flag_scan, (n + 1) * sizeof(int32_t), stream));
-    LK_TRY(cudaMallocAsync(&slot_out, table * sizeof(int32_t), stream));
-    LK_TRY(cudaMallocAsync(&bad, sizeof(int32_t), stream));
-    LK_TRY(cudaMemsetAsync(keys, 0xff, table * sizeof(unsigned long long), stream));
-    LK_TRY(cudaMemsetAsync(first, 0x7f, table * sizeof(int32_t), stream));
-    LK_TRY(cudaMemsetAsync(count, 0, table * sizeof(int32_t), stream));
-    LK_TRY(cudaMemsetAsync(flags, 0, n * sizeof(int32_t), stream));
-    LK_TRY(cudaMemsetAsync(bad, 0, sizeof(int32_t), stream));
-    if (d_nrm) k_validate_normals<<<nblocks(n, 256), 256, 0, stream>>>(d_nrm, n, bad);
-    k_vox_insert<<<nblocks(n, 256), 256, 0, stream>>>(d_pos, n, leaf, keys, table - 1, point_slot, first, count);
+    // members grouped by output voxel, ascending input index inside each: a
+    // stable LSD radix sort on the voxel ordinal (< n_out <= n)
+    int max_bit = 1;
+    while ((int64_t(1) << max_bit) < n) ++max_bit;
+    size_t sort_bytes = 0;
+    LK_TRY(cub::DeviceRadixSort::SortPairs(nullptr, sort_bytes, static_cast<const int32_t*>(nullptr),
+                                           static_cast<int32_t*>(nullptr), static_cast<const int32_t*>(nullptr),
+                                           static_cast<int32_t*>(nullptr), static_cast<int>(n), 0, max_bit, stream));
+    const size_t scan_bytes = scan_temp_bytes(n);
+    using S = Scratch;
+    const size_t tb = S::round(table * sizeof(unsigned long long)) + 3 * S::round(table * sizeof(int32_t));
+    const size_t nb = S::round(n * sizeof(int32_t));
+    Scratch sc(stream, tb + 8 * nb + 3 * S::round((n + 1) * sizeof(int32_t)) + S::round(sizeof(int32_t)) +
+                           S::round(scan_bytes) + S::round(sort_bytes));
+    unsigned long long* keys = sc.take<unsigned long long>(table);
+    int32_t* first = sc.take<int32_t>(table);
+    int32_t* count = sc.take<int32_t>(table);
+    int32_t* slot_out = sc.take<int32_t>(table);
+    int32_t* point_slot = sc.take<int32_t>(n);
+    int32_t* flags = sc.take<int32_t>(n);
+    int32_t* flag_scan = sc.take<int32_t>(n + 1);
+    int32_t* bad = sc.take<int32_t>(1);
+    void* scan_temp = sc.take<char>(scan_bytes);
+    int32_t* cnt_out = sc.take<int32_t>(n + 1);
+    int32_t* member_start = sc.take<int32_t>(n + 1);
+    int32_t* members = sc.take<int32_t>(n);
+    int32_t* skeys = sc.take<int32_t>(n);
+    int32_t* svals = sc.take<int32_t>(n);
+    int32_t* skeys_out = sc.take<int32_t>(n);
+    void* sort_temp = sc.take<char>(sort_bytes);
+    LK_TRY(sc.status());
+    const int64_t init_n = std::max<int64_t>(table, n);
+    k_vox_init<<<static_cast<unsigned>(std::min<int64_t>(nblocks(init_n, 256), 148 * 8)), 256, 0, stream>>>(
+        table, n, keys, first, count, flags, flag_scan, bad);
+    k_vox_insert<<<nblocks(n, 256), 256, 0, stream>>>(d_pos, d_nrm, n, leaf, keys, table - 1, point_slot, first,
+                                                     count, bad);
     k_vox_mark<<<nblocks(table, 256), 256, 0, stream>>>(keys, first, table, flags);
-    LK_TRY(exclusive_scan(flags, n, flag_scan, stream));
+    LK_TRY(exclusive_scan(flags, n, flag_scan, stream, scan_temp, scan_bytes, false));
+    trace_point("vox scan", stream);
     int32_t* host = static_cast<int32_t*>(host_scratch(2 * sizeof(int32_t)));
     if (!host) return cudaErrorMemoryAllocation;
     LK_TRY(cudaMemcpyAsync(&host[0], flag_scan + n, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
@@ -952,49 +1001,26 @@ cudaError_t voxel_downsample(const double* d_pos, const double* d_nrm, int64_t n
     LK_TRY(cudaStreamSynchronize(stream));
     if (host[1]) {
         *status = 5;
-    } else {
-        const int64_t n_out = host[0];
-        LK_TRY(cudaMallocAsync(&cnt_out, (n_out + 1) * sizeof(int32_t), stream));
-        LK_TRY(cudaMallocAsync(&member_start, (n_out + 1) * sizeof(int32_t), stream));
-        LK_TRY(cudaMallocAsync(&members, n * sizeof(int32_t), stream));
-        k_vox_out<<<nblocks(table, 256), 256, 0, stream>>>(keys, first, count, table, flag_scan, slot_out, cnt_out);
-        LK_TRY(exclusive_scan(cnt_out, n_out, member_start, stream));
-        // members grouped by output voxel, ascending input index inside each
-        // (a stable LSD radix sort on the voxel ordinal)
-        int32_t *skeys = nullptr, *svals = nullptr, *skeys_out = nullptr;
-        LK_TRY(cudaMallocAsync(&skeys, n * sizeof(int32_t), stream));
-        LK_TRY(cudaMallocAsync(&svals, n * sizeof(int32_t), stream));
-        LK_TRY(cudaMallocAsync(&skeys_out, n * sizeof(int32_t), stream));
-        k_vox_keys<<<nblocks(n, 256), 256, 0, stream>>>(point_slot, n, slot_out, skeys, svals);
-        int end_bit = 1;
-        while ((int64_t(1) << end_bit) < n_out) ++end_bit;
-        size_t temp_bytes = 0;
-        LK_TRY(cub::DeviceRadixSort::SortPairs(nullptr, temp_bytes, skeys, skeys_out, svals, members,
-                                               static_cast<int>(n), 0, end_bit, stream));
-        void* temp = nullptr;
-        LK_TRY(cudaMallocAsync(&temp, temp_bytes > 0 ? temp_bytes : 1, stream));
-        LK_TRY(cub::DeviceRadixSort::SortPairs(temp, temp_bytes, skeys, skeys_out, svals, members,
-                                               static_cast<int>(n), 0, end_bit, stream));
-        cudaFreeAsync(temp, stream);
-        cudaFreeAsync(skeys, stream);
-        cudaFreeAsync(svals, stream);
-        cudaFreeAsync(skeys_out, stream);
-        k_vox_reduce<<<nblocks(n_out, kSortWarps), 32 * kSortWarps, 0, stream>>>(members, member_start, n_out, d_pos,
-                                                                                  d_nrm, d_out_pos, d_out_nrm);
-        *out_count = n_out;
+        return cudaSuccess;
     }
-    LK_TRY(cudaGetLastError());
-    cudaFreeAsync(keys, stream);
-    cudaFreeAsync(point_slot, stream);
-    cudaFreeAsync(first, stream);
-    cudaFreeAsync(count, stream);
-    cudaFreeAsync(flags, stream);
-    cudaFreeAsync(flag_scan, stream);
-    cudaFreeAsync(slot_out, stream);
-    cudaFreeAsync(bad, stream);
-    if (cnt_out) cudaFreeAsync(cnt_out, stream);
-    if (member_start) cudaFreeAsync(member_start, stream);
-    if (members) cudaFreeAsync(members, stream);
+    const int64_t n_out = host[0];
+    trace_point("vox count back", stream);
+    k_vox_out<<<nblocks(table, 256), 256, 0, stream>>>(keys, first, count, table, flag_scan, slot_out, cnt_out,
+                                                       member_start);
+    LK_TRY(exclusive_scan(cnt_out, n_out, member_start, stream, scan_temp, scan_bytes, false));
+    k_vox_keys<<<nblocks(n, 256), 256, 0, stream>>>(point_slot, n, slot_out, skeys, svals);
+    int end_bit = 1;
+    while ((int64_t(1) << end_bit) < n_out) ++end_bit;
+    size_t sort_need = 0;
+    LK_TRY(cub::DeviceRadixSort::SortPairs(nullptr, sort_need, skeys, skeys_out, svals, members, static_cast<int>(n),
+                                           0, end_bit, stream));
+    if (sort_need > sort_bytes) return cudaErrorInvalidValue;  // fewer bits never need more storage
+    LK_TRY(cub::DeviceRadixSort::SortPairs(sort_temp, sort_bytes, skeys, skeys_out, svals, members,
+                                           static_cast<int>(n), 0, end_bit, stream));
+    trace_point("vox sorted", stream);
+    k_vox_reduce<<<nblocks(n_out, kSortWarps), 32 * kSortWarps, 0, stream>>>(members, member_start, n_out, d_pos,
+                                                                              d_nrm, d_out_pos, d_out_nrm);
+    *out_count = n_out;
     return cudaGetLastError();
 }
 
@@ -1074,43 +1100,55 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
     FpfhStage& st = t_stage;
     if (!st.head) LK_TRY(cudaHostAlloc(reinterpret_cast<void**>(&st.head), sizeof(FpfhStage::Head), 0));
     GridStorage g;
-    int32_t *counts = nullptr, *off = nullptr, *nbr = nullptr;
-    int4* cells = nullptr;
-    double* spfh = nullptr;
     const double r2 = radius * radius;
     const bool brute = n <= kBruteMax;
-    LK_TRY(cudaMallocAsync(&counts, n * sizeof(int32_t), stream));
-    LK_TRY(cudaMallocAsync(&off, (n + 1) * sizeof(int32_t), stream));
-    int32_t *slots = nullptr, *d_overflow = nullptr;
+    // speculative capacity (no host round trip for the total): 192 neighbours
+    // per point; an overflow turns the fill and the votes into no-ops and is
+    // redone below with the exact size (pool allocations, rare)
+    int64_t cap = std::max<int64_t>(192 * n, 4096);
+    int64_t a_cap = std::max<int64_t>(8 * n, 65536);  // list A: acos ties (planar faces: ~4 per point)
+    int64_t b_cap = 4096;                            // list B: theta bin edges (essentially never)
+    using S = Scratch;
+    const size_t scan_bytes = scan_temp_bytes(n);
+    const size_t lists_bytes = S::round(cap * sizeof(int32_t)) + S::round(a_cap * sizeof(int2)) +
+                               S::round(a_cap * sizeof(double2)) + S::round(b_cap * sizeof(int2)) +
+                               S::round(b_cap * sizeof(DeferredPair)) + 2 * S::round(a_cap) +
+                               S::round(a_cap * sizeof(int32_t)) + S::round(a_cap * sizeof(double4)) +
+                               S::round(b_cap * sizeof(uint32_t));
+    Scratch sc(stream, 2 * S::round((n + 1) * sizeof(int32_t)) + S::round(33 * n * sizeof(double)) +
+                           S::round(34 * n * sizeof(int32_t)) + 2 * S::round(4 * sizeof(int32_t)) + S::round(scan_bytes) +
+                           (brute ? S::round(n * sizeof(int4)) + S::round(n * kNbrSlots * sizeof(int32_t)) : 0) +
+                           lists_bytes);
+    int32_t* counts = sc.take<int32_t>(n + 1);
+    int32_t* off = sc.take<int32_t>(n + 1);
+    double* spfh = sc.take<double>(33 * n);
+    int32_t* votes = sc.take<int32_t>(34 * n);
+    int32_t* n_def = sc.take<int32_t>(4);
+    int32_t* d_overflow = sc.take<int32_t>(4);
+    void* scan_temp = sc.take<char>(scan_bytes);
+    int4* cells = brute ? sc.take<int4>(n) : nullptr;
+    int32_t* slots = brute ? sc.take<int32_t>(n * kNbrSlots) : nullptr;
+    LK_TRY(sc.status());
     if (brute) {
         // SearchGrid(cell = radius): block radius ceil(radius / cell) = 1;
         // one pass counts and keeps the lists in a fixed-stride table
-        LK_TRY(cudaMallocAsync(&cells, n * sizeof(int4), stream));
-        LK_TRY(cudaMallocAsync(&slots, n * kNbrSlots * sizeof(int32_t), stream));
-        LK_TRY(cudaMallocAsync(&d_overflow, sizeof(int32_t), stream));
-        LK_TRY(cudaMemsetAsync(d_overflow, 0, sizeof(int32_t), stream));
-        k_search_cells<<<nblocks(n, 256), 256, 0, stream>>>(d_pos, n, radius, cells);
+        k_search_cells<<<nblocks(n, 256), 256, 0, stream>>>(d_pos, n, radius, cells, off, n_def, d_overflow);
         k_nbr_brute_once<<<nblocks(n, kSortWarps), 32 * kSortWarps, 0, stream>>>(d_pos, cells, n, 1, r2, counts,
                                                                                  slots, d_overflow);
     } else {
         LK_TRY(build_grid(g, 1, d_pos, nullptr, n, radius, radius, stream, false));
         k_nbr_count<<<nblocks(n, kSortWarps), 32 * kSortWarps, 0, stream>>>(d_pos, n, g.view, r2, counts);
     }
-    LK_TRY(exclusive_scan(counts, n, off, stream));
-    // speculative capacity (no host round trip for the total): 192 neighbours
-    // per point; an overflow turns the fill and the votes into no-ops and is
-    // redone below with the exact size
-    int64_t cap = std::max<int64_t>(192 * n, 4096);
-    int64_t a_cap = std::max<int64_t>(8 * n, 65536);  // list A: acos ties (planar faces: ~4 per point)
-    int64_t b_cap = 4096;                            // list B: theta bin edges (essentially never)
-    int32_t *votes = nullptr, *n_def = nullptr;
+    LK_TRY(exclusive_scan(counts, n, off, stream, scan_temp, scan_bytes, !brute));
+    trace_point("fpfh nbr", stream);
+    int32_t* nbr = nullptr;
     DeferLists dl{};
     uint8_t* d_dec_a = nullptr;
     uint32_t* d_dec_b = nullptr;
-    LK_TRY(cudaMallocAsync(&spfh, 33 * n * sizeof(double), stream));
-    LK_TRY(cudaMallocAsync(&votes, 34 * n * sizeof(int32_t), stream));
-    LK_TRY(cudaMallocAsync(&n_def, 3 * sizeof(int32_t), stream));
+    bool pooled = false;  // this attempt's lists come from the pool (the retry)
     auto free_lists = [&] {
+        if (!pooled) return;
+        cudaFreeAsync(nbr, stream);
         cudaFreeAsync(dl.a_ij, stream);
         cudaFreeAsync(dl.a_x, stream);
         cudaFreeAsync(dl.b_ij, stream);
@@ -1118,20 +1156,42 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
         cudaFreeAsync(dl.a_dec, stream);
         cudaFreeAsync(dl.a2_k, stream);
         cudaFreeAsync(dl.a2_x, stream);
+        if (d_dec_a) cudaFreeAsync(d_dec_a, stream);
+        if (d_dec_b) cudaFreeAsync(d_dec_b, stream);
     };
     for (int attempt = 0; attempt < 2; ++attempt) {
-        LK_TRY(cudaMallocAsync(&nbr, cap * sizeof(int32_t), stream));
-        LK_TRY(cudaMallocAsync(&dl.a_ij, a_cap * sizeof(int2), stream));
-        LK_TRY(cudaMallocAsync(&dl.a_x, a_cap * sizeof(double2), stream));
-        LK_TRY(cudaMallocAsync(&dl.b_ij, b_cap * sizeof(int2), stream));
-        LK_TRY(cudaMallocAsync(&dl.b_x, b_cap * sizeof(DeferredPair), stream));
-        LK_TRY(cudaMallocAsync(&dl.a_dec, a_cap, stream));
-        LK_TRY(cudaMallocAsync(&dl.a2_k, a_cap * sizeof(int32_t), stream));
-        LK_TRY(cudaMallocAsync(&dl.a2_x, a_cap * sizeof(double4), stream));
+        if (attempt == 0) {
+            nbr = sc.take<int32_t>(cap);
+            dl.a_ij = sc.take<int2>(a_cap);
+            dl.a_x = sc.take<double2>(a_cap);
+            dl.b_ij = sc.take<int2>(b_cap);
+            dl.b_x = sc.take<DeferredPair>(b_cap);
+            dl.a_dec = sc.take<uint8_t>(a_cap);
+            dl.a2_k = sc.take<int32_t>(a_cap);
+            dl.a2_x = sc.take<double4>(a_cap);
+            d_dec_a = sc.take<uint8_t>(a_cap);
+            d_dec_b = sc.take<uint32_t>(b_cap);
+            LK_TRY(sc.status());
+        } else {
+            pooled = true;
+            d_dec_a = nullptr;
+            d_dec_b = nullptr;
+            LK_TRY(cudaMallocAsync(&nbr, cap * sizeof(int32_t), stream));
+            LK_TRY(cudaMallocAsync(&dl.a_ij, a_cap * sizeof(int2), stream));
+            LK_TRY(cudaMallocAsync(&dl.a_x, a_cap * sizeof(double2), stream));
+            LK_TRY(cudaMallocAsync(&dl.b_ij, b_cap * sizeof(int2), stream));
+            LK_TRY(cudaMallocAsync(&dl.b_x, b_cap * sizeof(DeferredPair), stream));
+            LK_TRY(cudaMallocAsync(&dl.a_dec, a_cap, stream));
+            LK_TRY(cudaMallocAsync(&dl.a2_k, a_cap * sizeof(int32_t), stream));
+            LK_TRY(cudaMallocAsync(&dl.a2_x, a_cap * sizeof(double4), stream));
+            LK_TRY(cudaMallocAsync(&d_dec_a, a_cap, stream));
+            LK_TRY(cudaMallocAsync(&d_dec_b, b_cap * sizeof(uint32_t), stream));
+        }
         dl.n = n_def;
         dl.a_cap = a_cap;
         dl.b_cap = b_cap;
-        LK_TRY(cudaMemsetAsync(n_def, 0, 3 * sizeof(int32_t), stream));
+        // zeroed by k_search_cells on the brute path's first attempt
+        if (!brute || attempt > 0) LK_TRY(cudaMemsetAsync(n_def, 0, 3 * sizeof(int32_t), stream));
         if (brute && attempt == 0)
             k_nbr_compact<<<nblocks(32 * n, 256), 256, 0, stream>>>(slots, off, n, d_overflow, nbr, cap);
         else if (brute)
@@ -1142,6 +1202,7 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
         // an overflowed slot table leaves nbr unfilled: the votes are skipped too
         k_spfh<<<nblocks(n, kFpfhWarps), 32 * kFpfhWarps, 0, stream>>>(d_pos, d_nrm, n, off, nbr, votes, dl, cap,
                                                                        (brute && attempt == 0) ? d_overflow : nullptr);
+        trace_point("fpfh spfh", stream);
         k_spfh_decide_a<<<nblocks(a_cap, 256), 256, 0, stream>>>(dl);
         // one round trip: total, list counts and the heads of lists A2 and B
         LK_TRY(cudaMemcpyAsync(&st.head->total, off + n, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
@@ -1155,7 +1216,6 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
                                stream));
         LK_TRY(cudaStreamSynchronize(stream));
         if (st.head->total <= cap && !st.head->overflow && st.head->n_a <= a_cap && st.head->n_b <= b_cap) break;
-        cudaFreeAsync(nbr, stream);
         free_lists();
         cap = std::max<int64_t>(cap, st.head->total);
         a_cap = std::max<int64_t>(a_cap, st.head->n_a);
@@ -1164,6 +1224,7 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
     // pairs the device cannot settle, decided with the reference's libm:
     // list A2 by its acos comparison (fpfh.cpp:28), list B whole (host_pair_bins)
     const int32_t na = st.head->n_a, ma = st.head->n_a2, mb = st.head->n_b;
+    trace_point("fpfh head back", stream);
     if (const char* tr = std::getenv("LK_TRACE"); tr && tr[0] == '1')
         std::fprintf(stderr, "[lk fpfh] n %lld neighbours %d deferred: acos ties %d (host %d), theta edges %d\n",
                      static_cast<long long>(n), st.head->total, na, ma, mb);
@@ -1196,7 +1257,6 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
             const double g2 = std::isnan(xs[k].w) ? std::acos(xs[k].y) : xs[k].w;
             st.dec_a[k] = g1 > g2 ? 1 : 0;
         }
-        LK_TRY(cudaMallocAsync(&d_dec_a, ma, stream));
         LK_TRY(cudaMemcpyAsync(d_dec_a, st.dec_a, ma, cudaMemcpyHostToDevice, stream));
         k_spfh_scatter_a2<<<nblocks(ma, 256), 256, 0, stream>>>(dl.a2_k, d_dec_a, ma, dl.a_dec);
     }
@@ -1218,39 +1278,28 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
             st.dec_b_cap = mb;
         }
         for (int32_t k = 0; k < mb; ++k) st.dec_b[k] = host_pair_bins(xs[k].v);
-        LK_TRY(cudaMallocAsync(&d_dec_b, mb * sizeof(uint32_t), stream));
         LK_TRY(cudaMemcpyAsync(d_dec_b, st.dec_b, mb * sizeof(uint32_t), cudaMemcpyHostToDevice, stream));
         k_spfh_resolve_b<<<nblocks(mb, 256), 256, 0, stream>>>(dl.b_ij, d_dec_b, mb, votes);
     }
+    trace_point("fpfh resolved", stream);
     k_spfh_scale<<<nblocks(33 * n, 256), 256, 0, stream>>>(votes, n, spfh);
     k_fpfh<<<nblocks(n, kFpfhWarps), 32 * kFpfhWarps, 0, stream>>>(d_pos, d_nrm, n, off, nbr, spfh, d_out);
     LK_TRY(cudaGetLastError());
     // stream-ordered frees: nothing here waits for the device (the pinned
     // staging is reused only after the caller synchronises this stream)
-    cudaFreeAsync(counts, stream);
-    cudaFreeAsync(off, stream);
-    cudaFreeAsync(nbr, stream);
-    if (cells) cudaFreeAsync(cells, stream);
-    if (slots) cudaFreeAsync(slots, stream);
-    if (d_overflow) cudaFreeAsync(d_overflow, stream);
-    cudaFreeAsync(spfh, stream);
-    cudaFreeAsync(votes, stream);
     free_lists();
-    cudaFreeAsync(n_def, stream);
-    if (d_dec_a) cudaFreeAsync(d_dec_a, stream);
-    if (d_dec_b) cudaFreeAsync(d_dec_b, stream);
     g.release();
     return cudaGetLastError();
 }
 
 cudaError_t cloud_stats_async(const double* d_pos, const double* d_nrm, int64_t n, unsigned long long* h_out2,
                               cudaStream_t stream) {
-    unsigned long long* d = nullptr;
-    LK_TRY(cudaMallocAsync(&d, 2 * sizeof(unsigned long long), stream));
+    Scratch sc(stream, Scratch::round(2 * sizeof(unsigned long long)));
+    unsigned long long* d = sc.take<unsigned long long>(2);
+    LK_TRY(sc.status());
     LK_TRY(cudaMemsetAsync(d, 0, 2 * sizeof(unsigned long long), stream));
     k_cloud_stats<<<nblocks(n, 256) < 64 ? nblocks(n, 256) : 64, 256, 0, stream>>>(d_pos, d_nrm, n, d);
     LK_TRY(cudaMemcpyAsync(h_out2, d, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream));
-    cudaFreeAsync(d, stream);
     return cudaGetLastError();
 }
 
