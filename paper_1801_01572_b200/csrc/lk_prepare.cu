@@ -369,10 +369,29 @@ __global__ void __launch_bounds__(32 * kSortWarps) k_nbr_count(const double* __r
 // the grid's to the bit even where rounding puts a point within r two cells away.
 constexpr int64_t kBruteMax = 24576;
 
-// zero (optional): off[0], the deferred-list counts and the overflow flag
+// Cells packed 10 bits per axis (mod 1024: x 22-31, y 11-20, z 0-9) with
+// guard bits 10 and 21 set: for a query key ki (guards clear),
+//   t = (((kj | G) - ki) & ~G) + ONE
+// holds (dc + 1) mod 1024 in each field without carries between fields, and
+// (t & kCellNearMask) == 0 iff every dc mod 1024 is in {-1, 0, 1, 2} -- a
+// superset of the block-radius-1 test, which the exact int4 test then
+// decides. Four ALU operations per pair instead of a dozen.
+constexpr uint32_t kCellGuards = (1u << 10) | (1u << 21);
+constexpr uint32_t kCellOne = 1u | (1u << 11) | (1u << 22);
+constexpr uint32_t kCellNearMask = (0x3fcu << 22) | (0x3fcu << 11) | 0x3fcu;
+__device__ __forceinline__ uint32_t pack_cell(int4 c) {
+    return ((static_cast<uint32_t>(c.x) & 1023u) << 22) | ((static_cast<uint32_t>(c.y) & 1023u) << 11) |
+           (static_cast<uint32_t>(c.z) & 1023u);
+}
+__device__ __forceinline__ bool cell_near(uint32_t kj_guarded, uint32_t ki) {
+    return ((((kj_guarded - ki) & ~kCellGuards) + kCellOne) & kCellNearMask) == 0;
+}
+
+// zero (optional): off[0], the deferred-list counts and the overflow flag;
+// keys (optional): the packed cells with their guard bits
 __global__ void k_search_cells(const double* __restrict__ pos, int64_t n, double cell, int4* __restrict__ out,
                                int32_t* __restrict__ off = nullptr, int32_t* __restrict__ n_def = nullptr,
-                               int32_t* __restrict__ overflow = nullptr) {
+                               int32_t* __restrict__ overflow = nullptr, uint32_t* __restrict__ keys = nullptr) {
     const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (i == 0 && off) {
         off[0] = 0;
@@ -380,8 +399,10 @@ __global__ void k_search_cells(const double* __restrict__ pos, int64_t n, double
         *overflow = 0;
     }
     if (i >= n) return;
-    out[i] = make_int4(floor_cell((pos[3 * i] - 0.0) / cell), floor_cell((pos[3 * i + 1] - 0.0) / cell),
-                       floor_cell((pos[3 * i + 2] - 0.0) / cell), 0);
+    const int4 c = make_int4(floor_cell((pos[3 * i] - 0.0) / cell), floor_cell((pos[3 * i + 1] - 0.0) / cell),
+                             floor_cell((pos[3 * i + 2] - 0.0) / cell), 0);
+    out[i] = c;
+    if (keys) keys[i] = pack_cell(c) | kCellGuards;
 }
 
 template <bool kFill>
@@ -418,39 +439,71 @@ __global__ void __launch_bounds__(32 * kSortWarps) k_nbr_brute(const double* __r
 constexpr int kNbrSlots = 192;
 
 __global__ void __launch_bounds__(32 * kSortWarps) k_nbr_brute_once(const double* __restrict__ pos,
-                                                                    const int4* __restrict__ cells, int64_t n,
+                                                                    const int4* __restrict__ cells,
+                                                                    const uint32_t* __restrict__ keys, int64_t n,
                                                                     int rad, double r2, int32_t* __restrict__ counts,
                                                                     int32_t* __restrict__ slots,
                                                                     int32_t* __restrict__ overflow) {
+    // per warp: candidates that pass the packed-cell filter, queued in index
+    // order and tested 32 at a time (exact cell test + distance), so the
+    // lanes stay busy although only a few percent of the cloud are candidates
+    __shared__ int32_t s_q[kSortWarps][64];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t i = blockIdx.x * static_cast<int64_t>(kSortWarps) + warp;
-    if (i >= n) return;
+    const int64_t i64 = blockIdx.x * static_cast<int64_t>(kSortWarps) + warp;
+    if (i64 >= n) return;
+    const int i = static_cast<int>(i64), ni = static_cast<int>(n);  // n <= kBruteMax
     const V3 p = ld3(pos, i);
     const int4 ci = cells[i];
-    int32_t* row = slots + i * kNbrSlots;
-    int32_t o = 0;
-    // four 32-point chunks per step: their cell loads are issued together
-    constexpr int kU = 4;
-    for (int64_t b0 = 0; b0 < n; b0 += 32 * kU) {
-        int4 cj[kU];
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-            const int64_t j = b0 + 32 * u + lane;
-            cj[u] = j < n ? __ldg(cells + j) : make_int4(INT32_MIN, INT32_MIN, INT32_MIN, 0);
+    const uint32_t ki = pack_cell(ci);
+    int32_t* row = slots + i64 * kNbrSlots;
+    int32_t* q = s_q[warp];
+    int o = 0, qn = 0;
+    const unsigned lt = (1u << lane) - 1u;
+    auto test = [&](int m) {  // the first m queued candidates, in order (i itself is one)
+        bool hit = false;
+        int j = 0;
+        if (lane < m) {
+            j = q[lane];
+            const int4 cj = __ldg(cells + j);
+            hit = j != i && abs(cj.x - ci.x) <= rad && abs(cj.y - ci.y) <= rad && abs(cj.z - ci.z) <= rad &&
+                  sqnorm(sub(ld3(pos, j), p)) <= r2;
         }
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-            const int64_t j = b0 + 32 * u + lane;
-            bool hit = false;
-            if (j < n && j != i && abs(cj[u].x - ci.x) <= rad && abs(cj[u].y - ci.y) <= rad &&
-                abs(cj[u].z - ci.z) <= rad)
-                hit = sqnorm(sub(ld3(pos, j), p)) <= r2;
-            const unsigned m = __ballot_sync(kFull, hit);
-            const int32_t at = o + __popc(m & ((1u << lane) - 1u));
-            if (hit && at < kNbrSlots) row[at] = static_cast<int32_t>(j);
-            o += __popc(m);
+        const unsigned hm = __ballot_sync(kFull, hit);
+        const int at = o + __popc(hm & lt);
+        if (hit && at < kNbrSlots) row[at] = j;
+        o += __popc(hm);
+    };
+    auto enqueue = [&](bool cand, int j) {
+        const unsigned m = __ballot_sync(kFull, cand);
+        if (m == 0u) return;  // the common case: one vote per 32 points
+        if (cand) q[qn + __popc(m & lt)] = j;
+        qn += __popc(m);
+        if (qn >= 32) {
+            __syncwarp();
+            test(32);
+            __syncwarp();
+            const int32_t rest = lane + 32 < qn ? q[lane + 32] : 0;
+            __syncwarp();
+            q[lane] = rest;
+            __syncwarp();
+            qn -= 32;
         }
+    };
+    constexpr int kU = 4;  // four 32-point chunks per step: their key loads issued together
+    int b0 = 0;
+    for (; b0 + 32 * kU <= ni; b0 += 32 * kU) {
+        uint32_t kj[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) kj[u] = __ldg(keys + b0 + 32 * u + lane);
+#pragma unroll
+        for (int u = 0; u < kU; ++u) enqueue(cell_near(kj[u], ki), b0 + 32 * u + lane);
     }
+    for (; b0 < ni; b0 += 32) {
+        const int j = b0 + lane;
+        enqueue(j < ni && cell_near(__ldg(keys + j), ki), j);
+    }
+    __syncwarp();
+    test(qn);
     if (lane == 0) {
         counts[i] = o;
         if (o > kNbrSlots) atomicExch(overflow, 1);
@@ -1117,7 +1170,9 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
                                S::round(b_cap * sizeof(uint32_t));
     Scratch sc(stream, 2 * S::round((n + 1) * sizeof(int32_t)) + S::round(33 * n * sizeof(double)) +
                            S::round(34 * n * sizeof(int32_t)) + 2 * S::round(4 * sizeof(int32_t)) + S::round(scan_bytes) +
-                           (brute ? S::round(n * sizeof(int4)) + S::round(n * kNbrSlots * sizeof(int32_t)) : 0) +
+                           (brute ? S::round(n * sizeof(int4)) + S::round(n * sizeof(uint32_t)) +
+                                      S::round(n * kNbrSlots * sizeof(int32_t))
+                                : 0) +
                            lists_bytes);
     int32_t* counts = sc.take<int32_t>(n + 1);
     int32_t* off = sc.take<int32_t>(n + 1);
@@ -1127,14 +1182,16 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
     int32_t* d_overflow = sc.take<int32_t>(4);
     void* scan_temp = sc.take<char>(scan_bytes);
     int4* cells = brute ? sc.take<int4>(n) : nullptr;
+    uint32_t* cell_keys = brute ? sc.take<uint32_t>(n) : nullptr;
     int32_t* slots = brute ? sc.take<int32_t>(n * kNbrSlots) : nullptr;
     LK_TRY(sc.status());
     if (brute) {
         // SearchGrid(cell = radius): block radius ceil(radius / cell) = 1;
         // one pass counts and keeps the lists in a fixed-stride table
-        k_search_cells<<<nblocks(n, 256), 256, 0, stream>>>(d_pos, n, radius, cells, off, n_def, d_overflow);
-        k_nbr_brute_once<<<nblocks(n, kSortWarps), 32 * kSortWarps, 0, stream>>>(d_pos, cells, n, 1, r2, counts,
-                                                                                 slots, d_overflow);
+        k_search_cells<<<nblocks(n, 256), 256, 0, stream>>>(d_pos, n, radius, cells, off, n_def, d_overflow,
+                                                            cell_keys);
+        k_nbr_brute_once<<<nblocks(n, kSortWarps), 32 * kSortWarps, 0, stream>>>(d_pos, cells, cell_keys, n, 1, r2,
+                                                                                 counts, slots, d_overflow);
     } else {
         LK_TRY(build_grid(g, 1, d_pos, nullptr, n, radius, radius, stream, false));
         k_nbr_count<<<nblocks(n, kSortWarps), 32 * kSortWarps, 0, stream>>>(d_pos, n, g.view, r2, counts);
