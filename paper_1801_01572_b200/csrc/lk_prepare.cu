@@ -25,6 +25,7 @@
 // costs the device front end several us while the other cloud's upload holds
 // the PCIe link, tools/launch_under_dma.cu).
 #include <cmath>
+#include <cstddef>
 #include <cstdint>
 #include <algorithm>
 #include <cstdio>
@@ -395,7 +396,7 @@ __global__ void k_search_cells(const double* __restrict__ pos, int64_t n, double
     const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (i == 0 && off) {
         off[0] = 0;
-        n_def[0] = n_def[1] = n_def[2] = 0;
+        n_def[0] = n_def[1] = n_def[2] = n_def[3] = 0;
         *overflow = 0;
     }
     if (i >= n) return;
@@ -595,23 +596,59 @@ struct DeferLists {
     double4* a2_x;   // (|a1|, |a2|, v1, v2): v = glibc's acos when certain, else NaN
 };
 
+// compute_fpfh's one device->host copy before the host decides the deferred
+// pairs: the counts, list B's first entries and, from a[], list A2's (|a1|,
+// |a2|, v1, v2) -- dl.a2_x points at a[0] and runs on past the struct
+constexpr int kStageA = 2048;
+constexpr int kStageB = 64;
+struct FpfhHead {
+    int32_t total, n_a, n_b, n_a2, overflow, pad[3];
+    DeferredPair b[kStageB];
+    double4 a[kStageA];
+};
+static_assert(offsetof(FpfhHead, b) == 32 && offsetof(FpfhHead, a) % 32 == 0, "FpfhHead layout");
+
 // List A's frame-source tests settled on the device where glibc's outcome is
 // certain (lk_acos_cr.hpp acos_greater); the rest go to list A2 for the host.
-__global__ void k_spfh_decide_a(DeferLists dl) {
+__global__ void k_spfh_decide_a(DeferLists dl, const int32_t* __restrict__ total, const int32_t* __restrict__ overflow,
+                                FpfhHead* __restrict__ head) {
     const int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= dl.n[0]) return;
-    const double2 x = dl.a_x[k];
-    double l1, h1, l2, h2;
-    const int r1 = lkacos::acos_bracket(x.x, &l1, &h1), r2 = lkacos::acos_bracket(x.y, &l2, &h2);
-    if (r1 && r2 && (l1 > h2 || h1 <= l2)) {  // lkacos::acos_greater, certain
-        dl.a_dec[k] = l1 > h2 ? 1 : 0;
-        return;
+    if (k < dl.n[0]) {
+        const double2 x = dl.a_x[k];
+        double l1, h1, l2, h2;
+        const int r1 = lkacos::acos_bracket(x.x, &l1, &h1), r2 = lkacos::acos_bracket(x.y, &l2, &h2);
+        if (r1 && r2 && (l1 > h2 || h1 <= l2)) {  // lkacos::acos_greater, certain
+            dl.a_dec[k] = l1 > h2 ? 1 : 0;
+        } else {
+            // the host evaluates only the values whose rounding is in doubt
+            const double nan = __longlong_as_double(0x7ff8000000000000ll);
+            const int32_t slot = atomicAdd(dl.n + 2, 1);
+            dl.a2_k[slot] = k;
+            dl.a2_x[slot] = make_double4(x.x, x.y, r1 == 1 ? l1 : nan, r2 == 1 ? l2 : nan);
+        }
     }
-    // the host evaluates only the values whose rounding is in doubt
-    const double nan = __longlong_as_double(0x7ff8000000000000ll);
-    const int32_t slot = atomicAdd(dl.n + 2, 1);
-    dl.a2_k[slot] = k;
-    dl.a2_x[slot] = make_double4(x.x, x.y, r1 == 1 ? l1 : nan, r2 == 1 ? l2 : nan);
+    // the last block to finish writes the head's counts and list B's first
+    // entries (dl.n[3]: blocks done, zeroed with the counts)
+    __shared__ bool last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(dl.n + 3, 1) == static_cast<int32_t>(gridDim.x) - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    const volatile int32_t* vn = dl.n;
+    const int32_t n_b = vn[1];
+    if (threadIdx.x == 0) {
+        head->total = *total;
+        head->n_a = vn[0];
+        head->n_b = n_b;
+        head->n_a2 = vn[2];
+        head->overflow = overflow ? *overflow : 0;
+    }
+    const int nb = n_b < kStageB ? n_b : kStageB;
+    for (int t = threadIdx.x; t < nb * 12; t += blockDim.x) head->b[t / 12].v[t % 12] = dl.b_x[t / 12].v[t % 12];
 }
 
 __global__ void k_spfh_scatter_a2(const int32_t* __restrict__ a2_k, const uint8_t* __restrict__ dec, int32_t m,
@@ -1020,7 +1057,7 @@ cudaError_t voxel_downsample(const double* d_pos, const double* d_nrm, int64_t n
     using S = Scratch;
     const size_t tb = S::round(table * sizeof(unsigned long long)) + 3 * S::round(table * sizeof(int32_t));
     const size_t nb = S::round(n * sizeof(int32_t));
-    Scratch sc(stream, tb + 8 * nb + 3 * S::round((n + 1) * sizeof(int32_t)) + S::round(sizeof(int32_t)) +
+    Scratch sc(stream, tb + 8 * nb + 3 * S::round((n + 2) * sizeof(int32_t)) +
                            S::round(scan_bytes) + S::round(sort_bytes));
     unsigned long long* keys = sc.take<unsigned long long>(table);
     int32_t* first = sc.take<int32_t>(table);
@@ -1028,8 +1065,8 @@ cudaError_t voxel_downsample(const double* d_pos, const double* d_nrm, int64_t n
     int32_t* slot_out = sc.take<int32_t>(table);
     int32_t* point_slot = sc.take<int32_t>(n);
     int32_t* flags = sc.take<int32_t>(n);
-    int32_t* flag_scan = sc.take<int32_t>(n + 1);
-    int32_t* bad = sc.take<int32_t>(1);
+    int32_t* flag_scan = sc.take<int32_t>(n + 2);
+    int32_t* bad = flag_scan + n + 1;  // read back with the total in one copy
     void* scan_temp = sc.take<char>(scan_bytes);
     int32_t* cnt_out = sc.take<int32_t>(n + 1);
     int32_t* member_start = sc.take<int32_t>(n + 1);
@@ -1049,8 +1086,7 @@ cudaError_t voxel_downsample(const double* d_pos, const double* d_nrm, int64_t n
     trace_point("vox scan", stream);
     int32_t* host = static_cast<int32_t*>(host_scratch(2 * sizeof(int32_t)));
     if (!host) return cudaErrorMemoryAllocation;
-    LK_TRY(cudaMemcpyAsync(&host[0], flag_scan + n, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
-    LK_TRY(cudaMemcpyAsync(&host[1], bad, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
+    LK_TRY(cudaMemcpyAsync(host, flag_scan + n, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
     LK_TRY(cudaStreamSynchronize(stream));
     if (host[1]) {
         *status = 5;
@@ -1125,15 +1161,8 @@ static uint32_t host_pair_bins(const double* v) {
 // the first kStageX deferred pairs come back in one copy; the decisions go
 // back from here. Reused only after the caller's stream has synchronised.
 struct FpfhStage {
-    static constexpr int kStageA = 2048;
-    static constexpr int kStageB = 64;
-    struct Head {
-        int32_t total, n_a, n_b, n_a2, overflow;
-        double4 a[kStageA];
-        DeferredPair b[kStageB];
-    };
-    Head* head = nullptr;
-    double4* more_a = nullptr;  // pinned: list A2 beyond the staged head
+    FpfhHead* head = nullptr;
+    double4* more_a = nullptr;  // list A2 beyond kStageA (rare)
     size_t more_cap = 0;
     uint8_t* dec_a = nullptr;
     uint32_t* dec_b = nullptr;
@@ -1151,7 +1180,7 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
                          cudaStream_t stream) {
     if (n <= 0) return cudaErrorInvalidValue;
     FpfhStage& st = t_stage;
-    if (!st.head) LK_TRY(cudaHostAlloc(reinterpret_cast<void**>(&st.head), sizeof(FpfhStage::Head), 0));
+    if (!st.head) LK_TRY(cudaHostAlloc(reinterpret_cast<void**>(&st.head), sizeof(FpfhHead), 0));
     GridStorage g;
     const double r2 = radius * radius;
     const bool brute = n <= kBruteMax;
@@ -1166,7 +1195,7 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
     const size_t lists_bytes = S::round(cap * sizeof(int32_t)) + S::round(a_cap * sizeof(int2)) +
                                S::round(a_cap * sizeof(double2)) + S::round(b_cap * sizeof(int2)) +
                                S::round(b_cap * sizeof(DeferredPair)) + 2 * S::round(a_cap) +
-                               S::round(a_cap * sizeof(int32_t)) + S::round(a_cap * sizeof(double4)) +
+                               S::round(a_cap * sizeof(int32_t)) + S::round(offsetof(FpfhHead, a) + a_cap * sizeof(double4)) +
                                S::round(b_cap * sizeof(uint32_t));
     Scratch sc(stream, 2 * S::round((n + 1) * sizeof(int32_t)) + S::round(33 * n * sizeof(double)) +
                            S::round(34 * n * sizeof(int32_t)) + 2 * S::round(4 * sizeof(int32_t)) + S::round(scan_bytes) +
@@ -1202,6 +1231,7 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
     DeferLists dl{};
     uint8_t* d_dec_a = nullptr;
     uint32_t* d_dec_b = nullptr;
+    FpfhHead* head_dev = nullptr;  // dl.a2_x = head_dev->a
     bool pooled = false;  // this attempt's lists come from the pool (the retry)
     auto free_lists = [&] {
         if (!pooled) return;
@@ -1212,7 +1242,7 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
         cudaFreeAsync(dl.b_x, stream);
         cudaFreeAsync(dl.a_dec, stream);
         cudaFreeAsync(dl.a2_k, stream);
-        cudaFreeAsync(dl.a2_x, stream);
+        cudaFreeAsync(head_dev, stream);
         if (d_dec_a) cudaFreeAsync(d_dec_a, stream);
         if (d_dec_b) cudaFreeAsync(d_dec_b, stream);
     };
@@ -1225,7 +1255,7 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
             dl.b_x = sc.take<DeferredPair>(b_cap);
             dl.a_dec = sc.take<uint8_t>(a_cap);
             dl.a2_k = sc.take<int32_t>(a_cap);
-            dl.a2_x = sc.take<double4>(a_cap);
+            head_dev = reinterpret_cast<FpfhHead*>(sc.take<char>(offsetof(FpfhHead, a) + a_cap * sizeof(double4)));
             d_dec_a = sc.take<uint8_t>(a_cap);
             d_dec_b = sc.take<uint32_t>(b_cap);
             LK_TRY(sc.status());
@@ -1240,15 +1270,17 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
             LK_TRY(cudaMallocAsync(&dl.b_x, b_cap * sizeof(DeferredPair), stream));
             LK_TRY(cudaMallocAsync(&dl.a_dec, a_cap, stream));
             LK_TRY(cudaMallocAsync(&dl.a2_k, a_cap * sizeof(int32_t), stream));
-            LK_TRY(cudaMallocAsync(&dl.a2_x, a_cap * sizeof(double4), stream));
+            LK_TRY(cudaMallocAsync(&head_dev, offsetof(FpfhHead, a) + a_cap * sizeof(double4), stream));
             LK_TRY(cudaMallocAsync(&d_dec_a, a_cap, stream));
             LK_TRY(cudaMallocAsync(&d_dec_b, b_cap * sizeof(uint32_t), stream));
         }
+        if (!head_dev) return cudaErrorMemoryAllocation;
+        dl.a2_x = head_dev->a;
         dl.n = n_def;
         dl.a_cap = a_cap;
         dl.b_cap = b_cap;
         // zeroed by k_search_cells on the brute path's first attempt
-        if (!brute || attempt > 0) LK_TRY(cudaMemsetAsync(n_def, 0, 3 * sizeof(int32_t), stream));
+        if (!brute || attempt > 0) LK_TRY(cudaMemsetAsync(n_def, 0, 4 * sizeof(int32_t), stream));
         if (brute && attempt == 0)
             k_nbr_compact<<<nblocks(32 * n, 256), 256, 0, stream>>>(slots, off, n, d_overflow, nbr, cap);
         else if (brute)
@@ -1260,17 +1292,11 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
         k_spfh<<<nblocks(n, kFpfhWarps), 32 * kFpfhWarps, 0, stream>>>(d_pos, d_nrm, n, off, nbr, votes, dl, cap,
                                                                        (brute && attempt == 0) ? d_overflow : nullptr);
         trace_point("fpfh spfh", stream);
-        k_spfh_decide_a<<<nblocks(a_cap, 256), 256, 0, stream>>>(dl);
-        // one round trip: total, list counts and the heads of lists A2 and B
-        LK_TRY(cudaMemcpyAsync(&st.head->total, off + n, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
-        LK_TRY(cudaMemcpyAsync(&st.head->n_a, n_def, 3 * sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
-        st.head->overflow = 0;
-        if (brute && attempt == 0)
-            LK_TRY(cudaMemcpyAsync(&st.head->overflow, d_overflow, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
-        LK_TRY(cudaMemcpyAsync(st.head->a, dl.a2_x, FpfhStage::kStageA * sizeof(double4), cudaMemcpyDeviceToHost,
-                               stream));
-        LK_TRY(cudaMemcpyAsync(st.head->b, dl.b_x, FpfhStage::kStageB * sizeof(DeferredPair), cudaMemcpyDeviceToHost,
-                               stream));
+        k_spfh_decide_a<<<nblocks(a_cap, 256), 256, 0, stream>>>(dl, off + n,
+                                                                 (brute && attempt == 0) ? d_overflow : nullptr,
+                                                                 head_dev);
+        // one round trip: the counts and the heads of lists A2 and B
+        LK_TRY(cudaMemcpyAsync(st.head, head_dev, sizeof(FpfhHead), cudaMemcpyDeviceToHost, stream));
         LK_TRY(cudaStreamSynchronize(stream));
         if (st.head->total <= cap && !st.head->overflow && st.head->n_a <= a_cap && st.head->n_b <= b_cap) break;
         free_lists();
@@ -1287,7 +1313,7 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
                      static_cast<long long>(n), st.head->total, na, ma, mb);
     if (ma > 0) {
         const double4* xs = st.head->a;
-        if (ma > FpfhStage::kStageA) {
+        if (ma > kStageA) {
             if (static_cast<size_t>(ma) > st.more_cap) {
                 if (st.more_a) cudaFreeHost(st.more_a);
                 st.more_a = nullptr;
@@ -1295,9 +1321,9 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
                 LK_TRY(cudaHostAlloc(reinterpret_cast<void**>(&st.more_a), ma * sizeof(double4), 0));
                 st.more_cap = ma;
             }
-            LK_TRY(cudaMemcpyAsync(st.more_a + FpfhStage::kStageA, dl.a2_x + FpfhStage::kStageA,
-                                   (ma - FpfhStage::kStageA) * sizeof(double4), cudaMemcpyDeviceToHost, stream));
-            std::memcpy(st.more_a, st.head->a, FpfhStage::kStageA * sizeof(double4));
+            LK_TRY(cudaMemcpyAsync(st.more_a + kStageA, dl.a2_x + kStageA,
+                                   (ma - kStageA) * sizeof(double4), cudaMemcpyDeviceToHost, stream));
+            std::memcpy(st.more_a, st.head->a, kStageA * sizeof(double4));
             LK_TRY(cudaStreamSynchronize(stream));
             xs = st.more_a;
         }
@@ -1321,7 +1347,7 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
     if (mb > 0) {
         std::vector<DeferredPair> more;
         const DeferredPair* xs = st.head->b;
-        if (mb > FpfhStage::kStageB) {
+        if (mb > kStageB) {
             more.resize(mb);
             LK_TRY(cudaMemcpyAsync(more.data(), dl.b_x, mb * sizeof(DeferredPair), cudaMemcpyDeviceToHost, stream));
             LK_TRY(cudaStreamSynchronize(stream));
