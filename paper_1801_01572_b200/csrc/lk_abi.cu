@@ -622,6 +622,8 @@ struct CloudSide {
     double *raw_pos = nullptr, *raw_nrm = nullptr;
     double *pos = nullptr, *nrm = nullptr;
     float* feat = nullptr;
+    float4* padded = nullptr;  // feat in the feature match's layout
+    float* q2 = nullptr;       // target side: |q|^2 per feature
     int64_t n = 0;
     int status = 0;  // 5: invalid normals
     int64_t usable = 0;
@@ -711,6 +713,11 @@ void prepare_side(CloudSide& cs, double feature_radius, double normal_radius, do
             }
             throw;
         }
+        // the feature match's per-cloud inputs, on this side's stream (the
+        // target's off the source's critical path)
+        CK(lkk::pool_alloc(&cs.padded, lkk::fnn_padded_bytes(cs.n), cs.s));
+        if (grid) CK(lkk::pool_alloc(&cs.q2, std::max<int64_t>(cs.n, 1) * sizeof(float), cs.s));
+        CK(lkk::fnn_prepare(cs.feat, cs.n, cs.padded, cs.q2, cs.s));
         mark("fpfh");
         // no wait here: the feature match is queued behind both sides'
         // streams, and prepare's final sync brings the stats back
@@ -824,6 +831,10 @@ lk_status prepare_impl(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_pa
     auto drop = [&](CloudSide& cs) {
         lkk::pool_free(cs.raw_pos, cs.s);
         lkk::pool_free(cs.raw_nrm, cs.s);
+        lkk::pool_free(cs.padded, cs.s);
+        lkk::pool_free(cs.q2, cs.s);
+        cs.padded = nullptr;
+        cs.q2 = nullptr;
     };
     try {
         // page-locked callers: the two uploads are enqueued here back to back,
@@ -889,7 +900,14 @@ lk_status prepare_impl(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_pa
                 cudaEventDestroy(done);
             }
             CK(lkk::pool_alloc(&c->d_cache, c->ns * sizeof(int32_t), s));
-            CK(lkk::feature_nn(c->d_sfeat, c->ns, c->d_tfeat, c->nt, c->d_cache, s));
+            CK(lkk::feature_nn_prepared(c->d_sfeat, S.padded, c->ns, c->d_tfeat, T.padded, T.q2, c->nt, c->d_cache,
+                                        s));
+            for (CloudSide* cs : {&S, &T}) {
+                lkk::pool_free(cs->padded, s);
+                lkk::pool_free(cs->q2, s);
+                cs->padded = nullptr;
+                cs->q2 = nullptr;
+            }
             tmark("joined, feature nn start", s, t0);
             ctx_finish_source(c);
             tmark("feature nn done", s, t0);

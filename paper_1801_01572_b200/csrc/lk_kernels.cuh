@@ -393,9 +393,18 @@ void cloud_stats_decode(const unsigned long long* h2, int64_t* usable, double* m
 cudaError_t cloud_stats(const double* d_pos, const double* d_nrm, int64_t n, int64_t* usable, double* max_norm,
                         cudaStream_t stream);
 
-// FP64 exhaustive feature NN, ties -> lowest index (reference.hpp:56-76).
+// Feature NN with the reference binary's float scores, ties -> lowest index
+// (grid.cpp:176-213).
 cudaError_t feature_nn(const float* d_sf, int64_t ns, const float* d_tf, int64_t nt, int32_t* d_out,
                        cudaStream_t stream);
+// The same in two steps: fnn_prepare per cloud as soon as its features exist
+// (the padded layout the match reads; for the target also |q|^2), then
+// feature_nn_prepared once both are ready.
+size_t fnn_padded_bytes(int64_t n);
+cudaError_t fnn_prepare(const float* d_f, int64_t n, float4* d_padded, float* d_q2, cudaStream_t stream);
+cudaError_t feature_nn_prepared(const float* d_sf, const float4* d_sp, int64_t ns, const float* d_tf,
+                                const float4* d_tp, const float* d_q2, int64_t nt, int32_t* d_out,
+                                cudaStream_t stream);
 
 // edge_info for one pair given a kind-1 grid over posed cloud_j.
 cudaError_t edge_info(const double* d_ci, int64_t ni, const double* Ti12, const GridView& grid, double eps,

@@ -1,5 +1,6 @@
 // lk_misc.cu -- feature pre-match (K1, the reference binary's float matcher), edge_info (K8), point transforms.
 #include <cstdint>
+#include <algorithm>
 #include <cstdlib>
 
 #include "lk_device_math.cuh"
@@ -82,11 +83,6 @@ __device__ __forceinline__ float eigen_score(float q2, const float* a, const flo
     return __fsub_rn(q2, __fmul_rn(2.0f, cc));
 }
 
-__global__ void k_fnn_qnorm(const float* __restrict__ tf, int64_t nt, float* __restrict__ q2) {
-    const int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-    if (j < nt) q2[j] = eigen_qnorm33(tf + j * kFeatDim);
-}
-
 // exhaustive: one thread per source over every target in order
 __global__ void __launch_bounds__(kFeatThreads) k_feature_nn_exact(const float* __restrict__ sf, int64_t ns,
                                                                    const float* __restrict__ tf, int64_t nt,
@@ -108,10 +104,13 @@ __global__ void __launch_bounds__(kFeatThreads) k_feature_nn_exact(const float* 
     out[i] = best;
 }
 
-__global__ void k_pad_features(const float* __restrict__ f, int64_t n, float4* __restrict__ out) {
+// q2 (optional): |q|^2 per feature, by the thread of its first float4
+__global__ void k_pad_features(const float* __restrict__ f, int64_t n, float4* __restrict__ out,
+                               float* __restrict__ q2) {
     const int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (t >= n * (kFnnPad / 4)) return;
     const int64_t i = t / (kFnnPad / 4), q = t % (kFnnPad / 4);
+    if (q2 && q == 0) q2[i] = eigen_qnorm33(f + i * kFeatDim);
     float v[4];
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
@@ -356,16 +355,21 @@ __global__ void k_info_final(const double* __restrict__ partials, int nb, const 
 
 }  // namespace
 
-cudaError_t feature_nn(const float* d_sf, int64_t ns, const float* d_tf, int64_t nt, int32_t* d_out,
-                       cudaStream_t stream) {
-    float* q2 = nullptr;
-    cudaError_t e;
-    if ((e = pool_alloc(&q2, nt * sizeof(float), stream)) != cudaSuccess) return e;
-    k_fnn_qnorm<<<static_cast<unsigned>((nt + 255) / 256), 256, 0, stream>>>(d_tf, nt, q2);
+size_t fnn_padded_bytes(int64_t n) { return static_cast<size_t>(n > 0 ? n : 1) * kFnnPad * sizeof(float); }
+
+cudaError_t fnn_prepare(const float* d_f, int64_t n, float4* d_padded, float* d_q2, cudaStream_t stream) {
+    if (n > 0)
+        k_pad_features<<<static_cast<unsigned>((n * (kFnnPad / 4) + 255) / 256), 256, 0, stream>>>(d_f, n, d_padded,
+                                                                                                 d_q2);
+    return cudaGetLastError();
+}
+
+cudaError_t feature_nn_prepared(const float* d_sf, const float4* d_sp, int64_t ns, const float* d_tf,
+                                const float4* d_tp, const float* d_q2, int64_t nt, int32_t* d_out,
+                                cudaStream_t stream) {
     if (const char* v = std::getenv("LK_FP64_ONLY"); v && v[0] == '1') {
         const unsigned blocks = static_cast<unsigned>((ns + kFeatThreads - 1) / kFeatThreads);
-        k_feature_nn_exact<<<blocks, kFeatThreads, 0, stream>>>(d_sf, ns, d_tf, nt, q2, d_out);
-        pool_free(q2, stream);
+        k_feature_nn_exact<<<blocks, kFeatThreads, 0, stream>>>(d_sf, ns, d_tf, nt, d_q2, d_out);
         return cudaGetLastError();
     }
     int dev = 0, sms = 148;
@@ -377,22 +381,32 @@ cudaError_t feature_nn(const float* d_sf, int64_t ns, const float* d_tf, int64_t
     if (n_chunks > (nt + kFnnTile - 1) / kFnnTile) n_chunks = (nt + kFnnTile - 1) / kFnnTile;
     const int64_t chunk = (nt + n_chunks - 1) / n_chunks;
     n_chunks = (nt + chunk - 1) / chunk;
-    float4 *sp = nullptr, *tp = nullptr;
-    BestF* partial = nullptr;
-    if ((e = pool_alloc(&sp, ns * kFnnPad * sizeof(float), stream)) != cudaSuccess) return e;
-    if ((e = pool_alloc(&tp, nt * kFnnPad * sizeof(float), stream)) != cudaSuccess) return e;
-    if ((e = pool_alloc(&partial, n_chunks * ns * sizeof(BestF), stream)) != cudaSuccess) return e;
-    k_pad_features<<<static_cast<unsigned>((ns * 9 + 255) / 256), 256, 0, stream>>>(d_sf, ns, sp);
-    k_pad_features<<<static_cast<unsigned>((nt * 9 + 255) / 256), 256, 0, stream>>>(d_tf, nt, tp);
+    Scratch sc(stream, Scratch::round(n_chunks * ns * sizeof(BestF)));
+    BestF* partial = sc.take<BestF>(n_chunks * ns);
+    cudaError_t e = sc.status();
+    if (e != cudaSuccess) return e;
     k_fnn_partial<<<dim3(static_cast<unsigned>(src_blocks), static_cast<unsigned>(n_chunks)), kFnnThreads, 0,
-                    stream>>>(sp, ns, tp, q2, nt, chunk, partial);
+                    stream>>>(d_sp, ns, d_tp, d_q2, nt, chunk, partial);
     k_fnn_merge<<<static_cast<unsigned>((ns + 255) / 256), 256, 0, stream>>>(ns, partial, static_cast<int>(n_chunks),
                                                                             d_out);
+    return cudaGetLastError();
+}
+
+cudaError_t feature_nn(const float* d_sf, int64_t ns, const float* d_tf, int64_t nt, int32_t* d_out,
+                       cudaStream_t stream) {
+    float* q2 = nullptr;
+    float4 *sp = nullptr, *tp = nullptr;
+    cudaError_t e;
+    if ((e = pool_alloc(&q2, std::max<int64_t>(nt, 1) * sizeof(float), stream)) != cudaSuccess) return e;
+    if ((e = pool_alloc(&sp, fnn_padded_bytes(ns), stream)) != cudaSuccess) return e;
+    if ((e = pool_alloc(&tp, fnn_padded_bytes(nt), stream)) != cudaSuccess) return e;
+    if ((e = fnn_prepare(d_sf, ns, sp, nullptr, stream)) == cudaSuccess &&
+        (e = fnn_prepare(d_tf, nt, tp, q2, stream)) == cudaSuccess)
+        e = feature_nn_prepared(d_sf, sp, ns, d_tf, tp, q2, nt, d_out, stream);
     pool_free(sp, stream);
     pool_free(tp, stream);
-    pool_free(partial, stream);
     pool_free(q2, stream);
-    return cudaGetLastError();
+    return e;
 }
 
 cudaError_t transform_points(const double* d_in, int64_t n, const double* T12, double* d_out, cudaStream_t stream) {
