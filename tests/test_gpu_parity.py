@@ -243,6 +243,22 @@ def test_device_downsample_full_frame_matches_oracle(oracle):
         lk.voxel_downsample(lk.PointCloud(src.positions, bad), 0.05)
 
 
+@pytest.mark.parametrize("cluster", [1000, 1024, 1025, 5000])
+def test_device_downsample_voxel_group_sizes(oracle, cluster):
+    # one voxel holding 1000-5000 of the points among sparse ones: members in
+    # input order through the stable radix sort, sums in the reference's order
+    rng = np.random.default_rng(cluster)
+    spread = rng.uniform(-2.0, 2.0, size=(20_000, 3))
+    dense = 0.4 + rng.uniform(0.0, 0.049, size=(cluster, 3))  # one 0.05 voxel
+    pos = np.concatenate([spread[:7_000], dense, spread[7_000:]])
+    nrm = rng.normal(size=pos.shape)
+    nrm /= np.linalg.norm(nrm, axis=1, keepdims=True)
+    cloud = lk.PointCloud(pos, nrm)
+    d = lk.voxel_downsample(cloud, 0.05)
+    ox, on = oracle.voxel_downsample(cloud.positions, cloud.normals, 0.05)
+    assert np.array_equal(d.positions, ox) and np.array_equal(d.normals, on)
+
+
 def test_negative_pair_returns_none(oracle):
     # test_registration.cpp:181-188
     pair = synth.synth_negative_pair(1)
