@@ -591,8 +591,7 @@ struct DeferLists {
     DeferredPair* b_x;
     int32_t* n;  // n[0] = list A, n[1] = list B, n[2] = list A2
     int64_t a_cap, b_cap;
-    uint8_t* a_dec;  // list A decisions (k_spfh_decide_a; the host's for A2)
-    int32_t* a2_k;   // A2: list A entries the host decides
+    int32_t* a_dec;  // list A decisions: 0 / 1, or 2 + the entry's list A2 slot (the host decides)
     double4* a2_x;   // (|a1|, |a2|, v1, v2): v = glibc's acos when certain, else NaN
 };
 
@@ -623,7 +622,7 @@ __global__ void k_spfh_decide_a(DeferLists dl, const int32_t* __restrict__ total
             // the host evaluates only the values whose rounding is in doubt
             const double nan = __longlong_as_double(0x7ff8000000000000ll);
             const int32_t slot = atomicAdd(dl.n + 2, 1);
-            dl.a2_k[slot] = k;
+            dl.a_dec[k] = 2 + slot;
             dl.a2_x[slot] = make_double4(x.x, x.y, r1 == 1 ? l1 : nan, r2 == 1 ? l2 : nan);
         }
     }
@@ -649,12 +648,6 @@ __global__ void k_spfh_decide_a(DeferLists dl, const int32_t* __restrict__ total
     }
     const int nb = n_b < kStageB ? n_b : kStageB;
     for (int t = threadIdx.x; t < nb * 12; t += blockDim.x) head->b[t / 12].v[t % 12] = dl.b_x[t / 12].v[t % 12];
-}
-
-__global__ void k_spfh_scatter_a2(const int32_t* __restrict__ a2_k, const uint8_t* __restrict__ dec, int32_t m,
-                                  uint8_t* __restrict__ a_dec) {
-    const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j < m) a_dec[a2_k[j]] = dec[j];
 }
 
 __global__ void __launch_bounds__(32 * kFpfhWarps) k_spfh(const double* __restrict__ pos,
@@ -732,16 +725,18 @@ __global__ void __launch_bounds__(32 * kFpfhWarps) k_spfh(const double* __restri
 // list A with the host's decisions (0/1) of the frame-source test (no theta
 // edge for either outcome: checked in k_spfh)
 __global__ void k_spfh_resolve_a(const double* __restrict__ pos, const double* __restrict__ nrm,
-                                 const int2* __restrict__ deferred, const uint8_t* __restrict__ decision, int32_t m,
-                                 int32_t* __restrict__ counts) {
+                                 const int2* __restrict__ deferred, const int32_t* __restrict__ decision,
+                                 const uint8_t* __restrict__ host_dec, int32_t m, int32_t* __restrict__ counts) {
     const int32_t k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= m) return;
     const int2 ij = deferred[k];
+    int32_t dec = decision[k];
+    if (dec >= 2) dec = host_dec[dec - 2];  // page-locked host memory, read in place
     const V3 n1 = ld3(nrm, ij.x), n2 = ld3(nrm, ij.y);
     PairSetup s;
     int3 bins;
     bool edge;
-    if (!pair_setup(ld3(pos, ij.x), n1, ld3(pos, ij.y), n2, s) || !pair_bins(s, n1, n2, decision[k], bins, edge))
+    if (!pair_setup(ld3(pos, ij.x), n1, ld3(pos, ij.y), n2, s) || !pair_bins(s, n1, n2, dec, bins, edge))
         return;
     int32_t* c = counts + 34 * static_cast<int64_t>(ij.x);
     atomicAdd(c + bins.x, 1);
@@ -1194,9 +1189,8 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
     const size_t scan_bytes = scan_temp_bytes(n);
     const size_t lists_bytes = S::round(cap * sizeof(int32_t)) + S::round(a_cap * sizeof(int2)) +
                                S::round(a_cap * sizeof(double2)) + S::round(b_cap * sizeof(int2)) +
-                               S::round(b_cap * sizeof(DeferredPair)) + 2 * S::round(a_cap) +
-                               S::round(a_cap * sizeof(int32_t)) + S::round(offsetof(FpfhHead, a) + a_cap * sizeof(double4)) +
-                               S::round(b_cap * sizeof(uint32_t));
+                               S::round(b_cap * sizeof(DeferredPair)) + S::round(a_cap * sizeof(int32_t)) +
+                               S::round(offsetof(FpfhHead, a) + a_cap * sizeof(double4));
     Scratch sc(stream, 2 * S::round((n + 1) * sizeof(int32_t)) + S::round(33 * n * sizeof(double)) +
                            S::round(34 * n * sizeof(int32_t)) + 2 * S::round(4 * sizeof(int32_t)) + S::round(scan_bytes) +
                            (brute ? S::round(n * sizeof(int4)) + S::round(n * sizeof(uint32_t)) +
@@ -1229,8 +1223,6 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
     trace_point("fpfh nbr", stream);
     int32_t* nbr = nullptr;
     DeferLists dl{};
-    uint8_t* d_dec_a = nullptr;
-    uint32_t* d_dec_b = nullptr;
     FpfhHead* head_dev = nullptr;  // dl.a2_x = head_dev->a
     bool pooled = false;  // this attempt's lists come from the pool (the retry)
     auto free_lists = [&] {
@@ -1241,10 +1233,7 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
         cudaFreeAsync(dl.b_ij, stream);
         cudaFreeAsync(dl.b_x, stream);
         cudaFreeAsync(dl.a_dec, stream);
-        cudaFreeAsync(dl.a2_k, stream);
         cudaFreeAsync(head_dev, stream);
-        if (d_dec_a) cudaFreeAsync(d_dec_a, stream);
-        if (d_dec_b) cudaFreeAsync(d_dec_b, stream);
     };
     for (int attempt = 0; attempt < 2; ++attempt) {
         if (attempt == 0) {
@@ -1253,26 +1242,18 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
             dl.a_x = sc.take<double2>(a_cap);
             dl.b_ij = sc.take<int2>(b_cap);
             dl.b_x = sc.take<DeferredPair>(b_cap);
-            dl.a_dec = sc.take<uint8_t>(a_cap);
-            dl.a2_k = sc.take<int32_t>(a_cap);
+            dl.a_dec = sc.take<int32_t>(a_cap);
             head_dev = reinterpret_cast<FpfhHead*>(sc.take<char>(offsetof(FpfhHead, a) + a_cap * sizeof(double4)));
-            d_dec_a = sc.take<uint8_t>(a_cap);
-            d_dec_b = sc.take<uint32_t>(b_cap);
             LK_TRY(sc.status());
         } else {
             pooled = true;
-            d_dec_a = nullptr;
-            d_dec_b = nullptr;
             LK_TRY(cudaMallocAsync(&nbr, cap * sizeof(int32_t), stream));
             LK_TRY(cudaMallocAsync(&dl.a_ij, a_cap * sizeof(int2), stream));
             LK_TRY(cudaMallocAsync(&dl.a_x, a_cap * sizeof(double2), stream));
             LK_TRY(cudaMallocAsync(&dl.b_ij, b_cap * sizeof(int2), stream));
             LK_TRY(cudaMallocAsync(&dl.b_x, b_cap * sizeof(DeferredPair), stream));
-            LK_TRY(cudaMallocAsync(&dl.a_dec, a_cap, stream));
-            LK_TRY(cudaMallocAsync(&dl.a2_k, a_cap * sizeof(int32_t), stream));
+            LK_TRY(cudaMallocAsync(&dl.a_dec, a_cap * sizeof(int32_t), stream));
             LK_TRY(cudaMallocAsync(&head_dev, offsetof(FpfhHead, a) + a_cap * sizeof(double4), stream));
-            LK_TRY(cudaMallocAsync(&d_dec_a, a_cap, stream));
-            LK_TRY(cudaMallocAsync(&d_dec_b, b_cap * sizeof(uint32_t), stream));
         }
         if (!head_dev) return cudaErrorMemoryAllocation;
         dl.a2_x = head_dev->a;
@@ -1340,10 +1321,11 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
             const double g2 = std::isnan(xs[k].w) ? std::acos(xs[k].y) : xs[k].w;
             st.dec_a[k] = g1 > g2 ? 1 : 0;
         }
-        LK_TRY(cudaMemcpyAsync(d_dec_a, st.dec_a, ma, cudaMemcpyHostToDevice, stream));
-        k_spfh_scatter_a2<<<nblocks(ma, 256), 256, 0, stream>>>(dl.a2_k, d_dec_a, ma, dl.a_dec);
     }
-    if (na > 0) k_spfh_resolve_a<<<nblocks(na, 256), 256, 0, stream>>>(d_pos, d_nrm, dl.a_ij, dl.a_dec, na, votes);
+    // the host's decisions are read by the kernels from the page-locked
+    // staging in place (a few bytes each: no copy command)
+    if (na > 0)
+        k_spfh_resolve_a<<<nblocks(na, 256), 256, 0, stream>>>(d_pos, d_nrm, dl.a_ij, dl.a_dec, st.dec_a, na, votes);
     if (mb > 0) {
         std::vector<DeferredPair> more;
         const DeferredPair* xs = st.head->b;
@@ -1361,8 +1343,7 @@ cudaError_t compute_fpfh(const double* d_pos, const double* d_nrm, int64_t n, do
             st.dec_b_cap = mb;
         }
         for (int32_t k = 0; k < mb; ++k) st.dec_b[k] = host_pair_bins(xs[k].v);
-        LK_TRY(cudaMemcpyAsync(d_dec_b, st.dec_b, mb * sizeof(uint32_t), cudaMemcpyHostToDevice, stream));
-        k_spfh_resolve_b<<<nblocks(mb, 256), 256, 0, stream>>>(dl.b_ij, d_dec_b, mb, votes);
+        k_spfh_resolve_b<<<nblocks(mb, 256), 256, 0, stream>>>(dl.b_ij, st.dec_b, mb, votes);
     }
     trace_point("fpfh resolved", stream);
     k_spfh_scale<<<nblocks(33 * n, 256), 256, 0, stream>>>(votes, n, spfh);
