@@ -667,7 +667,11 @@ void prepare_side(CloudSide& cs, double feature_radius, double normal_radius, do
         mark("upload");
         CK(lkk::pool_alloc(&cs.pos, 3 * n * sizeof(double), cs.s));
         CK(lkk::pool_alloc(&cs.nrm, 3 * n * sizeof(double), cs.s));
-        CK(lkk::voxel_downsample(cs.raw_pos, cs.raw_nrm, n, leaf, cs.pos, cs.nrm, &cs.n, &cs.status, cs.s));
+        // with input normals the downsample also produces the cloud stats
+        // (usable normals, |p|max); they land in cs.stats (the calling
+        // thread's pinned words) ahead of the FPFH, whose readback synchronises
+        CK(lkk::voxel_downsample(cs.raw_pos, cs.raw_nrm, n, leaf, cs.pos, cs.nrm, &cs.n, &cs.status, cs.s,
+                                 cs.raw_nrm ? cs.stats : nullptr));
         lkk::pool_free(cs.raw_pos, cs.s);
         lkk::pool_free(cs.raw_nrm, cs.s);
         cs.raw_pos = cs.raw_nrm = nullptr;
@@ -679,9 +683,7 @@ void prepare_side(CloudSide& cs, double feature_radius, double normal_radius, do
             CK(lkk::estimate_normals(cs.pos, cs.n, normal_radius, origin, cs.nrm, cs.s));
             mark("normals");
         }
-        // usable normals and |p|max land in cs.stats (the calling thread's
-        // pinned words) ahead of the FPFH, whose readback synchronises
-        CK(lkk::cloud_stats_async(cs.pos, cs.nrm, cs.n, cs.stats, cs.s));
+        if (!cs.in->nxyz) CK(lkk::cloud_stats_async(cs.pos, cs.nrm, cs.n, cs.stats, cs.s));
         // the EvalGrid (registration.cpp:249) only needs the downsampled
         // cloud: it is built on its own stream and host thread while this
         // one runs the FPFH

@@ -372,9 +372,11 @@ class Scratch {
 // voxel_downsample (proj/src/preprocess.cpp:14-59) on the device: returns the
 // downsampled count; out_pos / out_nrm (capacity n) in first-index order.
 // Status: 0 ok, 5 invalid normals (MissingNormals), 2 empty, or a CUDA error
-// reported through cudaError_t.
+// reported through cudaError_t. h_stats (optional, page-locked, 2 words):
+// cloud_stats_async of the output, copied back on the stream (d_nrm given).
 cudaError_t voxel_downsample(const double* d_pos, const double* d_nrm, int64_t n, double leaf, double* d_out_pos,
-                             double* d_out_nrm, int64_t* out_count, int* status, cudaStream_t stream);
+                             double* d_out_nrm, int64_t* out_count, int* status, cudaStream_t stream,
+                             unsigned long long* h_stats = nullptr);
 // estimate_normals (proj/src/preprocess.cpp:61-96) on the device: n x 3 normals
 // oriented to `viewpoint` (3 doubles, host), zero where fewer than 3
 // neighbours lie within `radius`.

@@ -78,7 +78,8 @@ __device__ __forceinline__ unsigned long long mix64(unsigned long long k) {
 // the table and the flags to their empty state, the flag scan's leading 0
 __global__ void k_vox_init(uint32_t table, int64_t n, unsigned long long* __restrict__ keys,
                            int32_t* __restrict__ first, int32_t* __restrict__ count, int32_t* __restrict__ flags,
-                           int32_t* __restrict__ flag_scan, int* __restrict__ bad) {
+                           int32_t* __restrict__ flag_scan, int* __restrict__ bad,
+                           unsigned long long* __restrict__ stats) {
     const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < table; i += stride) {
         keys[i] = kEmpty;
@@ -89,6 +90,7 @@ __global__ void k_vox_init(uint32_t table, int64_t n, unsigned long long* __rest
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         flag_scan[0] = 0;
         *bad = 0;
+        stats[0] = stats[1] = 0;
     }
 }
 
@@ -191,71 +193,96 @@ constexpr int kSortCap = 2048;
 // proj/src/preprocess.cpp:30-58, warp per voxel: members sorted by input
 // index, then the sums in that order (lane order within 32-member chunks).
 // A skipped (zero) normal contributes +0.0, which leaves the sum unchanged.
+// stats (optional, zeroed by k_vox_init): cloud_stats of the output -- usable
+// normals and max |p|, k_cloud_stats' arithmetic on the stored values --
+// one atomic pair per block, so the prepare needs no separate stats pass.
 __global__ void __launch_bounds__(32 * kSortWarps) k_vox_reduce(const int32_t* __restrict__ members,
                                                                 const int32_t* __restrict__ member_start, int64_t n_out,
                                                                 const double* __restrict__ pos,
                                                                 const double* __restrict__ nrm,
                                                                 double* __restrict__ out_pos,
-                                                                double* __restrict__ out_nrm) {
+                                                                double* __restrict__ out_nrm,
+                                                                unsigned long long* __restrict__ stats) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t o = blockIdx.x * static_cast<int64_t>(kSortWarps) + warp;
-    if (o >= n_out) return;
-    const int32_t s0 = member_start[o], s1 = member_start[o + 1];
-    const int k = s1 - s0;
-    const int32_t* sorted = members + s0;  // ascending input index (stable radix sort)
-    // lanes gather 32 members at a time (the next chunk's loads in flight
-    // while lane 0 runs the sequential sums over the current one from smem)
     __shared__ double s_v[kSortWarps][6][32];
-    auto fetch = [&](int c0, V3& p, V3& nv) {
-        p = mk(0.0, 0.0, 0.0);
-        nv = mk(0.0, 0.0, 0.0);
-        if (c0 + lane < k) {
-            const int64_t i = sorted[c0 + lane];
-            p = ld3(pos, i);
+    __shared__ unsigned long long s_usable[kSortWarps], s_max[kSortWarps];
+    unsigned long long usable = 0, max_bits = 0;
+    if (o < n_out) {
+        const int32_t s0 = member_start[o], s1 = member_start[o + 1];
+        const int k = s1 - s0;
+        const int32_t* sorted = members + s0;  // ascending input index (stable radix sort)
+        // lanes gather 32 members at a time (the next chunk's loads in flight
+        // while lane 0 runs the sequential sums over the current one from smem)
+        auto fetch = [&](int c0, V3& p, V3& nv) {
+            p = mk(0.0, 0.0, 0.0);
+            nv = mk(0.0, 0.0, 0.0);
+            if (c0 + lane < k) {
+                const int64_t i = sorted[c0 + lane];
+                p = ld3(pos, i);
+                if (nrm) {
+                    nv = ld3(nrm, i);
+                    if (is_zero(nv)) nv = mk(0.0, 0.0, 0.0);
+                }
+            }
+        };
+        // lane q < 6 runs component q's sequential chain (x, y, z of the
+        // positions, then of the normals): six chains side by side
+        double acc = 0.0;
+        V3 p, nv;
+        fetch(0, p, nv);
+        for (int c0 = 0; c0 < k; c0 += 32) {
+            s_v[warp][0][lane] = p.x;
+            s_v[warp][1][lane] = p.y;
+            s_v[warp][2][lane] = p.z;
+            s_v[warp][3][lane] = nv.x;
+            s_v[warp][4][lane] = nv.y;
+            s_v[warp][5][lane] = nv.z;
+            __syncwarp();
+            if (c0 + 32 < k) fetch(c0 + 32, p, nv);
+            if (lane < 6) {
+                const int m = k - c0 < 32 ? k - c0 : 32;
+                const double* col = s_v[warp][lane];
+#pragma unroll 8
+                for (int L = 0; L < m; ++L) acc += col[L];
+            }
+            __syncwarp();
+        }
+        const V3 ps = mk(__shfl_sync(kFull, acc, 0), __shfl_sync(kFull, acc, 1), __shfl_sync(kFull, acc, 2));
+        const V3 nsum = mk(__shfl_sync(kFull, acc, 3), __shfl_sync(kFull, acc, 4), __shfl_sync(kFull, acc, 5));
+        if (lane == 0) {
+            const double cnt = static_cast<double>(k);
+            const double x = ps.x / cnt, y = ps.y / cnt, z = ps.z / cnt;
+            out_pos[3 * o] = x;
+            out_pos[3 * o + 1] = y;
+            out_pos[3 * o + 2] = z;
+            const double r = sqrt(x * x + y * y + z * z);
+            if (r == r) max_bits = static_cast<unsigned long long>(__double_as_longlong(r));  // fmax drops NaN
             if (nrm) {
-                nv = ld3(nrm, i);
-                if (is_zero(nv)) nv = mk(0.0, 0.0, 0.0);
+                const double len = sqrt(sqnorm(nsum));
+                V3 nn = mk(0.0, 0.0, 0.0);
+                if (len > 1e-12) nn = mk(nsum.x / len, nsum.y / len, nsum.z / len);
+                out_nrm[3 * o] = nn.x;
+                out_nrm[3 * o + 1] = nn.y;
+                out_nrm[3 * o + 2] = nn.z;
+                usable = is_zero(nn) ? 0 : 1;
             }
         }
-    };
-    // lane q < 6 runs component q's sequential chain (x, y, z of the
-    // positions, then of the normals): six chains side by side
-    double acc = 0.0;
-    V3 p, nv;
-    fetch(0, p, nv);
-    for (int c0 = 0; c0 < k; c0 += 32) {
-        s_v[warp][0][lane] = p.x;
-        s_v[warp][1][lane] = p.y;
-        s_v[warp][2][lane] = p.z;
-        s_v[warp][3][lane] = nv.x;
-        s_v[warp][4][lane] = nv.y;
-        s_v[warp][5][lane] = nv.z;
-        __syncwarp();
-        if (c0 + 32 < k) fetch(c0 + 32, p, nv);
-        if (lane < 6) {
-            const int m = k - c0 < 32 ? k - c0 : 32;
-            const double* col = s_v[warp][lane];
-#pragma unroll 8
-            for (int L = 0; L < m; ++L) acc += col[L];
-        }
-        __syncwarp();
     }
-    const V3 ps = mk(__shfl_sync(kFull, acc, 0), __shfl_sync(kFull, acc, 1), __shfl_sync(kFull, acc, 2));
-    const V3 nsum = mk(__shfl_sync(kFull, acc, 3), __shfl_sync(kFull, acc, 4), __shfl_sync(kFull, acc, 5));
-    if (lane != 0) return;
-    const double cnt = static_cast<double>(k);
-    out_pos[3 * o] = ps.x / cnt;
-    out_pos[3 * o + 1] = ps.y / cnt;
-    out_pos[3 * o + 2] = ps.z / cnt;
-    if (nrm) {
-        const double len = sqrt(sqnorm(nsum));
-        if (len > 1e-12) {
-            out_nrm[3 * o] = nsum.x / len;
-            out_nrm[3 * o + 1] = nsum.y / len;
-            out_nrm[3 * o + 2] = nsum.z / len;
-        } else {
-            out_nrm[3 * o] = out_nrm[3 * o + 1] = out_nrm[3 * o + 2] = 0.0;
+    if (!stats) return;
+    if (lane == 0) {
+        s_usable[warp] = usable;
+        s_max[warp] = max_bits;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long u = 0, m = 0;
+        for (int w = 0; w < kSortWarps; ++w) {
+            u += s_usable[w];
+            m = s_max[w] > m ? s_max[w] : m;
         }
+        atomicAdd(&stats[0], u);
+        atomicMax(&stats[1], m);  // non-negative doubles order like their bit patterns
     }
 }
 
@@ -1030,7 +1057,8 @@ cudaError_t estimate_normals(const double* d_pos, int64_t n, double radius, cons
 }
 
 cudaError_t voxel_downsample(const double* d_pos, const double* d_nrm, int64_t n, double leaf, double* d_out_pos,
-                             double* d_out_nrm, int64_t* out_count, int* status, cudaStream_t stream) {
+                             double* d_out_nrm, int64_t* out_count, int* status, cudaStream_t stream,
+                             unsigned long long* h_stats) {
     *status = 0;
     *out_count = 0;
     if (n <= 0) {
@@ -1053,7 +1081,7 @@ cudaError_t voxel_downsample(const double* d_pos, const double* d_nrm, int64_t n
     const size_t tb = S::round(table * sizeof(unsigned long long)) + 3 * S::round(table * sizeof(int32_t));
     const size_t nb = S::round(n * sizeof(int32_t));
     Scratch sc(stream, tb + 8 * nb + 3 * S::round((n + 2) * sizeof(int32_t)) +
-                           S::round(scan_bytes) + S::round(sort_bytes));
+                           S::round(scan_bytes) + S::round(sort_bytes) + S::round(2 * sizeof(unsigned long long)));
     unsigned long long* keys = sc.take<unsigned long long>(table);
     int32_t* first = sc.take<int32_t>(table);
     int32_t* count = sc.take<int32_t>(table);
@@ -1070,10 +1098,11 @@ cudaError_t voxel_downsample(const double* d_pos, const double* d_nrm, int64_t n
     int32_t* svals = sc.take<int32_t>(n);
     int32_t* skeys_out = sc.take<int32_t>(n);
     void* sort_temp = sc.take<char>(sort_bytes);
+    unsigned long long* d_stats = sc.take<unsigned long long>(2);
     LK_TRY(sc.status());
     const int64_t init_n = std::max<int64_t>(table, n);
     k_vox_init<<<static_cast<unsigned>(std::min<int64_t>(nblocks(init_n, 256), 148 * 8)), 256, 0, stream>>>(
-        table, n, keys, first, count, flags, flag_scan, bad);
+        table, n, keys, first, count, flags, flag_scan, bad, d_stats);
     k_vox_insert<<<nblocks(n, 256), 256, 0, stream>>>(d_pos, d_nrm, n, leaf, keys, table - 1, point_slot, first,
                                                      count, bad);
     k_vox_mark<<<nblocks(table, 256), 256, 0, stream>>>(keys, first, table, flags);
@@ -1102,8 +1131,10 @@ cudaError_t voxel_downsample(const double* d_pos, const double* d_nrm, int64_t n
     LK_TRY(cub::DeviceRadixSort::SortPairs(sort_temp, sort_bytes, skeys, skeys_out, svals, members,
                                            static_cast<int>(n), 0, end_bit, stream));
     trace_point("vox sorted", stream);
-    k_vox_reduce<<<nblocks(n_out, kSortWarps), 32 * kSortWarps, 0, stream>>>(members, member_start, n_out, d_pos,
-                                                                              d_nrm, d_out_pos, d_out_nrm);
+    k_vox_reduce<<<nblocks(n_out, kSortWarps), 32 * kSortWarps, 0, stream>>>(
+        members, member_start, n_out, d_pos, d_nrm, d_out_pos, d_out_nrm, h_stats ? d_stats : nullptr);
+    if (h_stats)
+        LK_TRY(cudaMemcpyAsync(h_stats, d_stats, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream));
     *out_count = n_out;
     return cudaGetLastError();
 }
