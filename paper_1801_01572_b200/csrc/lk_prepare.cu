@@ -16,7 +16,7 @@
 //   k_spfh    warp per point: pair-angle votes as integer counts; pairs whose
 //             frame-source test (std::acos comparison) the device cannot
 //             decide, or whose theta (atan2) lies at a bin edge, are deferred
-//             to the host's libm (host_pair_bins, k_spfh_resolve), then
+//             to the host's libm (host_pair_bins, k_spfh_resolve_a/b), then
 //             k_spfh_scale applies fl(100 / votes) like `v *= 100.0 / votes`
 //   k_fpfh    warp per point, lane per bin: acc_b += spfh_j[b] / w_j over the
 //             neighbours in ascending order (the reference's summation order)
@@ -600,7 +600,7 @@ __device__ __forceinline__ double div_by(double a, double b, double r) {
 
 // pass 1 (proj/src/fpfh.cpp:76-100): warp per point, integer vote counts in
 // counts[i][0..32], votes in counts[i][33]. Pairs whose frame-source test the
-// device cannot decide are appended to the deferred list (k_spfh_resolve).
+// device cannot decide are appended to the deferred list (k_spfh_resolve_b).
 // Pairs the device cannot settle go to the host's libm on two lists:
 //   A  the frame-source test acos(|a1|) > acos(|a2|) is undecided here and
 //      the bins depend on it (common on planar faces): (i, j) and (|a1|,
@@ -1142,7 +1142,7 @@ cudaError_t voxel_downsample(const double* d_pos, const double* d_nrm, int64_t n
 // proj/src/fpfh.cpp:17-53 on the host with the reference's libm (std::acos,
 // std::atan2) for the pairs k_spfh defers. Same IEEE operation order as the
 // device (-ffp-contract=off), so everything but the two libm calls agrees
-// bit for bit. Returns the packed bins of k_spfh_resolve.
+// bit for bit. Returns the packed bins of k_spfh_resolve_b.
 static uint32_t host_pair_bins(const double* v) {
     struct H {
         double x, y, z;
@@ -1183,9 +1183,9 @@ static uint32_t host_pair_bins(const double* v) {
 }
 
 // Pinned host staging of compute_fpfh, one per host thread (each prepare side
-// runs on its own thread): the total neighbour count, the deferred count and
-// the first kStageX deferred pairs come back in one copy; the decisions go
-// back from here. Reused only after the caller's stream has synchronised.
+// runs on its own thread): the FpfhHead comes back in one copy; the host's
+// decisions are written here and read by the resolve kernels in place.
+// Reused only after the caller's stream has synchronised.
 struct FpfhStage {
     FpfhHead* head = nullptr;
     double4* more_a = nullptr;  // list A2 beyond kStageA (rare)
