@@ -335,7 +335,8 @@ __device__ __forceinline__ bool pair_setup(V3 p1, V3 n1, V3 p2, V3 n2, PairSetup
 // reference uses glibc's; its bin floor(11 (theta + pi) / 2 pi) is decided
 // here only when that value is more than 1e-12 from an inner bin edge (the
 // two libms put it within ~1e-14 of each other); otherwise theta_edge is set
-// and the pair goes to the host (k_spfh's deferred list). alpha and phi are
+// and the pair goes to the host (k_spfh's deferred list). Most pairs are
+// settled by an FP32 atan2 with a 1e-4 margin before any FP64 atan2. alpha and phi are
 // plain IEEE arithmetic, identical on both sides.
 __device__ __forceinline__ bool pair_bins(const PairSetup& s, V3 n1, V3 n2, int swap, int3& bins, bool& theta_edge) {
     V3 ns = n1, nt = n2, line = s.d;
@@ -355,12 +356,31 @@ __device__ __forceinline__ bool pair_bins(const PairSetup& s, V3 n1, V3 n2, int 
     V3 w = cross(u, v);
     const double alpha = dot(v, nt);
     const double phi = cos_line;
-    const double theta = atan2(dot(w, nt), dot(u, nt));
-    const double tv = 11 * (theta - -M_PI) / (M_PI - -M_PI);
-    const double edge = rint(tv);
-    theta_edge = edge >= 1.0 && edge <= 10.0 && fabs(tv - edge) < 1e-12;
-    bins = make_int3(bin_index(alpha, -1.0, 1.0), 11 + bin_index(phi, -1.0, 1.0),
-                     22 + bin_index(theta, -M_PI, M_PI));
+    const double ty = dot(w, nt), tx = dot(u, nt);
+    // theta's bin from FP32 first: its tv is within 1e-5 of the exact value
+    // (atan2f, the float rounding of tx and ty -- both normal floats near an
+    // inner edge, where |sin|, |cos| >= 0.14 -- and the float arithmetic), so
+    // more than 1e-4 from every integer it is the bin of glibc's theta too,
+    // and not within 1e-12 of an inner edge. Otherwise the FP64 path below.
+    const double m = fmax(fabs(tx), fabs(ty));
+    int tb = -1;
+    if (m >= 1e-30 && m <= 1e30) {
+        const float tf = atan2f(static_cast<float>(ty), static_cast<float>(tx));
+        const float tvf = 11.0f * (tf + 3.14159265f) / 6.28318531f;
+        if (fabsf(tvf - rintf(tvf)) > 1e-4f) {
+            const int b = static_cast<int>(floorf(tvf));
+            tb = b < 0 ? 0 : (b > 10 ? 10 : b);
+            theta_edge = false;
+        }
+    }
+    if (tb < 0) {
+        const double theta = atan2(ty, tx);
+        const double tv = 11 * (theta - -M_PI) / (M_PI - -M_PI);
+        const double edge = rint(tv);
+        theta_edge = edge >= 1.0 && edge <= 10.0 && fabs(tv - edge) < 1e-12;
+        tb = bin_index(theta, -M_PI, M_PI);
+    }
+    bins = make_int3(bin_index(alpha, -1.0, 1.0), 11 + bin_index(phi, -1.0, 1.0), 22 + tb);
     return true;
 }
 
