@@ -572,8 +572,8 @@ namespace {
 
 // Source-side tail shared by both constructors: the FP32 source copy, |p|max
 // bound for the guard bands and the record buffer.
-void ctx_finish_source(lk_reg_ctx* c) {
-    cudaStream_t s = c->stream;
+void ctx_finish_source(lk_reg_ctx* c, cudaStream_t s = nullptr) {
+    if (!s) s = c->stream;
     CK(lkk::pool_alloc(&c->d_spos32, std::max<int64_t>(c->ns, 1) * sizeof(float4), s));
     CK(lkk::make_source32(c->d_spos, c->ns, c->d_spos32, s));
     CK(lkk::pool_alloc(&c->d_spos4, std::max<int64_t>(c->ns, 1) * sizeof(double4), s));
@@ -630,6 +630,7 @@ struct CloudSide {
     double max_norm = 0.0;
     unsigned long long* stats = nullptr;  // 2 pinned words of the calling thread: usable normals, |p|max
     bool features = false;                 // feat is being computed on s
+    cudaEvent_t ready = nullptr;           // downsampled positions and normals final on s
     std::exception_ptr err;
 };
 
@@ -684,17 +685,15 @@ void prepare_side(CloudSide& cs, double feature_radius, double normal_radius, do
             mark("normals");
         }
         if (!cs.in->nxyz) CK(lkk::cloud_stats_async(cs.pos, cs.nrm, cs.n, cs.stats, cs.s));
+        CK(cudaEventCreateWithFlags(&cs.ready, cudaEventDisableTiming));
+        CK(cudaEventRecord(cs.ready, cs.s));
         // the EvalGrid (registration.cpp:249) only needs the downsampled
         // cloud: it is built on its own stream and host thread while this
         // one runs the FPFH
         Worker* gw = nullptr;
         cudaError_t grid_err = cudaSuccess;
         if (grid) {
-            cudaEvent_t ready;
-            CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-            CK(cudaEventRecord(ready, cs.s));
-            CK(cudaStreamWaitEvent(grid_stream, ready, 0));
-            cudaEventDestroy(ready);
+            CK(cudaStreamWaitEvent(grid_stream, cs.ready, 0));
             gw = acquire_worker();
             const double* pos = cs.pos;
             const double* nrm = cs.nrm;
@@ -837,6 +836,8 @@ lk_status prepare_impl(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_pa
         lkk::pool_free(cs.q2, cs.s);
         cs.padded = nullptr;
         cs.q2 = nullptr;
+        if (cs.ready) cudaEventDestroy(cs.ready);
+        cs.ready = nullptr;
     };
     try {
         // page-locked callers: the two uploads are enqueued here back to back,
@@ -911,7 +912,15 @@ lk_status prepare_impl(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_pa
                 cs->q2 = nullptr;
             }
             tmark("joined, feature nn start", s, t0);
-            ctx_finish_source(c);
+            // the source's FP32 copy and records need only its downsampled
+            // cloud: on the target's stream (idle by now), beside the match
+            CK(cudaStreamWaitEvent(T.s, S.ready, 0));
+            ctx_finish_source(c, T.s);
+            cudaEvent_t fin;
+            CK(cudaEventCreateWithFlags(&fin, cudaEventDisableTiming));
+            CK(cudaEventRecord(fin, T.s));
+            CK(cudaStreamWaitEvent(s, fin, 0));
+            cudaEventDestroy(fin);
             tmark("feature nn done", s, t0);
         }
         // no wait for the match: each side's stats were copied ahead of its
@@ -922,8 +931,11 @@ lk_status prepare_impl(const lk_cloud* src, const lk_cloud* tgt, const lk_reg_pa
             CK(cudaStreamSynchronize(T.s));
             CK(cudaStreamSynchronize(S.s));
         }
-        for (CloudSide* cs : {&S, &T})
+        for (CloudSide* cs : {&S, &T}) {
             if (cs->features) lkk::cloud_stats_decode(cs->stats, &cs->usable, &cs->max_norm);
+            if (cs->ready) cudaEventDestroy(cs->ready);  // its waits are enqueued
+            cs->ready = nullptr;
+        }
         c->src_max_norm = S.max_norm;
         // the reference's check order (registration.cpp:226-245)
         if (S.status == 5 || T.status == 5)
