@@ -230,8 +230,17 @@ __global__ void __launch_bounds__(32 * kSortWarps) k_vox_reduce(const int32_t* _
         // positions, then of the normals): six chains side by side
         double acc = 0.0;
         V3 p, nv;
+        // chunk c + 2's members pulled into L1 while chunk c + 1 is loaded
+        // into registers (their indices loaded one iteration earlier)
+        auto l1_prefetch = [&](int j) {
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(pos + 3 * static_cast<int64_t>(j)));
+            if (nrm) asm volatile("prefetch.global.L1 [%0];" ::"l"(nrm + 3 * static_cast<int64_t>(j)));
+        };
+        int32_t ahead = 64 + lane < k ? sorted[64 + lane] : -1;
         fetch(0, p, nv);
         for (int c0 = 0; c0 < k; c0 += 32) {
+            if (ahead >= 0) l1_prefetch(ahead);
+            ahead = c0 + 96 + lane < k ? sorted[c0 + 96 + lane] : -1;
             s_v[warp][0][lane] = p.x;
             s_v[warp][1][lane] = p.y;
             s_v[warp][2][lane] = p.z;
