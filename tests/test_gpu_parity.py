@@ -286,6 +286,29 @@ def test_prefix_stability_and_shards(prepared1, oracle):
         full.fitness < half.fitness or full.hypothesis_index == half.hypothesis_index)))
 
 
+@pytest.mark.parametrize("usable", [0, 3, 4])
+def test_usable_normal_count_after_downsampling(usable):
+    # registration.cpp:238-245: fewer than 4 non-zero normals after the
+    # downsample -> MissingData (counted by k_vox_reduce on the device)
+    rng = np.random.default_rng(usable)
+    pos = rng.uniform(0.0, 2.0, size=(3000, 3))
+    nrm = np.zeros_like(pos)
+    lone = np.array([[100.0 + 3 * k, 0.0, 0.0] for k in range(usable)]).reshape(-1, 3)  # own voxels
+    pos = np.concatenate([pos, lone])
+    nrm = np.concatenate([nrm, np.tile([0.0, 0.0, 1.0], (usable, 1))])
+    cloud = lk.PointCloud(pos, nrm)
+    ok = synth.random_cloud(2000, 53, 0, with_normals=True)
+    params = lk.RegistrationParams()
+    if usable < 4:
+        with pytest.raises(lk.MissingData):
+            lk.prepare_registration(cloud, ok, params)
+        with pytest.raises(lk.MissingData):
+            lk.prepare_registration(ok, cloud, params)
+    else:
+        lk.prepare_registration(cloud, ok, params).close()
+        lk.prepare_registration(ok, cloud, params).close()
+
+
 def test_too_few_points_and_cache_errors(oracle):
     tiny = lk.PointCloud(np.array([[0, 0, 0], [1, 0, 0], [0, 1, 0]], float), np.tile([0, 0, 1.0], (3, 1)))
     ok = synth.random_cloud(200, 52, 0, with_normals=True)
